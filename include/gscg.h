@@ -1,0 +1,188 @@
+/*
+ * gscg.h — C-ABI of the B200 crowd-render hot path (CrowdSplat, arXiv 2501.17792).
+ *
+ * This is the drop-in boundary the C++ host API (paper_2501_17792_b200/host, namespace
+ * gsc) calls. The reference renderer has no FFI of its own; the entry points below
+ * replace, one for one, the reference's public renderer / crowd calls
+ * (paths relative to /root/reference/proj):
+ *
+ *   gscg_create / gscg_destroy        FrameContext lifetime          include/gsc/renderer.hpp:57-79
+ *   gscg_upload_skeleton              Skeleton (bind/local/inverse)  include/gsc/avatar.hpp:16-31, src/avatar.cpp:40-72
+ *   gscg_upload_level                 LodLevel (+ finalize cov_cache) include/gsc/avatar.hpp:50-65, src/avatar.cpp:99-105
+ *   gscg_render_frame                 render_frame(Crowd&, Camera, time, settings,
+ *                                       static_pose, forced_lod, StageTimes*, FrameContext&)
+ *                                                                    include/gsc/renderer.hpp:121-123, src/renderer.cpp:249-280
+ *       - stage "update"   = update_crowd: LoD + FK + skin matrices  src/crowd.cpp:86-140
+ *       - stage "gather"   = gather_splats: LBS + EWA projection     src/renderer.cpp:25-73
+ *       - stage "sort"     = sort_splats + binning                   src/renderer.cpp:85-161
+ *       - stage "rasterize"= per-tile front-to-back blend            src/renderer.cpp:163-232
+ *   gscg_get_*                        parity / debug exports (no reference equivalent;
+ *                                     they expose FrameContext internals: frame.splats, bins)
+ *
+ * Conventions: one CUDA stream per context; a context is not thread-safe; every
+ * function returns GSCG_OK (0) or a negative status and records a message readable
+ * through gscg_last_error. Host buffers are caller-owned; device buffers are owned by
+ * the context and grow to a high-water mark. Matrices are column-major float[16]
+ * (Eigen's Mat4 storage order). There is no CPU fallback: without a CUDA device
+ * gscg_create fails with GSCG_ERR_CUDA.
+ */
+#ifndef GSCG_H_
+#define GSCG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSCG_OK 0
+#define GSCG_ERR_INVALID_ARGUMENT (-1) /* std::invalid_argument in the reference */
+#define GSCG_ERR_CUDA (-2)
+#define GSCG_ERR_NCCL (-3)
+#define GSCG_ERR_OOM (-4) /* std::bad_alloc in the reference (bench.cpp:94-97) */
+#define GSCG_ERR_STATE (-5)
+
+#define GSCG_MAX_JOINTS 64
+#define GSCG_MAX_LOD_THRESHOLDS 8
+#define GSCG_SH_FLOATS 45 /* SH degree 1..3 residual: 15 coefficients x RGB */
+
+typedef struct gscg_ctx gscg_ctx;
+
+/* Skeleton of one template (avatar.hpp:16-31). Derived transforms are passed in,
+ * computed by the host exactly as Skeleton::make does (avatar.cpp:40-72). */
+typedef struct {
+  uint32_t joint_count;      /* <= GSCG_MAX_JOINTS */
+  const int16_t* parents;    /* joint_count; parents[0] == -1 */
+  const float* local_bind;   /* joint_count x 16, column-major */
+  const float* inverse_bind; /* joint_count x 16, column-major */
+  float pelvis_y;            /* bind[0](1,3): the LoD root height (crowd.cpp:98-100) */
+} gscg_skeleton_desc;
+
+/* One LoD level of one template (avatar.hpp:50-65), structure-of-arrays. */
+typedef struct {
+  uint32_t gaussian_count;
+  const float* means;           /* N x 3 */
+  const float* cov6;            /* N x 6: cov_cache xx,xy,xz,yy,yz,zz (avatar.cpp:99-105) */
+  const float* opacities;       /* N */
+  const float* colors;          /* N x 3 linear RGB */
+  const uint16_t* skin_indices; /* N x 4 */
+  const float* skin_weights;    /* N x 4 */
+  const float* sh;              /* N x 45 SH residual coefficients, or NULL (RGB only) */
+} gscg_level_desc;
+
+/* Flattened camera (CameraBasis, math.hpp:85-96 / math.cpp:118-129). */
+typedef struct {
+  float world_to_view[9]; /* row-major W(i,j) */
+  float position[3];
+  float focal, cx, cy, near_m;
+  int32_t width, height;
+} gscg_camera;
+
+/* RenderSettings (renderer.hpp:15-22). */
+typedef struct {
+  int32_t tile_size;
+  float background[3];
+  float alpha_max;
+  float alpha_cutoff;
+  float transmittance_floor;
+  int32_t sh_enabled; /* 1: evaluate the SH-deg-3 residual colour extension */
+} gscg_render_settings;
+
+/* LodPolicy (lod.hpp:16-21). */
+typedef struct {
+  uint32_t threshold_count; /* <= GSCG_MAX_LOD_THRESHOLDS */
+  float thresholds_m[GSCG_MAX_LOD_THRESHOLDS];
+  float hysteresis_band_m;
+} gscg_lod_policy;
+
+#define GSCG_MEM_HOST 0
+#define GSCG_MEM_DEVICE 1
+
+/* Per-frame crowd state: what update_crowd reads from Crowd (crowd.hpp:18-45) after
+ * the host has sampled each instance's pose (avatar.cpp:247-283). */
+typedef struct {
+  uint32_t instance_count;
+  uint32_t joint_stride;        /* joints per pose record (max joint count over templates) */
+  const uint32_t* template_ids; /* n */
+  const float* placement;       /* n x 4: x, z, cos(yaw), sin(yaw) (crowd.cpp:20-30) */
+  const float* poses;           /* n x (4 + 4*joint_stride): root_translation xyz, pad,
+                                   then per joint quaternion (x, y, z, w) */
+  uint32_t* active_lod;         /* n, in/out: previous level (0xffffffff = unset) -> new level */
+  int32_t forced_lod;           /* -1: distance LoD; else pinned level (crowd.cpp:94-96) */
+  int32_t memory;               /* GSCG_MEM_HOST or GSCG_MEM_DEVICE for the pointers above */
+} gscg_frame_desc;
+
+/* StageTimes (renderer.hpp:105-112), measured with CUDA events on the context stream. */
+typedef struct {
+  double update_ms;
+  double gather_ms;
+  double sort_ms;
+  double rasterize_ms;
+  double h2d_ms;
+  double d2h_ms;
+  uint64_t splat_count;    /* surviving splats S */
+  uint64_t pair_count;     /* tile-splat pairs K */
+  uint64_t gaussian_count; /* instance-Gaussians G */
+  uint32_t sort_passes;
+  uint32_t kernel_launches;
+} gscg_stage_times;
+
+/* One surviving splat as gather_splats produces it (FrameSplat, renderer.hpp:39-44),
+ * plus the prepared conic (renderer.hpp:72-75). Exported only in debug mode. */
+typedef struct {
+  uint32_t ordinal; /* instance base + gaussian_index */
+  uint32_t instance_id;
+  uint32_t gaussian_index;
+  float depth;
+  float mean_px[2];
+  float cov_xx, cov_xy, cov_yy;
+  float conic[3];
+  float power_floor;
+  float opacity;
+  float color[3];
+  int32_t rect[4]; /* x0, y0, x1, y1 */
+} gscg_splat_record;
+
+#define GSCG_DEBUG_POSED 1u   /* keep posed means (G x 3) */
+#define GSCG_DEBUG_RECORDS 2u /* keep gscg_splat_record per survivor */
+
+int gscg_create(int device, gscg_ctx** out);
+int gscg_destroy(gscg_ctx* ctx);
+const char* gscg_last_error(const gscg_ctx* ctx);
+int gscg_device_count(int* out);
+
+int gscg_upload_skeleton(gscg_ctx* ctx, uint32_t template_id, const gscg_skeleton_desc* desc);
+int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level,
+                      const gscg_level_desc* desc);
+/* Device bytes held by uploaded templates (shared attribute store). */
+int gscg_template_bytes(const gscg_ctx* ctx, uint64_t* out);
+
+int gscg_set_debug(gscg_ctx* ctx, uint32_t flags);
+
+/* Renders one frame. fb_rgb (W*H*3) and fb_T (W*H) receive the framebuffer and the
+ * final transmittance; with memory == GSCG_MEM_HOST they are host pointers (copied back
+ * before return), with GSCG_MEM_DEVICE they may be NULL (result stays in the context,
+ * see gscg_framebuffer_device) and the call does not synchronise the host. */
+int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                      const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                      float* fb_rgb, float* fb_T, gscg_stage_times* times);
+
+/* Device pointers of the context's framebuffer (valid until the next render). */
+int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T);
+int gscg_synchronize(gscg_ctx* ctx);
+
+/* Parity / debug exports of the last frame. */
+int gscg_get_counts(gscg_ctx* ctx, uint64_t* gaussians, uint64_t* splats, uint64_t* pairs);
+int gscg_get_lod(gscg_ctx* ctx, uint32_t* out, uint32_t n);
+int gscg_get_instance_base(gscg_ctx* ctx, uint32_t* out, uint32_t n);
+int gscg_get_posed_means(gscg_ctx* ctx, float* out, uint64_t gaussians);
+int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splats);
+int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t tiles); /* tiles x 2 */
+int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GSCG_H_ */

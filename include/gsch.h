@@ -1,0 +1,121 @@
+/*
+ * gsch.h — C-ABI of the host scene layer (paper_2501_17792_b200/host, namespace gsc).
+ *
+ * It exposes the reference's host-side API to Python (ctypes) without torch types:
+ * synthetic assets (generate_synthetic_template / generate_synthetic_motion,
+ * /root/reference/proj/src/synthetic.cpp), build_crowd (crowd.cpp:46-84), the camera
+ * (Camera::look_at, math.cpp:42-64) and render_frame (renderer.hpp:114-123) running on
+ * the B200 path through gscg.h. Array views expose the host asset store so parity tests
+ * can feed the identical inputs to the CPU oracle.
+ */
+#ifndef GSCH_H_
+#define GSCH_H_
+
+#include <stdint.h>
+
+#include "gscg.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gsch_scene gsch_scene;
+typedef struct gsch_renderer gsch_renderer;
+
+typedef struct {
+  uint32_t template_count;
+  uint64_t template_seed_base; /* template i uses seed base + i, template_id = i */
+  uint32_t level_count;
+  uint32_t level_counts[4];
+  uint32_t joint_count;
+  int32_t with_sh;
+  uint32_t motion_count;
+  uint64_t motion_seed_base;
+  float motion_fps;
+  uint32_t motion_frames;
+  uint32_t grid_rows, grid_cols;
+  float grid_spacing;
+  uint32_t crowd_count;
+  uint64_t crowd_seed;
+  float cam_pos[3];
+  float cam_look[3];
+  float fov_y_deg;
+  uint32_t width, height;
+  float near_m;
+  uint32_t lod_threshold_count;
+  float lod_thresholds[8];
+  float lod_hysteresis;
+} gsch_scene_config;
+
+typedef struct {
+  uint32_t instance_id, template_id, motion_id;
+  float x, z, yaw, phase_offset_s;
+  uint32_t active_lod;
+} gsch_instance;
+
+typedef struct {
+  uint32_t count;
+  const float* means;         /* N x 3 */
+  const float* rotations;     /* N x 4 (x, y, z, w) */
+  const float* scales;        /* N x 3 */
+  const float* opacities;     /* N */
+  const float* colors;        /* N x 3 */
+  const uint16_t* skin_indices; /* N x 4 */
+  const float* skin_weights;  /* N x 4 */
+  const float* sh;            /* N x 45 or NULL */
+  const float* cov6;          /* N x 6 */
+} gsch_level_view;
+
+typedef struct {
+  int32_t tile_size;
+  float background[3];
+  float alpha_max, alpha_cutoff, transmittance_floor;
+  int32_t thread_count;
+  int32_t sh_colour;
+} gsch_render_settings;
+
+typedef struct {
+  double update_ms, gather_ms, sort_ms, rasterize_ms, pose_ms, total_ms;
+  uint64_t splat_count, pair_count, gaussian_count;
+} gsch_stage_times;
+
+const char* gsch_last_error(void);
+
+int gsch_scene_create(const gsch_scene_config* cfg, int threads, gsch_scene** out);
+int gsch_scene_destroy(gsch_scene* scene);
+int gsch_scene_counts(const gsch_scene* scene, uint32_t* templates, uint32_t* motions,
+                      uint32_t* instances);
+int gsch_scene_get_instances(const gsch_scene* scene, gsch_instance* out, uint32_t n);
+int gsch_scene_set_instances(gsch_scene* scene, const gsch_instance* in, uint32_t n);
+int gsch_scene_set_camera(gsch_scene* scene, const float* pos, const float* look, float fov_y_deg,
+                          uint32_t width, uint32_t height, float near_m);
+int gsch_scene_camera_basis(const gsch_scene* scene, gscg_camera* out);
+int gsch_scene_set_lod_policy(gsch_scene* scene, const float* thresholds, uint32_t count,
+                              float hysteresis);
+int gsch_scene_level_count(const gsch_scene* scene, uint32_t template_id, uint32_t* out);
+int gsch_scene_level_view(const gsch_scene* scene, uint32_t template_id, uint32_t level,
+                          gsch_level_view* out);
+int gsch_scene_skeleton(const gsch_scene* scene, uint32_t template_id, uint32_t* joint_count,
+                        const int16_t** parents, const float** inverse_bind);
+/* frames x (4 + 4*J): root xyz, pad, J quaternions (x, y, z, w); call with out = NULL to query */
+int gsch_scene_motion(const gsch_scene* scene, uint32_t motion_id, float* fps, uint32_t* frames,
+                      uint32_t* joints, float* out);
+
+int gsch_renderer_create(gsch_scene* scene, int device, gsch_renderer** out);
+int gsch_renderer_destroy(gsch_renderer* r);
+gscg_ctx* gsch_renderer_gpu(gsch_renderer* r);
+uint32_t gsch_renderer_joint_stride(gsch_renderer* r);
+/* render_frame(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx) */
+int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
+                const gsch_render_settings* settings, float* out_rgb, float* out_T,
+                gsch_stage_times* times);
+/* Host pose sampling only (the "update" host part) into caller buffers:
+ * template_ids n, placement n x 4, poses n x (4 + 4*joint_stride). */
+int gsch_sample_crowd(gsch_renderer* r, float time_s, int32_t static_pose, int32_t threads,
+                      uint32_t* template_ids, float* placement, float* poses);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GSCH_H_ */

@@ -1,0 +1,354 @@
+"""Python mirror of the reference's host API for the crowd render path.
+
+Names follow /root/reference/proj/include/gsc: ``SceneConfig`` (scene.hpp:33-43),
+``RenderSettings`` (renderer.hpp:15-22), ``StageTimes`` (renderer.hpp:105-112) and
+``render_frame`` (renderer.hpp:114-123). Everything below calls the in-tree native
+libraries; the render itself runs only on the B200 through include/gscg.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import native as N
+
+K_ALPHA_MAX = 0.99
+K_ALPHA_CUTOFF = np.float32(1.0) / np.float32(255.0)
+
+
+@dataclass
+class SceneConfig:
+    template_count: int = 1
+    template_seed_base: int = 100
+    level_counts: Sequence[int] = (60, 24, 8)
+    joint_count: int = 24
+    with_sh: bool = False
+    motion_count: int = 1
+    motion_seed_base: int = 500
+    motion_fps: float = 30.0
+    motion_frames: int = 24
+    grid_rows: int = 1
+    grid_cols: int = 1
+    grid_spacing: float = 1.0
+    crowd_count: int = 1
+    crowd_seed: int = 1
+    cam_pos: Sequence[float] = (0.0, 1.6, -3.0)
+    cam_look: Sequence[float] = (0.0, 1.0, 5.0)
+    fov_y_deg: float = 50.0
+    width: int = 160
+    height: int = 90
+    near_m: float = 0.1
+    lod_thresholds: Sequence[float] = (5.0, 10.0)
+    lod_hysteresis: float = 0.0
+
+    def native(self) -> N.GschSceneConfig:
+        c = N.GschSceneConfig()
+        c.template_count = self.template_count
+        c.template_seed_base = self.template_seed_base
+        c.level_count = len(self.level_counts)
+        for i, v in enumerate(self.level_counts):
+            c.level_counts[i] = int(v)
+        c.joint_count = self.joint_count
+        c.with_sh = int(bool(self.with_sh))
+        c.motion_count = self.motion_count
+        c.motion_seed_base = self.motion_seed_base
+        c.motion_fps = self.motion_fps
+        c.motion_frames = self.motion_frames
+        c.grid_rows, c.grid_cols = self.grid_rows, self.grid_cols
+        c.grid_spacing = self.grid_spacing
+        c.crowd_count = self.crowd_count
+        c.crowd_seed = self.crowd_seed
+        for i in range(3):
+            c.cam_pos[i] = self.cam_pos[i]
+            c.cam_look[i] = self.cam_look[i]
+        c.fov_y_deg = self.fov_y_deg
+        c.width, c.height = self.width, self.height
+        c.near_m = self.near_m
+        c.lod_threshold_count = len(self.lod_thresholds)
+        for i, v in enumerate(self.lod_thresholds):
+            c.lod_thresholds[i] = v
+        c.lod_hysteresis = self.lod_hysteresis
+        return c
+
+
+@dataclass
+class RenderSettings:
+    tile_size: int = 16
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+    alpha_max: float = K_ALPHA_MAX
+    alpha_cutoff: float = float(K_ALPHA_CUTOFF)
+    transmittance_floor: float = 1e-4
+    thread_count: int = 0
+    sh_colour: bool = True
+
+    def native(self) -> N.GschRenderSettings:
+        s = N.GschRenderSettings()
+        s.tile_size = self.tile_size
+        for i in range(3):
+            s.background[i] = self.background[i]
+        s.alpha_max = self.alpha_max
+        s.alpha_cutoff = self.alpha_cutoff
+        s.transmittance_floor = self.transmittance_floor
+        s.thread_count = self.thread_count
+        s.sh_colour = int(bool(self.sh_colour))
+        return s
+
+
+@dataclass
+class StageTimes:
+    update_ms: float = 0.0
+    gather_ms: float = 0.0
+    sort_ms: float = 0.0
+    rasterize_ms: float = 0.0
+    pose_ms: float = 0.0
+    splat_count: int = 0
+    pair_count: int = 0
+    gaussian_count: int = 0
+
+    @property
+    def total_ms(self) -> float:
+        return self.update_ms + self.gather_ms + self.sort_ms + self.rasterize_ms
+
+
+INSTANCE_DTYPE = np.dtype([("instance_id", "<u4"), ("template_id", "<u4"), ("motion_id", "<u4"), ("x", "<f4"),
+                           ("z", "<f4"), ("yaw", "<f4"), ("phase_offset_s", "<f4"), ("active_lod", "<u4")])
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class Scene:
+    """Synthetic templates + motions + crowd (build_crowd) + camera, held by the host lib."""
+
+    def __init__(self, cfg: SceneConfig, threads: int = 0):
+        self.cfg = cfg
+        h = C.c_void_p()
+        N.check_gsch(N.gsch().gsch_scene_create(C.byref(cfg.native()), threads, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.gsch().gsch_scene_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def counts(self) -> tuple[int, int, int]:
+        t, m, n = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        N.check_gsch(N.gsch().gsch_scene_counts(self._h, C.byref(t), C.byref(m), C.byref(n)))
+        return t.value, m.value, n.value
+
+    @property
+    def instances(self) -> np.ndarray:
+        n = self.counts()[2]
+        out = np.zeros(n, dtype=INSTANCE_DTYPE)
+        if n:
+            N.check_gsch(N.gsch().gsch_scene_get_instances(self._h, _ptr(out), n))
+        return out
+
+    @instances.setter
+    def instances(self, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr, dtype=INSTANCE_DTYPE)
+        N.check_gsch(N.gsch().gsch_scene_set_instances(self._h, _ptr(arr) if len(arr) else None, len(arr)))
+
+    def set_camera(self, pos, look, fov_y_deg=50.0, width=None, height=None, near_m=0.1) -> None:
+        p = np.asarray(pos, dtype=np.float32)
+        l = np.asarray(look, dtype=np.float32)
+        w = width if width is not None else self.cfg.width
+        hgt = height if height is not None else self.cfg.height
+        N.check_gsch(N.gsch().gsch_scene_set_camera(self._h, _ptr(p), _ptr(l), fov_y_deg, w, hgt, near_m))
+        self.cfg.cam_pos, self.cfg.cam_look, self.cfg.fov_y_deg = tuple(pos), tuple(look), fov_y_deg
+        self.cfg.width, self.cfg.height, self.cfg.near_m = w, hgt, near_m
+
+    def camera_basis(self) -> N.GscgCamera:
+        cam = N.GscgCamera()
+        N.check_gsch(N.gsch().gsch_scene_camera_basis(self._h, C.byref(cam)))
+        return cam
+
+    def set_lod_policy(self, thresholds: Sequence[float], hysteresis: float = 0.0) -> None:
+        th = np.asarray(thresholds, dtype=np.float32)
+        N.check_gsch(N.gsch().gsch_scene_set_lod_policy(self._h, _ptr(th) if len(th) else None, len(th), hysteresis))
+        self.cfg.lod_thresholds, self.cfg.lod_hysteresis = tuple(thresholds), hysteresis
+
+    def level_count(self, t: int) -> int:
+        out = C.c_uint32()
+        N.check_gsch(N.gsch().gsch_scene_level_count(self._h, t, C.byref(out)))
+        return out.value
+
+    def level_view(self, t: int, l: int) -> dict[str, np.ndarray]:
+        v = N.GschLevelView()
+        N.check_gsch(N.gsch().gsch_scene_level_view(self._h, t, l, C.byref(v)))
+        n = v.count
+
+        def arr(ptr, ctype, shape):
+            if not ptr:
+                return None
+            size = int(np.prod(shape))
+            buf = (ctype * size).from_address(ptr)
+            return np.ctypeslib.as_array(buf).reshape(shape).copy()
+
+        return {
+            "count": n,
+            "means": arr(v.means, C.c_float, (n, 3)),
+            "rotations": arr(v.rotations, C.c_float, (n, 4)),
+            "scales": arr(v.scales, C.c_float, (n, 3)),
+            "opacities": arr(v.opacities, C.c_float, (n,)),
+            "colors": arr(v.colors, C.c_float, (n, 3)),
+            "skin_indices": arr(v.skin_indices, C.c_uint16, (n, 4)),
+            "skin_weights": arr(v.skin_weights, C.c_float, (n, 4)),
+            "sh": arr(v.sh, C.c_float, (n, 45)),
+            "cov6": arr(v.cov6, C.c_float, (n, 6)),
+        }
+
+    def skeleton(self, t: int) -> dict[str, np.ndarray]:
+        j = C.c_uint32()
+        par, ib = C.c_void_p(), C.c_void_p()
+        N.check_gsch(N.gsch().gsch_scene_skeleton(self._h, t, C.byref(j), C.byref(par), C.byref(ib)))
+        J = j.value
+        parents = np.ctypeslib.as_array((C.c_int16 * J).from_address(par.value)).copy()
+        inv = np.ctypeslib.as_array((C.c_float * (16 * J)).from_address(ib.value)).reshape(J, 16).copy()
+        return {"joint_count": J, "parents": parents, "inverse_bind": inv}
+
+    def motion(self, m: int) -> dict:
+        fps, frames, joints = C.c_float(), C.c_uint32(), C.c_uint32()
+        N.check_gsch(N.gsch().gsch_scene_motion(self._h, m, C.byref(fps), C.byref(frames), C.byref(joints), None))
+        data = np.zeros((frames.value, 4 + 4 * joints.value), dtype=np.float32)
+        N.check_gsch(N.gsch().gsch_scene_motion(self._h, m, None, None, None, _ptr(data)))
+        return {"fps": fps.value, "frames": frames.value, "joints": joints.value, "data": data}
+
+
+class Renderer:
+    """FrameContext on a B200: owns the gscg context and the uploaded template store."""
+
+    def __init__(self, scene: Scene, device: int = 0):
+        self.scene = scene
+        h = C.c_void_p()
+        N.check_gsch(N.gsch().gsch_renderer_create(scene.handle, device, C.byref(h)))
+        self._h = h
+        self.gpu = C.c_void_p(N.gsch().gsch_renderer_gpu(h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.gsch().gsch_renderer_destroy(self._h)
+            self._h = None
+
+    @property
+    def joint_stride(self) -> int:
+        return int(N.gsch().gsch_renderer_joint_stride(self._h))
+
+    def render_frame(self, time_s: float, settings: Optional[RenderSettings] = None, static_pose: bool = False,
+                     forced_lod: Optional[int] = None, times: Optional[StageTimes] = None):
+        settings = settings or RenderSettings()
+        W, H = self.scene.cfg.width, self.scene.cfg.height
+        rgb = np.empty((H, W, 3), dtype=np.float32)
+        T = np.empty((H, W), dtype=np.float32)
+        st = N.GschStageTimes()
+        N.check_gsch(N.gsch().gsch_render(self._h, time_s, int(static_pose), -1 if forced_lod is None else forced_lod,
+                                          C.byref(settings.native()), _ptr(rgb), _ptr(T), C.byref(st)))
+        if times is not None:
+            for f in ("update_ms", "gather_ms", "sort_ms", "rasterize_ms", "pose_ms", "splat_count", "pair_count",
+                      "gaussian_count"):
+                setattr(times, f, getattr(st, f))
+        return rgb, T
+
+    def sample_crowd(self, time_s: float, static_pose: bool = False, threads: int = 0):
+        n = self.scene.counts()[2]
+        js = self.joint_stride
+        tids = np.zeros(n, dtype=np.uint32)
+        place = np.zeros((n, 4), dtype=np.float32)
+        poses = np.zeros((n, 4 + 4 * js), dtype=np.float32)
+        N.check_gsch(N.gsch().gsch_sample_crowd(self._h, time_s, int(static_pose), threads, _ptr(tids), _ptr(place),
+                                                _ptr(poses)))
+        return tids, place, poses
+
+    # ---- parity / debug exports (include/gscg.h) ----
+    def set_debug(self, flags: int) -> None:
+        N.check_gscg(N.gscg().gscg_set_debug(self.gpu, flags), self.gpu)
+
+    def counts(self) -> tuple[int, int, int]:
+        g, s, k = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        N.check_gscg(N.gscg().gscg_get_counts(self.gpu, C.byref(g), C.byref(s), C.byref(k)), self.gpu)
+        return g.value, s.value, k.value
+
+    def lods(self) -> np.ndarray:
+        n = self.scene.counts()[2]
+        out = np.zeros(n, dtype=np.uint32)
+        N.check_gscg(N.gscg().gscg_get_lod(self.gpu, _ptr(out), n), self.gpu)
+        return out
+
+    def instance_base(self) -> np.ndarray:
+        n = self.scene.counts()[2]
+        out = np.zeros(n, dtype=np.uint32)
+        N.check_gscg(N.gscg().gscg_get_instance_base(self.gpu, _ptr(out), n), self.gpu)
+        return out
+
+    def posed_means(self) -> np.ndarray:
+        g = self.counts()[0]
+        out = np.zeros((g, 3), dtype=np.float32)
+        N.check_gscg(N.gscg().gscg_get_posed_means(self.gpu, _ptr(out), g), self.gpu)
+        return out
+
+    def splat_records(self) -> np.ndarray:
+        s = self.counts()[1]
+        out = (N.GscgSplatRecord * max(s, 1))()
+        N.check_gscg(N.gscg().gscg_get_splat_records(self.gpu, C.addressof(out), s), self.gpu)
+        return np.ctypeslib.as_array(out)[:s].copy() if s else np.zeros(0, dtype=np.ctypeslib.as_array(out).dtype)
+
+    def tile_ranges(self, tiles: int) -> np.ndarray:
+        out = np.zeros((tiles, 2), dtype=np.uint32)
+        N.check_gscg(N.gscg().gscg_get_tile_ranges(self.gpu, _ptr(out), tiles), self.gpu)
+        return out
+
+    def sorted_ordinals(self) -> np.ndarray:
+        k = self.counts()[2]
+        out = np.zeros(max(k, 1), dtype=np.uint32)
+        N.check_gscg(N.gscg().gscg_get_sorted_ordinals(self.gpu, _ptr(out), k), self.gpu)
+        return out[:k]
+
+
+def render_frame(renderer: Renderer, time_s: float, settings: Optional[RenderSettings] = None,
+                 static_pose: bool = False, forced_lod: Optional[int] = None,
+                 times: Optional[StageTimes] = None) -> np.ndarray:
+    """render_frame(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx) -> Framebuffer."""
+    rgb, _ = renderer.render_frame(time_s, settings, static_pose, forced_lod, times)
+    return rgb
+
+
+# ---------------------------------------------------------------- BASELINE configs
+LEVELS_PAPER = (202738, 12661, 3176)
+
+
+def baseline_config(index: int) -> tuple[SceneConfig, dict]:
+    """Scene for BASELINE.json configs[index-1]; extra dict: time_s, forced_lod, instance override."""
+    if index == 1:
+        cfg = SceneConfig(template_count=1, template_seed_base=42, level_counts=(100000,), with_sh=True,
+                          motion_count=1, motion_seed_base=500, motion_frames=60, grid_rows=1, grid_cols=1,
+                          crowd_count=1, crowd_seed=1, cam_pos=(0.0, 0.95, -2.2), cam_look=(0.0, 0.95, 0.0),
+                          width=512, height=512)
+        return cfg, {"time_s": 0.5, "forced_lod": None, "origin_instance": True}
+    grids = {2: (10, 10, 100, 1920, 1080), 3: (59, 60, 3500, 1920, 1080), 4: (100, 100, 10000, 3840, 2160),
+             5: (59, 60, 3500, 1920, 1080)}
+    rows, cols, count, w, h = grids[index]
+    cx = (cols - 1) / 2.0
+    cfg = SceneConfig(template_count=14, template_seed_base=100, level_counts=LEVELS_PAPER, with_sh=True,
+                      motion_count=15, motion_seed_base=500, motion_frames=60, grid_rows=rows, grid_cols=cols,
+                      crowd_count=count, crowd_seed=1, cam_pos=(cx, 1.6, -3.0), cam_look=(cx, 1.0, 5.0),
+                      width=w, height=h)
+    return cfg, {"time_s": 0.0, "forced_lod": 0 if index == 5 else None, "origin_instance": False}
+
+
+def place_origin_instance(scene: Scene) -> None:
+    inst = scene.instances
+    inst["x"] = 0.0
+    inst["z"] = 0.0
+    inst["yaw"] = 0.0
+    inst["phase_offset_s"] = 0.0
+    inst["template_id"] = 0
+    inst["motion_id"] = 0
+    scene.instances = inst

@@ -1,0 +1,794 @@
+// C-ABI of the B200 crowd-render path (include/gscg.h): context, shared attribute store
+// upload, per-frame orchestration and parity exports.
+//
+// Frame schedule on the context stream (render_frame, renderer.cpp:249-280):
+//   H2D of the frame records (pinned staging, one copy)
+//   update:    k_lod_plan (1 CTA) -> k_fk_skin
+//   gather:    k_project (persistent, template-major)       -> counters readback (sync)
+//   sort:      k_digit_histogram -> k_digit_scan -> k_onesweep x P -> k_tie_fixup -> k_tile_ranges
+//   rasterize: k_raster16 (or k_raster_generic for other tile sizes)
+//   D2H of framebuffer / transmittance / active LoDs (host mode)
+// The one mid-frame synchronisation reads S, K and the depth-bit range: it sizes the
+// sort and detects capacity overflow (buffers grow to the high-water mark and the
+// gather is replayed, as the reference's buffers grow, crowd.hpp:26-28).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gscg_common.cuh"
+#include "gscg_kernels.h"
+
+using namespace gscg;
+
+namespace {
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+    // Grow-only; contents are not preserved.
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && ptr) return cudaSuccess;
+        release();
+        const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e != cudaSuccess) {
+            ptr = nullptr;
+            return e;
+        }
+        cap = want;
+        return cudaSuccess;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+};
+
+struct LevelStore {
+    uint32_t count = 0;
+    DevBuf core, weights, sh;
+    bool has_sh = false;
+    std::vector<float> opacities;  // host copy for the power-floor table
+    float pf_cutoff = -1.0f;
+};
+
+struct TemplateStore {
+    bool present = false;
+    uint32_t joint_count = 0;
+    std::vector<int16_t> parents;
+    std::vector<float> local_bind, inverse_bind;
+    float pelvis_y = 0.0f;
+    std::vector<LevelStore> levels;
+};
+
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            throw Status(_e == cudaErrorMemoryAllocation ? GSCG_ERR_OOM : GSCG_ERR_CUDA,   \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+    } while (0)
+
+}  // namespace
+
+struct gscg_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    std::string error;
+    uint32_t debug = 0;
+
+    std::vector<TemplateStore> templates;
+    bool tables_dirty = true;
+    DevBuf d_templates, d_groups, d_mats, d_parents;
+    uint32_t group_count = 0;
+    uint32_t joint_stride = 0;
+
+    // frame inputs
+    DevBuf template_ids, placement, poses, lod_prev, lod_out;
+    // plan outputs
+    DevBuf inst_group, inst_base, members, group_inst_start, group_inst_count, group_item_start;
+    DevBuf skin, counters;
+    // gather outputs
+    DevBuf records, record_ordinal, keys[2], vals[2];
+    uint64_t splat_capacity = 0, pair_capacity = 0;
+    // sort
+    DevBuf hist, status, ranges, sorted_ordinals;
+    uint32_t epoch = 1;
+    // output
+    DevBuf fb_rgb, fb_T;
+    // debug
+    DevBuf posed_dbg, rec_dbg;
+
+    void* pinned = nullptr;
+    size_t pinned_cap = 0;
+    FrameCounters* h_counters = nullptr;
+    cudaEvent_t ev[8] = {};
+
+    // last frame
+    uint32_t n = 0, tiles = 0, final_buf = 0;
+    uint64_t G = 0, S = 0, K = 0;
+
+    void ensure_pinned(size_t bytes) {
+        if (bytes <= pinned_cap) return;
+        if (pinned) cudaFreeHost(pinned);
+        pinned = nullptr;
+        const size_t want = bytes + bytes / 4;
+        CUDA_TRY(cudaMallocHost(&pinned, want));
+        pinned_cap = want;
+    }
+};
+
+namespace {
+
+int fail(gscg_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->error = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(gscg_ctx* ctx, F&& f) {
+    try {
+        f();
+        return GSCG_OK;
+    } catch (const Status& s) {
+        return fail(ctx, s.code, s.what());
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, GSCG_ERR_OOM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(ctx, GSCG_ERR_STATE, e.what());
+    }
+}
+
+void invalid(const std::string& msg) { throw Status(GSCG_ERR_INVALID_ARGUMENT, msg); }
+
+void upload_tables(gscg_ctx* ctx) {
+    if (!ctx->tables_dirty) return;
+    std::vector<TemplateDev> tdev(ctx->templates.size());
+    std::vector<GroupDev> gdev;
+    std::vector<float> mats;
+    std::vector<int32_t> parents;
+    uint32_t stride = 0;
+    for (size_t t = 0; t < ctx->templates.size(); ++t) {
+        const TemplateStore& ts = ctx->templates[t];
+        TemplateDev& d = tdev[t];
+        std::memset(&d, 0, sizeof(d));
+        if (!ts.present) continue;
+        d.joint_count = static_cast<int32_t>(ts.joint_count);
+        d.level_count = static_cast<int32_t>(ts.levels.size());
+        d.group_base = static_cast<int32_t>(gdev.size());
+        d.mat_offset = static_cast<int32_t>(mats.size() / 16);
+        d.parent_offset = static_cast<int32_t>(parents.size());
+        d.pelvis_y = ts.pelvis_y;
+        mats.insert(mats.end(), ts.local_bind.begin(), ts.local_bind.end());
+        mats.insert(mats.end(), ts.inverse_bind.begin(), ts.inverse_bind.end());
+        for (int16_t p : ts.parents) parents.push_back(p);
+        stride = std::max(stride, ts.joint_count);
+        for (size_t l = 0; l < ts.levels.size(); ++l) {
+            const LevelStore& ls = ts.levels[l];
+            if (ls.count == 0) invalid("template " + std::to_string(t) + " level " + std::to_string(l) + " missing");
+            GroupDev g{};
+            g.core = ls.core.as<float4>();
+            g.weights = ls.weights.as<float4>();
+            g.sh = ls.has_sh ? ls.sh.as<float>() : nullptr;
+            g.count = ls.count;
+            g.template_id = static_cast<uint32_t>(t);
+            g.level = static_cast<uint32_t>(l);
+            gdev.push_back(g);
+        }
+    }
+    if (gdev.size() > static_cast<size_t>(kMaxGroups)) invalid("too many (template, level) groups");
+    ctx->group_count = static_cast<uint32_t>(gdev.size());
+    ctx->joint_stride = stride;
+    CUDA_TRY(ctx->d_templates.ensure(std::max<size_t>(1, tdev.size()) * sizeof(TemplateDev)));
+    CUDA_TRY(ctx->d_groups.ensure(std::max<size_t>(1, gdev.size()) * sizeof(GroupDev)));
+    CUDA_TRY(ctx->d_mats.ensure(std::max<size_t>(1, mats.size()) * sizeof(float)));
+    CUDA_TRY(ctx->d_parents.ensure(std::max<size_t>(1, parents.size()) * sizeof(int32_t)));
+    if (!tdev.empty())
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_templates.ptr, tdev.data(), tdev.size() * sizeof(TemplateDev), cudaMemcpyHostToDevice, ctx->stream));
+    if (!gdev.empty())
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_groups.ptr, gdev.data(), gdev.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, ctx->stream));
+    if (!mats.empty())
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_mats.ptr, mats.data(), mats.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    if (!parents.empty())
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_parents.ptr, parents.data(), parents.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->tables_dirty = false;
+}
+
+// power_floor = logf(alpha_cutoff / opacity) with the host libm (renderer.cpp:140).
+void refresh_power_floor(gscg_ctx* ctx, float cutoff) {
+    std::vector<float> pf;
+    DevBuf tmp;
+    for (TemplateStore& ts : ctx->templates) {
+        if (!ts.present) continue;
+        for (LevelStore& ls : ts.levels) {
+            if (ls.pf_cutoff == cutoff) continue;
+            pf.resize(ls.count);
+            for (uint32_t i = 0; i < ls.count; ++i) pf[i] = std::log(cutoff / ls.opacities[i]);
+            CUDA_TRY(tmp.ensure(ls.count * sizeof(float)));
+            CUDA_TRY(cudaMemcpyAsync(tmp.ptr, pf.data(), ls.count * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+            k_set_power_floor<<<(ls.count + 255) / 256, 256, 0, ctx->stream>>>(ls.core.as<float4>(), tmp.as<float>(), ls.count);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            ls.pf_cutoff = cutoff;
+        }
+    }
+    tmp.release();
+}
+
+int bits_for(uint32_t v) { return v == 0 ? 0 : 32 - __builtin_clz(v); }
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gscg_device_count(int* out) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    if (out) *out = n;
+    return GSCG_OK;
+}
+
+int gscg_create(int device, gscg_ctx** out) {
+    if (!out) return GSCG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* ctx = new gscg_ctx();
+    ctx->device = device;
+    const int st = guarded(ctx, [&] {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            throw Status(GSCG_ERR_CUDA, "no CUDA device: the B200 render path has no CPU fallback");
+        if (device < 0 || device >= count) invalid("device index out of range");
+        CUDA_TRY(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            throw Status(GSCG_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (Blackwell)");
+        ctx->sm_count = prop.multiProcessorCount;
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+        CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
+        CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
+        CUDA_TRY(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSortTile * (sizeof(unsigned long long) + sizeof(uint32_t))));
+        CUDA_TRY(cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kProjectThreads * kShFloats * 4 + kMaxJoints * 12 * 4));
+    });
+    *out = ctx;
+    return st;
+}
+
+int gscg_destroy(gscg_ctx* ctx) {
+    if (!ctx) return GSCG_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (TemplateStore& t : ctx->templates)
+        for (LevelStore& l : t.levels) {
+            l.core.release();
+            l.weights.release();
+            l.sh.release();
+        }
+    DevBuf* bufs[] = {&ctx->d_templates, &ctx->d_groups, &ctx->d_mats, &ctx->d_parents,
+                      &ctx->template_ids, &ctx->placement, &ctx->poses, &ctx->lod_prev,
+                      &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members,
+                      &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
+                      &ctx->skin, &ctx->counters, &ctx->records, &ctx->record_ordinal,
+                      &ctx->keys[0], &ctx->keys[1], &ctx->vals[0], &ctx->vals[1], &ctx->hist,
+                      &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
+                      &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg};
+    for (DevBuf* b : bufs) b->release();
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return GSCG_OK;
+}
+
+const char* gscg_last_error(const gscg_ctx* ctx) { return ctx ? ctx->error.c_str() : "null context"; }
+
+int gscg_set_debug(gscg_ctx* ctx, uint32_t flags) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    ctx->debug = flags;
+    return GSCG_OK;
+}
+
+int gscg_upload_skeleton(gscg_ctx* ctx, uint32_t template_id, const gscg_skeleton_desc* d) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (!d || !d->parents || !d->local_bind || !d->inverse_bind) invalid("null skeleton field");
+        if (d->joint_count < 1 || d->joint_count > GSCG_MAX_JOINTS) invalid("joint_count outside [1, 64]");
+        if (d->parents[0] >= 0) invalid("Skeleton: exactly one root at index 0 required");
+        for (uint32_t j = 1; j < d->joint_count; ++j)
+            if (d->parents[j] < 0 || static_cast<uint32_t>(d->parents[j]) >= j)
+                invalid("Skeleton: parent index must precede child");
+        if (template_id >= ctx->templates.size()) ctx->templates.resize(template_id + 1);
+        TemplateStore& t = ctx->templates[template_id];
+        t.present = true;
+        t.joint_count = d->joint_count;
+        t.parents.assign(d->parents, d->parents + d->joint_count);
+        t.local_bind.assign(d->local_bind, d->local_bind + 16 * d->joint_count);
+        t.inverse_bind.assign(d->inverse_bind, d->inverse_bind + 16 * d->joint_count);
+        t.pelvis_y = d->pelvis_y;
+        ctx->tables_dirty = true;
+    });
+}
+
+int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level, const gscg_level_desc* d) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (template_id >= ctx->templates.size() || !ctx->templates[template_id].present)
+            invalid("upload the skeleton before its levels");
+        if (!d || !d->means || !d->cov6 || !d->opacities || !d->colors || !d->skin_indices || !d->skin_weights)
+            invalid("null level field");
+        const uint32_t n = d->gaussian_count;
+        if (n == 0) invalid("LodLevel: empty");
+        TemplateStore& t = ctx->templates[template_id];
+        if (level > t.levels.size()) invalid("levels must be uploaded in order");
+        if (level == t.levels.size()) t.levels.emplace_back();
+        LevelStore& ls = t.levels[level];
+        for (uint32_t i = 0; i < n; ++i)
+            for (int k = 0; k < 4; ++k)
+                if (d->skin_indices[4 * i + k] >= t.joint_count) invalid("LodLevel: skin index out of range");
+        std::vector<float> core(static_cast<size_t>(n) * 16);
+        for (uint32_t i = 0; i < n; ++i) {
+            float* c = core.data() + 16 * static_cast<size_t>(i);
+            c[0] = d->means[3 * i + 0];
+            c[1] = d->means[3 * i + 1];
+            c[2] = d->means[3 * i + 2];
+            c[3] = d->opacities[i];
+            for (int k = 0; k < 6; ++k) (k < 4 ? c[4 + k] : c[8 + (k - 4)]) = d->cov6[6 * i + k];
+            c[10] = d->colors[3 * i + 0];
+            c[11] = d->colors[3 * i + 1];
+            c[12] = d->colors[3 * i + 2];
+            c[13] = 0.0f;  // power floor, filled per alpha_cutoff
+            const uint32_t i01 = d->skin_indices[4 * i + 0] | (static_cast<uint32_t>(d->skin_indices[4 * i + 1]) << 16);
+            const uint32_t i23 = d->skin_indices[4 * i + 2] | (static_cast<uint32_t>(d->skin_indices[4 * i + 3]) << 16);
+            std::memcpy(&c[14], &i01, 4);
+            std::memcpy(&c[15], &i23, 4);
+        }
+        ls.count = n;
+        CUDA_TRY(ls.core.ensure(core.size() * sizeof(float)));
+        CUDA_TRY(cudaMemcpyAsync(ls.core.ptr, core.data(), core.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(ls.weights.ensure(static_cast<size_t>(n) * 16));
+        CUDA_TRY(cudaMemcpyAsync(ls.weights.ptr, d->skin_weights, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, ctx->stream));
+        ls.has_sh = d->sh != nullptr;
+        if (ls.has_sh) {
+            // Pad to a whole 256-Gaussian chunk so chunk copies stay in bounds.
+            const size_t chunks = (n + kProjectThreads - 1) / kProjectThreads;
+            const size_t bytes = chunks * kProjectThreads * kShFloats * sizeof(float);
+            CUDA_TRY(ls.sh.ensure(bytes));
+            CUDA_TRY(cudaMemsetAsync(ls.sh.ptr, 0, bytes, ctx->stream));
+            CUDA_TRY(cudaMemcpyAsync(ls.sh.ptr, d->sh, static_cast<size_t>(n) * kShFloats * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        } else {
+            ls.sh.release();
+        }
+        ls.opacities.assign(d->opacities, d->opacities + n);
+        ls.pf_cutoff = -1.0f;
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        ctx->tables_dirty = true;
+    });
+}
+
+int gscg_template_bytes(const gscg_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    uint64_t b = 0;
+    for (const TemplateStore& t : ctx->templates)
+        for (const LevelStore& l : t.levels) b += l.core.cap + l.weights.cap + l.sh.cap;
+    *out = b;
+    return GSCG_OK;
+}
+
+int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                      const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                      float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (!frame || !cam || !settings || !lod) invalid("null argument");
+        if (settings->tile_size < 1 || settings->tile_size > 64) invalid("RenderSettings: tile_size must be in [1, 64]");
+        if (!(settings->alpha_cutoff > 0.0f && settings->alpha_cutoff < 1.0f))
+            invalid("RenderSettings: alpha_cutoff outside (0,1)");
+        if (!(settings->transmittance_floor > 0.0f && settings->transmittance_floor < 1.0f))
+            invalid("RenderSettings: transmittance_floor outside (0,1)");
+        if (cam->width < 1 || cam->height < 1 || cam->width > 65535 || cam->height > 65535)
+            invalid("Camera: width and height must be in [1, 65535]");
+        if (!(cam->near_m > 0.0f)) invalid("Camera: near plane must be > 0");
+        if (lod->threshold_count > GSCG_MAX_LOD_THRESHOLDS) invalid("LodPolicy: too many thresholds");
+        const bool host = frame->memory == GSCG_MEM_HOST;
+        const uint32_t n = frame->instance_count;
+        if (n > 0 && (!frame->template_ids || !frame->placement || !frame->poses || !frame->active_lod))
+            invalid("null frame array");
+        upload_tables(ctx);
+        if (n > 0 && frame->joint_stride < ctx->joint_stride) invalid("joint_stride below the largest skeleton");
+        if (host) {
+            for (uint32_t i = 0; i < n; ++i) {
+                const uint32_t t = frame->template_ids[i];
+                if (t >= ctx->templates.size() || !ctx->templates[t].present || ctx->templates[t].levels.empty())
+                    invalid("instance " + std::to_string(i) + " references a missing template");
+            }
+        }
+        refresh_power_floor(ctx, settings->alpha_cutoff);
+
+        cudaStream_t s = ctx->stream;
+        const uint32_t js = std::max<uint32_t>(ctx->joint_stride, 1);
+        const uint32_t pose_stride = 4 + 4 * frame->joint_stride;
+        const int W = cam->width, H = cam->height, ts = settings->tile_size;
+        const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
+        const uint32_t tiles = static_cast<uint32_t>(tiles_x) * tiles_y;
+        uint32_t launches = 0;
+
+        CUDA_TRY(ctx->template_ids.ensure(std::max<size_t>(n, 1) * 4));
+        CUDA_TRY(ctx->placement.ensure(std::max<size_t>(n, 1) * 16));
+        CUDA_TRY(ctx->poses.ensure(std::max<size_t>(n, 1) * pose_stride * 4));
+        CUDA_TRY(ctx->lod_prev.ensure(std::max<size_t>(n, 1) * 4));
+        CUDA_TRY(ctx->lod_out.ensure(std::max<size_t>(n, 1) * 4));
+        CUDA_TRY(ctx->inst_group.ensure(std::max<size_t>(n, 1) * 4));
+        CUDA_TRY(ctx->inst_base.ensure(std::max<size_t>(n, 1) * 4));
+        CUDA_TRY(ctx->members.ensure(std::max<size_t>(n, 1) * 4));
+        CUDA_TRY(ctx->group_inst_start.ensure((kMaxGroups + 1) * 4));
+        CUDA_TRY(ctx->group_inst_count.ensure((kMaxGroups + 1) * 4));
+        CUDA_TRY(ctx->group_item_start.ensure((kMaxGroups + 1) * 4));
+        CUDA_TRY(ctx->skin.ensure(std::max<size_t>(n, 1) * js * 12 * 4));
+        CUDA_TRY(ctx->fb_rgb.ensure(static_cast<size_t>(W) * H * 12));
+        CUDA_TRY(ctx->fb_T.ensure(static_cast<size_t>(W) * H * 4));
+        CUDA_TRY(ctx->ranges.ensure(static_cast<size_t>(tiles) * 8));
+
+        // ---- H2D ----
+        CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
+        const uint32_t *d_tid, *d_lodprev;
+        const float *d_place, *d_poses;
+        if (host) {
+            const size_t b_tid = n * 4ull, b_place = n * 16ull, b_pose = n * 4ull * pose_stride, b_lod = n * 4ull;
+            ctx->ensure_pinned(b_tid + b_place + b_pose + b_lod + 64);
+            char* h = static_cast<char*>(ctx->pinned);
+            std::memcpy(h, frame->template_ids, b_tid);
+            std::memcpy(h + b_tid, frame->placement, b_place);
+            std::memcpy(h + b_tid + b_place, frame->poses, b_pose);
+            std::memcpy(h + b_tid + b_place + b_pose, frame->active_lod, b_lod);
+            if (n) {
+                CUDA_TRY(cudaMemcpyAsync(ctx->template_ids.ptr, h, b_tid, cudaMemcpyHostToDevice, s));
+                CUDA_TRY(cudaMemcpyAsync(ctx->placement.ptr, h + b_tid, b_place, cudaMemcpyHostToDevice, s));
+                CUDA_TRY(cudaMemcpyAsync(ctx->poses.ptr, h + b_tid + b_place, b_pose, cudaMemcpyHostToDevice, s));
+                CUDA_TRY(cudaMemcpyAsync(ctx->lod_prev.ptr, h + b_tid + b_place + b_pose, b_lod, cudaMemcpyHostToDevice, s));
+            }
+            d_tid = ctx->template_ids.as<uint32_t>();
+            d_place = ctx->placement.as<float>();
+            d_poses = ctx->poses.as<float>();
+            d_lodprev = ctx->lod_prev.as<uint32_t>();
+        } else {
+            d_tid = frame->template_ids;
+            d_place = frame->placement;
+            d_poses = frame->poses;
+            d_lodprev = frame->active_lod;
+        }
+        CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
+
+        const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + static_cast<int>(js) * 12 * 4;
+        int project_blocks_per_sm = 1;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project, kProjectThreads, project_smem));
+        project_blocks_per_sm = std::max(project_blocks_per_sm, 1);
+
+        auto* counters = ctx->counters.as<FrameCounters>();
+        for (int attempt = 0;; ++attempt) {
+            // ---- update ----
+            PlanParams pp{};
+            pp.n = n;
+            pp.template_ids = d_tid;
+            pp.placement = d_place;
+            pp.lod_prev = d_lodprev;
+            pp.forced_lod = frame->forced_lod;
+            pp.threshold_count = lod->threshold_count;
+            for (uint32_t i = 0; i < lod->threshold_count; ++i) pp.thresholds[i] = lod->thresholds_m[i];
+            pp.hysteresis = lod->hysteresis_band_m;
+            for (int i = 0; i < 3; ++i) pp.cam_pos[i] = cam->position[i];
+            pp.templates = ctx->d_templates.as<TemplateDev>();
+            pp.groups = ctx->d_groups.as<GroupDev>();
+            pp.group_count = ctx->group_count;
+            pp.lod_out = ctx->lod_out.as<uint32_t>();
+            pp.inst_group = ctx->inst_group.as<uint32_t>();
+            pp.inst_base = ctx->inst_base.as<uint32_t>();
+            pp.group_inst_start = ctx->group_inst_start.as<uint32_t>();
+            pp.group_inst_count = ctx->group_inst_count.as<uint32_t>();
+            pp.group_item_start = ctx->group_item_start.as<uint32_t>();
+            pp.members = ctx->members.as<uint32_t>();
+            pp.counters = counters;
+            k_lod_plan<<<1, 1024, 0, s>>>(pp);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+            if (n > 0) {
+                FkParams fp{};
+                fp.n = n;
+                fp.joint_stride = js;
+                fp.pose_stride = pose_stride;
+                fp.template_ids = d_tid;
+                fp.placement = d_place;
+                fp.poses = d_poses;
+                fp.templates = ctx->d_templates.as<TemplateDev>();
+                fp.mats = ctx->d_mats.as<float>();
+                fp.parents = ctx->d_parents.as<int32_t>();
+                fp.skin = ctx->skin.as<float>();
+                const int per_block = 16;
+                k_fk_skin<<<(n + per_block - 1) / per_block, 256, per_block * js * 16 * 4, s>>>(fp);
+                ++launches;
+                CUDA_TRY(cudaGetLastError());
+            }
+            CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
+
+            if (ctx->debug & GSCG_DEBUG_POSED) {
+                CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaStreamSynchronize(s));
+                CUDA_TRY(ctx->posed_dbg.ensure(std::max<uint64_t>(ctx->h_counters->gaussians, 1) * 12));
+            }
+            if (ctx->splat_capacity == 0) {
+                ctx->splat_capacity = 1u << 20;
+                ctx->pair_capacity = 1u << 21;
+            }
+            CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
+            CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
+            for (int b = 0; b < 2; ++b) {
+                CUDA_TRY(ctx->keys[b].ensure(ctx->pair_capacity * 8));
+                CUDA_TRY(ctx->vals[b].ensure(ctx->pair_capacity * 4));
+            }
+            if (ctx->debug & GSCG_DEBUG_RECORDS)
+                CUDA_TRY(ctx->rec_dbg.ensure(ctx->splat_capacity * sizeof(gscg_splat_record)));
+
+            // ---- gather ----
+            ProjectParams pj{};
+            std::memcpy(pj.cam.w, cam->world_to_view, sizeof(pj.cam.w));
+            std::memcpy(pj.cam.pos, cam->position, sizeof(pj.cam.pos));
+            pj.cam.focal = cam->focal;
+            pj.cam.cx = cam->cx;
+            pj.cam.cy = cam->cy;
+            pj.cam.near_m = cam->near_m;
+            pj.cam.width = W;
+            pj.cam.height = H;
+            pj.tile_size = ts;
+            pj.tiles_x = tiles_x;
+            pj.sh_enabled = settings->sh_enabled ? 1 : 0;
+            pj.joint_stride = js;
+            pj.group_count = ctx->group_count;
+            pj.groups = ctx->d_groups.as<GroupDev>();
+            pj.group_item_start = ctx->group_item_start.as<uint32_t>();
+            pj.group_inst_start = ctx->group_inst_start.as<uint32_t>();
+            pj.group_inst_count = ctx->group_inst_count.as<uint32_t>();
+            pj.members = ctx->members.as<uint32_t>();
+            pj.inst_base = ctx->inst_base.as<uint32_t>();
+            pj.skin = ctx->skin.as<float>();
+            pj.counters = counters;
+            pj.records = ctx->records.as<float4>();
+            pj.record_ordinal = ctx->record_ordinal.as<uint32_t>();
+            pj.keys = ctx->keys[0].as<unsigned long long>();
+            pj.values = ctx->vals[0].as<uint32_t>();
+            pj.splat_capacity = ctx->splat_capacity;
+            pj.pair_capacity = ctx->pair_capacity;
+            pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
+            pj.record_debug = (ctx->debug & GSCG_DEBUG_RECORDS) ? ctx->rec_dbg.as<gscg_splat_record>() : nullptr;
+            if (n > 0 && ctx->group_count > 0) {
+                k_project<<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
+                ++launches;
+                CUDA_TRY(cudaGetLastError());
+            }
+            CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
+            CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            const uint64_t S = ctx->h_counters->splat_pair >> 32;
+            const uint64_t K = ctx->h_counters->splat_pair & 0xffffffffull;
+            if (S <= ctx->splat_capacity && K <= ctx->pair_capacity) {
+                ctx->S = S;
+                ctx->K = K;
+                ctx->G = ctx->h_counters->gaussians;
+                break;
+            }
+            if (attempt > 2) throw Status(GSCG_ERR_STATE, "splat/pair capacity did not converge");
+            if (K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "tile-splat pair count exceeds 32-bit indexing");
+            ctx->splat_capacity = std::max<uint64_t>(ctx->splat_capacity, S + S / 4 + 1024);
+            ctx->pair_capacity = std::max<uint64_t>(ctx->pair_capacity, K + K / 4 + 1024);
+        }
+
+        // ---- sort ----
+        const uint32_t K = static_cast<uint32_t>(ctx->K);
+        CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(tiles) * 8, s));
+        uint32_t passes = 0, final_buf = 0;
+        if (K > 0) {
+            const uint32_t dmin = ctx->h_counters->depth_min_bits, dmax = ctx->h_counters->depth_max_bits;
+            const uint32_t dbits = static_cast<uint32_t>(bits_for(dmin ^ dmax));
+            const uint32_t tbits = static_cast<uint32_t>(bits_for(tiles - 1));
+            const unsigned long long dmask = dbits >= 32 ? 0xffffffffull : ((1ull << dbits) - 1ull);
+            passes = (dbits + tbits + 7) / 8;
+            const uint32_t nblocks = (K + kSortTile - 1) / kSortTile;
+            if (passes > 0) {
+                CUDA_TRY(ctx->hist.ensure(kMaxSortPasses * 256 * 4));
+                CUDA_TRY(ctx->status.ensure(static_cast<size_t>(nblocks) * 256 * 8));
+                CUDA_TRY(cudaMemsetAsync(ctx->hist.ptr, 0, kMaxSortPasses * 256 * 4, s));
+                const uint32_t hblocks = std::min<uint32_t>((K + 255) / 256, ctx->sm_count * 8);
+                k_digit_histogram<<<hblocks, 256, 0, s>>>(ctx->keys[0].as<unsigned long long>(), K, dbits, dmask, passes, ctx->hist.as<uint32_t>());
+                k_digit_scan<<<passes, 256, 0, s>>>(ctx->hist.as<uint32_t>(), passes);
+                launches += 2;
+                CUDA_TRY(cudaGetLastError());
+                for (uint32_t q = 0; q < passes; ++q) {
+                    SortPassParams sp{};
+                    sp.keys_in = ctx->keys[q & 1].as<unsigned long long>();
+                    sp.vals_in = ctx->vals[q & 1].as<uint32_t>();
+                    sp.keys_out = ctx->keys[(q + 1) & 1].as<unsigned long long>();
+                    sp.vals_out = ctx->vals[(q + 1) & 1].as<uint32_t>();
+                    sp.count = K;
+                    sp.dbits = dbits;
+                    sp.dmask = dmask;
+                    sp.shift = 8 * q;
+                    sp.digit_offsets = ctx->hist.as<uint32_t>() + 256 * q;
+                    sp.status = ctx->status.as<unsigned long long>();
+                    sp.ticket = &counters->sort_ticket[q];
+                    sp.epoch = ctx->epoch++;
+                    if (ctx->epoch >= 0x3fffffffu) ctx->epoch = 1;
+                    k_onesweep<<<nblocks, kSortThreads, kSortTile * 12, s>>>(sp);
+                    ++launches;
+                    CUDA_TRY(cudaGetLastError());
+                }
+                final_buf = passes & 1;
+            }
+            const uint32_t gblocks = std::min<uint32_t>((K + 255) / 256, ctx->sm_count * 8);
+            k_tie_fixup<<<gblocks, 256, 0, s>>>(ctx->keys[final_buf].as<unsigned long long>(), ctx->vals[final_buf].as<uint32_t>(), ctx->record_ordinal.as<uint32_t>(), K);
+            k_tile_ranges<<<gblocks, 256, 0, s>>>(ctx->keys[final_buf].as<unsigned long long>(), K, ctx->ranges.as<uint2>());
+            launches += 2;
+            CUDA_TRY(cudaGetLastError());
+        }
+        CUDA_TRY(cudaEventRecord(ctx->ev[4], s));
+
+        // ---- rasterize ----
+        RasterParams rp{};
+        rp.ranges = ctx->ranges.as<uint2>();
+        rp.values = ctx->vals[final_buf].as<uint32_t>();
+        rp.records = ctx->records.as<float4>();
+        rp.width = W;
+        rp.height = H;
+        rp.tile_size = ts;
+        rp.tiles_x = tiles_x;
+        for (int i = 0; i < 3; ++i) rp.bg[i] = settings->background[i];
+        rp.alpha_max = settings->alpha_max;
+        rp.t_floor = settings->transmittance_floor;
+        rp.out_rgb = ctx->fb_rgb.as<float>();
+        rp.out_T = ctx->fb_T.as<float>();
+        launch_raster(rp, tiles, s);
+        ++launches;
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(ctx->ev[5], s));
+
+        // ---- D2H ----
+        if (host) {
+            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, ctx->fb_rgb.ptr, static_cast<size_t>(W) * H * 12, cudaMemcpyDeviceToHost, s));
+            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, ctx->fb_T.ptr, static_cast<size_t>(W) * H * 4, cudaMemcpyDeviceToHost, s));
+            if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToHost, s));
+        } else {
+            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, ctx->fb_rgb.ptr, static_cast<size_t>(W) * H * 12, cudaMemcpyDeviceToDevice, s));
+            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, ctx->fb_T.ptr, static_cast<size_t>(W) * H * 4, cudaMemcpyDeviceToDevice, s));
+            if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice, s));
+        }
+        CUDA_TRY(cudaEventRecord(ctx->ev[6], s));
+        if (host || times) CUDA_TRY(cudaStreamSynchronize(s));
+
+        ctx->n = n;
+        ctx->tiles = tiles;
+        ctx->final_buf = final_buf;
+        if (times) {
+            times->h2d_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+            times->update_ms = elapsed(ctx->ev[1], ctx->ev[2]);
+            times->gather_ms = elapsed(ctx->ev[2], ctx->ev[3]);
+            times->sort_ms = elapsed(ctx->ev[3], ctx->ev[4]);
+            times->rasterize_ms = elapsed(ctx->ev[4], ctx->ev[5]);
+            times->d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+            times->splat_count = ctx->S;
+            times->pair_count = ctx->K;
+            times->gaussian_count = ctx->G;
+            times->sort_passes = passes;
+            times->kernel_launches = launches;
+        }
+    });
+}
+
+int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    if (rgb) *rgb = ctx->fb_rgb.as<float>();
+    if (T) *T = ctx->fb_T.as<float>();
+    return GSCG_OK;
+}
+
+int gscg_synchronize(gscg_ctx* ctx) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] { CUDA_TRY(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int gscg_get_counts(gscg_ctx* ctx, uint64_t* gaussians, uint64_t* splats, uint64_t* pairs) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    if (gaussians) *gaussians = ctx->G;
+    if (splats) *splats = ctx->S;
+    if (pairs) *pairs = ctx->K;
+    return GSCG_OK;
+}
+
+int gscg_get_lod(gscg_ctx* ctx, uint32_t* out, uint32_t n) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (n > ctx->n) invalid("more instances requested than rendered");
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gscg_get_instance_base(gscg_ctx* ctx, uint32_t* out, uint32_t n) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (n > ctx->n) invalid("more instances requested than rendered");
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->inst_base.ptr, n * 4ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gscg_get_posed_means(gscg_ctx* ctx, float* out, uint64_t gaussians) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (!(ctx->debug & GSCG_DEBUG_POSED)) invalid("enable GSCG_DEBUG_POSED before rendering");
+        if (gaussians > ctx->G) invalid("more Gaussians requested than rendered");
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->posed_dbg.ptr, gaussians * 12, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splats) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (!(ctx->debug & GSCG_DEBUG_RECORDS)) invalid("enable GSCG_DEBUG_RECORDS before rendering");
+        if (splats > ctx->S) invalid("more splats requested than rendered");
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->rec_dbg.ptr, splats * sizeof(gscg_splat_record), cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        std::sort(out, out + splats, [](const gscg_splat_record& a, const gscg_splat_record& b) {
+            return a.ordinal < b.ordinal;
+        });
+    });
+}
+
+int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t tiles) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (tiles > ctx->tiles) invalid("more tiles requested than rendered");
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->ranges.ptr, tiles * 8ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (pairs > ctx->K) invalid("more pairs requested than rendered");
+        if (pairs == 0) return;
+        CUDA_TRY(ctx->sorted_ordinals.ensure(pairs * 4));
+        k_sorted_ordinals<<<std::min<uint64_t>((pairs + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+            ctx->vals[ctx->final_buf].as<uint32_t>(), ctx->record_ordinal.as<uint32_t>(),
+            static_cast<uint32_t>(pairs), ctx->sorted_ordinals.as<uint32_t>());
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->sorted_ordinals.ptr, pairs * 4, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

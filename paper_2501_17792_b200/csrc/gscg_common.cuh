@@ -1,0 +1,77 @@
+// Shared device definitions for the B200 crowd-render kernels (sm_100a).
+//
+// Parity-critical arithmetic (skin matrices, LBS, LoD distance, EWA projection, conic,
+// per-pixel power) reproduces the reference's single-rounded SSE evaluation order
+// (SURVEY.md Appendix A). The translation units that hold it are compiled with
+// --fmad=false, and the expressions below are parenthesised in exactly the reference
+// order, so no FMA contraction or reassociation can change a bit.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gscg.h"
+
+namespace gscg {
+
+constexpr int kMaxJoints = GSCG_MAX_JOINTS;
+constexpr int kMaxGroups = 256;      // (template, level) pairs resident at once
+constexpr int kProjectThreads = 256; // Gaussians per work-item chunk
+constexpr int kBatch = 16;           // instances per template-major work item
+constexpr int kShFloats = GSCG_SH_FLOATS;
+
+// One (template, level) group of the shared attribute store in HBM.
+//   core[4*g+0] = mean.x, mean.y, mean.z, opacity
+//   core[4*g+1] = cov xx, xy, xz, yy
+//   core[4*g+2] = cov yz, zz, red, green
+//   core[4*g+3] = blue, power_floor, idx0|idx1<<16, idx2|idx3<<16
+//   weights[g]  = skin weights w0..w3
+//   sh[45*g+3*k+c] = SH residual coefficient k (degree 1..3) of channel c (optional)
+struct GroupDev {
+    const float4* core;
+    const float4* weights;
+    const float* sh;
+    uint32_t count;
+    uint32_t template_id;
+    uint32_t level;
+    uint32_t pad;
+};
+
+struct TemplateDev {
+    int32_t joint_count;
+    int32_t level_count;
+    int32_t group_base;  // group id of level 0
+    int32_t mat_offset;  // first matrix in the skeleton matrix table (local_bind then inverse_bind)
+    int32_t parent_offset;
+    float pelvis_y;
+    int32_t pad[2];
+};
+
+struct CameraDev {
+    float w[9];  // world_to_view row-major
+    float pos[3];
+    float focal, cx, cy, near_m;
+    int32_t width, height;
+};
+
+// Frame-level counters written by the kernels and read back once per frame.
+struct FrameCounters {
+    unsigned long long splat_pair;  // (splats << 32) | pairs, advanced by block aggregates
+    unsigned long long gaussians;   // G of the frame
+    uint32_t depth_min_bits;
+    uint32_t depth_max_bits;
+    uint32_t items_total;
+    uint32_t item_cursor;
+    uint32_t sort_ticket[8];
+};
+
+// float -> int as x86 cvttss2si (the reference's static_cast<int>): truncation, with
+// the "integer indefinite" INT_MIN for NaN and out-of-range values (SURVEY A8 note).
+__device__ __forceinline__ int x86_float_to_int(float v) {
+    if (!(v >= -2147483648.0f && v < 2147483648.0f)) return INT32_MIN;
+    return __float2int_rz(v);
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace gscg

@@ -1,0 +1,125 @@
+// Kernel parameter blocks and declarations shared by the gscg translation units.
+#pragma once
+
+#include "gscg_common.cuh"
+
+namespace gscg {
+
+struct PlanParams {
+    uint32_t n;
+    const uint32_t* template_ids;
+    const float* placement;
+    const uint32_t* lod_prev;
+    int32_t forced_lod;
+    uint32_t threshold_count;
+    float thresholds[GSCG_MAX_LOD_THRESHOLDS];
+    float hysteresis;
+    float cam_pos[3];
+    const TemplateDev* templates;
+    const GroupDev* groups;
+    uint32_t group_count;
+    uint32_t* lod_out;
+    uint32_t* inst_group;
+    uint32_t* inst_base;
+    uint32_t* group_inst_start;  // group_count + 1
+    uint32_t* group_inst_count;
+    uint32_t* group_item_start;  // group_count + 1
+    uint32_t* members;
+    FrameCounters* counters;
+};
+
+struct FkParams {
+    uint32_t n;
+    uint32_t joint_stride;
+    uint32_t pose_stride;
+    const uint32_t* template_ids;
+    const float* placement;
+    const float* poses;
+    const TemplateDev* templates;
+    const float* mats;
+    const int32_t* parents;
+    float* skin;  // n x joint_stride x 12 (rows 0..2 of each skin matrix, row-major)
+};
+
+struct ProjectParams {
+    CameraDev cam;
+    int32_t tile_size;
+    int32_t tiles_x;
+    int32_t sh_enabled;
+    uint32_t joint_stride;
+    uint32_t group_count;
+    const GroupDev* groups;
+    const uint32_t* group_item_start;
+    const uint32_t* group_inst_start;
+    const uint32_t* group_inst_count;
+    const uint32_t* members;
+    const uint32_t* inst_base;
+    const float* skin;
+    FrameCounters* counters;
+    // outputs (capacity-checked)
+    float4* records;  // 3 float4 per splat
+    uint32_t* record_ordinal;
+    unsigned long long* keys;
+    uint32_t* values;
+    uint64_t splat_capacity;
+    uint64_t pair_capacity;
+    // debug outputs (may be null)
+    float* posed_debug;              // G x 3 by ordinal
+    gscg_splat_record* record_debug; // per splat
+};
+
+struct SortPassParams {
+    const unsigned long long* keys_in;
+    const uint32_t* vals_in;
+    unsigned long long* keys_out;
+    uint32_t* vals_out;
+    uint32_t count;
+    uint32_t dbits;
+    unsigned long long dmask;
+    uint32_t shift;
+    const uint32_t* digit_offsets;  // 256 exclusive global offsets of this pass
+    unsigned long long* status;     // num_blocks x 256 look-back words
+    uint32_t* ticket;
+    uint32_t epoch;
+};
+
+struct RasterParams {
+    const uint2* ranges;
+    const uint32_t* values;
+    const float4* records;
+    int32_t width, height, tile_size, tiles_x;
+    float bg[3];
+    float alpha_max;
+    float t_floor;
+    float* out_rgb;
+    float* out_T;
+};
+
+__global__ void k_lod_plan(PlanParams p);
+__global__ void k_fk_skin(FkParams p);
+__global__ void k_project(ProjectParams p);
+__global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n);
+
+// sort
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kMaxSortPasses = 8;
+__global__ void k_digit_histogram(const unsigned long long* keys, uint32_t count, uint32_t dbits,
+                                  unsigned long long dmask, uint32_t passes, uint32_t* hist);
+__global__ void k_digit_scan(uint32_t* hist, uint32_t passes);
+__global__ void k_onesweep(SortPassParams p);
+__global__ void k_tie_fixup(const unsigned long long* keys, uint32_t* vals,
+                            const uint32_t* ordinal, uint32_t count);
+__global__ void k_tile_ranges(const unsigned long long* keys, uint32_t count, uint2* ranges);
+
+// raster
+__global__ void k_raster16(RasterParams p);
+// Picks the tile-size specialisation (16: one pixel per thread; else 1/4/16 per thread).
+void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream);
+
+// debug
+__global__ void k_sorted_ordinals(const uint32_t* vals, const uint32_t* ordinal, uint32_t count,
+                                  uint32_t* out);
+
+}  // namespace gscg

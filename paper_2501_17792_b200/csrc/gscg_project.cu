@@ -1,0 +1,336 @@
+// Stage "gather" on the B200: fused LBS skinning + EWA projection + cull + conic + SH
+// colour + tile-pair emission (reference: skin_means avatar.cpp:178-192 driven by
+// crowd.cpp:126-131; gather_splats renderer.cpp:25-73 -> project_covariance
+// math.cpp:131-170 and splat_bounds math.cpp:106-116; conic prep renderer.cpp:133-141;
+// tile range renderer.cpp:153-157). Compiled with --fmad=false (parity-critical).
+//
+// Template-major schedule: a work item is (template-level group, chunk of 256
+// Gaussians, batch of up to kBatch instances). A CTA loads the chunk's shared attributes
+// once (registers + SH in shared memory) and re-uses them for every instance of the
+// batch, so the shared store streams from HBM once per batch instead of once per
+// instance (CrowdSplat's attribute sharing, moved on-chip). Survivors are compacted with
+// a block scan and one 64-bit atomic per (CTA, instance); placement order is therefore
+// schedule-dependent, but the sort's key order plus the ordinal tie fix-up make the
+// per-tile lists and pixels deterministic.
+#include "gscg_common.cuh"
+#include "gscg_kernels.h"
+
+namespace gscg {
+
+namespace {
+
+// Real SH basis, degrees 1..3 (same constants and expression order as the oracle).
+__device__ __forceinline__ void sh_basis(float x, float y, float z, float Y[15]) {
+    const float C1 = 0.4886025119029199f;
+    const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f,
+                C22 = 0.31539156525252005f, C23 = -1.0925484305920792f,
+                C24 = 0.5462742152960396f;
+    const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f,
+                C32 = -0.4570457994644658f, C33 = 0.3731763325901154f,
+                C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+                C36 = -0.5900435899266435f;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    const float xy = x * y, yz = y * z, xz = x * z;
+    Y[0] = -C1 * y;
+    Y[1] = C1 * z;
+    Y[2] = -C1 * x;
+    Y[3] = C20 * xy;
+    Y[4] = C21 * yz;
+    Y[5] = C22 * ((2.0f * zz - xx) - yy);
+    Y[6] = C23 * xz;
+    Y[7] = C24 * (xx - yy);
+    Y[8] = (C30 * y) * (3.0f * xx - yy);
+    Y[9] = (C31 * xy) * z;
+    Y[10] = (C32 * y) * ((4.0f * zz - xx) - yy);
+    Y[11] = (C33 * z) * ((2.0f * zz - 3.0f * xx) - 3.0f * yy);
+    Y[12] = (C34 * x) * ((4.0f * zz - xx) - yy);
+    Y[13] = (C35 * z) * (xx - yy);
+    Y[14] = (C36 * x) * (xx - 3.0f * yy);
+}
+
+__device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long v,
+                                                             unsigned long long* s_warp,
+                                                             unsigned long long& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    unsigned long long before = 0ull, all = 0ull;
+#pragma unroll
+    for (int w = 0; w < kProjectThreads / 32; ++w) {
+        const unsigned long long t = s_warp[w];
+        if (w < warp) before += t;
+        all += t;
+    }
+    total = all;
+    return before + x - v;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kProjectThreads, 2)
+k_project(ProjectParams p) {
+    extern __shared__ float4 s_dyn[];
+    float* s_sh = reinterpret_cast<float*>(s_dyn);
+    float* s_mats = s_sh + (p.sh_enabled ? kProjectThreads * kShFloats : 0);
+    __shared__ uint32_t s_item_start[kMaxGroups + 1];
+    __shared__ unsigned long long s_warp[kProjectThreads / 32];
+    __shared__ unsigned long long s_base;
+    __shared__ uint32_t s_item;
+
+    const int tid = threadIdx.x;
+    for (uint32_t g = tid; g <= p.group_count; g += blockDim.x) s_item_start[g] = p.group_item_start[g];
+    const uint32_t items_total = p.counters->items_total;
+    const CameraDev& cam = p.cam;
+    const int ts = p.tile_size;
+    uint32_t dmin = 0xffffffffu, dmax = 0u;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_item = atomicAdd(&p.counters->item_cursor, 1u);
+        __syncthreads();
+        const uint32_t item = s_item;
+        if (item >= items_total) break;
+
+        // Group: last g with item_start[g] <= item.
+        uint32_t lo = 0, hi = p.group_count;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_item_start[mid] <= item) lo = mid; else hi = mid;
+        }
+        const uint32_t g = lo;
+        const GroupDev grp = p.groups[g];
+        const uint32_t local = item - s_item_start[g];
+        const uint32_t chunks = (grp.count + kProjectThreads - 1) / kProjectThreads;
+        const uint32_t chunk = local % chunks, batch = local / chunks;
+        const uint32_t gi = chunk * kProjectThreads + tid;
+        const bool gvalid = gi < grp.count;
+
+        float4 c0 = make_float4(0, 0, 0, 0), c1 = c0, c2 = c0, c3 = c0, wv = c0;
+        if (gvalid) {
+            c0 = grp.core[4 * gi + 0];
+            c1 = grp.core[4 * gi + 1];
+            c2 = grp.core[4 * gi + 2];
+            c3 = grp.core[4 * gi + 3];
+            wv = grp.weights[gi];
+        }
+        const bool use_sh = p.sh_enabled && grp.sh != nullptr;
+        if (use_sh) {
+            const uint32_t n_here = min(static_cast<uint32_t>(kProjectThreads),
+                                        grp.count - chunk * kProjectThreads);
+            const float* src = grp.sh + static_cast<size_t>(chunk) * kProjectThreads * kShFloats;
+            const uint32_t n4 = (n_here * kShFloats + 3) / 4;  // SH chunks are 16-B aligned
+            const float4* src4 = reinterpret_cast<const float4*>(src);
+            for (uint32_t k = tid; k < n4; k += blockDim.x) reinterpret_cast<float4*>(s_sh)[k] = src4[k];
+        }
+        const uint32_t inst_begin = p.group_inst_start[g] + batch * kBatch;
+        const uint32_t inst_count = min(static_cast<uint32_t>(kBatch),
+                                        p.group_inst_count[g] - batch * kBatch);
+        const uint32_t i01 = __float_as_uint(c3.z), i23 = __float_as_uint(c3.w);
+        const uint32_t jidx[4] = {i01 & 0xffffu, i01 >> 16, i23 & 0xffffu, i23 >> 16};
+        const float wk[4] = {wv.x, wv.y, wv.z, wv.w};
+
+        for (uint32_t k = 0; k < inst_count; ++k) {
+            const uint32_t inst = p.members[inst_begin + k];
+            {
+                const float4* src = reinterpret_cast<const float4*>(
+                    p.skin + static_cast<size_t>(inst) * p.joint_stride * 12);
+                for (uint32_t e = tid; e < p.joint_stride * 3; e += blockDim.x)
+                    reinterpret_cast<float4*>(s_mats)[e] = src[e];
+            }
+            __syncthreads();
+
+            bool survive = false;
+            uint32_t n_tiles = 0;
+            float mx = 0, my = 0, depth = 0, cxx = 0, cxy = 0, cyy = 0, ca = 0, cb = 0, cc = 0;
+            float col0 = 0, col1 = 0, col2 = 0;
+            int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+            float ax = 0.0f, ay = 0.0f, az = 0.0f;
+            if (gvalid) {
+                // Linear blend skinning (avatar.cpp:182-190), accumulator starts at +0.
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (wk[q] == 0.0f) continue;
+                    const float* S = s_mats + jidx[q] * 12;
+                    const float vx = ((S[0] * c0.x + S[1] * c0.y) + S[2] * c0.z) + S[3] * 1.0f;
+                    const float vy = ((S[4] * c0.x + S[5] * c0.y) + S[6] * c0.z) + S[7] * 1.0f;
+                    const float vz = ((S[8] * c0.x + S[9] * c0.y) + S[10] * c0.z) + S[11] * 1.0f;
+                    ax = ax + wk[q] * vx;
+                    ay = ay + wk[q] * vy;
+                    az = az + wk[q] * vz;
+                }
+                // EWA projection (math.cpp:131-170).
+                const bool finite_in = isfinite(ax) && isfinite(ay) && isfinite(az) &&
+                                       isfinite(c1.x) && isfinite(c1.y) && isfinite(c1.z) &&
+                                       isfinite(c1.w) && isfinite(c2.x) && isfinite(c2.y);
+                const float dx = ax - cam.pos[0], dy = ay - cam.pos[1], dz = az - cam.pos[2];
+                const float tx = cam.w[0] * dx + (cam.w[1] * dy + cam.w[2] * dz);
+                const float ty = cam.w[3] * dx + (cam.w[4] * dy + cam.w[5] * dz);
+                const float tz = cam.w[6] * dx + (cam.w[7] * dy + cam.w[8] * dz);
+                if (finite_in && tz > cam.near_m) {
+                    const float f = cam.focal;
+                    const float iz = 1.0f / tz;
+                    mx = (f * tx) * iz + cam.cx;
+                    my = (f * ty) * iz + cam.cy;
+                    const float j00 = f * iz, j01 = 0.0f, j02 = ((-f * tx) * iz) * iz;
+                    const float j10 = 0.0f, j11 = f * iz, j12 = ((-f * ty) * iz) * iz;
+                    // m = J * W (2x3)
+                    float m[2][3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        m[0][c] = j00 * cam.w[0 * 3 + c] + (j01 * cam.w[1 * 3 + c] + j02 * cam.w[2 * 3 + c]);
+                        m[1][c] = j10 * cam.w[0 * 3 + c] + (j11 * cam.w[1 * 3 + c] + j12 * cam.w[2 * 3 + c]);
+                    }
+                    const float S3[3][3] = {{c1.x, c1.y, c1.z}, {c1.y, c1.w, c2.x}, {c1.z, c2.x, c2.y}};
+                    float A[2][3];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            A[r][c] = m[r][0] * S3[0][c] + (m[r][1] * S3[1][c] + m[r][2] * S3[2][c]);
+                    float C[2][2];
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            C[i][j] = A[i][0] * m[j][0] + (A[i][1] * m[j][1] + A[i][2] * m[j][2]);
+                    C[0][0] = C[0][0] + 0.3f;
+                    C[1][1] = C[1][1] + 0.3f;
+                    const float rx = 3.0f * sqrtf(C[0][0]);
+                    const float ry = 3.0f * sqrtf(C[1][1]);
+                    x0 = max(0, x86_float_to_int(floorf(mx - rx)));
+                    y0 = max(0, x86_float_to_int(floorf(my - ry)));
+                    x1 = min(cam.width, x86_float_to_int(floorf(mx + rx)) + 1);
+                    y1 = min(cam.height, x86_float_to_int(floorf(my + ry)) + 1);
+                    if (x0 < x1 && y0 < y1) {
+                        survive = true;
+                        cxx = C[0][0];
+                        cxy = 0.5f * (C[0][1] + C[1][0]);
+                        cyy = C[1][1];
+                        depth = tz;
+                        // Conic (renderer.cpp:136-140).
+                        const float det = cxx * cyy - cxy * cxy;
+                        const float inv_det = 1.0f / det;
+                        ca = cyy * inv_det;
+                        cb = -cxy * inv_det;
+                        cc = cxx * inv_det;
+                        const int tx0 = x0 / ts, tx1 = (x1 - 1) / ts;
+                        const int ty0 = y0 / ts, ty1 = (y1 - 1) / ts;
+                        n_tiles = static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+                        col0 = c2.z;
+                        col1 = c2.w;
+                        col2 = c3.x;
+                        if (use_sh) {
+                            // SH residual colour: dir = normalize(mean - cam).
+                            const float vx = ax - cam.pos[0], vy = ay - cam.pos[1], vz = az - cam.pos[2];
+                            const float nrm = sqrtf(vx * vx + (vy * vy + vz * vz));
+                            float Y[15];
+                            sh_basis(vx / nrm, vy / nrm, vz / nrm, Y);
+                            const float* sh = s_sh + tid * kShFloats;
+#pragma unroll
+                            for (int q = 0; q < 15; ++q) {
+                                col0 = col0 + Y[q] * sh[3 * q + 0];
+                                col1 = col1 + Y[q] * sh[3 * q + 1];
+                                col2 = col2 + Y[q] * sh[3 * q + 2];
+                            }
+                            col0 = fmaxf(col0, 0.0f);
+                            col1 = fmaxf(col1, 0.0f);
+                            col2 = fmaxf(col2, 0.0f);
+                        }
+                    }
+                }
+            }
+
+            unsigned long long total;
+            const unsigned long long mine = (survive ? (1ull << 32) : 0ull) + n_tiles;
+            const unsigned long long excl = block_scan_u64(mine, s_warp, total);
+            if (tid == 0) s_base = atomicAdd(&p.counters->splat_pair, total);
+            __syncthreads();
+            const unsigned long long base = s_base;
+            const uint32_t ordinal = gvalid ? p.inst_base[inst] + gi : 0u;
+            if (p.posed_debug && gvalid) {
+                p.posed_debug[3ull * ordinal + 0] = ax;
+                p.posed_debug[3ull * ordinal + 1] = ay;
+                p.posed_debug[3ull * ordinal + 2] = az;
+            }
+            if (survive) {
+                const uint64_t ridx = (base >> 32) + (excl >> 32);
+                uint64_t pidx = (base & 0xffffffffull) + (excl & 0xffffffffull);
+                const uint32_t dbits = __float_as_uint(depth);
+                dmin = min(dmin, dbits);
+                dmax = max(dmax, dbits);
+                if (ridx < p.splat_capacity) {
+                    float4* rec = p.records + 3 * ridx;
+                    rec[0] = make_float4(mx, my, ca, cb);
+                    rec[1] = make_float4(cc, c0.w, c3.y, col0);
+                    rec[2] = make_float4(col1, col2,
+                                         __uint_as_float(static_cast<uint32_t>(x0) | (static_cast<uint32_t>(y0) << 16)),
+                                         __uint_as_float(static_cast<uint32_t>(x1) | (static_cast<uint32_t>(y1) << 16)));
+                    p.record_ordinal[ridx] = ordinal;
+                    if (p.record_debug) {
+                        gscg_splat_record d;
+                        d.ordinal = ordinal;
+                        d.instance_id = inst;
+                        d.gaussian_index = gi;
+                        d.depth = depth;
+                        d.mean_px[0] = mx;
+                        d.mean_px[1] = my;
+                        d.cov_xx = cxx;
+                        d.cov_xy = cxy;
+                        d.cov_yy = cyy;
+                        d.conic[0] = ca;
+                        d.conic[1] = cb;
+                        d.conic[2] = cc;
+                        d.power_floor = c3.y;
+                        d.opacity = c0.w;
+                        d.color[0] = col0;
+                        d.color[1] = col1;
+                        d.color[2] = col2;
+                        d.rect[0] = x0;
+                        d.rect[1] = y0;
+                        d.rect[2] = x1;
+                        d.rect[3] = y1;
+                        p.record_debug[ridx] = d;
+                    }
+                    const int tx0 = x0 / ts, tx1 = (x1 - 1) / ts;
+                    const int ty0 = y0 / ts, ty1 = (y1 - 1) / ts;
+                    for (int tyy = ty0; tyy <= ty1; ++tyy) {
+                        for (int txx = tx0; txx <= tx1; ++txx) {
+                            if (pidx < p.pair_capacity) {
+                                p.keys[pidx] = (static_cast<unsigned long long>(tyy * p.tiles_x + txx) << 32) | dbits;
+                                p.values[pidx] = static_cast<uint32_t>(ridx);
+                            }
+                            ++pidx;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    // Depth-bit range of the frame (sort pass planning).
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if ((tid & 31) == 0) {
+        if (dmin != 0xffffffffu) atomicMin(&p.counters->depth_min_bits, dmin);
+        if (dmax != 0u) atomicMax(&p.counters->depth_max_bits, dmax);
+    }
+}
+
+// Power floor column (core[4g+3].y) = logf(alpha_cutoff / opacity), computed on the host
+// with glibc exactly as the reference's conic prep does (renderer.cpp:140).
+__global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) core[4 * i + 3].y = pf[i];
+}
+
+}  // namespace gscg

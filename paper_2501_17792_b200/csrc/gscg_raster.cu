@@ -1,0 +1,183 @@
+// Stage "rasterize" on the B200: per-tile front-to-back alpha blending
+// (reference: rasterize_full renderer.cpp:121-232).
+//
+// One CTA per tile. The tile's sorted splat indices are consumed in batches of 256: each
+// thread gathers one 48-byte record into shared memory (3 x float4, coalesced per
+// record), then every pixel thread walks the batch in order. Semantics kept from the
+// reference (SURVEY.md §7 "reference raster semantics"):
+//   * a pixel is touched only inside the splat's clipped 3-sigma rectangle;
+//   * the cutoff test is power < power_floor with power_floor = logf(cutoff/opacity)
+//     precomputed by the host (glibc, bit-identical to the reference);
+//   * the splat that pushes T below the floor is blended, then the pixel stops;
+//   * output = rgb + T * background, and T itself.
+// The per-pixel power is computed with round-to-nearest intrinsics in the reference
+// order (renderer.cpp:197-204) so the set of contributing (pixel, splat) pairs is the
+// reference's; alpha uses the hardware exp2 path (tolerance-checked).
+#include "gscg_common.cuh"
+#include "gscg_kernels.h"
+
+namespace gscg {
+
+namespace {
+
+struct SplatView {
+    float mx, my, a, b, c, o, pf, r, g, bl;
+    int x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ SplatView unpack(const float4* s, int k) {
+    const float4 r0 = s[3 * k + 0], r1 = s[3 * k + 1], r2 = s[3 * k + 2];
+    SplatView v;
+    v.mx = r0.x;
+    v.my = r0.y;
+    v.a = r0.z;
+    v.b = r0.w;
+    v.c = r1.x;
+    v.o = r1.y;
+    v.pf = r1.z;
+    v.r = r1.w;
+    v.g = r2.x;
+    v.bl = r2.y;
+    const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
+    v.x0 = static_cast<int>(lo & 0xffffu);
+    v.y0 = static_cast<int>(lo >> 16);
+    v.x1 = static_cast<int>(hi & 0xffffu);
+    v.y1 = static_cast<int>(hi >> 16);
+    return v;
+}
+
+// power = -0.5f * (a*dx*dx + c*dy*dy) - b*dx*dy, single rounding per operation.
+__device__ __forceinline__ float pixel_power(const SplatView& s, float fx, float fy) {
+    const float dx = __fsub_rn(fx, s.mx);
+    const float dy = __fsub_rn(fy, s.my);
+    const float q = __fadd_rn(__fmul_rn(__fmul_rn(s.a, dx), dx), __fmul_rn(__fmul_rn(s.c, dy), dy));
+    return __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(s.b, dx), dy));
+}
+
+// Blend one splat into one pixel; returns true when the pixel reaches the floor.
+__device__ __forceinline__ bool blend(const SplatView& s, int px, int py, float& T, float& cr,
+                                      float& cg, float& cb, float amax, float tfloor) {
+    if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) return false;
+    const float power = pixel_power(s, static_cast<float>(px) + 0.5f, static_cast<float>(py) + 0.5f);
+    if (power < s.pf) return false;
+    const float alpha = fminf(s.o * __expf(power), amax);
+    const float w = T * alpha;
+    cr = fmaf(w, s.r, cr);
+    cg = fmaf(w, s.g, cg);
+    cb = fmaf(w, s.bl, cb);
+    T = T * (1.0f - alpha);
+    return T < tfloor;
+}
+
+}  // namespace
+
+// Tile size 16: one pixel per thread; warp w owns pixel rows 2w and 2w+1.
+__global__ void __launch_bounds__(256)
+k_raster16(RasterParams p) {
+    __shared__ float4 s_rec[256 * 3];
+    const int tile = blockIdx.x;
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int px = tx * 16 + (threadIdx.x & 15);
+    const int py = ty * 16 + (threadIdx.x >> 4);
+    const bool inside = px < p.width && py < p.height;
+    const uint2 range = p.ranges[tile];
+    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+    bool done = !inside;
+    for (uint32_t start = range.x; start < range.y; start += 256) {
+        if (__syncthreads_count(done) == 256) break;
+        const uint32_t i = start + threadIdx.x;
+        if (i < range.y) {
+            const float4* src = p.records + 3ull * p.values[i];
+            s_rec[3 * threadIdx.x + 0] = src[0];
+            s_rec[3 * threadIdx.x + 1] = src[1];
+            s_rec[3 * threadIdx.x + 2] = src[2];
+        }
+        __syncthreads();
+        const int n = min(256u, range.y - start);
+        if (!done) {
+            for (int k = 0; k < n; ++k) {
+                const SplatView s = unpack(s_rec, k);
+                if (blend(s, px, py, T, cr, cg, cb, p.alpha_max, p.t_floor)) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+    }
+    if (inside) {
+        const size_t o = static_cast<size_t>(py) * p.width + px;
+        p.out_rgb[3 * o + 0] = cr + T * p.bg[0];
+        p.out_rgb[3 * o + 1] = cg + T * p.bg[1];
+        p.out_rgb[3 * o + 2] = cb + T * p.bg[2];
+        p.out_T[o] = T;
+    }
+}
+
+// Any tile size up to 16*sqrt(PPT): PPT pixels per thread, pixel p = tid + k*256.
+template <int PPT>
+__global__ void __launch_bounds__(256)
+k_raster_generic(RasterParams p) {
+    __shared__ float4 s_rec[256 * 3];
+    const int ts = p.tile_size;
+    const int tile = blockIdx.x;
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    float T[PPT], cr[PPT], cg[PPT], cb[PPT];
+    int pxs[PPT], pys[PPT];
+    bool live[PPT];
+    int live_count = 0;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        const int lp = threadIdx.x + k * 256;
+        pxs[k] = tx * ts + lp % ts;
+        pys[k] = ty * ts + lp / ts;
+        live[k] = lp < ts * ts && pxs[k] < p.width && pys[k] < p.height;
+        T[k] = 1.0f;
+        cr[k] = cg[k] = cb[k] = 0.0f;
+        live_count += live[k] ? 1 : 0;
+    }
+    const uint2 range = p.ranges[tile];
+    for (uint32_t start = range.x; start < range.y; start += 256) {
+        if (__syncthreads_or(live_count > 0) == 0) break;
+        const uint32_t i = start + threadIdx.x;
+        if (i < range.y) {
+            const float4* src = p.records + 3ull * p.values[i];
+            s_rec[3 * threadIdx.x + 0] = src[0];
+            s_rec[3 * threadIdx.x + 1] = src[1];
+            s_rec[3 * threadIdx.x + 2] = src[2];
+        }
+        __syncthreads();
+        const int n = min(256u, range.y - start);
+        for (int s = 0; s < n && live_count > 0; ++s) {
+            const SplatView v = unpack(s_rec, s);
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                if (!live[k]) continue;
+                if (blend(v, pxs[k], pys[k], T[k], cr[k], cg[k], cb[k], p.alpha_max, p.t_floor)) {
+                    live[k] = false;
+                    --live_count;
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        const int lp = threadIdx.x + k * 256;
+        if (lp < ts * ts && pxs[k] < p.width && pys[k] < p.height) {
+            const size_t o = static_cast<size_t>(pys[k]) * p.width + pxs[k];
+            p.out_rgb[3 * o + 0] = cr[k] + T[k] * p.bg[0];
+            p.out_rgb[3 * o + 1] = cg[k] + T[k] * p.bg[1];
+            p.out_rgb[3 * o + 2] = cb[k] + T[k] * p.bg[2];
+            p.out_T[o] = T[k];
+        }
+    }
+}
+
+void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream) {
+    if (p.tile_size == 16) k_raster16<<<tiles, 256, 0, stream>>>(p);
+    else if (p.tile_size <= 16) k_raster_generic<1><<<tiles, 256, 0, stream>>>(p);
+    else if (p.tile_size <= 32) k_raster_generic<4><<<tiles, 256, 0, stream>>>(p);
+    else k_raster_generic<16><<<tiles, 256, 0, stream>>>(p);
+}
+
+}  // namespace gscg

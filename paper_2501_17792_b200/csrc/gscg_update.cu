@@ -1,0 +1,286 @@
+// Stage "update" of render_frame on the B200 (reference: update_crowd,
+// /root/reference/proj/src/crowd.cpp:86-140). Compiled with --fmad=false.
+//
+//  k_lod_plan  — one CTA: per-instance LoD (lod.cpp:22-41, crowd.cpp:93-110), the
+//                instance-Gaussian ordinal base of every instance (exclusive scan in
+//                instance order), the stable (template, level) grouping of instances
+//                and the template-major work-item table the projection kernel consumes.
+//  k_fk_skin   — half a warp per instance: forward kinematics and skin matrices
+//                (avatar.cpp:149-176, crowd.cpp:20-30, 126-128), one matrix element
+//                per lane, Eigen's packet product order.
+#include "gscg_common.cuh"
+#include "gscg_kernels.h"
+
+namespace gscg {
+
+namespace {
+
+constexpr int kPlanThreads = 1024;
+
+template <typename T>
+__device__ T block_exclusive_scan(T v, T* s_warp, T& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        T w = lane < nwarps ? s_warp[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < nwarps) s_warp[lane] = w;  // inclusive warp prefix
+    }
+    __syncthreads();
+    const T warp_excl = warp == 0 ? T(0) : s_warp[warp - 1];
+    total = s_warp[nwarps - 1];
+    __syncthreads();
+    return warp_excl + x - v;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kPlanThreads)
+k_lod_plan(PlanParams p) {
+    __shared__ unsigned long long s_scan64[32];
+    __shared__ uint32_t s_scan32[32];
+    __shared__ uint32_t s_gcount[kMaxGroups];
+    __shared__ uint32_t s_gstart[kMaxGroups];
+    __shared__ uint32_t s_carry[kMaxGroups];
+    __shared__ uint32_t s_tile_total[kMaxGroups];
+    __shared__ uint32_t s_wcount[32][kMaxGroups];
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int g = tid; g < kMaxGroups; g += blockDim.x) {
+        s_gcount[g] = 0;
+        s_carry[g] = 0;
+    }
+    if (tid == 0) {
+        p.counters->splat_pair = 0ull;
+        p.counters->depth_min_bits = 0xffffffffu;
+        p.counters->depth_max_bits = 0u;
+        p.counters->item_cursor = 0u;
+        for (int i = 0; i < 8; ++i) p.counters->sort_ticket[i] = 0u;
+    }
+    __syncthreads();
+
+    // Pass 1: LoD, group, per-instance Gaussian count; ordinal bases by block scan.
+    unsigned long long carry = 0ull;
+    for (uint32_t tile = 0; tile < p.n; tile += kPlanThreads) {
+        const uint32_t i = tile + tid;
+        uint32_t count = 0;
+        if (i < p.n) {
+            const uint32_t t = p.template_ids[i];
+            const TemplateDev tpl = p.templates[t];
+            const uint32_t levels = static_cast<uint32_t>(tpl.level_count);
+            uint32_t lod;
+            if (p.forced_lod >= 0) {
+                lod = min(static_cast<uint32_t>(p.forced_lod), levels - 1u);
+            } else {
+                // instance_distance((x, pelvis.y, z), camera.position): Eigen half-split norm.
+                const float dx = p.placement[4 * i + 0] - p.cam_pos[0];
+                const float dy = tpl.pelvis_y - p.cam_pos[1];
+                const float dz = p.placement[4 * i + 1] - p.cam_pos[2];
+                const float sq = dx * dx + (dy * dy + dz * dz);
+                const float dist = sqrtf(sq);
+                const uint32_t prev = p.lod_prev[i];
+                uint32_t sel = p.threshold_count;
+                for (uint32_t k = 0; k < p.threshold_count; ++k) {
+                    float th = p.thresholds[k];
+                    if (prev != 0xffffffffu && p.hysteresis > 0.0f)
+                        th = th + (k >= prev ? 0.5f : -0.5f) * p.hysteresis;
+                    if (dist < th) {
+                        sel = k;
+                        break;
+                    }
+                }
+                lod = min(sel, levels - 1u);
+            }
+            const uint32_t g = static_cast<uint32_t>(tpl.group_base) + lod;
+            p.lod_out[i] = lod;
+            p.inst_group[i] = g;
+            count = p.groups[g].count;
+            atomicAdd(&s_gcount[g], 1u);
+        }
+        unsigned long long total;
+        const unsigned long long excl =
+            block_exclusive_scan<unsigned long long>(count, s_scan64, total);
+        if (i < p.n) p.inst_base[i] = static_cast<uint32_t>(carry + excl);
+        carry += total;
+    }
+    if (tid == 0) p.counters->gaussians = carry;
+    __syncthreads();
+
+    // Group starts and work items (template-major: chunks of 256 Gaussians x batches).
+    {
+        uint32_t cnt = 0, items = 0;
+        if (tid < static_cast<int>(p.group_count)) {
+            cnt = s_gcount[tid];
+            const uint32_t N = p.groups[tid].count;
+            const uint32_t chunks = (N + kProjectThreads - 1) / kProjectThreads;
+            const uint32_t batches = (cnt + kBatch - 1) / kBatch;
+            items = cnt ? chunks * batches : 0u;
+        }
+        uint32_t tot_c, tot_i;
+        const uint32_t ex_c = block_exclusive_scan<uint32_t>(cnt, s_scan32, tot_c);
+        const uint32_t ex_i = block_exclusive_scan<uint32_t>(items, s_scan32, tot_i);
+        if (tid < static_cast<int>(p.group_count)) {
+            s_gstart[tid] = ex_c;
+            p.group_inst_start[tid] = ex_c;
+            p.group_inst_count[tid] = cnt;
+            p.group_item_start[tid] = ex_i;
+        }
+        if (tid == 0) {
+            p.group_inst_start[p.group_count] = tot_c;
+            p.group_item_start[p.group_count] = tot_i;
+            p.counters->items_total = tot_i;
+        }
+    }
+    __syncthreads();
+
+    // Pass 2: stable counting scatter of instance ids into their groups.
+    for (uint32_t tile = 0; tile < p.n; tile += kPlanThreads) {
+        for (int k = tid; k < 32 * kMaxGroups; k += blockDim.x) (&s_wcount[0][0])[k] = 0u;
+        __syncthreads();
+        const uint32_t i = tile + tid;
+        const bool valid = i < p.n;
+        const uint32_t g = valid ? p.inst_group[i] : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, g);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        if (valid && lane == __ffs(peers) - 1) s_wcount[warp][g] = __popc(peers);
+        __syncthreads();
+        if (tid < static_cast<int>(p.group_count)) {
+            uint32_t run = 0;
+            for (int w = 0; w < 32; ++w) {
+                const uint32_t c = s_wcount[w][tid];
+                s_wcount[w][tid] = run;
+                run += c;
+            }
+            s_tile_total[tid] = run;
+        }
+        __syncthreads();
+        if (valid) p.members[s_gstart[g] + s_carry[g] + s_wcount[warp][g] + rank] = i;
+        __syncthreads();
+        if (tid < static_cast<int>(p.group_count)) s_carry[tid] += s_tile_total[tid];
+        __syncthreads();
+    }
+}
+
+// Element (r, c) of a column-major 4x4 product A*B given A's row r and B's column c:
+// Eigen's packet chain ((a0*b0 + a1*b1) + a2*b2) + a3*b3, no FMA.
+__device__ __forceinline__ float chain4(float a0, float a1, float a2, float a3, float b0, float b1,
+                                        float b2, float b3) {
+    float acc = a0 * b0;
+    acc = acc + a1 * b1;
+    acc = acc + a2 * b2;
+    acc = acc + a3 * b3;
+    return acc;
+}
+
+// Element (r, c) of rotation_matrix(q) (avatar.cpp:19-23): Eigen toRotationMatrix in the
+// top-left 3x3 block, identity elsewhere.
+__device__ __forceinline__ float rot_elem(const float4 q, int r, int c) {
+    if (r == 3 || c == 3) return (r == c) ? 1.0f : 0.0f;
+    const float tx = 2.0f * q.x, ty = 2.0f * q.y, tz = 2.0f * q.z;
+    const float twx = tx * q.w, twy = ty * q.w, twz = tz * q.w;
+    const float txx = tx * q.x, txy = ty * q.x, txz = tz * q.x;
+    const float tyy = ty * q.y, tyz = tz * q.y, tzz = tz * q.z;
+    const int k = r * 3 + c;
+    switch (k) {
+        case 0: return 1.0f - (tyy + tzz);
+        case 1: return txy - twz;
+        case 2: return txz + twy;
+        case 3: return txy + twz;
+        case 4: return 1.0f - (txx + tzz);
+        case 5: return tyz - twx;
+        case 6: return txz - twy;
+        case 7: return tyz + twx;
+        default: return 1.0f - (txx + tyy);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_fk_skin(FkParams p) {
+    extern __shared__ float s_world[];  // [16 half-warps][kMaxJoints... joint_stride][16]
+    const int half = threadIdx.x >> 4;        // half-warp within the block
+    const int l = threadIdx.x & 15;           // matrix element, column-major
+    const int r = l & 3, c = l >> 2;
+    const uint32_t inst = blockIdx.x * (blockDim.x >> 4) + half;
+    const unsigned hmask = 0xffffu << ((threadIdx.x & 31) & 16);
+    if (inst >= p.n) return;
+    float* world = s_world + static_cast<size_t>(half) * p.joint_stride * 16;
+
+    const TemplateDev tpl = p.templates[p.template_ids[inst]];
+    const int J = tpl.joint_count;
+    const float* lb = p.mats + static_cast<size_t>(tpl.mat_offset) * 16;
+    const float* ib = lb + static_cast<size_t>(J) * 16;
+    const int32_t* parents = p.parents + tpl.parent_offset;
+    const float* pose = p.poses + static_cast<size_t>(inst) * p.pose_stride;
+
+    // Root transform (crowd.cpp:20-30) and root offset T(root_translation).
+    const float x = p.placement[4 * inst + 0], z = p.placement[4 * inst + 1];
+    const float cs = p.placement[4 * inst + 2], sn = p.placement[4 * inst + 3];
+    auto root_elem = [&](int rr, int cc) -> float {
+        if (rr == 0 && cc == 0) return cs;
+        if (rr == 0 && cc == 2) return sn;
+        if (rr == 2 && cc == 0) return -sn;
+        if (rr == 2 && cc == 2) return cs;
+        if (rr == 0 && cc == 3) return x;
+        if (rr == 2 && cc == 3) return z;
+        return rr == cc ? 1.0f : 0.0f;
+    };
+    auto offset_elem = [&](int rr, int cc) -> float {
+        if (cc == 3 && rr < 3) return pose[rr];
+        return rr == cc ? 1.0f : 0.0f;
+    };
+    const float m0 = chain4(root_elem(r, 0), root_elem(r, 1), root_elem(r, 2), root_elem(r, 3),
+                            offset_elem(0, c), offset_elem(1, c), offset_elem(2, c),
+                            offset_elem(3, c));
+
+    float* out = p.skin + static_cast<size_t>(inst) * p.joint_stride * 12;
+    for (int j = 0; j < J; ++j) {
+        const float4 q = *reinterpret_cast<const float4*>(pose + 4 + 4 * j);
+        const float* LB = lb + j * 16;
+        // local = local_bind[j] * rotation_matrix(q)
+        const float local = chain4(LB[0 * 4 + r], LB[1 * 4 + r], LB[2 * 4 + r], LB[3 * 4 + r],
+                                   rot_elem(q, 0, c), rot_elem(q, 1, c), rot_elem(q, 2, c),
+                                   rot_elem(q, 3, c));
+        // local(k, c) lives in lane c*4 + k of this half-warp.
+        const float lk0 = __shfl_sync(hmask, local, c * 4 + 0, 16);
+        const float lk1 = __shfl_sync(hmask, local, c * 4 + 1, 16);
+        const float lk2 = __shfl_sync(hmask, local, c * 4 + 2, 16);
+        const float lk3 = __shfl_sync(hmask, local, c * 4 + 3, 16);
+        float pr0, pr1, pr2, pr3;  // parent row r
+        if (j == 0) {
+            pr0 = __shfl_sync(hmask, m0, 0 * 4 + r, 16);
+            pr1 = __shfl_sync(hmask, m0, 1 * 4 + r, 16);
+            pr2 = __shfl_sync(hmask, m0, 2 * 4 + r, 16);
+            pr3 = __shfl_sync(hmask, m0, 3 * 4 + r, 16);
+        } else {
+            const float* P = world + parents[j] * 16;
+            pr0 = P[0 * 4 + r];
+            pr1 = P[1 * 4 + r];
+            pr2 = P[2 * 4 + r];
+            pr3 = P[3 * 4 + r];
+        }
+        const float wv = chain4(pr0, pr1, pr2, pr3, lk0, lk1, lk2, lk3);
+        world[j * 16 + l] = wv;
+        __syncwarp(hmask);
+        // skin = world[j] * inverse_bind[j]
+        const float* IB = ib + j * 16;
+        const float* W = world + j * 16;
+        const float sv = chain4(W[0 * 4 + r], W[1 * 4 + r], W[2 * 4 + r], W[3 * 4 + r],
+                                IB[c * 4 + 0], IB[c * 4 + 1], IB[c * 4 + 2], IB[c * 4 + 3]);
+        if (r < 3) out[j * 12 + r * 4 + c] = sv;
+    }
+}
+
+}  // namespace gscg

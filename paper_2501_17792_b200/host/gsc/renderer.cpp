@@ -1,0 +1,278 @@
+// Host side of render_frame on the B200 (see renderer.hpp). Stage structure follows
+// /root/reference/proj/src/renderer.cpp:249-280; the per-instance update follows
+// /root/reference/proj/src/crowd.cpp:86-140 up to the pose (LoD, FK, skinning run on
+// the GPU).
+#include "gsc/renderer.hpp"
+
+#include <chrono>
+#include <cstdlib>
+#include <string>
+
+namespace gsc {
+
+void validate(const RenderSettings& s) {
+    if (s.tile_size < 1) throw std::invalid_argument("RenderSettings: tile_size must be >= 1");
+    if (!(s.alpha_cutoff > 0.0f && s.alpha_cutoff < 1.0f))
+        throw std::invalid_argument("RenderSettings: alpha_cutoff outside (0,1)");
+    if (!(s.transmittance_floor > 0.0f && s.transmittance_floor < 1.0f))
+        throw std::invalid_argument("RenderSettings: transmittance_floor outside (0,1)");
+}
+
+void check_gscg(int status, const gscg_ctx* ctx) {
+    if (status == GSCG_OK) return;
+    const std::string msg = ctx ? gscg_last_error(ctx) : "gscg call failed";
+    if (status == GSCG_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    if (status == GSCG_ERR_OOM) throw std::bad_alloc();
+    throw GpuError(status, msg);
+}
+
+unsigned resolve_thread_count(int hint) {
+    if (hint > 0) return static_cast<unsigned>(hint);
+    if (const char* env = std::getenv("GSCROWD_THREADS")) {
+        const long v = std::strtol(env, nullptr, 10);
+        if (v > 0) return static_cast<unsigned>(v);
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw > 0 ? hw : 1;
+}
+
+HostPool::HostPool(unsigned threads) {
+    for (unsigned i = 1; i < threads; ++i) workers_.emplace_back([this, i] { worker(i); });
+}
+
+HostPool::~HostPool() {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        stop_ = true;
+        ++generation_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+}
+
+void HostPool::worker(unsigned index) {
+    uint64_t seen = 0;
+    for (;;) {
+        const std::function<void(size_t, size_t)>* job;
+        size_t count;
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return generation_ != seen; });
+            seen = generation_;
+            if (stop_) return;
+            job = job_;
+            count = count_;
+        }
+        const size_t parts = size();
+        const size_t chunk = (count + parts - 1) / parts;
+        const size_t b = index * chunk, e = std::min(count, b + chunk);
+        if (b < e) (*job)(b, e);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+}
+
+void HostPool::parallel_for(size_t count, const std::function<void(size_t, size_t)>& fn) {
+    if (count == 0) return;
+    if (workers_.empty() || count < 2) {
+        fn(0, count);
+        return;
+    }
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        job_ = &fn;
+        count_ = count;
+        pending_ = static_cast<unsigned>(workers_.size());
+        ++generation_;
+    }
+    cv_.notify_all();
+    const size_t chunk = (count + size() - 1) / size();
+    fn(0, std::min(count, chunk));
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+}
+
+FrameContext::FrameContext(int device) {
+    gscg_ctx* c = nullptr;
+    const int st = gscg_create(device, &c);
+    if (st != GSCG_OK) {
+        std::string msg = c ? gscg_last_error(c) : "gscg_create failed";
+        if (c) gscg_destroy(c);
+        throw GpuError(st, msg);
+    }
+    gpu_ = c;
+}
+
+FrameContext::~FrameContext() {
+    if (gpu_) gscg_destroy(gpu_);
+}
+
+void FrameContext::ensure_templates(const std::shared_ptr<const TemplateStore>& store) {
+    if (store.get() == uploaded_) return;
+    joint_stride = 0;
+    for (uint32_t t = 0; t < store->size(); ++t) {
+        const AvatarTemplate& tpl = (*store)[t];
+        const Skeleton& sk = tpl.skeleton;
+        const uint32_t J = sk.joint_count();
+        joint_stride = std::max(joint_stride, J);
+        std::vector<float> lb(J * 16), ib(J * 16);
+        for (uint32_t j = 0; j < J; ++j) {
+            std::copy(sk.local_bind[j].m, sk.local_bind[j].m + 16, lb.begin() + j * 16);
+            std::copy(sk.inverse_bind[j].m, sk.inverse_bind[j].m + 16, ib.begin() + j * 16);
+        }
+        gscg_skeleton_desc sd{J, sk.parents.data(), lb.data(), ib.data(), sk.bind[0](1, 3)};
+        check_gscg(gscg_upload_skeleton(gpu_, t, &sd), gpu_);
+        for (uint32_t l = 0; l < tpl.levels.size(); ++l) {
+            const LodLevel& lv = tpl.levels[l];
+            if (lv.cov_cache.size() != lv.means.size())
+                throw std::invalid_argument("LodLevel: finalize() not called");
+            gscg_level_desc d{};
+            d.gaussian_count = lv.gaussian_count();
+            d.means = lv.means.empty() ? nullptr : lv.means[0].v;
+            d.cov6 = lv.cov_cache[0].data();
+            d.opacities = lv.opacities.data();
+            d.colors = lv.colors[0].v;
+            d.skin_indices = lv.skin_indices[0].data();
+            d.skin_weights = lv.skin_weights[0].data();
+            d.sh = lv.sh.empty() ? nullptr : lv.sh.data();
+            check_gscg(gscg_upload_level(gpu_, t, l, &d), gpu_);
+        }
+    }
+    uploaded_ = store.get();
+    keep_ = store;
+}
+
+void FrameContext::sample_crowd(const Crowd& crowd, float time_s, bool static_pose,
+                                int thread_hint) {
+    const size_t n = crowd.instances.size();
+    const uint32_t rec = 4 + 4 * joint_stride;
+    template_ids.resize(n);
+    placement.resize(n * 4);
+    poses.resize(n * rec);
+    lods.resize(n);
+    const unsigned want = resolve_thread_count(thread_hint);
+    if (!pool_ || pool_->size() != want) pool_ = std::make_unique<HostPool>(want);
+    const TemplateStore& templates = *crowd.templates;
+    const MotionStore& motions = *crowd.motions;
+    for (const CrowdInstance& inst : crowd.instances) {
+        if (inst.template_id >= templates.size() || inst.motion_id >= motions.size())
+            throw std::invalid_argument("render_frame: instance references a missing asset");
+        if (!static_pose && motions[inst.motion_id].joint_count !=
+                                templates[inst.template_id].skeleton.joint_count())
+            throw std::invalid_argument("forward_kinematics: pose joint count mismatch");
+        if (!static_pose && motions[inst.motion_id].frames.empty())
+            throw std::invalid_argument("sample_pose: empty clip");
+    }
+    pool_->parallel_for(n, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            const CrowdInstance& inst = crowd.instances[i];
+            template_ids[i] = inst.template_id;
+            placement[i * 4 + 0] = inst.x;
+            placement[i * 4 + 1] = inst.z;
+            placement[i * 4 + 2] = std::cos(inst.yaw);
+            placement[i * 4 + 3] = std::sin(inst.yaw);
+            lods[i] = inst.active_lod;
+            float* rec_out = poses.data() + i * rec;
+            const uint32_t J = templates[inst.template_id].skeleton.joint_count();
+            if (static_pose) {
+                rec_out[0] = rec_out[1] = rec_out[2] = rec_out[3] = 0.0f;
+                for (uint32_t j = 0; j < J; ++j) {
+                    rec_out[4 + 4 * j + 0] = 0.0f;
+                    rec_out[4 + 4 * j + 1] = 0.0f;
+                    rec_out[4 + 4 * j + 2] = 0.0f;
+                    rec_out[4 + 4 * j + 3] = 1.0f;
+                }
+            } else {
+                const MotionClip& clip = motions[inst.motion_id];
+                sample_pose_into(clip, time_s + inst.phase_offset_s, true, rec_out, joint_stride);
+            }
+        }
+    });
+}
+
+gscg_camera camera_basis(const Camera& cam) {
+    gscg_camera c{};
+    const Mat3 w = cam.view_rotation();
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) c.world_to_view[r * 3 + k] = w(r, k);
+    for (int i = 0; i < 3; ++i) c.position[i] = cam.position[i];
+    c.focal = cam.focal_px();
+    c.cx = 0.5f * static_cast<float>(cam.width);
+    c.cy = 0.5f * static_cast<float>(cam.height);
+    c.near_m = cam.near_m;
+    c.width = cam.width;
+    c.height = cam.height;
+    return c;
+}
+
+void render_frame(Crowd& crowd, const Camera& camera, float time_s,
+                  const RenderSettings& settings, bool static_pose,
+                  std::optional<uint32_t> forced_lod, StageTimes* times, FrameContext& ctx) {
+    validate(settings);
+    validate(camera);
+    validate(crowd.lod);
+    if (crowd.lod.thresholds_m.size() > GSCG_MAX_LOD_THRESHOLDS)
+        throw std::invalid_argument("LodPolicy: too many thresholds for the GPU path");
+    ctx.ensure_templates(crowd.templates);
+
+    using clock = std::chrono::steady_clock;
+    const auto t0 = clock::now();
+    ctx.sample_crowd(crowd, time_s, static_pose, settings.thread_count);
+    const auto t1 = clock::now();
+
+    gscg_frame_desc fd{};
+    fd.instance_count = static_cast<uint32_t>(crowd.instances.size());
+    fd.joint_stride = ctx.joint_stride;
+    fd.template_ids = ctx.template_ids.data();
+    fd.placement = ctx.placement.data();
+    fd.poses = ctx.poses.data();
+    fd.active_lod = ctx.lods.data();
+    fd.forced_lod = forced_lod ? static_cast<int32_t>(*forced_lod) : -1;
+    fd.memory = GSCG_MEM_HOST;
+
+    const gscg_camera cam = camera_basis(camera);
+    gscg_render_settings rs{};
+    rs.tile_size = settings.tile_size;
+    for (int i = 0; i < 3; ++i) rs.background[i] = settings.background[i];
+    rs.alpha_max = settings.alpha_max;
+    rs.alpha_cutoff = settings.alpha_cutoff;
+    rs.transmittance_floor = settings.transmittance_floor;
+    rs.sh_enabled = settings.sh_colour ? 1 : 0;
+    gscg_lod_policy lp{};
+    lp.threshold_count = static_cast<uint32_t>(crowd.lod.thresholds_m.size());
+    for (uint32_t i = 0; i < lp.threshold_count; ++i) lp.thresholds_m[i] = crowd.lod.thresholds_m[i];
+    lp.hysteresis_band_m = crowd.lod.hysteresis_band_m;
+
+    if (ctx.out.color.width != camera.width || ctx.out.color.height != camera.height) {
+        ctx.out.color = Framebuffer(camera.width, camera.height);
+        ctx.out.transmittance.assign(static_cast<size_t>(camera.width) * camera.height, 0.0f);
+    }
+    gscg_stage_times st{};
+    check_gscg(gscg_render_frame(ctx.gpu(), &fd, &cam, &rs, &lp, ctx.out.color.rgb.data(),
+                                 ctx.out.transmittance.data(), &st),
+               ctx.gpu());
+    for (size_t i = 0; i < crowd.instances.size(); ++i) crowd.instances[i].active_lod = ctx.lods[i];
+
+    if (times) {
+        times->pose_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        times->update_ms = times->pose_ms + st.h2d_ms + st.update_ms;
+        times->gather_ms = st.gather_ms;
+        times->sort_ms = st.sort_ms;
+        times->rasterize_ms = st.rasterize_ms + st.d2h_ms;
+        times->splat_count = st.splat_count;
+        times->pair_count = st.pair_count;
+        times->gaussian_count = st.gaussian_count;
+    }
+}
+
+Framebuffer render_frame(Crowd& crowd, const Camera& camera, float time_s,
+                         const RenderSettings& settings, bool static_pose,
+                         std::optional<uint32_t> forced_lod, StageTimes* times) {
+    FrameContext ctx;
+    render_frame(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx);
+    return std::move(ctx.out.color);
+}
+
+}  // namespace gsc

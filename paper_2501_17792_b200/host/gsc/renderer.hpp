@@ -1,0 +1,129 @@
+// render_frame on the B200: host mirror of /root/reference/proj/include/gsc/renderer.hpp
+// (RenderSettings :15-22, Framebuffer :26-37, RasterOutput :52-55, FrameContext :57-79,
+// StageTimes :105-112, render_frame :114-123). The host samples poses (the only
+// transcendental-heavy step, kept on glibc for bit-exact parity) on a persistent
+// thread pool and hands everything else to the GPU through the gscg C-ABI
+// (include/gscg.h). There is no CPU fallback: construction fails without a GPU.
+#pragma once
+
+#include "gsc/crowd.hpp"
+#include "gscg.h"
+
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <stdexcept>
+#include <thread>
+
+namespace gsc {
+
+struct RenderSettings {
+    int tile_size = 16;
+    Vec3 background = Vec3::Zero();
+    float alpha_max = kAlphaMax;
+    float alpha_cutoff = kAlphaCutoff;
+    float transmittance_floor = 1e-4f;
+    int thread_count = 0;  // host pose-sampling threads; 0 = GSCROWD_THREADS / hardware
+    bool sh_colour = true; // evaluate the SH residual when templates carry it
+};
+
+void validate(const RenderSettings& s);
+
+struct Framebuffer {
+    int width = 0;
+    int height = 0;
+    std::vector<float> rgb;
+    Framebuffer() = default;
+    Framebuffer(int w, int h) : width(w), height(h), rgb(static_cast<size_t>(w) * h * 3, 0.0f) {}
+    float* pixel(int x, int y) { return rgb.data() + 3 * (static_cast<size_t>(y) * width + x); }
+    const float* pixel(int x, int y) const {
+        return rgb.data() + 3 * (static_cast<size_t>(y) * width + x);
+    }
+};
+
+struct RasterOutput {
+    Framebuffer color;
+    std::vector<float> transmittance;
+};
+
+struct StageTimes {
+    double update_ms = 0.0;     // host pose sampling + H2D + LoD/FK kernels
+    double gather_ms = 0.0;     // LBS + projection + pair emission
+    double sort_ms = 0.0;       // radix sort + tile ranges
+    double rasterize_ms = 0.0;  // tile blend + D2H
+    double pose_ms = 0.0;       // host part of update
+    double total_ms() const { return update_ms + gather_ms + sort_ms + rasterize_ms; }
+    uint64_t splat_count = 0;
+    uint64_t pair_count = 0;
+    uint64_t gaussian_count = 0;
+};
+
+// Error from the C-ABI, rethrown as the reference's exception types.
+struct GpuError : std::runtime_error {
+    int status;
+    GpuError(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+void check_gscg(int status, const gscg_ctx* ctx);
+
+// Static-partition fork/join over persistent threads (the reference spawns threads per
+// call, parallel.hpp:26-42; the partition is the same contiguous chunking).
+class HostPool {
+public:
+    explicit HostPool(unsigned threads);
+    ~HostPool();
+    unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
+    void parallel_for(size_t count, const std::function<void(size_t, size_t)>& fn);
+
+private:
+    void worker(unsigned index);
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t, size_t)>* job_ = nullptr;
+    size_t count_ = 0;
+    uint64_t generation_ = 0;
+    unsigned pending_ = 0;
+    bool stop_ = false;
+};
+
+unsigned resolve_thread_count(int hint);
+
+class FrameContext {
+public:
+    explicit FrameContext(int device = 0);
+    ~FrameContext();
+    FrameContext(const FrameContext&) = delete;
+    FrameContext& operator=(const FrameContext&) = delete;
+
+    gscg_ctx* gpu() { return gpu_; }
+    // Uploads the store once per pointer identity (shared-attribute residency).
+    void ensure_templates(const std::shared_ptr<const TemplateStore>& store);
+    // Fills the per-frame pose / placement records for the whole crowd on the pool.
+    void sample_crowd(const Crowd& crowd, float time_s, bool static_pose, int thread_hint);
+
+    RasterOutput out;
+    std::vector<uint32_t> template_ids;
+    std::vector<float> placement;  // n x 4
+    std::vector<float> poses;      // n x (4 + 4 * joint_stride)
+    std::vector<uint32_t> lods;
+    uint32_t joint_stride = 0;
+
+private:
+    gscg_ctx* gpu_ = nullptr;
+    const TemplateStore* uploaded_ = nullptr;
+    std::shared_ptr<const TemplateStore> keep_;
+    std::unique_ptr<HostPool> pool_;
+};
+
+gscg_camera camera_basis(const Camera& cam);
+
+void render_frame(Crowd& crowd, const Camera& camera, float time_s,
+                  const RenderSettings& settings, bool static_pose,
+                  std::optional<uint32_t> forced_lod, StageTimes* times, FrameContext& ctx);
+
+Framebuffer render_frame(Crowd& crowd, const Camera& camera, float time_s,
+                         const RenderSettings& settings, bool static_pose = false,
+                         std::optional<uint32_t> forced_lod = std::nullopt,
+                         StageTimes* times = nullptr);
+
+}  // namespace gsc
