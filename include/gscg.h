@@ -171,6 +171,8 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
 /* Device pointers of the context's framebuffer (valid until the next render). */
 int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T);
 int gscg_synchronize(gscg_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for event timing by the caller. */
+int gscg_stream(gscg_ctx* ctx, void** stream);
 
 /* Parity / debug exports of the last frame. */
 int gscg_get_counts(gscg_ctx* ctx, uint64_t* gaussians, uint64_t* splats, uint64_t* pairs);

@@ -723,6 +723,12 @@ int gscg_synchronize(gscg_ctx* ctx) {
     return guarded(ctx, [&] { CUDA_TRY(cudaStreamSynchronize(ctx->stream)); });
 }
 
+int gscg_stream(gscg_ctx* ctx, void** stream) {
+    if (!ctx || !stream) return GSCG_ERR_INVALID_ARGUMENT;
+    *stream = ctx->stream;
+    return GSCG_OK;
+}
+
 int gscg_get_counts(gscg_ctx* ctx, uint64_t* gaussians, uint64_t* splats, uint64_t* pairs) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     if (gaussians) *gaussians = ctx->G;

@@ -113,6 +113,7 @@ GSCG_SYMBOLS = {
                                     C.POINTER(GscgStageTimes)]),
     "gscg_framebuffer_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),
     "gscg_synchronize": (C.c_int, [_P]),
+    "gscg_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "gscg_get_counts": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "gscg_get_lod": (C.c_int, [_P, _P, C.c_uint32]),
     "gscg_get_instance_base": (C.c_int, [_P, _P, C.c_uint32]),
