@@ -101,6 +101,25 @@ int gsch_scene_skeleton(const gsch_scene* scene, uint32_t template_id, uint32_t*
 int gsch_scene_motion(const gsch_scene* scene, uint32_t motion_id, float* fps, uint32_t* frames,
                       uint32_t* joints, float* out);
 
+/* Host pose sampling without a GPU: same records as gsch_sample_crowd. */
+int gsch_scene_sample_crowd(gsch_scene* scene, float time_s, int32_t static_pose, int32_t threads,
+                            uint32_t joint_stride, uint32_t* template_ids, float* placement, float* poses);
+
+/* Replace (motion_id < count) or append (motion_id == count) a clip; same layout as above. */
+int gsch_scene_set_motion(gsch_scene* scene, uint32_t motion_id, float fps, uint32_t frames,
+                          uint32_t joints, const float* data);
+
+/* Shared-attribute memory accounting (crowd.cpp:142-210, MemoryLayoutModel defaults). */
+typedef struct {
+  uint64_t naive_bytes, shared_bytes;
+  double savings_fraction;
+  double naive_marginal_bytes_per_instance, shared_marginal_bytes_per_instance;
+  uint64_t resident_template_bytes, posed_mean_bytes, instance_count;
+} gsch_memory_report;
+int gsch_memory_report_cell(uint64_t instances, uint64_t gaussians, uint64_t fixed_overhead,
+                            gsch_memory_report* out);
+int gsch_scene_memory_report(const gsch_scene* scene, gsch_memory_report* out);
+
 int gsch_renderer_create(gsch_scene* scene, int device, gsch_renderer** out);
 int gsch_renderer_destroy(gsch_renderer* r);
 gscg_ctx* gsch_renderer_gpu(gsch_renderer* r);

@@ -215,12 +215,42 @@ class Scene:
         inv = np.ctypeslib.as_array((C.c_float * (16 * J)).from_address(ib.value)).reshape(J, 16).copy()
         return {"joint_count": J, "parents": parents, "inverse_bind": inv}
 
+    def sample_crowd(self, time_s: float, static_pose: bool = False, threads: int = 0, joint_stride: int = 24):
+        """Host pose records (no GPU needed): template ids, placement, poses."""
+        n = self.counts()[2]
+        tids = np.zeros(max(n, 1), dtype=np.uint32)
+        place = np.zeros((max(n, 1), 4), dtype=np.float32)
+        poses = np.zeros((max(n, 1), 4 + 4 * joint_stride), dtype=np.float32)
+        N.check_gsch(N.gsch().gsch_scene_sample_crowd(self._h, time_s, int(static_pose), threads, joint_stride,
+                                                      _ptr(tids), _ptr(place), _ptr(poses)))
+        return tids[:n], place[:n], poses[:n]
+
+    def set_motion(self, m: int, fps: float, data: np.ndarray, joints: int) -> None:
+        data = np.ascontiguousarray(data, dtype=np.float32)
+        N.check_gsch(N.gsch().gsch_scene_set_motion(self._h, m, fps, data.shape[0], joints, _ptr(data)))
+
+    def memory_report(self) -> dict:
+        r = N.GschMemoryReport()
+        N.check_gsch(N.gsch().gsch_scene_memory_report(self._h, C.byref(r)))
+        return _report(r)
+
     def motion(self, m: int) -> dict:
         fps, frames, joints = C.c_float(), C.c_uint32(), C.c_uint32()
         N.check_gsch(N.gsch().gsch_scene_motion(self._h, m, C.byref(fps), C.byref(frames), C.byref(joints), None))
         data = np.zeros((frames.value, 4 + 4 * joints.value), dtype=np.float32)
         N.check_gsch(N.gsch().gsch_scene_motion(self._h, m, None, None, None, _ptr(data)))
         return {"fps": fps.value, "frames": frames.value, "joints": joints.value, "data": data}
+
+
+def _report(r: N.GschMemoryReport) -> dict:
+    return {f: getattr(r, f) for f, _ in r._fields_}
+
+
+def memory_report_cell(instances: int, gaussians: int, fixed_overhead: int = 0) -> dict:
+    """MemoryLayoutModel accounting for one table cell (crowd.cpp:205-210)."""
+    r = N.GschMemoryReport()
+    N.check_gsch(N.gsch().gsch_memory_report_cell(instances, gaussians, fixed_overhead, C.byref(r)))
+    return _report(r)
 
 
 class Renderer:

@@ -144,28 +144,24 @@ void FrameContext::ensure_templates(const std::shared_ptr<const TemplateStore>& 
     keep_ = store;
 }
 
-void FrameContext::sample_crowd(const Crowd& crowd, float time_s, bool static_pose,
-                                int thread_hint) {
+void sample_crowd_records(const Crowd& crowd, float time_s, bool static_pose, uint32_t joint_stride,
+                          HostPool& pool, uint32_t* template_ids, float* placement, float* poses,
+                          uint32_t* lods) {
     const size_t n = crowd.instances.size();
     const uint32_t rec = 4 + 4 * joint_stride;
-    template_ids.resize(n);
-    placement.resize(n * 4);
-    poses.resize(n * rec);
-    lods.resize(n);
-    const unsigned want = resolve_thread_count(thread_hint);
-    if (!pool_ || pool_->size() != want) pool_ = std::make_unique<HostPool>(want);
     const TemplateStore& templates = *crowd.templates;
     const MotionStore& motions = *crowd.motions;
     for (const CrowdInstance& inst : crowd.instances) {
         if (inst.template_id >= templates.size() || inst.motion_id >= motions.size())
             throw std::invalid_argument("render_frame: instance references a missing asset");
-        if (!static_pose && motions[inst.motion_id].joint_count !=
-                                templates[inst.template_id].skeleton.joint_count())
+        const uint32_t J = templates[inst.template_id].skeleton.joint_count();
+        if (J > joint_stride) throw std::invalid_argument("joint_stride below the skeleton's joint count");
+        if (!static_pose && motions[inst.motion_id].joint_count != J)
             throw std::invalid_argument("forward_kinematics: pose joint count mismatch");
         if (!static_pose && motions[inst.motion_id].frames.empty())
             throw std::invalid_argument("sample_pose: empty clip");
     }
-    pool_->parallel_for(n, [&](size_t b, size_t e) {
+    pool.parallel_for(n, [&](size_t b, size_t e) {
         for (size_t i = b; i < e; ++i) {
             const CrowdInstance& inst = crowd.instances[i];
             template_ids[i] = inst.template_id;
@@ -173,8 +169,8 @@ void FrameContext::sample_crowd(const Crowd& crowd, float time_s, bool static_po
             placement[i * 4 + 1] = inst.z;
             placement[i * 4 + 2] = std::cos(inst.yaw);
             placement[i * 4 + 3] = std::sin(inst.yaw);
-            lods[i] = inst.active_lod;
-            float* rec_out = poses.data() + i * rec;
+            if (lods) lods[i] = inst.active_lod;
+            float* rec_out = poses + i * rec;
             const uint32_t J = templates[inst.template_id].skeleton.joint_count();
             if (static_pose) {
                 rec_out[0] = rec_out[1] = rec_out[2] = rec_out[3] = 0.0f;
@@ -185,11 +181,25 @@ void FrameContext::sample_crowd(const Crowd& crowd, float time_s, bool static_po
                     rec_out[4 + 4 * j + 3] = 1.0f;
                 }
             } else {
-                const MotionClip& clip = motions[inst.motion_id];
-                sample_pose_into(clip, time_s + inst.phase_offset_s, true, rec_out, joint_stride);
+                sample_pose_into(motions[inst.motion_id], time_s + inst.phase_offset_s, true, rec_out,
+                                 joint_stride);
             }
         }
     });
+}
+
+void FrameContext::sample_crowd(const Crowd& crowd, float time_s, bool static_pose,
+                                int thread_hint) {
+    const size_t n = crowd.instances.size();
+    const uint32_t rec = 4 + 4 * joint_stride;
+    template_ids.resize(n);
+    placement.resize(n * 4);
+    poses.resize(n * rec);
+    lods.resize(n);
+    const unsigned want = resolve_thread_count(thread_hint);
+    if (!pool_ || pool_->size() != want) pool_ = std::make_unique<HostPool>(want);
+    sample_crowd_records(crowd, time_s, static_pose, joint_stride, *pool_, template_ids.data(),
+                         placement.data(), poses.data(), lods.data());
 }
 
 gscg_camera camera_basis(const Camera& cam) {

@@ -88,6 +88,12 @@ private:
 
 unsigned resolve_thread_count(int hint);
 
+// Per-instance pose records for the GPU (update_crowd up to the pose, crowd.cpp:118-124):
+// template ids, placement (x, z, cos yaw, sin yaw) and sampled poses, on the pool.
+void sample_crowd_records(const Crowd& crowd, float time_s, bool static_pose, uint32_t joint_stride,
+                          HostPool& pool, uint32_t* template_ids, float* placement, float* poses,
+                          uint32_t* lods);
+
 class FrameContext {
 public:
     explicit FrameContext(int device = 0);

@@ -239,6 +239,71 @@ int gsch_scene_motion(const gsch_scene* s, uint32_t m, float* fps, uint32_t* fra
     return 0;
 }
 
+int gsch_scene_sample_crowd(gsch_scene* s, float time_s, int32_t static_pose, int32_t threads,
+                            uint32_t joint_stride, uint32_t* template_ids, float* placement, float* poses) {
+    return guarded([&] {
+        if (!s || !template_ids || !placement || !poses) throw std::invalid_argument("null argument");
+        HostPool pool(resolve_thread_count(threads));
+        sample_crowd_records(s->crowd, time_s, static_pose != 0, joint_stride, pool, template_ids, placement,
+                             poses, nullptr);
+    });
+}
+
+int gsch_scene_set_motion(gsch_scene* s, uint32_t m, float fps, uint32_t frames, uint32_t joints,
+                          const float* data) {
+    return guarded([&] {
+        if (!s || (frames && !data)) throw std::invalid_argument("bad motion");
+        if (m > s->motions->size()) throw std::invalid_argument("motion id beyond the store");
+        MotionClip clip;
+        clip.fps = fps;
+        clip.joint_count = static_cast<uint16_t>(joints);
+        clip.frames.resize(frames);
+        const size_t rec = 4 + 4 * static_cast<size_t>(joints);
+        for (uint32_t f = 0; f < frames; ++f) {
+            const float* d = data + f * rec;
+            clip.frames[f].root_translation = Vec3(d[0], d[1], d[2]);
+            clip.frames[f].local_rotations.resize(joints);
+            for (uint32_t j = 0; j < joints; ++j)
+                clip.frames[f].local_rotations[j] = Quat::FromCoeffs(d + 4 + 4 * j);
+        }
+        validate(clip);
+        // Copy-on-write: renderers keep the old store alive; motions are read per frame.
+        auto next = std::make_shared<MotionStore>(*s->motions);
+        if (m == next->size()) next->push_back(std::move(clip));
+        else (*next)[m] = std::move(clip);
+        s->motions = next;
+        s->crowd.motions = next;
+    });
+}
+
+static void fill_report(const MemoryReport& r, gsch_memory_report* out) {
+    out->naive_bytes = r.naive_bytes;
+    out->shared_bytes = r.shared_bytes;
+    out->savings_fraction = r.savings_fraction;
+    out->naive_marginal_bytes_per_instance = r.naive_marginal_bytes_per_instance;
+    out->shared_marginal_bytes_per_instance = r.shared_marginal_bytes_per_instance;
+    out->resident_template_bytes = r.resident_template_bytes;
+    out->posed_mean_bytes = r.posed_mean_bytes;
+    out->instance_count = r.instance_count;
+}
+
+int gsch_memory_report_cell(uint64_t instances, uint64_t gaussians, uint64_t fixed_overhead,
+                            gsch_memory_report* out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("null output");
+        MemoryLayoutModel model;
+        model.fixed_overhead_bytes = fixed_overhead;
+        fill_report(memory_report_cell(instances, gaussians, model), out);
+    });
+}
+
+int gsch_scene_memory_report(const gsch_scene* s, gsch_memory_report* out) {
+    return guarded([&] {
+        if (!s || !out) throw std::invalid_argument("null argument");
+        fill_report(memory_report(s->crowd, MemoryLayoutModel{}), out);
+    });
+}
+
 int gsch_renderer_create(gsch_scene* scene, int device, gsch_renderer** out) {
     return guarded([&] {
         if (!scene || !out) throw std::invalid_argument("null argument");

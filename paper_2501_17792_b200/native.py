@@ -92,6 +92,13 @@ class GschRenderSettings(C.Structure):
                 ("sh_colour", C.c_int32)]
 
 
+class GschMemoryReport(C.Structure):
+    _fields_ = [("naive_bytes", C.c_uint64), ("shared_bytes", C.c_uint64), ("savings_fraction", C.c_double),
+                ("naive_marginal_bytes_per_instance", C.c_double), ("shared_marginal_bytes_per_instance", C.c_double),
+                ("resident_template_bytes", C.c_uint64), ("posed_mean_bytes", C.c_uint64),
+                ("instance_count", C.c_uint64)]
+
+
 class GschStageTimes(C.Structure):
     _fields_ = [("update_ms", C.c_double), ("gather_ms", C.c_double), ("sort_ms", C.c_double),
                 ("rasterize_ms", C.c_double), ("pose_ms", C.c_double), ("total_ms", C.c_double),
@@ -138,6 +145,10 @@ GSCH_SYMBOLS = {
     "gsch_scene_skeleton": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(_P), C.POINTER(_P)]),
     "gsch_scene_motion": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_float), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_uint32), _P]),
+    "gsch_scene_sample_crowd": (C.c_int, [_P, C.c_float, C.c_int32, C.c_int32, C.c_uint32, _P, _P, _P]),
+    "gsch_scene_set_motion": (C.c_int, [_P, C.c_uint32, C.c_float, C.c_uint32, C.c_uint32, _P]),
+    "gsch_memory_report_cell": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(GschMemoryReport)]),
+    "gsch_scene_memory_report": (C.c_int, [_P, C.POINTER(GschMemoryReport)]),
     "gsch_renderer_create": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "gsch_renderer_destroy": (C.c_int, [_P]),
     "gsch_renderer_gpu": (_P, [_P]),

@@ -1,0 +1,87 @@
+"""GPU-vs-oracle parity checks shared by the GPU tests and smoke().
+
+Bars (BASELINE.json north_star): LoD, splat set, depth bits, rects, tile ranges and the
+per-tile (sort) order bit-exact; skinned positions within 1e-3 (they are in fact
+bit-identical and checked as such); pixels max abs <= 1e-3 per channel and PSNR >= 50 dB.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2501_17792_b200 import native as N
+
+PIXEL_TOL = 1e-3
+PSNR_MIN = 50.0
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    """metrics.cpp:8-23 (double accumulation, cap 99 dB)."""
+    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    return 99.0 if mse == 0 else min(99.0, 10.0 * np.log10(1.0 / mse))
+
+
+def render_both(scene, renderer, oracle_scene, time_s=0.0, tile_size=16, background=(0.0, 0.0, 0.0),
+                static_pose=False, forced_lod=None, sh=True, debug=True):
+    import paper_2501_17792_b200 as P
+    from oracle import orc
+
+    if debug:
+        renderer.set_debug(N.GSCG_DEBUG_POSED | N.GSCG_DEBUG_RECORDS)
+    st = P.RenderSettings(tile_size=tile_size, background=background, sh_colour=sh)
+    rgb, T = renderer.render_frame(time_s, st, static_pose, forced_lod)
+    orgb, oT, times = oracle_scene.render(time_s, orc.settings(tile_size=tile_size, background=background,
+                                                               sh_colour=sh), static_pose, forced_lod)
+    return (rgb, T), (orgb, oT, times)
+
+
+def check_frame(scene, renderer, oracle_scene, gpu_out, orc_out, tile_size=16, full=True) -> dict:
+    rgb, T = gpu_out
+    orgb, oT, times = orc_out
+    n = scene.counts()[2]
+    cfg = scene.cfg
+    report = {}
+    lods = renderer.lods()
+    assert np.array_equal(lods, oracle_scene.lods(n)), "LoD selection differs"
+    G, S, K = renderer.counts()
+    assert (G, S, K) == (times.gaussian_count, times.splat_count, times.pair_count), \
+        f"counts G/S/K gpu {(G, S, K)} oracle {(times.gaussian_count, times.splat_count, times.pair_count)}"
+    report.update(G=G, S=S, K=K)
+    if full:
+        pm, opm = renderer.posed_means(), oracle_scene.posed()
+        assert pm.shape == opm.shape
+        if len(pm):
+            err = float(np.abs(pm - opm).max())
+            assert err <= 1e-3, f"posed means max abs {err}"
+            assert pm.tobytes() == opm.tobytes(), "posed means are not bit-identical"
+        rec = renderer.splat_records()
+        osp = oracle_scene.splats()
+        base = renderer.instance_base()
+        oord = base[osp["instance_id"]].astype(np.int64) + osp["gaussian_index"]
+        by_ord = np.argsort(oord, kind="stable")
+        o_sorted = osp[by_ord]
+        assert np.array_equal(rec["ordinal"], oord[by_ord]), "surviving splat set differs"
+        for f in ("depth", "cov_xx", "cov_xy", "cov_yy"):
+            assert rec[f].tobytes() == o_sorted[f].tobytes(), f"{f} not bit-identical"
+        assert rec["mean_px"].tobytes() == o_sorted["mean_px"].tobytes(), "mean_px not bit-identical"
+        assert np.array_equal(rec["rect"], o_sorted["rect"]), "pixel rects differ"
+        if len(rec):
+            report["color_max_abs"] = float(np.abs(rec["color"] - o_sorted["color"]).max())
+            assert report["color_max_abs"] <= 1e-5
+        tiles_x = (cfg.width + tile_size - 1) // tile_size
+        tiles_y = (cfg.height + tile_size - 1) // tile_size
+        ranges = renderer.tile_ranges(tiles_x * tiles_y)
+        counts, items = oracle_scene.bins(tiles_x * tiles_y)
+        assert np.array_equal(ranges[:, 1] - ranges[:, 0], counts), "per-tile pair counts differ"
+        nz = counts > 0
+        starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
+        assert np.array_equal(ranges[nz, 0], starts[nz]), "tile ranges are not the prefix layout"
+        sorted_ord = renderer.sorted_ordinals()
+        assert np.array_equal(sorted_ord.astype(np.int64), oord[items]), "per-tile sort order differs"
+    diff = np.abs(rgb - orgb)
+    report["max_abs"] = float(diff.max()) if diff.size else 0.0
+    report["T_max_abs"] = float(np.abs(T - oT).max()) if T.size else 0.0
+    report["psnr"] = psnr(rgb, orgb)
+    assert report["max_abs"] <= PIXEL_TOL, f"pixel max abs {report['max_abs']}"
+    assert report["T_max_abs"] <= PIXEL_TOL, f"transmittance max abs {report['T_max_abs']}"
+    assert report["psnr"] >= PSNR_MIN, f"PSNR {report['psnr']}"
+    return report

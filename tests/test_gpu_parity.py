@@ -1,0 +1,180 @@
+"""GPU parity: the B200 render path (through the C-ABI) against the CPU oracle on the same
+seeded inputs — the reference's scene fixtures (test_renderer.cpp:13-37,
+test_crowd.cpp:14-44), BASELINE configs 1-3 at full size, and the edge cases the
+reference tests (empty crowd, culling, tile sizes 1..40, static pose, forced LoD,
+hysteresis, footprint locality, determinism)."""
+import numpy as np
+import pytest
+
+import paper_2501_17792_b200 as P
+from oracle import orc
+from tests.parity import check_frame, render_both
+
+pytestmark = pytest.mark.gpu
+
+
+def fixture_scene(count=4, rows=2, cols=2, seed=42, sh=False):
+    cfg = P.SceneConfig(template_count=1, template_seed_base=1, level_counts=(80, 30, 12), with_sh=sh,
+                        motion_count=1, motion_seed_base=2, motion_frames=24, grid_rows=rows, grid_cols=cols,
+                        grid_spacing=1.2, crowd_count=count, crowd_seed=seed, cam_pos=(0.6, 1.5, -3.5),
+                        cam_look=(0.6, 1.0, 2.0), width=200, height=120)
+    return P.Scene(cfg)
+
+
+def basic_scene(count=16, rows=4, cols=4, seed=77, templates=2, motions=3, sh=True):
+    cfg = P.SceneConfig(template_count=templates, level_counts=(60, 24, 8), with_sh=sh, motion_count=motions,
+                        motion_frames=24, grid_rows=rows, grid_cols=cols, crowd_count=count, crowd_seed=seed,
+                        cam_pos=(0.0, 1.6, -3.0), cam_look=(0.0, 1.0, 5.0), width=160, height=90)
+    return P.Scene(cfg)
+
+
+def parity(scene, time_s=0.0, **kw):
+    r = P.Renderer(scene)
+    o = orc.from_scene(scene)
+    g, c = render_both(scene, r, o, time_s, **kw)
+    return check_frame(scene, r, o, g, c, tile_size=kw.get("tile_size", 16))
+
+
+@pytest.mark.parametrize("time_s", [0.0, 0.37, 1.3])
+def test_fixture_scene(time_s):
+    parity(fixture_scene(), time_s, background=(0.1, 0.1, 0.15))
+
+
+@pytest.mark.parametrize("tile_size", [1, 3, 8, 16, 17, 32, 40])
+def test_tile_sizes(tile_size):
+    parity(fixture_scene(9, 3, 3, seed=55), 0.37, tile_size=tile_size, background=(0.2, 0.4, 0.6))
+
+
+def test_crowd_with_sh_and_lod_mix():
+    rep = parity(basic_scene(), 0.7, background=(0.05, 0.05, 0.05))
+    assert rep["S"] > 0
+
+
+@pytest.mark.parametrize("forced", [0, 1, 2, 5])
+def test_forced_lod(forced):
+    parity(basic_scene(sh=False), 0.4, forced_lod=forced)
+
+
+def test_static_pose():
+    parity(basic_scene(), 0.0, static_pose=True, background=(0.3, 0.2, 0.1))
+
+
+def test_empty_crowd_is_background():
+    s = basic_scene()
+    s.instances = s.instances[:0]
+    r = P.Renderer(s)
+    rgb, T = r.render_frame(0.0, P.RenderSettings(background=(0.2, 0.4, 0.6)))
+    assert np.all(rgb == np.array([0.2, 0.4, 0.6], np.float32)) and np.all(T == 1.0)
+    assert r.counts() == (0, 0, 0)
+
+
+def test_culled_instances_behind_and_offscreen():
+    s = basic_scene(count=4, rows=2, cols=2)
+    inst = s.instances
+    inst["z"] = [-10.0, -3.0, 5.0, 500.0]   # behind, at the camera plane, visible, far
+    inst["x"] = [0.0, 0.0, 60.0, 0.0]        # the visible-depth one is far off-screen sideways
+    s.instances = inst
+    rep = parity(s, 0.2)
+    assert rep["S"] < rep["G"]
+
+
+def test_hysteresis_across_frames():
+    s = basic_scene(count=4, rows=1, cols=4, sh=False)
+    s.set_lod_policy((3.0, 6.0), hysteresis=1.0)
+    r = P.Renderer(s)
+    o = orc.from_scene(s)
+    o.set_lod((3.0, 6.0), 1.0)
+    for z in (-0.5, 0.0, 0.3, 0.6, 0.3, -0.2, 3.0, 3.4, 2.8, 3.2):
+        s.set_camera((0.0, 1.6, -3.0 - z), (0.0, 1.0, 5.0))
+        o.set_camera((0.0, 1.6, -3.0 - z), (0.0, 1.0, 5.0), 50.0, 160, 90)
+        g, c = render_both(s, r, o, 0.1)
+        check_frame(s, r, o, g, c)
+        assert np.array_equal(s.instances["active_lod"], r.lods())
+
+
+def test_static_equals_motion_on_bind_pose_clip():
+    s = fixture_scene(4, 2, 2, seed=5)
+    clip = np.zeros((1, 4 + 96), np.float32)
+    clip[0, 7::4] = 1.0
+    s.set_motion(0, 1.0, clip, 24)
+    r = P.Renderer(s)
+    a, _ = r.render_frame(0.0, P.RenderSettings(), static_pose=False)
+    b, _ = r.render_frame(0.0, P.RenderSettings(), static_pose=True)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_moving_one_instance_changes_only_its_footprint():
+    near = fixture_scene(4, 2, 2, seed=9)
+    far = fixture_scene(4, 2, 2, seed=9)
+    inst = far.instances
+    inst["z"][1] += 9.0
+    far.instances = inst
+    st = P.RenderSettings(background=(0.05, 0.05, 0.05))
+    rn, rf = P.Renderer(near), P.Renderer(far)
+    box = [10 ** 9, 10 ** 9, -1, -1]
+    imgs = []
+    for s, r in ((near, rn), (far, rf)):
+        r.set_debug(2)
+        img, _ = r.render_frame(0.2, st)
+        imgs.append(img)
+        rec = r.splat_records()
+        mine = rec[rec["instance_id"] == 1]
+        box = [min(box[0], mine["rect"][:, 0].min()), min(box[1], mine["rect"][:, 1].min()),
+               max(box[2], mine["rect"][:, 2].max()), max(box[3], mine["rect"][:, 3].max())]
+    diff = np.any(imgs[0] != imgs[1], axis=2)
+    ys, xs = np.nonzero(diff)
+    assert len(xs) > 0
+    assert (xs >= box[0]).all() and (xs < box[2]).all() and (ys >= box[1]).all() and (ys < box[3]).all()
+
+
+def test_repeated_frames_are_byte_identical():
+    s = basic_scene(count=16)
+    r = P.Renderer(s)
+    outs = [r.render_frame(0.55, P.RenderSettings())[0].tobytes() for _ in range(3)]
+    assert outs[0] == outs[1] == outs[2]
+
+
+def test_invalid_settings_raise():
+    s = basic_scene(count=1, rows=1, cols=1)
+    r = P.Renderer(s)
+    with pytest.raises(ValueError):
+        r.render_frame(0.0, P.RenderSettings(tile_size=0))
+    with pytest.raises(ValueError):
+        r.render_frame(0.0, P.RenderSettings(alpha_cutoff=1.5))
+    with pytest.raises(ValueError):
+        r.render_frame(0.0, P.RenderSettings(transmittance_floor=0.0))
+
+
+def test_convex_hull_and_transmittance_range():
+    s = basic_scene(count=16)
+    r = P.Renderer(s)
+    rgb, T = r.render_frame(0.3, P.RenderSettings(background=(0.3, 0.3, 0.3), sh_colour=False))
+    assert rgb.min() >= 0.0 and rgb.max() <= 1.0 + 1e-5
+    assert T.min() >= 0.0 and T.max() <= 1.0
+
+
+def config_scene(idx):
+    cfg, extra = P.baseline_config(idx)
+    s = P.Scene(cfg)
+    if extra["origin_instance"]:
+        P.place_origin_instance(s)
+    return s, extra
+
+
+@pytest.mark.parametrize("idx", [1, 2])
+def test_baseline_config(idx):
+    s, extra = config_scene(idx)
+    rep = parity(s, extra["time_s"], forced_lod=extra["forced_lod"])
+    assert rep["S"] > 0 and rep["K"] > 0
+
+
+@pytest.mark.slow
+def test_baseline_config3_headline():
+    s, extra = config_scene(3)
+    r = P.Renderer(s)
+    o = orc.from_scene(s)
+    g, c = render_both(s, r, o, 0.5)
+    rep = check_frame(s, r, o, g, c)
+    assert rep["G"] == 14972565 and rep["S"] > 10_000_000
+    again, _ = r.render_frame(0.5, P.RenderSettings())
+    assert again.tobytes() == g[0].tobytes()
