@@ -253,7 +253,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     stage_ms = {k: med(k + "_ms") for k in ("update", "gather", "sort", "rasterize")}
     rb = roofline_bytes(cfg, counts, lods, scene, sh=True)
     dom = "rasterize" if stage_ms["rasterize"] >= stage_ms["gather"] else "gather"
-    kernel = {"rasterize": "k_raster16", "gather": "k_project"}[dom]
+    kernel = {"rasterize": "k_raster16q", "gather": "k_project"}[dom]
     kbytes = rb["raster"] if dom == "rasterize" else rb["project"]
     achieved = kbytes / (stage_ms[dom] * 1e-3) / 1e9
     traffic = None

@@ -180,7 +180,13 @@ int gscg_get_lod(gscg_ctx* ctx, uint32_t* out, uint32_t n);
 int gscg_get_instance_base(gscg_ctx* ctx, uint32_t* out, uint32_t n);
 int gscg_get_posed_means(gscg_ctx* ctx, float* out, uint64_t gaussians);
 int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splats);
-int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t tiles); /* tiles x 2 */
+/* Binning layout of the last frame: pairs are binned per cell; a cell is the whole tile,
+ * or for tile size 16 one 8x8 quadrant (cell = tile * 4 + (y & 1) * 2 + (x & 1) over
+ * quadrant coordinates), so every tile owns cells_per_tile consecutive cells and one
+ * contiguous range of the sorted pairs. The reference's per-tile list (bins,
+ * renderer.cpp:147-161) is the order-preserving merge of its cells' lists. */
+int gscg_get_cell_layout(gscg_ctx* ctx, uint32_t* tiles, uint32_t* cells_per_tile);
+int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells); /* cells x 2: [start, end) */
 int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs);
 
 #ifdef __cplusplus

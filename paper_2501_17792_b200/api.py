@@ -330,10 +330,39 @@ class Renderer:
         N.check_gscg(N.gscg().gscg_get_splat_records(self.gpu, C.addressof(out), s), self.gpu)
         return np.ctypeslib.as_array(out)[:s].copy() if s else np.zeros(0, dtype=np.ctypeslib.as_array(out).dtype)
 
-    def tile_ranges(self, tiles: int) -> np.ndarray:
-        out = np.zeros((tiles, 2), dtype=np.uint32)
-        N.check_gscg(N.gscg().gscg_get_tile_ranges(self.gpu, _ptr(out), tiles), self.gpu)
+    def cell_layout(self) -> tuple[int, int]:
+        """(tiles, cells per tile) of the last frame's binning (see gscg_get_cell_layout)."""
+        t, c = C.c_uint32(), C.c_uint32()
+        N.check_gscg(N.gscg().gscg_get_cell_layout(self.gpu, C.byref(t), C.byref(c)), self.gpu)
+        return t.value, c.value
+
+    def cell_ranges(self) -> np.ndarray:
+        """[start, end) into the sorted pairs for every binning cell (tiles x cells_per_tile)."""
+        tiles, cpt = self.cell_layout()
+        out = np.zeros((tiles * cpt, 2), dtype=np.uint32)
+        N.check_gscg(N.gscg().gscg_get_tile_ranges(self.gpu, _ptr(out), tiles * cpt), self.gpu)
         return out
+
+    def tile_lists(self, depth_of_ordinal=None) -> tuple[np.ndarray, np.ndarray]:
+        """The reference's per-tile lists (bins) as (counts per tile, concatenated splat
+        ordinals): each tile's cell lists merged in (depth, ordinal) order, duplicates of a
+        splat spanning several cells kept once. depth_of_ordinal maps ordinal -> depth bits
+        (from splat_records); needed only when cells_per_tile > 1."""
+        tiles, cpt = self.cell_layout()
+        ranges = self.cell_ranges()
+        ords = self.sorted_ordinals().astype(np.int64)
+        counts = np.zeros(tiles, dtype=np.int64)
+        items = []
+        for t in range(tiles):
+            segs = [ords[ranges[t * cpt + q, 0]:ranges[t * cpt + q, 1]] for q in range(cpt)]
+            lst = np.concatenate(segs) if cpt > 1 else segs[0]
+            if cpt > 1 and len(lst):
+                lst = np.unique(lst)
+                keys = depth_of_ordinal(lst)
+                lst = lst[np.lexsort((lst, keys))]
+            counts[t] = len(lst)
+            items.append(lst)
+        return counts, (np.concatenate(items) if items else np.zeros(0, np.int64))
 
     def sorted_ordinals(self) -> np.ndarray:
         k = self.counts()[2]

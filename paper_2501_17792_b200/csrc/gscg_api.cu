@@ -5,7 +5,9 @@
 //   H2D of the frame records (pinned staging, one copy)
 //   update:    k_lod_plan (1 CTA) -> k_fk_skin
 //   gather:    k_project (persistent, template-major)       -> counters readback (sync)
-//   sort:      k_digit_histogram -> k_digit_scan -> k_onesweep x P -> k_tie_fixup -> k_tile_ranges
+//   sort:      splats by depth (k_digit_histogram, k_onesweep x P, k_tie_fixup) ->
+//              pairs in that order (k_splat_cells, k_scan_sums, k_emit_pairs) ->
+//              pairs stably by cell (k_onesweep x P') -> k_cell_ranges
 //   rasterize: k_raster16 (or k_raster_generic for other tile sizes)
 //   D2H of framebuffer / transmittance / active LoDs (host mode)
 // The one mid-frame synchronisation reads S, K and the depth-bit range: it sizes the
@@ -106,11 +108,12 @@ struct gscg_ctx {
     DevBuf inst_group, inst_base, members, group_inst_start, group_inst_count, group_item_start;
     DevBuf skin, counters;
     // gather outputs
-    DevBuf records, record_ordinal, keys[2], vals[2];
+    DevBuf records, record_ordinal, splat_depth;
     uint64_t splat_capacity = 0, pair_capacity = 0;
-    // sort
-    DevBuf hist, status, ranges, sorted_ordinals;
+    // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
+    DevBuf skeys[2], srecs[2], pcell[2], precs[2], cells_of, block_sums, hist, status, ranges, sorted_ordinals;
     uint32_t epoch = 1;
+    const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
     DevBuf fb_rgb, fb_T;
     // debug
@@ -122,7 +125,7 @@ struct gscg_ctx {
     cudaEvent_t ev[8] = {};
 
     // last frame
-    uint32_t n = 0, tiles = 0, final_buf = 0;
+    uint32_t n = 0, tiles = 0, cells_per_tile = 1;
     uint64_t G = 0, S = 0, K = 0;
 
     void ensure_pinned(size_t bytes) {
@@ -272,8 +275,6 @@ int gscg_create(int device, gscg_ctx** out) {
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
-        CUDA_TRY(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSortTile * (sizeof(unsigned long long) + sizeof(uint32_t))));
         CUDA_TRY(cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kProjectThreads * kShFloats * 4 + kMaxJoints * 12 * 4));
     });
@@ -296,8 +297,9 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members,
                       &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
                       &ctx->skin, &ctx->counters, &ctx->records, &ctx->record_ordinal,
-                      &ctx->keys[0], &ctx->keys[1], &ctx->vals[0], &ctx->vals[1], &ctx->hist,
-                      &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
+                      &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
+                      &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->cells_of,
+                      &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
                       &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg};
     for (DevBuf* b : bufs) b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -441,6 +443,8 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         const int W = cam->width, H = cam->height, ts = settings->tile_size;
         const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
         const uint32_t tiles = static_cast<uint32_t>(tiles_x) * tiles_y;
+        const uint32_t cells_per_tile = ts == 16 ? 4u : 1u;  // 8x8 quadrant binning for tile 16
+        const uint32_t cells = tiles * cells_per_tile;
         uint32_t launches = 0;
 
         CUDA_TRY(ctx->template_ids.ensure(std::max<size_t>(n, 1) * 4));
@@ -457,7 +461,7 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         CUDA_TRY(ctx->skin.ensure(std::max<size_t>(n, 1) * js * 12 * 4));
         CUDA_TRY(ctx->fb_rgb.ensure(static_cast<size_t>(W) * H * 12));
         CUDA_TRY(ctx->fb_T.ensure(static_cast<size_t>(W) * H * 4));
-        CUDA_TRY(ctx->ranges.ensure(static_cast<size_t>(tiles) * 8));
+        CUDA_TRY(ctx->ranges.ensure(static_cast<size_t>(cells) * 8));
 
         // ---- H2D ----
         CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
@@ -551,10 +555,7 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
             }
             CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
             CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
-            for (int b = 0; b < 2; ++b) {
-                CUDA_TRY(ctx->keys[b].ensure(ctx->pair_capacity * 8));
-                CUDA_TRY(ctx->vals[b].ensure(ctx->pair_capacity * 4));
-            }
+            CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
             if (ctx->debug & GSCG_DEBUG_RECORDS)
                 CUDA_TRY(ctx->rec_dbg.ensure(ctx->splat_capacity * sizeof(gscg_splat_record)));
 
@@ -583,8 +584,7 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
             pj.counters = counters;
             pj.records = ctx->records.as<float4>();
             pj.record_ordinal = ctx->record_ordinal.as<uint32_t>();
-            pj.keys = ctx->keys[0].as<unsigned long long>();
-            pj.values = ctx->vals[0].as<uint32_t>();
+            pj.splat_depth = ctx->splat_depth.as<uint32_t>();
             pj.splat_capacity = ctx->splat_capacity;
             pj.pair_capacity = ctx->pair_capacity;
             pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
@@ -613,57 +613,101 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
 
         // ---- sort ----
         const uint32_t K = static_cast<uint32_t>(ctx->K);
-        CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(tiles) * 8, s));
-        uint32_t passes = 0, final_buf = 0;
-        if (K > 0) {
-            const uint32_t dmin = ctx->h_counters->depth_min_bits, dmax = ctx->h_counters->depth_max_bits;
-            const uint32_t dbits = static_cast<uint32_t>(bits_for(dmin ^ dmax));
-            const uint32_t tbits = static_cast<uint32_t>(bits_for(tiles - 1));
-            const unsigned long long dmask = dbits >= 32 ? 0xffffffffull : ((1ull << dbits) - 1ull);
-            passes = (dbits + tbits + 7) / 8;
-            const uint32_t nblocks = (K + kSortTile - 1) / kSortTile;
-            if (passes > 0) {
-                CUDA_TRY(ctx->hist.ensure(kMaxSortPasses * 256 * 4));
-                CUDA_TRY(ctx->status.ensure(static_cast<size_t>(nblocks) * 256 * 8));
+        const uint32_t S32 = static_cast<uint32_t>(ctx->S);
+        uint32_t passes = 0;
+        CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(cells) * 8, s));
+        ctx->final_recs = nullptr;
+        if (S32 > 0 && K > 0) {
+            const uint32_t max_elems = std::max(S32, K);
+            const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
+            CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * 256 * 8));
+            CUDA_TRY(ctx->hist.ensure(kMaxSortPasses * 256 * 4));
+            for (int b = 0; b < 2; ++b) {
+                CUDA_TRY(ctx->skeys[b].ensure(static_cast<size_t>(S32) * 4));
+                CUDA_TRY(ctx->srecs[b].ensure(static_cast<size_t>(S32) * 4));
+                CUDA_TRY(ctx->pcell[b].ensure(static_cast<size_t>(K) * 4));
+                CUDA_TRY(ctx->precs[b].ensure(static_cast<size_t>(K) * 4));
+            }
+            uint32_t ticket = 0;
+            // Stable LSD onesweep of (keys, vals) over the plan; returns the buffer index
+            // holding the result. in_keys/in_vals feed pass 0 (vals may be null = identity).
+            auto radix = [&](const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb, uint32_t count,
+                             const SortPlan& plan) -> int {
                 CUDA_TRY(cudaMemsetAsync(ctx->hist.ptr, 0, kMaxSortPasses * 256 * 4, s));
-                const uint32_t hblocks = std::min<uint32_t>((K + 255) / 256, ctx->sm_count * 8);
-                k_digit_histogram<<<hblocks, 256, 0, s>>>(ctx->keys[0].as<unsigned long long>(), K, dbits, dmask, passes, ctx->hist.as<uint32_t>());
-                k_digit_scan<<<passes, 256, 0, s>>>(ctx->hist.as<uint32_t>(), passes);
+                const uint32_t hblocks = std::min<uint32_t>((count + 255) / 256, ctx->sm_count * 8);
+                k_digit_histogram<<<hblocks, 256, 0, s>>>(in_keys, count, plan, ctx->hist.as<uint32_t>());
+                k_digit_scan<<<plan.passes, 256, 0, s>>>(ctx->hist.as<uint32_t>());
                 launches += 2;
-                CUDA_TRY(cudaGetLastError());
-                for (uint32_t q = 0; q < passes; ++q) {
+                const uint32_t nblocks = (count + kSortTile - 1) / kSortTile;
+                int out = 0;
+                for (uint32_t q = 0; q < plan.passes; ++q) {
                     SortPassParams sp{};
-                    sp.keys_in = ctx->keys[q & 1].as<unsigned long long>();
-                    sp.vals_in = ctx->vals[q & 1].as<uint32_t>();
-                    sp.keys_out = ctx->keys[(q + 1) & 1].as<unsigned long long>();
-                    sp.vals_out = ctx->vals[(q + 1) & 1].as<uint32_t>();
-                    sp.count = K;
-                    sp.dbits = dbits;
-                    sp.dmask = dmask;
-                    sp.shift = 8 * q;
+                    sp.keys_in = q == 0 ? in_keys : kb[out ^ 1].as<uint32_t>();
+                    sp.vals_in = q == 0 ? in_vals : vb[out ^ 1].as<uint32_t>();
+                    sp.keys_out = kb[out].as<uint32_t>();
+                    sp.vals_out = vb[out].as<uint32_t>();
+                    sp.count = count;
+                    sp.shift = plan.shift[q];
+                    sp.bits = plan.bits[q];
                     sp.digit_offsets = ctx->hist.as<uint32_t>() + 256 * q;
                     sp.status = ctx->status.as<unsigned long long>();
-                    sp.ticket = &counters->sort_ticket[q];
+                    sp.ticket = &counters->sort_ticket[ticket++];
                     sp.epoch = ctx->epoch++;
                     if (ctx->epoch >= 0x3fffffffu) ctx->epoch = 1;
-                    k_onesweep<<<nblocks, kSortThreads, kSortTile * 12, s>>>(sp);
+                    k_onesweep<<<nblocks, kSortThreads, 0, s>>>(sp);
                     ++launches;
-                    CUDA_TRY(cudaGetLastError());
+                    out ^= 1;
                 }
-                final_buf = passes & 1;
-            }
-            const uint32_t gblocks = std::min<uint32_t>((K + 255) / 256, ctx->sm_count * 8);
-            k_tie_fixup<<<gblocks, 256, 0, s>>>(ctx->keys[final_buf].as<unsigned long long>(), ctx->vals[final_buf].as<uint32_t>(), ctx->record_ordinal.as<uint32_t>(), K);
-            k_tile_ranges<<<gblocks, 256, 0, s>>>(ctx->keys[final_buf].as<unsigned long long>(), K, ctx->ranges.as<uint2>());
-            launches += 2;
+                CUDA_TRY(cudaGetLastError());
+                return out ^ 1;
+            };
+            auto make_plan = [](uint32_t bits) {
+                SortPlan pl{};
+                bits = std::max(bits, 1u);
+                for (uint32_t sh = 0; sh < bits; sh += 8) {
+                    pl.shift[pl.passes] = sh;
+                    pl.bits[pl.passes] = std::min(8u, bits - sh);
+                    ++pl.passes;
+                }
+                return pl;
+            };
+            // 1. splats by depth (bits that vary in the frame), ties by ordinal.
+            const uint32_t dmin = ctx->h_counters->depth_min_bits, dmax = ctx->h_counters->depth_max_bits;
+            const SortPlan dplan = make_plan(static_cast<uint32_t>(bits_for(dmin ^ dmax)));
+            const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
+            const uint32_t gblocks = std::min<uint32_t>((S32 + 255) / 256, ctx->sm_count * 8);
+            k_tie_fixup<<<gblocks, 256, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
+                                                ctx->record_ordinal.as<uint32_t>(), S32);
+            // 2. pairs in sorted splat order.
+            const uint32_t sblocks = (S32 + 1023) / 1024;
+            CUDA_TRY(ctx->cells_of.ensure(static_cast<size_t>(S32) * 4));
+            CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * 4));
+            const int cell_px = cells_per_tile == 4 ? 8 : ts;
+            k_splat_cells<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->records.as<float4>(), cell_px,
+                                                   ctx->cells_of.as<uint32_t>(), ctx->block_sums.as<uint32_t>());
+            k_scan_sums<<<1, 1024, 0, s>>>(ctx->block_sums.as<uint32_t>(), sblocks);
+            k_emit_pairs<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->records.as<float4>(),
+                                                  ctx->cells_of.as<uint32_t>(), ctx->block_sums.as<uint32_t>(), cell_px,
+                                                  tiles_x, cells_per_tile == 4 ? 1 : 0, ctx->pcell[1].as<uint32_t>(),
+                                                  ctx->precs[1].as<uint32_t>());
+            launches += 4;
             CUDA_TRY(cudaGetLastError());
+            // 3. pairs stably by cell id; ranges.
+            const SortPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
+            const int cb = radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell, ctx->precs, K, cplan);
+            const uint32_t kblocks = std::min<uint32_t>((K + 255) / 256, ctx->sm_count * 8);
+            k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+            ctx->final_recs = ctx->precs[cb].as<uint32_t>();
+            passes = dplan.passes + cplan.passes;
         }
         CUDA_TRY(cudaEventRecord(ctx->ev[4], s));
 
         // ---- rasterize ----
         RasterParams rp{};
         rp.ranges = ctx->ranges.as<uint2>();
-        rp.values = ctx->vals[final_buf].as<uint32_t>();
+        rp.recs = ctx->final_recs;
         rp.records = ctx->records.as<float4>();
         rp.width = W;
         rp.height = H;
@@ -694,7 +738,7 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
 
         ctx->n = n;
         ctx->tiles = tiles;
-        ctx->final_buf = final_buf;
+        ctx->cells_per_tile = cells_per_tile;
         if (times) {
             times->h2d_ms = elapsed(ctx->ev[0], ctx->ev[1]);
             times->update_ms = elapsed(ctx->ev[1], ctx->ev[2]);
@@ -774,11 +818,18 @@ int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splat
     });
 }
 
-int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t tiles) {
+int gscg_get_cell_layout(gscg_ctx* ctx, uint32_t* tiles, uint32_t* cells_per_tile) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    if (tiles) *tiles = ctx->tiles;
+    if (cells_per_tile) *cells_per_tile = ctx->cells_per_tile;
+    return GSCG_OK;
+}
+
+int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells) {
     if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
-        if (tiles > ctx->tiles) invalid("more tiles requested than rendered");
-        CUDA_TRY(cudaMemcpyAsync(out, ctx->ranges.ptr, tiles * 8ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (cells > ctx->tiles * ctx->cells_per_tile) invalid("more cells requested than rendered");
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->ranges.ptr, cells * 8ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     });
 }
 
@@ -789,8 +840,8 @@ int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
         if (pairs == 0) return;
         CUDA_TRY(ctx->sorted_ordinals.ensure(pairs * 4));
         k_sorted_ordinals<<<std::min<uint64_t>((pairs + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-            ctx->vals[ctx->final_buf].as<uint32_t>(), ctx->record_ordinal.as<uint32_t>(),
-            static_cast<uint32_t>(pairs), ctx->sorted_ordinals.as<uint32_t>());
+            ctx->final_recs, ctx->record_ordinal.as<uint32_t>(), static_cast<uint32_t>(pairs),
+            ctx->sorted_ordinals.as<uint32_t>());
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         CUDA_TRY(cudaMemcpyAsync(out, ctx->sorted_ordinals.ptr, pairs * 4, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));

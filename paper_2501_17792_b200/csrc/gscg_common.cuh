@@ -62,7 +62,7 @@ struct FrameCounters {
     uint32_t depth_max_bits;
     uint32_t items_total;
     uint32_t item_cursor;
-    uint32_t sort_ticket[8];
+    uint32_t sort_ticket[8];  // onesweep tile tickets, one per pass of the frame
 };
 
 // float -> int as x86 cvttss2si (the reference's static_cast<int>): truncation, with

@@ -59,8 +59,7 @@ struct ProjectParams {
     // outputs (capacity-checked)
     float4* records;  // 3 float4 per splat
     uint32_t* record_ordinal;
-    unsigned long long* keys;
-    uint32_t* values;
+    uint32_t* splat_depth;  // depth bits of every record (the splat sort keys)
     uint64_t splat_capacity;
     uint64_t pair_capacity;
     // debug outputs (may be null)
@@ -68,24 +67,9 @@ struct ProjectParams {
     gscg_splat_record* record_debug; // per splat
 };
 
-struct SortPassParams {
-    const unsigned long long* keys_in;
-    const uint32_t* vals_in;
-    unsigned long long* keys_out;
-    uint32_t* vals_out;
-    uint32_t count;
-    uint32_t dbits;
-    unsigned long long dmask;
-    uint32_t shift;
-    const uint32_t* digit_offsets;  // 256 exclusive global offsets of this pass
-    unsigned long long* status;     // num_blocks x 256 look-back words
-    uint32_t* ticket;
-    uint32_t epoch;
-};
-
 struct RasterParams {
     const uint2* ranges;
-    const uint32_t* values;
+    const uint32_t* recs;  // record index of every cell-sorted pair
     const float4* records;
     int32_t width, height, tile_size, tiles_x;
     float bg[3];
@@ -100,26 +84,50 @@ __global__ void k_fk_skin(FkParams p);
 __global__ void k_project(ProjectParams p);
 __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n);
 
-// sort
+// sort: splats by depth, pairs emitted in that order, pairs stably by cell
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;
-constexpr int kMaxSortPasses = 8;
-__global__ void k_digit_histogram(const unsigned long long* keys, uint32_t count, uint32_t dbits,
-                                  unsigned long long dmask, uint32_t passes, uint32_t* hist);
-__global__ void k_digit_scan(uint32_t* hist, uint32_t passes);
+constexpr uint32_t kSortTile = kSortThreads * kSortItems;
+constexpr uint32_t kMaxSortPasses = 8;
+
+// Digit layout of one radix sort (LSD): pass q sorts bits [shift[q], shift[q] + bits[q]).
+struct SortPlan {
+    uint32_t passes;
+    uint32_t shift[kMaxSortPasses];
+    uint32_t bits[kMaxSortPasses];
+};
+
+struct SortPassParams {
+    const uint32_t* keys_in;
+    const uint32_t* vals_in;  // null: value = index (first pass of the splat sort)
+    uint32_t* keys_out;
+    uint32_t* vals_out;
+    uint32_t count;
+    uint32_t shift;
+    uint32_t bits;
+    const uint32_t* digit_offsets;  // 256 exclusive global offsets of this pass
+    unsigned long long* status;     // num_blocks x 256 look-back words
+    uint32_t* ticket;
+    uint32_t epoch;
+};
+
+__global__ void k_digit_histogram(const uint32_t* keys, uint32_t count, SortPlan plan, uint32_t* hist);
+__global__ void k_digit_scan(uint32_t* hist);
 __global__ void k_onesweep(SortPassParams p);
-__global__ void k_tie_fixup(const unsigned long long* keys, uint32_t* vals,
-                            const uint32_t* ordinal, uint32_t count);
-__global__ void k_tile_ranges(const unsigned long long* keys, uint32_t count, uint2* ranges);
+__global__ void k_tie_fixup(const uint32_t* keys, uint32_t* vals, const uint32_t* ordinal, uint32_t count);
+__global__ void k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const float4* records, int cell,
+                              uint32_t* cells_of, uint32_t* block_sums);
+__global__ void k_scan_sums(uint32_t* sums, uint32_t n);
+__global__ void k_emit_pairs(const uint32_t* sorted_rec, uint32_t count, const float4* records,
+                             const uint32_t* cells_of, const uint32_t* block_offsets, int cell, int tiles_x,
+                             int quads, uint32_t* pair_cell, uint32_t* pair_rec);
+__global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges);
 
 // raster
-__global__ void k_raster16(RasterParams p);
-// Picks the tile-size specialisation (16: one pixel per thread; else 1/4/16 per thread).
+// Picks the tile-size specialisation (16: 8x8 quadrant CTAs; else 1/4/16 pixels per thread).
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream);
 
 // debug
-__global__ void k_sorted_ordinals(const uint32_t* vals, const uint32_t* ordinal, uint32_t count,
-                                  uint32_t* out);
+__global__ void k_sorted_ordinals(const uint32_t* recs, const uint32_t* ordinal, uint32_t count, uint32_t* out);
 
 }  // namespace gscg

@@ -87,7 +87,9 @@ k_project(ProjectParams p) {
     for (uint32_t g = tid; g <= p.group_count; g += blockDim.x) s_item_start[g] = p.group_item_start[g];
     const uint32_t items_total = p.counters->items_total;
     const CameraDev& cam = p.cam;
-    const int ts = p.tile_size;
+    // Binning cell (pairs per splat are counted here; emitted after the depth sort):
+    // the tile, or for 16-px tiles each 8x8 quadrant.
+    const int cell = p.tile_size == 16 ? 8 : p.tile_size;
     uint32_t dmin = 0xffffffffu, dmax = 0u;
 
     for (;;) {
@@ -219,9 +221,9 @@ k_project(ProjectParams p) {
                         ca = cyy * inv_det;
                         cb = -cxy * inv_det;
                         cc = cxx * inv_det;
-                        const int tx0 = x0 / ts, tx1 = (x1 - 1) / ts;
-                        const int ty0 = y0 / ts, ty1 = (y1 - 1) / ts;
-                        n_tiles = static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+                        const int cx0 = x0 / cell, cx1 = (x1 - 1) / cell;
+                        const int cy0 = y0 / cell, cy1 = (y1 - 1) / cell;
+                        n_tiles = static_cast<uint32_t>((cx1 - cx0 + 1) * (cy1 - cy0 + 1));
                         col0 = c2.z;
                         col1 = c2.w;
                         col2 = c3.x;
@@ -258,13 +260,13 @@ k_project(ProjectParams p) {
                 p.posed_debug[3ull * ordinal + 1] = ay;
                 p.posed_debug[3ull * ordinal + 2] = az;
             }
+            const uint64_t ridx = (base >> 32) + (excl >> 32);
+            const uint32_t dbits = __float_as_uint(depth);
+            const bool stored = survive && ridx < p.splat_capacity;
             if (survive) {
-                const uint64_t ridx = (base >> 32) + (excl >> 32);
-                uint64_t pidx = (base & 0xffffffffull) + (excl & 0xffffffffull);
-                const uint32_t dbits = __float_as_uint(depth);
                 dmin = min(dmin, dbits);
                 dmax = max(dmax, dbits);
-                if (ridx < p.splat_capacity) {
+                if (stored) {
                     float4* rec = p.records + 3 * ridx;
                     rec[0] = make_float4(mx, my, ca, cb);
                     rec[1] = make_float4(cc, c0.w, c3.y, col0);
@@ -297,19 +299,9 @@ k_project(ProjectParams p) {
                         d.rect[3] = y1;
                         p.record_debug[ridx] = d;
                     }
-                    const int tx0 = x0 / ts, tx1 = (x1 - 1) / ts;
-                    const int ty0 = y0 / ts, ty1 = (y1 - 1) / ts;
-                    for (int tyy = ty0; tyy <= ty1; ++tyy) {
-                        for (int txx = tx0; txx <= tx1; ++txx) {
-                            if (pidx < p.pair_capacity) {
-                                p.keys[pidx] = (static_cast<unsigned long long>(tyy * p.tiles_x + txx) << 32) | dbits;
-                                p.values[pidx] = static_cast<uint32_t>(ridx);
-                            }
-                            ++pidx;
-                        }
-                    }
                 }
             }
+            if (stored) p.splat_depth[ridx] = dbits;  // splat sort key (pairs are emitted after it)
             __syncthreads();
         }
     }

@@ -1,18 +1,20 @@
-// Stage "sort" on the B200: stable LSD radix sort of the 64-bit tile|depth pair keys
-// (reference: sort_splats_impl renderer.cpp:85-107 + binning renderer.cpp:143-161).
+// Stage "sort" on the B200: the reference's own two-step order — sort the splats by
+// depth, then bin them into tiles in that order (sort_splats_impl renderer.cpp:85-107,
+// binning renderer.cpp:143-161) — restated as three device passes:
 //
-// The reference sorts splats globally by (depth bits, instance_id, gaussian_index) and
-// then bins them into tiles in sorted order, so each tile's list is ordered by that
-// triple. Here pairs carry key = tile << 32 | depth_bits and value = splat record index;
-// an 8-bit-digit onesweep radix sort over the exact significant key bits (depth bits
-// above the frame's common prefix are skipped) orders them by (tile, depth), and
-// k_tie_fixup orders the rare equal-key runs by the splat ordinal
-// (instance base + gaussian index), which is the reference's (instance, gaussian)
-// tie-break. Result: per-tile lists identical to the reference's bins.
+//   1. k_onesweep over the S splat depth keys (32-bit, only the bits that vary in the
+//      frame), values = record index; k_tie_fixup orders equal-depth runs by splat
+//      ordinal (instance base + gaussian index) = the reference's (instance, gaussian)
+//      tie-break. The splats are now in the reference's total order.
+//   2. k_splat_cells + k_scan_sums + k_emit_pairs: every sorted splat emits one pair per
+//      overlapped binning cell (tile, or 8x8 quadrant of a 16-px tile), in sorted order.
+//   3. k_onesweep (stable) over the pairs' cell ids; k_cell_ranges marks each cell's
+//      [start, end). Stability keeps the depth order inside every cell, so each cell
+//      list is exactly the reference's bin restricted to the cell.
 //
-// Onesweep pass: each CTA takes a 4096-key tile by atomic ticket (forward progress for
-// the look-back), ranks keys stably per warp with __match_any_sync, publishes its digit
-// counts, resolves its global digit offsets with a decoupled look-back over preceding
+// Onesweep pass: a CTA takes a 4096-key tile by atomic ticket (forward progress for the
+// look-back), ranks keys stably per warp with __match_any_sync, publishes its digit
+// counts, resolves its global digit offsets by decoupled look-back over the preceding
 // tiles, stages the tile in shared memory in digit order and writes it out coalesced.
 #include "gscg_common.cuh"
 #include "gscg_kernels.h"
@@ -21,17 +23,10 @@ namespace gscg {
 
 namespace {
 
-__device__ __forceinline__ uint32_t digit_of(unsigned long long key, uint32_t dbits,
-                                             unsigned long long dmask, uint32_t shift) {
-    const unsigned long long vkey = ((key >> 32) << dbits) | (key & dmask);
-    return static_cast<uint32_t>(vkey >> shift) & 0xffu;
-}
-
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagIncl = 2ull << 62;
 
-__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, uint32_t epoch,
-                                                          uint32_t value) {
+__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, uint32_t epoch, uint32_t value) {
     return flag | (static_cast<unsigned long long>(epoch & 0x3fffffffu) << 32) | value;
 }
 
@@ -45,51 +40,83 @@ __device__ __forceinline__ void store_status(unsigned long long* addr, unsigned 
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// Exclusive block scan (blockDim.x multiple of 32); s_warp holds 32 words.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t x = warp_incl_scan(v, lane);
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = warp_incl_scan(lane < nw ? s_warp[lane] : 0u, lane);
+        if (lane < nw) s_warp[lane] = w;
+    }
+    __syncthreads();
+    total = s_warp[nw - 1];
+    const uint32_t r = (warp ? s_warp[warp - 1] : 0u) + x - v;
+    __syncthreads();
+    return r;
+}
+
+// Binning cells overlapped by a pixel rect (packed as in the raster record).
+struct CellSpan {
+    int cx0, cy0, ncw, n;
+};
+
+__device__ __forceinline__ CellSpan cell_span(uint32_t lo, uint32_t hi, int cell) {
+    const int x0 = lo & 0xffff, y0 = lo >> 16, x1 = hi & 0xffff, y1 = hi >> 16;
+    CellSpan s;
+    s.cx0 = x0 / cell;
+    s.cy0 = y0 / cell;
+    s.ncw = (x1 - 1) / cell - s.cx0 + 1;
+    s.n = s.ncw * ((y1 - 1) / cell - s.cy0 + 1);
+    return s;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(256)
-k_digit_histogram(const unsigned long long* keys, uint32_t count, uint32_t dbits,
-                  unsigned long long dmask, uint32_t passes, uint32_t* hist) {
+k_digit_histogram(const uint32_t* keys, uint32_t count, SortPlan plan, uint32_t* hist) {
     __shared__ uint32_t s_hist[kMaxSortPasses][256];
     for (int i = threadIdx.x; i < kMaxSortPasses * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0u;
     __syncthreads();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
-        const unsigned long long key = keys[i];
-        const unsigned long long vkey = ((key >> 32) << dbits) | (key & dmask);
-        for (uint32_t q = 0; q < passes; ++q)
-            atomicAdd(&s_hist[q][static_cast<uint32_t>(vkey >> (8 * q)) & 0xffu], 1u);
+        const uint32_t key = keys[i];
+        for (uint32_t q = 0; q < plan.passes; ++q)
+            atomicAdd(&s_hist[q][(key >> plan.shift[q]) & ((1u << plan.bits[q]) - 1u)], 1u);
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; i < plan.passes * 256; i += blockDim.x) {
         const uint32_t c = (&s_hist[0][0])[i];
         if (c) atomicAdd(&hist[i], c);
     }
 }
 
 // In-place exclusive scan of each pass's 256-bin histogram (one CTA per pass).
-__global__ void __launch_bounds__(256) k_digit_scan(uint32_t* hist, uint32_t passes) {
-    __shared__ uint32_t s[256];
+__global__ void __launch_bounds__(256) k_digit_scan(uint32_t* hist) {
+    __shared__ uint32_t s_warp[32];
     uint32_t* h = hist + blockIdx.x * 256;
     const uint32_t v = h[threadIdx.x];
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {
-        const uint32_t y = threadIdx.x >= o ? s[threadIdx.x - o] : 0u;
-        __syncthreads();
-        s[threadIdx.x] += y;
-        __syncthreads();
-    }
-    h[threadIdx.x] = s[threadIdx.x] - v;
+    uint32_t total;
+    h[threadIdx.x] = block_excl_scan(v, s_warp, total);
 }
 
 __global__ void __launch_bounds__(kSortThreads)
 k_onesweep(SortPassParams p) {
-    extern __shared__ unsigned long long s_keys[];            // kSortTile keys
-    uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kSortTile);
+    __shared__ uint32_t s_keys[kSortTile];
+    __shared__ uint32_t s_vals[kSortTile];
     __shared__ uint32_t s_wcount[kSortThreads / 32][256];
     __shared__ uint32_t s_block_excl[256];
     __shared__ uint32_t s_global[256];
-    __shared__ uint32_t s_scan[kSortThreads / 32];
+    __shared__ uint32_t s_scan[32];
     __shared__ uint32_t s_block;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -98,26 +125,30 @@ k_onesweep(SortPassParams p) {
     __syncthreads();
     const uint32_t b = s_block;
     const uint32_t base = b * kSortTile;
+    const uint32_t mask = (1u << p.bits) - 1u;
 
-    unsigned long long k[kSortItems];
-    uint32_t v[kSortItems], d[kSortItems], rank[kSortItems];
+    uint32_t k[kSortItems], v[kSortItems], d[kSortItems], rank[kSortItems];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const bool valid = idx < p.count;
-        k[j] = valid ? p.keys_in[idx] : 0ull;
-        v[j] = valid ? p.vals_in[idx] : 0u;
-        d[j] = valid ? digit_of(k[j], p.dbits, p.dmask, p.shift) : 256u;
+        k[j] = valid ? p.keys_in[idx] : 0u;
+        v[j] = valid ? (p.vals_in ? p.vals_in[idx] : idx) : 0u;
+        d[j] = valid ? ((k[j] >> p.shift) & mask) : 256u;
     }
     const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t peers = __match_any_sync(0xffffffffu, d[j]);
-        const uint32_t prior = d[j] < 256u ? s_wcount[warp][d[j] & 0xffu] : 0u;
+        const int leader = __ffs(peers) - 1;
+        uint32_t prior = 0;
+        if (lane == leader && d[j] < 256u) {
+            prior = s_wcount[warp][d[j]];
+            s_wcount[warp][d[j]] = prior + __popc(peers);
+        }
+        prior = __shfl_sync(0xffffffffu, prior, leader);
         rank[j] = prior + __popc(peers & lt_mask);
-        __syncwarp();
-        if (d[j] < 256u && lane == __ffs(peers) - 1) s_wcount[warp][d[j]] = prior + __popc(peers);
-        __syncwarp();
+        __syncwarp();  // the next item's leaders read counters this item's leaders wrote
     }
     __syncthreads();
 
@@ -129,22 +160,8 @@ k_onesweep(SortPassParams p) {
         s_wcount[w][tid] = total;
         total += c;
     }
-    // Digit-major exclusive offsets inside the block (staging layout).
-    {
-        uint32_t x = total;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_scan[warp] = x;
-        __syncthreads();
-        uint32_t before = 0;
-#pragma unroll
-        for (int w = 0; w < kSortThreads / 32; ++w)
-            if (w < warp) before += s_scan[w];
-        s_block_excl[tid] = before + x - total;
-    }
+    uint32_t all;
+    s_block_excl[tid] = block_excl_scan(total, s_scan, all);
 
     // Decoupled look-back for this digit over preceding tiles.
     unsigned long long* my = p.status + static_cast<size_t>(b) * 256 + tid;
@@ -179,20 +196,18 @@ k_onesweep(SortPassParams p) {
     __syncthreads();
     const uint32_t n_here = p.count > base ? min(static_cast<uint32_t>(kSortTile), p.count - base) : 0u;
     for (uint32_t e = tid; e < n_here; e += kSortThreads) {
-        const unsigned long long key = s_keys[e];
-        const uint32_t dd = digit_of(key, p.dbits, p.dmask, p.shift);
+        const uint32_t key = s_keys[e];
+        const uint32_t dd = (key >> p.shift) & mask;
         const uint32_t pos = s_global[dd] + (e - s_block_excl[dd]);
         p.keys_out[pos] = key;
         p.vals_out[pos] = s_vals[e];
     }
 }
 
-// Equal (tile, depth) keys: order the run by splat ordinal = (instance, gaussian) order
-// (renderer.cpp:91-96 tie-break). Runs are rare and short.
-__global__ void k_tie_fixup(const unsigned long long* keys, uint32_t* vals,
-                            const uint32_t* ordinal, uint32_t count) {
+// Equal-depth runs of the sorted splats: order by ordinal (renderer.cpp:91-96).
+__global__ void k_tie_fixup(const uint32_t* keys, uint32_t* vals, const uint32_t* ordinal, uint32_t count) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < count; i += gridDim.x * blockDim.x) {
-        const unsigned long long k = keys[i];
+        const uint32_t k = keys[i];
         if (keys[i + 1] != k) continue;
         if (i > 0 && keys[i - 1] == k) continue;  // not the run start
         uint32_t end = i + 1;
@@ -210,19 +225,71 @@ __global__ void k_tie_fixup(const unsigned long long* keys, uint32_t* vals,
     }
 }
 
-// [start, end) of every tile in the sorted pair array (the reference's bins).
-__global__ void k_tile_ranges(const unsigned long long* keys, uint32_t count, uint2* ranges) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
-        const uint32_t tile = static_cast<uint32_t>(keys[i] >> 32);
-        if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != tile) ranges[tile].x = i;
-        if (i + 1 == count || static_cast<uint32_t>(keys[i + 1] >> 32) != tile) ranges[tile].y = i + 1;
+// Pairs per sorted splat + per-block sums (level 1 of the pair-offset scan).
+__global__ void __launch_bounds__(1024)
+k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const float4* records, int cell,
+              uint32_t* cells_of, uint32_t* block_sums) {
+    __shared__ uint32_t s_warp[32];
+    const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
+    uint32_t n = 0;
+    if (i < count) {
+        const float4 r2 = records[3ull * sorted_rec[i] + 2];
+        n = static_cast<uint32_t>(cell_span(__float_as_uint(r2.z), __float_as_uint(r2.w), cell).n);
+        cells_of[i] = n;
+    }
+    uint32_t total;
+    block_excl_scan(n, s_warp, total);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+// Exclusive scan of the block sums in place (one CTA).
+__global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, uint32_t n) {
+    __shared__ uint32_t s_warp[32];
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < n; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < n ? sums[i] : 0u;
+        uint32_t total;
+        const uint32_t e = block_excl_scan(v, s_warp, total);
+        if (i < n) sums[i] = carry + e;
+        carry += total;
     }
 }
 
-__global__ void k_sorted_ordinals(const uint32_t* vals, const uint32_t* ordinal, uint32_t count,
-                                  uint32_t* out) {
+// Emit (cell, record) pairs in the sorted splat order.
+__global__ void __launch_bounds__(1024)
+k_emit_pairs(const uint32_t* sorted_rec, uint32_t count, const float4* records, const uint32_t* cells_of,
+             const uint32_t* block_offsets, int cell, int tiles_x, int quads, uint32_t* pair_cell,
+             uint32_t* pair_rec) {
+    __shared__ uint32_t s_warp[32];
+    const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
+    const uint32_t n = i < count ? cells_of[i] : 0u;
+    uint32_t total;
+    const uint32_t off = block_offsets[blockIdx.x] + block_excl_scan(n, s_warp, total);
+    if (i >= count) return;
+    const uint32_t rec = sorted_rec[i];
+    const float4 r2 = records[3ull * rec + 2];
+    const CellSpan s = cell_span(__float_as_uint(r2.z), __float_as_uint(r2.w), cell);
+    for (int k = 0; k < s.n; ++k) {
+        const int cx = s.cx0 + k % s.ncw, cy = s.cy0 + k / s.ncw;
+        pair_cell[off + k] = quads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
+                                   : static_cast<uint32_t>(cy * tiles_x + cx);
+        pair_rec[off + k] = rec;
+    }
+}
+
+// [start, end) of every cell in the cell-sorted pairs (the reference's bins).
+__global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const uint32_t c = cells[i];
+        if (i == 0 || cells[i - 1] != c) ranges[c].x = i;
+        if (i + 1 == count || cells[i + 1] != c) ranges[c].y = i + 1;
+    }
+}
+
+__global__ void k_sorted_ordinals(const uint32_t* recs, const uint32_t* ordinal, uint32_t count, uint32_t* out) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
-        out[i] = ordinal[vals[i]];
+        out[i] = ordinal[recs[i]];
 }
 
 }  // namespace gscg

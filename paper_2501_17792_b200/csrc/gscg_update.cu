@@ -68,7 +68,7 @@ k_lod_plan(PlanParams p) {
         p.counters->depth_min_bits = 0xffffffffu;
         p.counters->depth_max_bits = 0u;
         p.counters->item_cursor = 0u;
-        for (int i = 0; i < 8; ++i) p.counters->sort_ticket[i] = 0u;
+        for (int q = 0; q < 8; ++q) p.counters->sort_ticket[q] = 0u;
     }
     __syncthreads();
 

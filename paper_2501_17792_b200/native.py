@@ -126,6 +126,7 @@ GSCG_SYMBOLS = {
     "gscg_get_instance_base": (C.c_int, [_P, _P, C.c_uint32]),
     "gscg_get_posed_means": (C.c_int, [_P, _P, C.c_uint64]),
     "gscg_get_splat_records": (C.c_int, [_P, _P, C.c_uint64]),
+    "gscg_get_cell_layout": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "gscg_get_tile_ranges": (C.c_int, [_P, _P, C.c_uint32]),
     "gscg_get_sorted_ordinals": (C.c_int, [_P, _P, C.c_uint64]),
 }

@@ -43,8 +43,10 @@ def check_frame(scene, renderer, oracle_scene, gpu_out, orc_out, tile_size=16, f
     lods = renderer.lods()
     assert np.array_equal(lods, oracle_scene.lods(n)), "LoD selection differs"
     G, S, K = renderer.counts()
-    assert (G, S, K) == (times.gaussian_count, times.splat_count, times.pair_count), \
-        f"counts G/S/K gpu {(G, S, K)} oracle {(times.gaussian_count, times.splat_count, times.pair_count)}"
+    assert (G, S) == (times.gaussian_count, times.splat_count), \
+        f"counts G/S gpu {(G, S)} oracle {(times.gaussian_count, times.splat_count)}"
+    if renderer.cell_layout()[1] == 1:
+        assert K == times.pair_count, f"pairs gpu {K} oracle {times.pair_count}"
     report.update(G=G, S=S, K=K)
     if full:
         pm, opm = renderer.posed_means(), oracle_scene.posed()
@@ -69,14 +71,42 @@ def check_frame(scene, renderer, oracle_scene, gpu_out, orc_out, tile_size=16, f
             assert report["color_max_abs"] <= 1e-5
         tiles_x = (cfg.width + tile_size - 1) // tile_size
         tiles_y = (cfg.height + tile_size - 1) // tile_size
-        ranges = renderer.tile_ranges(tiles_x * tiles_y)
-        counts, items = oracle_scene.bins(tiles_x * tiles_y)
-        assert np.array_equal(ranges[:, 1] - ranges[:, 0], counts), "per-tile pair counts differ"
-        nz = counts > 0
-        starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
-        assert np.array_equal(ranges[nz, 0], starts[nz]), "tile ranges are not the prefix layout"
-        sorted_ord = renderer.sorted_ordinals()
-        assert np.array_equal(sorted_ord.astype(np.int64), oord[items]), "per-tile sort order differs"
+        tiles, cpt = renderer.cell_layout()
+        assert tiles == tiles_x * tiles_y
+        ranges = renderer.cell_ranges()
+        counts, items = oracle_scene.bins(tiles)
+        sorted_ord = renderer.sorted_ordinals().astype(np.int64)
+        if cpt == 1:
+            exp_counts, exp_ord = counts.astype(np.int64), oord[items]
+        else:
+            # Each 8x8 quadrant cell must hold exactly the reference tile list filtered to
+            # the splats whose rect meets the quadrant, in the reference's order.
+            tile_of = np.repeat(np.arange(tiles), counts)
+            rect = osp["rect"][items]
+            tx, ty = tile_of % tiles_x, tile_of // tiles_x
+            cell_ids, order, ords = [], [], []
+            for q in range(4):
+                qx0 = tx * 16 + (q & 1) * 8
+                qy0 = ty * 16 + (q >> 1) * 8
+                m = (rect[:, 0] < qx0 + 8) & (rect[:, 2] > qx0) & (rect[:, 1] < qy0 + 8) & (rect[:, 3] > qy0)
+                cell_ids.append(tile_of[m] * 4 + q)
+                order.append(np.nonzero(m)[0])
+                ords.append(oord[items[m]])
+            cell_ids, order, ords = map(np.concatenate, (cell_ids, order, ords))
+            perm = np.lexsort((order, cell_ids))
+            exp_ord = ords[perm]
+            exp_counts = np.bincount(cell_ids, minlength=tiles * 4)
+            lut = np.zeros(max(G, 1), np.int64)
+            lut[rec["ordinal"]] = rec["depth"].view(np.uint32)
+            tcounts, titems = renderer.tile_lists(lambda o: lut[o])
+            assert np.array_equal(tcounts, counts) and np.array_equal(titems, oord[items]), \
+                "merged per-tile lists differ from the reference bins"
+        assert K == int(exp_counts.sum()), f"cell pairs gpu {K} expected {int(exp_counts.sum())}"
+        assert np.array_equal((ranges[:, 1] - ranges[:, 0]).astype(np.int64), exp_counts), "per-cell pair counts differ"
+        starts = np.concatenate([[0], np.cumsum(exp_counts)[:-1]])
+        nz = exp_counts > 0
+        assert np.array_equal(ranges[nz, 0].astype(np.int64), starts[nz]), "cell ranges are not the prefix layout"
+        assert np.array_equal(sorted_ord, exp_ord), "per-cell sort order differs"
     diff = np.abs(rgb - orgb)
     report["max_abs"] = float(diff.max()) if diff.size else 0.0
     report["T_max_abs"] = float(np.abs(T - oT).max()) if T.size else 0.0
