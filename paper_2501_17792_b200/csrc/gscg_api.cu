@@ -111,7 +111,7 @@ struct gscg_ctx {
     DevBuf records, record_ordinal, splat_depth;
     uint64_t splat_capacity = 0, pair_capacity = 0;
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
-    DevBuf skeys[2], srecs[2], pcell[2], precs[2], cells_of, block_sums, hist, status, ranges, sorted_ordinals;
+    DevBuf skeys[2], srecs[2], pcell[2], precs[2], splat_span, span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     uint32_t epoch = 1;
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
@@ -298,7 +298,7 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
                       &ctx->skin, &ctx->counters, &ctx->records, &ctx->record_ordinal,
                       &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
-                      &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->cells_of,
+                      &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->splat_span, &ctx->span_sorted,
                       &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
                       &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg};
     for (DevBuf* b : bufs) b->release();
@@ -556,6 +556,7 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
             CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
             CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
             CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
+            CUDA_TRY(ctx->splat_span.ensure(ctx->splat_capacity * 8));
             if (ctx->debug & GSCG_DEBUG_RECORDS)
                 CUDA_TRY(ctx->rec_dbg.ensure(ctx->splat_capacity * sizeof(gscg_splat_record)));
 
@@ -585,6 +586,7 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
             pj.records = ctx->records.as<float4>();
             pj.record_ordinal = ctx->record_ordinal.as<uint32_t>();
             pj.splat_depth = ctx->splat_depth.as<uint32_t>();
+            pj.splat_span = ctx->splat_span.as<uint2>();
             pj.splat_capacity = ctx->splat_capacity;
             pj.pair_capacity = ctx->pair_capacity;
             pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
@@ -675,27 +677,25 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
             const uint32_t dmin = ctx->h_counters->depth_min_bits, dmax = ctx->h_counters->depth_max_bits;
             const SortPlan dplan = make_plan(static_cast<uint32_t>(bits_for(dmin ^ dmax)));
             const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
-            const uint32_t gblocks = std::min<uint32_t>((S32 + 255) / 256, ctx->sm_count * 8);
+            const uint32_t gblocks = (S32 + 255) / 256;
             k_tie_fixup<<<gblocks, 256, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
                                                 ctx->record_ordinal.as<uint32_t>(), S32);
             // 2. pairs in sorted splat order.
             const uint32_t sblocks = (S32 + 1023) / 1024;
-            CUDA_TRY(ctx->cells_of.ensure(static_cast<size_t>(S32) * 4));
+            CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
             CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * 4));
-            const int cell_px = cells_per_tile == 4 ? 8 : ts;
-            k_splat_cells<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->records.as<float4>(), cell_px,
-                                                   ctx->cells_of.as<uint32_t>(), ctx->block_sums.as<uint32_t>());
+            k_splat_cells<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->splat_span.as<uint2>(),
+                                                   ctx->span_sorted.as<uint2>(), ctx->block_sums.as<uint32_t>());
             k_scan_sums<<<1, 1024, 0, s>>>(ctx->block_sums.as<uint32_t>(), sblocks);
-            k_emit_pairs<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->records.as<float4>(),
-                                                  ctx->cells_of.as<uint32_t>(), ctx->block_sums.as<uint32_t>(), cell_px,
-                                                  tiles_x, cells_per_tile == 4 ? 1 : 0, ctx->pcell[1].as<uint32_t>(),
-                                                  ctx->precs[1].as<uint32_t>());
+            k_emit_pairs<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
+                                                  ctx->block_sums.as<uint32_t>(), tiles_x, cells_per_tile == 4 ? 1 : 0,
+                                                  ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
             launches += 4;
             CUDA_TRY(cudaGetLastError());
             // 3. pairs stably by cell id; ranges.
             const SortPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
             const int cb = radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell, ctx->precs, K, cplan);
-            const uint32_t kblocks = std::min<uint32_t>((K + 255) / 256, ctx->sm_count * 8);
+            const uint32_t kblocks = (K + 255) / 256;
             k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
             ++launches;
             CUDA_TRY(cudaGetLastError());

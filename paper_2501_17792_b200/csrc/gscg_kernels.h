@@ -60,6 +60,7 @@ struct ProjectParams {
     float4* records;  // 3 float4 per splat
     uint32_t* record_ordinal;
     uint32_t* splat_depth;  // depth bits of every record (the splat sort keys)
+    uint2* splat_span;      // binning cells of every record: cx0 | cy0 << 16, across | down << 16
     uint64_t splat_capacity;
     uint64_t pair_capacity;
     // debug outputs (may be null)
@@ -115,12 +116,12 @@ __global__ void k_digit_histogram(const uint32_t* keys, uint32_t count, SortPlan
 __global__ void k_digit_scan(uint32_t* hist);
 __global__ void k_onesweep(SortPassParams p);
 __global__ void k_tie_fixup(const uint32_t* keys, uint32_t* vals, const uint32_t* ordinal, uint32_t count);
-__global__ void k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const float4* records, int cell,
-                              uint32_t* cells_of, uint32_t* block_sums);
+__global__ void k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const uint2* span, uint2* span_sorted,
+                              uint32_t* block_sums);
 __global__ void k_scan_sums(uint32_t* sums, uint32_t n);
-__global__ void k_emit_pairs(const uint32_t* sorted_rec, uint32_t count, const float4* records,
-                             const uint32_t* cells_of, const uint32_t* block_offsets, int cell, int tiles_x,
-                             int quads, uint32_t* pair_cell, uint32_t* pair_rec);
+__global__ void k_emit_pairs(const uint32_t* sorted_rec, uint32_t count, const uint2* span_sorted,
+                             const uint32_t* block_offsets, int tiles_x, int quads, uint32_t* pair_cell,
+                             uint32_t* pair_rec);
 __global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges);
 
 // raster

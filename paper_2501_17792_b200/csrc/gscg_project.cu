@@ -301,7 +301,14 @@ k_project(ProjectParams p) {
                     }
                 }
             }
-            if (stored) p.splat_depth[ridx] = dbits;  // splat sort key (pairs are emitted after it)
+            if (stored) {
+                p.splat_depth[ridx] = dbits;  // splat sort key (pairs are emitted after it)
+                // Binning cells of the rect: first cell, cells across, cells down.
+                const int cx0 = x0 / cell, cy0 = y0 / cell;
+                p.splat_span[ridx] = make_uint2(static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16),
+                                                static_cast<uint32_t>((x1 - 1) / cell - cx0 + 1) |
+                                                    (static_cast<uint32_t>((y1 - 1) / cell - cy0 + 1) << 16));
+            }
             __syncthreads();
         }
     }

@@ -191,21 +191,37 @@ k_raster16q(RasterParams p) {
         const int n = min(64u, range.y - start);
         if (__all_sync(0xffffffffu, done)) continue;
         for (int base = 0; base < n; base += 32) {
-            bool hit = false;
+            // Lane L: which of this warp's 32 pixels splat base+L's rect covers (bit = lane).
+            uint32_t cover = 0;
             if (base + lane < n) {
                 const uint2 r = s_rect[base + lane];
-                const int x0 = r.x & 0xffff, y0 = r.x >> 16, x1 = r.y & 0xffff, y1 = r.y >> 16;
-                hit = x0 < bx0 + 8 && x1 > bx0 && y0 < by0 + 4 && y1 > by0;
+                const int cx0 = max(static_cast<int>(r.x & 0xffff) - bx0, 0);
+                const int cx1 = min(static_cast<int>(r.y & 0xffff) - bx0, 8);
+                const int cy0 = max(static_cast<int>(r.x >> 16) - by0, 0);
+                const int cy1 = min(static_cast<int>(r.y >> 16) - by0, 4);
+                if (cx0 < cx1 && cy0 < cy1) {
+                    const uint32_t row = ((1u << cx1) - 1u) & ~((1u << cx0) - 1u);
+                    const uint32_t rows = static_cast<uint32_t>(((1ull << (8 * cy1)) - 1ull) & ~((1ull << (8 * cy0)) - 1ull));
+                    cover = (row * 0x01010101u) & rows;
+                }
             }
-            uint32_t mask = __ballot_sync(0xffffffffu, hit);
-            while (mask) {
-                const int k = base + __ffs(mask) - 1;
-                mask &= mask - 1;
-                if (done) continue;
-                const uint2 r = s_rect[k];
-                if (px < static_cast<int>(r.x & 0xffff) || px >= static_cast<int>(r.y & 0xffff) ||
-                    py < static_cast<int>(r.x >> 16) || py >= static_cast<int>(r.y >> 16))
-                    continue;
+            // Bit-matrix transpose across the warp: lane L now holds, in list order, the
+            // chunk's splats that cover pixel L.
+            uint32_t todo = cover;
+#pragma unroll
+            for (int s = 16; s >= 1; s >>= 1) {
+                const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu
+                                                         : s == 2 ? 0x33333333u : 0x55555555u;
+                const uint32_t y = __shfl_xor_sync(0xffffffffu, todo, s);
+                todo = (lane & s) ? ((todo & ~m) | ((y & ~m) >> s)) : ((todo & m) | ((y & m) << s));
+            }
+            if (done) todo = 0u;
+            // Every lane walks its own splats in order; lanes with disjoint splats work
+            // concurrently instead of idling through each other's splats.
+            while (__any_sync(0xffffffffu, todo != 0u)) {
+                if (todo == 0u) continue;
+                const int k = base + __ffs(todo) - 1;
+                todo &= todo - 1u;
                 const float4 g = s_geo[k];
                 const float dx = __fsub_rn(fx, g.x);
                 const float dy = __fsub_rn(fy, g.y);
@@ -220,7 +236,10 @@ k_raster16q(RasterParams p) {
                 cg = fmaf(w, c2.x, cg);
                 cb = fmaf(w, c2.y, cb);
                 T = T * (1.0f - alpha);
-                done = T < p.t_floor;
+                if (T < p.t_floor) {
+                    done = true;
+                    todo = 0u;
+                }
             }
             if (__all_sync(0xffffffffu, done)) break;
         }

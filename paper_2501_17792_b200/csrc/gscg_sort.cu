@@ -66,21 +66,6 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
     return r;
 }
 
-// Binning cells overlapped by a pixel rect (packed as in the raster record).
-struct CellSpan {
-    int cx0, cy0, ncw, n;
-};
-
-__device__ __forceinline__ CellSpan cell_span(uint32_t lo, uint32_t hi, int cell) {
-    const int x0 = lo & 0xffff, y0 = lo >> 16, x1 = hi & 0xffff, y1 = hi >> 16;
-    CellSpan s;
-    s.cx0 = x0 / cell;
-    s.cy0 = y0 / cell;
-    s.ncw = (x1 - 1) / cell - s.cx0 + 1;
-    s.n = s.ncw * ((y1 - 1) / cell - s.cy0 + 1);
-    return s;
-}
-
 }  // namespace
 
 __global__ void __launch_bounds__(256)
@@ -225,17 +210,17 @@ __global__ void k_tie_fixup(const uint32_t* keys, uint32_t* vals, const uint32_t
     }
 }
 
-// Pairs per sorted splat + per-block sums (level 1 of the pair-offset scan).
+// Cell spans gathered into sorted order + per-block pair sums (level 1 of the scan).
 __global__ void __launch_bounds__(1024)
-k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const float4* records, int cell,
-              uint32_t* cells_of, uint32_t* block_sums) {
+k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const uint2* span, uint2* span_sorted,
+              uint32_t* block_sums) {
     __shared__ uint32_t s_warp[32];
     const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
     uint32_t n = 0;
     if (i < count) {
-        const float4 r2 = records[3ull * sorted_rec[i] + 2];
-        n = static_cast<uint32_t>(cell_span(__float_as_uint(r2.z), __float_as_uint(r2.w), cell).n);
-        cells_of[i] = n;
+        const uint2 sp = span[sorted_rec[i]];
+        span_sorted[i] = sp;
+        n = (sp.y & 0xffffu) * (sp.y >> 16);
     }
     uint32_t total;
     block_excl_scan(n, s_warp, total);
@@ -258,20 +243,20 @@ __global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, uint32_t n) 
 
 // Emit (cell, record) pairs in the sorted splat order.
 __global__ void __launch_bounds__(1024)
-k_emit_pairs(const uint32_t* sorted_rec, uint32_t count, const float4* records, const uint32_t* cells_of,
-             const uint32_t* block_offsets, int cell, int tiles_x, int quads, uint32_t* pair_cell,
-             uint32_t* pair_rec) {
+k_emit_pairs(const uint32_t* sorted_rec, uint32_t count, const uint2* span_sorted, const uint32_t* block_offsets,
+             int tiles_x, int quads, uint32_t* pair_cell, uint32_t* pair_rec) {
     __shared__ uint32_t s_warp[32];
     const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
-    const uint32_t n = i < count ? cells_of[i] : 0u;
+    const uint2 sp = i < count ? span_sorted[i] : make_uint2(0u, 0u);
+    const int ncw = static_cast<int>(sp.y & 0xffffu);
+    const uint32_t n = static_cast<uint32_t>(ncw) * (sp.y >> 16);
     uint32_t total;
     const uint32_t off = block_offsets[blockIdx.x] + block_excl_scan(n, s_warp, total);
     if (i >= count) return;
     const uint32_t rec = sorted_rec[i];
-    const float4 r2 = records[3ull * rec + 2];
-    const CellSpan s = cell_span(__float_as_uint(r2.z), __float_as_uint(r2.w), cell);
-    for (int k = 0; k < s.n; ++k) {
-        const int cx = s.cx0 + k % s.ncw, cy = s.cy0 + k / s.ncw;
+    const int cx0 = static_cast<int>(sp.x & 0xffffu), cy0 = static_cast<int>(sp.x >> 16);
+    for (int k = 0; k < static_cast<int>(n); ++k) {
+        const int cx = cx0 + k % ncw, cy = cy0 + k / ncw;
         pair_cell[off + k] = quads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
                                    : static_cast<uint32_t>(cy * tiles_x + cx);
         pair_rec[off + k] = rec;
