@@ -112,7 +112,6 @@ struct gscg_ctx {
     uint64_t splat_capacity = 0, pair_capacity = 0;
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], splat_span, span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
-    uint32_t epoch = 1;
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
     DevBuf fb_rgb, fb_T;
@@ -236,6 +235,13 @@ void refresh_power_floor(gscg_ctx* ctx, float cutoff) {
     tmp.release();
 }
 
+// Digit layout of one LSD sort: pass q sorts bits [shift[q], shift[q] + bits[q]).
+struct RadixPlan {
+    uint32_t passes = 0;
+    uint32_t shift[kMaxSortPasses] = {};
+    uint32_t bits[kMaxSortPasses] = {};
+};
+
 int bits_for(uint32_t v) { return v == 0 ? 0 : 32 - __builtin_clz(v); }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -276,7 +282,7 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
         CUDA_TRY(cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kProjectThreads * kShFloats * 4 + kMaxJoints * 12 * 4));
+                                      kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
     });
     *out = ctx;
     return st;
@@ -493,7 +499,7 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         }
         CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
 
-        const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + static_cast<int>(js) * 12 * 4;
+        const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + kBatch * static_cast<int>(js) * 12 * 4;
         int project_blocks_per_sm = 1;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project, kProjectThreads, project_smem));
         project_blocks_per_sm = std::max(project_blocks_per_sm, 1);
@@ -622,25 +628,22 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         if (S32 > 0 && K > 0) {
             const uint32_t max_elems = std::max(S32, K);
             const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
-            CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * 256 * 8));
-            CUDA_TRY(ctx->hist.ensure(kMaxSortPasses * 256 * 4));
+            CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * 256 * 4));  // tile digit counts
+            CUDA_TRY(ctx->hist.ensure(256 * 4));                                        // digit bases
             for (int b = 0; b < 2; ++b) {
                 CUDA_TRY(ctx->skeys[b].ensure(static_cast<size_t>(S32) * 4));
                 CUDA_TRY(ctx->srecs[b].ensure(static_cast<size_t>(S32) * 4));
                 CUDA_TRY(ctx->pcell[b].ensure(static_cast<size_t>(K) * 4));
                 CUDA_TRY(ctx->precs[b].ensure(static_cast<size_t>(K) * 4));
             }
-            uint32_t ticket = 0;
             // Stable LSD onesweep of (keys, vals) over the plan; returns the buffer index
             // holding the result. in_keys/in_vals feed pass 0 (vals may be null = identity).
+            // Stable LSD radix sort of (keys, vals) over the plan (reduce-then-scan passes);
+            // returns the buffer index holding the result. in_keys/in_vals feed pass 0
+            // (vals may be null = identity).
             auto radix = [&](const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb, uint32_t count,
-                             const SortPlan& plan) -> int {
-                CUDA_TRY(cudaMemsetAsync(ctx->hist.ptr, 0, kMaxSortPasses * 256 * 4, s));
-                const uint32_t hblocks = std::min<uint32_t>((count + 255) / 256, ctx->sm_count * 8);
-                k_digit_histogram<<<hblocks, 256, 0, s>>>(in_keys, count, plan, ctx->hist.as<uint32_t>());
-                k_digit_scan<<<plan.passes, 256, 0, s>>>(ctx->hist.as<uint32_t>());
-                launches += 2;
-                const uint32_t nblocks = (count + kSortTile - 1) / kSortTile;
+                             const RadixPlan& plan) -> int {
+                const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
                 int out = 0;
                 for (uint32_t q = 0; q < plan.passes; ++q) {
                     SortPassParams sp{};
@@ -651,35 +654,36 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                     sp.count = count;
                     sp.shift = plan.shift[q];
                     sp.bits = plan.bits[q];
-                    sp.digit_offsets = ctx->hist.as<uint32_t>() + 256 * q;
-                    sp.status = ctx->status.as<unsigned long long>();
-                    sp.ticket = &counters->sort_ticket[ticket++];
-                    sp.epoch = ctx->epoch++;
-                    if (ctx->epoch >= 0x3fffffffu) ctx->epoch = 1;
-                    k_onesweep<<<nblocks, kSortThreads, 0, s>>>(sp);
-                    ++launches;
+                    sp.tiles = tiles;
+                    sp.counts = ctx->status.as<uint32_t>();
+                    sp.digit_base = ctx->hist.as<uint32_t>();
+                    k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+                    k_sort_rows<<<kRadix, 1024, 0, s>>>(sp);
+                    k_sort_bases<<<1, kRadix, 0, s>>>(sp);
+                    k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+                    launches += 4;
                     out ^= 1;
                 }
                 CUDA_TRY(cudaGetLastError());
                 return out ^ 1;
             };
             auto make_plan = [](uint32_t bits) {
-                SortPlan pl{};
+                RadixPlan pl{};
                 bits = std::max(bits, 1u);
-                for (uint32_t sh = 0; sh < bits; sh += 8) {
+                for (uint32_t sh = 0; sh < bits; sh += kRadixBits) {
                     pl.shift[pl.passes] = sh;
-                    pl.bits[pl.passes] = std::min(8u, bits - sh);
+                    pl.bits[pl.passes] = std::min<uint32_t>(kRadixBits, bits - sh);
                     ++pl.passes;
                 }
                 return pl;
             };
             // 1. splats by depth (bits that vary in the frame), ties by ordinal.
             const uint32_t dmin = ctx->h_counters->depth_min_bits, dmax = ctx->h_counters->depth_max_bits;
-            const SortPlan dplan = make_plan(static_cast<uint32_t>(bits_for(dmin ^ dmax)));
+            const RadixPlan dplan = make_plan(static_cast<uint32_t>(bits_for(dmin ^ dmax)));
             const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
-            const uint32_t gblocks = (S32 + 255) / 256;
-            k_tie_fixup<<<gblocks, 256, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
-                                                ctx->record_ordinal.as<uint32_t>(), S32);
+            const uint32_t sgrid = (S32 + 256 * kStreamItems - 1) / (256 * kStreamItems);
+            k_tie_fixup<<<sgrid, 256, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
+                                              ctx->record_ordinal.as<uint32_t>(), S32);
             // 2. pairs in sorted splat order.
             const uint32_t sblocks = (S32 + 1023) / 1024;
             CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
@@ -693,9 +697,9 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
             launches += 4;
             CUDA_TRY(cudaGetLastError());
             // 3. pairs stably by cell id; ranges.
-            const SortPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
+            const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
             const int cb = radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell, ctx->precs, K, cplan);
-            const uint32_t kblocks = (K + 255) / 256;
+            const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);
             k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
             ++launches;
             CUDA_TRY(cudaGetLastError());

@@ -87,17 +87,14 @@ __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n);
 
 // sort: splats by depth, pairs emitted in that order, pairs stably by cell
 constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 16;
+constexpr int kRadixBits = 5;  // digit width of one LSD pass
+constexpr int kRadix = 1 << kRadixBits;
 constexpr uint32_t kSortTile = kSortThreads * kSortItems;
 constexpr uint32_t kMaxSortPasses = 8;
 
-// Digit layout of one radix sort (LSD): pass q sorts bits [shift[q], shift[q] + bits[q]).
-struct SortPlan {
-    uint32_t passes;
-    uint32_t shift[kMaxSortPasses];
-    uint32_t bits[kMaxSortPasses];
-};
-
+// One stable LSD pass (reduce-then-scan): digit = (key >> shift) & (2^bits - 1).
 struct SortPassParams {
     const uint32_t* keys_in;
     const uint32_t* vals_in;  // null: value = index (first pass of the splat sort)
@@ -106,23 +103,24 @@ struct SortPassParams {
     uint32_t count;
     uint32_t shift;
     uint32_t bits;
-    const uint32_t* digit_offsets;  // 256 exclusive global offsets of this pass
-    unsigned long long* status;     // num_blocks x 256 look-back words
-    uint32_t* ticket;
-    uint32_t epoch;
+    uint32_t tiles;      // ceil(count / kSortTile)
+    uint32_t* counts;      // kRadix x tiles, digit-major: tile digit counts -> exclusive offsets
+    uint32_t* digit_base;  // kRadix: row totals -> exclusive digit bases
 };
 
-__global__ void k_digit_histogram(const uint32_t* keys, uint32_t count, SortPlan plan, uint32_t* hist);
-__global__ void k_digit_scan(uint32_t* hist);
-__global__ void k_onesweep(SortPassParams p);
-__global__ void k_tie_fixup(const uint32_t* keys, uint32_t* vals, const uint32_t* ordinal, uint32_t count);
+__global__ void k_sort_upsweep(SortPassParams p);
+__global__ void k_sort_rows(SortPassParams p);
+__global__ void k_sort_bases(SortPassParams p);
+__global__ void k_sort_downsweep(SortPassParams p);
+__global__ void k_tie_fixup(const uint32_t* keys, uint32_t* recs, const uint32_t* ordinal, uint32_t count);
 __global__ void k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const uint2* span, uint2* span_sorted,
                               uint32_t* block_sums);
 __global__ void k_scan_sums(uint32_t* sums, uint32_t n);
-__global__ void k_emit_pairs(const uint32_t* sorted_rec, uint32_t count, const uint2* span_sorted,
+__global__ void k_emit_pairs(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted,
                              const uint32_t* block_offsets, int tiles_x, int quads, uint32_t* pair_cell,
                              uint32_t* pair_rec);
 __global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges);
+constexpr int kStreamItems = 8;  // elements per thread in the streaming sort kernels
 
 // raster
 // Picks the tile-size specialisation (16: 8x8 quadrant CTAs; else 1/4/16 pixels per thread).

@@ -71,9 +71,16 @@ __device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long 
     return before + x - v;
 }
 
+__device__ __forceinline__ void copy_async16(float* smem_dst, const float* gmem_src) {
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem_src) : "memory");
+}
+
+__device__ __forceinline__ void copy_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 }  // namespace
 
-__global__ void __launch_bounds__(kProjectThreads, 2)
+__global__ void __launch_bounds__(kProjectThreads, 3)
 k_project(ProjectParams p) {
     extern __shared__ float4 s_dyn[];
     float* s_sh = reinterpret_cast<float*>(s_dyn);
@@ -122,30 +129,33 @@ k_project(ProjectParams p) {
             wv = grp.weights[gi];
         }
         const bool use_sh = p.sh_enabled && grp.sh != nullptr;
+        // Stage the chunk's SH coefficients and every batch instance's skin matrices
+        // with asynchronous copies (LDGSTS), once per work item.
         if (use_sh) {
             const uint32_t n_here = min(static_cast<uint32_t>(kProjectThreads),
                                         grp.count - chunk * kProjectThreads);
             const float* src = grp.sh + static_cast<size_t>(chunk) * kProjectThreads * kShFloats;
             const uint32_t n4 = (n_here * kShFloats + 3) / 4;  // SH chunks are 16-B aligned
-            const float4* src4 = reinterpret_cast<const float4*>(src);
-            for (uint32_t k = tid; k < n4; k += blockDim.x) reinterpret_cast<float4*>(s_sh)[k] = src4[k];
+            for (uint32_t k = tid; k < n4; k += blockDim.x) copy_async16(s_sh + 4 * k, src + 4 * k);
         }
         const uint32_t inst_begin = p.group_inst_start[g] + batch * kBatch;
         const uint32_t inst_count = min(static_cast<uint32_t>(kBatch),
                                         p.group_inst_count[g] - batch * kBatch);
+        const uint32_t mat_f4 = p.joint_stride * 3;  // float4s per instance
+        for (uint32_t e = tid; e < inst_count * mat_f4; e += blockDim.x) {
+            const uint32_t k = e / mat_f4, r = e - k * mat_f4;
+            const float* src = p.skin + static_cast<size_t>(p.members[inst_begin + k]) * p.joint_stride * 12;
+            copy_async16(s_mats + 4 * e, src + 4 * r);
+        }
+        copy_async_wait_all();
+        __syncthreads();
         const uint32_t i01 = __float_as_uint(c3.z), i23 = __float_as_uint(c3.w);
         const uint32_t jidx[4] = {i01 & 0xffffu, i01 >> 16, i23 & 0xffffu, i23 >> 16};
         const float wk[4] = {wv.x, wv.y, wv.z, wv.w};
 
         for (uint32_t k = 0; k < inst_count; ++k) {
             const uint32_t inst = p.members[inst_begin + k];
-            {
-                const float4* src = reinterpret_cast<const float4*>(
-                    p.skin + static_cast<size_t>(inst) * p.joint_stride * 12);
-                for (uint32_t e = tid; e < p.joint_stride * 3; e += blockDim.x)
-                    reinterpret_cast<float4*>(s_mats)[e] = src[e];
-            }
-            __syncthreads();
+            const float* s_inst = s_mats + k * p.joint_stride * 12;
 
             bool survive = false;
             uint32_t n_tiles = 0;
@@ -158,7 +168,7 @@ k_project(ProjectParams p) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (wk[q] == 0.0f) continue;
-                    const float* S = s_mats + jidx[q] * 12;
+                    const float* S = s_inst + jidx[q] * 12;
                     const float vx = ((S[0] * c0.x + S[1] * c0.y) + S[2] * c0.z) + S[3] * 1.0f;
                     const float vy = ((S[4] * c0.x + S[5] * c0.y) + S[6] * c0.z) + S[7] * 1.0f;
                     const float vz = ((S[8] * c0.x + S[9] * c0.y) + S[10] * c0.z) + S[11] * 1.0f;
@@ -305,11 +315,10 @@ k_project(ProjectParams p) {
                 p.splat_depth[ridx] = dbits;  // splat sort key (pairs are emitted after it)
                 // Binning cells of the rect: first cell, cells across, cells down.
                 const int cx0 = x0 / cell, cy0 = y0 / cell;
-                p.splat_span[ridx] = make_uint2(static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16),
-                                                static_cast<uint32_t>((x1 - 1) / cell - cx0 + 1) |
-                                                    (static_cast<uint32_t>((y1 - 1) / cell - cy0 + 1) << 16));
+                p.splat_span[ridx] = make_uint2(
+                    static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16),
+                    static_cast<uint32_t>((x1 - 1) / cell - cx0 + 1) | (static_cast<uint32_t>((y1 - 1) / cell - cy0 + 1) << 16));
             }
-            __syncthreads();
         }
     }
 
