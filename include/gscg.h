@@ -46,6 +46,8 @@ extern "C" {
 #define GSCG_MAX_JOINTS 64
 #define GSCG_MAX_LOD_THRESHOLDS 8
 #define GSCG_SH_FLOATS 45 /* SH degree 1..3 residual: 15 coefficients x RGB */
+#define GSCG_MAX_BANDS 64
+#define GSCG_BAND_SPLAT_BYTES 64 /* one routed splat: 48 B record + ordinal + depth bits + pad */
 
 typedef struct gscg_ctx gscg_ctx;
 
@@ -188,6 +190,32 @@ int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splat
 int gscg_get_cell_layout(gscg_ctx* ctx, uint32_t* tiles, uint32_t* cells_per_tile);
 int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells); /* cells x 2: [start, end) */
 int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs);
+
+/* ---- Multi-GPU frame: instance shards -> screen bands ----
+ * The reference renders one frame in one process (renderer.cpp:249-280); these three
+ * calls split it at its only coupling, the splat -> tile routing (renderer.cpp:143-161),
+ * so P ranks can each project an instance shard and rasterise a screen band:
+ *   1. gscg_project_shard: update + gather for instances [shard_begin, shard_end) (LoD and
+ *      global ordinals are computed over the whole crowd, so every rank numbers splats
+ *      identically), then counts the surviving splats per screen band. band_rows holds
+ *      bands + 1 screen rows (band b = [band_rows[b], band_rows[b+1]), starting on tile
+ *      rows, covering [0, height)); band_counts receives the per-band splat counts (the
+ *      all-to-all send counts). Synchronises the host.
+ *   2. gscg_pack_bands: writes the routed splats, GSCG_BAND_SPLAT_BYTES each, grouped by
+ *      band at the exclusive prefix of band_counts, into a caller device buffer.
+ *      Asynchronous on gscg_stream.
+ *   3. after the caller's exchange (e.g. NCCL all-to-all ordered on gscg_stream),
+ *      gscg_render_band sorts the received splats by the reference's total order
+ *      (depth, instance, gaussian) and rasterises rows [row_begin, row_end) into fb_rgb
+ *      (rows x width x 3) / fb_T. The result is identical to the same rows of
+ *      gscg_render_frame. Chunk order inside the receive buffer does not matter. */
+int gscg_project_shard(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                       const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                       uint32_t shard_begin, uint32_t shard_end, uint32_t bands, const uint32_t* band_rows,
+                       uint64_t* band_counts, gscg_stage_times* times);
+int gscg_pack_bands(gscg_ctx* ctx, void* send_dev);
+int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, uint32_t row_begin,
+                     uint32_t row_end, float* fb_rgb, float* fb_T, int32_t memory, gscg_stage_times* times);
 
 #ifdef __cplusplus
 }

@@ -8,7 +8,7 @@
 //   sort:      splats by depth (k_digit_histogram, k_onesweep x P, k_tie_fixup) ->
 //              pairs in that order (k_splat_cells, k_scan_sums, k_emit_pairs) ->
 //              pairs stably by cell (k_onesweep x P') -> k_cell_ranges
-//   rasterize: k_raster16 (or k_raster_generic for other tile sizes)
+//   rasterize: k_raster16q (or k_raster_generic for other tile sizes)
 //   D2H of framebuffer / transmittance / active LoDs (host mode)
 // The one mid-frame synchronisation reads S, K and the depth-bit range: it sizes the
 // sort and detects capacity overflow (buffers grow to the high-water mark and the
@@ -89,6 +89,11 @@ struct Status : std::runtime_error {
 
 }  // namespace
 
+struct FrameGeom {
+    int W = 0, H = 0, ts = 16, tiles_x = 0, tiles_y = 0, cell = 8;
+    uint32_t cells_per_tile = 1;
+};
+
 struct gscg_ctx {
     int device = 0;
     int sm_count = 0;
@@ -126,6 +131,17 @@ struct gscg_ctx {
     // last frame
     uint32_t n = 0, tiles = 0, cells_per_tile = 1;
     uint64_t G = 0, S = 0, K = 0;
+    uint32_t dmin = 0, dmax = 0;  // depth-bit range of the frame's splats
+    FrameGeom geom;
+    gscg_render_settings settings{};
+    uint32_t launches = 0;
+    // screen-band exchange: 0 none, 1 routed, 2 packed, 3 band rendered
+    int band_state = 0;
+    BandParams band{};
+    DevBuf band_scratch;
+    unsigned long long* h_band_counts = nullptr;
+    uint64_t band_total = 0;
+    uint32_t band_row0 = 0;
 
     void ensure_pinned(size_t bytes) {
         if (bytes <= pinned_cap) return;
@@ -252,6 +268,376 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 }  // namespace
 
+namespace {
+
+void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                    const gscg_render_settings* settings, const gscg_lod_policy* lod) {
+    if (!frame || !cam || !settings || !lod) invalid("null argument");
+    if (settings->tile_size < 1 || settings->tile_size > 64) invalid("RenderSettings: tile_size must be in [1, 64]");
+    if (!(settings->alpha_cutoff > 0.0f && settings->alpha_cutoff < 1.0f))
+        invalid("RenderSettings: alpha_cutoff outside (0,1)");
+    if (!(settings->transmittance_floor > 0.0f && settings->transmittance_floor < 1.0f))
+        invalid("RenderSettings: transmittance_floor outside (0,1)");
+    if (cam->width < 1 || cam->height < 1 || cam->width > 65535 || cam->height > 65535)
+        invalid("Camera: width and height must be in [1, 65535]");
+    if (!(cam->near_m > 0.0f)) invalid("Camera: near plane must be > 0");
+    if (lod->threshold_count > GSCG_MAX_LOD_THRESHOLDS) invalid("LodPolicy: too many thresholds");
+    const uint32_t n = frame->instance_count;
+    if (n > 0 && (!frame->template_ids || !frame->placement || !frame->poses || !frame->active_lod))
+        invalid("null frame array");
+    upload_tables(ctx);
+    if (n > 0 && frame->joint_stride < ctx->joint_stride) invalid("joint_stride below the largest skeleton");
+    if (frame->memory == GSCG_MEM_HOST) {
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t t = frame->template_ids[i];
+            if (t >= ctx->templates.size() || !ctx->templates[t].present || ctx->templates[t].levels.empty())
+                invalid("instance " + std::to_string(i) + " references a missing template");
+        }
+    }
+    refresh_power_floor(ctx, settings->alpha_cutoff);
+    FrameGeom& g = ctx->geom;
+    g.W = cam->width;
+    g.H = cam->height;
+    g.ts = settings->tile_size;
+    g.tiles_x = (g.W + g.ts - 1) / g.ts;
+    g.tiles_y = (g.H + g.ts - 1) / g.ts;
+    g.cells_per_tile = g.ts == 16 ? 4u : 1u;  // 8x8 quadrant binning for tile 16
+    g.cell = g.ts == 16 ? 8 : g.ts;
+    ctx->settings = *settings;
+}
+
+// H2D of the frame records, update (LoD plan + FK) and gather (projection) for the
+// instances [shard_begin, shard_end); sets S, K, G and the depth-bit range. Events 0..3.
+void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                   const gscg_lod_policy* lod, uint32_t shard_begin, uint32_t shard_end, uint32_t& launches) {
+    cudaStream_t s = ctx->stream;
+    const FrameGeom& geo = ctx->geom;
+    const gscg_render_settings* settings = &ctx->settings;
+    const bool host = frame->memory == GSCG_MEM_HOST;
+    const uint32_t n = frame->instance_count;
+    const uint32_t js = std::max<uint32_t>(ctx->joint_stride, 1);
+    const uint32_t pose_stride = 4 + 4 * frame->joint_stride;
+
+    CUDA_TRY(ctx->template_ids.ensure(std::max<size_t>(n, 1) * 4));
+    CUDA_TRY(ctx->placement.ensure(std::max<size_t>(n, 1) * 16));
+    CUDA_TRY(ctx->poses.ensure(std::max<size_t>(n, 1) * pose_stride * 4));
+    CUDA_TRY(ctx->lod_prev.ensure(std::max<size_t>(n, 1) * 4));
+    CUDA_TRY(ctx->lod_out.ensure(std::max<size_t>(n, 1) * 4));
+    CUDA_TRY(ctx->inst_group.ensure(std::max<size_t>(n, 1) * 4));
+    CUDA_TRY(ctx->inst_base.ensure(std::max<size_t>(n, 1) * 4));
+    CUDA_TRY(ctx->members.ensure(std::max<size_t>(n, 1) * 4));
+    CUDA_TRY(ctx->group_inst_start.ensure((kMaxGroups + 1) * 4));
+    CUDA_TRY(ctx->group_inst_count.ensure((kMaxGroups + 1) * 4));
+    CUDA_TRY(ctx->group_item_start.ensure((kMaxGroups + 1) * 4));
+    CUDA_TRY(ctx->skin.ensure(std::max<size_t>(n, 1) * js * 12 * 4));
+
+    // ---- H2D ----
+    CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
+    const uint32_t *d_tid, *d_lodprev;
+    const float *d_place, *d_poses;
+    if (host) {
+        const size_t b_tid = n * 4ull, b_place = n * 16ull, b_pose = n * 4ull * pose_stride, b_lod = n * 4ull;
+        ctx->ensure_pinned(b_tid + b_place + b_pose + b_lod + 64);
+        char* h = static_cast<char*>(ctx->pinned);
+        std::memcpy(h, frame->template_ids, b_tid);
+        std::memcpy(h + b_tid, frame->placement, b_place);
+        std::memcpy(h + b_tid + b_place, frame->poses, b_pose);
+        std::memcpy(h + b_tid + b_place + b_pose, frame->active_lod, b_lod);
+        if (n) {
+            CUDA_TRY(cudaMemcpyAsync(ctx->template_ids.ptr, h, b_tid, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(ctx->placement.ptr, h + b_tid, b_place, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(ctx->poses.ptr, h + b_tid + b_place, b_pose, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(ctx->lod_prev.ptr, h + b_tid + b_place + b_pose, b_lod, cudaMemcpyHostToDevice, s));
+        }
+        d_tid = ctx->template_ids.as<uint32_t>();
+        d_place = ctx->placement.as<float>();
+        d_poses = ctx->poses.as<float>();
+        d_lodprev = ctx->lod_prev.as<uint32_t>();
+    } else {
+        d_tid = frame->template_ids;
+        d_place = frame->placement;
+        d_poses = frame->poses;
+        d_lodprev = frame->active_lod;
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
+
+    const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + kBatch * static_cast<int>(js) * 12 * 4;
+    int project_blocks_per_sm = 1;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project, kProjectThreads, project_smem));
+    project_blocks_per_sm = std::max(project_blocks_per_sm, 1);
+
+    auto* counters = ctx->counters.as<FrameCounters>();
+    for (int attempt = 0;; ++attempt) {
+        // ---- update ----
+        PlanParams pp{};
+        pp.n = n;
+        pp.shard_begin = shard_begin;
+        pp.shard_end = shard_end;
+        pp.template_ids = d_tid;
+        pp.placement = d_place;
+        pp.lod_prev = d_lodprev;
+        pp.forced_lod = frame->forced_lod;
+        pp.threshold_count = lod->threshold_count;
+        for (uint32_t i = 0; i < lod->threshold_count; ++i) pp.thresholds[i] = lod->thresholds_m[i];
+        pp.hysteresis = lod->hysteresis_band_m;
+        for (int i = 0; i < 3; ++i) pp.cam_pos[i] = cam->position[i];
+        pp.templates = ctx->d_templates.as<TemplateDev>();
+        pp.groups = ctx->d_groups.as<GroupDev>();
+        pp.group_count = ctx->group_count;
+        pp.lod_out = ctx->lod_out.as<uint32_t>();
+        pp.inst_group = ctx->inst_group.as<uint32_t>();
+        pp.inst_base = ctx->inst_base.as<uint32_t>();
+        pp.group_inst_start = ctx->group_inst_start.as<uint32_t>();
+        pp.group_inst_count = ctx->group_inst_count.as<uint32_t>();
+        pp.group_item_start = ctx->group_item_start.as<uint32_t>();
+        pp.members = ctx->members.as<uint32_t>();
+        pp.counters = counters;
+        k_lod_plan<<<1, 1024, 0, s>>>(pp);
+        ++launches;
+        CUDA_TRY(cudaGetLastError());
+        if (shard_end > shard_begin) {
+            FkParams fp{};
+            fp.n = shard_end;
+            fp.first = shard_begin;
+            fp.joint_stride = js;
+            fp.pose_stride = pose_stride;
+            fp.template_ids = d_tid;
+            fp.placement = d_place;
+            fp.poses = d_poses;
+            fp.templates = ctx->d_templates.as<TemplateDev>();
+            fp.mats = ctx->d_mats.as<float>();
+            fp.parents = ctx->d_parents.as<int32_t>();
+            fp.skin = ctx->skin.as<float>();
+            const int per_block = 16;
+            const uint32_t m = shard_end - shard_begin;
+            k_fk_skin<<<(m + per_block - 1) / per_block, 256, per_block * js * 16 * 4, s>>>(fp);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+        }
+        CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
+
+        if (ctx->debug & GSCG_DEBUG_POSED) {
+            CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            CUDA_TRY(ctx->posed_dbg.ensure(std::max<uint64_t>(ctx->h_counters->gaussians, 1) * 12));
+        }
+        if (ctx->splat_capacity == 0) {
+            ctx->splat_capacity = 1u << 20;
+            ctx->pair_capacity = 1u << 21;
+        }
+        CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
+        CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->splat_span.ensure(ctx->splat_capacity * 8));
+        if (ctx->debug & GSCG_DEBUG_RECORDS)
+            CUDA_TRY(ctx->rec_dbg.ensure(ctx->splat_capacity * sizeof(gscg_splat_record)));
+
+        // ---- gather ----
+        ProjectParams pj{};
+        std::memcpy(pj.cam.w, cam->world_to_view, sizeof(pj.cam.w));
+        std::memcpy(pj.cam.pos, cam->position, sizeof(pj.cam.pos));
+        pj.cam.focal = cam->focal;
+        pj.cam.cx = cam->cx;
+        pj.cam.cy = cam->cy;
+        pj.cam.near_m = cam->near_m;
+        pj.cam.width = geo.W;
+        pj.cam.height = geo.H;
+        pj.tile_size = geo.ts;
+        pj.tiles_x = geo.tiles_x;
+        pj.sh_enabled = settings->sh_enabled ? 1 : 0;
+        pj.joint_stride = js;
+        pj.group_count = ctx->group_count;
+        pj.groups = ctx->d_groups.as<GroupDev>();
+        pj.group_item_start = ctx->group_item_start.as<uint32_t>();
+        pj.group_inst_start = ctx->group_inst_start.as<uint32_t>();
+        pj.group_inst_count = ctx->group_inst_count.as<uint32_t>();
+        pj.members = ctx->members.as<uint32_t>();
+        pj.inst_base = ctx->inst_base.as<uint32_t>();
+        pj.skin = ctx->skin.as<float>();
+        pj.counters = counters;
+        pj.records = ctx->records.as<float4>();
+        pj.record_ordinal = ctx->record_ordinal.as<uint32_t>();
+        pj.splat_depth = ctx->splat_depth.as<uint32_t>();
+        pj.splat_span = ctx->splat_span.as<uint2>();
+        pj.splat_capacity = ctx->splat_capacity;
+        pj.pair_capacity = ctx->pair_capacity;
+        pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
+        pj.record_debug = (ctx->debug & GSCG_DEBUG_RECORDS) ? ctx->rec_dbg.as<gscg_splat_record>() : nullptr;
+        if (shard_end > shard_begin && ctx->group_count > 0) {
+            k_project<<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+        }
+        CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const uint64_t S = ctx->h_counters->splat_pair >> 32;
+        const uint64_t K = ctx->h_counters->splat_pair & 0xffffffffull;
+        if (S <= ctx->splat_capacity && K <= ctx->pair_capacity) {
+            ctx->S = S;
+            ctx->K = K;
+            ctx->G = ctx->h_counters->gaussians;
+            ctx->dmin = ctx->h_counters->depth_min_bits;
+            ctx->dmax = ctx->h_counters->depth_max_bits;
+            break;
+        }
+        if (attempt > 2) throw Status(GSCG_ERR_STATE, "splat/pair capacity did not converge");
+        if (K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "tile-splat pair count exceeds 32-bit indexing");
+        ctx->splat_capacity = std::max<uint64_t>(ctx->splat_capacity, S + S / 4 + 1024);
+        ctx->pair_capacity = std::max<uint64_t>(ctx->pair_capacity, K + K / 4 + 1024);
+    }
+    ctx->n = n;
+}
+
+// Sort (splats by depth + ordinal, pairs in that order, pairs stably by cell) and
+// rasterise tile rows [tile_row0, tile_row0 + tile_rows) from the context's records
+// (ctx->S splats, ctx->K pairs whose spans are relative to tile_row0). Events 3..5.
+uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& launches) {
+    cudaStream_t s = ctx->stream;
+    const FrameGeom& geo = ctx->geom;
+    const uint32_t tiles = static_cast<uint32_t>(geo.tiles_x) * static_cast<uint32_t>(tile_rows);
+    const uint32_t cells = tiles * geo.cells_per_tile;
+    CUDA_TRY(ctx->fb_rgb.ensure(static_cast<size_t>(geo.W) * geo.H * 12));
+    CUDA_TRY(ctx->fb_T.ensure(static_cast<size_t>(geo.W) * geo.H * 4));
+    CUDA_TRY(ctx->ranges.ensure(std::max<size_t>(cells, 1) * 8));
+
+    const uint32_t K = static_cast<uint32_t>(ctx->K);
+    const uint32_t S32 = static_cast<uint32_t>(ctx->S);
+    uint32_t passes = 0;
+    if (cells) CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(cells) * 8, s));
+    ctx->final_recs = nullptr;
+    if (S32 > 0 && K > 0) {
+        const uint32_t max_elems = std::max(S32, K);
+        const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
+        CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * 256 * 4));  // tile digit counts
+        CUDA_TRY(ctx->hist.ensure(256 * 4));                                        // digit bases
+        for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(ctx->skeys[b].ensure(static_cast<size_t>(S32) * 4));
+            CUDA_TRY(ctx->srecs[b].ensure(static_cast<size_t>(S32) * 4));
+            CUDA_TRY(ctx->pcell[b].ensure(static_cast<size_t>(K) * 4));
+            CUDA_TRY(ctx->precs[b].ensure(static_cast<size_t>(K) * 4));
+        }
+        // Stable LSD radix sort of (keys, vals) over the plan (reduce-then-scan passes);
+        // returns the buffer index holding the result. in_keys/in_vals feed pass 0
+        // (vals may be null = identity).
+        auto radix = [&](const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb, uint32_t count,
+                         const RadixPlan& plan) -> int {
+            const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
+            int out = 0;
+            for (uint32_t q = 0; q < plan.passes; ++q) {
+                SortPassParams sp{};
+                sp.keys_in = q == 0 ? in_keys : kb[out ^ 1].as<uint32_t>();
+                sp.vals_in = q == 0 ? in_vals : vb[out ^ 1].as<uint32_t>();
+                sp.keys_out = kb[out].as<uint32_t>();
+                sp.vals_out = vb[out].as<uint32_t>();
+                sp.count = count;
+                sp.shift = plan.shift[q];
+                sp.bits = plan.bits[q];
+                sp.tiles = tiles;
+                sp.counts = ctx->status.as<uint32_t>();
+                sp.digit_base = ctx->hist.as<uint32_t>();
+                k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+                k_sort_rows<<<kRadix, 1024, 0, s>>>(sp);
+                k_sort_bases<<<1, kRadix, 0, s>>>(sp);
+                k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+                launches += 4;
+                out ^= 1;
+            }
+            CUDA_TRY(cudaGetLastError());
+            return out ^ 1;
+        };
+        auto make_plan = [](uint32_t bits) {
+            RadixPlan pl{};
+            bits = std::max(bits, 1u);
+            for (uint32_t sh = 0; sh < bits; sh += kRadixBits) {
+                pl.shift[pl.passes] = sh;
+                pl.bits[pl.passes] = std::min<uint32_t>(kRadixBits, bits - sh);
+                ++pl.passes;
+            }
+            return pl;
+        };
+        // 1. splats by depth (bits that vary in the frame), ties by ordinal.
+        const RadixPlan dplan = make_plan(static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax)));
+        const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
+        const uint32_t sgrid = (S32 + 256 * kStreamItems - 1) / (256 * kStreamItems);
+        k_tie_fixup<<<sgrid, 256, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
+                                          ctx->record_ordinal.as<uint32_t>(), S32);
+        // 2. pairs in sorted splat order.
+        const uint32_t sblocks = (S32 + 1023) / 1024;
+        CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
+        CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * 4));
+        k_splat_cells<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->splat_span.as<uint2>(),
+                                               ctx->span_sorted.as<uint2>(), ctx->block_sums.as<uint32_t>());
+        k_scan_sums<<<1, 1024, 0, s>>>(ctx->block_sums.as<uint32_t>(), sblocks);
+        k_emit_pairs<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
+                                              ctx->block_sums.as<uint32_t>(), geo.tiles_x, geo.cells_per_tile == 4 ? 1 : 0,
+                                              ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
+        launches += 4;
+        CUDA_TRY(cudaGetLastError());
+        // 3. pairs stably by cell id; ranges.
+        const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
+        const int cb = radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell, ctx->precs, K, cplan);
+        const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);
+        k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
+        ++launches;
+        CUDA_TRY(cudaGetLastError());
+        ctx->final_recs = ctx->precs[cb].as<uint32_t>();
+        passes = dplan.passes + cplan.passes;
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev[4], s));
+
+    // ---- rasterize ----
+    if (tiles) {
+        RasterParams rp{};
+        rp.ranges = ctx->ranges.as<uint2>();
+        rp.recs = ctx->final_recs;
+        rp.records = ctx->records.as<float4>();
+        rp.width = geo.W;
+        rp.height = geo.H;
+        rp.tile_size = geo.ts;
+        rp.tiles_x = geo.tiles_x;
+        rp.tile_row0 = tile_row0;
+        rp.out_row0 = tile_row0 * geo.ts;
+        for (int i = 0; i < 3; ++i) rp.bg[i] = ctx->settings.background[i];
+        rp.alpha_max = ctx->settings.alpha_max;
+        rp.t_floor = ctx->settings.transmittance_floor;
+        rp.out_rgb = ctx->fb_rgb.as<float>();
+        rp.out_T = ctx->fb_T.as<float>();
+        launch_raster(rp, tiles, s);
+        ++launches;
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev[5], s));
+    ctx->tiles = tiles;
+    ctx->cells_per_tile = geo.cells_per_tile;
+    return passes;
+}
+
+// D2H (host mode) or D2D of `rows` framebuffer rows starting at the context's row 0.
+void copy_out(gscg_ctx* ctx, int rows, float* fb_rgb, float* fb_T, bool host) {
+    cudaStream_t s = ctx->stream;
+    const size_t px = static_cast<size_t>(ctx->geom.W) * rows;
+    const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (fb_rgb && px) CUDA_TRY(cudaMemcpyAsync(fb_rgb, ctx->fb_rgb.ptr, px * 12, kind, s));
+    if (fb_T && px) CUDA_TRY(cudaMemcpyAsync(fb_T, ctx->fb_T.ptr, px * 4, kind, s));
+}
+
+void fill_times(gscg_ctx* ctx, gscg_stage_times* times, uint32_t passes, uint32_t launches) {
+    times->h2d_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+    times->update_ms = elapsed(ctx->ev[1], ctx->ev[2]);
+    times->gather_ms = elapsed(ctx->ev[2], ctx->ev[3]);
+    times->sort_ms = elapsed(ctx->ev[3], ctx->ev[4]);
+    times->rasterize_ms = elapsed(ctx->ev[4], ctx->ev[5]);
+    times->d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+    times->splat_count = ctx->S;
+    times->pair_count = ctx->K;
+    times->gaussian_count = ctx->G;
+    times->sort_passes = passes;
+    times->kernel_launches = launches;
+}
+
+}  // namespace
+
 extern "C" {
 
 int gscg_device_count(int* out) {
@@ -280,6 +666,7 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
+        CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_band_counts), GSCG_MAX_BANDS * sizeof(unsigned long long)));
         CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
         CUDA_TRY(cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
@@ -306,10 +693,11 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
                       &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->splat_span, &ctx->span_sorted,
                       &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
-                      &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg};
+                      &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch};
     for (DevBuf* b : bufs) b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+    if (ctx->h_band_counts) cudaFreeHost(ctx->h_band_counts);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -418,343 +806,176 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
         CUDA_TRY(cudaSetDevice(ctx->device));
-        if (!frame || !cam || !settings || !lod) invalid("null argument");
-        if (settings->tile_size < 1 || settings->tile_size > 64) invalid("RenderSettings: tile_size must be in [1, 64]");
-        if (!(settings->alpha_cutoff > 0.0f && settings->alpha_cutoff < 1.0f))
-            invalid("RenderSettings: alpha_cutoff outside (0,1)");
-        if (!(settings->transmittance_floor > 0.0f && settings->transmittance_floor < 1.0f))
-            invalid("RenderSettings: transmittance_floor outside (0,1)");
-        if (cam->width < 1 || cam->height < 1 || cam->width > 65535 || cam->height > 65535)
-            invalid("Camera: width and height must be in [1, 65535]");
-        if (!(cam->near_m > 0.0f)) invalid("Camera: near plane must be > 0");
-        if (lod->threshold_count > GSCG_MAX_LOD_THRESHOLDS) invalid("LodPolicy: too many thresholds");
+        validate_frame(ctx, frame, cam, settings, lod);
         const bool host = frame->memory == GSCG_MEM_HOST;
         const uint32_t n = frame->instance_count;
-        if (n > 0 && (!frame->template_ids || !frame->placement || !frame->poses || !frame->active_lod))
-            invalid("null frame array");
-        upload_tables(ctx);
-        if (n > 0 && frame->joint_stride < ctx->joint_stride) invalid("joint_stride below the largest skeleton");
-        if (host) {
-            for (uint32_t i = 0; i < n; ++i) {
-                const uint32_t t = frame->template_ids[i];
-                if (t >= ctx->templates.size() || !ctx->templates[t].present || ctx->templates[t].levels.empty())
-                    invalid("instance " + std::to_string(i) + " references a missing template");
-            }
-        }
-        refresh_power_floor(ctx, settings->alpha_cutoff);
-
-        cudaStream_t s = ctx->stream;
-        const uint32_t js = std::max<uint32_t>(ctx->joint_stride, 1);
-        const uint32_t pose_stride = 4 + 4 * frame->joint_stride;
-        const int W = cam->width, H = cam->height, ts = settings->tile_size;
-        const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
-        const uint32_t tiles = static_cast<uint32_t>(tiles_x) * tiles_y;
-        const uint32_t cells_per_tile = ts == 16 ? 4u : 1u;  // 8x8 quadrant binning for tile 16
-        const uint32_t cells = tiles * cells_per_tile;
         uint32_t launches = 0;
+        ctx->band_state = 0;
+        update_gather(ctx, frame, cam, lod, 0, n, launches);
+        const uint32_t passes = sort_raster(ctx, 0, ctx->geom.tiles_y, launches);
+        copy_out(ctx, ctx->geom.H, fb_rgb, fb_T, host);
+        if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull,
+                                        host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+        CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->stream));
+        if (host || times) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (times) fill_times(ctx, times, passes, launches);
+    });
+}
 
-        CUDA_TRY(ctx->template_ids.ensure(std::max<size_t>(n, 1) * 4));
-        CUDA_TRY(ctx->placement.ensure(std::max<size_t>(n, 1) * 16));
-        CUDA_TRY(ctx->poses.ensure(std::max<size_t>(n, 1) * pose_stride * 4));
-        CUDA_TRY(ctx->lod_prev.ensure(std::max<size_t>(n, 1) * 4));
-        CUDA_TRY(ctx->lod_out.ensure(std::max<size_t>(n, 1) * 4));
-        CUDA_TRY(ctx->inst_group.ensure(std::max<size_t>(n, 1) * 4));
-        CUDA_TRY(ctx->inst_base.ensure(std::max<size_t>(n, 1) * 4));
-        CUDA_TRY(ctx->members.ensure(std::max<size_t>(n, 1) * 4));
-        CUDA_TRY(ctx->group_inst_start.ensure((kMaxGroups + 1) * 4));
-        CUDA_TRY(ctx->group_inst_count.ensure((kMaxGroups + 1) * 4));
-        CUDA_TRY(ctx->group_item_start.ensure((kMaxGroups + 1) * 4));
-        CUDA_TRY(ctx->skin.ensure(std::max<size_t>(n, 1) * js * 12 * 4));
-        CUDA_TRY(ctx->fb_rgb.ensure(static_cast<size_t>(W) * H * 12));
-        CUDA_TRY(ctx->fb_T.ensure(static_cast<size_t>(W) * H * 4));
-        CUDA_TRY(ctx->ranges.ensure(static_cast<size_t>(cells) * 8));
-
-        // ---- H2D ----
-        CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
-        const uint32_t *d_tid, *d_lodprev;
-        const float *d_place, *d_poses;
-        if (host) {
-            const size_t b_tid = n * 4ull, b_place = n * 16ull, b_pose = n * 4ull * pose_stride, b_lod = n * 4ull;
-            ctx->ensure_pinned(b_tid + b_place + b_pose + b_lod + 64);
-            char* h = static_cast<char*>(ctx->pinned);
-            std::memcpy(h, frame->template_ids, b_tid);
-            std::memcpy(h + b_tid, frame->placement, b_place);
-            std::memcpy(h + b_tid + b_place, frame->poses, b_pose);
-            std::memcpy(h + b_tid + b_place + b_pose, frame->active_lod, b_lod);
-            if (n) {
-                CUDA_TRY(cudaMemcpyAsync(ctx->template_ids.ptr, h, b_tid, cudaMemcpyHostToDevice, s));
-                CUDA_TRY(cudaMemcpyAsync(ctx->placement.ptr, h + b_tid, b_place, cudaMemcpyHostToDevice, s));
-                CUDA_TRY(cudaMemcpyAsync(ctx->poses.ptr, h + b_tid + b_place, b_pose, cudaMemcpyHostToDevice, s));
-                CUDA_TRY(cudaMemcpyAsync(ctx->lod_prev.ptr, h + b_tid + b_place + b_pose, b_lod, cudaMemcpyHostToDevice, s));
-            }
-            d_tid = ctx->template_ids.as<uint32_t>();
-            d_place = ctx->placement.as<float>();
-            d_poses = ctx->poses.as<float>();
-            d_lodprev = ctx->lod_prev.as<uint32_t>();
-        } else {
-            d_tid = frame->template_ids;
-            d_place = frame->placement;
-            d_poses = frame->poses;
-            d_lodprev = frame->active_lod;
+int gscg_project_shard(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                       const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                       uint32_t shard_begin, uint32_t shard_end, uint32_t bands, const uint32_t* band_rows,
+                       uint64_t* band_counts, gscg_stage_times* times) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        validate_frame(ctx, frame, cam, settings, lod);
+        const uint32_t n = frame->instance_count;
+        if (shard_begin > shard_end || shard_end > n) invalid("instance shard outside [0, instance_count]");
+        if (bands < 1 || bands > GSCG_MAX_BANDS || !band_rows || !band_counts) invalid("bad screen band table");
+        const FrameGeom& geo = ctx->geom;
+        if (band_rows[0] != 0 || band_rows[bands] != static_cast<uint32_t>(geo.H))
+            invalid("screen bands must cover rows [0, height)");
+        for (uint32_t b = 0; b < bands; ++b) {
+            if (band_rows[b + 1] < band_rows[b]) invalid("screen band rows must be non-decreasing");
+            if (band_rows[b] % static_cast<uint32_t>(geo.ts) != 0) invalid("screen bands must start on a tile row");
         }
-        CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
-
-        const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + kBatch * static_cast<int>(js) * 12 * 4;
-        int project_blocks_per_sm = 1;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project, kProjectThreads, project_smem));
-        project_blocks_per_sm = std::max(project_blocks_per_sm, 1);
-
-        auto* counters = ctx->counters.as<FrameCounters>();
-        for (int attempt = 0;; ++attempt) {
-            // ---- update ----
-            PlanParams pp{};
-            pp.n = n;
-            pp.template_ids = d_tid;
-            pp.placement = d_place;
-            pp.lod_prev = d_lodprev;
-            pp.forced_lod = frame->forced_lod;
-            pp.threshold_count = lod->threshold_count;
-            for (uint32_t i = 0; i < lod->threshold_count; ++i) pp.thresholds[i] = lod->thresholds_m[i];
-            pp.hysteresis = lod->hysteresis_band_m;
-            for (int i = 0; i < 3; ++i) pp.cam_pos[i] = cam->position[i];
-            pp.templates = ctx->d_templates.as<TemplateDev>();
-            pp.groups = ctx->d_groups.as<GroupDev>();
-            pp.group_count = ctx->group_count;
-            pp.lod_out = ctx->lod_out.as<uint32_t>();
-            pp.inst_group = ctx->inst_group.as<uint32_t>();
-            pp.inst_base = ctx->inst_base.as<uint32_t>();
-            pp.group_inst_start = ctx->group_inst_start.as<uint32_t>();
-            pp.group_inst_count = ctx->group_inst_count.as<uint32_t>();
-            pp.group_item_start = ctx->group_item_start.as<uint32_t>();
-            pp.members = ctx->members.as<uint32_t>();
-            pp.counters = counters;
-            k_lod_plan<<<1, 1024, 0, s>>>(pp);
+        ctx->band_state = 0;
+        uint32_t launches = 0;
+        update_gather(ctx, frame, cam, lod, shard_begin, shard_end, launches);
+        if (frame->memory == GSCG_MEM_HOST) {
+            if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToHost, ctx->stream));
+        } else if (n) {
+            CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        // Route: splats per destination band.
+        BandParams& bp = ctx->band;
+        bp = BandParams{};
+        bp.records = ctx->records.as<float4>();
+        bp.ordinal = ctx->record_ordinal.as<uint32_t>();
+        bp.depth = ctx->splat_depth.as<uint32_t>();
+        bp.count = static_cast<uint32_t>(ctx->S);
+        bp.bands = bands;
+        for (uint32_t b = 0; b <= bands; ++b) bp.rows[b] = band_rows[b];
+        CUDA_TRY(ctx->band_scratch.ensure(2 * kMaxBands * sizeof(unsigned long long)));
+        bp.band_counts = ctx->band_scratch.as<unsigned long long>();
+        bp.band_cursor = bp.band_counts + kMaxBands;
+        CUDA_TRY(cudaMemsetAsync(ctx->band_scratch.ptr, 0, 2 * kMaxBands * sizeof(unsigned long long), ctx->stream));
+        const uint32_t grid = (bp.count + 256 * kStreamItems - 1) / (256 * kStreamItems);
+        if (grid) {
+            k_band_count<<<grid, 256, 0, ctx->stream>>>(bp);
             ++launches;
             CUDA_TRY(cudaGetLastError());
-            if (n > 0) {
-                FkParams fp{};
-                fp.n = n;
-                fp.joint_stride = js;
-                fp.pose_stride = pose_stride;
-                fp.template_ids = d_tid;
-                fp.placement = d_place;
-                fp.poses = d_poses;
-                fp.templates = ctx->d_templates.as<TemplateDev>();
-                fp.mats = ctx->d_mats.as<float>();
-                fp.parents = ctx->d_parents.as<int32_t>();
-                fp.skin = ctx->skin.as<float>();
-                const int per_block = 16;
-                k_fk_skin<<<(n + per_block - 1) / per_block, 256, per_block * js * 16 * 4, s>>>(fp);
-                ++launches;
-                CUDA_TRY(cudaGetLastError());
-            }
-            CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
-
-            if (ctx->debug & GSCG_DEBUG_POSED) {
-                CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
-                CUDA_TRY(cudaStreamSynchronize(s));
-                CUDA_TRY(ctx->posed_dbg.ensure(std::max<uint64_t>(ctx->h_counters->gaussians, 1) * 12));
-            }
-            if (ctx->splat_capacity == 0) {
-                ctx->splat_capacity = 1u << 20;
-                ctx->pair_capacity = 1u << 21;
-            }
-            CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
-            CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
-            CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
-            CUDA_TRY(ctx->splat_span.ensure(ctx->splat_capacity * 8));
-            if (ctx->debug & GSCG_DEBUG_RECORDS)
-                CUDA_TRY(ctx->rec_dbg.ensure(ctx->splat_capacity * sizeof(gscg_splat_record)));
-
-            // ---- gather ----
-            ProjectParams pj{};
-            std::memcpy(pj.cam.w, cam->world_to_view, sizeof(pj.cam.w));
-            std::memcpy(pj.cam.pos, cam->position, sizeof(pj.cam.pos));
-            pj.cam.focal = cam->focal;
-            pj.cam.cx = cam->cx;
-            pj.cam.cy = cam->cy;
-            pj.cam.near_m = cam->near_m;
-            pj.cam.width = W;
-            pj.cam.height = H;
-            pj.tile_size = ts;
-            pj.tiles_x = tiles_x;
-            pj.sh_enabled = settings->sh_enabled ? 1 : 0;
-            pj.joint_stride = js;
-            pj.group_count = ctx->group_count;
-            pj.groups = ctx->d_groups.as<GroupDev>();
-            pj.group_item_start = ctx->group_item_start.as<uint32_t>();
-            pj.group_inst_start = ctx->group_inst_start.as<uint32_t>();
-            pj.group_inst_count = ctx->group_inst_count.as<uint32_t>();
-            pj.members = ctx->members.as<uint32_t>();
-            pj.inst_base = ctx->inst_base.as<uint32_t>();
-            pj.skin = ctx->skin.as<float>();
-            pj.counters = counters;
-            pj.records = ctx->records.as<float4>();
-            pj.record_ordinal = ctx->record_ordinal.as<uint32_t>();
-            pj.splat_depth = ctx->splat_depth.as<uint32_t>();
-            pj.splat_span = ctx->splat_span.as<uint2>();
-            pj.splat_capacity = ctx->splat_capacity;
-            pj.pair_capacity = ctx->pair_capacity;
-            pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
-            pj.record_debug = (ctx->debug & GSCG_DEBUG_RECORDS) ? ctx->rec_dbg.as<gscg_splat_record>() : nullptr;
-            if (n > 0 && ctx->group_count > 0) {
-                k_project<<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
-                ++launches;
-                CUDA_TRY(cudaGetLastError());
-            }
-            CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
-            CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
-            const uint64_t S = ctx->h_counters->splat_pair >> 32;
-            const uint64_t K = ctx->h_counters->splat_pair & 0xffffffffull;
-            if (S <= ctx->splat_capacity && K <= ctx->pair_capacity) {
-                ctx->S = S;
-                ctx->K = K;
-                ctx->G = ctx->h_counters->gaussians;
-                break;
-            }
-            if (attempt > 2) throw Status(GSCG_ERR_STATE, "splat/pair capacity did not converge");
-            if (K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "tile-splat pair count exceeds 32-bit indexing");
-            ctx->splat_capacity = std::max<uint64_t>(ctx->splat_capacity, S + S / 4 + 1024);
-            ctx->pair_capacity = std::max<uint64_t>(ctx->pair_capacity, K + K / 4 + 1024);
         }
-
-        // ---- sort ----
-        const uint32_t K = static_cast<uint32_t>(ctx->K);
-        const uint32_t S32 = static_cast<uint32_t>(ctx->S);
-        uint32_t passes = 0;
-        CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(cells) * 8, s));
-        ctx->final_recs = nullptr;
-        if (S32 > 0 && K > 0) {
-            const uint32_t max_elems = std::max(S32, K);
-            const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
-            CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * 256 * 4));  // tile digit counts
-            CUDA_TRY(ctx->hist.ensure(256 * 4));                                        // digit bases
-            for (int b = 0; b < 2; ++b) {
-                CUDA_TRY(ctx->skeys[b].ensure(static_cast<size_t>(S32) * 4));
-                CUDA_TRY(ctx->srecs[b].ensure(static_cast<size_t>(S32) * 4));
-                CUDA_TRY(ctx->pcell[b].ensure(static_cast<size_t>(K) * 4));
-                CUDA_TRY(ctx->precs[b].ensure(static_cast<size_t>(K) * 4));
-            }
-            // Stable LSD onesweep of (keys, vals) over the plan; returns the buffer index
-            // holding the result. in_keys/in_vals feed pass 0 (vals may be null = identity).
-            // Stable LSD radix sort of (keys, vals) over the plan (reduce-then-scan passes);
-            // returns the buffer index holding the result. in_keys/in_vals feed pass 0
-            // (vals may be null = identity).
-            auto radix = [&](const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb, uint32_t count,
-                             const RadixPlan& plan) -> int {
-                const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
-                int out = 0;
-                for (uint32_t q = 0; q < plan.passes; ++q) {
-                    SortPassParams sp{};
-                    sp.keys_in = q == 0 ? in_keys : kb[out ^ 1].as<uint32_t>();
-                    sp.vals_in = q == 0 ? in_vals : vb[out ^ 1].as<uint32_t>();
-                    sp.keys_out = kb[out].as<uint32_t>();
-                    sp.vals_out = vb[out].as<uint32_t>();
-                    sp.count = count;
-                    sp.shift = plan.shift[q];
-                    sp.bits = plan.bits[q];
-                    sp.tiles = tiles;
-                    sp.counts = ctx->status.as<uint32_t>();
-                    sp.digit_base = ctx->hist.as<uint32_t>();
-                    k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
-                    k_sort_rows<<<kRadix, 1024, 0, s>>>(sp);
-                    k_sort_bases<<<1, kRadix, 0, s>>>(sp);
-                    k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
-                    launches += 4;
-                    out ^= 1;
-                }
-                CUDA_TRY(cudaGetLastError());
-                return out ^ 1;
-            };
-            auto make_plan = [](uint32_t bits) {
-                RadixPlan pl{};
-                bits = std::max(bits, 1u);
-                for (uint32_t sh = 0; sh < bits; sh += kRadixBits) {
-                    pl.shift[pl.passes] = sh;
-                    pl.bits[pl.passes] = std::min<uint32_t>(kRadixBits, bits - sh);
-                    ++pl.passes;
-                }
-                return pl;
-            };
-            // 1. splats by depth (bits that vary in the frame), ties by ordinal.
-            const uint32_t dmin = ctx->h_counters->depth_min_bits, dmax = ctx->h_counters->depth_max_bits;
-            const RadixPlan dplan = make_plan(static_cast<uint32_t>(bits_for(dmin ^ dmax)));
-            const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
-            const uint32_t sgrid = (S32 + 256 * kStreamItems - 1) / (256 * kStreamItems);
-            k_tie_fixup<<<sgrid, 256, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
-                                              ctx->record_ordinal.as<uint32_t>(), S32);
-            // 2. pairs in sorted splat order.
-            const uint32_t sblocks = (S32 + 1023) / 1024;
-            CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
-            CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * 4));
-            k_splat_cells<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->splat_span.as<uint2>(),
-                                                   ctx->span_sorted.as<uint2>(), ctx->block_sums.as<uint32_t>());
-            k_scan_sums<<<1, 1024, 0, s>>>(ctx->block_sums.as<uint32_t>(), sblocks);
-            k_emit_pairs<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
-                                                  ctx->block_sums.as<uint32_t>(), tiles_x, cells_per_tile == 4 ? 1 : 0,
-                                                  ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
-            launches += 4;
-            CUDA_TRY(cudaGetLastError());
-            // 3. pairs stably by cell id; ranges.
-            const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
-            const int cb = radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell, ctx->precs, K, cplan);
-            const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);
-            k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
-            ++launches;
-            CUDA_TRY(cudaGetLastError());
-            ctx->final_recs = ctx->precs[cb].as<uint32_t>();
-            passes = dplan.passes + cplan.passes;
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_band_counts, bp.band_counts, bands * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaEventRecord(ctx->ev[4], ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        unsigned long long off = 0;
+        for (uint32_t b = 0; b < bands; ++b) {
+            band_counts[b] = ctx->h_band_counts[b];
+            bp.band_offsets[b] = off;
+            off += ctx->h_band_counts[b];
         }
-        CUDA_TRY(cudaEventRecord(ctx->ev[4], s));
-
-        // ---- rasterize ----
-        RasterParams rp{};
-        rp.ranges = ctx->ranges.as<uint2>();
-        rp.recs = ctx->final_recs;
-        rp.records = ctx->records.as<float4>();
-        rp.width = W;
-        rp.height = H;
-        rp.tile_size = ts;
-        rp.tiles_x = tiles_x;
-        for (int i = 0; i < 3; ++i) rp.bg[i] = settings->background[i];
-        rp.alpha_max = settings->alpha_max;
-        rp.t_floor = settings->transmittance_floor;
-        rp.out_rgb = ctx->fb_rgb.as<float>();
-        rp.out_T = ctx->fb_T.as<float>();
-        launch_raster(rp, tiles, s);
-        ++launches;
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaEventRecord(ctx->ev[5], s));
-
-        // ---- D2H ----
-        if (host) {
-            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, ctx->fb_rgb.ptr, static_cast<size_t>(W) * H * 12, cudaMemcpyDeviceToHost, s));
-            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, ctx->fb_T.ptr, static_cast<size_t>(W) * H * 4, cudaMemcpyDeviceToHost, s));
-            if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToHost, s));
-        } else {
-            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, ctx->fb_rgb.ptr, static_cast<size_t>(W) * H * 12, cudaMemcpyDeviceToDevice, s));
-            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, ctx->fb_T.ptr, static_cast<size_t>(W) * H * 4, cudaMemcpyDeviceToDevice, s));
-            if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice, s));
-        }
-        CUDA_TRY(cudaEventRecord(ctx->ev[6], s));
-        if (host || times) CUDA_TRY(cudaStreamSynchronize(s));
-
-        ctx->n = n;
-        ctx->tiles = tiles;
-        ctx->cells_per_tile = cells_per_tile;
+        ctx->band_total = off;
+        ctx->band_state = 1;
+        ctx->launches = launches;
         if (times) {
+            *times = gscg_stage_times{};
             times->h2d_ms = elapsed(ctx->ev[0], ctx->ev[1]);
             times->update_ms = elapsed(ctx->ev[1], ctx->ev[2]);
             times->gather_ms = elapsed(ctx->ev[2], ctx->ev[3]);
-            times->sort_ms = elapsed(ctx->ev[3], ctx->ev[4]);
-            times->rasterize_ms = elapsed(ctx->ev[4], ctx->ev[5]);
-            times->d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+            times->sort_ms = elapsed(ctx->ev[3], ctx->ev[4]);  // routing
             times->splat_count = ctx->S;
-            times->pair_count = ctx->K;
             times->gaussian_count = ctx->G;
-            times->sort_passes = passes;
             times->kernel_launches = launches;
+        }
+    });
+}
+
+int gscg_pack_bands(gscg_ctx* ctx, void* send_dev) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (ctx->band_state != 1) throw Status(GSCG_ERR_STATE, "gscg_pack_bands needs gscg_project_shard first");
+        if (!send_dev && ctx->band_total) invalid("null send buffer");
+        BandParams bp = ctx->band;
+        bp.packed = static_cast<uint4*>(send_dev);
+        const uint32_t grid = (bp.count + 256 * kStreamItems - 1) / (256 * kStreamItems);
+        if (grid && ctx->band_total) {
+            k_band_pack<<<grid, 256, 0, ctx->stream>>>(bp);
+            CUDA_TRY(cudaGetLastError());
+        }
+        ctx->band_state = 2;
+    });
+}
+
+int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, uint32_t row_begin, uint32_t row_end,
+                     float* fb_rgb, float* fb_T, int32_t memory, gscg_stage_times* times) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (ctx->band_state < 1) throw Status(GSCG_ERR_STATE, "gscg_render_band needs gscg_project_shard first");
+        const FrameGeom& geo = ctx->geom;
+        if (row_begin > row_end || row_end > static_cast<uint32_t>(geo.H) || row_begin % geo.ts != 0 ||
+            (row_end % geo.ts != 0 && row_end != static_cast<uint32_t>(geo.H)))
+            invalid("band rows must be tile-aligned and inside the frame");
+        if (recv_count && !recv_dev) invalid("null receive buffer");
+        if (recv_count > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "band splat count exceeds 32-bit indexing");
+        cudaStream_t s = ctx->stream;
+        uint32_t launches = 0;
+        CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
+        // The band's splats replace the context's records (the shard's were packed already).
+        const uint64_t cap = std::max<uint64_t>(recv_count, 1);
+        if (cap > ctx->splat_capacity) ctx->splat_capacity = cap + cap / 4;
+        CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
+        CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->splat_span.ensure(ctx->splat_capacity * 8));
+        FrameCounters init{};
+        init.depth_min_bits = 0xffffffffu;
+        *ctx->h_counters = init;
+        auto* counters = ctx->counters.as<FrameCounters>();
+        CUDA_TRY(cudaMemcpyAsync(counters, ctx->h_counters, sizeof(FrameCounters), cudaMemcpyHostToDevice, s));
+        BandUnpackParams up{};
+        up.packed = static_cast<const uint4*>(recv_dev);
+        up.count = static_cast<uint32_t>(recv_count);
+        up.row_begin = static_cast<int32_t>(row_begin);
+        up.row_end = static_cast<int32_t>(row_end);
+        up.cell = geo.cell;
+        up.records = ctx->records.as<float4>();
+        up.ordinal = ctx->record_ordinal.as<uint32_t>();
+        up.depth = ctx->splat_depth.as<uint32_t>();
+        up.span = ctx->splat_span.as<uint2>();
+        up.counters = counters;
+        const uint32_t grid = (up.count + 256 * kStreamItems - 1) / (256 * kStreamItems);
+        if (grid) {
+            k_band_unpack<<<grid, 256, 0, s>>>(up);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+        }
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        ctx->S = recv_count;
+        ctx->K = ctx->h_counters->splat_pair;
+        if (ctx->K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "band pair count exceeds 32-bit indexing");
+        ctx->dmin = ctx->h_counters->depth_min_bits;
+        ctx->dmax = ctx->h_counters->depth_max_bits;
+        const int tile_row0 = static_cast<int>(row_begin) / geo.ts;
+        const int tile_rows = (static_cast<int>(row_end) - static_cast<int>(row_begin) + geo.ts - 1) / geo.ts;
+        const uint32_t passes = sort_raster(ctx, tile_row0, tile_rows, launches);
+        const bool host = memory == GSCG_MEM_HOST;
+        copy_out(ctx, static_cast<int>(row_end - row_begin), fb_rgb, fb_T, host);
+        CUDA_TRY(cudaEventRecord(ctx->ev[6], s));
+        if (host || times) CUDA_TRY(cudaStreamSynchronize(s));
+        ctx->band_row0 = row_begin;
+        ctx->band_state = 3;
+        if (times) {
+            fill_times(ctx, times, passes, launches);
+            times->h2d_ms = 0.0f;
+            times->update_ms = 0.0f;
+            times->gather_ms = elapsed(ctx->ev[0], ctx->ev[3]);  // unpack
         }
     });
 }

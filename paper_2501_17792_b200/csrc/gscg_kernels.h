@@ -7,6 +7,7 @@ namespace gscg {
 
 struct PlanParams {
     uint32_t n;
+    uint32_t shard_begin, shard_end;  // instances projected by this context (all: 0, n)
     const uint32_t* template_ids;
     const float* placement;
     const uint32_t* lod_prev;
@@ -29,7 +30,8 @@ struct PlanParams {
 };
 
 struct FkParams {
-    uint32_t n;
+    uint32_t n;      // end of the launch's instance range (bounds check)
+    uint32_t first;  // first instance of the launch (shard begin)
     uint32_t joint_stride;
     uint32_t pose_stride;
     const uint32_t* template_ids;
@@ -73,6 +75,8 @@ struct RasterParams {
     const uint32_t* recs;  // record index of every cell-sorted pair
     const float4* records;
     int32_t width, height, tile_size, tiles_x;
+    int32_t tile_row0;  // first tile row of the launch (screen band), 0 for a full frame
+    int32_t out_row0;   // screen row stored in row 0 of out_rgb / out_T
     float bg[3];
     float alpha_max;
     float t_floor;
@@ -121,6 +125,38 @@ __global__ void k_emit_pairs(const uint32_t* rec_sorted, uint32_t count, const u
                              uint32_t* pair_rec);
 __global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges);
 constexpr int kStreamItems = 8;  // elements per thread in the streaming sort kernels
+
+// screen-band exchange (multi-GPU frame)
+constexpr int kMaxBands = GSCG_MAX_BANDS;
+
+struct BandParams {
+    const float4* records;
+    const uint32_t* ordinal;
+    const uint32_t* depth;
+    uint32_t count;
+    uint32_t bands;
+    uint32_t rows[kMaxBands + 1];  // band b = screen rows [rows[b], rows[b+1])
+    unsigned long long* band_counts;  // count pass
+    unsigned long long* band_cursor;  // pack pass (zeroed)
+    unsigned long long band_offsets[kMaxBands];
+    uint4* packed;  // 4 x uint4 per BandSplat: r0, r1, r2, (ordinal, depth, 0, 0)
+};
+
+struct BandUnpackParams {
+    const uint4* packed;
+    uint32_t count;
+    int32_t row_begin, row_end;  // the band's screen rows
+    int32_t cell;                // binning cell edge in pixels
+    float4* records;
+    uint32_t* ordinal;
+    uint32_t* depth;
+    uint2* span;
+    FrameCounters* counters;
+};
+
+__global__ void k_band_count(BandParams p);
+__global__ void k_band_pack(BandParams p);
+__global__ void k_band_unpack(BandUnpackParams p);
 
 // raster
 // Picks the tile-size specialisation (16: 8x8 quadrant CTAs; else 1/4/16 pixels per thread).

@@ -71,86 +71,6 @@ __device__ __forceinline__ bool blend(const SplatView& s, int px, int py, float&
 
 }  // namespace
 
-// Tile size 16: one pixel per thread; warp w owns the 16x2 strip of rows 2w, 2w+1.
-// Warp-level culling: for every 32 staged splats each lane tests one splat's rectangle
-// against the warp's strip and a ballot yields the splats the warp must walk, in list
-// order; splats that miss the strip (most of them: crowd splats are a few pixels wide)
-// cost the warp 1/32 of a rectangle test instead of a full per-pixel pass.
-__global__ void __launch_bounds__(256)
-k_raster16(RasterParams p) {
-    __shared__ float4 s_geo[256];    // mx, my, a, b
-    __shared__ float4 s_col[256];    // c, opacity, power_floor, red
-    __shared__ float2 s_col2[256];   // green, blue
-    __shared__ uint2 s_rect[256];    // x0 | y0 << 16, x1 | y1 << 16
-    const int tile = blockIdx.x;
-    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int px = tx * 16 + (lane & 15);
-    const int py = ty * 16 + warp * 2 + (lane >> 4);
-    const int sx0 = tx * 16, sy0 = ty * 16 + warp * 2;  // warp strip origin
-    const bool inside = px < p.width && py < p.height;
-    const uint2 range = p.ranges[tile];
-    const float fx = static_cast<float>(px) + 0.5f, fy = static_cast<float>(py) + 0.5f;
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-    bool done = !inside;
-    for (uint32_t start = range.x; start < range.y; start += 256) {
-        if (__syncthreads_count(done) == 256) break;
-        const uint32_t i = start + threadIdx.x;
-        if (i < range.y) {
-            const float4* src = p.records + 3ull * p.recs[i];
-            const float4 r0 = src[0], r1 = src[1], r2 = src[2];
-            s_geo[threadIdx.x] = r0;
-            s_col[threadIdx.x] = r1;
-            s_col2[threadIdx.x] = make_float2(r2.x, r2.y);
-            s_rect[threadIdx.x] = make_uint2(__float_as_uint(r2.z), __float_as_uint(r2.w));
-        }
-        __syncthreads();
-        const int n = min(256u, range.y - start);
-        if (__all_sync(0xffffffffu, done)) continue;
-        for (int base = 0; base < n; base += 32) {
-            bool hit = false;
-            if (base + lane < n) {
-                const uint2 r = s_rect[base + lane];
-                const int x0 = r.x & 0xffff, y0 = r.x >> 16, x1 = r.y & 0xffff, y1 = r.y >> 16;
-                hit = x0 < sx0 + 16 && x1 > sx0 && y0 < sy0 + 2 && y1 > sy0;
-            }
-            uint32_t mask = __ballot_sync(0xffffffffu, hit);
-            while (mask) {
-                const int k = base + __ffs(mask) - 1;
-                mask &= mask - 1;
-                if (done) continue;
-                const uint2 r = s_rect[k];
-                if (px < static_cast<int>(r.x & 0xffff) || px >= static_cast<int>(r.y & 0xffff) ||
-                    py < static_cast<int>(r.x >> 16) || py >= static_cast<int>(r.y >> 16))
-                    continue;
-                const float4 g = s_geo[k];
-                const float dx = __fsub_rn(fx, g.x);
-                const float dy = __fsub_rn(fy, g.y);
-                const float4 c = s_col[k];
-                const float q = __fadd_rn(__fmul_rn(__fmul_rn(g.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
-                const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(g.w, dx), dy));
-                if (power < c.z) continue;
-                const float alpha = fminf(c.y * __expf(power), p.alpha_max);
-                const float w = T * alpha;
-                const float2 c2 = s_col2[k];
-                cr = fmaf(w, c.w, cr);
-                cg = fmaf(w, c2.x, cg);
-                cb = fmaf(w, c2.y, cb);
-                T = T * (1.0f - alpha);
-                done = T < p.t_floor;
-            }
-            if (__all_sync(0xffffffffu, done)) break;
-        }
-    }
-    if (inside) {
-        const size_t o = static_cast<size_t>(py) * p.width + px;
-        p.out_rgb[3 * o + 0] = cr + T * p.bg[0];
-        p.out_rgb[3 * o + 1] = cg + T * p.bg[1];
-        p.out_rgb[3 * o + 2] = cb + T * p.bg[2];
-        p.out_T[o] = T;
-    }
-}
-
 // Tile size 16, quadrant form: one 64-thread CTA per 8x8 quadrant of a tile (grid =
 // 4 x tiles). Crowd frames are extremely skewed — horizon tiles carry tens of thousands
 // of pairs and mix saturated crowd pixels with never-saturating sky — so splitting a tile
@@ -165,7 +85,7 @@ k_raster16q(RasterParams p) {
     __shared__ float2 s_col2[64];
     __shared__ uint2 s_rect[64];
     const int tile = blockIdx.x >> 2, quad = blockIdx.x & 3;
-    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bx0 = tx * 16 + (quad & 1) * 8;
     const int by0 = ty * 16 + (quad >> 1) * 8 + warp * 4;  // warp block origin (8 x 4)
@@ -245,7 +165,7 @@ k_raster16q(RasterParams p) {
         }
     }
     if (inside) {
-        const size_t o = static_cast<size_t>(py) * p.width + px;
+        const size_t o = static_cast<size_t>(py - p.out_row0) * p.width + px;
         p.out_rgb[3 * o + 0] = cr + T * p.bg[0];
         p.out_rgb[3 * o + 1] = cg + T * p.bg[1];
         p.out_rgb[3 * o + 2] = cb + T * p.bg[2];
@@ -260,7 +180,7 @@ k_raster_generic(RasterParams p) {
     __shared__ float4 s_rec[256 * 3];
     const int ts = p.tile_size;
     const int tile = blockIdx.x;
-    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
     float T[PPT], cr[PPT], cg[PPT], cb[PPT];
     int pxs[PPT], pys[PPT];
     bool live[PPT];
@@ -304,7 +224,7 @@ k_raster_generic(RasterParams p) {
     for (int k = 0; k < PPT; ++k) {
         const int lp = threadIdx.x + k * 256;
         if (lp < ts * ts && pxs[k] < p.width && pys[k] < p.height) {
-            const size_t o = static_cast<size_t>(pys[k]) * p.width + pxs[k];
+            const size_t o = static_cast<size_t>(pys[k] - p.out_row0) * p.width + pxs[k];
             p.out_rgb[3 * o + 0] = cr[k] + T[k] * p.bg[0];
             p.out_rgb[3 * o + 1] = cg[k] + T[k] * p.bg[1];
             p.out_rgb[3 * o + 2] = cb[k] + T[k] * p.bg[2];

@@ -108,7 +108,9 @@ k_lod_plan(PlanParams p) {
             p.lod_out[i] = lod;
             p.inst_group[i] = g;
             count = p.groups[g].count;
-            atomicAdd(&s_gcount[g], 1u);
+            // Every rank numbers the whole crowd (ordinals are global); only its own
+            // instance shard is projected.
+            if (i >= p.shard_begin && i < p.shard_end) atomicAdd(&s_gcount[g], 1u);
         }
         unsigned long long total;
         const unsigned long long excl =
@@ -151,7 +153,7 @@ k_lod_plan(PlanParams p) {
         for (int k = tid; k < 32 * kMaxGroups; k += blockDim.x) (&s_wcount[0][0])[k] = 0u;
         __syncthreads();
         const uint32_t i = tile + tid;
-        const bool valid = i < p.n;
+        const bool valid = i < p.n && i >= p.shard_begin && i < p.shard_end;
         const uint32_t g = valid ? p.inst_group[i] : 0xffffffffu;
         const uint32_t peers = __match_any_sync(0xffffffffu, g);
         const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
@@ -213,7 +215,7 @@ k_fk_skin(FkParams p) {
     const int half = threadIdx.x >> 4;        // half-warp within the block
     const int l = threadIdx.x & 15;           // matrix element, column-major
     const int r = l & 3, c = l >> 2;
-    const uint32_t inst = blockIdx.x * (blockDim.x >> 4) + half;
+    const uint32_t inst = p.first + blockIdx.x * (blockDim.x >> 4) + half;
     const unsigned hmask = 0xffffu << ((threadIdx.x & 31) & 16);
     if (inst >= p.n) return;
     float* world = s_world + static_cast<size_t>(half) * p.joint_stride * 16;

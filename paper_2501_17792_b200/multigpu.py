@@ -1,0 +1,325 @@
+"""Multi-GPU crowd frame: instance shards -> screen bands.
+
+The reference renders a frame in one process (renderer.cpp:249-280). Its per-instance
+stages (skinning, projection: crowd.cpp:89, renderer.cpp:35) and its per-tile stage
+(rasterisation: renderer.cpp:170) are independent. The only coupling is the
+splat -> tile routing (renderer.cpp:143-161), so P GPUs split a frame as follows.
+Rank r of P:
+  1. projects the contiguous instance shard r. LoD and ordinals cover the whole crowd,
+     so every rank numbers splats identically (gscg_project_shard).
+  2. routes each surviving splat to every screen band its rect overlaps and packs the
+     routed splats band-major, 64 B each (gscg_pack_bands).
+  3. exchanges splats in one all-to-all: NCCL over NVLink, ordered on the context
+     stream, after a P-int count all-to-all.
+  4. sorts its band's splats by the reference's total order (depth, instance, gaussian)
+     and rasterises band r (gscg_render_band).
+  5. sends its band to rank 0.
+Band pixels equal the same rows of the 1-GPU frame, so the image is byte-identical for
+every P (tests/test_multigpu.py).
+
+`TorchExchange` is the collective layer (NCCL on CUDA tensors, gloo on CPU tensors for the
+host tests). `render_frame_virtual` drives P ranks of one process on one GPU in
+sequence: every rank finishes each phase before the next rank starts, so no kernel ever
+waits on another rank. That is how the band path is checked on a single GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import native as N
+
+BAND_SPLAT_BYTES = N.GSCG_BAND_SPLAT_BYTES
+
+
+# ---------------------------------------------------------------------------------------
+# partition arithmetic (host)
+
+
+def shard_ranges(n: int, parts: int, weights: Optional[Sequence[float]] = None) -> list[tuple[int, int]]:
+    """Contiguous instance ranges [begin, end), one per rank, balanced by `weights` (e.g.
+    each instance's Gaussian count at its active LoD) or by count."""
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    if weights is None:
+        return [(n * r // parts, n * (r + 1) // parts) for r in range(parts)]
+    w = np.asarray(weights, dtype=np.float64)
+    if len(w) != n:
+        raise ValueError("one weight per instance")
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, parts):
+        cuts.append(max(cuts[-1], int(np.searchsorted(cum, total * r / parts, side="left"))))
+    cuts.append(n)
+    cuts = [min(c, n) for c in cuts]
+    return [(cuts[r], cuts[r + 1]) for r in range(parts)]
+
+
+def band_rows(height: int, tile: int, parts: int, row_weights: Optional[Sequence[float]] = None) -> list[int]:
+    """Screen-band boundaries: parts + 1 rows, each band starting on a tile row.
+
+    Without weights the tile rows are split evenly. With one weight per tile row (the
+    previous frame's pairs per tile row), the cumulative weight is split evenly instead.
+    Bands may be empty when parts exceeds the tile-row count."""
+    if parts < 1 or tile < 1 or height < 1:
+        raise ValueError("parts, tile and height must be >= 1")
+    trows = (height + tile - 1) // tile
+    if row_weights is None:
+        cuts = [trows * b // parts for b in range(parts + 1)]
+    else:
+        w = np.asarray(row_weights, dtype=np.float64)
+        if len(w) != trows:
+            raise ValueError("one weight per tile row")
+        cum = np.concatenate([[0.0], np.cumsum(w)])
+        cuts = [0]
+        for b in range(1, parts):
+            c = int(np.searchsorted(cum, cum[-1] * b / parts, side="left"))
+            cuts.append(min(max(c, cuts[-1]), trows))
+        cuts.append(trows)
+    return [min(c * tile, height) for c in cuts]
+
+
+def route_counts(rects_y: np.ndarray, rows: Sequence[int]) -> np.ndarray:
+    """Splats per band for pixel-row intervals [y0, y1) (host restatement of k_band_count,
+    used by the exchange tests)."""
+    rows = np.asarray(rows)
+    y0, y1 = rects_y[:, 0], rects_y[:, 1]
+    return np.array([int(np.count_nonzero((y0 < rows[b + 1]) & (y1 > rows[b]) & (y1 > y0)))
+                     for b in range(len(rows) - 1)], dtype=np.int64)
+
+
+# ---------------------------------------------------------------------------------------
+# collectives
+
+
+class TorchExchange:
+    """The band exchange over torch.distributed: NCCL for CUDA tensors, gloo for CPU tensors."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_to_all(self, send, send_counts: Sequence[int], unit: int = BAND_SPLAT_BYTES):
+        """send: 1-D uint8 tensor, band-major chunks of send_counts[b] * unit bytes.
+        Returns (recv, recv_counts); recv holds the chunks of ranks 0..P-1 in order."""
+        import torch
+
+        dev = send.device
+        sc = torch.tensor([int(c) for c in send_counts], dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = [int(x) for x in rc.cpu().tolist()]
+        recv = torch.empty(sum(recv_counts) * unit, dtype=torch.uint8, device=dev)
+        self.dist.all_to_all_single(recv, send, [c * unit for c in recv_counts],
+                                    [int(c) * unit for c in send_counts], group=self.group)
+        return recv, recv_counts
+
+    def gather_rows(self, band, rows: Sequence[int]):
+        """Gathers every rank's band (rows[r+1] - rows[r] leading rows) into the full
+        frame on rank 0 (None elsewhere). Bands are padded to the tallest band."""
+        import torch
+
+        heights = [rows[r + 1] - rows[r] for r in range(self.world)]
+        hmax = max(max(heights), 1)
+        pad = torch.zeros((hmax,) + tuple(band.shape[1:]), dtype=band.dtype, device=band.device)
+        pad[: band.shape[0]] = band
+        if self.dist.get_backend(self.group) == "nccl":
+            out = [torch.empty_like(pad) for _ in range(self.world)]
+            self.dist.all_gather(out, pad, group=self.group)
+        else:
+            out = [torch.empty_like(pad) for _ in range(self.world)] if self.rank == 0 else None
+            self.dist.gather(pad, out, dst=0, group=self.group)
+        if self.rank != 0:
+            return None
+        return torch.cat([out[r][: heights[r]] for r in range(self.world)], dim=0)
+
+
+# ---------------------------------------------------------------------------------------
+# one rank's share of a frame
+
+
+@dataclass
+class FrameArgs:
+    time_s: float
+    static_pose: bool = False
+    forced_lod: Optional[int] = None
+
+
+class BandRank:
+    """A rank's gscg context: projects an instance shard, packs routed splats, renders a band."""
+
+    def __init__(self, scene, device: int = 0, renderer=None):
+        import paper_2501_17792_b200 as P
+
+        self.scene = scene
+        self.renderer = renderer or P.Renderer(scene, device=device)
+        self.device = device
+        self.ctx = self.renderer.gpu
+        self.lib = N.gscg()
+        n = scene.counts()[2]
+        self.lods = np.full(max(n, 1), 0xFFFFFFFF, dtype=np.uint32)
+        self.counts = None
+        self.band_times = N.GscgStageTimes()
+        self.shard_times = N.GscgStageTimes()
+
+    def _check(self, rc):
+        N.check_gscg(rc, self.ctx)
+
+    def stream(self):
+        import torch
+
+        s = C.c_void_p()
+        self._check(self.lib.gscg_stream(self.ctx, C.byref(s)))
+        return torch.cuda.ExternalStream(s.value, device=torch.device("cuda", self.device))
+
+    def project(self, fa: FrameArgs, settings, shard: tuple[int, int], rows: Sequence[int]) -> np.ndarray:
+        cfg = self.scene.cfg
+        n = self.scene.counts()[2]
+        tids, place, poses = self.renderer.sample_crowd(fa.time_s, fa.static_pose)
+        self._keep = (tids, place, poses)
+        fd = N.GscgFrameDesc()
+        fd.instance_count = n
+        fd.joint_stride = self.renderer.joint_stride
+        fd.template_ids = tids.ctypes.data
+        fd.placement = place.ctypes.data
+        fd.poses = poses.ctypes.data
+        fd.active_lod = self.lods.ctypes.data
+        fd.forced_lod = -1 if fa.forced_lod is None else int(fa.forced_lod)
+        fd.memory = N.GSCG_MEM_HOST
+        cam = self.scene.camera_basis()
+        rs = gscg_settings(settings)
+        lp = N.GscgLodPolicy()
+        lp.threshold_count = len(cfg.lod_thresholds)
+        for i, v in enumerate(cfg.lod_thresholds):
+            lp.thresholds_m[i] = v
+        lp.hysteresis_band_m = cfg.lod_hysteresis
+        bands = len(rows) - 1
+        rows_arr = (C.c_uint32 * (bands + 1))(*[int(r) for r in rows])
+        counts = np.zeros(bands, dtype=np.uint64)
+        self._check(self.lib.gscg_project_shard(self.ctx, C.byref(fd), C.byref(cam), C.byref(rs), C.byref(lp),
+                                                int(shard[0]), int(shard[1]), bands, rows_arr,
+                                                counts.ctypes.data, C.byref(self.shard_times)))
+        self.counts = counts
+        return counts
+
+    def pack(self):
+        """Routed splats in a fresh device buffer (uint8), ordered on the context stream."""
+        import torch
+
+        total = int(self.counts.sum())
+        buf = torch.empty(max(total, 1) * BAND_SPLAT_BYTES, dtype=torch.uint8,
+                          device=torch.device("cuda", self.device))
+        # The allocation belongs to torch's stream; the context stream must not write it early.
+        self.stream().wait_stream(torch.cuda.current_stream(buf.device))
+        self._check(self.lib.gscg_pack_bands(self.ctx, C.c_void_p(buf.data_ptr())))
+        return buf[: total * BAND_SPLAT_BYTES]
+
+    def render_band(self, recv, count: int, row_begin: int, row_end: int):
+        """(rgb, T) device tensors of rows [row_begin, row_end), ordered on the context stream."""
+        import torch
+
+        W = self.scene.cfg.width
+        h = row_end - row_begin
+        dev = torch.device("cuda", self.device)
+        rgb = torch.empty((max(h, 0), W, 3), dtype=torch.float32, device=dev)
+        T = torch.empty((max(h, 0), W), dtype=torch.float32, device=dev)
+        self.stream().wait_stream(torch.cuda.current_stream(dev))
+        ptr = C.c_void_p(recv.data_ptr()) if count else None
+        self._check(self.lib.gscg_render_band(self.ctx, ptr, int(count), int(row_begin), int(row_end),
+                                              C.c_void_p(rgb.data_ptr()), C.c_void_p(T.data_ptr()),
+                                              N.GSCG_MEM_DEVICE, C.byref(self.band_times)))
+        return rgb, T
+
+
+def gscg_settings(settings) -> N.GscgRenderSettings:
+    rs = N.GscgRenderSettings()
+    rs.tile_size = settings.tile_size
+    for i in range(3):
+        rs.background[i] = settings.background[i]
+    rs.alpha_max = settings.alpha_max
+    rs.alpha_cutoff = settings.alpha_cutoff
+    rs.transmittance_floor = settings.transmittance_floor
+    rs.sh_enabled = int(bool(settings.sh_colour))
+    return rs
+
+
+# ---------------------------------------------------------------------------------------
+# drivers
+
+
+class DistributedRenderer:
+    """One rank of a P-GPU frame (torch.distributed initialised with NCCL, one process per GPU)."""
+
+    def __init__(self, scene, device: int, exchange: Optional[TorchExchange] = None):
+        self.exchange = exchange or TorchExchange()
+        self.rank, self.world = self.exchange.rank, self.exchange.world
+        self.band = BandRank(scene, device=device)
+        self.scene = scene
+        self.rows: Optional[list[int]] = None
+
+    def render_frame(self, time_s: float, settings=None, static_pose: bool = False,
+                     forced_lod: Optional[int] = None, rows: Optional[Sequence[int]] = None):
+        """Returns (rgb, T) numpy on rank 0, None on the other ranks."""
+        import torch
+        import paper_2501_17792_b200 as P
+
+        settings = settings or P.RenderSettings()
+        cfg = self.scene.cfg
+        n = self.scene.counts()[2]
+        rows = list(rows) if rows is not None else band_rows(cfg.height, settings.tile_size, self.world)
+        shard = shard_ranges(n, self.world)[self.rank]
+        fa = FrameArgs(time_s, static_pose, forced_lod)
+        self.band.project(fa, settings, shard, rows)
+        send = self.band.pack()
+        with torch.cuda.stream(self.band.stream()):
+            recv, rc = self.exchange.all_to_all(send, self.band.counts.tolist())
+            rgb, T = self.band.render_band(recv, sum(rc), rows[self.rank], rows[self.rank + 1])
+            full = self.exchange.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
+        if full is None:
+            return None
+        full = full.cpu().numpy()
+        return np.ascontiguousarray(full[..., :3]), np.ascontiguousarray(full[..., 3])
+
+
+def render_frame_virtual(ranks: list[BandRank], time_s: float, settings=None, static_pose: bool = False,
+                         forced_lod: Optional[int] = None, rows: Optional[Sequence[int]] = None,
+                         shards: Optional[list[tuple[int, int]]] = None):
+    """P virtual ranks in one process, phase by phase. The exchange is a device-side
+    concatenation in source-rank order, the chunk layout an all-to-all delivers."""
+    import torch
+    import paper_2501_17792_b200 as P
+
+    settings = settings or P.RenderSettings()
+    world = len(ranks)
+    scene = ranks[0].scene
+    cfg = scene.cfg
+    n = scene.counts()[2]
+    rows = list(rows) if rows is not None else band_rows(cfg.height, settings.tile_size, world)
+    shards = shards or shard_ranges(n, world)
+    fa = FrameArgs(time_s, static_pose, forced_lod)
+    sends = []
+    for r, br in enumerate(ranks):
+        br.project(fa, settings, shards[r], rows)
+        sends.append(br.pack())
+    torch.cuda.synchronize()
+    offs = [np.concatenate([[0], np.cumsum(br.counts.astype(np.int64))]) for br in ranks]
+    bands_rgb, bands_T = [], []
+    for d, br in enumerate(ranks):
+        chunks = [sends[s][offs[s][d] * BAND_SPLAT_BYTES: offs[s][d + 1] * BAND_SPLAT_BYTES] for s in range(world)]
+        recv = torch.cat(chunks) if chunks else torch.empty(0, dtype=torch.uint8, device="cuda")
+        count = sum(int(ranks[s].counts[d]) for s in range(world))
+        rgb, T = br.render_band(recv, count, rows[d], rows[d + 1])
+        torch.cuda.synchronize()
+        bands_rgb.append(rgb)
+        bands_T.append(T)
+    rgb = torch.cat(bands_rgb).cpu().numpy()
+    T = torch.cat(bands_T).cpu().numpy()
+    return rgb, T

@@ -23,6 +23,8 @@ GSCG_MEM_HOST = 0
 GSCG_MEM_DEVICE = 1
 GSCG_DEBUG_POSED = 1
 GSCG_DEBUG_RECORDS = 2
+GSCG_MAX_BANDS = 64
+GSCG_BAND_SPLAT_BYTES = 64
 MAX_LOD_THRESHOLDS = 8
 
 
@@ -129,6 +131,12 @@ GSCG_SYMBOLS = {
     "gscg_get_cell_layout": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "gscg_get_tile_ranges": (C.c_int, [_P, _P, C.c_uint32]),
     "gscg_get_sorted_ordinals": (C.c_int, [_P, _P, C.c_uint64]),
+    "gscg_project_shard": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
+                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), C.c_uint32,
+                                     C.c_uint32, C.c_uint32, _P, _P, C.POINTER(GscgStageTimes)]),
+    "gscg_pack_bands": (C.c_int, [_P, _P]),
+    "gscg_render_band": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, C.c_uint32, _P, _P, C.c_int32,
+                                   C.POINTER(GscgStageTimes)]),
 }
 
 GSCH_SYMBOLS = {

@@ -1,0 +1,74 @@
+"""Regenerates tests/golden/*.npz: small crowd frames rendered by the CPU oracle.
+
+The reference ships no golden images and cannot be built here, so
+these fixtures freeze the oracle's output once it has passed the reference's own
+known-answer and property tests (tests/test_oracle.py, tests/test_host.py). They pin
+the host generator + oracle against drift (tests/test_golden.py, CPU) and give the
+GPU path a fixed target that does not need the oracle at run time (-m gpu).
+
+Run from the repo root after building:  python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+
+# (name, SceneConfig kwargs, render kwargs)
+CASES = [
+    ("crowd6_sh_t16",
+     dict(template_count=2, template_seed_base=100, level_counts=(1500, 400, 100), with_sh=True,
+          motion_count=2, motion_frames=60, grid_rows=2, grid_cols=3, crowd_count=6, crowd_seed=11,
+          cam_pos=(1.0, 1.4, -2.5), cam_look=(1.0, 1.0, 3.0), width=160, height=120,
+          lod_thresholds=(3.0, 4.5)),
+     dict(time_s=0.41, tile_size=16, background=(0.05, 0.1, 0.2), sh=True)),
+    ("crowd4_rgb_t8_static",
+     dict(template_count=1, template_seed_base=300, level_counts=(1200, 300), with_sh=False,
+          motion_count=1, motion_frames=30, grid_rows=2, grid_cols=2, crowd_count=4, crowd_seed=5,
+          cam_pos=(0.5, 1.2, -2.0), cam_look=(0.5, 0.9, 2.0), width=96, height=80,
+          lod_thresholds=(3.0,)),
+     dict(time_s=0.0, tile_size=8, background=(0.0, 0.0, 0.0), sh=False, static_pose=True)),
+]
+
+
+def render_case(cfg_kw: dict, r_kw: dict):
+    import paper_2501_17792_b200 as P
+    from oracle import orc
+
+    scene = P.Scene(P.SceneConfig(**cfg_kw))
+    o = orc.from_scene(scene)
+    st = orc.settings(tile_size=r_kw["tile_size"], background=r_kw["background"], sh_colour=r_kw["sh"])
+    rgb, T, times = o.render(r_kw["time_s"], st, r_kw.get("static_pose", False), r_kw.get("forced_lod"))
+    n = scene.counts()[2]
+    lods = o.lods(n)
+    sp = o.splats()
+    ts = r_kw["tile_size"]
+    tiles = ((cfg_kw["width"] + ts - 1) // ts) * ((cfg_kw["height"] + ts - 1) // ts)
+    counts, items = o.bins(tiles)
+    return dict(
+        rgb=rgb, T=T, lods=lods,
+        counts=np.array([times.gaussian_count, times.splat_count, times.pair_count], dtype=np.uint64),
+        splats=sp, posed=o.posed(), bin_counts=counts, bin_items=items,
+    )
+
+
+def main() -> None:
+    from paper_2501_17792_b200.build import build, build_oracle
+    build()
+    build_oracle()
+    out = Path(__file__).resolve().parent
+    for name, cfg_kw, r_kw in CASES:
+        arrays = render_case(cfg_kw, r_kw)
+        meta = json.dumps(dict(config=cfg_kw, render=r_kw))
+        np.savez_compressed(out / f"{name}.npz", meta=np.array(meta), **arrays)
+        c = arrays["counts"]
+        print(f"{name}: G={c[0]} S={c[1]} K={c[2]} -> {name}.npz")
+
+
+if __name__ == "__main__":
+    main()
