@@ -8,9 +8,10 @@ distinct animation time t = f/30 s. `value` times K steps with every input alrea
 (poses sampled and uploaded before the timed region) using CUDA events on the render
 stream; `e2e` times the public API (host pose sampling, pinned H2D, kernels, D2H of the
 framebuffer) per step. `--impl reference` times the CPU oracle (the reference's render
-path restated in C++, reference/oracle "port") on the host cores. Multi-GPU runs split the
-instances across ranks (each rank renders its shard's frame; no data-path collective yet,
-see DESIGN.md "Multi-GPU"), timing max over ranks.
+path restated in C++, oracle "port") on the host cores. Multi-GPU runs render the same frame
+on N GPUs (strong scaling): each rank projects an instance shard, splats are exchanged
+by screen band with one NCCL all-to-all, each rank sorts and rasterises its band and the
+bands are gathered; timing is the max over ranks.
 """
 from __future__ import annotations
 
@@ -42,83 +43,124 @@ def _peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled every 2 ms during the timed
+    region through NVML (nvidia-smi's source); falls back to nvidia-smi -lms 100."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_s: float = 0.002):
         self.device = device
-        self.proc = None
-        self.lines: list[str] = []
+        self.period = period_s
+        self.sm: list[float] = []
+        self.mask = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self._smi = None
+
+    def _nvml_index(self) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if self.device < len(ids) and ids[self.device].isdigit():
+                return int(ids[self.device])
+        return self.device
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        self.mask |= int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=poll, daemon=True)
             self._t.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:
+            self._start_smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _start_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.hw_power_brake_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        try:
+            self._smi = subprocess.Popen(["nvidia-smi", "-i", str(self._nvml_index()), f"--query-gpu={fields}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self._smi = None
+            return
+        names = list(self.REASONS)
+
+        def read():
+            for line in self._smi.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.max_mhz = max(self.max_mhz or 0.0, float(parts[1]))
+                except (ValueError, IndexError):
+                    continue
+                for name, v in zip(names, parts[2:7]):
+                    if v.lower() == "active":
+                        self.mask |= self.REASONS[name]
+
+        self._t = threading.Thread(target=read, daemon=True)
+        self._t.start()
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
+        self._stop.set()
+        if self._smi:
+            self._smi.terminate()
             try:
-                self.proc.wait(timeout=5)
+                self._smi.wait(timeout=5)
             except subprocess.TimeoutExpired:
-                self.proc.kill()
+                self._smi.kill()
+        if self._t:
             self._t.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = sorted(n for n, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.sm)}
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
 
 
 def dist_env() -> tuple[int, int, int]:
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def build_scene(config: int, rank: int, world: int):
+def build_scene(config: int):
     import paper_2501_17792_b200 as P
 
     cfg, extra = P.baseline_config(config)
     scene = P.Scene(cfg)
     if extra["origin_instance"]:
         P.place_origin_instance(scene)
-    if world > 1:
-        inst = scene.instances
-        lo = len(inst) * rank // world
-        hi = len(inst) * (rank + 1) // world
-        scene.instances = inst[lo:hi]
     return P, cfg, extra, scene
 
 
 def roofline_bytes(cfg, counts, lods, scene, sh: bool) -> dict:
-    """Algorithmic bytes (SURVEY.md §8d / DESIGN.md) for the frame and its two big kernels."""
+    """Algorithmic bytes (SURVEY.md §8d / DESIGN.md §4) for the frame and its big kernels."""
     G, S, K = counts
-    a = 256 if sh else 76
+    a = 260 if sh else 80  # core 64 + skin weights 16 (+ SH 180) per resident template Gaussian
     inst = scene.instances
     resident = set(zip(inst["template_id"].tolist(), lods.tolist()))
     A = sum(cfg.level_counts[l] for _, l in resident) * a
@@ -129,8 +171,8 @@ def roofline_bytes(cfg, counts, lods, scene, sh: bool) -> dict:
     tiles = ((W + 15) // 16) * ((H + 15) // 16)
     P = 6
     frame = A + M + 2 * S * R + K * (12 + 24 * P + 4) + 16 * W * H
-    project = A + M + S * (R + 4) + K * 12          # template stream + matrices + records/ordinals + pairs
-    raster = K * (4 + R) + 16 * W * H + tiles * 8  # sorted values + record gathers + framebuffer
+    project = A + M + S * (R + 4 + 4 + 8)           # template stream + matrices + record, ordinal, depth, span
+    raster = K * (4 + R) + 16 * W * H + tiles * 4 * 8  # sorted pair records + record gathers + framebuffer + ranges
     return {"frame": frame, "project": project, "raster": raster, "A": A, "M": M}
 
 
@@ -138,11 +180,18 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     import torch
 
     torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     dist = None
-    if world > 1:
+    band_path = world > 1 or args.band_path
+    if band_path:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    P, cfg, extra, scene = build_scene(args.config, rank, world)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        dist.init_process_group("nccl", device_id=dev)
+    P, cfg, extra, scene = build_scene(args.config)
     from paper_2501_17792_b200 import native as N
 
     r = P.Renderer(scene, device=local_rank)
@@ -157,16 +206,13 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     # ---- device-resident inputs: sample all poses on the host up front, upload once ----
     tids, place, _ = r.sample_crowd(times_s[0])
     poses_host = np.stack([r.sample_crowd(t)[2] for t in times_s])
-    dev = torch.device("cuda", local_rank)
     d_tids = torch.from_numpy(tids.view(np.int32)).to(dev)
     d_place = torch.from_numpy(place).to(dev)
     d_poses = torch.from_numpy(poses_host).to(dev)
     d_lods = torch.full((max(n, 1),), -1, dtype=torch.int32, device=dev)
     cam = scene.camera_basis()
-    rs = N.GscgRenderSettings()
-    rs.tile_size = settings.tile_size
-    rs.alpha_max, rs.alpha_cutoff, rs.transmittance_floor = settings.alpha_max, settings.alpha_cutoff, settings.transmittance_floor
-    rs.sh_enabled = 1
+    from paper_2501_17792_b200.multigpu import gscg_settings
+    rs = gscg_settings(settings)
     lp = N.GscgLodPolicy()
     lp.threshold_count = len(cfg.lod_thresholds)
     for i, v in enumerate(cfg.lod_thresholds):
@@ -178,7 +224,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     N.check_gscg(lib.gscg_stream(ctx, C.byref(stream_ptr)), ctx)
     stream = torch.cuda.ExternalStream(stream_ptr.value, device=dev)
 
-    def frame(f: int, st: N.GscgStageTimes):
+    def frame_desc(f: int) -> N.GscgFrameDesc:
         fd = N.GscgFrameDesc()
         fd.instance_count = n
         fd.joint_stride = js
@@ -188,48 +234,81 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         fd.active_lod = d_lods.data_ptr()
         fd.forced_lod = -1 if forced is None else forced
         fd.memory = N.GSCG_MEM_DEVICE
-        N.check_gscg(lib.gscg_render_frame(ctx, C.byref(fd), C.byref(cam), C.byref(rs), C.byref(lp), None, None,
-                                           C.byref(st)), ctx)
+        return fd
 
-    stage = []
+    if not band_path:
+        def frame(f: int) -> dict:
+            st = N.GscgStageTimes()
+            N.check_gscg(lib.gscg_render_frame(ctx, C.byref(frame_desc(f)), C.byref(cam), C.byref(rs), C.byref(lp),
+                                               None, None, C.byref(st)), ctx)
+            return {"update": st.update_ms, "gather": st.gather_ms, "sort": st.sort_ms, "rasterize": st.rasterize_ms,
+                    "launches": st.kernel_launches, "counts": (st.gaussian_count, st.splat_count, st.pair_count)}
+    else:
+        # Band path: shard projection -> NCCL all-to-all -> band render -> gather.
+        from paper_2501_17792_b200.multigpu import BandRank, FrameArgs, TorchExchange, band_rows, shard_ranges
+        ex = TorchExchange()
+        br = BandRank(scene, device=local_rank, renderer=r)
+        rows = band_rows(cfg.height, settings.tile_size, world)
+        shard = shard_ranges(n, world)[rank]
+
+        def frame(f: int) -> dict:
+            br.project(FrameArgs(times_s[f], False, forced), settings, shard, rows, frame=frame_desc(f))
+            send = br.pack()
+            with torch.cuda.stream(stream):
+                recv, rc = ex.all_to_all(send, br.counts.tolist())
+                rgb, T = br.render_band(recv, sum(rc), rows[rank], rows[rank + 1])
+                ex.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
+            a, b = br.shard_times, br.band_times
+            return {"update": a.update_ms, "gather": a.gather_ms, "route": a.sort_ms, "unpack": b.gather_ms,
+                    "sort": b.sort_ms, "rasterize": b.rasterize_ms,
+                    "launches": a.kernel_launches + 1 + b.kernel_launches,
+                    "counts": (a.gaussian_count, a.splat_count, b.pair_count)}
+
     for f in range(args.warmup):
-        st = N.GscgStageTimes()
-        frame(f, st)
+        frame(f)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
+    stage = []
     with ClockSampler(local_rank) as clocks:
         ev0.record(stream)
         for f in range(args.warmup, frames):
-            st = N.GscgStageTimes()
-            frame(f, st)
-            stage.append(st)
-            launches += st.kernel_launches
+            stage.append(frame(f))
         ev1.record(stream)
         torch.cuda.synchronize()
-    ms_total = ev0.elapsed_time(ev1)
     if dist:
         dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    if dist:
         t = torch.tensor([ms_total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    counts = (stage[-1].gaussian_count, stage[-1].splat_count, stage[-1].pair_count)
+    launches = sum(s["launches"] for s in stage)
+    counts = stage[-1]["counts"]
     lods = d_lods[:n].cpu().numpy().astype(np.uint32)
 
     # ---- end-to-end through the public API (host poses + pinned H2D + kernels + D2H) ----
-    e2e_times = []
+    if not band_path:
+        def e2e_frame(f):
+            r.render_frame(times_s[f], settings, forced_lod=forced)
+    else:
+        from paper_2501_17792_b200.multigpu import DistributedRenderer
+        drr = DistributedRenderer(scene, local_rank, exchange=ex, band=br)
+
+        def e2e_frame(f):
+            drr.render_frame(times_s[f], settings, forced_lod=forced)
     for f in range(min(args.warmup, 2)):
-        r.render_frame(times_s[f], settings, forced_lod=forced)
+        e2e_frame(f)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t_start = time.perf_counter()
     for f in range(args.warmup, frames):
-        r.render_frame(times_s[f], settings, forced_lod=forced)
+        e2e_frame(f)
     e2e_s = time.perf_counter() - t_start
     if dist:
         t = torch.tensor([e2e_s], device=dev)
@@ -240,18 +319,19 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     d2h = cfg.width * cfg.height * 16 + n * 4
 
     if dist:
-        tot = torch.tensor(list(counts), dtype=torch.float64, device=dev)
+        tot = torch.tensor([float(counts[1])], dtype=torch.float64, device=dev)
         dist.all_reduce(tot)
-        counts = tuple(int(x) for x in tot.tolist())
+        counts = (counts[0], int(tot.item()), counts[2])
     if rank != 0:
-        if dist:
-            dist.destroy_process_group()
+        dist.destroy_process_group()
         return None
 
     peaks = _peaks()
-    med = lambda attr: float(np.median([getattr(s, attr) for s in stage]))
-    stage_ms = {k: med(k + "_ms") for k in ("update", "gather", "sort", "rasterize")}
+    keys = [k for k in stage[0] if k not in ("launches", "counts")]
+    stage_ms = {k: float(np.median([s[k] for s in stage])) for k in keys}
     rb = roofline_bytes(cfg, counts, lods, scene, sh=True)
+    # The single longest kernel of the frame: k_project (gather) or k_raster16q (rasterize);
+    # the sort stage is ~35 short launches, none longer than either.
     dom = "rasterize" if stage_ms["rasterize"] >= stage_ms["gather"] else "gather"
     kernel = {"rasterize": "k_raster16q", "gather": "k_project"}[dom]
     kbytes = rb["raster"] if dom == "rasterize" else rb["project"]
@@ -273,8 +353,9 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                                f"{cfg.crowd_count} animated characters, distance LoD 5/10 m, {cfg.width}x{cfg.height}, tile 16",
                    "instances": cfg.crowd_count, "resolution": [cfg.width, cfg.height],
                    "gaussians": counts[0], "splats": counts[1], "pairs": counts[2],
-                   "l2": "per-frame working set (templates ~0.5 GB + records/pairs ~0.8 GB) exceeds the 126 MB L2",
-                   "parallelism": f"instance shards x{world}" if world > 1 else "single GPU"},
+                   "l2": "no flush: the per-frame working set (templates ~0.5 GB + records/pairs ~0.8 GB) exceeds the 126 MB L2",
+                   "parallelism": (f"{world} instance shards -> {world} screen bands, NCCL all-to-all"
+                                   if band_path else "single GPU")},
         "splats_per_s": round(counts[1] * fps, 1),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "frame_roofline": {"bytes": rb["frame"], "ms": round(frame_roofline_ms, 4),
@@ -361,6 +442,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-frames", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--band-path", action="store_true",
+                    help="use the multi-GPU band path (shard -> NCCL all-to-all -> band) even on one GPU")
     ap.add_argument("--reference-budget-s", type=float, default=150.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -537,8 +537,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                 sp.counts = ctx->status.as<uint32_t>();
                 sp.digit_base = ctx->hist.as<uint32_t>();
                 k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
-                k_sort_rows<<<kRadix, 1024, 0, s>>>(sp);
-                k_sort_bases<<<1, kRadix, 0, s>>>(sp);
+                k_sort_rows<<<1u << plan.bits[q], 1024, 0, s>>>(sp);
+                k_sort_bases<<<1, kRadix, 0, s>>>(sp);  // digits beyond 2^bits stay unused
                 k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
                 launches += 4;
                 out ^= 1;
@@ -546,13 +546,17 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             CUDA_TRY(cudaGetLastError());
             return out ^ 1;
         };
+        // ceil(bits / kRadixBits) passes with the bits spread evenly (27 -> 7,7,7,6).
         auto make_plan = [](uint32_t bits) {
             RadixPlan pl{};
             bits = std::max(bits, 1u);
-            for (uint32_t sh = 0; sh < bits; sh += kRadixBits) {
-                pl.shift[pl.passes] = sh;
-                pl.bits[pl.passes] = std::min<uint32_t>(kRadixBits, bits - sh);
-                ++pl.passes;
+            pl.passes = (bits + kRadixBits - 1) / kRadixBits;
+            uint32_t sh = 0;
+            for (uint32_t q = 0; q < pl.passes; ++q) {
+                const uint32_t w = (bits - sh) / (pl.passes - q) + ((bits - sh) % (pl.passes - q) ? 1u : 0u);
+                pl.shift[q] = sh;
+                pl.bits[q] = w;
+                sh += w;
             }
             return pl;
         };

@@ -93,7 +93,7 @@ __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n);
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 16;
-constexpr int kRadixBits = 5;  // digit width of one LSD pass
+constexpr int kRadixBits = 5;  // widest digit of one LSD pass
 constexpr int kRadix = 1 << kRadixBits;
 constexpr uint32_t kSortTile = kSortThreads * kSortItems;
 constexpr uint32_t kMaxSortPasses = 8;

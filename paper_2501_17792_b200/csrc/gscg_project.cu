@@ -48,29 +48,6 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float Y[15])
     Y[14] = (C36 * x) * (xx - 3.0f * yy);
 }
 
-__device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long v,
-                                                             unsigned long long* s_warp,
-                                                             unsigned long long& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    unsigned long long before = 0ull, all = 0ull;
-#pragma unroll
-    for (int w = 0; w < kProjectThreads / 32; ++w) {
-        const unsigned long long t = s_warp[w];
-        if (w < warp) before += t;
-        all += t;
-    }
-    total = all;
-    return before + x - v;
-}
-
 __device__ __forceinline__ void copy_async16(float* smem_dst, const float* gmem_src) {
     const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem_src) : "memory");
@@ -86,7 +63,7 @@ k_project(ProjectParams p) {
     float* s_sh = reinterpret_cast<float*>(s_dyn);
     float* s_mats = s_sh + (p.sh_enabled ? kProjectThreads * kShFloats : 0);
     __shared__ uint32_t s_item_start[kMaxGroups + 1];
-    __shared__ unsigned long long s_warp[kProjectThreads / 32];
+    __shared__ uint32_t s_wcnt[kProjectThreads / 32];
     __shared__ unsigned long long s_base;
     __shared__ uint32_t s_item;
 
@@ -97,7 +74,12 @@ k_project(ProjectParams p) {
     // Binning cell (pairs per splat are counted here; emitted after the depth sort):
     // the tile, or for 16-px tiles each 8x8 quadrant.
     const int cell = p.tile_size == 16 ? 8 : p.tile_size;
+    const int cshift = (cell & (cell - 1)) == 0 ? __ffs(cell) - 1 : -1;
+    auto cdiv = [&](int v) { return cshift >= 0 ? v >> cshift : v / cell; };  // v >= 0
     uint32_t dmin = 0xffffffffu, dmax = 0u;
+    uint32_t pairs = 0;  // binning cells of this thread's splats (summed once at the end)
+    const int lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
 
     for (;;) {
         __syncthreads();
@@ -162,6 +144,7 @@ k_project(ProjectParams p) {
             float mx = 0, my = 0, depth = 0, cxx = 0, cxy = 0, cyy = 0, ca = 0, cb = 0, cc = 0;
             float col0 = 0, col1 = 0, col2 = 0;
             int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+            uint32_t span_lo = 0, span_hi = 0;
             float ax = 0.0f, ay = 0.0f, az = 0.0f;
             if (gvalid) {
                 // Linear blend skinning (avatar.cpp:182-190), accumulator starts at +0.
@@ -231,9 +214,12 @@ k_project(ProjectParams p) {
                         ca = cyy * inv_det;
                         cb = -cxy * inv_det;
                         cc = cxx * inv_det;
-                        const int cx0 = x0 / cell, cx1 = (x1 - 1) / cell;
-                        const int cy0 = y0 / cell, cy1 = (y1 - 1) / cell;
+                        // Binning cells of the rect: first cell, cells across, cells down.
+                        const int cx0 = cdiv(x0), cx1 = cdiv(x1 - 1);
+                        const int cy0 = cdiv(y0), cy1 = cdiv(y1 - 1);
                         n_tiles = static_cast<uint32_t>((cx1 - cx0 + 1) * (cy1 - cy0 + 1));
+                        span_lo = static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16);
+                        span_hi = static_cast<uint32_t>(cx1 - cx0 + 1) | (static_cast<uint32_t>(cy1 - cy0 + 1) << 16);
                         col0 = c2.z;
                         col1 = c2.w;
                         col2 = c3.x;
@@ -258,10 +244,20 @@ k_project(ProjectParams p) {
                 }
             }
 
-            unsigned long long total;
-            const unsigned long long mine = (survive ? (1ull << 32) : 0ull) + n_tiles;
-            const unsigned long long excl = block_scan_u64(mine, s_warp, total);
-            if (tid == 0) s_base = atomicAdd(&p.counters->splat_pair, total);
+            // Record slots: ballot ranks inside the warp, warp counts across the CTA, one
+            // atomic per (CTA, instance) on the splat count (high word of splat_pair).
+            pairs += n_tiles;
+            const uint32_t bal = __ballot_sync(0xffffffffu, survive);
+            if (lane == 0) s_wcnt[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t before = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < kProjectThreads / 32; ++w) {
+                const uint32_t t = s_wcnt[w];
+                before += w < warp ? t : 0u;
+                total += t;
+            }
+            if (tid == 0) s_base = atomicAdd(&p.counters->splat_pair, static_cast<unsigned long long>(total) << 32) >> 32;
             __syncthreads();
             const unsigned long long base = s_base;
             const uint32_t ordinal = gvalid ? p.inst_base[inst] + gi : 0u;
@@ -270,7 +266,7 @@ k_project(ProjectParams p) {
                 p.posed_debug[3ull * ordinal + 1] = ay;
                 p.posed_debug[3ull * ordinal + 2] = az;
             }
-            const uint64_t ridx = (base >> 32) + (excl >> 32);
+            const uint64_t ridx = base + before + __popc(bal & lt);
             const uint32_t dbits = __float_as_uint(depth);
             const bool stored = survive && ridx < p.splat_capacity;
             if (survive) {
@@ -313,11 +309,7 @@ k_project(ProjectParams p) {
             }
             if (stored) {
                 p.splat_depth[ridx] = dbits;  // splat sort key (pairs are emitted after it)
-                // Binning cells of the rect: first cell, cells across, cells down.
-                const int cx0 = x0 / cell, cy0 = y0 / cell;
-                p.splat_span[ridx] = make_uint2(
-                    static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16),
-                    static_cast<uint32_t>((x1 - 1) / cell - cx0 + 1) | (static_cast<uint32_t>((y1 - 1) / cell - cy0 + 1) << 16));
+                p.splat_span[ridx] = make_uint2(span_lo, span_hi);
             }
         }
     }
@@ -328,9 +320,11 @@ k_project(ProjectParams p) {
         dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
         dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     }
+    pairs = __reduce_add_sync(0xffffffffu, pairs);
     if ((tid & 31) == 0) {
         if (dmin != 0xffffffffu) atomicMin(&p.counters->depth_min_bits, dmin);
         if (dmax != 0u) atomicMax(&p.counters->depth_max_bits, dmax);
+        if (pairs) atomicAdd(&p.counters->splat_pair, static_cast<unsigned long long>(pairs));  // low word: K
     }
 }
 

@@ -75,15 +75,16 @@ __device__ __forceinline__ bool blend(const SplatView& s, int px, int py, float&
 // 4 x tiles). Crowd frames are extremely skewed — horizon tiles carry tens of thousands
 // of pairs and mix saturated crowd pixels with never-saturating sky — so splitting a tile
 // four ways cuts the serial list walk of the heaviest tiles by 4x and lets each quadrant
-// stop on its own saturation; small CTAs keep ~32 resident per SM, which hides the
-// record-gather latency. Each pixel still walks the tile's list in order, so results are
-// identical to the whole-tile kernel. Warp w covers the 8x4 block at rows 4w..4w+3.
+// stop on its own saturation. Warp w covers the 8x4 block at rows 4w..4w+3 and walks the
+// quadrant's list on its own (no CTA barrier: a saturated warp never waits for the
+// other), staging 32 records at a time with the next 32 already in flight. Each pixel
+// still walks the tile's list in order, so results are identical to the whole-tile form.
 __global__ void __launch_bounds__(64)
 k_raster16q(RasterParams p) {
-    __shared__ float4 s_geo[64];
-    __shared__ float4 s_col[64];
-    __shared__ float2 s_col2[64];
-    __shared__ uint2 s_rect[64];
+    __shared__ float4 s_geo[2][32];
+    __shared__ float4 s_col[2][32];
+    __shared__ float2 s_col2[2][32];
+    __shared__ uint2 s_rect[2][32];
     const int tile = blockIdx.x >> 2, quad = blockIdx.x & 3;
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -94,74 +95,84 @@ k_raster16q(RasterParams p) {
     const bool inside = px < p.width && py < p.height;
     const uint2 range = p.ranges[blockIdx.x];  // this quadrant's cell: tile * 4 + quad
     const float fx = static_cast<float>(px) + 0.5f, fy = static_cast<float>(py) + 0.5f;
+    float4* geo = s_geo[warp];
+    float4* col = s_col[warp];
+    float2* col2 = s_col2[warp];
+    uint2* rect = s_rect[warp];
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
-    for (uint32_t start = range.x; start < range.y; start += 64) {
-        if (__syncthreads_count(done) == 64) break;
-        const uint32_t i = start + threadIdx.x;
-        if (i < range.y) {
-            const float4* src = p.records + 3ull * p.recs[i];
-            const float4 r0 = src[0], r1 = src[1], r2 = src[2];
-            s_geo[threadIdx.x] = r0;
-            s_col[threadIdx.x] = r1;
-            s_col2[threadIdx.x] = make_float2(r2.x, r2.y);
-            s_rect[threadIdx.x] = make_uint2(__float_as_uint(r2.z), __float_as_uint(r2.w));
+    // Records of the chunk after the current one, loaded while the current one is walked.
+    float4 n0 = make_float4(0, 0, 0, 0), n1 = n0, n2 = n0;
+    if (range.x + lane < range.y) {
+        const float4* src = p.records + 3ull * p.recs[range.x + lane];
+        n0 = src[0];
+        n1 = src[1];
+        n2 = src[2];
+    }
+    for (uint32_t start = range.x; start < range.y; start += 32) {
+        if (__all_sync(0xffffffffu, done)) break;
+        __syncwarp();
+        geo[lane] = n0;
+        col[lane] = n1;
+        col2[lane] = make_float2(n2.x, n2.y);
+        rect[lane] = make_uint2(__float_as_uint(n2.z), __float_as_uint(n2.w));
+        __syncwarp();
+        if (start + 32 + lane < range.y) {
+            const float4* src = p.records + 3ull * p.recs[start + 32 + lane];
+            n0 = src[0];
+            n1 = src[1];
+            n2 = src[2];
         }
-        __syncthreads();
-        const int n = min(64u, range.y - start);
-        if (__all_sync(0xffffffffu, done)) continue;
-        for (int base = 0; base < n; base += 32) {
-            // Lane L: which of this warp's 32 pixels splat base+L's rect covers (bit = lane).
-            uint32_t cover = 0;
-            if (base + lane < n) {
-                const uint2 r = s_rect[base + lane];
-                const int cx0 = max(static_cast<int>(r.x & 0xffff) - bx0, 0);
-                const int cx1 = min(static_cast<int>(r.y & 0xffff) - bx0, 8);
-                const int cy0 = max(static_cast<int>(r.x >> 16) - by0, 0);
-                const int cy1 = min(static_cast<int>(r.y >> 16) - by0, 4);
-                if (cx0 < cx1 && cy0 < cy1) {
-                    const uint32_t row = ((1u << cx1) - 1u) & ~((1u << cx0) - 1u);
-                    const uint32_t rows = static_cast<uint32_t>(((1ull << (8 * cy1)) - 1ull) & ~((1ull << (8 * cy0)) - 1ull));
-                    cover = (row * 0x01010101u) & rows;
-                }
+        const int n = min(32u, range.y - start);
+        // Lane L: which of this warp's 32 pixels splat L's rect covers (bit = lane).
+        uint32_t cover = 0;
+        if (lane < n) {
+            const uint2 r = rect[lane];
+            const int cx0 = max(static_cast<int>(r.x & 0xffff) - bx0, 0);
+            const int cx1 = min(static_cast<int>(r.y & 0xffff) - bx0, 8);
+            const int cy0 = max(static_cast<int>(r.x >> 16) - by0, 0);
+            const int cy1 = min(static_cast<int>(r.y >> 16) - by0, 4);
+            if (cx0 < cx1 && cy0 < cy1) {
+                const uint32_t row = ((1u << cx1) - 1u) & ~((1u << cx0) - 1u);
+                const uint32_t rows = static_cast<uint32_t>(((1ull << (8 * cy1)) - 1ull) & ~((1ull << (8 * cy0)) - 1ull));
+                cover = (row * 0x01010101u) & rows;
             }
-            // Bit-matrix transpose across the warp: lane L now holds, in list order, the
-            // chunk's splats that cover pixel L.
-            uint32_t todo = cover;
+        }
+        // Bit-matrix transpose across the warp: lane L now holds, in list order, the
+        // chunk's splats that cover pixel L.
+        uint32_t todo = cover;
 #pragma unroll
-            for (int s = 16; s >= 1; s >>= 1) {
-                const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu
-                                                         : s == 2 ? 0x33333333u : 0x55555555u;
-                const uint32_t y = __shfl_xor_sync(0xffffffffu, todo, s);
-                todo = (lane & s) ? ((todo & ~m) | ((y & ~m) >> s)) : ((todo & m) | ((y & m) << s));
+        for (int s = 16; s >= 1; s >>= 1) {
+            const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu
+                                                     : s == 2 ? 0x33333333u : 0x55555555u;
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, todo, s);
+            todo = (lane & s) ? ((todo & ~m) | ((y & ~m) >> s)) : ((todo & m) | ((y & m) << s));
+        }
+        if (done) todo = 0u;
+        // Every lane walks its own splats in order; lanes with disjoint splats work
+        // concurrently instead of idling through each other's splats.
+        while (__any_sync(0xffffffffu, todo != 0u)) {
+            if (todo == 0u) continue;
+            const int k = __ffs(todo) - 1;
+            todo &= todo - 1u;
+            const float4 g = geo[k];
+            const float dx = __fsub_rn(fx, g.x);
+            const float dy = __fsub_rn(fy, g.y);
+            const float4 c = col[k];
+            const float q = __fadd_rn(__fmul_rn(__fmul_rn(g.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
+            const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(g.w, dx), dy));
+            if (power < c.z) continue;
+            const float alpha = fminf(c.y * __expf(power), p.alpha_max);
+            const float w = T * alpha;
+            const float2 c2 = col2[k];
+            cr = fmaf(w, c.w, cr);
+            cg = fmaf(w, c2.x, cg);
+            cb = fmaf(w, c2.y, cb);
+            T = T * (1.0f - alpha);
+            if (T < p.t_floor) {
+                done = true;
+                todo = 0u;
             }
-            if (done) todo = 0u;
-            // Every lane walks its own splats in order; lanes with disjoint splats work
-            // concurrently instead of idling through each other's splats.
-            while (__any_sync(0xffffffffu, todo != 0u)) {
-                if (todo == 0u) continue;
-                const int k = base + __ffs(todo) - 1;
-                todo &= todo - 1u;
-                const float4 g = s_geo[k];
-                const float dx = __fsub_rn(fx, g.x);
-                const float dy = __fsub_rn(fy, g.y);
-                const float4 c = s_col[k];
-                const float q = __fadd_rn(__fmul_rn(__fmul_rn(g.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
-                const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(g.w, dx), dy));
-                if (power < c.z) continue;
-                const float alpha = fminf(c.y * __expf(power), p.alpha_max);
-                const float w = T * alpha;
-                const float2 c2 = s_col2[k];
-                cr = fmaf(w, c.w, cr);
-                cg = fmaf(w, c2.x, cg);
-                cb = fmaf(w, c2.y, cb);
-                T = T * (1.0f - alpha);
-                if (T < p.t_floor) {
-                    done = true;
-                    todo = 0u;
-                }
-            }
-            if (__all_sync(0xffffffffu, done)) break;
         }
     }
     if (inside) {

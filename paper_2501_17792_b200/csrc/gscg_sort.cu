@@ -12,11 +12,13 @@
 //      [start, end). Stability keeps the depth order inside every cell, so each cell
 //      list is exactly the reference's bin restricted to the cell.
 //
-// Each LSD pass (5-bit digits) is reduce-then-scan: k_sort_upsweep counts digits per
-// 4096-key tile, k_sort_rows / k_sort_bases turn the counts into global offsets,
-// k_sort_downsweep ranks keys stably inside the tile with a register-only warp multisplit
-// (ballots + shuffles, no shared-memory atomics), stages the tile in digit order and
-// writes it out coalesced. No tile waits on another: a decoupled look-back onesweep and
+// Each LSD pass (digits of up to 5 bits; a b-bit key takes ceil(b/5) passes with the bits
+// spread evenly) is reduce-then-scan: k_sort_upsweep counts digits per 4096-key tile,
+// k_sort_rows / k_sort_bases turn the counts into global offsets, k_sort_downsweep ranks
+// keys stably inside the tile with a register-only warp multisplit (ballots + shuffles,
+// lane d keeps the warp's count of digit d), stages the tile in digit order and writes it
+// out coalesced. 8-bit digits with shared-memory counters were measured no faster overall
+// (fewer passes, but each ~1.6x slower). No tile waits on another: a decoupled look-back onesweep and
 // 8-bit shared-atomic ranking were both measured slower here (serial look-back chains,
 // ATOMS throughput).
 #include "gscg_common.cuh"
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(32) k_sort_bases(SortPassParams p) {
 // ballots give each key the lanes sharing its digit; lane d keeps the warp's running
 // count of digit d), stage the tile in shared memory in digit order, write it out
 // coalesced at digit_base[d] + counts[d][tile] + rank-within-digit.
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, 3)
 k_sort_downsweep(SortPassParams p) {
     __shared__ uint32_t s_keys[kSortTile];
     __shared__ uint16_t s_perm[kSortTile];  // tile-local source index of each staged key
@@ -180,14 +182,29 @@ k_sort_downsweep(SortPassParams p) {
         }
     }
     __syncthreads();
+    // Write-out: every gather of the thread issued before any store (the value gathers
+    // stay inside this tile's 16 KB input window, so they hit L2).
     const uint32_t n_here = p.count > base ? min(kSortTile, p.count - base) : 0u;
-    for (uint32_t e = tid; e < n_here; e += kSortThreads) {
-        const uint32_t key = s_keys[e];
-        const uint32_t dd = (key >> p.shift) & mask;
-        const uint32_t pos = s_global[dd] + (e - s_block_excl[dd]);
-        const uint32_t src = base + s_perm[e];  // the value gather stays inside this tile's window
-        p.keys_out[pos] = key;
-        p.vals_out[pos] = p.vals_in ? p.vals_in[src] : src;
+    const uint32_t* __restrict__ vals_in = p.vals_in;
+    uint32_t okey[kSortItems], opos[kSortItems], oval[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t e = tid + j * kSortThreads;
+        if (e < n_here) {
+            okey[j] = s_keys[e];
+            const uint32_t dd = (okey[j] >> p.shift) & mask;
+            opos[j] = s_global[dd] + (e - s_block_excl[dd]);
+            const uint32_t src = base + s_perm[e];
+            oval[j] = vals_in ? __ldg(vals_in + src) : src;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t e = tid + j * kSortThreads;
+        if (e < n_here) {
+            p.keys_out[opos[j]] = okey[j];
+            p.vals_out[opos[j]] = oval[j];
+        }
     }
 }
 
@@ -196,13 +213,80 @@ k_sort_downsweep(SortPassParams p) {
 // common: far crowd depths share float bit patterns).
 __global__ void __launch_bounds__(256)
 k_tie_fixup(const uint32_t* keys, uint32_t* recs, const uint32_t* ordinal, uint32_t count) {
+    static_assert(kStreamItems == 8, "two uint4 loads per thread");
     const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) * kStreamItems;
     if (b >= count) return;
+    uint32_t s = b;  // first position left to the scalar path below
+    if (b + kStreamItems < count) {
+        uint32_t k[kStreamItems + 1];
+        const uint4 lo = *reinterpret_cast<const uint4*>(keys + b);
+        const uint4 hi = *reinterpret_cast<const uint4*>(keys + b + 4);
+        k[0] = lo.x; k[1] = lo.y; k[2] = lo.z; k[3] = lo.w;
+        k[4] = hi.x; k[5] = hi.y; k[6] = hi.z; k[7] = hi.w;
+        k[8] = keys[b + kStreamItems];
+        bool tie = false;
+#pragma unroll
+        for (int j = 0; j < kStreamItems; ++j) tie |= k[j] == k[j + 1];
+        if (!tie) return;
+        const uint32_t prev = b > 0 ? keys[b - 1] : ~0u;
+        // [w0, w1): the runs that start and end inside the window, sorted in registers.
+        // A run entering from the left belongs to the thread where it starts; a run
+        // leaving on the right is finished by the scalar path from its start.
+        int w0 = 0;
+        if (b > 0 && k[0] == prev) {
+            w0 = 1;
+#pragma unroll
+            for (int j = 1; j < kStreamItems; ++j)
+                if (w0 == j && k[j] == k[j - 1]) w0 = j + 1;
+        }
+        int w1 = kStreamItems;
+        if (k[kStreamItems - 1] == k[kStreamItems]) {
+            w1 = kStreamItems - 1;
+#pragma unroll
+            for (int j = kStreamItems - 2; j >= 0; --j)
+                if (w1 == j + 1 && k[j] == k[j + 1]) w1 = j;
+            w1 = max(w1, w0);
+        }
+        uint32_t r[kStreamItems], o[kStreamItems];
+        const uint4 rlo = *reinterpret_cast<const uint4*>(recs + b);
+        const uint4 rhi = *reinterpret_cast<const uint4*>(recs + b + 4);
+        r[0] = rlo.x; r[1] = rlo.y; r[2] = rlo.z; r[3] = rlo.w;
+        r[4] = rhi.x; r[5] = rhi.y; r[6] = rhi.z; r[7] = rhi.w;
+#pragma unroll
+        for (int j = 0; j < kStreamItems; ++j) {
+            const bool in = j >= w0 && j < w1;
+            const bool tied = (j > 0 && k[j] == k[j - 1]) || k[j] == k[j + 1];
+            o[j] = in && tied ? ordinal[r[j]] : 0u;  // independent gathers, all in flight
+        }
+        // Odd-even transposition: equal keys are contiguous, so only runs reorder.
+        bool moved = false;
+#pragma unroll
+        for (int round = 0; round < kStreamItems; ++round) {
+#pragma unroll
+            for (int j = round & 1; j + 1 < kStreamItems; j += 2) {
+                if (j >= w0 && j + 1 < w1 && k[j] == k[j + 1] && o[j] > o[j + 1]) {
+                    const uint32_t t0 = o[j]; o[j] = o[j + 1]; o[j + 1] = t0;
+                    const uint32_t t1 = r[j]; r[j] = r[j + 1]; r[j + 1] = t1;
+                    moved = true;
+                }
+            }
+        }
+        if (moved) {
+            // Only [w0, w1) is this thread's: the runs crossing the window edges are being
+            // reordered by the threads where they start.
+#pragma unroll
+            for (int j = 0; j < kStreamItems; ++j)
+                if (j >= w0 && j < w1) recs[b + j] = r[j];
+        }
+        if (w1 == kStreamItems) return;
+        s = b + static_cast<uint32_t>(w1);  // start of the run leaving the window
+    }
+    // Scalar path: the window tail of the last thread, and runs that leave a window.
     const uint32_t e = min(count, b + kStreamItems);
-    uint32_t prev = b > 0 ? keys[b - 1] : ~0u;
-    for (uint32_t i = b; i < e; ++i) {
+    uint32_t prev = s > 0 ? keys[s - 1] : ~0u;
+    for (uint32_t i = s; i < e; ++i) {
         const uint32_t k = keys[i];
-        if (k != prev && i + 1 < count && keys[i + 1] == k) {
+        if ((i == 0 || k != prev) && i + 1 < count && keys[i + 1] == k) {
             uint32_t end = i + 1;
             while (end < count && keys[end] == k) ++end;
             for (uint32_t a = i + 1; a < end; ++a) {

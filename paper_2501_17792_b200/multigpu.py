@@ -180,20 +180,26 @@ class BandRank:
         self._check(self.lib.gscg_stream(self.ctx, C.byref(s)))
         return torch.cuda.ExternalStream(s.value, device=torch.device("cuda", self.device))
 
-    def project(self, fa: FrameArgs, settings, shard: tuple[int, int], rows: Sequence[int]) -> np.ndarray:
+    def project(self, fa: FrameArgs, settings, shard: tuple[int, int], rows: Sequence[int],
+                frame: Optional[N.GscgFrameDesc] = None) -> np.ndarray:
+        """Update + gather of the shard, then per-band splat counts. `frame` passes
+        device-resident inputs (GSCG_MEM_DEVICE); by default poses are sampled on the host."""
         cfg = self.scene.cfg
         n = self.scene.counts()[2]
-        tids, place, poses = self.renderer.sample_crowd(fa.time_s, fa.static_pose)
-        self._keep = (tids, place, poses)
-        fd = N.GscgFrameDesc()
-        fd.instance_count = n
-        fd.joint_stride = self.renderer.joint_stride
-        fd.template_ids = tids.ctypes.data
-        fd.placement = place.ctypes.data
-        fd.poses = poses.ctypes.data
-        fd.active_lod = self.lods.ctypes.data
-        fd.forced_lod = -1 if fa.forced_lod is None else int(fa.forced_lod)
-        fd.memory = N.GSCG_MEM_HOST
+        if frame is None:
+            tids, place, poses = self.renderer.sample_crowd(fa.time_s, fa.static_pose)
+            self._keep = (tids, place, poses)
+            fd = N.GscgFrameDesc()
+            fd.instance_count = n
+            fd.joint_stride = self.renderer.joint_stride
+            fd.template_ids = tids.ctypes.data
+            fd.placement = place.ctypes.data
+            fd.poses = poses.ctypes.data
+            fd.active_lod = self.lods.ctypes.data
+            fd.forced_lod = -1 if fa.forced_lod is None else int(fa.forced_lod)
+            fd.memory = N.GSCG_MEM_HOST
+        else:
+            fd = frame
         cam = self.scene.camera_basis()
         rs = gscg_settings(settings)
         lp = N.GscgLodPolicy()
@@ -258,10 +264,11 @@ def gscg_settings(settings) -> N.GscgRenderSettings:
 class DistributedRenderer:
     """One rank of a P-GPU frame (torch.distributed initialised with NCCL, one process per GPU)."""
 
-    def __init__(self, scene, device: int, exchange: Optional[TorchExchange] = None):
+    def __init__(self, scene, device: int, exchange: Optional[TorchExchange] = None,
+                 band: Optional[BandRank] = None):
         self.exchange = exchange or TorchExchange()
         self.rank, self.world = self.exchange.rank, self.exchange.world
-        self.band = BandRank(scene, device=device)
+        self.band = band or BandRank(scene, device=device)
         self.scene = scene
         self.rows: Optional[list[int]] = None
 
