@@ -5,9 +5,10 @@
 //   H2D of the frame records (pinned staging, one copy)
 //   update:    k_lod_plan (1 CTA) -> k_fk_skin
 //   gather:    k_project (persistent, template-major)       -> counters readback (sync)
-//   sort:      splats by depth (k_digit_histogram, k_onesweep x P, k_tie_fixup) ->
-//              pairs in that order (k_splat_cells, k_scan_sums, k_emit_pairs) ->
-//              pairs stably by cell (k_onesweep x P') -> k_cell_ranges
+//   sort:      splats by depth (k_sort_{upsweep,rows,bases,downsweep} x P) ->
+//              ties by ordinal + spans in sorted order (k_sorted_spans) ->
+//              pairs in that order (k_scan_sums, k_emit_pairs) ->
+//              pairs stably by cell (radix x P') -> k_cell_ranges
 //   rasterize: k_raster16q (or k_raster_generic for other tile sizes)
 //   D2H of framebuffer / transmittance / active LoDs (host mode)
 // The one mid-frame synchronisation reads S, K and the depth-bit range: it sizes the
@@ -113,10 +114,10 @@ struct gscg_ctx {
     DevBuf inst_group, inst_base, members, group_inst_start, group_inst_count, group_item_start;
     DevBuf skin, counters;
     // gather outputs
-    DevBuf records, record_ordinal, splat_depth;
+    DevBuf records, splat_meta, splat_depth;
     uint64_t splat_capacity = 0, pair_capacity = 0;
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
-    DevBuf skeys[2], srecs[2], pcell[2], precs[2], splat_span, span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
+    DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
     DevBuf fb_rgb, fb_T;
@@ -426,9 +427,8 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             ctx->pair_capacity = 1u << 21;
         }
         CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
-        CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->splat_meta.ensure(ctx->splat_capacity * 16));
         CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
-        CUDA_TRY(ctx->splat_span.ensure(ctx->splat_capacity * 8));
         if (ctx->debug & GSCG_DEBUG_RECORDS)
             CUDA_TRY(ctx->rec_dbg.ensure(ctx->splat_capacity * sizeof(gscg_splat_record)));
 
@@ -456,9 +456,8 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pj.skin = ctx->skin.as<float>();
         pj.counters = counters;
         pj.records = ctx->records.as<float4>();
-        pj.record_ordinal = ctx->record_ordinal.as<uint32_t>();
         pj.splat_depth = ctx->splat_depth.as<uint32_t>();
-        pj.splat_span = ctx->splat_span.as<uint2>();
+        pj.splat_meta = ctx->splat_meta.as<uint4>();
         pj.splat_capacity = ctx->splat_capacity;
         pj.pair_capacity = ctx->pair_capacity;
         pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
@@ -563,17 +562,17 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         // 1. splats by depth (bits that vary in the frame), ties by ordinal.
         const RadixPlan dplan = make_plan(static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax)));
         const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
-        const uint32_t sgrid = (S32 + 256 * kStreamItems - 1) / (256 * kStreamItems);
-        k_tie_fixup<<<sgrid, 256, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
-                                          ctx->record_ordinal.as<uint32_t>(), S32);
-        // 2. pairs in sorted splat order.
+        // 2. equal-depth runs by ordinal, cell spans in sorted order, pairs per 1024 splats.
         const uint32_t sblocks = (S32 + 1023) / 1024;
         CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * 4));
-        k_splat_cells<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->splat_span.as<uint2>(),
-                                               ctx->span_sorted.as<uint2>(), ctx->block_sums.as<uint32_t>());
+        CUDA_TRY(cudaMemsetAsync(ctx->block_sums.ptr, 0, static_cast<size_t>(sblocks) * 4, s));
+        static_assert(kMetaThreads * kStreamItems == 1024, "one pair block per CTA");
+        k_sorted_spans<<<sblocks, kMetaThreads, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
+                                                        ctx->splat_meta.as<uint4>(), S32, ctx->span_sorted.as<uint2>(),
+                                                        ctx->block_sums.as<uint32_t>());
         k_scan_sums<<<1, 1024, 0, s>>>(ctx->block_sums.as<uint32_t>(), sblocks);
-        k_emit_pairs<<<sblocks, 1024, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
+        k_emit_pairs<<<sblocks, kEmitThreads, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
                                               ctx->block_sums.as<uint32_t>(), geo.tiles_x, geo.cells_per_tile == 4 ? 1 : 0,
                                               ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
         launches += 4;
@@ -693,9 +692,9 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->template_ids, &ctx->placement, &ctx->poses, &ctx->lod_prev,
                       &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members,
                       &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
-                      &ctx->skin, &ctx->counters, &ctx->records, &ctx->record_ordinal,
+                      &ctx->skin, &ctx->counters, &ctx->records, &ctx->splat_meta,
                       &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
-                      &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->splat_span, &ctx->span_sorted,
+                      &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                       &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
                       &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch};
     for (DevBuf* b : bufs) b->release();
@@ -856,7 +855,7 @@ int gscg_project_shard(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_c
         BandParams& bp = ctx->band;
         bp = BandParams{};
         bp.records = ctx->records.as<float4>();
-        bp.ordinal = ctx->record_ordinal.as<uint32_t>();
+        bp.meta = ctx->splat_meta.as<uint4>();
         bp.depth = ctx->splat_depth.as<uint32_t>();
         bp.count = static_cast<uint32_t>(ctx->S);
         bp.bands = bands;
@@ -933,9 +932,8 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
         const uint64_t cap = std::max<uint64_t>(recv_count, 1);
         if (cap > ctx->splat_capacity) ctx->splat_capacity = cap + cap / 4;
         CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
-        CUDA_TRY(ctx->record_ordinal.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->splat_meta.ensure(ctx->splat_capacity * 16));
         CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
-        CUDA_TRY(ctx->splat_span.ensure(ctx->splat_capacity * 8));
         FrameCounters init{};
         init.depth_min_bits = 0xffffffffu;
         *ctx->h_counters = init;
@@ -948,9 +946,8 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
         up.row_end = static_cast<int32_t>(row_end);
         up.cell = geo.cell;
         up.records = ctx->records.as<float4>();
-        up.ordinal = ctx->record_ordinal.as<uint32_t>();
         up.depth = ctx->splat_depth.as<uint32_t>();
-        up.span = ctx->splat_span.as<uint2>();
+        up.meta = ctx->splat_meta.as<uint4>();
         up.counters = counters;
         const uint32_t grid = (up.count + 256 * kStreamItems - 1) / (256 * kStreamItems);
         if (grid) {
@@ -1069,7 +1066,7 @@ int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
         if (pairs == 0) return;
         CUDA_TRY(ctx->sorted_ordinals.ensure(pairs * 4));
         k_sorted_ordinals<<<std::min<uint64_t>((pairs + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-            ctx->final_recs, ctx->record_ordinal.as<uint32_t>(), static_cast<uint32_t>(pairs),
+            ctx->final_recs, ctx->splat_meta.as<uint4>(), static_cast<uint32_t>(pairs),
             ctx->sorted_ordinals.as<uint32_t>());
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));

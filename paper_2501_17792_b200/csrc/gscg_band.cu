@@ -93,7 +93,7 @@ k_band_pack(BandParams p) {
         if (b1s[k] < b0s[k]) continue;
         const float4* src = p.records + 3ull * i;
         const float4 r0 = src[0], r1 = src[1], r2 = src[2];
-        const uint4 meta = make_uint4(p.ordinal[i], p.depth[i], 0u, 0u);
+        const uint4 meta = make_uint4(p.meta[i].x, p.depth[i], 0u, 0u);
         for (int b = b0s[k]; b <= b1s[k]; ++b) {
             const unsigned long long slot = s_base[b] + atomicAdd(&s_cnt[b], 1u);
             float4* dst = reinterpret_cast<float4*>(p.packed + 4ull * slot);
@@ -129,7 +129,6 @@ k_band_unpack(BandUnpackParams p) {
         dst[0] = r0;
         dst[1] = r1;
         dst[2] = r2;
-        p.ordinal[i] = meta.x;
         p.depth[i] = meta.y;
         const uint32_t xy0 = __float_as_uint(r2.z), xy1 = __float_as_uint(r2.w);
         const int x0 = static_cast<int>(xy0 & 0xffffu), y0 = static_cast<int>(xy0 >> 16);
@@ -139,8 +138,8 @@ k_band_unpack(BandUnpackParams p) {
         const int cx0 = x0 / p.cell, cy0 = yc0 / p.cell;
         const uint32_t across = static_cast<uint32_t>((x1 - 1) / p.cell - cx0 + 1);
         const uint32_t down = static_cast<uint32_t>((yc1 - 1) / p.cell - cy0 + 1);
-        p.span[i] = make_uint2(static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0 - p.row_begin / p.cell) << 16),
-                               across | (down << 16));
+        p.meta[i] = make_uint4(meta.x, static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0 - p.row_begin / p.cell) << 16),
+                               across | (down << 16), 0u);
         pairs += across * down;
         dmin = min(dmin, meta.y);
         dmax = max(dmax, meta.y);

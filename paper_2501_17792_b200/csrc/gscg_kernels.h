@@ -60,9 +60,8 @@ struct ProjectParams {
     FrameCounters* counters;
     // outputs (capacity-checked)
     float4* records;  // 3 float4 per splat
-    uint32_t* record_ordinal;
     uint32_t* splat_depth;  // depth bits of every record (the splat sort keys)
-    uint2* splat_span;      // binning cells of every record: cx0 | cy0 << 16, across | down << 16
+    uint4* splat_meta;      // per record: ordinal, cx0 | cy0 << 16, across | down << 16, 0
     uint64_t splat_capacity;
     uint64_t pair_capacity;
     // debug outputs (may be null)
@@ -116,22 +115,23 @@ __global__ void k_sort_upsweep(SortPassParams p);
 __global__ void k_sort_rows(SortPassParams p);
 __global__ void k_sort_bases(SortPassParams p);
 __global__ void k_sort_downsweep(SortPassParams p);
-__global__ void k_tie_fixup(const uint32_t* keys, uint32_t* recs, const uint32_t* ordinal, uint32_t count);
-__global__ void k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const uint2* span, uint2* span_sorted,
-                              uint32_t* block_sums);
+constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat pair block
+__global__ void k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
+                               uint2* span_sorted, uint32_t* block_sums);
 __global__ void k_scan_sums(uint32_t* sums, uint32_t n);
 __global__ void k_emit_pairs(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted,
                              const uint32_t* block_offsets, int tiles_x, int quads, uint32_t* pair_cell,
                              uint32_t* pair_rec);
 __global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges);
 constexpr int kStreamItems = 8;  // elements per thread in the streaming sort kernels
+constexpr int kEmitThreads = 256;  // k_emit_pairs: 4 sorted splats per thread
 
 // screen-band exchange (multi-GPU frame)
 constexpr int kMaxBands = GSCG_MAX_BANDS;
 
 struct BandParams {
     const float4* records;
-    const uint32_t* ordinal;
+    const uint4* meta;
     const uint32_t* depth;
     uint32_t count;
     uint32_t bands;
@@ -148,9 +148,8 @@ struct BandUnpackParams {
     int32_t row_begin, row_end;  // the band's screen rows
     int32_t cell;                // binning cell edge in pixels
     float4* records;
-    uint32_t* ordinal;
     uint32_t* depth;
-    uint2* span;
+    uint4* meta;
     FrameCounters* counters;
 };
 
@@ -163,6 +162,6 @@ __global__ void k_band_unpack(BandUnpackParams p);
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream);
 
 // debug
-__global__ void k_sorted_ordinals(const uint32_t* recs, const uint32_t* ordinal, uint32_t count, uint32_t* out);
+__global__ void k_sorted_ordinals(const uint32_t* recs, const uint4* meta, uint32_t count, uint32_t* out);
 
 }  // namespace gscg

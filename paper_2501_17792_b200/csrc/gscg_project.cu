@@ -279,7 +279,6 @@ k_project(ProjectParams p) {
                     rec[2] = make_float4(col1, col2,
                                          __uint_as_float(static_cast<uint32_t>(x0) | (static_cast<uint32_t>(y0) << 16)),
                                          __uint_as_float(static_cast<uint32_t>(x1) | (static_cast<uint32_t>(y1) << 16)));
-                    p.record_ordinal[ridx] = ordinal;
                     if (p.record_debug) {
                         gscg_splat_record d;
                         d.ordinal = ordinal;
@@ -309,7 +308,7 @@ k_project(ProjectParams p) {
             }
             if (stored) {
                 p.splat_depth[ridx] = dbits;  // splat sort key (pairs are emitted after it)
-                p.splat_span[ridx] = make_uint2(span_lo, span_hi);
+                p.splat_meta[ridx] = make_uint4(ordinal, span_lo, span_hi, 0u);
             }
         }
     }

@@ -3,10 +3,10 @@
 // binning renderer.cpp:143-161) — restated as three device passes:
 //
 //   1. LSD radix sort of the S splat depth keys (32-bit, only the bits that vary in the
-//      frame), values = record index; k_tie_fixup orders equal-depth runs by splat
+//      frame), values = record index; k_sorted_spans orders equal-depth runs by splat
 //      ordinal (instance base + gaussian index) = the reference's (instance, gaussian)
 //      tie-break. The splats are now in the reference's total order.
-//   2. k_splat_cells + k_scan_sums + k_emit_pairs: every sorted splat emits one pair per
+//   2. k_sorted_spans + k_scan_sums + k_emit_pairs: every sorted splat emits one pair per
 //      overlapped binning cell (tile, or 8x8 quadrant of a 16-px tile), in sorted order.
 //   3. stable LSD radix sort of the pairs' cell ids; k_cell_ranges marks each cell's
 //      [start, end). Stability keeps the depth order inside every cell, so each cell
@@ -208,15 +208,66 @@ k_sort_downsweep(SortPassParams p) {
     }
 }
 
-// Equal-depth runs of the sorted splats: order by ordinal (renderer.cpp:91-96). Each
-// thread scans kStreamItems positions and fixes the runs that start there (ties are
-// common: far crowd depths share float bit patterns).
-__global__ void __launch_bounds__(256)
-k_tie_fixup(const uint32_t* keys, uint32_t* recs, const uint32_t* ordinal, uint32_t count) {
+// After the depth sort: equal-depth runs ordered by splat ordinal (renderer.cpp:91-96:
+// the reference breaks depth ties by (instance, gaussian), and ordinal = instance base +
+// gaussian index), each sorted splat's binning span gathered into sorted order, and the
+// pair count of every 1024-splat block (level 1 of the emission scan). One 16-byte meta
+// gather per splat serves both the tie-break and the span.
+//
+// Thread t owns the runs that START in its 8-position window. Runs inside the window are
+// ordered in registers (odd-even transposition on (key, ordinal); equal keys are
+// contiguous, so only runs move). A run leaving the window is finished by its owner in
+// global memory; the next windows skip it. Ties are frequent: same-pose characters on
+// one grid row share depth bit patterns.
+namespace {
+
+struct SpanSink {
+    uint32_t block_begin, block_end;  // this CTA's positions
+    uint32_t local = 0;               // pairs of this CTA's positions
+    uint32_t* block_sums;
+    uint2* span_sorted;
+    __device__ void put(uint32_t pos, uint4 m) {
+        span_sorted[pos] = make_uint2(m.y, m.z);
+        const uint32_t n = (m.z & 0xffffu) * (m.z >> 16);
+        if (pos >= block_begin && pos < block_end) local += n;
+        else atomicAdd(&block_sums[pos >> 10], n);
+    }
+};
+
+// Orders the run of equal keys starting at s by ordinal (insertion sort in global memory)
+// and emits its spans; returns the run's end.
+__device__ __forceinline__ uint32_t finish_run(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t s,
+                               SpanSink& sink) {
+    const uint32_t k = keys[s];
+    uint32_t end = s + 1;
+    while (end < count && keys[end] == k) ++end;
+    for (uint32_t a = s + 1; a < end; ++a) {
+        const uint32_t ra = recs[a];
+        const uint32_t oa = meta[ra].x;
+        uint32_t j = a;
+        while (j > s && meta[recs[j - 1]].x > oa) {
+            recs[j] = recs[j - 1];
+            --j;
+        }
+        recs[j] = ra;
+    }
+    for (uint32_t a = s; a < end; ++a) sink.put(a, meta[recs[a]]);
+    return end;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kMetaThreads)
+k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted,
+               uint32_t* block_sums) {
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
-    const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) * kStreamItems;
-    if (b >= count) return;
-    uint32_t s = b;  // first position left to the scalar path below
+    __shared__ uint32_t s_warp[kMetaThreads / 32];
+    SpanSink sink;
+    sink.block_begin = blockIdx.x * (kMetaThreads * kStreamItems);
+    sink.block_end = sink.block_begin + kMetaThreads * kStreamItems;
+    sink.block_sums = block_sums;
+    sink.span_sorted = span_sorted;
+    const uint32_t b = sink.block_begin + threadIdx.x * kStreamItems;
     if (b + kStreamItems < count) {
         uint32_t k[kStreamItems + 1];
         const uint4 lo = *reinterpret_cast<const uint4*>(keys + b);
@@ -224,14 +275,8 @@ k_tie_fixup(const uint32_t* keys, uint32_t* recs, const uint32_t* ordinal, uint3
         k[0] = lo.x; k[1] = lo.y; k[2] = lo.z; k[3] = lo.w;
         k[4] = hi.x; k[5] = hi.y; k[6] = hi.z; k[7] = hi.w;
         k[8] = keys[b + kStreamItems];
-        bool tie = false;
-#pragma unroll
-        for (int j = 0; j < kStreamItems; ++j) tie |= k[j] == k[j + 1];
-        if (!tie) return;
         const uint32_t prev = b > 0 ? keys[b - 1] : ~0u;
-        // [w0, w1): the runs that start and end inside the window, sorted in registers.
-        // A run entering from the left belongs to the thread where it starts; a run
-        // leaving on the right is finished by the scalar path from its start.
+        // [w0, w1): the positions whose runs start and end inside the window.
         int w0 = 0;
         if (b > 0 && k[0] == prev) {
             w0 = 1;
@@ -247,78 +292,76 @@ k_tie_fixup(const uint32_t* keys, uint32_t* recs, const uint32_t* ordinal, uint3
                 if (w1 == j + 1 && k[j] == k[j + 1]) w1 = j;
             w1 = max(w1, w0);
         }
-        uint32_t r[kStreamItems], o[kStreamItems];
+        uint32_t r[kStreamItems];
         const uint4 rlo = *reinterpret_cast<const uint4*>(recs + b);
         const uint4 rhi = *reinterpret_cast<const uint4*>(recs + b + 4);
         r[0] = rlo.x; r[1] = rlo.y; r[2] = rlo.z; r[3] = rlo.w;
         r[4] = rhi.x; r[5] = rhi.y; r[6] = rhi.z; r[7] = rhi.w;
+        uint4 m[kStreamItems];
 #pragma unroll
-        for (int j = 0; j < kStreamItems; ++j) {
-            const bool in = j >= w0 && j < w1;
-            const bool tied = (j > 0 && k[j] == k[j - 1]) || k[j] == k[j + 1];
-            o[j] = in && tied ? ordinal[r[j]] : 0u;  // independent gathers, all in flight
-        }
-        // Odd-even transposition: equal keys are contiguous, so only runs reorder.
+        for (int j = 0; j < kStreamItems; ++j)  // independent gathers, all in flight
+            m[j] = (j >= w0 && j < w1) ? meta[r[j]] : make_uint4(0u, 0u, 0u, 0u);
         bool moved = false;
 #pragma unroll
         for (int round = 0; round < kStreamItems; ++round) {
 #pragma unroll
             for (int j = round & 1; j + 1 < kStreamItems; j += 2) {
-                if (j >= w0 && j + 1 < w1 && k[j] == k[j + 1] && o[j] > o[j + 1]) {
-                    const uint32_t t0 = o[j]; o[j] = o[j + 1]; o[j + 1] = t0;
-                    const uint32_t t1 = r[j]; r[j] = r[j + 1]; r[j + 1] = t1;
+                if (j >= w0 && j + 1 < w1 && k[j] == k[j + 1] && m[j].x > m[j + 1].x) {
+                    const uint4 tm = m[j]; m[j] = m[j + 1]; m[j + 1] = tm;
+                    const uint32_t tr = r[j]; r[j] = r[j + 1]; r[j + 1] = tr;
                     moved = true;
                 }
             }
         }
-        if (moved) {
-            // Only [w0, w1) is this thread's: the runs crossing the window edges are being
+        if (w0 == 0 && w1 == kStreamItems) {
+            if (moved) {
+                *reinterpret_cast<uint4*>(recs + b) = make_uint4(r[0], r[1], r[2], r[3]);
+                *reinterpret_cast<uint4*>(recs + b + 4) = make_uint4(r[4], r[5], r[6], r[7]);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(span_sorted + b);
+#pragma unroll
+            for (int j = 0; j < kStreamItems; j += 2) {
+                dst[j / 2] = make_uint4(m[j].y, m[j].z, m[j + 1].y, m[j + 1].z);
+                sink.local += (m[j].z & 0xffffu) * (m[j].z >> 16) + (m[j + 1].z & 0xffffu) * (m[j + 1].z >> 16);
+            }
+        } else {
+            // Only [w0, w1) is this thread's: the runs crossing the window edges are
             // reordered by the threads where they start.
 #pragma unroll
-            for (int j = 0; j < kStreamItems; ++j)
-                if (j >= w0 && j < w1) recs[b + j] = r[j];
-        }
-        if (w1 == kStreamItems) return;
-        s = b + static_cast<uint32_t>(w1);  // start of the run leaving the window
-    }
-    // Scalar path: the window tail of the last thread, and runs that leave a window.
-    const uint32_t e = min(count, b + kStreamItems);
-    uint32_t prev = s > 0 ? keys[s - 1] : ~0u;
-    for (uint32_t i = s; i < e; ++i) {
-        const uint32_t k = keys[i];
-        if ((i == 0 || k != prev) && i + 1 < count && keys[i + 1] == k) {
-            uint32_t end = i + 1;
-            while (end < count && keys[end] == k) ++end;
-            for (uint32_t a = i + 1; a < end; ++a) {
-                const uint32_t ra = recs[a];
-                const uint32_t oa = ordinal[ra];
-                uint32_t j = a;
-                while (j > i && ordinal[recs[j - 1]] > oa) {
-                    recs[j] = recs[j - 1];
-                    --j;
+            for (int j = 0; j < kStreamItems; ++j) {
+                if (j >= w0 && j < w1) {
+                    if (moved) recs[b + j] = r[j];
+                    sink.put(b + j, m[j]);
                 }
-                recs[j] = ra;
+            }
+            if (w1 < kStreamItems) finish_run(keys, recs, meta, count, b + static_cast<uint32_t>(w1), sink);
+        }
+    } else if (b < count) {
+        // Last window: positions one by one.
+        uint32_t i = b;
+        if (b > 0) {
+            const uint32_t prev = keys[b - 1];
+            while (i < count && keys[i] == prev) ++i;  // a run entering from the left
+        }
+        while (i < count) {
+            if (i + 1 < count && keys[i + 1] == keys[i]) {
+                i = finish_run(keys, recs, meta, count, i, sink);
+            } else {
+                sink.put(i, meta[recs[i]]);
+                ++i;
             }
         }
-        prev = k;
     }
-}
-
-// Cell spans gathered into sorted order + per-block pair sums (level 1 of the scan).
-__global__ void __launch_bounds__(1024)
-k_splat_cells(const uint32_t* sorted_rec, uint32_t count, const uint2* span, uint2* span_sorted,
-              uint32_t* block_sums) {
-    __shared__ uint32_t s_warp[32];
-    const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
-    uint32_t n = 0;
-    if (i < count) {
-        const uint2 sp = span[sorted_rec[i]];
-        span_sorted[i] = sp;
-        n = (sp.y & 0xffffu) * (sp.y >> 16);
+    // Pairs of this CTA's positions: one atomic per CTA (crossing runs added theirs).
+    uint32_t v = __reduce_add_sync(0xffffffffu, sink.local);
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < kMetaThreads / 32; ++w) t += s_warp[w];
+        if (t) atomicAdd(&block_sums[blockIdx.x], t);
     }
-    uint32_t total;
-    block_excl_scan(n, s_warp, total);
-    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
 }
 
 // Exclusive scan of the block sums in place (one CTA).
@@ -335,60 +378,101 @@ __global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, uint32_t n) 
     }
 }
 
-// Emit (cell, record) pairs in sorted splat order. Warp-cooperative: the warp's pairs are
-// numbered 0..total-1 and lane L writes pairs L, L+32, ... (coalesced), finding each
-// pair's splat by a 5-step search over the warp's exclusive prefix.
-__global__ void __launch_bounds__(1024)
+// Emit (cell, record) pairs in sorted splat order, one CTA per 1024 sorted splats (the
+// block granularity of k_sorted_spans' pair sums). Each thread loads 4 consecutive
+// splats (vector loads, all in flight), the CTA scans their pair counts, and then the
+// CTA's pairs are written with consecutive threads on consecutive pairs (coalesced);
+// each pair finds its splat by binary search over the CTA's splat offsets in shared
+// memory.
+namespace {
+__device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x, int quads) {
+    return quads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
+                 : static_cast<uint32_t>(cy * tiles_x + cx);
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kEmitThreads)
 k_emit_pairs(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted, const uint32_t* block_offsets,
              int tiles_x, int quads, uint32_t* pair_cell, uint32_t* pair_rec) {
+    static_assert(kEmitThreads * 4 == 1024, "one 1024-splat pair block per CTA");
+    __shared__ uint32_t s_off[1024];
+    __shared__ uint2 s_span[1024];
+    __shared__ uint32_t s_rec[1024];
     __shared__ uint32_t s_warp[32];
-    const int lane = threadIdx.x & 31;
-    const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
-    const uint2 sp = i < count ? span_sorted[i] : make_uint2(0u, 0u);
-    const uint32_t rec = i < count ? rec_sorted[i] : 0u;
-    const uint32_t n = (sp.y & 0xffffu) * (sp.y >> 16);
-    uint32_t total;
-    const uint32_t off = block_offsets[blockIdx.x] + block_excl_scan(n, s_warp, total);
-    uint32_t incl = n;
+    const uint32_t base = blockIdx.x * 1024u;
+    const uint32_t i0 = base + 4u * threadIdx.x;
+    uint2 sp[4];
+    uint32_t rc[4];
+    if (i0 + 4 <= count) {
+        const uint4 a = *reinterpret_cast<const uint4*>(span_sorted + i0);
+        const uint4 b = *reinterpret_cast<const uint4*>(span_sorted + i0 + 2);
+        const uint4 r = *reinterpret_cast<const uint4*>(rec_sorted + i0);
+        sp[0] = make_uint2(a.x, a.y); sp[1] = make_uint2(a.z, a.w);
+        sp[2] = make_uint2(b.x, b.y); sp[3] = make_uint2(b.z, b.w);
+        rc[0] = r.x; rc[1] = r.y; rc[2] = r.z; rc[3] = r.w;
+    } else {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        for (int q = 0; q < 4; ++q) {
+            sp[q] = i0 + q < count ? span_sorted[i0 + q] : make_uint2(0u, 0u);
+            rc[q] = i0 + q < count ? rec_sorted[i0 + q] : 0u;
+        }
     }
-    const uint32_t excl = incl - n;
-    const uint32_t warp_total = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t warp_base = __shfl_sync(0xffffffffu, off, 0);
-    for (uint32_t t0 = 0; t0 < warp_total; t0 += 32) {
-        const uint32_t t = t0 + lane;
-        // owner: the last lane whose exclusive prefix is <= t
-        int owner = 0;
+    uint32_t n[4], sum = 0;
 #pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            const uint32_t e = __shfl_sync(0xffffffffu, excl, owner + step);
-            if (owner + step < 32 && e <= t) owner += step;
-        }
-        const uint32_t e_own = __shfl_sync(0xffffffffu, excl, owner);
-        const uint2 s2 = make_uint2(__shfl_sync(0xffffffffu, sp.x, owner), __shfl_sync(0xffffffffu, sp.y, owner));
-        const uint32_t r = __shfl_sync(0xffffffffu, rec, owner);
-        if (t < warp_total) {
-            const int k = static_cast<int>(t - e_own);
-            const int ncw = static_cast<int>(s2.y & 0xffffu);
-            const int cx = static_cast<int>(s2.x & 0xffffu) + k % ncw, cy = static_cast<int>(s2.x >> 16) + k / ncw;
-            pair_cell[warp_base + t] = quads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
-                                             : static_cast<uint32_t>(cy * tiles_x + cx);
-            pair_rec[warp_base + t] = r;
-        }
+    for (int q = 0; q < 4; ++q) {
+        n[q] = (sp[q].y & 0xffffu) * (sp[q].y >> 16);
+        sum += n[q];
+    }
+    uint32_t total;
+    uint32_t off = block_excl_scan(sum, s_warp, total);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        s_off[4 * threadIdx.x + q] = off;
+        s_span[4 * threadIdx.x + q] = sp[q];
+        s_rec[4 * threadIdx.x + q] = rc[q];
+        off += n[q];
+    }
+    __syncthreads();
+    const uint32_t out0 = block_offsets[blockIdx.x];
+    for (uint32_t t = threadIdx.x; t < total; t += kEmitThreads) {
+        // owner: the last splat whose offset is <= t (empty splats share offsets; the
+        // last of a tie is the one holding the pairs)
+        uint32_t lo = 0;
+#pragma unroll
+        for (uint32_t step = 512; step >= 1; step >>= 1)
+            if (lo + step < 1024 && s_off[lo + step] <= t) lo += step;
+        const uint2 s2 = s_span[lo];
+        const int k = static_cast<int>(t - s_off[lo]);
+        const int ncw = static_cast<int>(s2.y & 0xffffu);
+        const int cx = static_cast<int>(s2.x & 0xffffu) + k % ncw, cy = static_cast<int>(s2.x >> 16) + k / ncw;
+        pair_cell[out0 + t] = cell_id(cx, cy, tiles_x, quads);
+        pair_rec[out0 + t] = s_rec[lo];
     }
 }
 
 // [start, end) of every cell in the cell-sorted pairs (the reference's bins).
 __global__ void __launch_bounds__(256)
 k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges) {
+    static_assert(kStreamItems == 8, "two uint4 loads per thread");
     const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) * kStreamItems;
     if (b >= count) return;
-    const uint32_t e = min(count, b + kStreamItems);
     uint32_t prev = b > 0 ? cells[b - 1] : ~0u;
-    for (uint32_t i = b; i < e; ++i) {
+    if (b + kStreamItems <= count) {
+        const uint4 lo = *reinterpret_cast<const uint4*>(cells + b);
+        const uint4 hi = *reinterpret_cast<const uint4*>(cells + b + 4);
+        const uint32_t c[kStreamItems] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+        for (int j = 0; j < kStreamItems; ++j) {
+            if (c[j] != prev) {
+                ranges[c[j]].x = b + j;
+                if (b + j > 0) ranges[prev].y = b + j;
+            }
+            prev = c[j];
+        }
+        if (b + kStreamItems == count) ranges[prev].y = count;
+        return;
+    }
+    for (uint32_t i = b; i < count; ++i) {
         const uint32_t c = cells[i];
         if (c != prev) {
             ranges[c].x = i;
@@ -396,12 +480,12 @@ k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges) {
         }
         prev = c;
     }
-    if (e == count) ranges[prev].y = count;
+    ranges[prev].y = count;
 }
 
-__global__ void k_sorted_ordinals(const uint32_t* recs, const uint32_t* ordinal, uint32_t count, uint32_t* out) {
+__global__ void k_sorted_ordinals(const uint32_t* recs, const uint4* meta, uint32_t count, uint32_t* out) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
-        out[i] = ordinal[recs[i]];
+        out[i] = meta[recs[i]].x;
 }
 
 }  // namespace gscg
