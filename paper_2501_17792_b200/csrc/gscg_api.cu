@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -508,8 +509,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
     if (S32 > 0 && K > 0) {
         const uint32_t max_elems = std::max(S32, K);
         const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
-        CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * 256 * 4));  // tile digit counts
-        CUDA_TRY(ctx->hist.ensure(256 * 4));                                        // digit bases
+        CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * kRadix * 4));  // tile digit counts
+        CUDA_TRY(ctx->hist.ensure(kRadix * 4));                                        // digit bases
         for (int b = 0; b < 2; ++b) {
             CUDA_TRY(ctx->skeys[b].ensure(static_cast<size_t>(S32) * 4));
             CUDA_TRY(ctx->srecs[b].ensure(static_cast<size_t>(S32) * 4));
@@ -537,19 +538,21 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                 sp.digit_base = ctx->hist.as<uint32_t>();
                 k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
                 k_sort_rows<<<1u << plan.bits[q], 1024, 0, s>>>(sp);
-                k_sort_bases<<<1, kRadix, 0, s>>>(sp);  // digits beyond 2^bits stay unused
                 k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
-                launches += 4;
+                launches += 3;
                 out ^= 1;
             }
             CUDA_TRY(cudaGetLastError());
             return out ^ 1;
         };
-        // ceil(bits / kRadixBits) passes with the bits spread evenly (27 -> 7,7,7,6).
-        auto make_plan = [](uint32_t bits) {
+        // ceil(bits / 5) passes with the bits spread evenly (27 -> 5,5,5,4,4,4). 8-bit digits
+        // ranked with warp match (CUB onesweep style) measured slower here: __match_any_sync
+        // is slow on sm_100 (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
+        const uint32_t digit_bits = kRadixBits;
+        auto make_plan = [digit_bits](uint32_t bits) {
             RadixPlan pl{};
             bits = std::max(bits, 1u);
-            pl.passes = (bits + kRadixBits - 1) / kRadixBits;
+            pl.passes = (bits + digit_bits - 1) / digit_bits;
             uint32_t sh = 0;
             for (uint32_t q = 0; q < pl.passes; ++q) {
                 const uint32_t w = (bits - sh) / (pl.passes - q) + ((bits - sh) % (pl.passes - q) ? 1u : 0u);

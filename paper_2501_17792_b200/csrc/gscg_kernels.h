@@ -108,13 +108,13 @@ struct SortPassParams {
     uint32_t bits;
     uint32_t tiles;      // ceil(count / kSortTile)
     uint32_t* counts;      // kRadix x tiles, digit-major: tile digit counts -> exclusive offsets
-    uint32_t* digit_base;  // kRadix: row totals -> exclusive digit bases
+    uint32_t* digit_base;  // kRadix: row totals (scanned by each downsweep CTA)
 };
 
 __global__ void k_sort_upsweep(SortPassParams p);
 __global__ void k_sort_rows(SortPassParams p);
-__global__ void k_sort_bases(SortPassParams p);
 __global__ void k_sort_downsweep(SortPassParams p);
+
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat pair block
 __global__ void k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
                                uint2* span_sorted, uint32_t* block_sums);

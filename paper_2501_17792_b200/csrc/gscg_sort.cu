@@ -14,7 +14,7 @@
 //
 // Each LSD pass (digits of up to 5 bits; a b-bit key takes ceil(b/5) passes with the bits
 // spread evenly) is reduce-then-scan: k_sort_upsweep counts digits per 4096-key tile,
-// k_sort_rows / k_sort_bases turn the counts into global offsets, k_sort_downsweep ranks
+// k_sort_rows turns the counts into per-tile offsets and digit totals, k_sort_downsweep ranks
 // keys stably inside the tile with a register-only warp multisplit (ballots + shuffles,
 // lane d keeps the warp's count of digit d), stages the tile in digit order and writes it
 // out coalesced. 8-bit digits with shared-memory counters were measured no faster overall
@@ -71,18 +71,19 @@ k_sort_upsweep(SortPassParams p) {
     }
     // Lane d counts digit d of the warp's keys: per item, five ballots select the lanes
     // holding digit d.
+    uint32_t lane_mask[kRadixBits];  // all-ones where lane's bit b is set
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) lane_mask[b] = 0u - ((static_cast<uint32_t>(lane) >> b) & 1u);
     uint32_t cnt = 0;
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
-        uint32_t mine = __ballot_sync(0xffffffffu, idx < p.count);
+        // Lanes whose digit differs from lane's index in some bit: OR of (ballot ^ lane mask).
+        uint32_t differ = 0u;
 #pragma unroll
-        for (int b = 0; b < kRadixBits; ++b) {
-            const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            mine &= ((lane >> b) & 1) ? bb : ~bb;
-        }
-        cnt += __popc(mine);
+        for (int b = 0; b < kRadixBits; ++b) differ |= __ballot_sync(0xffffffffu, (d >> b) & 1u) ^ lane_mask[b];
+        cnt += __popc(__ballot_sync(0xffffffffu, idx < p.count) & ~differ);
     }
     s_hist[warp][lane] = cnt;
     __syncthreads();
@@ -95,7 +96,7 @@ k_sort_upsweep(SortPassParams p) {
 }
 
 // Row scans: CTA d turns digit d's tile counts into exclusive offsets; row total ->
-// digit_base[d].
+// digit_base[d] (the downsweep scans the row totals itself).
 __global__ void __launch_bounds__(1024)
 k_sort_rows(SortPassParams p) {
     __shared__ uint32_t s_warp[32];
@@ -112,12 +113,6 @@ k_sort_rows(SortPassParams p) {
     if (threadIdx.x == 0) p.digit_base[blockIdx.x] = carry;
 }
 
-// Exclusive scan of the kRadix digit totals (one warp).
-__global__ void __launch_bounds__(32) k_sort_bases(SortPassParams p) {
-    const uint32_t v = p.digit_base[threadIdx.x];
-    p.digit_base[threadIdx.x] = warp_incl_scan(v, threadIdx.x) - v;
-}
-
 // Downsweep: stable rank inside the tile with a register-only warp multisplit (five
 // ballots give each key the lanes sharing its digit; lane d keeps the warp's running
 // count of digit d), stage the tile in shared memory in digit order, write it out
@@ -131,9 +126,12 @@ k_sort_downsweep(SortPassParams p) {
     __shared__ uint32_t s_global[kRadix];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid < kRadix) s_global[tid] = p.digit_base[tid] + p.counts[tid * p.tiles + blockIdx.x];
-    const uint32_t base = blockIdx.x * kSortTile;
     const uint32_t mask = (1u << p.bits) - 1u;
+    if (tid < kRadix) {  // global digit base (exclusive scan of the row totals) + this tile's offset
+        const uint32_t total = static_cast<uint32_t>(tid) <= mask ? p.digit_base[tid] : 0u;
+        s_global[tid] = warp_incl_scan(total, lane) - total + p.counts[tid * p.tiles + blockIdx.x];
+    }
+    const uint32_t base = blockIdx.x * kSortTile;
     const uint32_t lt = (1u << lane) - 1u;
 
     uint32_t k[kSortItems], rank[kSortItems];
@@ -142,21 +140,24 @@ k_sort_downsweep(SortPassParams p) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         k[j] = idx < p.count ? p.keys_in[idx] : 0u;
     }
+    uint32_t lane_mask[kRadixBits];  // all-ones where lane's bit b is set
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) lane_mask[b] = 0u - ((static_cast<uint32_t>(lane) >> b) & 1u);
     uint32_t cnt = 0;  // lane d: keys of digit d so far in this warp's segment
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
         const uint32_t vm = __ballot_sync(0xffffffffu, idx < p.count);
-        uint32_t peers = vm, mine = vm;
+        uint32_t peers_differ = 0u, mine_differ = 0u;
 #pragma unroll
         for (int b = 0; b < kRadixBits; ++b) {
             const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            peers &= ((d >> b) & 1u) ? bb : ~bb;
-            mine &= ((lane >> b) & 1) ? bb : ~bb;
+            peers_differ |= bb ^ (0u - ((d >> b) & 1u));
+            mine_differ |= bb ^ lane_mask[b];
         }
-        rank[j] = __shfl_sync(0xffffffffu, cnt, static_cast<int>(d)) + __popc(peers & lt);
-        cnt += __popc(mine);
+        rank[j] = __shfl_sync(0xffffffffu, cnt, static_cast<int>(d)) + __popc(vm & ~peers_differ & lt);
+        cnt += __popc(vm & ~mine_differ);
     }
     s_woff[warp][lane] = cnt;
     __syncthreads();
