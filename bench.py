@@ -293,8 +293,10 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
 
     # ---- end-to-end through the public API (host poses + pinned H2D + kernels + D2H) ----
     if not band_path:
+        out_frame = r.alloc_frame(pinned=True)  # the frame is read back into page-locked memory
+
         def e2e_frame(f):
-            r.render_frame(times_s[f], settings, forced_lod=forced)
+            r.render_frame(times_s[f], settings, forced_lod=forced, out=out_frame)
     else:
         from paper_2501_17792_b200.multigpu import DistributedRenderer
         drr = DistributedRenderer(scene, local_rank, exchange=ex, band=br)

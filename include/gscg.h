@@ -170,6 +170,12 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                       const gscg_render_settings* settings, const gscg_lod_policy* lod,
                       float* fb_rgb, float* fb_T, gscg_stage_times* times);
 
+/* Page-locked host memory (cudaMallocHost) for frame inputs/outputs: device <-> host copies
+ * to and from it run at full DMA speed (gscg_render_frame's host-mode framebuffer read-back
+ * goes straight into it). */
+int gscg_host_alloc(uint64_t bytes, void** out);
+int gscg_host_free(void* ptr);
+
 /* Device pointers of the context's framebuffer (valid until the next render). */
 int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T);
 int gscg_synchronize(gscg_ctx* ctx);

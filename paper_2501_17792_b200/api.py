@@ -253,6 +253,18 @@ def memory_report_cell(instances: int, gaussians: int, fixed_overhead: int = 0) 
     return _report(r)
 
 
+def pinned_array(shape, dtype=np.float32) -> np.ndarray:
+    """A numpy array in page-locked host memory (freed with the array)."""
+    import weakref
+
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    ptr = C.c_void_p()
+    N.check_gscg(N.gscg().gscg_host_alloc(nbytes, C.byref(ptr)), None)
+    raw = (C.c_uint8 * max(nbytes, 1)).from_address(ptr.value)
+    weakref.finalize(raw, N.gscg().gscg_host_free, ptr.value)
+    return np.frombuffer(raw, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+
 class Renderer:
     """FrameContext on a B200: owns the gscg context and the uploaded template store."""
 
@@ -272,12 +284,27 @@ class Renderer:
     def joint_stride(self) -> int:
         return int(N.gsch().gsch_renderer_joint_stride(self._h))
 
+    def alloc_frame(self, pinned: bool = True):
+        """(rgb HxWx3, T HxW) float32 output arrays; pinned ones take the direct DMA path."""
+        W, H = self.scene.cfg.width, self.scene.cfg.height
+        if not pinned:
+            return np.empty((H, W, 3), dtype=np.float32), np.empty((H, W), dtype=np.float32)
+        return pinned_array((H, W, 3)), pinned_array((H, W))
+
     def render_frame(self, time_s: float, settings: Optional[RenderSettings] = None, static_pose: bool = False,
-                     forced_lod: Optional[int] = None, times: Optional[StageTimes] = None):
+                     forced_lod: Optional[int] = None, times: Optional[StageTimes] = None, out=None):
+        """Renders one frame; returns (rgb, T). `out` = (rgb, T) arrays to fill (e.g. from
+        alloc_frame(pinned=True)), else fresh arrays are returned."""
         settings = settings or RenderSettings()
         W, H = self.scene.cfg.width, self.scene.cfg.height
-        rgb = np.empty((H, W, 3), dtype=np.float32)
-        T = np.empty((H, W), dtype=np.float32)
+        if out is None:
+            rgb = np.empty((H, W, 3), dtype=np.float32)
+            T = np.empty((H, W), dtype=np.float32)
+        else:
+            rgb, T = out
+            if rgb.shape != (H, W, 3) or T.shape != (H, W) or rgb.dtype != np.float32 or T.dtype != np.float32 \
+                    or not rgb.flags.c_contiguous or not T.flags.c_contiguous:
+                raise ValueError("out must be C-contiguous float32 arrays of shape (H, W, 3) and (H, W)")
         st = N.GschStageTimes()
         N.check_gsch(N.gsch().gsch_render(self._h, time_s, int(static_pose), -1 if forced_lod is None else forced_lod,
                                           C.byref(settings.native()), _ptr(rgb), _ptr(T), C.byref(st)))

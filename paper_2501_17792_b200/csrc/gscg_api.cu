@@ -984,6 +984,22 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
     });
 }
 
+int gscg_host_alloc(uint64_t bytes, void** out) {
+    if (!out) return GSCG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    const cudaError_t e = cudaMallocHost(out, std::max<uint64_t>(bytes, 1));
+    if (e != cudaSuccess) {
+        *out = nullptr;
+        return e == cudaErrorMemoryAllocation ? GSCG_ERR_OOM : GSCG_ERR_CUDA;
+    }
+    return GSCG_OK;
+}
+
+int gscg_host_free(void* ptr) {
+    if (ptr) cudaFreeHost(ptr);
+    return GSCG_OK;
+}
+
 int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     if (rgb) *rgb = ctx->fb_rgb.as<float>();

@@ -220,6 +220,17 @@ gscg_camera camera_basis(const Camera& cam) {
 void render_frame(Crowd& crowd, const Camera& camera, float time_s,
                   const RenderSettings& settings, bool static_pose,
                   std::optional<uint32_t> forced_lod, StageTimes* times, FrameContext& ctx) {
+    if (ctx.out.color.width != camera.width || ctx.out.color.height != camera.height) {
+        ctx.out.color = Framebuffer(camera.width, camera.height);
+        ctx.out.transmittance.assign(static_cast<size_t>(camera.width) * camera.height, 0.0f);
+    }
+    render_frame_into(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx,
+                      ctx.out.color.rgb.data(), ctx.out.transmittance.data());
+}
+
+void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+                       bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
+                       FrameContext& ctx, float* out_rgb, float* out_T) {
     validate(settings);
     validate(camera);
     validate(crowd.lod);
@@ -255,14 +266,8 @@ void render_frame(Crowd& crowd, const Camera& camera, float time_s,
     for (uint32_t i = 0; i < lp.threshold_count; ++i) lp.thresholds_m[i] = crowd.lod.thresholds_m[i];
     lp.hysteresis_band_m = crowd.lod.hysteresis_band_m;
 
-    if (ctx.out.color.width != camera.width || ctx.out.color.height != camera.height) {
-        ctx.out.color = Framebuffer(camera.width, camera.height);
-        ctx.out.transmittance.assign(static_cast<size_t>(camera.width) * camera.height, 0.0f);
-    }
     gscg_stage_times st{};
-    check_gscg(gscg_render_frame(ctx.gpu(), &fd, &cam, &rs, &lp, ctx.out.color.rgb.data(),
-                                 ctx.out.transmittance.data(), &st),
-               ctx.gpu());
+    check_gscg(gscg_render_frame(ctx.gpu(), &fd, &cam, &rs, &lp, out_rgb, out_T, &st), ctx.gpu());
     for (size_t i = 0; i < crowd.instances.size(); ++i) crowd.instances[i].active_lod = ctx.lods[i];
 
     if (times) {

@@ -127,6 +127,12 @@ void render_frame(Crowd& crowd, const Camera& camera, float time_s,
                   const RenderSettings& settings, bool static_pose,
                   std::optional<uint32_t> forced_lod, StageTimes* times, FrameContext& ctx);
 
+// Same frame, written straight into caller buffers (width*height*3 RGB and width*height
+// transmittance; either may be null). Pinned (page-locked) buffers get a direct DMA.
+void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+                       bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
+                       FrameContext& ctx, float* out_rgb, float* out_T);
+
 Framebuffer render_frame(Crowd& crowd, const Camera& camera, float time_s,
                          const RenderSettings& settings, bool static_pose = false,
                          std::optional<uint32_t> forced_lod = std::nullopt,

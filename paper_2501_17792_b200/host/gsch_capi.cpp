@@ -339,10 +339,8 @@ int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t for
         StageTimes t;
         std::optional<uint32_t> forced;
         if (forced_lod >= 0) forced = static_cast<uint32_t>(forced_lod);
-        render_frame(r->scene->crowd, r->scene->camera, time_s, rs, static_pose != 0, forced, &t, *r->ctx);
-        const size_t px = static_cast<size_t>(r->scene->camera.width) * r->scene->camera.height;
-        if (out_rgb) std::memcpy(out_rgb, r->ctx->out.color.rgb.data(), px * 12);
-        if (out_T) std::memcpy(out_T, r->ctx->out.transmittance.data(), px * 4);
+        render_frame_into(r->scene->crowd, r->scene->camera, time_s, rs, static_pose != 0, forced, &t, *r->ctx,
+                          out_rgb, out_T);
         if (times) {
             times->update_ms = t.update_ms;
             times->gather_ms = t.gather_ms;

@@ -120,6 +120,8 @@ GSCG_SYMBOLS = {
     "gscg_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P,
                                     C.POINTER(GscgStageTimes)]),
+    "gscg_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
+    "gscg_host_free": (C.c_int, [_P]),
     "gscg_framebuffer_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),
     "gscg_synchronize": (C.c_int, [_P]),
     "gscg_stream": (C.c_int, [_P, C.POINTER(_P)]),

@@ -134,6 +134,19 @@ def test_repeated_frames_are_byte_identical():
     assert outs[0] == outs[1] == outs[2]
 
 
+def test_pinned_output_matches_fresh_arrays():
+    scene = basic_scene()
+    r1, r2 = P.Renderer(scene), P.Renderer(scene)
+    st = P.RenderSettings(background=(0.2, 0.1, 0.0))
+    rgb, T = r1.render_frame(0.5, st)
+    out = r2.alloc_frame(pinned=True)
+    rgb2, T2 = r2.render_frame(0.5, st, out=out)
+    assert rgb2 is out[0] and T2 is out[1]
+    assert rgb.tobytes() == rgb2.tobytes() and T.tobytes() == T2.tobytes()
+    with pytest.raises(ValueError):
+        r2.render_frame(0.5, st, out=(out[0][:, :-1], out[1]))
+
+
 def test_invalid_settings_raise():
     s = basic_scene(count=1, rows=1, cols=1)
     r = P.Renderer(s)
