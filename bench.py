@@ -176,6 +176,17 @@ def roofline_bytes(cfg, counts, lods, scene, sh: bool) -> dict:
     return {"frame": frame, "project": project, "raster": raster, "A": A, "M": M}
 
 
+def memory_block(r, scene) -> dict:
+    """Measured device bytes (shared template store, frame buffers) beside the reference's
+    MemoryLayoutModel (crowd.cpp:142-210): the config-5 shared-attribute ablation."""
+    mu = r.memory_usage()
+    model = scene.memory_report()
+    return {"template_store_bytes": mu["template_bytes"], "frame_buffers_bytes": mu["frame_bytes"],
+            "device_used_bytes": mu["device_total_bytes"] - mu["device_free_bytes"],
+            "model_shared_bytes": model["shared_bytes"], "model_naive_bytes": model["naive_bytes"],
+            "model_savings_fraction": round(model["savings_fraction"], 4)}
+
+
 def run_ours(args, rank, world, local_rank) -> dict | None:
     import torch
 
@@ -368,6 +379,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         "e2e": {"value": round(e2e_fps, 3), "unit": "FPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
+        "memory": memory_block(r, scene),
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(scene, args.config, frames_sample=args.cpu_frames)

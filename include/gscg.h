@@ -160,6 +160,16 @@ int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level,
 /* Device bytes held by uploaded templates (shared attribute store). */
 int gscg_template_bytes(const gscg_ctx* ctx, uint64_t* out);
 
+/* Device memory of the context (config-5 ablation: shared-attribute store vs the
+ * reference's analytic MemoryLayoutModel, crowd.cpp:142-210). */
+typedef struct {
+  uint64_t template_bytes; /* shared template store: core + skin weights + SH, all levels */
+  uint64_t frame_bytes;    /* per-frame device buffers at their high-water mark */
+  uint64_t pinned_bytes;   /* page-locked staging */
+  uint64_t device_free_bytes, device_total_bytes; /* cudaMemGetInfo */
+} gscg_memory_info;
+int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out);
+
 int gscg_set_debug(gscg_ctx* ctx, uint32_t flags);
 
 /* Renders one frame. fb_rgb (W*H*3) and fb_T (W*H) receive the framebuffer and the

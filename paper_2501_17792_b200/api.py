@@ -314,6 +314,12 @@ class Renderer:
                 setattr(times, f, getattr(st, f))
         return rgb, T
 
+    def memory_usage(self) -> dict:
+        """Device bytes of the shared template store and the per-frame buffers (gscg_memory_usage)."""
+        m = N.GscgMemoryUsage()
+        N.check_gscg(N.gscg().gscg_memory_usage(self.gpu, C.byref(m)), self.gpu)
+        return {f: getattr(m, f) for f, _ in m._fields_}
+
     def sample_crowd(self, time_s: float, static_pose: bool = False, threads: int = 0):
         n = self.scene.counts()[2]
         js = self.joint_stride

@@ -53,6 +53,18 @@ struct DevBuf {
         cap = want;
         return cudaSuccess;
     }
+    // Exactly `bytes` (the shared template store is sized once, without growth slack).
+    cudaError_t ensure_exact(size_t bytes) {
+        if (ptr && cap == bytes) return cudaSuccess;
+        release();
+        cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(bytes, 16));
+        if (e != cudaSuccess) {
+            ptr = nullptr;
+            return e;
+        }
+        cap = bytes;
+        return cudaSuccess;
+    }
     template <typename T>
     T* as() const {
         return static_cast<T*>(ptr);
@@ -775,16 +787,16 @@ int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level, const
             std::memcpy(&c[15], &i23, 4);
         }
         ls.count = n;
-        CUDA_TRY(ls.core.ensure(core.size() * sizeof(float)));
+        CUDA_TRY(ls.core.ensure_exact(core.size() * sizeof(float)));
         CUDA_TRY(cudaMemcpyAsync(ls.core.ptr, core.data(), core.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
-        CUDA_TRY(ls.weights.ensure(static_cast<size_t>(n) * 16));
+        CUDA_TRY(ls.weights.ensure_exact(static_cast<size_t>(n) * 16));
         CUDA_TRY(cudaMemcpyAsync(ls.weights.ptr, d->skin_weights, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, ctx->stream));
         ls.has_sh = d->sh != nullptr;
         if (ls.has_sh) {
             // Pad to a whole 256-Gaussian chunk so chunk copies stay in bounds.
             const size_t chunks = (n + kProjectThreads - 1) / kProjectThreads;
             const size_t bytes = chunks * kProjectThreads * kShFloats * sizeof(float);
-            CUDA_TRY(ls.sh.ensure(bytes));
+            CUDA_TRY(ls.sh.ensure_exact(bytes));
             CUDA_TRY(cudaMemsetAsync(ls.sh.ptr, 0, bytes, ctx->stream));
             CUDA_TRY(cudaMemcpyAsync(ls.sh.ptr, d->sh, static_cast<size_t>(n) * kShFloats * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
         } else {
@@ -981,6 +993,31 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
             times->update_ms = 0.0f;
             times->gather_ms = elapsed(ctx->ev[0], ctx->ev[3]);  // unpack
         }
+    });
+}
+
+int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        *out = gscg_memory_info{};
+        for (const TemplateStore& t : ctx->templates)
+            for (const LevelStore& l : t.levels) out->template_bytes += l.core.cap + l.weights.cap + l.sh.cap;
+        const DevBuf* bufs[] = {&ctx->d_templates, &ctx->d_groups, &ctx->d_mats, &ctx->d_parents,
+                                &ctx->template_ids, &ctx->placement, &ctx->poses, &ctx->lod_prev,
+                                &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members,
+                                &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
+                                &ctx->skin, &ctx->counters, &ctx->records, &ctx->splat_meta,
+                                &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
+                                &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
+                                &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals,
+                                &ctx->fb_rgb, &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch};
+        for (const DevBuf* b : bufs) out->frame_bytes += b->cap;
+        out->pinned_bytes = ctx->pinned_cap + sizeof(FrameCounters) + GSCG_MAX_BANDS * 8;
+        size_t fr = 0, tot = 0;
+        CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+        out->device_free_bytes = fr;
+        out->device_total_bytes = tot;
     });
 }
 

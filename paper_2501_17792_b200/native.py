@@ -57,6 +57,11 @@ class GscgStageTimes(C.Structure):
                 ("sort_passes", C.c_uint32), ("kernel_launches", C.c_uint32)]
 
 
+class GscgMemoryUsage(C.Structure):
+    _fields_ = [("template_bytes", C.c_uint64), ("frame_bytes", C.c_uint64), ("pinned_bytes", C.c_uint64),
+                ("device_free_bytes", C.c_uint64), ("device_total_bytes", C.c_uint64)]
+
+
 class GscgSplatRecord(C.Structure):
     _fields_ = [("ordinal", C.c_uint32), ("instance_id", C.c_uint32), ("gaussian_index", C.c_uint32),
                 ("depth", C.c_float), ("mean_px", C.c_float * 2), ("cov_xx", C.c_float), ("cov_xy", C.c_float),
@@ -120,6 +125,7 @@ GSCG_SYMBOLS = {
     "gscg_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P,
                                     C.POINTER(GscgStageTimes)]),
+    "gscg_memory_usage": (C.c_int, [_P, C.POINTER(GscgMemoryUsage)]),
     "gscg_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
     "gscg_host_free": (C.c_int, [_P]),
     "gscg_framebuffer_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),

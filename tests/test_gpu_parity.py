@@ -147,6 +147,20 @@ def test_pinned_output_matches_fresh_arrays():
         r2.render_frame(0.5, st, out=(out[0][:, :-1], out[1]))
 
 
+def test_memory_usage_counts_the_shared_store_once():
+    scene = basic_scene(count=16, templates=2, sh=True)
+    r = P.Renderer(scene)
+    r.render_frame(0.0)
+    mu = r.memory_usage()
+    expect = 0
+    for t in range(2):
+        for l in range(scene.level_count(t)):
+            n = len(scene.level_view(t, l)["opacities"])
+            expect += n * 64 + n * 16 + ((n + 255) // 256) * 256 * 45 * 4
+    assert mu["template_bytes"] == expect  # independent of the 16 instances
+    assert mu["frame_bytes"] > 0 and mu["device_total_bytes"] > mu["device_free_bytes"]
+
+
 def test_invalid_settings_raise():
     s = basic_scene(count=1, rows=1, cols=1)
     r = P.Renderer(s)
