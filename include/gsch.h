@@ -109,6 +109,17 @@ int gsch_scene_sample_crowd(gsch_scene* scene, float time_s, int32_t static_pose
 int gsch_scene_set_motion(gsch_scene* scene, uint32_t motion_id, float fps, uint32_t frames,
                           uint32_t joints, const float* data);
 
+/* Asset files (reference io.hpp:38-43, io_assets.cpp): GSAT templates (v1 = the
+ * reference's layout; v2 adds SH residual blocks) and GSMO motion clips. load_* replace
+ * id < count or append id == count; renderers re-upload the changed store on their next
+ * frame. Format failures return GSCH_ERR_FORMAT with "[Kind] message" in gsch_last_error
+ * (Kind: IoError, BadMagic, VersionMismatch, Truncated, InvariantViolation). */
+#define GSCH_ERR_FORMAT (-6)
+int gsch_scene_save_template(const gsch_scene* scene, uint32_t template_id, const char* path);
+int gsch_scene_load_template(gsch_scene* scene, uint32_t template_id, const char* path);
+int gsch_scene_save_motion(const gsch_scene* scene, uint32_t motion_id, const char* path);
+int gsch_scene_load_motion(gsch_scene* scene, uint32_t motion_id, const char* path);
+
 /* Shared-attribute memory accounting (crowd.cpp:142-210, MemoryLayoutModel defaults). */
 typedef struct {
   uint64_t naive_bytes, shared_bytes;

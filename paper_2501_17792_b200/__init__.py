@@ -8,7 +8,7 @@ template / instance / camera interface; this package is its Python face.
 """
 from .api import (RenderSettings, Renderer, Scene, SceneConfig, StageTimes, baseline_config,  # noqa: F401
                   place_origin_instance, render_frame)
-from .native import NativeError  # noqa: F401
+from .native import FormatError, NativeError  # noqa: F401
 
 __all__ = ["RenderSettings", "Renderer", "Scene", "SceneConfig", "StageTimes", "baseline_config",
-           "place_origin_instance", "render_frame", "NativeError"]
+           "place_origin_instance", "render_frame", "NativeError", "FormatError"]

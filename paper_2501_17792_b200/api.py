@@ -229,6 +229,24 @@ class Scene:
         data = np.ascontiguousarray(data, dtype=np.float32)
         N.check_gsch(N.gsch().gsch_scene_set_motion(self._h, m, fps, data.shape[0], joints, _ptr(data)))
 
+    # ---- asset files (GSAT templates, GSMO motions; reference io.hpp:38-43) ----
+    def save_template(self, t: int, path) -> None:
+        N.check_gsch(N.gsch().gsch_scene_save_template(self._h, t, str(path).encode()))
+
+    def load_template(self, path, t: Optional[int] = None) -> int:
+        """Loads a GSAT file into template slot t (default: append); returns the slot."""
+        t = self.counts()[0] if t is None else t
+        N.check_gsch(N.gsch().gsch_scene_load_template(self._h, t, str(path).encode()))
+        return t
+
+    def save_motion(self, m: int, path) -> None:
+        N.check_gsch(N.gsch().gsch_scene_save_motion(self._h, m, str(path).encode()))
+
+    def load_motion(self, path, m: Optional[int] = None) -> int:
+        m = self.counts()[1] if m is None else m
+        N.check_gsch(N.gsch().gsch_scene_load_motion(self._h, m, str(path).encode()))
+        return m
+
     def memory_report(self) -> dict:
         r = N.GschMemoryReport()
         N.check_gsch(N.gsch().gsch_scene_memory_report(self._h, C.byref(r)))

@@ -1,5 +1,6 @@
 // C-ABI of the host scene layer (include/gsch.h) over the gsc host API.
 #include "gsch.h"
+#include "gsc/io.hpp"
 
 #include <cstring>
 #include <string>
@@ -41,6 +42,9 @@ int guarded(F&& f) {
     } catch (const std::bad_alloc&) {
         g_error = "out of memory";
         return GSCG_ERR_OOM;
+    } catch (const FormatError& e) {
+        g_error = std::string("[") + to_string(e.kind()) + "] " + e.what();
+        return GSCH_ERR_FORMAT;
     } catch (const std::exception& e) {
         g_error = e.what();
         return GSCG_ERR_STATE;
@@ -268,6 +272,50 @@ int gsch_scene_set_motion(gsch_scene* s, uint32_t m, float fps, uint32_t frames,
         }
         validate(clip);
         // Copy-on-write: renderers keep the old store alive; motions are read per frame.
+        auto next = std::make_shared<MotionStore>(*s->motions);
+        if (m == next->size()) next->push_back(std::move(clip));
+        else (*next)[m] = std::move(clip);
+        s->motions = next;
+        s->crowd.motions = next;
+    });
+}
+
+int gsch_scene_save_template(const gsch_scene* s, uint32_t t, const char* path) {
+    return guarded([&] {
+        if (!s || !path) throw std::invalid_argument("null argument");
+        if (t >= s->templates->size()) throw std::invalid_argument("template id beyond the store");
+        save_template((*s->templates)[t], path);
+    });
+}
+
+int gsch_scene_load_template(gsch_scene* s, uint32_t t, const char* path) {
+    return guarded([&] {
+        if (!s || !path) throw std::invalid_argument("null argument");
+        if (t > s->templates->size()) throw std::invalid_argument("template id beyond the store");
+        AvatarTemplate tpl = load_template(path);
+        tpl.template_id = t;
+        // Copy-on-write: a renderer re-uploads when it sees a new store (FrameContext).
+        auto next = std::make_shared<TemplateStore>(*s->templates);
+        if (t == next->size()) next->push_back(std::move(tpl));
+        else (*next)[t] = std::move(tpl);
+        s->templates = next;
+        s->crowd.templates = next;
+    });
+}
+
+int gsch_scene_save_motion(const gsch_scene* s, uint32_t m, const char* path) {
+    return guarded([&] {
+        if (!s || !path) throw std::invalid_argument("null argument");
+        if (m >= s->motions->size()) throw std::invalid_argument("motion id beyond the store");
+        save_motion((*s->motions)[m], path);
+    });
+}
+
+int gsch_scene_load_motion(gsch_scene* s, uint32_t m, const char* path) {
+    return guarded([&] {
+        if (!s || !path) throw std::invalid_argument("null argument");
+        if (m > s->motions->size()) throw std::invalid_argument("motion id beyond the store");
+        MotionClip clip = load_motion(path);
         auto next = std::make_shared<MotionStore>(*s->motions);
         if (m == next->size()) next->push_back(std::move(clip));
         else (*next)[m] = std::move(clip);

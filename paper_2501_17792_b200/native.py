@@ -147,7 +147,13 @@ GSCG_SYMBOLS = {
                                    C.POINTER(GscgStageTimes)]),
 }
 
+GSCH_ERR_FORMAT = -6
+
 GSCH_SYMBOLS = {
+    "gsch_scene_save_template": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
+    "gsch_scene_load_template": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
+    "gsch_scene_save_motion": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
+    "gsch_scene_load_motion": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
     "gsch_last_error": (C.c_char_p, []),
     "gsch_scene_create": (C.c_int, [C.POINTER(GschSceneConfig), C.c_int, C.POINTER(_P)]),
     "gsch_scene_destroy": (C.c_int, [_P]),
@@ -209,11 +215,23 @@ class NativeError(RuntimeError):
         self.status = status
 
 
+class FormatError(NativeError):
+    """Typed asset-file failure (reference io.hpp FormatError); .kind is one of IoError,
+    BadMagic, VersionMismatch, Truncated, InvariantViolation."""
+
+    def __init__(self, message: str):
+        kind, _, rest = message.partition("] ")
+        self.kind = kind.lstrip("[") if rest else "Unknown"
+        super().__init__(GSCH_ERR_FORMAT, rest or message)
+
+
 def check_gsch(status: int) -> None:
     if status != 0:
         msg = gsch().gsch_last_error().decode(errors="replace")
         if status == GSCG_ERR_INVALID_ARGUMENT:
             raise ValueError(msg)
+        if status == GSCH_ERR_FORMAT:
+            raise FormatError(msg)
         raise NativeError(status, msg)
 
 

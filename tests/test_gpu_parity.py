@@ -161,6 +161,20 @@ def test_memory_usage_counts_the_shared_store_once():
     assert mu["frame_bytes"] > 0 and mu["device_total_bytes"] > mu["device_free_bytes"]
 
 
+def test_loaded_template_reuploads_and_matches(tmp_path):
+    scene = basic_scene(templates=2, sh=True)
+    r = P.Renderer(scene)
+    rgb0, T0 = r.render_frame(0.4)
+    path = tmp_path / "t0.gsat"
+    scene.save_template(1, path)
+    scene.load_template(path, 0)  # slot 0 <- template 1: a new store, re-uploaded on the next frame
+    rgb1, _ = r.render_frame(0.4)
+    assert rgb1.tobytes() != rgb0.tobytes()
+    o = orc.from_scene(scene)
+    g, c = render_both(scene, r, o, 0.4)
+    check_frame(scene, r, o, g, c)
+
+
 def test_invalid_settings_raise():
     s = basic_scene(count=1, rows=1, cols=1)
     r = P.Renderer(s)
