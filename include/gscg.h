@@ -113,7 +113,29 @@ typedef struct {
   uint32_t* active_lod;         /* n, in/out: previous level (0xffffffff = unset) -> new level */
   int32_t forced_lod;           /* -1: distance LoD; else pinned level (crowd.cpp:94-96) */
   int32_t memory;               /* GSCG_MEM_HOST or GSCG_MEM_DEVICE for the pointers above */
+  /* Pose source. GSCG_POSES_GIVEN: `poses` holds the sampled poses. GSCG_POSES_SAMPLED:
+   * the device samples each instance's clip (gscg_upload_motion) at time_s + its phase
+   * offset (sample_pose with wrap, avatar.cpp:247-283; crowd.cpp:118-128), bit-identical
+   * to the host: the per-keyframe-pair acos/sin come from the host libm at upload and the
+   * per-instance sinf is an exact replica of glibc's; `poses` may be NULL. */
+  int32_t pose_source;
+  float time_s;
+  int32_t static_pose;          /* sampled mode: 1 = every instance in bind pose */
+  const uint32_t* motion_ids;   /* n (sampled mode) */
+  const float* phase_offsets;   /* n (sampled mode) */
 } gscg_frame_desc;
+
+#define GSCG_POSES_GIVEN 0
+#define GSCG_POSES_SAMPLED 1
+
+/* A motion clip for device pose sampling: frame_count x (4 + 4*joint_count) floats, the
+ * frame pose record layout above (MotionClip, avatar.hpp:40-48). */
+typedef struct {
+  float fps;
+  uint32_t frame_count;
+  uint32_t joint_count;
+  const float* frames;
+} gscg_motion_desc;
 
 /* StageTimes (renderer.hpp:105-112), measured with CUDA events on the context stream. */
 typedef struct {
@@ -159,6 +181,8 @@ int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level,
                       const gscg_level_desc* desc);
 /* Device bytes held by uploaded templates (shared attribute store). */
 int gscg_template_bytes(const gscg_ctx* ctx, uint64_t* out);
+/* Replaces (id < count) or appends (id == count) a motion clip. */
+int gscg_upload_motion(gscg_ctx* ctx, uint32_t motion_id, const gscg_motion_desc* desc);
 
 /* Device memory of the context (config-5 ablation: shared-attribute store vs the
  * reference's analytic MemoryLayoutModel, crowd.cpp:142-210). */
@@ -206,6 +230,8 @@ int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splat
 int gscg_get_cell_layout(gscg_ctx* ctx, uint32_t* tiles, uint32_t* cells_per_tile);
 int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells); /* cells x 2: [start, end) */
 int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs);
+/* The device pose sampler's sinf (glibc replica) over host arguments. */
+int gscg_eval_sinf(gscg_ctx* ctx, const float* in, float* out, uint32_t n);
 
 /* ---- Multi-GPU frame: instance shards -> screen bands ----
  * The reference renders one frame in one process (renderer.cpp:249-280); these three

@@ -135,6 +135,9 @@ int gsch_renderer_create(gsch_scene* scene, int device, gsch_renderer** out);
 int gsch_renderer_destroy(gsch_renderer* r);
 gscg_ctx* gsch_renderer_gpu(gsch_renderer* r);
 uint32_t gsch_renderer_joint_stride(gsch_renderer* r);
+/* Pose sampling on the GPU (GSCG_POSES_SAMPLED, bit-identical to host sampling): per frame
+ * only placements, motion ids and phase offsets are uploaded. Default off (host sampling). */
+int gsch_renderer_set_device_poses(gsch_renderer* r, int32_t enabled);
 /* render_frame(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx) */
 int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
                 const gsch_render_settings* settings, float* out_rgb, float* out_T,

@@ -953,3 +953,7 @@ int orc_skin_means(orc_scene* s, uint32_t tid, uint32_t level, const float* worl
 }
 
 }  // extern "C"
+
+extern "C" void orc_libm_sinf(const float* in, float* out, uint64_t n) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = std::sin(in[i]);
+}

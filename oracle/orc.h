@@ -104,6 +104,9 @@ int orc_forward_kinematics(orc_scene* s, uint32_t template_id, const float* pose
                            const float* root16, float* world_out);
 int orc_skin_means(orc_scene* s, uint32_t template_id, uint32_t level, const float* world,
                    float* posed_out);
+/* The host libm's sinf (what slerp_shortest calls, avatar.cpp:240-241) over an array: the
+ * checker for the device pose sampler's replica. */
+void orc_libm_sinf(const float* in, float* out, uint64_t n);
 
 #ifdef __cplusplus
 }

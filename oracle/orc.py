@@ -65,6 +65,7 @@ _SIGS = {
     "orc_pair_count": (C.c_uint64, [_P]),
     "orc_get_bins": (C.c_int, [_P, _P, _P]),
     "orc_get_level_cov": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
+    "orc_libm_sinf": (None, [_P, _P, C.c_uint64]),
     "orc_build_covariance": (C.c_int, [_P, _P, _P]),
     "orc_camera": (C.c_int, [_P, _P, C.c_float, C.c_int32, C.c_int32, C.c_float, _P, _P, _P]),
     "orc_project": (C.c_int, [_P, _P, _P, C.c_float, _P, _P, C.c_float, C.c_int32, C.c_int32, C.c_float, _P]),
@@ -221,3 +222,11 @@ def from_scene(scene, with_instances: bool = True) -> OracleScene:
     o.set_camera(c.cam_pos, c.cam_look, c.fov_y_deg, c.width, c.height, c.near_m)
     o.set_lod(c.lod_thresholds, c.lod_hysteresis)
     return o
+
+
+def libm_sinf(x: np.ndarray) -> np.ndarray:
+    """The host libm's sinf, elementwise (checker for the device sinf replica)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    lib().orc_libm_sinf(_p(x), _p(out), x.size)
+    return out

@@ -286,12 +286,24 @@ def pinned_array(shape, dtype=np.float32) -> np.ndarray:
 class Renderer:
     """FrameContext on a B200: owns the gscg context and the uploaded template store."""
 
-    def __init__(self, scene: Scene, device: int = 0):
+    def __init__(self, scene: Scene, device: int = 0, device_poses: bool = False):
         self.scene = scene
         h = C.c_void_p()
         N.check_gsch(N.gsch().gsch_renderer_create(scene.handle, device, C.byref(h)))
         self._h = h
         self.gpu = C.c_void_p(N.gsch().gsch_renderer_gpu(h))
+        self._device_poses = False
+        self.device_poses = device_poses
+
+    @property
+    def device_poses(self) -> bool:
+        """Sample poses on the GPU (bit-identical to host sampling; uploads no pose records)."""
+        return self._device_poses
+
+    @device_poses.setter
+    def device_poses(self, on: bool) -> None:
+        N.check_gsch(N.gsch().gsch_renderer_set_device_poses(self._h, int(bool(on))))
+        self._device_poses = bool(on)
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -27,7 +27,7 @@ INCLUDE = ROOT / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
               "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"] + ARCH
-EXACT_TUS = {"gscg_update.cu", "gscg_project.cu"}
+EXACT_TUS = {"gscg_update.cu", "gscg_project.cu", "gscg_pose.cu"}
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
              f"-I{INCLUDE}", f"-I{HOST}"]
 

@@ -79,6 +79,15 @@ struct LevelStore {
     float pf_cutoff = -1.0f;
 };
 
+// A clip as device slerp tables (gscg_pose.cu): roots per frame, key pairs per
+// (frame, joint) with the host-libm acos/sin of the pair angle.
+struct MotionStore {
+    float fps = 0.0f;
+    uint32_t frames = 0, joints = 0;
+    std::vector<float4> roots;
+    std::vector<KeyPairDev> keys;
+};
+
 struct TemplateStore {
     bool present = false;
     uint32_t joint_count = 0;
@@ -116,6 +125,9 @@ struct gscg_ctx {
     uint32_t debug = 0;
 
     std::vector<TemplateStore> templates;
+    std::vector<MotionStore> motions;
+    bool motions_dirty = false;
+    DevBuf d_motions, d_roots, d_keys, motion_ids, phases;
     bool tables_dirty = true;
     DevBuf d_templates, d_groups, d_mats, d_parents;
     uint32_t group_count = 0;
@@ -244,6 +256,34 @@ void upload_tables(gscg_ctx* ctx) {
     ctx->tables_dirty = false;
 }
 
+void upload_motions(gscg_ctx* ctx) {
+    if (!ctx->motions_dirty) return;
+    std::vector<MotionDev> md(ctx->motions.size());
+    std::vector<float4> roots;
+    std::vector<KeyPairDev> keys;
+    for (size_t i = 0; i < ctx->motions.size(); ++i) {
+        const MotionStore& m = ctx->motions[i];
+        md[i].fps = m.fps;
+        md[i].frames = m.frames;
+        md[i].joints = m.joints;
+        md[i].root_offset = static_cast<uint32_t>(roots.size());
+        md[i].key_offset = keys.size();
+        roots.insert(roots.end(), m.roots.begin(), m.roots.end());
+        keys.insert(keys.end(), m.keys.begin(), m.keys.end());
+    }
+    CUDA_TRY(ctx->d_motions.ensure_exact(std::max<size_t>(md.size(), 1) * sizeof(MotionDev)));
+    CUDA_TRY(ctx->d_roots.ensure_exact(std::max<size_t>(roots.size(), 1) * sizeof(float4)));
+    CUDA_TRY(ctx->d_keys.ensure_exact(std::max<size_t>(keys.size(), 1) * sizeof(KeyPairDev)));
+    if (!md.empty())
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_motions.ptr, md.data(), md.size() * sizeof(MotionDev), cudaMemcpyHostToDevice, ctx->stream));
+    if (!roots.empty())
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_roots.ptr, roots.data(), roots.size() * sizeof(float4), cudaMemcpyHostToDevice, ctx->stream));
+    if (!keys.empty())
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_keys.ptr, keys.data(), keys.size() * sizeof(KeyPairDev), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->motions_dirty = false;
+}
+
 // power_floor = logf(alpha_cutoff / opacity) with the host libm (renderer.cpp:140).
 void refresh_power_floor(gscg_ctx* ctx, float cutoff) {
     std::vector<float> pf;
@@ -297,15 +337,26 @@ void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_came
     if (!(cam->near_m > 0.0f)) invalid("Camera: near plane must be > 0");
     if (lod->threshold_count > GSCG_MAX_LOD_THRESHOLDS) invalid("LodPolicy: too many thresholds");
     const uint32_t n = frame->instance_count;
-    if (n > 0 && (!frame->template_ids || !frame->placement || !frame->poses || !frame->active_lod))
+    const bool sampled = frame->pose_source == GSCG_POSES_SAMPLED;
+    if (frame->pose_source != GSCG_POSES_GIVEN && !sampled) invalid("unknown pose_source");
+    if (n > 0 && (!frame->template_ids || !frame->placement || !frame->active_lod || (!sampled && !frame->poses)))
         invalid("null frame array");
+    if (n > 0 && sampled && !frame->static_pose && (!frame->motion_ids || !frame->phase_offsets))
+        invalid("sampled poses need motion_ids and phase_offsets");
     upload_tables(ctx);
+    if (sampled) upload_motions(ctx);
     if (n > 0 && frame->joint_stride < ctx->joint_stride) invalid("joint_stride below the largest skeleton");
     if (frame->memory == GSCG_MEM_HOST) {
         for (uint32_t i = 0; i < n; ++i) {
             const uint32_t t = frame->template_ids[i];
             if (t >= ctx->templates.size() || !ctx->templates[t].present || ctx->templates[t].levels.empty())
                 invalid("instance " + std::to_string(i) + " references a missing template");
+            if (sampled && !frame->static_pose) {
+                const uint32_t m = frame->motion_ids[i];
+                if (m >= ctx->motions.size()) invalid("instance " + std::to_string(i) + " references a missing motion");
+                if (ctx->motions[m].joints != ctx->templates[t].joint_count)
+                    invalid("forward_kinematics: pose joint count mismatch");
+            }
         }
     }
     refresh_power_floor(ctx, settings->alpha_cutoff);
@@ -349,31 +400,68 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
     CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
     const uint32_t *d_tid, *d_lodprev;
     const float *d_place, *d_poses;
+    const bool sampled = frame->pose_source == GSCG_POSES_SAMPLED;
+    const bool need_motion = sampled && !frame->static_pose && n > 0;
+    const uint32_t *d_mid = nullptr;
+    const float* d_phase = nullptr;
+    if (sampled) {
+        CUDA_TRY(ctx->motion_ids.ensure(std::max<size_t>(n, 1) * 4));
+        CUDA_TRY(ctx->phases.ensure(std::max<size_t>(n, 1) * 4));
+    }
     if (host) {
-        const size_t b_tid = n * 4ull, b_place = n * 16ull, b_pose = n * 4ull * pose_stride, b_lod = n * 4ull;
-        ctx->ensure_pinned(b_tid + b_place + b_pose + b_lod + 64);
+        // One pinned staging block, one copy per array.
+        const size_t b_tid = n * 4ull, b_place = n * 16ull, b_pose = sampled ? 0 : n * 4ull * pose_stride,
+                     b_lod = n * 4ull, b_mid = need_motion ? n * 4ull : 0, b_ph = need_motion ? n * 4ull : 0;
+        ctx->ensure_pinned(b_tid + b_place + b_pose + b_lod + b_mid + b_ph + 64);
         char* h = static_cast<char*>(ctx->pinned);
-        std::memcpy(h, frame->template_ids, b_tid);
-        std::memcpy(h + b_tid, frame->placement, b_place);
-        std::memcpy(h + b_tid + b_place, frame->poses, b_pose);
-        std::memcpy(h + b_tid + b_place + b_pose, frame->active_lod, b_lod);
-        if (n) {
-            CUDA_TRY(cudaMemcpyAsync(ctx->template_ids.ptr, h, b_tid, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(ctx->placement.ptr, h + b_tid, b_place, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(ctx->poses.ptr, h + b_tid + b_place, b_pose, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(ctx->lod_prev.ptr, h + b_tid + b_place + b_pose, b_lod, cudaMemcpyHostToDevice, s));
+        size_t off = 0;
+        auto stage = [&](const void* src, size_t bytes, void* dst) {
+            if (!bytes) return;
+            std::memcpy(h + off, src, bytes);
+            CUDA_TRY(cudaMemcpyAsync(dst, h + off, bytes, cudaMemcpyHostToDevice, s));
+            off += bytes;
+        };
+        stage(frame->template_ids, b_tid, ctx->template_ids.ptr);
+        stage(frame->placement, b_place, ctx->placement.ptr);
+        if (!sampled) stage(frame->poses, b_pose, ctx->poses.ptr);
+        stage(frame->active_lod, b_lod, ctx->lod_prev.ptr);
+        if (need_motion) {
+            stage(frame->motion_ids, b_mid, ctx->motion_ids.ptr);
+            stage(frame->phase_offsets, b_ph, ctx->phases.ptr);
         }
         d_tid = ctx->template_ids.as<uint32_t>();
         d_place = ctx->placement.as<float>();
         d_poses = ctx->poses.as<float>();
         d_lodprev = ctx->lod_prev.as<uint32_t>();
+        d_mid = ctx->motion_ids.as<uint32_t>();
+        d_phase = ctx->phases.as<float>();
     } else {
         d_tid = frame->template_ids;
         d_place = frame->placement;
-        d_poses = frame->poses;
+        d_poses = sampled ? ctx->poses.as<float>() : frame->poses;
         d_lodprev = frame->active_lod;
+        d_mid = frame->motion_ids;
+        d_phase = frame->phase_offsets;
     }
     CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
+    if (sampled && shard_end > shard_begin) {
+        // update_crowd's pose sampling on the device (gscg_pose.cu); FK reads ctx->poses.
+        PoseParams pp{};
+        pp.n = n;
+        pp.joint_stride = frame->joint_stride;
+        pp.time_s = frame->time_s;
+        pp.static_pose = frame->static_pose ? 1 : 0;
+        pp.motion_ids = d_mid;
+        pp.phase = d_phase;
+        pp.motions = ctx->d_motions.as<MotionDev>();
+        pp.roots = ctx->d_roots.as<float4>();
+        pp.keys = ctx->d_keys.as<KeyPairDev>();
+        pp.poses = ctx->poses.as<float>();
+        const uint64_t threads = static_cast<uint64_t>(n) * (frame->joint_stride + 1);
+        k_sample_poses<<<static_cast<uint32_t>((threads + 255) / 256), 256, 0, s>>>(pp);
+        ++launches;
+        CUDA_TRY(cudaGetLastError());
+    }
 
     const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + kBatch * static_cast<int>(js) * 12 * 4;
     int project_blocks_per_sm = 1;
@@ -711,7 +799,8 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
                       &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                       &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
-                      &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch};
+                      &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch, &ctx->d_motions, &ctx->d_roots,
+                      &ctx->d_keys, &ctx->motion_ids, &ctx->phases};
     for (DevBuf* b : bufs) b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
@@ -806,6 +895,50 @@ int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level, const
         ls.pf_cutoff = -1.0f;
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         ctx->tables_dirty = true;
+    });
+}
+
+int gscg_upload_motion(gscg_ctx* ctx, uint32_t motion_id, const gscg_motion_desc* d) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (!d || !d->frames) invalid("null motion");
+        if (!(d->fps > 0.0f)) invalid("MotionClip: fps must be > 0");
+        if (d->frame_count < 1) invalid("sample_pose: empty clip");
+        if (d->joint_count < 1 || d->joint_count > GSCG_MAX_JOINTS) invalid("MotionClip: joint count outside [1, 64]");
+        if (motion_id > ctx->motions.size()) invalid("motion id beyond the store");
+        MotionStore m;
+        m.fps = d->fps;
+        m.frames = d->frame_count;
+        m.joints = d->joint_count;
+        const size_t rec = 4 + 4 * static_cast<size_t>(m.joints);
+        m.roots.resize(m.frames);
+        m.keys.resize(static_cast<size_t>(m.frames) * m.joints);
+        for (uint32_t f = 0; f < m.frames; ++f) {
+            const float* a = d->frames + f * rec;
+            const float* b = d->frames + ((f + 1) % m.frames) * rec;
+            m.roots[f] = make_float4(a[0], a[1], a[2], 0.0f);
+            for (uint32_t j = 0; j < m.joints; ++j) {
+                const float* qa = a + 4 + 4 * j;
+                const float* qb = b + 4 + 4 * j;
+                // slerp_shortest's angle terms (avatar.cpp:226-245) with the host libm.
+                float dot = (qa[0] * qb[0] + qa[2] * qb[2]) + (qa[1] * qb[1] + qa[3] * qb[3]);
+                float sgn = 1.0f;
+                if (dot < 0.0f) {
+                    dot = -dot;
+                    sgn = -1.0f;
+                }
+                KeyPairDev& k = m.keys[static_cast<size_t>(f) * m.joints + j];
+                k.a = make_float4(qa[0], qa[1], qa[2], qa[3]);
+                k.b = sgn < 0.0f ? make_float4(-qb[0], -qb[1], -qb[2], -qb[3]) : make_float4(qb[0], qb[1], qb[2], qb[3]);
+                k.lerp = dot > 0.9995f ? 1u : 0u;
+                k.theta = k.lerp ? 0.0f : std::acos(std::min(dot, 1.0f));
+                k.sin_theta = k.lerp ? 1.0f : std::sin(k.theta);
+                k.pad = 0;
+            }
+        }
+        if (motion_id == ctx->motions.size()) ctx->motions.push_back(std::move(m));
+        else ctx->motions[motion_id] = std::move(m);
+        ctx->motions_dirty = true;
     });
 }
 
@@ -1018,6 +1151,24 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
         CUDA_TRY(cudaMemGetInfo(&fr, &tot));
         out->device_free_bytes = fr;
         out->device_total_bytes = tot;
+    });
+}
+
+int gscg_eval_sinf(gscg_ctx* ctx, const float* in, float* out, uint32_t n) {
+    if (!ctx || (n && (!in || !out))) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (!n) return;
+        DevBuf a, b;
+        CUDA_TRY(a.ensure_exact(n * 4ull));
+        CUDA_TRY(b.ensure_exact(n * 4ull));
+        CUDA_TRY(cudaMemcpyAsync(a.ptr, in, n * 4ull, cudaMemcpyHostToDevice, ctx->stream));
+        k_eval_sinf<<<std::min<uint32_t>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(a.as<float>(), b.as<float>(), n);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(out, b.ptr, n * 4ull, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        a.release();
+        b.release();
     });
 }
 

@@ -83,6 +83,37 @@ struct RasterParams {
     float* out_T;
 };
 
+// Device pose sampling (gscg_pose.cu): uploaded clips as per-keyframe-pair slerp tables.
+struct MotionDev {
+    float fps;
+    uint32_t frames, joints;
+    uint32_t root_offset;  // into PoseParams::roots (one float4 per frame)
+    uint64_t key_offset;   // into PoseParams::keys (frames x joints pairs (i, (i+1) % frames))
+};
+
+struct KeyPairDev {
+    float4 a, b;           // keyframe i and keyframe i+1 (negated when dot < 0), x y z w
+    float theta, sin_theta;  // acos(min(|dot|, 1)), sin(theta): host libm
+    uint32_t lerp;         // |dot| > 0.9995: normalized lerp instead of slerp
+    uint32_t pad;
+};
+
+struct PoseParams {
+    uint32_t n;
+    uint32_t joint_stride;
+    float time_s;
+    int32_t static_pose;
+    const uint32_t* motion_ids;
+    const float* phase;
+    const MotionDev* motions;
+    const float4* roots;
+    const KeyPairDev* keys;
+    float* poses;  // n x (4 + 4 * joint_stride)
+};
+
+__global__ void k_sample_poses(PoseParams p);
+__global__ void k_eval_sinf(const float* in, float* out, uint32_t n);
+
 __global__ void k_lod_plan(PlanParams p);
 __global__ void k_fk_skin(FkParams p);
 __global__ void k_project(ProjectParams p);

@@ -188,6 +188,65 @@ void sample_crowd_records(const Crowd& crowd, float time_s, bool static_pose, ui
     });
 }
 
+void FrameContext::ensure_motions(const std::shared_ptr<const MotionStore>& store) {
+    if (!store || store.get() == motions_uploaded_) return;
+    for (uint32_t m = 0; m < store->size(); ++m) {
+        const MotionClip& clip = (*store)[m];
+        if (clip.frames.empty()) continue;  // rejected per instance when sampled
+        const uint32_t J = clip.joint_count;
+        const size_t rec = 4 + 4 * static_cast<size_t>(J);
+        std::vector<float> frames(clip.frames.size() * rec);
+        for (size_t f = 0; f < clip.frames.size(); ++f) {
+            float* r = frames.data() + f * rec;
+            const Pose& p = clip.frames[f];
+            r[0] = p.root_translation[0];
+            r[1] = p.root_translation[1];
+            r[2] = p.root_translation[2];
+            r[3] = 0.0f;
+            for (uint32_t j = 0; j < J; ++j)
+                for (int k = 0; k < 4; ++k) r[4 + 4 * j + k] = p.local_rotations[j].c[k];
+        }
+        gscg_motion_desc d{};
+        d.fps = clip.fps;
+        d.frame_count = static_cast<uint32_t>(clip.frames.size());
+        d.joint_count = J;
+        d.frames = frames.data();
+        check_gscg(gscg_upload_motion(gpu_, m, &d), gpu_);
+    }
+    motions_uploaded_ = store.get();
+    keep_motions_ = store;
+}
+
+void FrameContext::fill_instances(const Crowd& crowd, bool static_pose) {
+    const size_t n = crowd.instances.size();
+    const TemplateStore& templates = *crowd.templates;
+    const MotionStore& motions = *crowd.motions;
+    template_ids.resize(n);
+    placement.resize(n * 4);
+    lods.resize(n);
+    motion_ids.resize(n);
+    phases.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+        const CrowdInstance& inst = crowd.instances[i];
+        if (inst.template_id >= templates.size() || inst.motion_id >= motions.size())
+            throw std::invalid_argument("render_frame: instance references a missing asset");
+        const uint32_t J = templates[inst.template_id].skeleton.joint_count();
+        if (J > joint_stride) throw std::invalid_argument("joint_stride below the skeleton's joint count");
+        if (!static_pose && motions[inst.motion_id].joint_count != J)
+            throw std::invalid_argument("forward_kinematics: pose joint count mismatch");
+        if (!static_pose && motions[inst.motion_id].frames.empty())
+            throw std::invalid_argument("sample_pose: empty clip");
+        template_ids[i] = inst.template_id;
+        placement[i * 4 + 0] = inst.x;
+        placement[i * 4 + 1] = inst.z;
+        placement[i * 4 + 2] = std::cos(inst.yaw);
+        placement[i * 4 + 3] = std::sin(inst.yaw);
+        lods[i] = inst.active_lod;
+        motion_ids[i] = inst.motion_id;
+        phases[i] = inst.phase_offset_s;
+    }
+}
+
 void FrameContext::sample_crowd(const Crowd& crowd, float time_s, bool static_pose,
                                 int thread_hint) {
     const size_t n = crowd.instances.size();
@@ -240,15 +299,26 @@ void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const R
 
     using clock = std::chrono::steady_clock;
     const auto t0 = clock::now();
-    ctx.sample_crowd(crowd, time_s, static_pose, settings.thread_count);
+    gscg_frame_desc fd{};
+    if (ctx.device_poses) {
+        ctx.ensure_motions(crowd.motions);
+        ctx.fill_instances(crowd, static_pose);
+        fd.pose_source = GSCG_POSES_SAMPLED;
+        fd.time_s = time_s;
+        fd.static_pose = static_pose ? 1 : 0;
+        fd.motion_ids = ctx.motion_ids.data();
+        fd.phase_offsets = ctx.phases.data();
+    } else {
+        ctx.sample_crowd(crowd, time_s, static_pose, settings.thread_count);
+        fd.pose_source = GSCG_POSES_GIVEN;
+        fd.poses = ctx.poses.data();
+    }
     const auto t1 = clock::now();
 
-    gscg_frame_desc fd{};
     fd.instance_count = static_cast<uint32_t>(crowd.instances.size());
     fd.joint_stride = ctx.joint_stride;
     fd.template_ids = ctx.template_ids.data();
     fd.placement = ctx.placement.data();
-    fd.poses = ctx.poses.data();
     fd.active_lod = ctx.lods.data();
     fd.forced_lod = forced_lod ? static_cast<int32_t>(*forced_lod) : -1;
     fd.memory = GSCG_MEM_HOST;

@@ -104,20 +104,30 @@ public:
     gscg_ctx* gpu() { return gpu_; }
     // Uploads the store once per pointer identity (shared-attribute residency).
     void ensure_templates(const std::shared_ptr<const TemplateStore>& store);
+    // Uploads every clip once per store identity (device pose sampling tables).
+    void ensure_motions(const std::shared_ptr<const MotionStore>& store);
     // Fills the per-frame pose / placement records for the whole crowd on the pool.
     void sample_crowd(const Crowd& crowd, float time_s, bool static_pose, int thread_hint);
+    // Device pose sampling mode: per frame only placement, motion ids and phase offsets
+    // go to the GPU, which samples every clip itself (bit-identical to the host path).
+    void fill_instances(const Crowd& crowd, bool static_pose);
 
     RasterOutput out;
     std::vector<uint32_t> template_ids;
     std::vector<float> placement;  // n x 4
     std::vector<float> poses;      // n x (4 + 4 * joint_stride)
     std::vector<uint32_t> lods;
+    std::vector<uint32_t> motion_ids;
+    std::vector<float> phases;
     uint32_t joint_stride = 0;
+    bool device_poses = false;  // sample poses on the GPU (GSCG_POSES_SAMPLED)
 
 private:
     gscg_ctx* gpu_ = nullptr;
     const TemplateStore* uploaded_ = nullptr;
     std::shared_ptr<const TemplateStore> keep_;
+    const MotionStore* motions_uploaded_ = nullptr;
+    std::shared_ptr<const MotionStore> keep_motions_;
     std::unique_ptr<HostPool> pool_;
 };
 

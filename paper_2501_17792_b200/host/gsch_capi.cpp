@@ -372,6 +372,13 @@ gscg_ctx* gsch_renderer_gpu(gsch_renderer* r) { return r ? r->ctx->gpu() : nullp
 
 uint32_t gsch_renderer_joint_stride(gsch_renderer* r) { return r ? r->ctx->joint_stride : 0; }
 
+int gsch_renderer_set_device_poses(gsch_renderer* r, int32_t enabled) {
+    return guarded([&] {
+        if (!r) throw std::invalid_argument("null renderer");
+        r->ctx->device_poses = enabled != 0;
+    });
+}
+
 int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
                 const gsch_render_settings* st, float* out_rgb, float* out_T, gsch_stage_times* times) {
     return guarded([&] {

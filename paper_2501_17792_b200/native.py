@@ -44,10 +44,21 @@ class GscgLodPolicy(C.Structure):
                 ("hysteresis_band_m", C.c_float)]
 
 
+GSCG_POSES_GIVEN = 0
+GSCG_POSES_SAMPLED = 1
+
+
 class GscgFrameDesc(C.Structure):
     _fields_ = [("instance_count", C.c_uint32), ("joint_stride", C.c_uint32), ("template_ids", C.c_void_p),
                 ("placement", C.c_void_p), ("poses", C.c_void_p), ("active_lod", C.c_void_p),
-                ("forced_lod", C.c_int32), ("memory", C.c_int32)]
+                ("forced_lod", C.c_int32), ("memory", C.c_int32), ("pose_source", C.c_int32),
+                ("time_s", C.c_float), ("static_pose", C.c_int32), ("motion_ids", C.c_void_p),
+                ("phase_offsets", C.c_void_p)]
+
+
+class GscgMotionDesc(C.Structure):
+    _fields_ = [("fps", C.c_float), ("frame_count", C.c_uint32), ("joint_count", C.c_uint32),
+                ("frames", C.c_void_p)]
 
 
 class GscgStageTimes(C.Structure):
@@ -121,6 +132,8 @@ GSCG_SYMBOLS = {
     "gscg_upload_skeleton": (C.c_int, [_P, C.c_uint32, _P]),
     "gscg_upload_level": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "gscg_template_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "gscg_upload_motion": (C.c_int, [_P, C.c_uint32, C.POINTER(GscgMotionDesc)]),
+    "gscg_eval_sinf": (C.c_int, [_P, _P, _P, C.c_uint32]),
     "gscg_set_debug": (C.c_int, [_P, C.c_uint32]),
     "gscg_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P,
@@ -172,6 +185,7 @@ GSCH_SYMBOLS = {
     "gsch_scene_set_motion": (C.c_int, [_P, C.c_uint32, C.c_float, C.c_uint32, C.c_uint32, _P]),
     "gsch_memory_report_cell": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(GschMemoryReport)]),
     "gsch_scene_memory_report": (C.c_int, [_P, C.POINTER(GschMemoryReport)]),
+    "gsch_renderer_set_device_poses": (C.c_int, [_P, C.c_int32]),
     "gsch_renderer_create": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "gsch_renderer_destroy": (C.c_int, [_P]),
     "gsch_renderer_gpu": (_P, [_P]),

@@ -32,7 +32,7 @@ def test_every_declared_symbol_is_exported(header, loader):
 def test_struct_layouts_match_headers():
     assert C.sizeof(N.GscgCamera) == 4 * (9 + 3 + 4 + 2)
     assert C.sizeof(N.GscgSplatRecord) == 4 * (3 + 1 + 2 + 3 + 3 + 1 + 1 + 3 + 4)
-    assert C.sizeof(N.GscgFrameDesc) == 8 + 4 * 8 + 8
+    assert C.sizeof(N.GscgFrameDesc) == 8 + 4 * 8 + 8 + 4 * 4 + 2 * 8
 
 
 @pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")

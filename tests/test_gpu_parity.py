@@ -175,6 +175,50 @@ def test_loaded_template_reuploads_and_matches(tmp_path):
     check_frame(scene, r, o, g, c)
 
 
+def test_device_sinf_replica_matches_libm():
+    import ctypes as C
+
+    from paper_2501_17792_b200 import native as N
+
+    r = P.Renderer(basic_scene())
+    bits = np.arange(0, np.float32(np.pi / 2).view(np.uint32) + 1, 53, dtype=np.uint32)
+    rng = np.random.default_rng(5)
+    x = np.concatenate([bits.view(np.float32), rng.uniform(0, np.pi / 2, 1 << 20).astype(np.float32),
+                        np.array([0.0, 1e-30, 2.4e-4, 0.785398, 0.7853982, 1.5707963, 1.5707964], np.float32)])
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    N.check_gscg(N.gscg().gscg_eval_sinf(r.gpu, x.ctypes.data, out.ctypes.data, x.size), r.gpu)
+    ref = orc.libm_sinf(x)
+    bad = np.nonzero(out.view(np.uint32) != ref.view(np.uint32))[0]
+    assert bad.size == 0, f"{bad.size} mismatches, e.g. x={x[bad[:3]]}"
+
+
+@pytest.mark.parametrize("time_s", [0.0, 0.37, 1.3, 7.9])
+def test_device_pose_sampling_is_bit_identical(time_s):
+    from paper_2501_17792_b200 import native as N
+
+    scene = basic_scene(count=16, templates=2, motions=3)
+    host, dev = P.Renderer(scene), P.Renderer(scene, device_poses=True)
+    for r in (host, dev):
+        r.set_debug(N.GSCG_DEBUG_POSED)
+    a = host.render_frame(time_s)
+    b = dev.render_frame(time_s)
+    assert host.posed_means().tobytes() == dev.posed_means().tobytes()
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    sa = host.render_frame(time_s, static_pose=True)
+    sb = dev.render_frame(time_s, static_pose=True)
+    assert sa[0].tobytes() == sb[0].tobytes()
+
+
+def test_device_pose_sampling_config2_against_oracle():
+    cfg, extra = P.baseline_config(2)
+    scene = P.Scene(cfg)
+    r = P.Renderer(scene, device_poses=True)
+    o = orc.from_scene(scene)
+    g, c = render_both(scene, r, o, 0.73)
+    check_frame(scene, r, o, g, c)
+
+
 def test_invalid_settings_raise():
     s = basic_scene(count=1, rows=1, cols=1)
     r = P.Renderer(s)
