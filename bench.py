@@ -456,7 +456,7 @@ def run_reference(args, rank, world) -> dict | None:
 
 
 def main():
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+    os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line (no version banner)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)

@@ -138,6 +138,14 @@ uint32_t gsch_renderer_joint_stride(gsch_renderer* r);
 /* Pose sampling on the GPU (GSCG_POSES_SAMPLED, bit-identical to host sampling): per frame
  * only placements, motion ids and phase offsets are uploaded. Default off (host sampling). */
 int gsch_renderer_set_device_poses(gsch_renderer* r, int32_t enabled);
+/* Uploads the scene's templates and motion clips to the renderer's context now (they are
+ * otherwise uploaded by the first render). */
+int gsch_renderer_prepare(gsch_renderer* r);
+/* Per-instance frame records for device pose sampling (any pointer may be NULL):
+ * template ids, placement (x, z, cos yaw, sin yaw; host libm), motion ids, phase offsets
+ * and active LoDs, n each (n x 4 for placement). */
+int gsch_fill_instances(gsch_renderer* r, int32_t static_pose, uint32_t* template_ids, float* placement,
+                        uint32_t* motion_ids, float* phase_offsets, uint32_t* lods);
 /* render_frame(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx) */
 int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
                 const gsch_render_settings* settings, float* out_rgb, float* out_T,

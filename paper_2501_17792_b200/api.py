@@ -350,6 +350,22 @@ class Renderer:
         N.check_gscg(N.gscg().gscg_memory_usage(self.gpu, C.byref(m)), self.gpu)
         return {f: getattr(m, f) for f, _ in m._fields_}
 
+    def prepare(self) -> None:
+        """Upload the scene's templates and motion clips now (else on the first render)."""
+        N.check_gsch(N.gsch().gsch_renderer_prepare(self._h))
+
+    def instance_records(self, static_pose: bool = False) -> dict:
+        """Per-instance records of a device-sampled frame: template_ids, placement (n x 4),
+        motion_ids, phase_offsets, lods."""
+        n = self.scene.counts()[2]
+        out = {"template_ids": np.zeros(n, np.uint32), "placement": np.zeros((n, 4), np.float32),
+               "motion_ids": np.zeros(n, np.uint32), "phase_offsets": np.zeros(n, np.float32),
+               "lods": np.zeros(n, np.uint32)}
+        N.check_gsch(N.gsch().gsch_fill_instances(
+            self._h, int(static_pose), _ptr(out["template_ids"]), _ptr(out["placement"]), _ptr(out["motion_ids"]),
+            _ptr(out["phase_offsets"]), _ptr(out["lods"])))
+        return out
+
     def sample_crowd(self, time_s: float, static_pose: bool = False, threads: int = 0):
         n = self.scene.counts()[2]
         js = self.joint_stride

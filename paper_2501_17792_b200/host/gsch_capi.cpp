@@ -372,6 +372,29 @@ gscg_ctx* gsch_renderer_gpu(gsch_renderer* r) { return r ? r->ctx->gpu() : nullp
 
 uint32_t gsch_renderer_joint_stride(gsch_renderer* r) { return r ? r->ctx->joint_stride : 0; }
 
+int gsch_fill_instances(gsch_renderer* r, int32_t static_pose, uint32_t* template_ids, float* placement,
+                        uint32_t* motion_ids, float* phase_offsets, uint32_t* lods) {
+    return guarded([&] {
+        if (!r) throw std::invalid_argument("null renderer");
+        FrameContext& c = *r->ctx;
+        c.fill_instances(r->scene->crowd, static_pose != 0);
+        const size_t n = r->scene->crowd.instances.size();
+        if (template_ids) std::memcpy(template_ids, c.template_ids.data(), n * 4);
+        if (placement) std::memcpy(placement, c.placement.data(), n * 16);
+        if (motion_ids) std::memcpy(motion_ids, c.motion_ids.data(), n * 4);
+        if (phase_offsets) std::memcpy(phase_offsets, c.phases.data(), n * 4);
+        if (lods) std::memcpy(lods, c.lods.data(), n * 4);
+    });
+}
+
+int gsch_renderer_prepare(gsch_renderer* r) {
+    return guarded([&] {
+        if (!r) throw std::invalid_argument("null renderer");
+        r->ctx->ensure_templates(r->scene->crowd.templates);
+        r->ctx->ensure_motions(r->scene->crowd.motions);
+    });
+}
+
 int gsch_renderer_set_device_poses(gsch_renderer* r, int32_t enabled) {
     return guarded([&] {
         if (!r) throw std::invalid_argument("null renderer");

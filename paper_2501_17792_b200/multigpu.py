@@ -187,17 +187,24 @@ class BandRank:
         cfg = self.scene.cfg
         n = self.scene.counts()[2]
         if frame is None:
-            tids, place, poses = self.renderer.sample_crowd(fa.time_s, fa.static_pose)
-            self._keep = (tids, place, poses)
+            # Poses are sampled on the device (bit-identical to host sampling): only the
+            # per-instance records travel.
+            self.renderer.prepare()
+            rec = self.renderer.instance_records(fa.static_pose)
+            self._keep = rec
             fd = N.GscgFrameDesc()
             fd.instance_count = n
             fd.joint_stride = self.renderer.joint_stride
-            fd.template_ids = tids.ctypes.data
-            fd.placement = place.ctypes.data
-            fd.poses = poses.ctypes.data
+            fd.template_ids = rec["template_ids"].ctypes.data
+            fd.placement = rec["placement"].ctypes.data
             fd.active_lod = self.lods.ctypes.data
             fd.forced_lod = -1 if fa.forced_lod is None else int(fa.forced_lod)
             fd.memory = N.GSCG_MEM_HOST
+            fd.pose_source = N.GSCG_POSES_SAMPLED
+            fd.time_s = fa.time_s
+            fd.static_pose = int(bool(fa.static_pose))
+            fd.motion_ids = rec["motion_ids"].ctypes.data
+            fd.phase_offsets = rec["phase_offsets"].ctypes.data
         else:
             fd = frame
         cam = self.scene.camera_basis()
@@ -290,10 +297,14 @@ class DistributedRenderer:
             recv, rc = self.exchange.all_to_all(send, self.band.counts.tolist())
             rgb, T = self.band.render_band(recv, sum(rc), rows[self.rank], rows[self.rank + 1])
             full = self.exchange.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
-        if full is None:
-            return None
-        full = full.cpu().numpy()
-        return np.ascontiguousarray(full[..., :3]), np.ascontiguousarray(full[..., 3])
+            if full is None:
+                return None
+            # one read-back into page-locked memory, then split into the API's two arrays
+            if getattr(self, "_pinned", None) is None or self._pinned.shape != full.shape:
+                self._pinned = torch.empty(full.shape, dtype=full.dtype, pin_memory=True)
+            self._pinned.copy_(full)
+        host = self._pinned.numpy()
+        return np.ascontiguousarray(host[..., :3]), np.ascontiguousarray(host[..., 3])
 
 
 def render_frame_virtual(ranks: list[BandRank], time_s: float, settings=None, static_pose: bool = False,

@@ -186,6 +186,8 @@ GSCH_SYMBOLS = {
     "gsch_memory_report_cell": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(GschMemoryReport)]),
     "gsch_scene_memory_report": (C.c_int, [_P, C.POINTER(GschMemoryReport)]),
     "gsch_renderer_set_device_poses": (C.c_int, [_P, C.c_int32]),
+    "gsch_renderer_prepare": (C.c_int, [_P]),
+    "gsch_fill_instances": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P]),
     "gsch_renderer_create": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "gsch_renderer_destroy": (C.c_int, [_P]),
     "gsch_renderer_gpu": (_P, [_P]),

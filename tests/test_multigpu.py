@@ -206,3 +206,32 @@ def test_band_api_errors():
     br.project(FrameArgs(0.0), st, (0, 9), [0, 240])
     rc = lib.gscg_render_band(br.ctx, None, 0, 8, 240, None, None, N.GSCG_MEM_DEVICE, None)
     assert rc == N.GSCG_ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.gpu
+def test_distributed_renderer_nccl_world1():
+    """The NCCL plumbing of the band path (all-to-all, gather, stream ordering) on a
+    one-rank group: the frame equals the single-GPU render byte for byte."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_17792_b200 as P
+    from paper_2501_17792_b200.multigpu import DistributedRenderer
+
+    scene = _gpu_scene()
+    st = P.RenderSettings(background=(0.05, 0.0, 0.1))
+    ref = P.Renderer(scene, device=0)
+    rgb0, T0 = ref.render_frame(0.61, st)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        dr = DistributedRenderer(scene, 0)
+        out = dr.render_frame(0.61, st)
+        assert out is not None
+        rgb, T = out
+        assert rgb.tobytes() == rgb0.tobytes() and T.tobytes() == T0.tobytes()
+        out2 = dr.render_frame(0.61, st)  # steady state reuses the pinned read-back buffer
+        assert out2[0].tobytes() == rgb0.tobytes()
+    finally:
+        dist.destroy_process_group()
