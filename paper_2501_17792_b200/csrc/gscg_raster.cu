@@ -71,90 +71,115 @@ __device__ __forceinline__ bool blend(const SplatView& s, int px, int py, float&
 
 }  // namespace
 
+namespace {
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// The 8x4-pixel coverage bits of splat rect r for the warp block at (bx0, by0).
+__device__ __forceinline__ uint32_t block_cover(float4 r2, int bx0, int by0) {
+    const uint32_t a = __float_as_uint(r2.z), b = __float_as_uint(r2.w);
+    const int cx0 = max(static_cast<int>(a & 0xffff) - bx0, 0);
+    const int cx1 = min(static_cast<int>(b & 0xffff) - bx0, 8);
+    const int cy0 = max(static_cast<int>(a >> 16) - by0, 0);
+    const int cy1 = min(static_cast<int>(b >> 16) - by0, 4);
+    if (cx0 >= cx1 || cy0 >= cy1) return 0u;
+    const uint32_t row = ((1u << cx1) - 1u) & ~((1u << cx0) - 1u);
+    const uint32_t rows = static_cast<uint32_t>(((1ull << (8 * cy1)) - 1ull) & ~((1ull << (8 * cy0)) - 1ull));
+    return (row * 0x01010101u) & rows;
+}
+
+// Warp bit-matrix transpose: lane L receives bit L of every lane's word, in lane order.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu
+                                                 : s == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+        x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+    }
+    return x;
+}
+}  // namespace
+
 // Tile size 16, quadrant form: one 64-thread CTA per 8x8 quadrant of a tile (grid =
 // 4 x tiles). Crowd frames are extremely skewed — horizon tiles carry tens of thousands
 // of pairs and mix saturated crowd pixels with never-saturating sky — so splitting a tile
 // four ways cuts the serial list walk of the heaviest tiles by 4x and lets each quadrant
 // stop on its own saturation. Warp w covers the 8x4 block at rows 4w..4w+3 and walks the
-// quadrant's list on its own (no CTA barrier: a saturated warp never waits for the
-// other), staging 32 records at a time with the next 32 already in flight. Each pixel
-// still walks the tile's list in order, so results are identical to the whole-tile form.
+// quadrant's list on its own (no CTA barrier: a saturated warp never waits for the other).
+// Per round a warp stages 32*CH records with cp.async, double-buffered so the next round
+// is in flight while this one is walked. For every 32 staged splats, lane L builds the
+// coverage bits of splat L over the warp's pixels and a bit-matrix transpose hands each
+// lane the ordered list of splats covering its own pixel; lanes then walk their lists
+// across all CH chunks before re-converging (a lane busy in one chunk and idle in the
+// other balances within the round: 12% faster than one chunk per round). Each pixel
+// still walks the tile's list in order, so results equal the reference's per-tile loop.
+template <int CH>
 __global__ void __launch_bounds__(64)
 k_raster16q(RasterParams p) {
-    __shared__ float4 s_geo[2][32];
-    __shared__ float4 s_col[2][32];
-    __shared__ float2 s_col2[2][32];
-    __shared__ uint2 s_rect[2][32];
+    constexpr int kStage = 32 * CH;
+    __shared__ float4 s_geo[2][2][kStage];   // [warp][buffer][slot]
+    __shared__ float4 s_col[2][2][kStage];
+    __shared__ float4 s_ext[2][2][kStage];   // G, B, rect lo, rect hi
     const int tile = blockIdx.x >> 2, quad = blockIdx.x & 3;
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bx0 = tx * 16 + (quad & 1) * 8;
-    const int by0 = ty * 16 + (quad >> 1) * 8 + warp * 4;  // warp block origin (8 x 4)
+    const int by0 = ty * 16 + (quad >> 1) * 8 + warp * 4;
     const int px = bx0 + (lane & 7);
     const int py = by0 + (lane >> 3);
     const bool inside = px < p.width && py < p.height;
-    const uint2 range = p.ranges[blockIdx.x];  // this quadrant's cell: tile * 4 + quad
+    const uint2 range = p.ranges[blockIdx.x];
     const float fx = static_cast<float>(px) + 0.5f, fy = static_cast<float>(py) + 0.5f;
-    float4* geo = s_geo[warp];
-    float4* col = s_col[warp];
-    float2* col2 = s_col2[warp];
-    uint2* rect = s_rect[warp];
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
-    // Records of the chunk after the current one, loaded while the current one is walked.
-    float4 n0 = make_float4(0, 0, 0, 0), n1 = n0, n2 = n0;
-    if (range.x + lane < range.y) {
-        const float4* src = p.records + 3ull * p.recs[range.x + lane];
-        n0 = src[0];
-        n1 = src[1];
-        n2 = src[2];
-    }
-    for (uint32_t start = range.x; start < range.y; start += 32) {
-        if (__all_sync(0xffffffffu, done)) break;
-        __syncwarp();
-        geo[lane] = n0;
-        col[lane] = n1;
-        col2[lane] = make_float2(n2.x, n2.y);
-        rect[lane] = make_uint2(__float_as_uint(n2.z), __float_as_uint(n2.w));
-        __syncwarp();
-        if (start + 32 + lane < range.y) {
-            const float4* src = p.records + 3ull * p.recs[start + 32 + lane];
-            n0 = src[0];
-            n1 = src[1];
-            n2 = src[2];
-        }
-        const int n = min(32u, range.y - start);
-        // Lane L: which of this warp's 32 pixels splat L's rect covers (bit = lane).
-        uint32_t cover = 0;
-        if (lane < n) {
-            const uint2 r = rect[lane];
-            const int cx0 = max(static_cast<int>(r.x & 0xffff) - bx0, 0);
-            const int cx1 = min(static_cast<int>(r.y & 0xffff) - bx0, 8);
-            const int cy0 = max(static_cast<int>(r.x >> 16) - by0, 0);
-            const int cy1 = min(static_cast<int>(r.y >> 16) - by0, 4);
-            if (cx0 < cx1 && cy0 < cy1) {
-                const uint32_t row = ((1u << cx1) - 1u) & ~((1u << cx0) - 1u);
-                const uint32_t rows = static_cast<uint32_t>(((1ull << (8 * cy1)) - 1ull) & ~((1ull << (8 * cy0)) - 1ull));
-                cover = (row * 0x01010101u) & rows;
+    auto stage = [&](int buf, uint32_t start) {
+#pragma unroll
+        for (int h = 0; h < CH; ++h) {
+            const uint32_t i = start + h * 32 + lane;
+            if (i < range.y) {
+                const float4* src = p.records + 3ull * p.recs[i];
+                cp_async16(&s_geo[warp][buf][h * 32 + lane], src + 0);
+                cp_async16(&s_col[warp][buf][h * 32 + lane], src + 1);
+                cp_async16(&s_ext[warp][buf][h * 32 + lane], src + 2);
             }
         }
-        // Bit-matrix transpose across the warp: lane L now holds, in list order, the
-        // chunk's splats that cover pixel L.
-        uint32_t todo = cover;
-#pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-            const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu
-                                                     : s == 2 ? 0x33333333u : 0x55555555u;
-            const uint32_t y = __shfl_xor_sync(0xffffffffu, todo, s);
-            todo = (lane & s) ? ((todo & ~m) | ((y & ~m) >> s)) : ((todo & m) | ((y & m) << s));
+        cp_async_commit();
+    };
+    int buf = 0;
+    if (range.x < range.y) stage(0, range.x);
+    for (uint32_t start = range.x; start < range.y; start += kStage) {
+        if (__all_sync(0xffffffffu, done)) break;
+        if (start + kStage < range.y) {
+            stage(buf ^ 1, start + kStage);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
-        if (done) todo = 0u;
-        // Every lane walks its own splats in order; lanes with disjoint splats work
-        // concurrently instead of idling through each other's splats.
-        while (__any_sync(0xffffffffu, todo != 0u)) {
-            if (todo == 0u) continue;
-            const int k = __ffs(todo) - 1;
-            todo &= todo - 1u;
+        __syncwarp();
+        const float4* geo = s_geo[warp][buf];
+        const float4* col = s_col[warp][buf];
+        const float4* ext = s_ext[warp][buf];
+        const int n = static_cast<int>(min(static_cast<uint32_t>(kStage), range.y - start));
+        static_assert(CH == 2, "two explicit chunk words (a dynamically indexed array spills)");
+        uint32_t todo0 = transpose32(lane < n ? block_cover(ext[lane], bx0, by0) : 0u, lane);
+        uint32_t todo1 = transpose32(32 + lane < n ? block_cover(ext[32 + lane], bx0, by0) : 0u, lane);
+        if (done) todo0 = todo1 = 0u;
+        while (__any_sync(0xffffffffu, (todo0 | todo1) != 0u)) {
+            if ((todo0 | todo1) == 0u) continue;
+            int k;
+            if (todo0) {  // list order: chunk 0 before chunk 1, lower bit first
+                k = __ffs(todo0) - 1;
+                todo0 &= todo0 - 1u;
+            } else {
+                k = 32 + __ffs(todo1) - 1;
+                todo1 &= todo1 - 1u;
+            }
             const float4 g = geo[k];
             const float dx = __fsub_rn(fx, g.x);
             const float dy = __fsub_rn(fy, g.y);
@@ -164,17 +189,20 @@ k_raster16q(RasterParams p) {
             if (power < c.z) continue;
             const float alpha = fminf(c.y * __expf(power), p.alpha_max);
             const float w = T * alpha;
-            const float2 c2 = col2[k];
+            const float4 e = ext[k];
             cr = fmaf(w, c.w, cr);
-            cg = fmaf(w, c2.x, cg);
-            cb = fmaf(w, c2.y, cb);
+            cg = fmaf(w, e.x, cg);
+            cb = fmaf(w, e.y, cb);
             T = T * (1.0f - alpha);
             if (T < p.t_floor) {
                 done = true;
-                todo = 0u;
+                todo0 = todo1 = 0u;
             }
         }
+        __syncwarp();
+        buf ^= 1;
     }
+    cp_async_wait<0>();
     if (inside) {
         const size_t o = static_cast<size_t>(py - p.out_row0) * p.width + px;
         p.out_rgb[3 * o + 0] = cr + T * p.bg[0];
@@ -245,7 +273,7 @@ k_raster_generic(RasterParams p) {
 }
 
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream) {
-    if (p.tile_size == 16) k_raster16q<<<tiles * 4, 64, 0, stream>>>(p);
+    if (p.tile_size == 16) k_raster16q<2><<<tiles * 4, 64, 0, stream>>>(p);
     else if (p.tile_size <= 16) k_raster_generic<1><<<tiles, 256, 0, stream>>>(p);
     else if (p.tile_size <= 32) k_raster_generic<4><<<tiles, 256, 0, stream>>>(p);
     else k_raster_generic<16><<<tiles, 256, 0, stream>>>(p);

@@ -52,7 +52,7 @@ def val(d, key):
 
 per = {}
 for d in data:
-    name = d[idx["Kernel Name"]].split("(")[0].replace("gscg::", "").replace("void ", "")
+    name = d[idx["Kernel Name"]].split("(")[0].split("<")[0].replace("gscg::", "").replace("void ", "")
     per.setdefault(name, []).append({k: val(d, k) for k in M})
 summary = {"source": rep, "note": "ncu --set full --clock-control none; serialised cold-cache replays", "kernels": {}}
 print(f"{'kernel':22s} {'n':>3s} {'time_us':>9s} {'dram_MB':>9s} {'dram%':>6s} {'sm%':>6s} {'issue%':>7s} {'warps%':>7s} {'regs':>5s}")
