@@ -210,6 +210,16 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
 int gscg_host_alloc(uint64_t bytes, void** out);
 int gscg_host_free(void* ptr);
 
+/* Device memory on the context's GPU (e.g. framebuffers gscg_render_frame writes into:
+ * its fb_rgb / fb_T may be host or device pointers in either memory mode). */
+int gscg_device_alloc(gscg_ctx* ctx, uint64_t bytes, void** out);
+int gscg_device_free(gscg_ctx* ctx, void* ptr);
+
+/* PSNR of two images of `floats` floats (host or device pointers) as the reference's
+ * psnr (metrics.cpp:8-23): 10 log10(1 / MSE) over all channels, squared error summed in
+ * double on the device (deterministic order), 99 dB for identical images. */
+int gscg_psnr(gscg_ctx* ctx, const float* a, const float* b, uint64_t floats, float* out_db);
+
 /* Device pointers of the context's framebuffer (valid until the next render). */
 int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T);
 int gscg_synchronize(gscg_ctx* ctx);

@@ -120,6 +120,22 @@ int gsch_scene_load_template(gsch_scene* scene, uint32_t template_id, const char
 int gsch_scene_save_motion(const gsch_scene* scene, uint32_t motion_id, const char* path);
 int gsch_scene_load_motion(gsch_scene* scene, uint32_t motion_id, const char* path);
 
+/* Metrics (reference metrics.hpp:13-31). gsch_psnr is the reference's CPU psnr over two
+ * width x height x 3 images. gsch_lod_quality_sweep renders one bind-posed character of
+ * the template per (distance, level) on GPU `device` with the scene camera's fov, size and
+ * near plane, and scores each level against level 0 with the on-device PSNR (gscg_psnr);
+ * rows = count x levels (query with rows = NULL). */
+typedef struct {
+  float distance_m;
+  uint32_t level;
+  uint32_t gaussian_count;
+  float psnr_db;
+} gsch_quality_row;
+int gsch_psnr(const float* a, const float* b, uint32_t width, uint32_t height, float* out_db);
+int gsch_lod_quality_sweep(gsch_scene* scene, uint32_t template_id, const float* distances, uint32_t count,
+                           const gsch_render_settings* settings, int device, gsch_quality_row* rows,
+                           uint32_t capacity, uint32_t* row_count);
+
 /* Shared-attribute memory accounting (crowd.cpp:142-210, MemoryLayoutModel defaults). */
 typedef struct {
   uint64_t naive_bytes, shared_bytes;

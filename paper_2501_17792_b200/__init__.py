@@ -7,8 +7,8 @@ include/gscg.h. The C++ host API (host/gsc, C-ABI include/gsch.h) keeps the refe
 template / instance / camera interface; this package is its Python face.
 """
 from .api import (RenderSettings, Renderer, Scene, SceneConfig, StageTimes, baseline_config,  # noqa: F401
-                  place_origin_instance, render_frame)
+                  place_origin_instance, psnr, render_frame)
 from .native import FormatError, NativeError  # noqa: F401
 
 __all__ = ["RenderSettings", "Renderer", "Scene", "SceneConfig", "StageTimes", "baseline_config",
-           "place_origin_instance", "render_frame", "NativeError", "FormatError"]
+           "place_origin_instance", "psnr", "render_frame", "NativeError", "FormatError"]

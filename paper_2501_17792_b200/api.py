@@ -247,6 +247,22 @@ class Scene:
         N.check_gsch(N.gsch().gsch_scene_load_motion(self._h, m, str(path).encode()))
         return m
 
+    def lod_quality_sweep(self, template_id: int, distances, settings: Optional[RenderSettings] = None,
+                          device: int = 0) -> list[dict]:
+        """PSNR of every LoD level against level 0 for one bind-posed character at each
+        distance (reference lod_quality_sweep, metrics.cpp:25-75), rendered and scored on GPU."""
+        settings = settings or RenderSettings()
+        d = np.ascontiguousarray(distances, dtype=np.float32)
+        n = C.c_uint32()
+        st = settings.native()
+        N.check_gsch(N.gsch().gsch_lod_quality_sweep(self._h, template_id, _ptr(d), d.size, C.byref(st), device,
+                                                     None, 0, C.byref(n)))
+        rows = (N.GschQualityRow * max(n.value, 1))()
+        N.check_gsch(N.gsch().gsch_lod_quality_sweep(self._h, template_id, _ptr(d), d.size, C.byref(st), device,
+                                                     rows, n.value, C.byref(n)))
+        return [{"distance_m": r.distance_m, "level": r.level, "gaussian_count": r.gaussian_count,
+                 "psnr_db": r.psnr_db} for r in rows[:n.value]]
+
     def memory_report(self) -> dict:
         r = N.GschMemoryReport()
         N.check_gsch(N.gsch().gsch_scene_memory_report(self._h, C.byref(r)))
@@ -269,6 +285,17 @@ def memory_report_cell(instances: int, gaussians: int, fixed_overhead: int = 0) 
     r = N.GschMemoryReport()
     N.check_gsch(N.gsch().gsch_memory_report_cell(instances, gaussians, fixed_overhead, C.byref(r)))
     return _report(r)
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    """The reference's PSNR (metrics.cpp:8-23) on the host: two H x W x 3 float images."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError("psnr: dimension mismatch")
+    out = C.c_float()
+    N.check_gsch(N.gsch().gsch_psnr(_ptr(a), _ptr(b), a.shape[1], a.shape[0], C.byref(out)))
+    return out.value
 
 
 def pinned_array(shape, dtype=np.float32) -> np.ndarray:

@@ -723,9 +723,11 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
 void copy_out(gscg_ctx* ctx, int rows, float* fb_rgb, float* fb_T, bool host) {
     cudaStream_t s = ctx->stream;
     const size_t px = static_cast<size_t>(ctx->geom.W) * rows;
-    const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    if (fb_rgb && px) CUDA_TRY(cudaMemcpyAsync(fb_rgb, ctx->fb_rgb.ptr, px * 12, kind, s));
-    if (fb_T && px) CUDA_TRY(cudaMemcpyAsync(fb_T, ctx->fb_T.ptr, px * 4, kind, s));
+    // Destinations may be host (pinned or pageable) or device memory in either mode: the
+    // direction comes from unified addressing.
+    (void)host;
+    if (fb_rgb && px) CUDA_TRY(cudaMemcpyAsync(fb_rgb, ctx->fb_rgb.ptr, px * 12, cudaMemcpyDefault, s));
+    if (fb_T && px) CUDA_TRY(cudaMemcpyAsync(fb_T, ctx->fb_T.ptr, px * 4, cudaMemcpyDefault, s));
 }
 
 void fill_times(gscg_ctx* ctx, gscg_stage_times* times, uint32_t passes, uint32_t launches) {
@@ -1169,6 +1171,63 @@ int gscg_eval_sinf(gscg_ctx* ctx, const float* in, float* out, uint32_t n) {
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         a.release();
         b.release();
+    });
+}
+
+int gscg_device_alloc(gscg_ctx* ctx, uint64_t bytes, void** out) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        CUDA_TRY(cudaMalloc(out, std::max<uint64_t>(bytes, 1)));
+    });
+}
+
+int gscg_device_free(gscg_ctx* ctx, void* ptr) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (ptr) CUDA_TRY(cudaFree(ptr));
+    });
+}
+
+int gscg_psnr(gscg_ctx* ctx, const float* a, const float* b, uint64_t floats, float* out_db) {
+    if (!ctx || !out_db || (floats && (!a || !b))) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        if (floats == 0) invalid("psnr: empty images");
+        // Host inputs are staged to the device; device inputs are read in place.
+        DevBuf ta, tb, part;
+        auto on_device = [&](const float* p, DevBuf& tmp) -> const float* {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice) return p;
+            cudaGetLastError();
+            CUDA_TRY(tmp.ensure_exact(floats * 4));
+            CUDA_TRY(cudaMemcpyAsync(tmp.ptr, p, floats * 4, cudaMemcpyDefault, s));
+            return tmp.as<float>();
+        };
+        const float* da = on_device(a, ta);
+        const float* db = on_device(b, tb);
+        CUDA_TRY(part.ensure_exact((kSseBlocks + 1) * sizeof(double)));
+        k_sse_partial<<<kSseBlocks, kSseThreads, 0, s>>>(da, db, floats, part.as<double>());
+        k_sse_final<<<1, kSseThreads, 0, s>>>(part.as<double>(), kSseBlocks, part.as<double>() + kSseBlocks);
+        CUDA_TRY(cudaGetLastError());
+        double sse = 0.0;
+        CUDA_TRY(cudaMemcpyAsync(&sse, part.as<double>() + kSseBlocks, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        // PSNR as the reference (metrics.cpp:8-23): 99 dB cap for identical images.
+        constexpr float kCap = 99.0f;
+        if (sse == 0.0) {
+            *out_db = kCap;
+        } else {
+            const double mse = sse / static_cast<double>(floats);
+            *out_db = std::min(static_cast<float>(10.0 * std::log10(1.0 / mse)), kCap);
+        }
+        ta.release();
+        tb.release();
+        part.release();
     });
 }
 

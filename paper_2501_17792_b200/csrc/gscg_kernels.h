@@ -188,6 +188,12 @@ __global__ void k_band_count(BandParams p);
 __global__ void k_band_pack(BandParams p);
 __global__ void k_band_unpack(BandUnpackParams p);
 
+// metrics
+constexpr int kSseThreads = 256;
+constexpr uint32_t kSseBlocks = 1024;
+__global__ void k_sse_partial(const float* a, const float* b, uint64_t n, double* partial);
+__global__ void k_sse_final(const double* partial, uint32_t blocks, double* out);
+
 // raster
 // Picks the tile-size specialisation (16: 8x8 quadrant CTAs; else 1/4/16 pixels per thread).
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream);

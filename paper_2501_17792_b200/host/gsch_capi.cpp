@@ -1,6 +1,7 @@
 // C-ABI of the host scene layer (include/gsch.h) over the gsc host API.
 #include "gsch.h"
 #include "gsc/io.hpp"
+#include "gsc/metrics.hpp"
 
 #include <cstring>
 #include <string>
@@ -399,6 +400,49 @@ int gsch_renderer_set_device_poses(gsch_renderer* r, int32_t enabled) {
     return guarded([&] {
         if (!r) throw std::invalid_argument("null renderer");
         r->ctx->device_poses = enabled != 0;
+    });
+}
+
+static RenderSettings to_settings(const gsch_render_settings* st) {
+    RenderSettings rs;
+    rs.tile_size = st->tile_size;
+    rs.background = v3(st->background);
+    rs.alpha_max = st->alpha_max;
+    rs.alpha_cutoff = st->alpha_cutoff;
+    rs.transmittance_floor = st->transmittance_floor;
+    rs.thread_count = st->thread_count;
+    rs.sh_colour = st->sh_colour != 0;
+    return rs;
+}
+
+int gsch_psnr(const float* a, const float* b, uint32_t width, uint32_t height, float* out_db) {
+    return guarded([&] {
+        if (!a || !b || !out_db) throw std::invalid_argument("null argument");
+        Framebuffer fa(static_cast<int>(width), static_cast<int>(height)), fb(static_cast<int>(width), static_cast<int>(height));
+        std::memcpy(fa.rgb.data(), a, fa.rgb.size() * 4);
+        std::memcpy(fb.rgb.data(), b, fb.rgb.size() * 4);
+        *out_db = psnr(fa, fb);
+    });
+}
+
+int gsch_lod_quality_sweep(gsch_scene* s, uint32_t template_id, const float* distances, uint32_t count,
+                           const gsch_render_settings* st, int device, gsch_quality_row* rows, uint32_t capacity,
+                           uint32_t* row_count) {
+    return guarded([&] {
+        if (!s || !st || (count && !distances) || !row_count) throw std::invalid_argument("null argument");
+        if (template_id >= s->templates->size()) throw std::invalid_argument("template id beyond the store");
+        const AvatarTemplate& tpl = (*s->templates)[template_id];
+        *row_count = count * static_cast<uint32_t>(tpl.levels.size());
+        if (!rows) return;  // size query
+        if (capacity < *row_count) throw std::invalid_argument("row buffer too small");
+        const QualityTable t = lod_quality_sweep(tpl, std::span<const float>(distances, count), s->camera,
+                                                 to_settings(st), device);
+        for (size_t i = 0; i < t.size(); ++i) {
+            rows[i].distance_m = t[i].distance_m;
+            rows[i].level = t[i].level;
+            rows[i].gaussian_count = t[i].gaussian_count;
+            rows[i].psnr_db = t[i].psnr_db;
+        }
     });
 }
 

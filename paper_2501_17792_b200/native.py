@@ -139,6 +139,9 @@ GSCG_SYMBOLS = {
                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P,
                                     C.POINTER(GscgStageTimes)]),
     "gscg_memory_usage": (C.c_int, [_P, C.POINTER(GscgMemoryUsage)]),
+    "gscg_device_alloc": (C.c_int, [_P, C.c_uint64, C.POINTER(_P)]),
+    "gscg_device_free": (C.c_int, [_P, _P]),
+    "gscg_psnr": (C.c_int, [_P, _P, _P, C.c_uint64, C.POINTER(C.c_float)]),
     "gscg_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
     "gscg_host_free": (C.c_int, [_P]),
     "gscg_framebuffer_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),
@@ -162,7 +165,16 @@ GSCG_SYMBOLS = {
 
 GSCH_ERR_FORMAT = -6
 
+
+class GschQualityRow(C.Structure):
+    _fields_ = [("distance_m", C.c_float), ("level", C.c_uint32), ("gaussian_count", C.c_uint32),
+                ("psnr_db", C.c_float)]
+
+
 GSCH_SYMBOLS = {
+    "gsch_psnr": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, C.POINTER(C.c_float)]),
+    "gsch_lod_quality_sweep": (C.c_int, [_P, C.c_uint32, _P, C.c_uint32, _P, C.c_int, _P, C.c_uint32,
+                                         C.POINTER(C.c_uint32)]),
     "gsch_scene_save_template": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
     "gsch_scene_load_template": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
     "gsch_scene_save_motion": (C.c_int, [_P, C.c_uint32, C.c_char_p]),

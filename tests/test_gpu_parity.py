@@ -219,6 +219,28 @@ def test_device_pose_sampling_config2_against_oracle():
     check_frame(scene, r, o, g, c)
 
 
+def test_lod_quality_sweep_on_device_matches_host_psnr():
+    cfg = P.SceneConfig(template_count=1, template_seed_base=9, level_counts=(4000, 900, 200), with_sh=True,
+                        motion_count=1, motion_frames=10, grid_rows=1, grid_cols=1, crowd_count=1,
+                        width=256, height=192, fov_y_deg=45.0)
+    scene = P.Scene(cfg)
+    dists = [2.0, 6.0]
+    rows = scene.lod_quality_sweep(0, dists)
+    assert len(rows) == 6 and all(r["level"] == i % 3 for i, r in enumerate(rows))
+    assert [r["gaussian_count"] for r in rows[:3]] == [4000, 900, 200]
+    P.place_origin_instance(scene)
+    r = P.Renderer(scene)
+    for k, d in enumerate(dists):
+        scene.set_camera((0.0, 0.95, -d), (0.0, 0.95, 0.0), 45.0, 256, 192)
+        frames = [r.render_frame(0.0, static_pose=True, forced_lod=l)[0] for l in range(3)]
+        for l in range(3):
+            got = rows[3 * k + l]["psnr_db"]
+            want = 99.0 if l == 0 else P.psnr(frames[l], frames[0])
+            assert abs(got - want) < 1e-3, (d, l, got, want)
+            if l:
+                assert got < 99.0
+
+
 def test_invalid_settings_raise():
     s = basic_scene(count=1, rows=1, cols=1)
     r = P.Renderer(s)

@@ -259,3 +259,20 @@ def test_memory_model_marginal_slopes():
         assert hi["shared_bytes"] - lo["shared_bytes"] == 12 * 3176
     zero = memory_report_cell(0, 12661, 1 << 20)
     assert zero["shared_bytes"] == zero["naive_bytes"] == 1 << 20
+
+
+def test_psnr_reference_definition():
+    import paper_2501_17792_b200 as P
+
+    rng = np.random.default_rng(3)
+    a = rng.random((6, 7, 3), dtype=np.float32)
+    assert P.psnr(a, a.copy()) == 99.0  # identical -> cap
+    b = a.copy()
+    b[2, 3, 1] += 0.25
+    want = 10 * np.log10(1.0 / np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    assert abs(P.psnr(a, b) - want) < 1e-4
+    c = a.copy()
+    c[0, 0, 0] += 1e-9  # below float resolution at that value? still capped only if identical
+    assert P.psnr(a, c) <= 99.0
+    with pytest.raises(ValueError):
+        P.psnr(a, a[:, :-1])
