@@ -28,13 +28,15 @@ def main():
     scene = P.Scene(cfg)
     if extra["origin_instance"]:
         P.place_origin_instance(scene)
-    r = P.Renderer(scene, device=0)
+    r = P.Renderer(scene, device=0, device_poses=True)
+    r.prepare()  # templates + motion tables
     n = scene.counts()[2]
     dev = torch.device("cuda", 0)
-    tids, place, poses = r.sample_crowd(extra["time_s"])
-    d_tids = torch.from_numpy(tids.view(np.int32)).to(dev)
-    d_place = torch.from_numpy(place).to(dev)
-    d_poses = torch.from_numpy(poses).to(dev)
+    rec = r.instance_records()
+    d_tids = torch.from_numpy(rec["template_ids"].view(np.int32)).to(dev)
+    d_place = torch.from_numpy(rec["placement"]).to(dev)
+    d_mid = torch.from_numpy(rec["motion_ids"].view(np.int32)).to(dev)
+    d_phase = torch.from_numpy(rec["phase_offsets"]).to(dev)
     d_lods = torch.full((max(n, 1),), -1, dtype=torch.int32, device=dev)
     cam = scene.camera_basis()
     rs = gscg_settings(P.RenderSettings())
@@ -46,11 +48,14 @@ def main():
     fd.instance_count = n
     fd.joint_stride = r.joint_stride
     fd.template_ids, fd.placement = d_tids.data_ptr(), d_place.data_ptr()
-    fd.poses, fd.active_lod = d_poses.data_ptr(), d_lods.data_ptr()
+    fd.active_lod = d_lods.data_ptr()
     fd.forced_lod = -1 if extra["forced_lod"] is None else extra["forced_lod"]
     fd.memory = N.GSCG_MEM_DEVICE
+    fd.pose_source = N.GSCG_POSES_SAMPLED  # poses sampled on the device, as bench.py
+    fd.motion_ids, fd.phase_offsets = d_mid.data_ptr(), d_phase.data_ptr()
     lib = N.gscg()
     for f in range(args.frames):
+        fd.time_s = extra["time_s"] + f / 30.0
         st = N.GscgStageTimes()
         N.check_gscg(lib.gscg_render_frame(r.gpu, C.byref(fd), C.byref(cam), C.byref(rs), C.byref(lp), None, None,
                                            C.byref(st)), r.gpu)
