@@ -63,6 +63,7 @@ k_project(ProjectParams p) {
     float* s_sh = reinterpret_cast<float*>(s_dyn);
     float* s_mats = s_sh + (p.sh_enabled ? kProjectThreads * kShFloats : 0);
     __shared__ uint32_t s_item_start[kMaxGroups + 1];
+    __shared__ uint32_t s_member[kBatch], s_member_base[kBatch];  // batch instance ids, ordinal bases
     __shared__ uint32_t s_wcnt[kProjectThreads / 32];
     __shared__ unsigned long long s_base;
     __shared__ uint32_t s_item;
@@ -129,6 +130,11 @@ k_project(ProjectParams p) {
             const float* src = p.skin + static_cast<size_t>(p.members[inst_begin + k]) * p.joint_stride * 12;
             copy_async16(s_mats + 4 * e, src + 4 * r);
         }
+        if (tid < static_cast<int>(inst_count)) {
+            const uint32_t m = p.members[inst_begin + tid];
+            s_member[tid] = m;
+            s_member_base[tid] = p.inst_base[m];
+        }
         copy_async_wait_all();
         __syncthreads();
         const uint32_t i01 = __float_as_uint(c3.z), i23 = __float_as_uint(c3.w);
@@ -136,7 +142,7 @@ k_project(ProjectParams p) {
         const float wk[4] = {wv.x, wv.y, wv.z, wv.w};
 
         for (uint32_t k = 0; k < inst_count; ++k) {
-            const uint32_t inst = p.members[inst_begin + k];
+            const uint32_t inst = s_member[k];
             const float* s_inst = s_mats + k * p.joint_stride * 12;
 
             bool survive = false;
@@ -260,7 +266,7 @@ k_project(ProjectParams p) {
             if (tid == 0) s_base = atomicAdd(&p.counters->splat_pair, static_cast<unsigned long long>(total) << 32) >> 32;
             __syncthreads();
             const unsigned long long base = s_base;
-            const uint32_t ordinal = gvalid ? p.inst_base[inst] + gi : 0u;
+            const uint32_t ordinal = gvalid ? s_member_base[k] + gi : 0u;
             if (p.posed_debug && gvalid) {
                 p.posed_debug[3ull * ordinal + 0] = ax;
                 p.posed_debug[3ull * ordinal + 1] = ay;
