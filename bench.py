@@ -312,7 +312,9 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
 
     # ---- end-to-end through the public API (host poses + pinned H2D + kernels + D2H) ----
     if not band_path:
-        out_frame = r.alloc_frame(pinned=True)  # the frame is read back into page-locked memory
+        # The frame (the reference render_frame's Framebuffer: RGB) is read back into
+        # page-locked memory every step.
+        out_frame = (r.alloc_frame(pinned=True)[0], None)
 
         def e2e_frame(f):
             r.render_frame(times_s[f], settings, forced_lod=forced, out=out_frame)
@@ -337,7 +339,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         e2e_s = float(t.item())
     e2e_fps = args.steps / e2e_s
     h2d = n * (4 + 16 + 4 + 4 + 4)  # template id, placement, previous LoD, motion id, phase offset
-    d2h = cfg.width * cfg.height * 16 + n * 4
+    d2h = cfg.width * cfg.height * (12 if not band_path else 16) + n * 4
 
     if dist:
         tot = torch.tensor([float(counts[1])], dtype=torch.float64, device=dev)

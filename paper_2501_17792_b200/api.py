@@ -351,7 +351,9 @@ class Renderer:
     def render_frame(self, time_s: float, settings: Optional[RenderSettings] = None, static_pose: bool = False,
                      forced_lod: Optional[int] = None, times: Optional[StageTimes] = None, out=None):
         """Renders one frame; returns (rgb, T). `out` = (rgb, T) arrays to fill (e.g. from
-        alloc_frame(pinned=True)), else fresh arrays are returned."""
+        alloc_frame(pinned=True)), else fresh arrays are returned. With out = (rgb, None)
+        only the colour is read back (the reference render_frame returns just the
+        Framebuffer; T is rasterize_full's extra output) and T is returned as None."""
         settings = settings or RenderSettings()
         W, H = self.scene.cfg.width, self.scene.cfg.height
         if out is None:
@@ -359,12 +361,13 @@ class Renderer:
             T = np.empty((H, W), dtype=np.float32)
         else:
             rgb, T = out
-            if rgb.shape != (H, W, 3) or T.shape != (H, W) or rgb.dtype != np.float32 or T.dtype != np.float32 \
-                    or not rgb.flags.c_contiguous or not T.flags.c_contiguous:
+            if rgb.shape != (H, W, 3) or rgb.dtype != np.float32 or not rgb.flags.c_contiguous or (
+                    T is not None and (T.shape != (H, W) or T.dtype != np.float32 or not T.flags.c_contiguous)):
                 raise ValueError("out must be C-contiguous float32 arrays of shape (H, W, 3) and (H, W)")
         st = N.GschStageTimes()
         N.check_gsch(N.gsch().gsch_render(self._h, time_s, int(static_pose), -1 if forced_lod is None else forced_lod,
-                                          C.byref(settings.native()), _ptr(rgb), _ptr(T), C.byref(st)))
+                                          C.byref(settings.native()), _ptr(rgb), None if T is None else _ptr(T),
+                                          C.byref(st)))
         if times is not None:
             for f in ("update_ms", "gather_ms", "sort_ms", "rasterize_ms", "pose_ms", "splat_count", "pair_count",
                       "gaussian_count"):

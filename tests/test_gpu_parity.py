@@ -145,6 +145,9 @@ def test_pinned_output_matches_fresh_arrays():
     assert rgb.tobytes() == rgb2.tobytes() and T.tobytes() == T2.tobytes()
     with pytest.raises(ValueError):
         r2.render_frame(0.5, st, out=(out[0][:, :-1], out[1]))
+    out[0][:] = 0
+    rgb3, T3 = r2.render_frame(0.5, st, out=(out[0], None))  # colour only, as the reference render_frame
+    assert T3 is None and rgb3.tobytes() == rgb.tobytes()
 
 
 def test_memory_usage_counts_the_shared_store_once():
