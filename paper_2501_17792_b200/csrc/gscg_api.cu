@@ -6,8 +6,8 @@
 //   update:    k_lod_plan (1 CTA) -> k_fk_skin
 //   gather:    k_project (persistent, template-major)       -> counters readback (sync)
 //   sort:      splats by depth (k_sort_{upsweep,rows,bases,downsweep} x P) ->
-//              ties by ordinal + spans in sorted order (k_sorted_spans) ->
-//              pairs in that order (k_scan_sums, k_emit_pairs) ->
+//              ties by ordinal + spans + first cell digit histogram (k_sorted_spans) ->
+//              pairs scattered in first-cell-pass order (k_sort_rows, k_emit_scatter) ->
 //              pairs stably by cell (radix x P') -> k_cell_ranges
 //   rasterize: k_raster16q (or k_raster_generic for other tile sizes)
 //   D2H of framebuffer / transmittance / active LoDs (host mode)
@@ -665,24 +665,42 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         // 1. splats by depth (bits that vary in the frame), ties by ordinal.
         const RadixPlan dplan = make_plan(static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax)));
         const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
-        // 2. equal-depth runs by ordinal, cell spans in sorted order, pairs per 1024 splats.
+        // 2. equal-depth runs by ordinal + cell spans in sorted order + the first cell-sort
+        //    digit histogram per 1024 sorted splats; digit offsets; pairs emitted straight
+        //    into the order of the first stable cell-sort pass.
+        const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
+        const uint32_t dmask = (1u << cplan.bits[0]) - 1u;
         const uint32_t sblocks = (S32 + 1023) / 1024;
         CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
-        CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * 4));
-        CUDA_TRY(cudaMemsetAsync(ctx->block_sums.ptr, 0, static_cast<size_t>(sblocks) * 4, s));
-        static_assert(kMetaThreads * kStreamItems == 1024, "one pair block per CTA");
+        CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * kRadix * 4));
+        static_assert(kMetaThreads * kStreamItems == 1024, "one splat block per CTA");
+        const int quads = geo.cells_per_tile == 4 ? 1 : 0;
         k_sorted_spans<<<sblocks, kMetaThreads, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
-                                                        ctx->splat_meta.as<uint4>(), S32, ctx->span_sorted.as<uint2>(),
-                                                        ctx->block_sums.as<uint32_t>());
-        k_scan_sums<<<1, 1024, 0, s>>>(ctx->block_sums.as<uint32_t>(), sblocks);
-        k_emit_pairs<<<sblocks, kEmitThreads, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
-                                              ctx->block_sums.as<uint32_t>(), geo.tiles_x, geo.cells_per_tile == 4 ? 1 : 0,
-                                              ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
-        launches += 4;
+                                                        ctx->splat_meta.as<uint4>(), S32, ctx->span_sorted.as<uint2>());
+        launch_emit(true, sblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
+                    ctx->block_sums.as<uint32_t>(), nullptr, geo.tiles_x, quads, dmask, nullptr, nullptr);
+        SortPassParams bp{};
+        bp.counts = ctx->block_sums.as<uint32_t>();
+        bp.digit_base = ctx->hist.as<uint32_t>();
+        bp.tiles = sblocks;
+        bp.bits = cplan.bits[0];
+        k_sort_rows<<<dmask + 1, 1024, 0, s>>>(bp);
+        launch_emit(false, sblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
+                    ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), geo.tiles_x, quads, dmask,
+                    ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
+        ++launches;
+        launches += 3;
         CUDA_TRY(cudaGetLastError());
-        // 3. pairs stably by cell id; ranges.
-        const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
-        const int cb = radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell, ctx->precs, K, cplan);
+        // 3. the remaining stable cell-sort passes; ranges.
+        RadixPlan rest{};
+        for (uint32_t q = 1; q < cplan.passes; ++q) {
+            rest.shift[rest.passes] = cplan.shift[q];
+            rest.bits[rest.passes] = cplan.bits[q];
+            ++rest.passes;
+        }
+        const int cb = rest.passes ? radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell,
+                                           ctx->precs, K, rest)
+                                   : 1;
         const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);
         k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
         ++launches;

@@ -146,16 +146,22 @@ __global__ void k_sort_upsweep(SortPassParams p);
 __global__ void k_sort_rows(SortPassParams p);
 __global__ void k_sort_downsweep(SortPassParams p);
 
-constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat pair block
+constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
 __global__ void k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
-                               uint2* span_sorted, uint32_t* block_sums);
-__global__ void k_scan_sums(uint32_t* sums, uint32_t n);
-__global__ void k_emit_pairs(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted,
-                             const uint32_t* block_offsets, int tiles_x, int quads, uint32_t* pair_cell,
-                             uint32_t* pair_rec);
+                               uint2* span_sorted);
+constexpr int kEmitThreads = 256;  // k_emit_scatter: 4 sorted splats per thread
+constexpr uint32_t kEmitStage = 4096;  // pairs per block staged in shared memory for coalesced writes
+constexpr int kEmitSmem = (32 * kEmitThreads + 2 * kEmitStage) * 4;  // dynamic shared bytes
+template <bool kCount>
+__global__ void k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted,
+                               uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x,
+                               int quads, uint32_t dmask, uint32_t* pair_cell, uint32_t* pair_rec);
+// Launches count (true) or scatter (false); defined in the sort TU (template instantiation).
+void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, uint32_t count,
+                 const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total, int tiles_x, int quads,
+                 uint32_t dmask, uint32_t* pair_cell, uint32_t* pair_rec);
 __global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges);
 constexpr int kStreamItems = 8;  // elements per thread in the streaming sort kernels
-constexpr int kEmitThreads = 256;  // k_emit_pairs: 4 sorted splats per thread
 
 // screen-band exchange (multi-GPU frame)
 constexpr int kMaxBands = GSCG_MAX_BANDS;

@@ -222,17 +222,14 @@ k_sort_downsweep(SortPassParams p) {
 // one grid row share depth bit patterns.
 namespace {
 
+__device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x, int quads) {
+    return quads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
+                 : static_cast<uint32_t>(cy * tiles_x + cx);
+}
+
 struct SpanSink {
-    uint32_t block_begin, block_end;  // this CTA's positions
-    uint32_t local = 0;               // pairs of this CTA's positions
-    uint32_t* block_sums;
     uint2* span_sorted;
-    __device__ void put(uint32_t pos, uint4 m) {
-        span_sorted[pos] = make_uint2(m.y, m.z);
-        const uint32_t n = (m.z & 0xffffu) * (m.z >> 16);
-        if (pos >= block_begin && pos < block_end) local += n;
-        else atomicAdd(&block_sums[pos >> 10], n);
-    }
+    __device__ void put(uint32_t pos, uint4 m) { span_sorted[pos] = make_uint2(m.y, m.z); }
 };
 
 // Orders the run of equal keys starting at s by ordinal (insertion sort in global memory)
@@ -259,16 +256,11 @@ __device__ __forceinline__ uint32_t finish_run(const uint32_t* keys, uint32_t* r
 }  // namespace
 
 __global__ void __launch_bounds__(kMetaThreads)
-k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted,
-               uint32_t* block_sums) {
+k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted) {
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
-    __shared__ uint32_t s_warp[kMetaThreads / 32];
     SpanSink sink;
-    sink.block_begin = blockIdx.x * (kMetaThreads * kStreamItems);
-    sink.block_end = sink.block_begin + kMetaThreads * kStreamItems;
-    sink.block_sums = block_sums;
     sink.span_sorted = span_sorted;
-    const uint32_t b = sink.block_begin + threadIdx.x * kStreamItems;
+    const uint32_t b = (blockIdx.x * kMetaThreads + threadIdx.x) * kStreamItems;
     if (b + kStreamItems < count) {
         uint32_t k[kStreamItems + 1];
         const uint4 lo = *reinterpret_cast<const uint4*>(keys + b);
@@ -321,10 +313,7 @@ k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t
             }
             uint4* dst = reinterpret_cast<uint4*>(span_sorted + b);
 #pragma unroll
-            for (int j = 0; j < kStreamItems; j += 2) {
-                dst[j / 2] = make_uint4(m[j].y, m[j].z, m[j + 1].y, m[j + 1].z);
-                sink.local += (m[j].z & 0xffffu) * (m[j].z >> 16) + (m[j + 1].z & 0xffffu) * (m[j + 1].z >> 16);
-            }
+            for (int j = 0; j < kStreamItems; j += 2) dst[j / 2] = make_uint4(m[j].y, m[j].z, m[j + 1].y, m[j + 1].z);
         } else {
             // Only [w0, w1) is this thread's: the runs crossing the window edges are
             // reordered by the threads where they start.
@@ -353,55 +342,34 @@ k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t
             }
         }
     }
-    // Pairs of this CTA's positions: one atomic per CTA (crossing runs added theirs).
-    uint32_t v = __reduce_add_sync(0xffffffffu, sink.local);
-    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-#pragma unroll
-        for (int w = 0; w < kMetaThreads / 32; ++w) t += s_warp[w];
-        if (t) atomicAdd(&block_sums[blockIdx.x], t);
-    }
 }
 
-// Exclusive scan of the block sums in place (one CTA).
-__global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, uint32_t n) {
-    __shared__ uint32_t s_warp[32];
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < n; base += 1024) {
-        const uint32_t i = base + threadIdx.x;
-        const uint32_t v = i < n ? sums[i] : 0u;
-        uint32_t total;
-        const uint32_t e = block_excl_scan(v, s_warp, total);
-        if (i < n) sums[i] = carry + e;
-        carry += total;
-    }
-}
-
-// Emit (cell, record) pairs in sorted splat order, one CTA per 1024 sorted splats (the
-// block granularity of k_sorted_spans' pair sums). Each thread loads 4 consecutive
-// splats (vector loads, all in flight), the CTA scans their pair counts, and then the
-// CTA's pairs are written with consecutive threads on consecutive pairs (coalesced);
-// each pair finds its splat by binary search over the CTA's splat offsets in shared
-// memory.
-namespace {
-__device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x, int quads) {
-    return quads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
-                 : static_cast<uint32_t>(cy * tiles_x + cx);
-}
-}  // namespace
-
+// Emit the (cell, record) pairs of every sorted splat directly in the order of the first
+// stable cell-sort pass (LSD digit = cell & dmask): a pair's position is the digit's
+// global base + this block's offset for the digit (k_sort_rows over k_sorted_spans'
+// block histograms) + the pairs of that digit from earlier threads of the block + its
+// rank among this thread's pairs of the digit. Threads own 4 consecutive sorted splats and
+// enumerate each splat's cells row by row, so pairs of one digit keep the splat order: the
+// output equals emitting in sorted order and running the first LSD pass on it.
+// kCount: only count the block's pairs per digit (block_digit[d][block], the input of
+// k_sort_rows); else scatter them.
+template <bool kCount>
 __global__ void __launch_bounds__(kEmitThreads)
-k_emit_pairs(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted, const uint32_t* block_offsets,
-             int tiles_x, int quads, uint32_t* pair_cell, uint32_t* pair_rec) {
-    static_assert(kEmitThreads * 4 == 1024, "one 1024-splat pair block per CTA");
-    __shared__ uint32_t s_off[1024];
-    __shared__ uint2 s_span[1024];
-    __shared__ uint32_t s_rec[1024];
-    __shared__ uint32_t s_warp[32];
-    const uint32_t base = blockIdx.x * 1024u;
-    const uint32_t i0 = base + 4u * threadIdx.x;
+k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted, uint32_t* block_digit,
+               const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads, uint32_t dmask,
+               uint32_t* pair_cell, uint32_t* pair_rec) {
+    static_assert(kEmitThreads * 4 == 1024, "one 1024-splat block per CTA");
+    static_assert(kRadix == 32 && kEmitThreads == 256, "8 warps x 4 digits in the scan");
+    constexpr uint32_t kStage = kEmitStage;            // pairs staged for coalesced writes
+    extern __shared__ uint32_t s_dyn_emit[];
+    auto s_cnt = reinterpret_cast<uint32_t (*)[kEmitThreads]>(s_dyn_emit);  // [digit][thread]: count, then start
+    uint32_t* s_stage_cell = s_dyn_emit + kRadix * kEmitThreads;
+    uint32_t* s_stage_rec = s_stage_cell + kStage;
+    __shared__ uint32_t s_base[kRadix];   // global position of the block's first pair of each digit
+    __shared__ uint32_t s_local[kRadix];  // block-local start of each digit
+    __shared__ uint32_t s_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t i0 = blockIdx.x * 1024u + 4u * tid;
     uint2 sp[4];
     uint32_t rc[4];
     if (i0 + 4 <= count) {
@@ -418,37 +386,109 @@ k_emit_pairs(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorte
             rc[q] = i0 + q < count ? rec_sorted[i0 + q] : 0u;
         }
     }
-    uint32_t n[4], sum = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        n[q] = (sp[q].y & 0xffffu) * (sp[q].y >> 16);
-        sum += n[q];
+    for (int d = 0; d < kRadix; ++d) s_cnt[d][tid] = 0u;
+    if (!kCount && tid < kRadix) {  // global base of digit tid: scanned digit totals + this block's offset
+        const uint32_t t = static_cast<uint32_t>(tid) <= dmask ? digit_total[tid] : 0u;
+        s_base[tid] = warp_incl_scan(t, lane) - t + (static_cast<uint32_t>(tid) <= dmask ? block_digit[tid * blocks + blockIdx.x] : 0u);
     }
-    uint32_t total;
-    uint32_t off = block_excl_scan(sum, s_warp, total);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        s_off[4 * threadIdx.x + q] = off;
-        s_span[4 * threadIdx.x + q] = sp[q];
-        s_rec[4 * threadIdx.x + q] = rc[q];
-        off += n[q];
+        const int cx0 = static_cast<int>(sp[q].x & 0xffffu), cy0 = static_cast<int>(sp[q].x >> 16);
+        const int w = static_cast<int>(sp[q].y & 0xffffu), h = static_cast<int>(sp[q].y >> 16);
+        for (int cy = cy0; cy < cy0 + h; ++cy)
+            for (int cx = cx0; cx < cx0 + w; ++cx) ++s_cnt[cell_id(cx, cy, tiles_x, quads) & dmask][tid];
     }
     __syncthreads();
-    const uint32_t out0 = block_offsets[blockIdx.x];
-    for (uint32_t t = threadIdx.x; t < total; t += kEmitThreads) {
-        // owner: the last splat whose offset is <= t (empty splats share offsets; the
-        // last of a tie is the one holding the pairs)
-        uint32_t lo = 0;
+    if (kCount) {  // digit d's pairs in this block: warp w sums digits 4w..4w+3 over the 256 threads
 #pragma unroll
-        for (uint32_t step = 512; step >= 1; step >>= 1)
-            if (lo + step < 1024 && s_off[lo + step] <= t) lo += step;
-        const uint2 s2 = s_span[lo];
-        const int k = static_cast<int>(t - s_off[lo]);
-        const int ncw = static_cast<int>(s2.y & 0xffffu);
-        const int cx = static_cast<int>(s2.x & 0xffffu) + k % ncw, cy = static_cast<int>(s2.x >> 16) + k / ncw;
-        pair_cell[out0 + t] = cell_id(cx, cy, tiles_x, quads);
-        pair_rec[out0 + t] = s_rec[lo];
+        for (int dd = 0; dd < 4; ++dd) {
+            const int d = warp * 4 + dd;
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v += s_cnt[d][lane * 8 + k];
+            v = __reduce_add_sync(0xffffffffu, v);
+            if (lane == 0 && static_cast<uint32_t>(d) <= dmask) block_digit[d * blocks + blockIdx.x] = v;
+        }
+        return;
     }
+    // Exclusive scan over threads for each digit (warp w: digits 4w..4w+3, lane l: threads
+    // 8l..8l+7), then over digits: s_cnt becomes each thread's block-local start.
+#pragma unroll
+    for (int dd = 0; dd < 4; ++dd) {
+        const int d = warp * 4 + dd;
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = s_cnt[d][lane * 8 + k];
+            sum += v[k];
+        }
+        const uint32_t incl = warp_incl_scan(sum, lane);
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            s_cnt[d][lane * 8 + k] = run;
+            run += v[k];
+        }
+        if (lane == 31) s_local[d] = incl;  // digit total for now
+    }
+    __syncthreads();
+    if (tid < kRadix) {
+        const uint32_t t = s_local[tid];
+        const uint32_t incl = warp_incl_scan(t, lane);
+        s_local[tid] = incl - t;
+        if (tid == kRadix - 1) s_total = incl;
+    }
+    __syncthreads();
+    const uint32_t total = s_total;
+    const bool staged = total <= kStage;  // else every pair goes straight to its global slot
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int cx0 = static_cast<int>(sp[q].x & 0xffffu), cy0 = static_cast<int>(sp[q].x >> 16);
+        const int w = static_cast<int>(sp[q].y & 0xffffu), h = static_cast<int>(sp[q].y >> 16);
+        for (int cy = cy0; cy < cy0 + h; ++cy)
+            for (int cx = cx0; cx < cx0 + w; ++cx) {
+                const uint32_t c = cell_id(cx, cy, tiles_x, quads);
+                const uint32_t d = c & dmask;
+                const uint32_t r = s_cnt[d][tid]++;  // rank among the block's pairs of digit d
+                if (staged) {
+                    s_stage_cell[s_local[d] + r] = c;
+                    s_stage_rec[s_local[d] + r] = rc[q];
+                } else {
+                    pair_cell[s_base[d] + r] = c;
+                    pair_rec[s_base[d] + r] = rc[q];
+                }
+            }
+    }
+    if (!staged) return;
+    __syncthreads();
+    // Staged pairs are in digit order: each digit's run goes to consecutive global slots.
+    for (uint32_t e = tid; e < total; e += kEmitThreads) {
+        const uint32_t c = s_stage_cell[e];
+        const uint32_t d = c & dmask;
+        const uint32_t pos = s_base[d] + (e - s_local[d]);
+        pair_cell[pos] = c;
+        pair_rec[pos] = s_stage_rec[e];
+    }
+}
+
+void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, uint32_t count,
+                 const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total, int tiles_x, int quads,
+                 uint32_t dmask, uint32_t* pair_cell, uint32_t* pair_rec) {
+    static bool attr = [] {
+        cudaFuncSetAttribute(k_emit_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        return true;
+    }();
+    (void)attr;
+    if (count_only)
+        k_emit_scatter<true><<<blocks, kEmitThreads, kRadix * kEmitThreads * 4, s>>>(rec_sorted, count, span_sorted, block_digit,
+                                                                    digit_total, blocks, tiles_x, quads, dmask,
+                                                                    pair_cell, pair_rec);
+    else
+        k_emit_scatter<false><<<blocks, kEmitThreads, kEmitSmem, s>>>(rec_sorted, count, span_sorted, block_digit,
+                                                                     digit_total, blocks, tiles_x, quads, dmask,
+                                                                     pair_cell, pair_rec);
 }
 
 // [start, end) of every cell in the cell-sorted pairs (the reference's bins).
