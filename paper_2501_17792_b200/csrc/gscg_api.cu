@@ -670,22 +670,23 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         //    into the order of the first stable cell-sort pass.
         const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
         const uint32_t dmask = (1u << cplan.bits[0]) - 1u;
-        const uint32_t sblocks = (S32 + 1023) / 1024;
+        const uint32_t sblocks = (S32 + 1023) / 1024;                 // k_sorted_spans CTAs
+        const uint32_t eblocks = (S32 + kEmitSplats - 1) / kEmitSplats;  // emission blocks
         CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
-        CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(sblocks) * kRadix * 4));
+        CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
         static_assert(kMetaThreads * kStreamItems == 1024, "one splat block per CTA");
         const int quads = geo.cells_per_tile == 4 ? 1 : 0;
         k_sorted_spans<<<sblocks, kMetaThreads, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
                                                         ctx->splat_meta.as<uint4>(), S32, ctx->span_sorted.as<uint2>());
-        launch_emit(true, sblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
+        launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), nullptr, geo.tiles_x, quads, dmask, nullptr, nullptr);
         SortPassParams bp{};
         bp.counts = ctx->block_sums.as<uint32_t>();
         bp.digit_base = ctx->hist.as<uint32_t>();
-        bp.tiles = sblocks;
+        bp.tiles = eblocks;
         bp.bits = cplan.bits[0];
         k_sort_rows<<<dmask + 1, 1024, 0, s>>>(bp);
-        launch_emit(false, sblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
+        launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), geo.tiles_x, quads, dmask,
                     ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
         ++launches;

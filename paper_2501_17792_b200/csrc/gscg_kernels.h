@@ -149,8 +149,9 @@ __global__ void k_sort_downsweep(SortPassParams p);
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
 __global__ void k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
                                uint2* span_sorted);
-constexpr int kEmitThreads = 256;  // k_emit_scatter: 4 sorted splats per thread
-constexpr uint32_t kEmitStage = 4096;  // pairs per block staged in shared memory for coalesced writes
+constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
+constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
+constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes
 constexpr int kEmitSmem = (32 * kEmitThreads + 2 * kEmitStage) * 4;  // dynamic shared bytes
 template <bool kCount>
 __global__ void k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted,

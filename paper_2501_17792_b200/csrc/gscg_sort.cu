@@ -358,8 +358,8 @@ __global__ void __launch_bounds__(kEmitThreads)
 k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted, uint32_t* block_digit,
                const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads, uint32_t dmask,
                uint32_t* pair_cell, uint32_t* pair_rec) {
-    static_assert(kEmitThreads * 4 == 1024, "one 1024-splat block per CTA");
-    static_assert(kRadix == 32 && kEmitThreads == 256, "8 warps x 4 digits in the scan");
+    constexpr int kWarps = kEmitThreads / 32, kDigitsPerWarp = kRadix / kWarps, kPerLane = kEmitThreads / 32;
+    static_assert(kRadix % kWarps == 0, "digits split evenly over the warps");
     constexpr uint32_t kStage = kEmitStage;            // pairs staged for coalesced writes
     extern __shared__ uint32_t s_dyn_emit[];
     auto s_cnt = reinterpret_cast<uint32_t (*)[kEmitThreads]>(s_dyn_emit);  // [digit][thread]: count, then start
@@ -369,7 +369,7 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
     __shared__ uint32_t s_local[kRadix];  // block-local start of each digit
     __shared__ uint32_t s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t i0 = blockIdx.x * 1024u + 4u * tid;
+    const uint32_t i0 = blockIdx.x * kEmitSplats + 4u * tid;
     uint2 sp[4];
     uint32_t rc[4];
     if (i0 + 4 <= count) {
@@ -400,34 +400,34 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
             for (int cx = cx0; cx < cx0 + w; ++cx) ++s_cnt[cell_id(cx, cy, tiles_x, quads) & dmask][tid];
     }
     __syncthreads();
-    if (kCount) {  // digit d's pairs in this block: warp w sums digits 4w..4w+3 over the 256 threads
+    if (kCount) {  // digit d's pairs in this block: warp w sums its digits over all threads
 #pragma unroll
-        for (int dd = 0; dd < 4; ++dd) {
-            const int d = warp * 4 + dd;
+        for (int dd = 0; dd < kDigitsPerWarp; ++dd) {
+            const int d = warp * kDigitsPerWarp + dd;
             uint32_t v = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v += s_cnt[d][lane * 8 + k];
+            for (int k = 0; k < kPerLane; ++k) v += s_cnt[d][lane * kPerLane + k];
             v = __reduce_add_sync(0xffffffffu, v);
             if (lane == 0 && static_cast<uint32_t>(d) <= dmask) block_digit[d * blocks + blockIdx.x] = v;
         }
         return;
     }
-    // Exclusive scan over threads for each digit (warp w: digits 4w..4w+3, lane l: threads
-    // 8l..8l+7), then over digits: s_cnt becomes each thread's block-local start.
+    // Exclusive scan over threads for each digit (warp w: kDigitsPerWarp digits, lane l:
+    // kPerLane consecutive threads), then over digits: s_cnt becomes each thread's start.
 #pragma unroll
-    for (int dd = 0; dd < 4; ++dd) {
-        const int d = warp * 4 + dd;
-        uint32_t v[8], sum = 0;
+    for (int dd = 0; dd < kDigitsPerWarp; ++dd) {
+        const int d = warp * kDigitsPerWarp + dd;
+        uint32_t v[kPerLane], sum = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            v[k] = s_cnt[d][lane * 8 + k];
+        for (int k = 0; k < kPerLane; ++k) {
+            v[k] = s_cnt[d][lane * kPerLane + k];
             sum += v[k];
         }
         const uint32_t incl = warp_incl_scan(sum, lane);
         uint32_t run = incl - sum;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            s_cnt[d][lane * 8 + k] = run;
+        for (int k = 0; k < kPerLane; ++k) {
+            s_cnt[d][lane * kPerLane + k] = run;
             run += v[k];
         }
         if (lane == 31) s_local[d] = incl;  // digit total for now
