@@ -264,19 +264,21 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                     "launches": st.kernel_launches, "counts": (st.gaussian_count, st.splat_count, st.pair_count)}
     else:
         # Band path: shard projection -> NCCL all-to-all -> band render -> gather.
-        from paper_2501_17792_b200.multigpu import BandRank, FrameArgs, TorchExchange, band_rows, shard_ranges
+        from paper_2501_17792_b200.multigpu import BandRank, FrameArgs, LoadBalancer, TorchExchange
         ex = TorchExchange()
         br = BandRank(scene, device=local_rank, renderer=r)
-        rows = band_rows(cfg.height, settings.tile_size, world)
-        shard = shard_ranges(n, world)[rank]
+        balancer = LoadBalancer(scene, world, settings.tile_size)
 
         def frame(f: int) -> dict:
-            br.project(FrameArgs(times_s[f], False, forced), settings, shard, rows, frame=frame_desc(f))
+            # shards by last frame's Gaussians per instance, bands by last frame's pairs per tile row
+            shards, rows = balancer.plan()
+            br.project(FrameArgs(times_s[f], False, forced), settings, shards[rank], rows, frame=frame_desc(f))
             send = br.pack()
             with torch.cuda.stream(stream):
                 recv, rc = ex.all_to_all(send, br.counts.tolist())
                 rgb, T = br.render_band(recv, sum(rc), rows[rank], rows[rank + 1])
                 ex.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
+                balancer.observe(d_lods[:n].cpu().numpy(), br.band_row_pairs(), rows[rank] // settings.tile_size, ex)
             a, b = br.shard_times, br.band_times
             return {"update": a.update_ms, "gather": a.gather_ms, "route": a.sort_ms, "unpack": b.gather_ms,
                     "sort": b.sort_ms, "rasterize": b.rasterize_ms,

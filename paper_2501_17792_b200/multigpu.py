@@ -214,6 +214,7 @@ class BandRank:
         for i, v in enumerate(cfg.lod_thresholds):
             lp.thresholds_m[i] = v
         lp.hysteresis_band_m = cfg.lod_hysteresis
+        self._tile = settings.tile_size
         bands = len(rows) - 1
         rows_arr = (C.c_uint32 * (bands + 1))(*[int(r) for r in rows])
         counts = np.zeros(bands, dtype=np.uint64)
@@ -234,6 +235,16 @@ class BandRank:
         self.stream().wait_stream(torch.cuda.current_stream(buf.device))
         self._check(self.lib.gscg_pack_bands(self.ctx, C.c_void_p(buf.data_ptr())))
         return buf[: total * BAND_SPLAT_BYTES]
+
+    def band_row_pairs(self) -> np.ndarray:
+        """Binned pairs per tile row of the last band render (band-local rows)."""
+        tiles, cpt = self.renderer.cell_layout()
+        if tiles == 0:
+            return np.zeros(0)
+        ranges = self.renderer.cell_ranges().astype(np.int64)
+        per_cell = ranges[:, 1] - ranges[:, 0]
+        tiles_x = (self.scene.cfg.width + self._tile - 1) // self._tile
+        return per_cell.reshape(-1, tiles_x * cpt).sum(axis=1).astype(np.float64)
 
     def render_band(self, recv, count: int, row_begin: int, row_end: int):
         """(rgb, T) device tensors of rows [row_begin, row_end), ordered on the context stream."""
@@ -268,6 +279,52 @@ def gscg_settings(settings) -> N.GscgRenderSettings:
 # drivers
 
 
+class LoadBalancer:
+    """Frame-to-frame load balance of the band path. Instance shards are split by the
+    Gaussians each instance drew in the previous frame (its LoD level's count), and
+    screen bands by the previous frame's binned pairs per tile row. The row histogram is
+    summed over ranks, since each rank sees only its own band."""
+
+    def __init__(self, scene, world: int, tile: int):
+        self.world, self.tile = world, tile
+        nt = scene.counts()[0]
+        levels = [scene.level_count(t) for t in range(nt)]
+        self.max_level = np.array(levels, dtype=np.int64) - 1
+        self.level_gauss = np.zeros((max(nt, 1), max(levels + [1])), dtype=np.float64)
+        for t in range(nt):
+            for l in range(levels[t]):
+                self.level_gauss[t, l] = len(scene.level_view(t, l)["opacities"])
+        self.template_ids = np.asarray(scene.instances["template_id"], dtype=np.int64)
+        self.height = scene.cfg.height
+        self.inst_w: Optional[np.ndarray] = None
+        self.row_w: Optional[np.ndarray] = None
+
+    def plan(self) -> tuple[list[tuple[int, int]], list[int]]:
+        n = len(self.template_ids)
+        shards = shard_ranges(n, self.world, self.inst_w if self.inst_w is not None and self.inst_w.sum() > 0 else None)
+        rows = band_rows(self.height, self.tile, self.world,
+                         self.row_w if self.row_w is not None and self.row_w.sum() > 0 else None)
+        return shards, rows
+
+    def observe(self, lods: np.ndarray, band_row_pairs: np.ndarray, row0_tile: int, exchange=None) -> None:
+        """lods: every instance's level this frame (identical on all ranks); band_row_pairs:
+        this rank's pairs per tile row of its band, starting at tile row row0_tile."""
+        lods = np.minimum(np.asarray(lods, dtype=np.int64), self.max_level[self.template_ids])
+        self.inst_w = self.level_gauss[self.template_ids, lods]
+        trows = (self.height + self.tile - 1) // self.tile
+        local = np.zeros(trows, dtype=np.float64)
+        k = len(band_row_pairs)
+        local[row0_tile:row0_tile + k] = band_row_pairs
+        if exchange is not None and exchange.world > 1:
+            import torch
+
+            t = torch.from_numpy(local).to(torch.device("cuda", torch.cuda.current_device())
+                                           if exchange.dist.get_backend(exchange.group) == "nccl" else "cpu")
+            exchange.dist.all_reduce(t, group=exchange.group)
+            local = t.cpu().numpy()
+        self.row_w = local
+
+
 class DistributedRenderer:
     """One rank of a P-GPU frame (torch.distributed initialised with NCCL, one process per GPU)."""
 
@@ -278,6 +335,7 @@ class DistributedRenderer:
         self.band = band or BandRank(scene, device=device)
         self.scene = scene
         self.rows: Optional[list[int]] = None
+        self.balancer: Optional[LoadBalancer] = None
 
     def render_frame(self, time_s: float, settings=None, static_pose: bool = False,
                      forced_lod: Optional[int] = None, rows: Optional[Sequence[int]] = None):
@@ -288,8 +346,11 @@ class DistributedRenderer:
         settings = settings or P.RenderSettings()
         cfg = self.scene.cfg
         n = self.scene.counts()[2]
-        rows = list(rows) if rows is not None else band_rows(cfg.height, settings.tile_size, self.world)
-        shard = shard_ranges(n, self.world)[self.rank]
+        if self.balancer is None or self.balancer.tile != settings.tile_size:
+            self.balancer = LoadBalancer(self.scene, self.world, settings.tile_size)
+        shards, auto_rows = self.balancer.plan()
+        rows = list(rows) if rows is not None else auto_rows
+        shard = shards[self.rank]
         fa = FrameArgs(time_s, static_pose, forced_lod)
         self.band.project(fa, settings, shard, rows)
         send = self.band.pack()
@@ -297,6 +358,8 @@ class DistributedRenderer:
             recv, rc = self.exchange.all_to_all(send, self.band.counts.tolist())
             rgb, T = self.band.render_band(recv, sum(rc), rows[self.rank], rows[self.rank + 1])
             full = self.exchange.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
+            self.balancer.observe(self.band.lods[:n], self.band.band_row_pairs(), rows[self.rank] // settings.tile_size,
+                                  self.exchange)
             if full is None:
                 return None
             # one read-back into page-locked memory, then split into the API's two arrays

@@ -58,6 +58,22 @@ def test_band_rows_weighted_balance():
     assert all(r % 16 == 0 for r in rows[:-1])
 
 
+def test_load_balancer_plans_from_observed_work():
+    from paper_2501_17792_b200.multigpu import LoadBalancer
+
+    scene = _small_scene()
+    lb = LoadBalancer(scene, 2, 16)
+    shards, rows = lb.plan()
+    assert shards == shard_ranges(6, 2) and rows == band_rows(120, 16, 2)
+    lods = np.array([0, 0, 2, 2, 2, 2])  # two heavy near characters first
+    trows = (120 + 15) // 16
+    lb.observe(lods, np.arange(1, trows + 1, dtype=np.float64) ** 3, 0)
+    shards, rows = lb.plan()
+    assert shards[0][1] <= 2  # the heavy instances fill the first shard
+    assert rows[1] > band_rows(120, 16, 2)[1]  # heavy bottom rows -> the first band grows
+    assert all(r % 16 == 0 for r in rows[:-1]) and rows[-1] == 120
+
+
 def test_route_counts():
     rects = np.array([[0, 10], [10, 20], [15, 40], [5, 5]])
     assert route_counts(rects, [0, 16, 32, 48]).tolist() == [3, 2, 1]
