@@ -153,6 +153,8 @@ struct gscg_ctx {
     size_t pinned_cap = 0;
     FrameCounters* h_counters = nullptr;
     cudaEvent_t ev[8] = {};
+    cudaStream_t copy_stream = nullptr;  // framebuffer read-back overlapped with the raster bands
+    cudaEvent_t band_ev[kReadbackBands] = {};
 
     // last frame
     uint32_t n = 0, tiles = 0, cells_per_tile = 1;
@@ -592,7 +594,20 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
 // Sort (splats by depth + ordinal, pairs in that order, pairs stably by cell) and
 // rasterise tile rows [tile_row0, tile_row0 + tile_rows) from the context's records
 // (ctx->S splats, ctx->K pairs whose spans are relative to tile_row0). Events 3..5.
-uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& launches) {
+void copy_out(gscg_ctx* ctx, int rows, float* fb_rgb, float* fb_T, bool host);
+
+bool is_host_pointer(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;  // unregistered host memory
+    }
+    return at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged;
+}
+
+uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& launches, float* read_rgb = nullptr,
+                     float* read_T = nullptr) {
     cudaStream_t s = ctx->stream;
     const FrameGeom& geo = ctx->geom;
     const uint32_t tiles = static_cast<uint32_t>(geo.tiles_x) * static_cast<uint32_t>(tile_rows);
@@ -728,9 +743,41 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         rp.t_floor = ctx->settings.transmittance_floor;
         rp.out_rgb = ctx->fb_rgb.as<float>();
         rp.out_T = ctx->fb_T.as<float>();
-        launch_raster(rp, tiles, s);
-        ++launches;
+        if (!read_rgb && !read_T) {
+            launch_raster(rp, tiles, s);
+            ++launches;
+        } else {
+            // Host read-back overlapped with the raster: tile-row bands are rasterised in
+            // order and each band's rows are copied out on the copy stream while the next
+            // band renders.
+            const int bands = std::min(kReadbackBands, tile_rows);
+            const size_t row_floats = static_cast<size_t>(geo.W);
+            for (int b = 0; b < bands; ++b) {
+                const int r0 = tile_rows * b / bands, r1 = tile_rows * (b + 1) / bands;
+                if (r1 <= r0) continue;
+                RasterParams bp = rp;
+                bp.ranges = rp.ranges + static_cast<size_t>(r0) * geo.tiles_x * geo.cells_per_tile;
+                bp.tile_row0 = tile_row0 + r0;
+                launch_raster(bp, static_cast<uint32_t>((r1 - r0) * geo.tiles_x), s);
+                ++launches;
+                CUDA_TRY(cudaEventRecord(ctx->band_ev[b], s));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_ev[b], 0));
+                const int y0 = r0 * geo.ts, y1 = std::min(r1 * geo.ts, geo.H - tile_row0 * geo.ts);
+                const size_t off = static_cast<size_t>(y0) * row_floats, n = static_cast<size_t>(y1 - y0) * row_floats;
+                if (read_rgb)
+                    CUDA_TRY(cudaMemcpyAsync(read_rgb + 3 * off, ctx->fb_rgb.as<float>() + 3 * off, n * 12,
+                                             cudaMemcpyDefault, ctx->copy_stream));
+                if (read_T)
+                    CUDA_TRY(cudaMemcpyAsync(read_T + off, ctx->fb_T.as<float>() + off, n * 4, cudaMemcpyDefault,
+                                             ctx->copy_stream));
+            }
+            // The frame's stream resumes only after the read-back (ordering for the caller).
+            CUDA_TRY(cudaEventRecord(ctx->band_ev[kReadbackBands - 1], ctx->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(s, ctx->band_ev[kReadbackBands - 1], 0));
+        }
         CUDA_TRY(cudaGetLastError());
+    } else if (read_rgb || read_T) {
+        copy_out(ctx, geo.H - tile_row0 * geo.ts, read_rgb, read_T, true);
     }
     CUDA_TRY(cudaEventRecord(ctx->ev[5], s));
     ctx->tiles = tiles;
@@ -792,6 +839,8 @@ int gscg_create(int device, gscg_ctx** out) {
         ctx->sm_count = prop.multiProcessorCount;
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+        for (auto& e : ctx->band_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_band_counts), GSCG_MAX_BANDS * sizeof(unsigned long long)));
         CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
@@ -828,6 +877,9 @@ int gscg_destroy(gscg_ctx* ctx) {
     if (ctx->h_band_counts) cudaFreeHost(ctx->h_band_counts);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->band_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GSCG_OK;
@@ -984,8 +1036,12 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         uint32_t launches = 0;
         ctx->band_state = 0;
         update_gather(ctx, frame, cam, lod, 0, n, launches);
-        const uint32_t passes = sort_raster(ctx, 0, ctx->geom.tiles_y, launches);
-        copy_out(ctx, ctx->geom.H, fb_rgb, fb_T, host);
+        // Host destinations: read-back overlapped with the raster bands (sort_raster).
+        // Device destinations: one device-to-device copy after the frame.
+        const bool overlap = is_host_pointer(fb_rgb) || is_host_pointer(fb_T);
+        const uint32_t passes = overlap ? sort_raster(ctx, 0, ctx->geom.tiles_y, launches, fb_rgb, fb_T)
+                                        : sort_raster(ctx, 0, ctx->geom.tiles_y, launches);
+        if (!overlap) copy_out(ctx, ctx->geom.H, fb_rgb, fb_T, host);
         if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull,
                                         host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
         CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->stream));

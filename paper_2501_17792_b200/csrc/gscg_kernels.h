@@ -202,6 +202,7 @@ __global__ void k_sse_partial(const float* a, const float* b, uint64_t n, double
 __global__ void k_sse_final(const double* partial, uint32_t blocks, double* out);
 
 // raster
+constexpr int kReadbackBands = 4;  // tile-row bands of a frame whose host read-back overlaps the raster
 // Picks the tile-size specialisation (16: 8x8 quadrant CTAs; else 1/4/16 pixels per thread).
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream);
 
