@@ -467,7 +467,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--cpu-frames", type=int, default=5)  # ~12 s of host CPU work at config 3
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--band-path", action="store_true",
                     help="use the multi-GPU band path (shard -> NCCL all-to-all -> band) even on one GPU")
