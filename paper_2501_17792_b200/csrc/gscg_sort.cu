@@ -96,18 +96,30 @@ k_sort_upsweep(SortPassParams p) {
 }
 
 // Row scans: CTA d turns digit d's tile counts into exclusive offsets; row total ->
-// digit_base[d] (the downsweep scans the row totals itself).
+// digit_base[d] (the downsweep scans the row totals itself). Each thread owns up to
+// kRowItems consecutive entries of a 1024 * kRowItems window, so a row of up to 8192 tiles
+// takes one block scan.
+constexpr int kRowItems = 8;
 __global__ void __launch_bounds__(1024)
 k_sort_rows(SortPassParams p) {
     __shared__ uint32_t s_warp[32];
     uint32_t* row = p.counts + static_cast<size_t>(blockIdx.x) * p.tiles;
     uint32_t carry = 0;
-    for (uint32_t b = 0; b < p.tiles; b += 1024) {
-        const uint32_t i = b + threadIdx.x;
-        const uint32_t v = i < p.tiles ? row[i] : 0u;
+    for (uint32_t b = 0; b < p.tiles; b += 1024 * kRowItems) {
+        const uint32_t i0 = b + threadIdx.x * kRowItems;
+        uint32_t v[kRowItems], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kRowItems; ++k) {
+            v[k] = i0 + k < p.tiles ? row[i0 + k] : 0u;
+            sum += v[k];
+        }
         uint32_t total;
-        const uint32_t e = block_excl_scan(v, s_warp, total);
-        if (i < p.tiles) row[i] = carry + e;
+        uint32_t run = carry + block_excl_scan(sum, s_warp, total);
+#pragma unroll
+        for (int k = 0; k < kRowItems; ++k) {
+            if (i0 + k < p.tiles) row[i0 + k] = run;
+            run += v[k];
+        }
         carry += total;
     }
     if (threadIdx.x == 0) p.digit_base[blockIdx.x] = carry;
