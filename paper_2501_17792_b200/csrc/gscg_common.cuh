@@ -17,7 +17,7 @@ namespace gscg {
 constexpr int kMaxJoints = GSCG_MAX_JOINTS;
 constexpr int kMaxGroups = 256;      // (template, level) pairs resident at once
 constexpr int kProjectThreads = 256; // Gaussians per work-item chunk
-constexpr int kBatch = 16;           // instances per template-major work item
+constexpr int kBatch = 8;           // instances per template-major work item
 constexpr int kShFloats = GSCG_SH_FLOATS;
 
 // One (template, level) group of the shared attribute store in HBM.

@@ -57,7 +57,7 @@ __device__ __forceinline__ void copy_async_wait_all() { asm volatile("cp.async.w
 
 }  // namespace
 
-__global__ void __launch_bounds__(kProjectThreads, 3)
+__global__ void __launch_bounds__(kProjectThreads, 4)
 k_project(ProjectParams p) {
     extern __shared__ float4 s_dyn[];
     float* s_sh = reinterpret_cast<float*>(s_dyn);
