@@ -239,6 +239,22 @@ __device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x, int qua
                  : static_cast<uint32_t>(cy * tiles_x + cx);
 }
 
+// Calls f(cell) for every binning cell of a packed span, row by row (the emission order);
+// along a row the cell id advances without recomputing it (quadrant cells: +1 inside a
+// tile, +3 into the next tile).
+template <typename F>
+__device__ __forceinline__ void for_each_cell(uint2 sp, int tiles_x, int quads, F&& f) {
+    const int cx0 = static_cast<int>(sp.x & 0xffffu), cy0 = static_cast<int>(sp.x >> 16);
+    const int w = static_cast<int>(sp.y & 0xffffu), h = static_cast<int>(sp.y >> 16);
+    for (int cy = cy0; cy < cy0 + h; ++cy) {
+        uint32_t c = cell_id(cx0, cy, tiles_x, quads);
+        for (int cx = cx0; cx < cx0 + w; ++cx) {
+            f(c);
+            c += quads ? ((cx & 1) ? 3u : 1u) : 1u;
+        }
+    }
+}
+
 struct SpanSink {
     uint2* span_sorted;
     __device__ void put(uint32_t pos, uint4 m) { span_sorted[pos] = make_uint2(m.y, m.z); }
@@ -405,12 +421,7 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
         s_base[tid] = warp_incl_scan(t, lane) - t + (static_cast<uint32_t>(tid) <= dmask ? block_digit[tid * blocks + blockIdx.x] : 0u);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int cx0 = static_cast<int>(sp[q].x & 0xffffu), cy0 = static_cast<int>(sp[q].x >> 16);
-        const int w = static_cast<int>(sp[q].y & 0xffffu), h = static_cast<int>(sp[q].y >> 16);
-        for (int cy = cy0; cy < cy0 + h; ++cy)
-            for (int cx = cx0; cx < cx0 + w; ++cx) ++s_cnt[cell_id(cx, cy, tiles_x, quads) & dmask][tid];
-    }
+    for (int q = 0; q < 4; ++q) for_each_cell(sp[q], tiles_x, quads, [&](uint32_t c) { ++s_cnt[c & dmask][tid]; });
     __syncthreads();
     if (kCount) {  // digit d's pairs in this block: warp w sums its digits over all threads
 #pragma unroll
@@ -456,21 +467,18 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
     const bool staged = total <= kStage;  // else every pair goes straight to its global slot
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const int cx0 = static_cast<int>(sp[q].x & 0xffffu), cy0 = static_cast<int>(sp[q].x >> 16);
-        const int w = static_cast<int>(sp[q].y & 0xffffu), h = static_cast<int>(sp[q].y >> 16);
-        for (int cy = cy0; cy < cy0 + h; ++cy)
-            for (int cx = cx0; cx < cx0 + w; ++cx) {
-                const uint32_t c = cell_id(cx, cy, tiles_x, quads);
-                const uint32_t d = c & dmask;
-                const uint32_t r = s_cnt[d][tid]++;  // rank among the block's pairs of digit d
-                if (staged) {
-                    s_stage_cell[s_local[d] + r] = c;
-                    s_stage_rec[s_local[d] + r] = rc[q];
-                } else {
-                    pair_cell[s_base[d] + r] = c;
-                    pair_rec[s_base[d] + r] = rc[q];
-                }
+        const uint32_t rec = rc[q];
+        for_each_cell(sp[q], tiles_x, quads, [&](uint32_t c) {
+            const uint32_t d = c & dmask;
+            const uint32_t r = s_cnt[d][tid]++;  // rank among the block's pairs of digit d
+            if (staged) {
+                s_stage_cell[s_local[d] + r] = c;
+                s_stage_rec[s_local[d] + r] = rec;
+            } else {
+                pair_cell[s_base[d] + r] = c;
+                pair_rec[s_base[d] + r] = rec;
             }
+        });
     }
     if (!staged) return;
     __syncthreads();
