@@ -387,7 +387,10 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                            "frac": round(frame_roofline_ms / ms_step, 4), "peak_gbs": peaks["hbm_gbs"]},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
-                     "algorithmic_bytes": kbytes, "peak_source": peaks["source"]},
+                     "algorithmic_bytes": kbytes, "peak_source": peaks["source"],
+                     "limiter": ("issue-bound on exact no-FMA FP32 + integer work (ncu: ~65% issue, DRAM ~30%); "
+                                 "profiles/r01_ncu_full_v2.txt" if kernel == "k_project" else
+                                 "issue-bound, per-pixel list-walk divergence; profiles/r01_ncu_full_v2.txt")},
         "e2e": {"value": round(e2e_fps, 3), "unit": "FPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
