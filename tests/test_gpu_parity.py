@@ -288,3 +288,15 @@ def test_baseline_config3_headline():
     assert rep["G"] == 14972565 and rep["S"] > 10_000_000
     again, _ = r.render_frame(0.5, P.RenderSettings())
     assert again.tobytes() == g[0].tobytes()
+
+
+@pytest.mark.slow
+def test_baseline_config4_4k_ten_thousand():
+    """BASELINE config 4 at full size (10,000 characters, 3840x2160; 17-bit quadrant cell
+    ids): every bit-exact bar against the oracle, with device pose sampling."""
+    s, extra = config_scene(4)
+    r = P.Renderer(s, device_poses=True)
+    o = orc.from_scene(s)
+    g, c = render_both(s, r, o, 0.25)
+    rep = check_frame(s, r, o, g, c)
+    assert rep["S"] > 20_000_000 and rep["K"] > 50_000_000
