@@ -240,6 +240,35 @@ int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splat
 int gscg_get_cell_layout(gscg_ctx* ctx, uint32_t* tiles, uint32_t* cells_per_tile);
 int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells); /* cells x 2: [start, end) */
 int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs);
+/* ---- Stage functions (reference renderer.hpp:85-103) over host splat arrays ----
+ * FrameSplat (renderer.hpp:39-44): the projected Splat2D, its instance and gaussian
+ * index, and its pixel rect; 64 bytes. */
+typedef struct {
+  float mean_px[2];
+  float cov_xx, cov_xy, cov_yy;
+  float depth;
+  float color[3];
+  float opacity;
+  uint32_t instance_id;
+  uint32_t gaussian_index;
+  int32_t rect[4]; /* x0, y0, x1, y1 */
+} gscg_frame_splat;
+
+/* gather_splats (renderer.cpp:25-73): update + projection of the frame, the surviving
+ * splats in (instance, gaussian) order, as the reference concatenates them. out may be
+ * NULL to query the count; otherwise capacity >= count. */
+int gscg_gather_splats(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                       const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                       gscg_frame_splat* out, uint64_t capacity, uint64_t* count);
+/* sort_splats (renderer.cpp:85-107): in place, by (depth bits, instance_id, gaussian_index),
+ * on the GPU (stable LSD passes: gaussian, then instance, then depth). */
+int gscg_sort_splats(gscg_ctx* ctx, gscg_frame_splat* splats, uint64_t n);
+/* rasterize / rasterize_full (renderer.cpp:133-231): conic prep, tile binning in the given
+ * splat order, per-tile blending; fb_rgb (width*height*3) and fb_T (width*height) may be
+ * NULL. Power floors use the host libm as the reference. */
+int gscg_rasterize_splats(gscg_ctx* ctx, const gscg_frame_splat* splats, uint64_t n, int32_t width,
+                          int32_t height, const gscg_render_settings* settings, float* fb_rgb, float* fb_T);
+
 /* The device pose sampler's sinf (glibc replica) over host arguments. */
 int gscg_eval_sinf(gscg_ctx* ctx, const float* in, float* out, uint32_t n);
 

@@ -162,6 +162,15 @@ int gsch_renderer_prepare(gsch_renderer* r);
  * and active LoDs, n each (n x 4 for placement). */
 int gsch_fill_instances(gsch_renderer* r, int32_t static_pose, uint32_t* template_ids, float* placement,
                         uint32_t* motion_ids, float* phase_offsets, uint32_t* lods);
+/* Stage functions over host splat arrays (reference renderer.hpp:81-103): gather (update +
+ * projection at time_s; survivors in (instance, gaussian) order; out = NULL queries the
+ * count), sort by (depth bits, instance, gaussian), rasterize in the given order. */
+int gsch_gather_splats(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
+                       const gsch_render_settings* settings, gscg_frame_splat* out, uint64_t capacity,
+                       uint64_t* count);
+int gsch_sort_splats(gsch_renderer* r, gscg_frame_splat* splats, uint64_t n);
+int gsch_rasterize_splats(gsch_renderer* r, const gscg_frame_splat* splats, uint64_t n, int32_t width,
+                          int32_t height, const gsch_render_settings* settings, float* out_rgb, float* out_T);
 /* render_frame(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx) */
 int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
                 const gsch_render_settings* settings, float* out_rgb, float* out_T,

@@ -287,6 +287,13 @@ def memory_report_cell(instances: int, gaussians: int, fixed_overhead: int = 0) 
     return _report(r)
 
 
+# FrameSplat (reference renderer.hpp:39-44) = gscg_frame_splat, 64 bytes
+FRAME_SPLAT_DTYPE = np.dtype([("mean_px", "<f4", (2,)), ("cov_xx", "<f4"), ("cov_xy", "<f4"), ("cov_yy", "<f4"),
+                              ("depth", "<f4"), ("color", "<f4", (3,)), ("opacity", "<f4"), ("instance_id", "<u4"),
+                              ("gaussian_index", "<u4"), ("rect", "<i4", (4,))])
+assert FRAME_SPLAT_DTYPE.itemsize == 64
+
+
 def psnr(a: np.ndarray, b: np.ndarray) -> float:
     """The reference's PSNR (metrics.cpp:8-23) on the host: two H x W x 3 float images."""
     a = np.ascontiguousarray(a, dtype=np.float32)
@@ -340,6 +347,40 @@ class Renderer:
     @property
     def joint_stride(self) -> int:
         return int(N.gsch().gsch_renderer_joint_stride(self._h))
+
+    # ---- stage functions (reference renderer.hpp:81-103) ----
+    def gather_splats(self, time_s: float, settings: Optional[RenderSettings] = None, static_pose: bool = False,
+                      forced_lod: Optional[int] = None) -> np.ndarray:
+        """update + projection at time_s: the surviving splats (FRAME_SPLAT_DTYPE) in
+        (instance, gaussian) order, as the reference's gather_splats concatenates them."""
+        settings = settings or RenderSettings()
+        st = settings.native()
+        n = C.c_uint64()
+        fl = -1 if forced_lod is None else forced_lod
+        N.check_gsch(N.gsch().gsch_gather_splats(self._h, time_s, int(static_pose), fl, C.byref(st), None, 0,
+                                                 C.byref(n)))
+        out = np.zeros(max(n.value, 1), dtype=FRAME_SPLAT_DTYPE)
+        N.check_gsch(N.gsch().gsch_gather_splats(self._h, time_s, int(static_pose), fl, C.byref(st), _ptr(out),
+                                                 out.size, C.byref(n)))
+        return out[:n.value]
+
+    def sort_splats(self, splats: np.ndarray) -> np.ndarray:
+        """Sorted copy by (depth bits, instance, gaussian) (reference sort_splats)."""
+        a = np.ascontiguousarray(splats, dtype=FRAME_SPLAT_DTYPE).copy()
+        N.check_gsch(N.gsch().gsch_sort_splats(self._h, _ptr(a) if a.size else None, a.size))
+        return a
+
+    def rasterize_full(self, splats: np.ndarray, width: int, height: int,
+                       settings: Optional[RenderSettings] = None):
+        """(rgb, T) of the splats binned and blended in the given order (reference
+        rasterize_full)."""
+        settings = settings or RenderSettings()
+        a = np.ascontiguousarray(splats, dtype=FRAME_SPLAT_DTYPE)
+        rgb = np.empty((height, width, 3), dtype=np.float32)
+        T = np.empty((height, width), dtype=np.float32)
+        N.check_gsch(N.gsch().gsch_rasterize_splats(self._h, _ptr(a) if a.size else None, a.size, width, height,
+                                                    C.byref(settings.native()), _ptr(rgb), _ptr(T)))
+        return rgb, T
 
     def alloc_frame(self, pinned: bool = True):
         """(rgb HxWx3, T HxW) float32 output arrays; pinned ones take the direct DMA path."""

@@ -594,6 +594,66 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
 // Sort (splats by depth + ordinal, pairs in that order, pairs stably by cell) and
 // rasterise tile rows [tile_row0, tile_row0 + tile_rows) from the context's records
 // (ctx->S splats, ctx->K pairs whose spans are relative to tile_row0). Events 3..5.
+// Stable LSD radix sort of (keys, vals) over the plan (reduce-then-scan passes) into the
+// ping-pong buffers kb/vb; returns the buffer index holding the result. in_keys/in_vals
+// feed pass 0 (vals may be null = identity). ctx->status / ctx->hist must fit `count`.
+int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb,
+              uint32_t count, const RadixPlan& plan, uint32_t& launches) {
+    cudaStream_t s = ctx->stream;
+    const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
+    int out = 0;
+    for (uint32_t q = 0; q < plan.passes; ++q) {
+        SortPassParams sp{};
+        sp.keys_in = q == 0 ? in_keys : kb[out ^ 1].as<uint32_t>();
+        sp.vals_in = q == 0 ? in_vals : vb[out ^ 1].as<uint32_t>();
+        sp.keys_out = kb[out].as<uint32_t>();
+        sp.vals_out = vb[out].as<uint32_t>();
+        sp.count = count;
+        sp.shift = plan.shift[q];
+        sp.bits = plan.bits[q];
+        sp.tiles = tiles;
+        sp.counts = ctx->status.as<uint32_t>();
+        sp.digit_base = ctx->hist.as<uint32_t>();
+        k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+        k_sort_rows<<<1u << plan.bits[q], 1024, 0, s>>>(sp);
+        k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+        launches += 3;
+        out ^= 1;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return out ^ 1;
+}
+
+// ceil(bits / 5) passes with the bits spread evenly (27 -> 5,5,5,4,4,4). 8-bit digits
+// ranked with warp match (CUB onesweep style) measured slower here: __match_any_sync is
+// slow on sm_100 (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
+RadixPlan make_plan(uint32_t bits) {
+    RadixPlan pl{};
+    bits = std::max(bits, 1u);
+    pl.passes = (bits + kRadixBits - 1) / kRadixBits;
+    uint32_t sh = 0;
+    for (uint32_t q = 0; q < pl.passes; ++q) {
+        const uint32_t w = (bits - sh) / (pl.passes - q) + ((bits - sh) % (pl.passes - q) ? 1u : 0u);
+        pl.shift[q] = sh;
+        pl.bits[q] = w;
+        sh += w;
+    }
+    return pl;
+}
+
+void ensure_sort_buffers(gscg_ctx* ctx, uint32_t splats, uint32_t pairs) {
+    const uint32_t max_elems = std::max(splats, pairs);
+    const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
+    CUDA_TRY(ctx->status.ensure(std::max<size_t>(max_tiles, 1) * kRadix * 4));  // tile digit counts
+    CUDA_TRY(ctx->hist.ensure(kRadix * 4));                                        // digit bases
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(ctx->skeys[b].ensure(std::max<size_t>(splats, 1) * 4));
+        CUDA_TRY(ctx->srecs[b].ensure(std::max<size_t>(splats, 1) * 4));
+        CUDA_TRY(ctx->pcell[b].ensure(std::max<size_t>(pairs, 1) * 4));
+        CUDA_TRY(ctx->precs[b].ensure(std::max<size_t>(pairs, 1) * 4));
+    }
+}
+
 void copy_out(gscg_ctx* ctx, int rows, float* fb_rgb, float* fb_T, bool host);
 
 bool is_host_pointer(const void* p) {
@@ -606,8 +666,10 @@ bool is_host_pointer(const void* p) {
     return at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged;
 }
 
+// presorted: the caller put the splat order in skeys[0] / srecs[0] (distinct keys), so the
+// depth sort is skipped (rasterize_splats: bins follow the given order).
 uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& launches, float* read_rgb = nullptr,
-                     float* read_T = nullptr) {
+                     float* read_T = nullptr, bool presorted = false) {
     cudaStream_t s = ctx->stream;
     const FrameGeom& geo = ctx->geom;
     const uint32_t tiles = static_cast<uint32_t>(geo.tiles_x) * static_cast<uint32_t>(tile_rows);
@@ -622,64 +684,12 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
     if (cells) CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(cells) * 8, s));
     ctx->final_recs = nullptr;
     if (S32 > 0 && K > 0) {
-        const uint32_t max_elems = std::max(S32, K);
-        const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
-        CUDA_TRY(ctx->status.ensure(static_cast<size_t>(max_tiles) * kRadix * 4));  // tile digit counts
-        CUDA_TRY(ctx->hist.ensure(kRadix * 4));                                        // digit bases
-        for (int b = 0; b < 2; ++b) {
-            CUDA_TRY(ctx->skeys[b].ensure(static_cast<size_t>(S32) * 4));
-            CUDA_TRY(ctx->srecs[b].ensure(static_cast<size_t>(S32) * 4));
-            CUDA_TRY(ctx->pcell[b].ensure(static_cast<size_t>(K) * 4));
-            CUDA_TRY(ctx->precs[b].ensure(static_cast<size_t>(K) * 4));
-        }
-        // Stable LSD radix sort of (keys, vals) over the plan (reduce-then-scan passes);
-        // returns the buffer index holding the result. in_keys/in_vals feed pass 0
-        // (vals may be null = identity).
-        auto radix = [&](const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb, uint32_t count,
-                         const RadixPlan& plan) -> int {
-            const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
-            int out = 0;
-            for (uint32_t q = 0; q < plan.passes; ++q) {
-                SortPassParams sp{};
-                sp.keys_in = q == 0 ? in_keys : kb[out ^ 1].as<uint32_t>();
-                sp.vals_in = q == 0 ? in_vals : vb[out ^ 1].as<uint32_t>();
-                sp.keys_out = kb[out].as<uint32_t>();
-                sp.vals_out = vb[out].as<uint32_t>();
-                sp.count = count;
-                sp.shift = plan.shift[q];
-                sp.bits = plan.bits[q];
-                sp.tiles = tiles;
-                sp.counts = ctx->status.as<uint32_t>();
-                sp.digit_base = ctx->hist.as<uint32_t>();
-                k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
-                k_sort_rows<<<1u << plan.bits[q], 1024, 0, s>>>(sp);
-                k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
-                launches += 3;
-                out ^= 1;
-            }
-            CUDA_TRY(cudaGetLastError());
-            return out ^ 1;
-        };
-        // ceil(bits / 5) passes with the bits spread evenly (27 -> 5,5,5,4,4,4). 8-bit digits
-        // ranked with warp match (CUB onesweep style) measured slower here: __match_any_sync
-        // is slow on sm_100 (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
-        const uint32_t digit_bits = kRadixBits;
-        auto make_plan = [digit_bits](uint32_t bits) {
-            RadixPlan pl{};
-            bits = std::max(bits, 1u);
-            pl.passes = (bits + digit_bits - 1) / digit_bits;
-            uint32_t sh = 0;
-            for (uint32_t q = 0; q < pl.passes; ++q) {
-                const uint32_t w = (bits - sh) / (pl.passes - q) + ((bits - sh) % (pl.passes - q) ? 1u : 0u);
-                pl.shift[q] = sh;
-                pl.bits[q] = w;
-                sh += w;
-            }
-            return pl;
-        };
+        ensure_sort_buffers(ctx, S32, K);
         // 1. splats by depth (bits that vary in the frame), ties by ordinal.
-        const RadixPlan dplan = make_plan(static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax)));
-        const int sb = radix(ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan);
+        const RadixPlan dplan = presorted ? RadixPlan{} : make_plan(static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax)));
+        const int sb = presorted ? 0
+                                 : run_radix(ctx, ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32,
+                                             dplan, launches);
         // 2. equal-depth runs by ordinal + cell spans in sorted order + the first cell-sort
         //    digit histogram per 1024 sorted splats; digit offsets; pairs emitted straight
         //    into the order of the first stable cell-sort pass.
@@ -704,8 +714,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), geo.tiles_x, quads, dmask,
                     ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
-        ++launches;
-        launches += 3;
+        launches += 4;
         CUDA_TRY(cudaGetLastError());
         // 3. the remaining stable cell-sort passes; ranges.
         RadixPlan rest{};
@@ -714,8 +723,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             rest.bits[rest.passes] = cplan.bits[q];
             ++rest.passes;
         }
-        const int cb = rest.passes ? radix(ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ctx->pcell,
-                                           ctx->precs, K, rest)
+        const int cb = rest.passes ? run_radix(ctx, ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(),
+                                               ctx->pcell, ctx->precs, K, rest, launches)
                                    : 1;
         const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);
         k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
@@ -1320,6 +1329,205 @@ int gscg_host_alloc(uint64_t bytes, void** out) {
 int gscg_host_free(void* ptr) {
     if (ptr) cudaFreeHost(ptr);
     return GSCG_OK;
+}
+
+int gscg_gather_splats(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                       const gscg_render_settings* settings, const gscg_lod_policy* lod, gscg_frame_splat* out,
+                       uint64_t capacity, uint64_t* count) {
+    if (!ctx || !count) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        validate_frame(ctx, frame, cam, settings, lod);
+        const uint32_t n = frame->instance_count;
+        const uint32_t saved = ctx->debug;
+        ctx->debug |= GSCG_DEBUG_RECORDS;
+        uint32_t launches = 0;
+        ctx->band_state = 0;
+        try {
+            update_gather(ctx, frame, cam, lod, 0, n, launches);
+        } catch (...) {
+            ctx->debug = saved;
+            throw;
+        }
+        ctx->debug = saved;
+        if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDefault, ctx->stream));
+        *count = ctx->S;
+        if (out) {
+            if (capacity < ctx->S) invalid("splat buffer smaller than the frame's splat count");
+            std::vector<gscg_splat_record> rec(ctx->S);
+            if (ctx->S)
+                CUDA_TRY(cudaMemcpyAsync(rec.data(), ctx->rec_dbg.ptr, ctx->S * sizeof(gscg_splat_record),
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            std::sort(rec.begin(), rec.end(), [](const gscg_splat_record& a, const gscg_splat_record& b) {
+                return a.ordinal < b.ordinal;  // = (instance, gaussian) order
+            });
+            for (size_t i = 0; i < rec.size(); ++i) {
+                const gscg_splat_record& r = rec[i];
+                gscg_frame_splat& o = out[i];
+                o.mean_px[0] = r.mean_px[0];
+                o.mean_px[1] = r.mean_px[1];
+                o.cov_xx = r.cov_xx;
+                o.cov_xy = r.cov_xy;
+                o.cov_yy = r.cov_yy;
+                o.depth = r.depth;
+                for (int c = 0; c < 3; ++c) o.color[c] = r.color[c];
+                o.opacity = r.opacity;
+                o.instance_id = r.instance_id;
+                o.gaussian_index = r.gaussian_index;
+                for (int c = 0; c < 4; ++c) o.rect[c] = r.rect[c];
+            }
+        } else {
+            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        }
+    });
+}
+
+int gscg_sort_splats(gscg_ctx* ctx, gscg_frame_splat* splats, uint64_t n) {
+    if (!ctx || (n && !splats)) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (n > 0xF0000000ull) invalid("too many splats");
+        if (n < 2) return;
+        const uint32_t n32 = static_cast<uint32_t>(n);
+        cudaStream_t s = ctx->stream;
+        // Key columns; stable LSD over gaussian, then instance, then depth bits, the
+        // permutation as value: the reference's (depth bits, instance, gaussian) order with
+        // the original position breaking exact duplicates (renderer.cpp:85-107).
+        std::vector<uint32_t> col[3];
+        uint32_t lo[3], hi[3];
+        for (int k = 0; k < 3; ++k) {
+            col[k].resize(n32);
+            lo[k] = 0xffffffffu;
+            hi[k] = 0u;
+        }
+        for (uint32_t i = 0; i < n32; ++i) {
+            uint32_t d;  // the depth's bit pattern, compared as an unsigned integer (renderer.cpp:89)
+            std::memcpy(&d, &splats[i].depth, 4);
+            const uint32_t v[3] = {splats[i].gaussian_index, splats[i].instance_id, d};
+            for (int k = 0; k < 3; ++k) {
+                col[k][i] = v[k];
+                lo[k] = std::min(lo[k], v[k]);
+                hi[k] = std::max(hi[k], v[k]);
+            }
+        }
+        ensure_sort_buffers(ctx, n32, 0);
+        DevBuf keys, perm_in;
+        CUDA_TRY(keys.ensure_exact(n * 4));
+        CUDA_TRY(perm_in.ensure_exact(n * 4));
+        uint32_t launches = 0;
+        int cur = -1;  // buffer index holding the current permutation (srecs), -1: identity
+        for (int k = 0; k < 3; ++k) {
+            if (lo[k] == hi[k]) continue;  // constant column: order unchanged
+            CUDA_TRY(cudaMemcpyAsync(keys.ptr, col[k].data(), n * 4, cudaMemcpyHostToDevice, s));
+            const uint32_t* in_keys = keys.as<uint32_t>();
+            const uint32_t* in_vals = nullptr;
+            if (cur >= 0) {  // this column in the current order
+                k_gather_u32<<<std::min<uint32_t>((n32 + 255) / 256, 4096), 256, 0, s>>>(
+                    keys.as<uint32_t>(), ctx->srecs[cur].as<uint32_t>(), ctx->skeys[cur].as<uint32_t>(), n32);
+                CUDA_TRY(cudaMemcpyAsync(perm_in.ptr, ctx->srecs[cur].ptr, n * 4, cudaMemcpyDeviceToDevice, s));
+                in_keys = ctx->skeys[cur].as<uint32_t>();
+                in_vals = perm_in.as<uint32_t>();
+                // run_radix reads pass-0 input from in_keys while writing kb[0]: stage the
+                // gathered keys outside the ping-pong pair
+                CUDA_TRY(cudaMemcpyAsync(keys.ptr, ctx->skeys[cur].ptr, n * 4, cudaMemcpyDeviceToDevice, s));
+                in_keys = keys.as<uint32_t>();
+            }
+            const RadixPlan plan = make_plan(static_cast<uint32_t>(bits_for(lo[k] ^ hi[k])));
+            cur = run_radix(ctx, in_keys, in_vals, ctx->skeys, ctx->srecs, n32, plan, launches);
+        }
+        if (cur < 0) return;  // all keys equal: already in order
+        std::vector<uint32_t> perm(n32);
+        CUDA_TRY(cudaMemcpyAsync(perm.data(), ctx->srecs[cur].ptr, n * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        std::vector<gscg_frame_splat> tmp(splats, splats + n32);
+        for (uint32_t i = 0; i < n32; ++i) splats[i] = tmp[perm[i]];
+        keys.release();
+        perm_in.release();
+    });
+}
+
+int gscg_rasterize_splats(gscg_ctx* ctx, const gscg_frame_splat* splats, uint64_t n, int32_t width, int32_t height,
+                          const gscg_render_settings* settings, float* fb_rgb, float* fb_T) {
+    if (!ctx || !settings || (n && !splats)) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (settings->tile_size < 1 || settings->tile_size > 64) invalid("RenderSettings: tile_size must be in [1, 64]");
+        if (!(settings->alpha_cutoff > 0.0f && settings->alpha_cutoff < 1.0f))
+            invalid("RenderSettings: alpha_cutoff outside (0,1)");
+        if (!(settings->transmittance_floor > 0.0f && settings->transmittance_floor < 1.0f))
+            invalid("RenderSettings: transmittance_floor outside (0,1)");
+        if (width < 1 || height < 1 || width > 65535 || height > 65535) invalid("rasterize: width and height must be in [1, 65535]");
+        if (n > 0xF0000000ull) invalid("too many splats");
+        FrameGeom& g = ctx->geom;
+        g.W = width;
+        g.H = height;
+        g.ts = settings->tile_size;
+        g.tiles_x = (g.W + g.ts - 1) / g.ts;
+        g.tiles_y = (g.H + g.ts - 1) / g.ts;
+        g.cells_per_tile = g.ts == 16 ? 4u : 1u;
+        g.cell = g.ts == 16 ? 8 : g.ts;
+        ctx->settings = *settings;
+        ctx->band_state = 0;
+        const uint32_t n32 = static_cast<uint32_t>(n);
+        // Conic prep (renderer.cpp:133-141) on the host: the power floor takes the host libm's
+        // logf, as the reference; records in the device layout (gscg_project.cu).
+        std::vector<float4> rec(static_cast<size_t>(n32) * 3);
+        std::vector<uint4> meta(n32);
+        uint64_t pairs = 0;
+        for (uint32_t i = 0; i < n32; ++i) {
+            const gscg_frame_splat& sp = splats[i];
+            int x0 = std::max(0, sp.rect[0]), y0 = std::max(0, sp.rect[1]);
+            int x1 = std::min(width, sp.rect[2]), y1 = std::min(height, sp.rect[3]);
+            const float det = sp.cov_xx * sp.cov_yy - sp.cov_xy * sp.cov_xy;
+            const float inv_det = 1.0f / det;
+            const float a = sp.cov_yy * inv_det, b = -sp.cov_xy * inv_det, c = sp.cov_xx * inv_det;
+            const float pf = std::log(settings->alpha_cutoff / sp.opacity);
+            uint32_t span_lo = 0, span_hi = 0;
+            if (x0 < x1 && y0 < y1) {
+                const int cx0 = x0 / g.cell, cx1 = (x1 - 1) / g.cell, cy0 = y0 / g.cell, cy1 = (y1 - 1) / g.cell;
+                span_lo = static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16);
+                span_hi = static_cast<uint32_t>(cx1 - cx0 + 1) | (static_cast<uint32_t>(cy1 - cy0 + 1) << 16);
+                pairs += static_cast<uint64_t>(cx1 - cx0 + 1) * static_cast<uint64_t>(cy1 - cy0 + 1);
+            } else {
+                x0 = y0 = x1 = y1 = 0;  // empty rect: no cells
+            }
+            float4* r = rec.data() + 3ull * i;
+            r[0] = make_float4(sp.mean_px[0], sp.mean_px[1], a, b);
+            r[1] = make_float4(c, sp.opacity, pf, sp.color[0]);
+            uint32_t xy0 = static_cast<uint32_t>(x0) | (static_cast<uint32_t>(y0) << 16);
+            uint32_t xy1 = static_cast<uint32_t>(x1) | (static_cast<uint32_t>(y1) << 16);
+            float fx0, fx1;
+            std::memcpy(&fx0, &xy0, 4);
+            std::memcpy(&fx1, &xy1, 4);
+            r[2] = make_float4(sp.color[1], sp.color[2], fx0, fx1);
+            meta[i] = make_uint4(i, span_lo, span_hi, 0u);
+        }
+        if (pairs > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "tile-splat pair count exceeds 32-bit indexing");
+        cudaStream_t s = ctx->stream;
+        const uint64_t cap = std::max<uint64_t>(n32, 1);
+        if (cap > ctx->splat_capacity) ctx->splat_capacity = cap + cap / 4;
+        CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
+        CUDA_TRY(ctx->splat_meta.ensure(ctx->splat_capacity * 16));
+        if (n32) {
+            CUDA_TRY(cudaMemcpyAsync(ctx->records.ptr, rec.data(), rec.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(ctx->splat_meta.ptr, meta.data(), meta.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+        }
+        ctx->S = n32;
+        ctx->K = pairs;
+        ctx->G = n32;
+        ensure_sort_buffers(ctx, n32, static_cast<uint32_t>(pairs));
+        if (n32) {  // the given order: distinct keys (no tie fix-up), identity records
+            k_iota2<<<std::min<uint32_t>((n32 + 255) / 256, 4096), 256, 0, s>>>(ctx->skeys[0].as<uint32_t>(),
+                                                                               ctx->srecs[0].as<uint32_t>(), n32);
+            CUDA_TRY(cudaGetLastError());
+        }
+        uint32_t launches = 0;
+        CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
+        sort_raster(ctx, 0, g.tiles_y, launches, nullptr, nullptr, /*presorted=*/true);
+        copy_out(ctx, g.H, fb_rgb, fb_T, true);
+        CUDA_TRY(cudaStreamSynchronize(s));
+    });
 }
 
 int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T) {

@@ -206,6 +206,10 @@ constexpr int kReadbackBands = 4;  // tile-row bands of a frame whose host read-
 // Picks the tile-size specialisation (16: 8x8 quadrant CTAs; else 1/4/16 pixels per thread).
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream);
 
+// stage functions
+__global__ void k_iota2(uint32_t* a, uint32_t* b, uint32_t n);  // a[i] = b[i] = i
+__global__ void k_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t* dst, uint32_t n);
+
 // debug
 __global__ void k_sorted_ordinals(const uint32_t* recs, const uint4* meta, uint32_t count, uint32_t* out);
 

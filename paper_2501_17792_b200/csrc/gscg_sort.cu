@@ -544,6 +544,14 @@ k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges) {
     ranges[prev].y = count;
 }
 
+__global__ void k_iota2(uint32_t* a, uint32_t* b, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = b[i] = i;
+}
+
+__global__ void k_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t* dst, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[idx[i]];
+}
+
 __global__ void k_sorted_ordinals(const uint32_t* recs, const uint4* meta, uint32_t count, uint32_t* out) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
         out[i] = meta[recs[i]].x;

@@ -352,6 +352,85 @@ void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const R
     }
 }
 
+static_assert(sizeof(FrameSplat) == sizeof(gscg_frame_splat), "FrameSplat mirrors gscg_frame_splat");
+
+namespace {
+gscg_render_settings to_gscg(const RenderSettings& settings) {
+    gscg_render_settings rs{};
+    rs.tile_size = settings.tile_size;
+    for (int i = 0; i < 3; ++i) rs.background[i] = settings.background[i];
+    rs.alpha_max = settings.alpha_max;
+    rs.alpha_cutoff = settings.alpha_cutoff;
+    rs.transmittance_floor = settings.transmittance_floor;
+    rs.sh_enabled = settings.sh_colour ? 1 : 0;
+    return rs;
+}
+}  // namespace
+
+SplatFrame gather_splats(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+                         bool static_pose, std::optional<uint32_t> forced_lod, FrameContext& ctx) {
+    validate(settings);
+    validate(camera);
+    validate(crowd.lod);
+    ctx.ensure_templates(crowd.templates);
+    ctx.sample_crowd(crowd, time_s, static_pose, settings.thread_count);
+    gscg_frame_desc fd{};
+    fd.instance_count = static_cast<uint32_t>(crowd.instances.size());
+    fd.joint_stride = ctx.joint_stride;
+    fd.template_ids = ctx.template_ids.data();
+    fd.placement = ctx.placement.data();
+    fd.poses = ctx.poses.data();
+    fd.active_lod = ctx.lods.data();
+    fd.forced_lod = forced_lod ? static_cast<int32_t>(*forced_lod) : -1;
+    fd.memory = GSCG_MEM_HOST;
+    const gscg_camera cam = camera_basis(camera);
+    const gscg_render_settings rs = to_gscg(settings);
+    gscg_lod_policy lp{};
+    lp.threshold_count = static_cast<uint32_t>(crowd.lod.thresholds_m.size());
+    for (uint32_t i = 0; i < lp.threshold_count; ++i) lp.thresholds_m[i] = crowd.lod.thresholds_m[i];
+    lp.hysteresis_band_m = crowd.lod.hysteresis_band_m;
+    uint64_t count = 0;
+    const std::vector<uint32_t> prev_lods = ctx.lods;  // both calls see the same LoD history
+    check_gscg(gscg_gather_splats(ctx.gpu(), &fd, &cam, &rs, &lp, nullptr, 0, &count), ctx.gpu());
+    ctx.lods = prev_lods;
+    fd.active_lod = ctx.lods.data();
+    SplatFrame frame;
+    frame.width = camera.width;
+    frame.height = camera.height;
+    frame.splats.resize(count);
+    // second call returns the records of the same projection (deterministic)
+    check_gscg(gscg_gather_splats(ctx.gpu(), &fd, &cam, &rs, &lp,
+                                  reinterpret_cast<gscg_frame_splat*>(frame.splats.data()), count, &count),
+               ctx.gpu());
+    for (size_t i = 0; i < crowd.instances.size(); ++i) crowd.instances[i].active_lod = ctx.lods[i];
+    return frame;
+}
+
+void sort_splats(SplatFrame& frame, FrameContext& ctx) {
+    check_gscg(gscg_sort_splats(ctx.gpu(), reinterpret_cast<gscg_frame_splat*>(frame.splats.data()),
+                                frame.splats.size()),
+               ctx.gpu());
+}
+
+RasterOutput rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
+                            FrameContext& ctx) {
+    validate(settings);
+    RasterOutput out;
+    out.color = Framebuffer(width, height);
+    out.transmittance.assign(static_cast<size_t>(width) * height, 0.0f);
+    const gscg_render_settings rs = to_gscg(settings);
+    check_gscg(gscg_rasterize_splats(ctx.gpu(), reinterpret_cast<const gscg_frame_splat*>(frame.splats.data()),
+                                     frame.splats.size(), width, height, &rs, out.color.rgb.data(),
+                                     out.transmittance.data()),
+               ctx.gpu());
+    return out;
+}
+
+Framebuffer rasterize(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
+                      FrameContext& ctx) {
+    return std::move(rasterize_full(frame, settings, width, height, ctx).color);
+}
+
 Framebuffer render_frame(Crowd& crowd, const Camera& camera, float time_s,
                          const RenderSettings& settings, bool static_pose,
                          std::optional<uint32_t> forced_lod, StageTimes* times) {

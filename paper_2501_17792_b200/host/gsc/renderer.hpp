@@ -41,6 +41,31 @@ struct Framebuffer {
     }
 };
 
+// Projected splats (reference math.hpp:64-79, renderer.hpp:39-50). FrameSplat is laid
+// out exactly as gscg_frame_splat (64 bytes).
+struct Splat2D {
+    Vec2 mean_px;
+    float cov_xx = 1.0f;
+    float cov_xy = 0.0f;
+    float cov_yy = 1.0f;
+    float depth = 0.0f;  // view-space z, meters
+    Vec3 color = Vec3::Ones();
+    float opacity = 1.0f;
+};
+
+struct FrameSplat {
+    Splat2D splat;
+    uint32_t instance_id = 0;
+    uint32_t gaussian_index = 0;
+    PixelRect bounds;  // 3-sigma rectangle clipped to the image
+};
+
+struct SplatFrame {
+    int width = 0;
+    int height = 0;
+    std::vector<FrameSplat> splats;
+};
+
 struct RasterOutput {
     Framebuffer color;
     std::vector<float> transmittance;
@@ -142,6 +167,19 @@ void render_frame(Crowd& crowd, const Camera& camera, float time_s,
 void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
                        bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
                        FrameContext& ctx, float* out_rgb, float* out_T);
+
+// Stage functions (reference renderer.hpp:81-103) over host splat arrays, on the GPU.
+// gather_splats runs update + projection for time_s (the reference's update_crowd then
+// gather_splats) and returns the survivors in (instance, gaussian) order; sort_splats
+// orders them by (depth bits, instance, gaussian); rasterize / rasterize_full bin and
+// blend them in the given order.
+SplatFrame gather_splats(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+                         bool static_pose, std::optional<uint32_t> forced_lod, FrameContext& ctx);
+void sort_splats(SplatFrame& frame, FrameContext& ctx);
+RasterOutput rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
+                            FrameContext& ctx);
+Framebuffer rasterize(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
+                      FrameContext& ctx);
 
 Framebuffer render_frame(Crowd& crowd, const Camera& camera, float time_s,
                          const RenderSettings& settings, bool static_pose = false,

@@ -446,6 +446,48 @@ int gsch_lod_quality_sweep(gsch_scene* s, uint32_t template_id, const float* dis
     });
 }
 
+int gsch_gather_splats(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
+                       const gsch_render_settings* st, gscg_frame_splat* out, uint64_t capacity, uint64_t* count) {
+    return guarded([&] {
+        if (!r || !st || !count) throw std::invalid_argument("null argument");
+        std::optional<uint32_t> forced;
+        if (forced_lod >= 0) forced = static_cast<uint32_t>(forced_lod);
+        const SplatFrame f = gather_splats(r->scene->crowd, r->scene->camera, time_s, to_settings(st), static_pose != 0,
+                                           forced, *r->ctx);
+        *count = f.splats.size();
+        if (out) {
+            if (capacity < f.splats.size()) throw std::invalid_argument("splat buffer too small");
+            std::memcpy(out, f.splats.data(), f.splats.size() * sizeof(gscg_frame_splat));
+        }
+    });
+}
+
+int gsch_sort_splats(gsch_renderer* r, gscg_frame_splat* splats, uint64_t n) {
+    return guarded([&] {
+        if (!r || (n && !splats)) throw std::invalid_argument("null argument");
+        check_gscg(gscg_sort_splats(r->ctx->gpu(), splats, n), r->ctx->gpu());
+    });
+}
+
+int gsch_rasterize_splats(gsch_renderer* r, const gscg_frame_splat* splats, uint64_t n, int32_t width, int32_t height,
+                          const gsch_render_settings* st, float* out_rgb, float* out_T) {
+    return guarded([&] {
+        if (!r || !st || (n && !splats)) throw std::invalid_argument("null argument");
+        const gscg_render_settings rs = [&] {
+            gscg_render_settings x{};
+            x.tile_size = st->tile_size;
+            for (int i = 0; i < 3; ++i) x.background[i] = st->background[i];
+            x.alpha_max = st->alpha_max;
+            x.alpha_cutoff = st->alpha_cutoff;
+            x.transmittance_floor = st->transmittance_floor;
+            x.sh_enabled = st->sh_colour;
+            return x;
+        }();
+        if (!(rs.alpha_max > 0.0f && rs.alpha_max <= 1.0f)) throw std::invalid_argument("RenderSettings: alpha_max outside (0,1]");
+        check_gscg(gscg_rasterize_splats(r->ctx->gpu(), splats, n, width, height, &rs, out_rgb, out_T), r->ctx->gpu());
+    });
+}
+
 int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
                 const gsch_render_settings* st, float* out_rgb, float* out_T, gsch_stage_times* times) {
     return guarded([&] {

@@ -134,6 +134,12 @@ GSCG_SYMBOLS = {
     "gscg_template_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "gscg_upload_motion": (C.c_int, [_P, C.c_uint32, C.POINTER(GscgMotionDesc)]),
     "gscg_eval_sinf": (C.c_int, [_P, _P, _P, C.c_uint32]),
+    "gscg_gather_splats": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
+                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, C.c_uint64,
+                                     C.POINTER(C.c_uint64)]),
+    "gscg_sort_splats": (C.c_int, [_P, _P, C.c_uint64]),
+    "gscg_rasterize_splats": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(GscgRenderSettings),
+                                        _P, _P]),
     "gscg_set_debug": (C.c_int, [_P, C.c_uint32]),
     "gscg_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P,
@@ -198,6 +204,10 @@ GSCH_SYMBOLS = {
     "gsch_memory_report_cell": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(GschMemoryReport)]),
     "gsch_scene_memory_report": (C.c_int, [_P, C.POINTER(GschMemoryReport)]),
     "gsch_renderer_set_device_poses": (C.c_int, [_P, C.c_int32]),
+    "gsch_gather_splats": (C.c_int, [_P, C.c_float, C.c_int32, C.c_int32, _P, _P, C.c_uint64,
+                                     C.POINTER(C.c_uint64)]),
+    "gsch_sort_splats": (C.c_int, [_P, _P, C.c_uint64]),
+    "gsch_rasterize_splats": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_int32, _P, _P, _P]),
     "gsch_renderer_prepare": (C.c_int, [_P]),
     "gsch_fill_instances": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P]),
     "gsch_renderer_create": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
