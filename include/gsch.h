@@ -115,6 +115,9 @@ int gsch_scene_set_motion(gsch_scene* scene, uint32_t motion_id, float fps, uint
  * frame. Format failures return GSCH_ERR_FORMAT with "[Kind] message" in gsch_last_error
  * (Kind: IoError, BadMagic, VersionMismatch, Truncated, InvariantViolation). */
 #define GSCH_ERR_FORMAT (-6)
+/* update_crowd's LoD step (crowd.cpp:86-110) on the host: sets every instance's active
+ * level for the scene camera (forced_lod < 0: distance LoD with hysteresis). */
+int gsch_scene_update_crowd(gsch_scene* scene, int32_t forced_lod);
 int gsch_scene_save_template(const gsch_scene* scene, uint32_t template_id, const char* path);
 int gsch_scene_load_template(gsch_scene* scene, uint32_t template_id, const char* path);
 int gsch_scene_save_motion(const gsch_scene* scene, uint32_t motion_id, const char* path);

@@ -229,6 +229,10 @@ class Scene:
         data = np.ascontiguousarray(data, dtype=np.float32)
         N.check_gsch(N.gsch().gsch_scene_set_motion(self._h, m, fps, data.shape[0], joints, _ptr(data)))
 
+    def update_crowd(self, forced_lod: Optional[int] = None) -> None:
+        """update_crowd's LoD step on the host (crowd.cpp:86-110): instances' active_lod."""
+        N.check_gsch(N.gsch().gsch_scene_update_crowd(self._h, -1 if forced_lod is None else forced_lod))
+
     # ---- asset files (GSAT templates, GSMO motions; reference io.hpp:38-43) ----
     def save_template(self, t: int, path) -> None:
         N.check_gsch(N.gsch().gsch_scene_save_template(self._h, t, str(path).encode()))

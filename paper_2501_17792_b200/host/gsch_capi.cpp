@@ -281,6 +281,15 @@ int gsch_scene_set_motion(gsch_scene* s, uint32_t m, float fps, uint32_t frames,
     });
 }
 
+int gsch_scene_update_crowd(gsch_scene* s, int32_t forced_lod) {
+    return guarded([&] {
+        if (!s) throw std::invalid_argument("null scene");
+        UpdateOptions opts;
+        if (forced_lod >= 0) opts.forced_lod = static_cast<uint32_t>(forced_lod);
+        update_crowd(s->crowd, s->camera, opts);
+    });
+}
+
 int gsch_scene_save_template(const gsch_scene* s, uint32_t t, const char* path) {
     return guarded([&] {
         if (!s || !path) throw std::invalid_argument("null argument");

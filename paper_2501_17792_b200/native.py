@@ -181,6 +181,7 @@ GSCH_SYMBOLS = {
     "gsch_psnr": (C.c_int, [_P, _P, C.c_uint32, C.c_uint32, C.POINTER(C.c_float)]),
     "gsch_lod_quality_sweep": (C.c_int, [_P, C.c_uint32, _P, C.c_uint32, _P, C.c_int, _P, C.c_uint32,
                                          C.POINTER(C.c_uint32)]),
+    "gsch_scene_update_crowd": (C.c_int, [_P, C.c_int32]),
     "gsch_scene_save_template": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
     "gsch_scene_load_template": (C.c_int, [_P, C.c_uint32, C.c_char_p]),
     "gsch_scene_save_motion": (C.c_int, [_P, C.c_uint32, C.c_char_p]),

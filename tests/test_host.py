@@ -276,3 +276,20 @@ def test_psnr_reference_definition():
     assert P.psnr(a, c) <= 99.0
     with pytest.raises(ValueError):
         P.psnr(a, a[:, :-1])
+
+
+def test_update_crowd_lod_matches_oracle():
+    import paper_2501_17792_b200 as P
+    from oracle import orc
+
+    cfg, _ = P.baseline_config(2)
+    cfg.lod_hysteresis = 0.5
+    scene = P.Scene(cfg)
+    o = orc.from_scene(scene)
+    o.render(0.0, orc.settings(sh_colour=True), threads=4)
+    scene.update_crowd()
+    lods = scene.instances["active_lod"]
+    assert np.array_equal(lods, o.lods(len(lods)))
+    assert len(set(lods.tolist())) == 3  # all three levels present at config 2
+    scene.update_crowd(forced_lod=7)  # clamped to the coarsest level
+    assert np.all(scene.instances["active_lod"] == 2)
