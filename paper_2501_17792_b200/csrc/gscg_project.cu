@@ -236,11 +236,14 @@ k_project(ProjectParams p) {
                             float Y[15];
                             sh_basis(vx / nrm, vy / nrm, vz / nrm, Y);
                             const float* sh = s_sh + tid * kShFloats;
+                            // Colour only reaches pixels (1e-3 tolerance), never the
+                            // bit-exact geometry: fused multiply-adds here (colours agree
+                            // with the oracle to ~1e-7).
 #pragma unroll
                             for (int q = 0; q < 15; ++q) {
-                                col0 = col0 + Y[q] * sh[3 * q + 0];
-                                col1 = col1 + Y[q] * sh[3 * q + 1];
-                                col2 = col2 + Y[q] * sh[3 * q + 2];
+                                col0 = fmaf(Y[q], sh[3 * q + 0], col0);
+                                col1 = fmaf(Y[q], sh[3 * q + 1], col1);
+                                col2 = fmaf(Y[q], sh[3 * q + 2], col2);
                             }
                             col0 = fmaxf(col0, 0.0f);
                             col1 = fmaxf(col1, 0.0f);
