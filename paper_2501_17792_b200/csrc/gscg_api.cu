@@ -143,6 +143,7 @@ struct gscg_ctx {
     uint64_t splat_capacity = 0, pair_capacity = 0;
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
+    DevBuf long_runs;  // long equal-depth runs found by k_sorted_spans (+ their count)
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
     DevBuf fb_rgb, fb_T;
@@ -701,8 +702,20 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
         static_assert(kMetaThreads * kStreamItems == 1024, "one splat block per CTA");
         const int quads = geo.cells_per_tile == 4 ? 1 : 0;
+        const uint32_t long_cap = S32 / kLongRun + 1;  // runs longer than kLongRun: at most S / kLongRun
+        CUDA_TRY(ctx->long_runs.ensure(static_cast<size_t>(long_cap) * 8 + 16));
+        uint32_t* long_count = reinterpret_cast<uint32_t*>(ctx->long_runs.as<uint2>() + long_cap);
+        CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
         k_sorted_spans<<<sblocks, kMetaThreads, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
-                                                        ctx->splat_meta.as<uint4>(), S32, ctx->span_sorted.as<uint2>());
+                                                        ctx->splat_meta.as<uint4>(), S32, ctx->span_sorted.as<uint2>(),
+                                                        ctx->long_runs.as<uint2>(), long_count, long_cap);
+        k_long_runs_warp<<<ctx->sm_count * 4, 256, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
+                                                           ctx->span_sorted.as<uint2>(), ctx->long_runs.as<uint2>(),
+                                                           long_count, long_cap);
+        k_long_runs<<<ctx->sm_count * 2, 256, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
+                                                      ctx->span_sorted.as<uint2>(), ctx->long_runs.as<uint2>(),
+                                                      long_count, long_cap);
+        launches += 2;
         launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), nullptr, geo.tiles_x, quads, dmask, nullptr, nullptr);
         SortPassParams bp{};
@@ -879,7 +892,7 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                       &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
                       &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch, &ctx->d_motions, &ctx->d_roots,
-                      &ctx->d_keys, &ctx->motion_ids, &ctx->phases};
+                      &ctx->d_keys, &ctx->motion_ids, &ctx->phases, &ctx->long_runs};
     for (DevBuf* b : bufs) b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
@@ -1230,7 +1243,8 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
                                 &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
                                 &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                                 &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals,
-                                &ctx->fb_rgb, &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch};
+                                &ctx->fb_rgb, &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch,
+                                &ctx->long_runs};
         for (const DevBuf* b : bufs) out->frame_bytes += b->cap;
         out->pinned_bytes = ctx->pinned_cap + sizeof(FrameCounters) + GSCG_MAX_BANDS * 8;
         size_t fr = 0, tot = 0;

@@ -147,8 +147,15 @@ __global__ void k_sort_rows(SortPassParams p);
 __global__ void k_sort_downsweep(SortPassParams p);
 
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
+constexpr uint32_t kLongRun = 32;       // equal-depth runs longer than this go to k_long_runs
+constexpr uint32_t kLongRunCap = 4096;  // k_long_runs sorts runs up to this size in shared memory
+constexpr uint32_t kWarpRunCap = 256;   // runs up to this size: one warp each (k_long_runs_warp)
+__global__ void k_long_runs_warp(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
+                                 const uint32_t* long_count, uint32_t long_cap);
 __global__ void k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
-                               uint2* span_sorted);
+                               uint2* span_sorted, uint2* long_runs, uint32_t* long_count, uint32_t long_cap);
+__global__ void k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
+                            const uint32_t* long_count, uint32_t long_cap);
 constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
 constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
 constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes

@@ -257,6 +257,9 @@ __device__ __forceinline__ void for_each_cell(uint2 sp, int tiles_x, int quads, 
 
 struct SpanSink {
     uint2* span_sorted;
+    uint2* long_runs;  // (start, length) of runs longer than kLongRun, ordered by k_long_runs
+    uint32_t* long_count;
+    uint32_t long_cap;
     __device__ void put(uint32_t pos, uint4 m) { span_sorted[pos] = make_uint2(m.y, m.z); }
 };
 
@@ -267,6 +270,13 @@ __device__ __forceinline__ uint32_t finish_run(const uint32_t* keys, uint32_t* r
     const uint32_t k = keys[s];
     uint32_t end = s + 1;
     while (end < count && keys[end] == k) ++end;
+    if (end - s > kLongRun) {  // long run (e.g. a row of same-pose characters at full detail)
+        const uint32_t slot = atomicAdd(sink.long_count, 1u);
+        if (slot < sink.long_cap) {
+            sink.long_runs[slot] = make_uint2(s, end - s);
+            return end;
+        }
+    }
     for (uint32_t a = s + 1; a < end; ++a) {
         const uint32_t ra = recs[a];
         const uint32_t oa = meta[ra].x;
@@ -284,10 +294,14 @@ __device__ __forceinline__ uint32_t finish_run(const uint32_t* keys, uint32_t* r
 }  // namespace
 
 __global__ void __launch_bounds__(kMetaThreads)
-k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted) {
+k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted,
+               uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
     SpanSink sink;
     sink.span_sorted = span_sorted;
+    sink.long_runs = long_runs;
+    sink.long_count = long_count;
+    sink.long_cap = long_cap;
     const uint32_t b = (blockIdx.x * kMetaThreads + threadIdx.x) * kStreamItems;
     if (b + kStreamItems < count) {
         uint32_t k[kStreamItems + 1];
@@ -369,6 +383,122 @@ k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t
                 ++i;
             }
         }
+    }
+}
+
+// Long equal-depth runs (> kLongRun splats) recorded by k_sorted_spans: one CTA per run
+// sorts (ordinal, record) in shared memory (bitonic, up to kLongRunCap) and writes the
+// records and their spans; longer runs fall back to one thread's insertion sort.
+__global__ void __launch_bounds__(256)
+k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
+            const uint32_t* long_count, uint32_t long_cap) {
+    __shared__ unsigned long long s_kv[kLongRunCap];
+    const uint32_t runs = min(*long_count, long_cap);
+    for (uint32_t r = blockIdx.x; r < runs; r += gridDim.x) {
+        const uint2 run = long_runs[r];
+        const uint32_t s = run.x, n = run.y;
+        if (n <= kWarpRunCap) continue;  // k_long_runs_warp
+        if (n <= kLongRunCap) {
+            uint32_t P = 1;
+            while (P < n) P <<= 1;
+            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                unsigned long long kv = ~0ull;
+                if (i < n) {
+                    const uint32_t rec = recs[s + i];
+                    kv = (static_cast<unsigned long long>(meta[rec].x) << 32) | rec;
+                }
+                s_kv[i] = kv;
+            }
+            __syncthreads();
+            for (uint32_t k = 2; k <= P; k <<= 1) {
+                for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                        const uint32_t l = i ^ j;
+                        if (l > i) {
+                            const unsigned long long a = s_kv[i], b = s_kv[l];
+                            const bool up = (i & k) == 0;
+                            if ((a > b) == up) {
+                                s_kv[i] = b;
+                                s_kv[l] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint32_t rec = static_cast<uint32_t>(s_kv[i]);
+                recs[s + i] = rec;
+                const uint4 m = meta[rec];
+                span_sorted[s + i] = make_uint2(m.y, m.z);
+            }
+            __syncthreads();
+        } else if (threadIdx.x == 0) {
+            for (uint32_t a = s + 1; a < s + n; ++a) {
+                const uint32_t ra = recs[a];
+                const uint32_t oa = meta[ra].x;
+                uint32_t j = a;
+                while (j > s && meta[recs[j - 1]].x > oa) {
+                    recs[j] = recs[j - 1];
+                    --j;
+                }
+                recs[j] = ra;
+            }
+            for (uint32_t a = s; a < s + n; ++a) {
+                const uint4 m = meta[recs[a]];
+                span_sorted[a] = make_uint2(m.y, m.z);
+            }
+        }
+    }
+}
+
+// The runs of up to kWarpRunCap splats (most long runs: a few dozen same-depth splats):
+// one warp per run, bitonic on (ordinal, record) in the warp's shared slice.
+__global__ void __launch_bounds__(256)
+k_long_runs_warp(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
+                 const uint32_t* long_count, uint32_t long_cap) {
+    __shared__ unsigned long long s_kv[8][kWarpRunCap];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long* kv = s_kv[warp];
+    const uint32_t runs = min(*long_count, long_cap);
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp; r < runs; r += warps) {
+        const uint2 run = long_runs[r];
+        const uint32_t s = run.x, n = run.y;
+        if (n > kWarpRunCap) continue;  // k_long_runs
+        uint32_t P = 32;
+        while (P < n) P <<= 1;
+        for (uint32_t i = lane; i < P; i += 32) {
+            unsigned long long v = ~0ull;
+            if (i < n) {
+                const uint32_t rec = recs[s + i];
+                v = (static_cast<unsigned long long>(meta[rec].x) << 32) | rec;
+            }
+            kv[i] = v;
+        }
+        __syncwarp();
+        for (uint32_t k = 2; k <= P; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = lane; i < P; i += 32) {
+                    const uint32_t l = i ^ j;
+                    if (l > i) {
+                        const unsigned long long a = kv[i], b = kv[l];
+                        if ((a > b) == ((i & k) == 0)) {
+                            kv[i] = b;
+                            kv[l] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t rec = static_cast<uint32_t>(kv[i]);
+            recs[s + i] = rec;
+            const uint4 m = meta[rec];
+            span_sorted[s + i] = make_uint2(m.y, m.z);
+        }
+        __syncwarp();
     }
 }
 
