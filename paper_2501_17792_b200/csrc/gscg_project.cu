@@ -157,10 +157,11 @@ k_project(ProjectParams p) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (wk[q] == 0.0f) continue;
-                    const float* S = s_inst + jidx[q] * 12;
-                    const float vx = ((S[0] * c0.x + S[1] * c0.y) + S[2] * c0.z) + S[3] * 1.0f;
-                    const float vy = ((S[4] * c0.x + S[5] * c0.y) + S[6] * c0.z) + S[7] * 1.0f;
-                    const float vz = ((S[8] * c0.x + S[9] * c0.y) + S[10] * c0.z) + S[11] * 1.0f;
+                    const float4* S = reinterpret_cast<const float4*>(s_inst + jidx[q] * 12);  // 3 rows, 48-B aligned
+                    const float4 r0 = S[0], r1 = S[1], r2 = S[2];
+                    const float vx = ((r0.x * c0.x + r0.y * c0.y) + r0.z * c0.z) + r0.w * 1.0f;
+                    const float vy = ((r1.x * c0.x + r1.y * c0.y) + r1.z * c0.z) + r1.w * 1.0f;
+                    const float vz = ((r2.x * c0.x + r2.y * c0.y) + r2.z * c0.z) + r2.w * 1.0f;
                     ax = ax + wk[q] * vx;
                     ay = ay + wk[q] * vy;
                     az = az + wk[q] * vz;
