@@ -278,7 +278,8 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                 recv, rc = ex.all_to_all(send, br.counts.tolist())
                 rgb, T = br.render_band(recv, sum(rc), rows[rank], rows[rank + 1])
                 ex.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
-                balancer.observe(d_lods[:n].cpu().numpy(), br.band_row_pairs(), rows[rank] // settings.tile_size, ex)
+                if f % 4 == 0:  # re-balance every 4th frame (the observation reads back LoDs and cell ranges)
+                    balancer.observe(d_lods[:n].cpu().numpy(), br.band_row_pairs(), rows[rank] // settings.tile_size, ex)
             a, b = br.shard_times, br.band_times
             return {"update": a.update_ms, "gather": a.gather_ms, "route": a.sort_ms, "unpack": b.gather_ms,
                     "sort": b.sort_ms, "rasterize": b.rasterize_ms,

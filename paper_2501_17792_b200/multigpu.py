@@ -336,6 +336,7 @@ class DistributedRenderer:
         self.scene = scene
         self.rows: Optional[list[int]] = None
         self.balancer: Optional[LoadBalancer] = None
+        self.balance_every = 4  # frames between load-balance observations (each reads back small state)
 
     def render_frame(self, time_s: float, settings=None, static_pose: bool = False,
                      forced_lod: Optional[int] = None, rows: Optional[Sequence[int]] = None):
@@ -358,8 +359,10 @@ class DistributedRenderer:
             recv, rc = self.exchange.all_to_all(send, self.band.counts.tolist())
             rgb, T = self.band.render_band(recv, sum(rc), rows[self.rank], rows[self.rank + 1])
             full = self.exchange.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
-            self.balancer.observe(self.band.lods[:n], self.band.band_row_pairs(), rows[self.rank] // settings.tile_size,
-                                  self.exchange)
+            self._frames = getattr(self, "_frames", 0) + 1
+            if self._frames % self.balance_every == 1 or self.balance_every == 1:
+                self.balancer.observe(self.band.lods[:n], self.band.band_row_pairs(),
+                                      rows[self.rank] // settings.tile_size, self.exchange)
             if full is None:
                 return None
             # one read-back into page-locked memory, then split into the API's two arrays
