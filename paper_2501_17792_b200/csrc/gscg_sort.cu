@@ -388,7 +388,7 @@ k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t
 
 // Long equal-depth runs (> kLongRun splats) recorded by k_sorted_spans: one CTA per run
 // sorts (ordinal, record) in shared memory (bitonic, up to kLongRunCap) and writes the
-// records and their spans; longer runs fall back to one thread's insertion sort.
+// records and their spans; longer runs are sorted in place in global memory.
 __global__ void __launch_bounds__(256)
 k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
             const uint32_t* long_count, uint32_t long_cap) {
@@ -433,21 +433,43 @@ k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* 
                 span_sorted[s + i] = make_uint2(m.y, m.z);
             }
             __syncthreads();
-        } else if (threadIdx.x == 0) {
-            for (uint32_t a = s + 1; a < s + n; ++a) {
-                const uint32_t ra = recs[a];
-                const uint32_t oa = meta[ra].x;
-                uint32_t j = a;
-                while (j > s && meta[recs[j - 1]].x > oa) {
-                    recs[j] = recs[j - 1];
-                    --j;
+        } else {
+            // Longer runs: bitonic in place in global memory over the whole CTA, in the
+            // all-ascending form (each merge starts by comparing i with its mirror in the
+            // block) so positions >= n act as +inf and are simply skipped. Ordinals are
+            // unique per splat.
+            uint32_t* r = recs + s;
+            uint32_t P = 1;
+            while (P < n) P <<= 1;
+            for (uint32_t k = 2; k <= P; k <<= 1) {
+                for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                    for (uint32_t t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+                        uint32_t i, l;
+                        if (j == (k >> 1)) {  // mirror step
+                            const uint32_t blk = t / j, off = t % j;
+                            i = blk * k + off;
+                            l = blk * k + k - 1u - off;
+                        } else {  // half-cleaner
+                            const uint32_t blk = t / j, off = t % j;
+                            i = blk * 2u * j + off;
+                            l = i + j;
+                        }
+                        if (l < n) {
+                            const uint32_t ra = r[i], rb = r[l];
+                            if (meta[ra].x > meta[rb].x) {
+                                r[i] = rb;
+                                r[l] = ra;
+                            }
+                        }
+                    }
+                    __syncthreads();
                 }
-                recs[j] = ra;
             }
-            for (uint32_t a = s; a < s + n; ++a) {
-                const uint4 m = meta[recs[a]];
-                span_sorted[a] = make_uint2(m.y, m.z);
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint4 m = meta[r[i]];
+                span_sorted[s + i] = make_uint2(m.y, m.z);
             }
+            __syncthreads();
         }
     }
 }

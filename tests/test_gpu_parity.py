@@ -127,6 +127,38 @@ def test_moving_one_instance_changes_only_its_footprint():
     assert (xs >= box[0]).all() and (xs < box[2]).all() and (ys >= box[1]).all() and (ys < box[3]).all()
 
 
+def test_long_equal_depth_runs_are_ordered_by_ordinal():
+    """Stacked same-pose characters give every template Gaussian one depth per stack, so
+    the depth sort sees equal-key runs of each stack's size: <= 32 (k_sorted_spans in
+    registers), <= 256 (k_long_runs_warp), <= 4096 (k_long_runs, shared memory) and
+    beyond (k_long_runs, global bitonic). The reference orders ties by (instance,
+    gaussian) (renderer.cpp:91-96)."""
+    cfg = P.SceneConfig(template_count=1, template_seed_base=5, level_counts=(24, 12, 6), with_sh=False,
+                        motion_count=1, motion_frames=8, grid_rows=1, grid_cols=1, crowd_count=1, crowd_seed=1,
+                        cam_pos=(0.0, 1.0, -4.0), cam_look=(0.0, 1.0, 6.0), width=160, height=96)
+    s = P.Scene(cfg)
+    proto = s.instances[:1]
+    stacks = [5, 33, 200, 257, 1500, 4097, 5000]
+    inst = np.concatenate([np.repeat(proto, n) for n in stacks])
+    inst["instance_id"] = np.arange(len(inst))
+    inst["yaw"] = 0.0
+    inst["phase_offset_s"] = 0.0
+    inst["x"] = np.concatenate([np.full(n, -1.2 + 0.4 * g, np.float32) for g, n in enumerate(stacks)])
+    inst["z"] = np.concatenate([np.full(n, 0.25 * g, np.float32) for g, n in enumerate(stacks)])
+    rng = np.random.default_rng(5)
+    inst = inst[rng.permutation(len(inst))]  # stacks interleaved in instance order
+    inst["instance_id"] = np.arange(len(inst))
+    s.instances = inst
+    rep = parity(s, 0.0, static_pose=True, forced_lod=0)
+    assert rep["S"] > 0
+    # the runs really are long: one depth value per (stack, gaussian)
+    r = P.Renderer(s)
+    r.set_debug(2)
+    r.render_frame(0.0, P.RenderSettings(), True, 0)
+    _, run_len = np.unique(r.splat_records()["depth"], return_counts=True)
+    assert run_len.max() >= 4097
+
+
 def test_repeated_frames_are_byte_identical():
     s = basic_scene(count=16)
     r = P.Renderer(s)
