@@ -233,9 +233,11 @@ k_project(ProjectParams p) {
                         if (use_sh) {
                             // SH residual colour: dir = normalize(mean - cam).
                             const float vx = ax - cam.pos[0], vy = ay - cam.pos[1], vz = az - cam.pos[2];
-                            const float nrm = sqrtf(vx * vx + (vy * vy + vz * vz));
+                            // One MUFU.RSQ instead of an IEEE sqrt and three IEEE
+                            // divisions (colour tolerance, see below).
+                            const float inrm = rsqrtf(vx * vx + (vy * vy + vz * vz));
                             float Y[15];
-                            sh_basis(vx / nrm, vy / nrm, vz / nrm, Y);
+                            sh_basis(vx * inrm, vy * inrm, vz * inrm, Y);
                             const float* sh = s_sh + tid * kShFloats;
                             // Colour only reaches pixels (1e-3 tolerance), never the
                             // bit-exact geometry: fused multiply-adds here (colours agree
