@@ -204,6 +204,20 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                       const gscg_render_settings* settings, const gscg_lod_policy* lod,
                       float* fb_rgb, float* fb_T, gscg_stage_times* times);
 
+/* Pipelined gscg_render_frame for streaming callers (same arguments and errors; the
+ * reference's render_frame, renderer.cpp:249-280, called once per frame). With host
+ * destinations it returns once the frame is rendered and the LoD state written back;
+ * the framebuffer read-back into fb_rgb / fb_T keeps running on a copy stream,
+ * overlapped with the next frame, which renders into a second device framebuffer.
+ * fb_rgb / fb_T of a frame are valid after gscg_wait_readback; a caller alternating two
+ * host buffers submits frame k, then waits for frame k-1 (frames_back = 1). */
+int gscg_render_frame_async(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                            const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                            float* fb_rgb, float* fb_T, gscg_stage_times* times);
+/* Blocks until the host read-back of the frame submitted `frames_back` submissions ago
+ * (0 = the last one) has landed. Frames further back than 1 are always complete. */
+int gscg_wait_readback(gscg_ctx* ctx, uint32_t frames_back);
+
 /* Page-locked host memory (cudaMallocHost) for frame inputs/outputs: device <-> host copies
  * to and from it run at full DMA speed (gscg_render_frame's host-mode framebuffer read-back
  * goes straight into it). */

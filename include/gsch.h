@@ -178,6 +178,13 @@ int gsch_rasterize_splats(gsch_renderer* r, const gscg_frame_splat* splats, uint
 int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
                 const gsch_render_settings* settings, float* out_rgb, float* out_T,
                 gsch_stage_times* times);
+/* Streaming render (render_frame_async / gscg_render_frame_async): out_rgb / out_T are
+ * filled in the background while the next frame renders; valid after
+ * gsch_wait_readback(r, frames_back) (0 = the last submitted frame). */
+int gsch_render_async(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
+                      const gsch_render_settings* settings, float* out_rgb, float* out_T,
+                      gsch_stage_times* times);
+int gsch_wait_readback(gsch_renderer* r, uint32_t frames_back);
 /* Host pose sampling only (the "update" host part) into caller buffers:
  * template_ids n, placement n x 4, poses n x (4 + 4*joint_stride). */
 int gsch_sample_crowd(gsch_renderer* r, float time_s, int32_t static_pose, int32_t threads,

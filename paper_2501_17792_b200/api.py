@@ -394,11 +394,16 @@ class Renderer:
         return pinned_array((H, W, 3)), pinned_array((H, W))
 
     def render_frame(self, time_s: float, settings: Optional[RenderSettings] = None, static_pose: bool = False,
-                     forced_lod: Optional[int] = None, times: Optional[StageTimes] = None, out=None):
+                     forced_lod: Optional[int] = None, times: Optional[StageTimes] = None, out=None,
+                     pipelined: bool = False):
         """Renders one frame; returns (rgb, T). `out` = (rgb, T) arrays to fill (e.g. from
         alloc_frame(pinned=True)), else fresh arrays are returned. With out = (rgb, None)
         only the colour is read back (the reference render_frame returns just the
-        Framebuffer; T is rasterize_full's extra output) and T is returned as None."""
+        Framebuffer; T is rasterize_full's extra output) and T is returned as None.
+
+        pipelined=True (gsch_render_async): returns once the frame is rendered while its
+        read-back into `out` continues, overlapped with the next frame; the arrays are
+        valid after wait_readback(). Streaming callers alternate two `out` pairs."""
         settings = settings or RenderSettings()
         W, H = self.scene.cfg.width, self.scene.cfg.height
         if out is None:
@@ -410,14 +415,19 @@ class Renderer:
                     T is not None and (T.shape != (H, W) or T.dtype != np.float32 or not T.flags.c_contiguous)):
                 raise ValueError("out must be C-contiguous float32 arrays of shape (H, W, 3) and (H, W)")
         st = N.GschStageTimes()
-        N.check_gsch(N.gsch().gsch_render(self._h, time_s, int(static_pose), -1 if forced_lod is None else forced_lod,
-                                          C.byref(settings.native()), _ptr(rgb), None if T is None else _ptr(T),
-                                          C.byref(st)))
+        fn = N.gsch().gsch_render_async if pipelined else N.gsch().gsch_render
+        N.check_gsch(fn(self._h, time_s, int(static_pose), -1 if forced_lod is None else forced_lod,
+                        C.byref(settings.native()), _ptr(rgb), None if T is None else _ptr(T), C.byref(st)))
         if times is not None:
             for f in ("update_ms", "gather_ms", "sort_ms", "rasterize_ms", "pose_ms", "splat_count", "pair_count",
                       "gaussian_count"):
                 setattr(times, f, getattr(st, f))
         return rgb, T
+
+    def wait_readback(self, frames_back: int = 0) -> None:
+        """Blocks until the read-back of the pipelined frame submitted `frames_back`
+        frames ago (0 = the last) has landed in its `out` arrays."""
+        N.check_gsch(N.gsch().gsch_wait_readback(self._h, frames_back))
 
     def memory_usage(self) -> dict:
         """Device bytes of the shared template store and the per-frame buffers (gscg_memory_usage)."""

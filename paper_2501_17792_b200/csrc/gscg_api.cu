@@ -147,12 +147,19 @@ struct gscg_ctx {
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
     DevBuf fb_rgb, fb_T;
+    // Pipelined host frames alternate two framebuffers: one is read back on the copy
+    // stream while the next frame renders into the other. rb_ev marks the end of the
+    // read-back of fb_rgb/fb_T (the _alt members travel with their buffer).
+    DevBuf fb_rgb_alt, fb_T_alt;
+    cudaEvent_t rb_ev = nullptr, rb_ev_alt = nullptr;
     // debug
     DevBuf posed_dbg, rec_dbg;
 
     void* pinned = nullptr;
     size_t pinned_cap = 0;
     FrameCounters* h_counters = nullptr;
+    uint32_t* h_lod = nullptr;  // page-locked LoD read-back (host frames)
+    size_t h_lod_cap = 0;
     cudaEvent_t ev[8] = {};
     cudaStream_t copy_stream = nullptr;  // framebuffer read-back overlapped with the raster bands
     cudaEvent_t band_ev[kReadbackBands] = {};
@@ -376,8 +383,11 @@ void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_came
 
 // H2D of the frame records, update (LoD plan + FK) and gather (projection) for the
 // instances [shard_begin, shard_end); sets S, K, G and the depth-bit range. Events 0..3.
+// lod_back: host frames get active_lod back with the mid-frame counter read-back (the LoD
+// is final after k_lod_plan), so the frame's end needs no host synchronisation for it.
 void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
-                   const gscg_lod_policy* lod, uint32_t shard_begin, uint32_t shard_end, uint32_t& launches) {
+                   const gscg_lod_policy* lod, uint32_t shard_begin, uint32_t shard_end, uint32_t& launches,
+                   bool lod_back = false) {
     cudaStream_t s = ctx->stream;
     const FrameGeom& geo = ctx->geom;
     const gscg_render_settings* settings = &ctx->settings;
@@ -412,17 +422,24 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         CUDA_TRY(ctx->phases.ensure(std::max<size_t>(n, 1) * 4));
     }
     if (host) {
-        // One pinned staging block, one copy per array.
+        // One pinned staging block; the arrays are pulled into HBM by one k_copy_segments
+        // launch (mapped page-locked memory, no copy-engine queueing behind a read-back).
         const size_t b_tid = n * 4ull, b_place = n * 16ull, b_pose = sampled ? 0 : n * 4ull * pose_stride,
                      b_lod = n * 4ull, b_mid = need_motion ? n * 4ull : 0, b_ph = need_motion ? n * 4ull : 0;
-        ctx->ensure_pinned(b_tid + b_place + b_pose + b_lod + b_mid + b_ph + 64);
+        ctx->ensure_pinned(b_tid + b_place + b_pose + b_lod + b_mid + b_ph + 6 * 16 + 64);
         char* h = static_cast<char*>(ctx->pinned);
         size_t off = 0;
+        CopySegs segs{};
+        uint32_t nseg = 0, max_words = 0;
         auto stage = [&](const void* src, size_t bytes, void* dst) {
             if (!bytes) return;
             std::memcpy(h + off, src, bytes);
-            CUDA_TRY(cudaMemcpyAsync(dst, h + off, bytes, cudaMemcpyHostToDevice, s));
-            off += bytes;
+            segs.src[nseg] = reinterpret_cast<const uint32_t*>(h + off);
+            segs.dst[nseg] = static_cast<uint32_t*>(dst);
+            segs.words[nseg] = static_cast<uint32_t>(bytes / 4);
+            max_words = std::max(max_words, segs.words[nseg]);
+            ++nseg;
+            off += (bytes + 15) & ~size_t(15);
         };
         stage(frame->template_ids, b_tid, ctx->template_ids.ptr);
         stage(frame->placement, b_place, ctx->placement.ptr);
@@ -431,6 +448,12 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         if (need_motion) {
             stage(frame->motion_ids, b_mid, ctx->motion_ids.ptr);
             stage(frame->phase_offsets, b_ph, ctx->phases.ptr);
+        }
+        if (nseg) {
+            const uint32_t bx = std::min<uint32_t>((max_words + 255) / 256, 4u * ctx->sm_count);
+            k_copy_segments<<<dim3(bx, nseg), 256, 0, s>>>(segs);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
         }
         d_tid = ctx->template_ids.as<uint32_t>();
         d_place = ctx->placement.as<float>();
@@ -500,6 +523,13 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         k_lod_plan<<<1, 1024, 0, s>>>(pp);
         ++launches;
         CUDA_TRY(cudaGetLastError());
+        if (lod_back && n && ctx->h_lod_cap < n) {
+            if (ctx->h_lod) CUDA_TRY(cudaFreeHost(ctx->h_lod));
+            ctx->h_lod = nullptr;
+            ctx->h_lod_cap = 0;
+            CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_lod), n * 4ull));
+            ctx->h_lod_cap = n;
+        }
         if (shard_end > shard_begin) {
             FkParams fp{};
             fp.n = shard_end;
@@ -572,11 +602,27 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             CUDA_TRY(cudaGetLastError());
         }
         CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
-        CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        {  // counters (+ the final LoD for host frames) into page-locked memory by a kernel
+            CopySegs segs{};
+            segs.src[0] = reinterpret_cast<const uint32_t*>(counters);
+            segs.dst[0] = reinterpret_cast<uint32_t*>(ctx->h_counters);
+            segs.words[0] = sizeof(FrameCounters) / 4;
+            uint32_t nseg = 1;
+            if (lod_back && n) {
+                segs.src[1] = ctx->lod_out.as<uint32_t>();
+                segs.dst[1] = ctx->h_lod;
+                segs.words[1] = n;
+                nseg = 2;
+            }
+            k_copy_segments<<<dim3(std::min<uint32_t>((n + 255) / 256 + 1, 64u), nseg), 256, 0, s>>>(segs);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+        }
         CUDA_TRY(cudaStreamSynchronize(s));
         const uint64_t S = ctx->h_counters->splat_pair >> 32;
         const uint64_t K = ctx->h_counters->splat_pair & 0xffffffffull;
         if (S <= ctx->splat_capacity && K <= ctx->pair_capacity) {
+            if (lod_back && n) std::memcpy(frame->active_lod, ctx->h_lod, n * 4ull);
             ctx->S = S;
             ctx->K = K;
             ctx->G = ctx->h_counters->gaussians;
@@ -669,14 +715,23 @@ bool is_host_pointer(const void* p) {
 
 // presorted: the caller put the splat order in skeys[0] / srecs[0] (distinct keys), so the
 // depth sort is skipped (rasterize_splats: bins follow the given order).
+// pipelined: render into the other framebuffer and leave its read-back running on the
+// copy stream (gscg_render_frame_async).
 uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& launches, float* read_rgb = nullptr,
-                     float* read_T = nullptr, bool presorted = false) {
+                     float* read_T = nullptr, bool presorted = false, bool pipelined = false) {
     cudaStream_t s = ctx->stream;
     const FrameGeom& geo = ctx->geom;
     const uint32_t tiles = static_cast<uint32_t>(geo.tiles_x) * static_cast<uint32_t>(tile_rows);
     const uint32_t cells = tiles * geo.cells_per_tile;
+    if (pipelined) {
+        std::swap(ctx->fb_rgb, ctx->fb_rgb_alt);
+        std::swap(ctx->fb_T, ctx->fb_T_alt);
+        std::swap(ctx->rb_ev, ctx->rb_ev_alt);
+    }
     CUDA_TRY(ctx->fb_rgb.ensure(static_cast<size_t>(geo.W) * geo.H * 12));
     CUDA_TRY(ctx->fb_T.ensure(static_cast<size_t>(geo.W) * geo.H * 4));
+    // An earlier pipelined frame may still be reading this framebuffer back.
+    CUDA_TRY(cudaStreamWaitEvent(s, ctx->rb_ev, 0));
     CUDA_TRY(ctx->ranges.ensure(std::max<size_t>(cells, 1) * 8));
 
     const uint32_t K = static_cast<uint32_t>(ctx->K);
@@ -771,8 +826,9 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         } else {
             // Host read-back overlapped with the raster: tile-row bands are rasterised in
             // order and each band's rows are copied out on the copy stream while the next
-            // band renders.
-            const int bands = std::min(kReadbackBands, tile_rows);
+            // band renders. Pipelined frames overlap the read-back with the next frame
+            // instead, so their raster stays one launch (no per-band tail).
+            const int bands = pipelined ? 1 : std::min(kReadbackBands, tile_rows);
             const size_t row_floats = static_cast<size_t>(geo.W);
             for (int b = 0; b < bands; ++b) {
                 const int r0 = tile_rows * b / bands, r1 = tile_rows * (b + 1) / bands;
@@ -793,9 +849,14 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                     CUDA_TRY(cudaMemcpyAsync(read_T + off, ctx->fb_T.as<float>() + off, n * 4, cudaMemcpyDefault,
                                              ctx->copy_stream));
             }
-            // The frame's stream resumes only after the read-back (ordering for the caller).
-            CUDA_TRY(cudaEventRecord(ctx->band_ev[kReadbackBands - 1], ctx->copy_stream));
-            CUDA_TRY(cudaStreamWaitEvent(s, ctx->band_ev[kReadbackBands - 1], 0));
+            if (pipelined) {
+                // The read-back overlaps the next frame; gscg_wait_readback waits on rb_ev.
+                CUDA_TRY(cudaEventRecord(ctx->rb_ev, ctx->copy_stream));
+            } else {
+                // The frame's stream resumes only after the read-back (ordering for the caller).
+                CUDA_TRY(cudaEventRecord(ctx->band_ev[kReadbackBands - 1], ctx->copy_stream));
+                CUDA_TRY(cudaStreamWaitEvent(s, ctx->band_ev[kReadbackBands - 1], 0));
+            }
         }
         CUDA_TRY(cudaGetLastError());
     } else if (read_rgb || read_T) {
@@ -862,6 +923,8 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
         for (auto& e : ctx->band_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->rb_ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->rb_ev_alt, cudaEventDisableTiming));
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_band_counts), GSCG_MAX_BANDS * sizeof(unsigned long long)));
@@ -892,15 +955,19 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                       &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
                       &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch, &ctx->d_motions, &ctx->d_roots,
-                      &ctx->d_keys, &ctx->motion_ids, &ctx->phases, &ctx->long_runs};
+                      &ctx->d_keys, &ctx->motion_ids, &ctx->phases, &ctx->long_runs, &ctx->fb_rgb_alt,
+                      &ctx->fb_T_alt};
     for (DevBuf* b : bufs) b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+    if (ctx->h_lod) cudaFreeHost(ctx->h_lod);
     if (ctx->h_band_counts) cudaFreeHost(ctx->h_band_counts);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->band_ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->rb_ev) cudaEventDestroy(ctx->rb_ev);
+    if (ctx->rb_ev_alt) cudaEventDestroy(ctx->rb_ev_alt);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1046,9 +1113,10 @@ int gscg_template_bytes(const gscg_ctx* ctx, uint64_t* out) {
     return GSCG_OK;
 }
 
-int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
-                      const gscg_render_settings* settings, const gscg_lod_policy* lod,
-                      float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+namespace {
+int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                      const gscg_render_settings* settings, const gscg_lod_policy* lod, float* fb_rgb,
+                      float* fb_T, gscg_stage_times* times, bool pipelined) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
         CUDA_TRY(cudaSetDevice(ctx->device));
@@ -1057,18 +1125,54 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         const uint32_t n = frame->instance_count;
         uint32_t launches = 0;
         ctx->band_state = 0;
-        update_gather(ctx, frame, cam, lod, 0, n, launches);
+        update_gather(ctx, frame, cam, lod, 0, n, launches, host);  // host: active_lod written back here
         // Host destinations: read-back overlapped with the raster bands (sort_raster).
         // Device destinations: one device-to-device copy after the frame.
         const bool overlap = is_host_pointer(fb_rgb) || is_host_pointer(fb_T);
-        const uint32_t passes = overlap ? sort_raster(ctx, 0, ctx->geom.tiles_y, launches, fb_rgb, fb_T)
+        pipelined = pipelined && overlap;
+        const uint32_t passes = overlap ? sort_raster(ctx, 0, ctx->geom.tiles_y, launches, fb_rgb, fb_T, false,
+                                                      pipelined)
                                         : sort_raster(ctx, 0, ctx->geom.tiles_y, launches);
         if (!overlap) copy_out(ctx, ctx->geom.H, fb_rgb, fb_T, host);
-        if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull,
-                                        host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+        if (n && !host)
+            CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice,
+                                     ctx->stream));
         CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->stream));
+        if (pipelined) {
+            // No host synchronisation: the next frame's inputs go in while this one's raster
+            // and read-back finish. Counts are known (mid-frame read-back); stage times are not.
+            if (times) {
+                *times = gscg_stage_times{};
+                times->splat_count = ctx->S;
+                times->pair_count = ctx->K;
+                times->gaussian_count = ctx->G;
+                times->kernel_launches = launches;
+            }
+            return;
+        }
         if (host || times) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         if (times) fill_times(ctx, times, passes, launches);
+    });
+}
+}  // namespace
+
+int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                      const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                      float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+    return render_frame_impl(ctx, frame, cam, settings, lod, fb_rgb, fb_T, times, false);
+}
+
+int gscg_render_frame_async(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                            const gscg_render_settings* settings, const gscg_lod_policy* lod,
+                            float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+    return render_frame_impl(ctx, frame, cam, settings, lod, fb_rgb, fb_T, times, true);
+}
+
+int gscg_wait_readback(gscg_ctx* ctx, uint32_t frames_back) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (frames_back == 0) CUDA_TRY(cudaEventSynchronize(ctx->rb_ev));
+        else if (frames_back == 1) CUDA_TRY(cudaEventSynchronize(ctx->rb_ev_alt));
     });
 }
 
@@ -1553,7 +1657,10 @@ int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T) {
 
 int gscg_synchronize(gscg_ctx* ctx) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
-    return guarded(ctx, [&] { CUDA_TRY(cudaStreamSynchronize(ctx->stream)); });
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
+    });
 }
 
 int gscg_stream(gscg_ctx* ctx, void** stream) {

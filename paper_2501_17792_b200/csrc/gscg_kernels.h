@@ -115,6 +115,17 @@ __global__ void k_sample_poses(PoseParams p);
 __global__ void k_eval_sinf(const float* in, float* out, uint32_t n);
 
 __global__ void k_lod_plan(PlanParams p);
+
+// Small host <-> device transfers through mapped page-locked memory, done by a kernel so
+// they never queue behind a framebuffer read-back on the copy engines (pipelined frames):
+// segment y copies words[y] 32-bit words src[y] -> dst[y].
+constexpr int kMaxCopySegs = 8;
+struct CopySegs {
+    const uint32_t* src[kMaxCopySegs];
+    uint32_t* dst[kMaxCopySegs];
+    uint32_t words[kMaxCopySegs];
+};
+__global__ void k_copy_segments(CopySegs c);
 __global__ void k_fk_skin(FkParams p);
 __global__ void k_project(ProjectParams p);
 __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n);

@@ -285,4 +285,12 @@ k_fk_skin(FkParams p) {
     }
 }
 
+__global__ void k_copy_segments(CopySegs c) {
+    const uint32_t seg = blockIdx.y;
+    const uint32_t* __restrict__ src = c.src[seg];
+    uint32_t* __restrict__ dst = c.dst[seg];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c.words[seg]; i += gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 }  // namespace gscg

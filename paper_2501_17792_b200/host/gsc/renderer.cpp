@@ -287,9 +287,10 @@ void render_frame(Crowd& crowd, const Camera& camera, float time_s,
                       ctx.out.color.rgb.data(), ctx.out.transmittance.data());
 }
 
-void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+namespace {
+void render_frame_host(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
                        bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
-                       FrameContext& ctx, float* out_rgb, float* out_T) {
+                       FrameContext& ctx, float* out_rgb, float* out_T, bool pipelined) {
     validate(settings);
     validate(camera);
     validate(crowd.lod);
@@ -337,7 +338,9 @@ void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const R
     lp.hysteresis_band_m = crowd.lod.hysteresis_band_m;
 
     gscg_stage_times st{};
-    check_gscg(gscg_render_frame(ctx.gpu(), &fd, &cam, &rs, &lp, out_rgb, out_T, &st), ctx.gpu());
+    check_gscg(pipelined ? gscg_render_frame_async(ctx.gpu(), &fd, &cam, &rs, &lp, out_rgb, out_T, &st)
+                         : gscg_render_frame(ctx.gpu(), &fd, &cam, &rs, &lp, out_rgb, out_T, &st),
+               ctx.gpu());
     for (size_t i = 0; i < crowd.instances.size(); ++i) crowd.instances[i].active_lod = ctx.lods[i];
 
     if (times) {
@@ -350,6 +353,23 @@ void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const R
         times->pair_count = st.pair_count;
         times->gaussian_count = st.gaussian_count;
     }
+}
+}  // namespace
+
+void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+                       bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
+                       FrameContext& ctx, float* out_rgb, float* out_T) {
+    render_frame_host(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx, out_rgb, out_T, false);
+}
+
+void render_frame_async(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+                        bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
+                        FrameContext& ctx, float* out_rgb, float* out_T) {
+    render_frame_host(crowd, camera, time_s, settings, static_pose, forced_lod, times, ctx, out_rgb, out_T, true);
+}
+
+void wait_readback(FrameContext& ctx, uint32_t frames_back) {
+    check_gscg(gscg_wait_readback(ctx.gpu(), frames_back), ctx.gpu());
 }
 
 static_assert(sizeof(FrameSplat) == sizeof(gscg_frame_splat), "FrameSplat mirrors gscg_frame_splat");

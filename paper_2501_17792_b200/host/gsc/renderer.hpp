@@ -167,6 +167,13 @@ void render_frame(Crowd& crowd, const Camera& camera, float time_s,
 void render_frame_into(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
                        bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
                        FrameContext& ctx, float* out_rgb, float* out_T);
+// Streaming form of render_frame_into (gscg_render_frame_async): returns once the frame is
+// rendered; out_rgb / out_T fill in the background while the next frame renders and are
+// valid after wait_readback(ctx, frames_back) (0 = the last submitted frame).
+void render_frame_async(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
+                        bool static_pose, std::optional<uint32_t> forced_lod, StageTimes* times,
+                        FrameContext& ctx, float* out_rgb, float* out_T);
+void wait_readback(FrameContext& ctx, uint32_t frames_back);
 
 // Stage functions (reference renderer.hpp:81-103) over host splat arrays, on the GPU.
 // gather_splats runs update + projection for time_s (the reference's update_crowd then

@@ -497,8 +497,9 @@ int gsch_rasterize_splats(gsch_renderer* r, const gscg_frame_splat* splats, uint
     });
 }
 
-int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
-                const gsch_render_settings* st, float* out_rgb, float* out_T, gsch_stage_times* times) {
+static int render_host(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
+                       const gsch_render_settings* st, float* out_rgb, float* out_T, gsch_stage_times* times,
+                       bool pipelined) {
     return guarded([&] {
         if (!r || !st) throw std::invalid_argument("null argument");
         RenderSettings rs;
@@ -512,8 +513,8 @@ int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t for
         StageTimes t;
         std::optional<uint32_t> forced;
         if (forced_lod >= 0) forced = static_cast<uint32_t>(forced_lod);
-        render_frame_into(r->scene->crowd, r->scene->camera, time_s, rs, static_pose != 0, forced, &t, *r->ctx,
-                          out_rgb, out_T);
+        (pipelined ? render_frame_async : render_frame_into)(r->scene->crowd, r->scene->camera, time_s, rs,
+                                                             static_pose != 0, forced, &t, *r->ctx, out_rgb, out_T);
         if (times) {
             times->update_ms = t.update_ms;
             times->gather_ms = t.gather_ms;
@@ -525,6 +526,23 @@ int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t for
             times->pair_count = t.pair_count;
             times->gaussian_count = t.gaussian_count;
         }
+    });
+}
+
+int gsch_render(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
+                const gsch_render_settings* st, float* out_rgb, float* out_T, gsch_stage_times* times) {
+    return render_host(r, time_s, static_pose, forced_lod, st, out_rgb, out_T, times, false);
+}
+
+int gsch_render_async(gsch_renderer* r, float time_s, int32_t static_pose, int32_t forced_lod,
+                      const gsch_render_settings* st, float* out_rgb, float* out_T, gsch_stage_times* times) {
+    return render_host(r, time_s, static_pose, forced_lod, st, out_rgb, out_T, times, true);
+}
+
+int gsch_wait_readback(gsch_renderer* r, uint32_t frames_back) {
+    return guarded([&] {
+        if (!r) throw std::invalid_argument("null argument");
+        wait_readback(*r->ctx, frames_back);
     });
 }
 

@@ -144,6 +144,10 @@ GSCG_SYMBOLS = {
     "gscg_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                     C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P,
                                     C.POINTER(GscgStageTimes)]),
+    "gscg_render_frame_async": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
+                                          C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P,
+                                          C.POINTER(GscgStageTimes)]),
+    "gscg_wait_readback": (C.c_int, [_P, C.c_uint32]),
     "gscg_memory_usage": (C.c_int, [_P, C.POINTER(GscgMemoryUsage)]),
     "gscg_device_alloc": (C.c_int, [_P, C.c_uint64, C.POINTER(_P)]),
     "gscg_device_free": (C.c_int, [_P, _P]),
@@ -217,6 +221,9 @@ GSCH_SYMBOLS = {
     "gsch_renderer_joint_stride": (C.c_uint32, [_P]),
     "gsch_render": (C.c_int, [_P, C.c_float, C.c_int32, C.c_int32, C.POINTER(GschRenderSettings), _P, _P,
                               C.POINTER(GschStageTimes)]),
+    "gsch_render_async": (C.c_int, [_P, C.c_float, C.c_int32, C.c_int32, C.POINTER(GschRenderSettings), _P, _P,
+                                    C.POINTER(GschStageTimes)]),
+    "gsch_wait_readback": (C.c_int, [_P, C.c_uint32]),
     "gsch_sample_crowd": (C.c_int, [_P, C.c_float, C.c_int32, C.c_int32, _P, _P, _P]),
 }
 

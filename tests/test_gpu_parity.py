@@ -182,6 +182,33 @@ def test_pinned_output_matches_fresh_arrays():
     assert T3 is None and rgb3.tobytes() == rgb.tobytes()
 
 
+@pytest.mark.parametrize("which", ["basic", "config2"])
+def test_pipelined_frames_match_synchronous(which):
+    """render_frame(pipelined=True) (gscg_render_frame_async): frame k's read-back runs
+    while frame k+1 renders into the second device framebuffer; every frame equals the
+    synchronous render."""
+    s = basic_scene(count=16) if which == "basic" else P.Scene(P.baseline_config(2)[0])
+    st = P.RenderSettings()
+    times = [0.1, 0.45, 0.8, 1.15, 1.5]
+    sync = P.Renderer(s)
+    ref = [tuple(a.copy() for a in sync.render_frame(t, st)) for t in times]
+    r = P.Renderer(s)
+    bufs = [r.alloc_frame(pinned=True), r.alloc_frame(pinned=True)]
+    got = []
+    for k, t in enumerate(times):
+        r.render_frame(t, st, out=bufs[k % 2], pipelined=True)
+        if k:
+            r.wait_readback(1)
+            got.append(tuple(a.copy() for a in bufs[(k - 1) % 2]))
+    r.wait_readback(0)
+    got.append(tuple(a.copy() for a in bufs[(len(times) - 1) % 2]))
+    for (a, b), (c, d) in zip(got, ref):
+        assert a.tobytes() == c.tobytes() and b.tobytes() == d.tobytes()
+    # a synchronous frame after pipelined ones still returns its own image
+    again = r.render_frame(times[0], st)
+    assert again[0].tobytes() == ref[0][0].tobytes()
+
+
 def test_memory_usage_counts_the_shared_store_once():
     scene = basic_scene(count=16, templates=2, sh=True)
     r = P.Renderer(scene)
