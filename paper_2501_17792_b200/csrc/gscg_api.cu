@@ -940,6 +940,7 @@ int gscg_destroy(gscg_ctx* ctx) {
     if (!ctx) return GSCG_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);  // pipelined read-backs
     for (TemplateStore& t : ctx->templates)
         for (LevelStore& l : t.levels) {
             l.core.release();
