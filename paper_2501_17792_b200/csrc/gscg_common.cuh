@@ -68,8 +68,8 @@ struct FrameCounters {
 // float -> int as x86 cvttss2si (the reference's static_cast<int>): truncation, with
 // the "integer indefinite" INT_MIN for NaN and out-of-range values (SURVEY A8 note).
 __device__ __forceinline__ int x86_float_to_int(float v) {
-    if (!(v >= -2147483648.0f && v < 2147483648.0f)) return INT32_MIN;
-    return __float2int_rz(v);
+    // |v| < 2^31 is exactly the in-range set: -2^31 itself converts to INT_MIN either way.
+    return fabsf(v) < 2147483648.0f ? __float2int_rz(v) : INT32_MIN;
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }

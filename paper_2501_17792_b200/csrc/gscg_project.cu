@@ -48,12 +48,35 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float Y[15])
     Y[14] = (C36 * x) * (xx - 3.0f * yy);
 }
 
-__device__ __forceinline__ void copy_async16(float* smem_dst, const float* gmem_src) {
-    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem_src) : "memory");
+// Bulk (TMA) copies global -> shared completing on an mbarrier: one instruction per
+// contiguous block instead of a 16-byte cp.async per thread and iteration.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
-__device__ __forceinline__ void copy_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
 
 }  // namespace
 
@@ -67,6 +90,7 @@ k_project(ProjectParams p) {
     __shared__ uint32_t s_wcnt[kProjectThreads / 32];
     __shared__ unsigned long long s_base;
     __shared__ uint32_t s_item;
+    __shared__ __align__(8) uint64_t s_bar;  // the work item's bulk copies (SH + skin matrices)
 
     const int tid = threadIdx.x;
     for (uint32_t g = tid; g <= p.group_count; g += blockDim.x) s_item_start[g] = p.group_item_start[g];
@@ -81,6 +105,8 @@ k_project(ProjectParams p) {
     uint32_t pairs = 0;  // binning cells of this thread's splats (summed once at the end)
     const int lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
+    if (tid == 0) mbar_init(&s_bar, 1);
+    uint32_t phase = 0;
 
     for (;;) {
         __syncthreads();
@@ -112,31 +138,39 @@ k_project(ProjectParams p) {
             wv = grp.weights[gi];
         }
         const bool use_sh = p.sh_enabled && grp.sh != nullptr;
-        // Stage the chunk's SH coefficients and every batch instance's skin matrices
-        // with asynchronous copies (LDGSTS), once per work item.
-        if (use_sh) {
-            const uint32_t n_here = min(static_cast<uint32_t>(kProjectThreads),
-                                        grp.count - chunk * kProjectThreads);
-            const float* src = grp.sh + static_cast<size_t>(chunk) * kProjectThreads * kShFloats;
-            const uint32_t n4 = (n_here * kShFloats + 3) / 4;  // SH chunks are 16-B aligned
-            for (uint32_t k = tid; k < n4; k += blockDim.x) copy_async16(s_sh + 4 * k, src + 4 * k);
-        }
+        // Stage the chunk's SH coefficients and every batch instance's skin matrices with
+        // bulk copies (TMA engine), once per work item: thread 0 the SH block, thread k
+        // instance k's matrices, all completing on s_bar.
         const uint32_t inst_begin = p.group_inst_start[g] + batch * kBatch;
         const uint32_t inst_count = min(static_cast<uint32_t>(kBatch),
                                         p.group_inst_count[g] - batch * kBatch);
-        const uint32_t mat_f4 = p.joint_stride * 3;  // float4s per instance
-        for (uint32_t e = tid; e < inst_count * mat_f4; e += blockDim.x) {
-            const uint32_t k = e / mat_f4, r = e - k * mat_f4;
-            const float* src = p.skin + static_cast<size_t>(p.members[inst_begin + k]) * p.joint_stride * 12;
-            copy_async16(s_mats + 4 * e, src + 4 * r);
+        const uint32_t mat_bytes = p.joint_stride * 48u;  // 3 x 4 floats per joint
+        if (tid == 0) {
+            // Earlier generic-proxy reads of this shared memory precede the async writes.
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            uint32_t bytes = inst_count * mat_bytes;
+            if (use_sh) {
+                const uint32_t n_here = min(static_cast<uint32_t>(kProjectThreads),
+                                            grp.count - chunk * kProjectThreads);
+                const uint32_t sh_bytes = (n_here * kShFloats * 4u + 15u) & ~15u;  // chunks are padded
+                bytes += sh_bytes;
+                mbar_arrive_expect_tx(&s_bar, bytes);
+                bulk_g2s(s_sh, grp.sh + static_cast<size_t>(chunk) * kProjectThreads * kShFloats, sh_bytes, &s_bar);
+            } else {
+                mbar_arrive_expect_tx(&s_bar, bytes);
+            }
         }
         if (tid < static_cast<int>(inst_count)) {
             const uint32_t m = p.members[inst_begin + tid];
             s_member[tid] = m;
             s_member_base[tid] = p.inst_base[m];
+            if (tid != 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_g2s(s_mats + tid * p.joint_stride * 12, p.skin + static_cast<size_t>(m) * p.joint_stride * 12,
+                     mat_bytes, &s_bar);
         }
-        copy_async_wait_all();
         __syncthreads();
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
         const uint32_t i01 = __float_as_uint(c3.z), i23 = __float_as_uint(c3.w);
         const uint32_t jidx[4] = {i01 & 0xffffu, i01 >> 16, i23 & 0xffffu, i23 >> 16};
         const float wk[4] = {wv.x, wv.y, wv.z, wv.w};
