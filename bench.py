@@ -312,6 +312,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     ms_step = ms_total / args.steps
     launches = sum(s["launches"] for s in stage)
     counts = stage[-1]["counts"]
+    culled = r.instances_culled()
     lods = d_lods[:n].cpu().numpy().astype(np.uint32)
 
     # ---- end-to-end through the public API (host poses + pinned H2D + kernels + D2H) ----
@@ -395,6 +396,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                                f"{cfg.crowd_count} animated characters, distance LoD 5/10 m, {cfg.width}x{cfg.height}, tile 16",
                    "instances": cfg.crowd_count, "resolution": [cfg.width, cfg.height],
                    "gaussians": counts[0], "splats": counts[1], "pairs": counts[2],
+                   "instances_culled": culled,
                    "l2": "no flush: the per-frame working set (templates ~0.5 GB + records/pairs ~0.8 GB) exceeds the 126 MB L2",
                    "parallelism": (f"{world} instance shards -> {world} screen bands, NCCL all-to-all"
                                    if band_path else "single GPU")},

@@ -170,6 +170,7 @@ typedef struct {
 
 #define GSCG_DEBUG_POSED 1u   /* keep posed means (G x 3) */
 #define GSCG_DEBUG_RECORDS 2u /* keep gscg_splat_record per survivor */
+#define GSCG_DEBUG_NO_CULL 4u /* project every instance (no instance frustum cull; A/B runs) */
 
 int gscg_create(int device, gscg_ctx** out);
 int gscg_destroy(gscg_ctx* ctx);
@@ -242,6 +243,9 @@ int gscg_stream(gscg_ctx* ctx, void** stream);
 
 /* Parity / debug exports of the last frame. */
 int gscg_get_counts(gscg_ctx* ctx, uint64_t* gaussians, uint64_t* splats, uint64_t* pairs);
+/* Instances of the last frame the conservative instance frustum cull left out of the
+ * projection (none of their splats can survive gather_splats' cull, renderer.cpp:38-50). */
+int gscg_get_instances_culled(gscg_ctx* ctx, uint32_t* out);
 int gscg_get_lod(gscg_ctx* ctx, uint32_t* out, uint32_t n);
 int gscg_get_instance_base(gscg_ctx* ctx, uint32_t* out, uint32_t n);
 int gscg_get_posed_means(gscg_ctx* ctx, float* out, uint64_t gaussians);

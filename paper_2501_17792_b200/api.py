@@ -470,6 +470,12 @@ class Renderer:
         N.check_gscg(N.gscg().gscg_get_counts(self.gpu, C.byref(g), C.byref(s), C.byref(k)), self.gpu)
         return g.value, s.value, k.value
 
+    def instances_culled(self) -> int:
+        """Instances of the last frame left out by the instance frustum cull."""
+        v = C.c_uint32()
+        N.check_gscg(N.gscg().gscg_get_instances_culled(self.gpu, C.byref(v)), self.gpu)
+        return v.value
+
     def lods(self) -> np.ndarray:
         n = self.scene.counts()[2]
         out = np.zeros(n, dtype=np.uint32)

@@ -3,12 +3,14 @@
 //
 // Frame schedule on the context stream (render_frame, renderer.cpp:249-280):
 //   H2D of the frame records (pinned staging, one copy)
-//   update:    k_lod_plan (1 CTA) -> k_fk_skin
+//   update:    k_fk_skin -> k_inst_cull -> k_lod_plan (1 CTA)
 //   gather:    k_project (persistent, template-major)       -> counters readback (sync)
-//   sort:      splats by depth (k_sort_{upsweep,rows,bases,downsweep} x P) ->
-//              ties by ordinal + spans + first cell digit histogram (k_sorted_spans) ->
-//              pairs scattered in first-cell-pass order (k_sort_rows, k_emit_scatter) ->
-//              pairs stably by cell (radix x P') -> k_cell_ranges
+//   sort:      splats by the top <= 20 varying depth bits (k_sort_{upsweep,rows,downsweep} x P) ->
+//              spans in sorted order (k_sorted_spans) ->
+//              pairs scattered in first-cell-pass order, keys tagged with the truncated depth
+//              (k_emit_scatter count, k_sort_rows, k_emit_scatter scatter) ->
+//              pairs stably by cell (radix x P') -> cell ranges + per-cell (depth, ordinal)
+//              order of tied runs (k_cell_fixup, k_pair_long_runs)
 //   rasterize: k_raster16q (or k_raster_generic for other tile sizes)
 //   D2H of framebuffer / transmittance / active LoDs (host mode)
 // The one mid-frame synchronisation reads S, K and the depth-bit range: it sizes the
@@ -77,6 +79,9 @@ struct LevelStore {
     bool has_sh = false;
     std::vector<float> opacities;  // host copy for the power-floor table
     float pf_cutoff = -1.0f;
+    // Instance-cull bounds (k_inst_cull): max |mean|, max sqrt of the Gershgorin bound of
+    // the covariance, max sum |w|, max |sum w - 1|; +inf when any input is non-finite.
+    float mean_r = 0.0f, sigma = 0.0f, wabs = 0.0f, wdev = 0.0f;
 };
 
 // A clip as device slerp tables (gscg_pose.cu): roots per frame, key pairs per
@@ -136,14 +141,15 @@ struct gscg_ctx {
     // frame inputs
     DevBuf template_ids, placement, poses, lod_prev, lod_out;
     // plan outputs
-    DevBuf inst_group, inst_base, members, group_inst_start, group_inst_count, group_item_start;
+    DevBuf inst_group, inst_base, members, group_inst_start, group_inst_count, group_item_start, visible;
     DevBuf skin, counters;
     // gather outputs
     DevBuf records, splat_meta, splat_depth;
     uint64_t splat_capacity = 0, pair_capacity = 0;
+    uint32_t culled = 0;  // instances dropped by k_inst_cull in the last frame
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
-    DevBuf long_runs;  // long equal-depth runs found by k_sorted_spans (+ their count)
+    DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
     DevBuf fb_rgb, fb_T;
@@ -230,6 +236,13 @@ void upload_tables(gscg_ctx* ctx) {
         d.mat_offset = static_cast<int32_t>(mats.size() / 16);
         d.parent_offset = static_cast<int32_t>(parents.size());
         d.pelvis_y = ts.pelvis_y;
+        d.cull_mean_r = d.cull_sigma = d.cull_wabs = d.cull_wdev = 0.0f;
+        for (const LevelStore& ls : ts.levels) {
+            d.cull_mean_r = std::max(d.cull_mean_r, ls.mean_r);
+            d.cull_sigma = std::max(d.cull_sigma, ls.sigma);
+            d.cull_wabs = std::max(d.cull_wabs, ls.wabs);
+            d.cull_wdev = std::max(d.cull_wdev, ls.wdev);
+        }
         mats.insert(mats.end(), ts.local_bind.begin(), ts.local_bind.end());
         mats.insert(mats.end(), ts.inverse_bind.begin(), ts.inverse_bind.end());
         for (int16_t p : ts.parents) parents.push_back(p);
@@ -314,6 +327,9 @@ void refresh_power_floor(gscg_ctx* ctx, float cutoff) {
     }
     tmp.release();
 }
+
+// Depth bits the splat sort orders (4 passes of <= 5 bits); lower bits are settled per cell.
+constexpr uint32_t kDepthSortBits = 20;
 
 // Digit layout of one LSD sort: pass q sorts bits [shift[q], shift[q] + bits[q]).
 struct RadixPlan {
@@ -404,6 +420,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
     CUDA_TRY(ctx->inst_group.ensure(std::max<size_t>(n, 1) * 4));
     CUDA_TRY(ctx->inst_base.ensure(std::max<size_t>(n, 1) * 4));
     CUDA_TRY(ctx->members.ensure(std::max<size_t>(n, 1) * 4));
+    CUDA_TRY(ctx->visible.ensure(std::max<size_t>(n, 1) * 4));
     CUDA_TRY(ctx->group_inst_start.ensure((kMaxGroups + 1) * 4));
     CUDA_TRY(ctx->group_inst_count.ensure((kMaxGroups + 1) * 4));
     CUDA_TRY(ctx->group_item_start.ensure((kMaxGroups + 1) * 4));
@@ -494,9 +511,62 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project, kProjectThreads, project_smem));
     project_blocks_per_sm = std::max(project_blocks_per_sm, 1);
 
+    CameraDev camdev{};
+    std::memcpy(camdev.w, cam->world_to_view, sizeof(camdev.w));
+    std::memcpy(camdev.pos, cam->position, sizeof(camdev.pos));
+    camdev.focal = cam->focal;
+    camdev.cx = cam->cx;
+    camdev.cy = cam->cy;
+    camdev.near_m = cam->near_m;
+    camdev.width = geo.W;
+    camdev.height = geo.H;
     auto* counters = ctx->counters.as<FrameCounters>();
     for (int attempt = 0;; ++attempt) {
-        // ---- update ----
+        if (lod_back && n && ctx->h_lod_cap < n) {
+            if (ctx->h_lod) CUDA_TRY(cudaFreeHost(ctx->h_lod));
+            ctx->h_lod = nullptr;
+            ctx->h_lod_cap = 0;
+            CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_lod), n * 4ull));
+            ctx->h_lod_cap = n;
+        }
+        // ---- update ---- (FK first: the cull reads the skin matrices, the plan the cull)
+        if (shard_end > shard_begin) {
+            FkParams fp{};
+            fp.n = shard_end;
+            fp.first = shard_begin;
+            fp.joint_stride = js;
+            fp.pose_stride = pose_stride;
+            fp.template_ids = d_tid;
+            fp.placement = d_place;
+            fp.poses = d_poses;
+            fp.templates = ctx->d_templates.as<TemplateDev>();
+            fp.mats = ctx->d_mats.as<float>();
+            fp.parents = ctx->d_parents.as<int32_t>();
+            fp.skin = ctx->skin.as<float>();
+            const int per_block = 16;
+            const uint32_t m = shard_end - shard_begin;
+            k_fk_skin<<<(m + per_block - 1) / per_block, 256, per_block * js * 16 * 4, s>>>(fp);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+        }
+        // Instance frustum cull (off with GSCG_DEBUG_POSED, which keeps every posed mean,
+        // and GSCG_DEBUG_NO_CULL).
+        const bool cull = shard_end > shard_begin && !(ctx->debug & (GSCG_DEBUG_POSED | GSCG_DEBUG_NO_CULL));
+        if (cull) {
+            CullParams cp{};
+            cp.n = shard_end;
+            cp.first = shard_begin;
+            cp.joint_stride = js;
+            cp.template_ids = d_tid;
+            cp.templates = ctx->d_templates.as<TemplateDev>();
+            cp.skin = ctx->skin.as<float>();
+            cp.cam = camdev;
+            cp.visible = ctx->visible.as<uint32_t>();
+            const uint32_t m = shard_end - shard_begin;
+            k_inst_cull<<<(m + 7) / 8, 256, 0, s>>>(cp);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+        }
         PlanParams pp{};
         pp.n = n;
         pp.shard_begin = shard_begin;
@@ -519,36 +589,11 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pp.group_inst_count = ctx->group_inst_count.as<uint32_t>();
         pp.group_item_start = ctx->group_item_start.as<uint32_t>();
         pp.members = ctx->members.as<uint32_t>();
+        pp.visible = cull ? ctx->visible.as<uint32_t>() : nullptr;
         pp.counters = counters;
         k_lod_plan<<<1, 1024, 0, s>>>(pp);
         ++launches;
         CUDA_TRY(cudaGetLastError());
-        if (lod_back && n && ctx->h_lod_cap < n) {
-            if (ctx->h_lod) CUDA_TRY(cudaFreeHost(ctx->h_lod));
-            ctx->h_lod = nullptr;
-            ctx->h_lod_cap = 0;
-            CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_lod), n * 4ull));
-            ctx->h_lod_cap = n;
-        }
-        if (shard_end > shard_begin) {
-            FkParams fp{};
-            fp.n = shard_end;
-            fp.first = shard_begin;
-            fp.joint_stride = js;
-            fp.pose_stride = pose_stride;
-            fp.template_ids = d_tid;
-            fp.placement = d_place;
-            fp.poses = d_poses;
-            fp.templates = ctx->d_templates.as<TemplateDev>();
-            fp.mats = ctx->d_mats.as<float>();
-            fp.parents = ctx->d_parents.as<int32_t>();
-            fp.skin = ctx->skin.as<float>();
-            const int per_block = 16;
-            const uint32_t m = shard_end - shard_begin;
-            k_fk_skin<<<(m + per_block - 1) / per_block, 256, per_block * js * 16 * 4, s>>>(fp);
-            ++launches;
-            CUDA_TRY(cudaGetLastError());
-        }
         CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
 
         if (ctx->debug & GSCG_DEBUG_POSED) {
@@ -568,14 +613,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
 
         // ---- gather ----
         ProjectParams pj{};
-        std::memcpy(pj.cam.w, cam->world_to_view, sizeof(pj.cam.w));
-        std::memcpy(pj.cam.pos, cam->position, sizeof(pj.cam.pos));
-        pj.cam.focal = cam->focal;
-        pj.cam.cx = cam->cx;
-        pj.cam.cy = cam->cy;
-        pj.cam.near_m = cam->near_m;
-        pj.cam.width = geo.W;
-        pj.cam.height = geo.H;
+        pj.cam = camdev;
         pj.tile_size = geo.ts;
         pj.tiles_x = geo.tiles_x;
         pj.sh_enabled = settings->sh_enabled ? 1 : 0;
@@ -628,6 +666,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             ctx->G = ctx->h_counters->gaussians;
             ctx->dmin = ctx->h_counters->depth_min_bits;
             ctx->dmax = ctx->h_counters->depth_max_bits;
+            ctx->culled = ctx->h_counters->instances_culled;
             break;
         }
         if (attempt > 2) throw Status(GSCG_ERR_STATE, "splat/pair capacity did not converge");
@@ -741,15 +780,24 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
     ctx->final_recs = nullptr;
     if (S32 > 0 && K > 0) {
         ensure_sort_buffers(ctx, S32, K);
-        // 1. splats by depth (bits that vary in the frame), ties by ordinal.
-        const RadixPlan dplan = presorted ? RadixPlan{} : make_plan(static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax)));
+        // 1. splats by the top (at most kDepthSortBits) varying bits of their depth keys;
+        //    the dropped low bits and the ordinal tie-break are settled per cell in step 4.
+        const uint32_t dbits = static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax));
+        const uint32_t drop = dbits > kDepthSortBits ? dbits - kDepthSortBits : 0u;
+        RadixPlan dplan{};
+        if (!presorted) {
+            dplan = make_plan(dbits - drop);
+            for (uint32_t q = 0; q < dplan.passes; ++q) dplan.shift[q] += drop;
+        }
         const int sb = presorted ? 0
                                  : run_radix(ctx, ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32,
                                              dplan, launches);
-        // 2. equal-depth runs by ordinal + cell spans in sorted order + the first cell-sort
-        //    digit histogram per 1024 sorted splats; digit offsets; pairs emitted straight
-        //    into the order of the first stable cell-sort pass.
+        // 2. cell spans in sorted order; the first cell-sort digit histogram per emission
+        //    block; digit offsets; pairs emitted straight into the order of the first stable
+        //    cell-sort pass, each key word tagged with its splat's truncated depth.
         const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
+        const uint32_t cell_bits = std::max(1, bits_for(cells - 1));
+        const uint32_t cell_mask = cell_bits >= 32 ? 0xffffffffu : (1u << cell_bits) - 1u;
         const uint32_t dmask = (1u << cplan.bits[0]) - 1u;
         const uint32_t sblocks = (S32 + 1023) / 1024;                 // k_sorted_spans CTAs
         const uint32_t eblocks = (S32 + kEmitSplats - 1) / kEmitSplats;  // emission blocks
@@ -757,34 +805,24 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
         static_assert(kMetaThreads * kStreamItems == 1024, "one splat block per CTA");
         const int quads = geo.cells_per_tile == 4 ? 1 : 0;
-        const uint32_t long_cap = S32 / kLongRun + 1;  // runs longer than kLongRun: at most S / kLongRun
-        CUDA_TRY(ctx->long_runs.ensure(static_cast<size_t>(long_cap) * 8 + 16));
-        uint32_t* long_count = reinterpret_cast<uint32_t*>(ctx->long_runs.as<uint2>() + long_cap);
-        CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
-        k_sorted_spans<<<sblocks, kMetaThreads, 0, s>>>(ctx->skeys[sb].as<uint32_t>(), ctx->srecs[sb].as<uint32_t>(),
-                                                        ctx->splat_meta.as<uint4>(), S32, ctx->span_sorted.as<uint2>(),
-                                                        ctx->long_runs.as<uint2>(), long_count, long_cap);
-        k_long_runs_warp<<<ctx->sm_count * 4, 256, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
-                                                           ctx->span_sorted.as<uint2>(), ctx->long_runs.as<uint2>(),
-                                                           long_count, long_cap);
-        k_long_runs<<<ctx->sm_count * 2, 256, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
-                                                      ctx->span_sorted.as<uint2>(), ctx->long_runs.as<uint2>(),
-                                                      long_count, long_cap);
-        launches += 2;
-        launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
-                    ctx->block_sums.as<uint32_t>(), nullptr, geo.tiles_x, quads, dmask, nullptr, nullptr);
+        k_sorted_spans<<<sblocks, kMetaThreads, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(), S32,
+                                                        ctx->span_sorted.as<uint2>());
+        ++launches;
+        const uint32_t* tag_keys = presorted ? nullptr : ctx->skeys[sb].as<uint32_t>();
+        launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
+                    ctx->block_sums.as<uint32_t>(), nullptr, geo.tiles_x, quads, dmask, drop, cell_bits, nullptr, nullptr);
         SortPassParams bp{};
         bp.counts = ctx->block_sums.as<uint32_t>();
         bp.digit_base = ctx->hist.as<uint32_t>();
         bp.tiles = eblocks;
         bp.bits = cplan.bits[0];
         k_sort_rows<<<dmask + 1, 1024, 0, s>>>(bp);
-        launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), S32, ctx->span_sorted.as<uint2>(),
-                    ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), geo.tiles_x, quads, dmask,
+        launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
+                    ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), geo.tiles_x, quads, dmask, drop, cell_bits,
                     ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
-        launches += 4;
+        launches += 3;
         CUDA_TRY(cudaGetLastError());
-        // 3. the remaining stable cell-sort passes; ranges.
+        // 3. the remaining stable cell-sort passes (cell bits only; the tags ride along).
         RadixPlan rest{};
         for (uint32_t q = 1; q < cplan.passes; ++q) {
             rest.shift[rest.passes] = cplan.shift[q];
@@ -794,9 +832,21 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         const int cb = rest.passes ? run_radix(ctx, ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(),
                                                ctx->pcell, ctx->precs, K, rest, launches)
                                    : 1;
+        // 4. cell ranges + every run of equal (cell, tag) ordered by (depth bits, ordinal).
+        const uint32_t long_cap = K / kLongRun + 1;  // runs longer than kLongRun: at most K / kLongRun
+        CUDA_TRY(ctx->long_runs.ensure(static_cast<size_t>(long_cap) * 8 + 16));
+        uint32_t* long_count = reinterpret_cast<uint32_t*>(ctx->long_runs.as<uint2>() + long_cap);
+        CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
         const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);
-        k_cell_ranges<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K, ctx->ranges.as<uint2>());
+        k_cell_fixup<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), ctx->precs[cb].as<uint32_t>(),
+                                             ctx->splat_meta.as<uint4>(), K, cell_mask, presorted ? 0 : 1,
+                                             ctx->ranges.as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap);
         ++launches;
+        if (!presorted) {
+            k_pair_long_runs<<<ctx->sm_count * 2, 256, 0, s>>>(ctx->precs[cb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
+                                                              ctx->long_runs.as<uint2>(), long_count, long_cap);
+            ++launches;
+        }
         CUDA_TRY(cudaGetLastError());
         ctx->final_recs = ctx->precs[cb].as<uint32_t>();
         passes = dplan.passes + cplan.passes;
@@ -949,7 +999,7 @@ int gscg_destroy(gscg_ctx* ctx) {
         }
     DevBuf* bufs[] = {&ctx->d_templates, &ctx->d_groups, &ctx->d_mats, &ctx->d_parents,
                       &ctx->template_ids, &ctx->placement, &ctx->poses, &ctx->lod_prev,
-                      &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members,
+                      &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members, &ctx->visible,
                       &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
                       &ctx->skin, &ctx->counters, &ctx->records, &ctx->splat_meta,
                       &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
@@ -1056,6 +1106,35 @@ int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level, const
         }
         ls.opacities.assign(d->opacities, d->opacities + n);
         ls.pf_cutoff = -1.0f;
+        {  // instance-cull bounds, rounded up; non-finite input disables the cull
+            double mr = 0.0, s2 = 0.0, wa = 0.0, wd = 0.0;
+            bool finite = true;
+            for (uint32_t i = 0; i < n; ++i) {
+                const float* m = d->means + 3ull * i;
+                const float* cv = d->cov6 + 6ull * i;
+                const float* w = d->skin_weights + 4ull * i;
+                const double r2 = double(m[0]) * m[0] + double(m[1]) * m[1] + double(m[2]) * m[2];
+                const double g0 = std::fabs(double(cv[0])) + std::fabs(double(cv[1])) + std::fabs(double(cv[2]));
+                const double g1 = std::fabs(double(cv[1])) + std::fabs(double(cv[3])) + std::fabs(double(cv[4]));
+                const double g2 = std::fabs(double(cv[2])) + std::fabs(double(cv[4])) + std::fabs(double(cv[5]));
+                double sa = 0.0, sw = 0.0;
+                for (int k = 0; k < 4; ++k) {
+                    sa += std::fabs(double(w[k]));
+                    sw += double(w[k]);
+                }
+                finite = finite && std::isfinite(r2) && std::isfinite(g0) && std::isfinite(g1) && std::isfinite(g2) &&
+                         std::isfinite(sa);
+                mr = std::max(mr, r2);
+                s2 = std::max(s2, std::max(g0, std::max(g1, g2)));
+                wa = std::max(wa, sa);
+                wd = std::max(wd, std::fabs(sw - 1.0));
+            }
+            auto up = [](double v) { return static_cast<float>(v * (1.0 + 1e-6) + 1e-12); };
+            ls.mean_r = finite ? up(std::sqrt(mr)) : INFINITY;
+            ls.sigma = finite ? up(std::sqrt(s2)) : INFINITY;
+            ls.wabs = finite ? up(wa) : INFINITY;
+            ls.wdev = finite ? up(wd) : INFINITY;
+        }
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         ctx->tables_dirty = true;
     });
@@ -1342,7 +1421,7 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
             for (const LevelStore& l : t.levels) out->template_bytes += l.core.cap + l.weights.cap + l.sh.cap;
         const DevBuf* bufs[] = {&ctx->d_templates, &ctx->d_groups, &ctx->d_mats, &ctx->d_parents,
                                 &ctx->template_ids, &ctx->placement, &ctx->poses, &ctx->lod_prev,
-                                &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members,
+                                &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members, &ctx->visible,
                                 &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
                                 &ctx->skin, &ctx->counters, &ctx->records, &ctx->splat_meta,
                                 &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
@@ -1675,6 +1754,12 @@ int gscg_get_counts(gscg_ctx* ctx, uint64_t* gaussians, uint64_t* splats, uint64
     if (gaussians) *gaussians = ctx->G;
     if (splats) *splats = ctx->S;
     if (pairs) *pairs = ctx->K;
+    return GSCG_OK;
+}
+
+int gscg_get_instances_culled(gscg_ctx* ctx, uint32_t* out) {
+    if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    *out = ctx->culled;
     return GSCG_OK;
 }
 

@@ -139,7 +139,7 @@ k_band_unpack(BandUnpackParams p) {
         const uint32_t across = static_cast<uint32_t>((x1 - 1) / p.cell - cx0 + 1);
         const uint32_t down = static_cast<uint32_t>((yc1 - 1) / p.cell - cy0 + 1);
         p.meta[i] = make_uint4(meta.x, static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0 - p.row_begin / p.cell) << 16),
-                               across | (down << 16), 0u);
+                               across | (down << 16), meta.y);
         pairs += across * down;
         dmin = min(dmin, meta.y);
         dmax = max(dmax, meta.y);

@@ -44,6 +44,10 @@ struct TemplateDev {
     int32_t mat_offset;  // first matrix in the skeleton matrix table (local_bind then inverse_bind)
     int32_t parent_offset;
     float pelvis_y;
+    // Conservative bounds over all levels for the instance frustum cull (k_inst_cull):
+    // max |mean|, max sqrt(Gershgorin bound of the covariance), max sum |w_k|,
+    // max |sum w_k - 1|. +inf disables the cull for the template.
+    float cull_mean_r, cull_sigma, cull_wabs, cull_wdev;
     int32_t pad[2];
 };
 
@@ -63,6 +67,7 @@ struct FrameCounters {
     uint32_t items_total;
     uint32_t item_cursor;
     uint32_t sort_ticket[8];  // onesweep tile tickets, one per pass of the frame
+    uint32_t instances_culled;  // instances whose every splat is provably off-screen (k_inst_cull)
 };
 
 // float -> int as x86 cvttss2si (the reference's static_cast<int>): truncation, with

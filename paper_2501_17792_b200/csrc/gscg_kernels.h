@@ -26,7 +26,21 @@ struct PlanParams {
     uint32_t* group_inst_count;
     uint32_t* group_item_start;  // group_count + 1
     uint32_t* members;
+    const uint32_t* visible;  // k_inst_cull flags (null: every instance is projected)
     FrameCounters* counters;
+};
+
+// Instance frustum cull: one warp per instance bounds its posed means by a ball from its
+// skin matrices and the template bounds, and proves every splat off-screen (see k_inst_cull).
+struct CullParams {
+    uint32_t n;      // end of the instance range
+    uint32_t first;  // first instance (shard begin)
+    uint32_t joint_stride;
+    const uint32_t* template_ids;
+    const TemplateDev* templates;
+    const float* skin;
+    CameraDev cam;
+    uint32_t* visible;  // 1 = project, 0 = culled
 };
 
 struct FkParams {
@@ -61,7 +75,7 @@ struct ProjectParams {
     // outputs (capacity-checked)
     float4* records;  // 3 float4 per splat
     uint32_t* splat_depth;  // depth bits of every record (the splat sort keys)
-    uint4* splat_meta;      // per record: ordinal, cx0 | cy0 << 16, across | down << 16, 0
+    uint4* splat_meta;      // per record: ordinal, cx0 | cy0 << 16, across | down << 16, depth bits
     uint64_t splat_capacity;
     uint64_t pair_capacity;
     // debug outputs (may be null)
@@ -127,6 +141,7 @@ struct CopySegs {
 };
 __global__ void k_copy_segments(CopySegs c);
 __global__ void k_fk_skin(FkParams p);
+__global__ void k_inst_cull(CullParams p);
 __global__ void k_project(ProjectParams p);
 __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n);
 
@@ -158,28 +173,30 @@ __global__ void k_sort_rows(SortPassParams p);
 __global__ void k_sort_downsweep(SortPassParams p);
 
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
-constexpr uint32_t kLongRun = 32;       // equal-depth runs longer than this go to k_long_runs
-constexpr uint32_t kLongRunCap = 4096;  // k_long_runs sorts runs up to this size in shared memory
-constexpr uint32_t kWarpRunCap = 256;   // runs up to this size: one warp each (k_long_runs_warp)
-__global__ void k_long_runs_warp(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
-                                 const uint32_t* long_count, uint32_t long_cap);
-__global__ void k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
-                               uint2* span_sorted, uint2* long_runs, uint32_t* long_count, uint32_t long_cap);
-__global__ void k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
-                            const uint32_t* long_count, uint32_t long_cap);
+constexpr uint32_t kLongRun = 32;       // runs of equal pair keys longer than this go to k_pair_long_runs
+constexpr uint32_t kPairRunCap = 2048;  // k_pair_long_runs sorts runs up to this size in shared memory
+__global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted);
+__global__ void k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
+                             uint32_t cell_mask, int fix, uint2* ranges, uint2* long_runs, uint32_t* long_count,
+                             uint32_t long_cap);
+__global__ void k_pair_long_runs(uint32_t* recs, const uint4* meta, const uint2* long_runs, const uint32_t* long_count,
+                                 uint32_t long_cap);
 constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
 constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
 constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes
 constexpr int kEmitSmem = (32 * kEmitThreads + 2 * kEmitStage) * 4;  // dynamic shared bytes
 template <bool kCount>
-__global__ void k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted,
-                               uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x,
-                               int quads, uint32_t dmask, uint32_t* pair_cell, uint32_t* pair_rec);
+__global__ void k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count,
+                               const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
+                               uint32_t blocks, int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop,
+                               uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec);
 // Launches count (true) or scatter (false); defined in the sort TU (template instantiation).
-void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, uint32_t count,
-                 const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total, int tiles_x, int quads,
-                 uint32_t dmask, uint32_t* pair_cell, uint32_t* pair_rec);
-__global__ void k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges);
+// key_sorted (may be null: no tags) are the depth-sorted keys; a pair's key word is
+// cell | ((key >> tag_drop) << tag_shift) (see k_cell_fixup).
+void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, const uint32_t* key_sorted,
+                 uint32_t count, const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
+                 int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
+                 uint32_t* pair_rec);
 constexpr int kStreamItems = 8;  // elements per thread in the streaming sort kernels
 
 // screen-band exchange (multi-GPU frame)

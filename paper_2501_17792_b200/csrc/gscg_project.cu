@@ -354,7 +354,7 @@ k_project(ProjectParams p) {
             }
             if (stored) {
                 p.splat_depth[ridx] = dbits;  // splat sort key (pairs are emitted after it)
-                p.splat_meta[ridx] = make_uint4(ordinal, span_lo, span_hi, 0u);
+                p.splat_meta[ridx] = make_uint4(ordinal, span_lo, span_hi, dbits);
             }
         }
     }

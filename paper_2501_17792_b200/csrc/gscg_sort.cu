@@ -221,17 +221,6 @@ k_sort_downsweep(SortPassParams p) {
     }
 }
 
-// After the depth sort: equal-depth runs ordered by splat ordinal (renderer.cpp:91-96:
-// the reference breaks depth ties by (instance, gaussian), and ordinal = instance base +
-// gaussian index), each sorted splat's binning span gathered into sorted order, and the
-// pair count of every 1024-splat block (level 1 of the emission scan). One 16-byte meta
-// gather per splat serves both the tie-break and the span.
-//
-// Thread t owns the runs that START in its 8-position window. Runs inside the window are
-// ordered in registers (odd-even transposition on (key, ordinal); equal keys are
-// contiguous, so only runs move). A run leaving the window is finished by its owner in
-// global memory; the next windows skip it. Ties are frequent: same-pose characters on
-// one grid row share depth bit patterns.
 namespace {
 
 __device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x, int quads) {
@@ -255,159 +244,207 @@ __device__ __forceinline__ void for_each_cell(uint2 sp, int tiles_x, int quads, 
     }
 }
 
-struct SpanSink {
-    uint2* span_sorted;
-    uint2* long_runs;  // (start, length) of runs longer than kLongRun, ordered by k_long_runs
-    uint32_t* long_count;
-    uint32_t long_cap;
-    __device__ void put(uint32_t pos, uint4 m) { span_sorted[pos] = make_uint2(m.y, m.z); }
-};
+}  // namespace
 
-// Orders the run of equal keys starting at s by ordinal (insertion sort in global memory)
-// and emits its spans; returns the run's end.
-__device__ __forceinline__ uint32_t finish_run(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t s,
-                               SpanSink& sink) {
+// After the depth sort: every sorted splat's binning span, gathered into sorted order
+// (one 16-byte meta gather per splat, all eight of a thread in flight).
+__global__ void __launch_bounds__(kMetaThreads)
+k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted) {
+    static_assert(kStreamItems == 8, "two uint4 loads per thread");
+    const uint32_t b = (blockIdx.x * kMetaThreads + threadIdx.x) * kStreamItems;
+    if (b + kStreamItems <= count) {
+        const uint4 rlo = *reinterpret_cast<const uint4*>(recs + b);
+        const uint4 rhi = *reinterpret_cast<const uint4*>(recs + b + 4);
+        const uint32_t r[kStreamItems] = {rlo.x, rlo.y, rlo.z, rlo.w, rhi.x, rhi.y, rhi.z, rhi.w};
+        uint4 m[kStreamItems];
+#pragma unroll
+        for (int j = 0; j < kStreamItems; ++j) m[j] = meta[r[j]];
+        uint4* dst = reinterpret_cast<uint4*>(span_sorted + b);
+#pragma unroll
+        for (int j = 0; j < kStreamItems; j += 2) dst[j / 2] = make_uint4(m[j].y, m[j].z, m[j + 1].y, m[j + 1].z);
+    } else {
+        for (uint32_t i = b; i < count; ++i) {
+            const uint4 m = meta[recs[i]];
+            span_sorted[i] = make_uint2(m.y, m.z);
+        }
+    }
+}
+
+// Per-cell order fix-up and cell ranges, over the cell-sorted pairs.
+//
+// The depth sort orders splats by the top bits of their depth keys only (at most 20
+// varying bits: 4 LSD passes); splats whose truncated keys tie keep an arbitrary order.
+// Emission tags every pair's key word with the low bits of its splat's truncated key above
+// the cell id, and the stable cell passes keep the truncated-depth order inside every
+// cell. Inside a cell, a run of equal key words (same cell, same tag) holds pairs of equal
+// truncated depth, or, when tags alias, of increasing truncated depth; sorting every such
+// run by the full (depth bits, ordinal) key (renderer.cpp:85-107) therefore yields exactly
+// the reference's bin order. Runs are short (a few pairs; ties inside one 8x8 cell), so a
+// thread orders the runs inside its 8-pair window in registers (odd-even transposition),
+// finishes a run leaving its window in global memory, and hands runs longer than kLongRun
+// to k_pair_long_runs. Pairs outside runs are never gathered.
+namespace {
+
+__device__ __forceinline__ unsigned long long pair_order_key(const uint4& m) {  // (depth bits, ordinal)
+    return (static_cast<unsigned long long>(m.w) << 32) | m.x;
+}
+
+// Orders the run of equal key words starting at s (insertion sort in global memory).
+__device__ void finish_pair_run(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t s,
+                                uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
     const uint32_t k = keys[s];
     uint32_t end = s + 1;
     while (end < count && keys[end] == k) ++end;
-    if (end - s > kLongRun) {  // long run (e.g. a row of same-pose characters at full detail)
-        const uint32_t slot = atomicAdd(sink.long_count, 1u);
-        if (slot < sink.long_cap) {
-            sink.long_runs[slot] = make_uint2(s, end - s);
-            return end;
+    if (end - s > kLongRun) {
+        const uint32_t slot = atomicAdd(long_count, 1u);
+        if (slot < long_cap) {
+            long_runs[slot] = make_uint2(s, end - s);
+            return;
         }
     }
     for (uint32_t a = s + 1; a < end; ++a) {
         const uint32_t ra = recs[a];
-        const uint32_t oa = meta[ra].x;
+        const unsigned long long oa = pair_order_key(meta[ra]);
         uint32_t j = a;
-        while (j > s && meta[recs[j - 1]].x > oa) {
+        while (j > s && pair_order_key(meta[recs[j - 1]]) > oa) {
             recs[j] = recs[j - 1];
             --j;
         }
         recs[j] = ra;
     }
-    for (uint32_t a = s; a < end; ++a) sink.put(a, meta[recs[a]]);
-    return end;
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kMetaThreads)
-k_sorted_spans(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted,
-               uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
+__global__ void __launch_bounds__(256)
+k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t cell_mask, int fix,
+             uint2* ranges, uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
-    SpanSink sink;
-    sink.span_sorted = span_sorted;
-    sink.long_runs = long_runs;
-    sink.long_count = long_count;
-    sink.long_cap = long_cap;
-    const uint32_t b = (blockIdx.x * kMetaThreads + threadIdx.x) * kStreamItems;
-    if (b + kStreamItems < count) {
-        uint32_t k[kStreamItems + 1];
+    const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) * kStreamItems;
+    if (b >= count) return;
+    const uint32_t prev_key = b > 0 ? keys[b - 1] : 0u;
+    if (b + kStreamItems <= count) {
         const uint4 lo = *reinterpret_cast<const uint4*>(keys + b);
         const uint4 hi = *reinterpret_cast<const uint4*>(keys + b + 4);
-        k[0] = lo.x; k[1] = lo.y; k[2] = lo.z; k[3] = lo.w;
-        k[4] = hi.x; k[5] = hi.y; k[6] = hi.z; k[7] = hi.w;
-        k[8] = keys[b + kStreamItems];
-        const uint32_t prev = b > 0 ? keys[b - 1] : ~0u;
-        // [w0, w1): the positions whose runs start and end inside the window.
+        const uint32_t k[kStreamItems] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        const bool has_next = b + kStreamItems < count;
+        const uint32_t next_key = has_next ? keys[b + kStreamItems] : 0u;
+        // Cell ranges (the reference's bins).
+        uint32_t pc = b > 0 ? (prev_key & cell_mask) : ~0u;
+#pragma unroll
+        for (int j = 0; j < kStreamItems; ++j) {
+            const uint32_t c = k[j] & cell_mask;
+            if (c != pc) {
+                ranges[c].x = b + j;
+                if (b + j > 0) ranges[pc].y = b + j;
+            }
+            pc = c;
+        }
+        if (!has_next) ranges[pc].y = count;
+        if (!fix) return;
+        // [w0, w1): positions whose runs start and end inside the window.
         int w0 = 0;
-        if (b > 0 && k[0] == prev) {
+        if (b > 0 && k[0] == prev_key) {
             w0 = 1;
 #pragma unroll
             for (int j = 1; j < kStreamItems; ++j)
                 if (w0 == j && k[j] == k[j - 1]) w0 = j + 1;
         }
         int w1 = kStreamItems;
-        if (k[kStreamItems - 1] == k[kStreamItems]) {
+        if (has_next && k[kStreamItems - 1] == next_key) {
             w1 = kStreamItems - 1;
 #pragma unroll
             for (int j = kStreamItems - 2; j >= 0; --j)
                 if (w1 == j + 1 && k[j] == k[j + 1]) w1 = j;
             w1 = max(w1, w0);
         }
-        uint32_t r[kStreamItems];
-        const uint4 rlo = *reinterpret_cast<const uint4*>(recs + b);
-        const uint4 rhi = *reinterpret_cast<const uint4*>(recs + b + 4);
-        r[0] = rlo.x; r[1] = rlo.y; r[2] = rlo.z; r[3] = rlo.w;
-        r[4] = rhi.x; r[5] = rhi.y; r[6] = rhi.z; r[7] = rhi.w;
-        uint4 m[kStreamItems];
+        bool tie[kStreamItems];
+        bool any = false;
 #pragma unroll
-        for (int j = 0; j < kStreamItems; ++j)  // independent gathers, all in flight
-            m[j] = (j >= w0 && j < w1) ? meta[r[j]] : make_uint4(0u, 0u, 0u, 0u);
-        bool moved = false;
+        for (int j = 0; j < kStreamItems; ++j) {
+            const bool l = j > 0 && k[j] == k[j - 1];
+            const bool r = j + 1 < kStreamItems && k[j] == k[j + 1];
+            tie[j] = j >= w0 && j < w1 && ((l && j - 1 >= w0) || (r && j + 1 < w1));
+            any |= tie[j];
+        }
+        if (any) {
+            const uint4 rlo = *reinterpret_cast<const uint4*>(recs + b);
+            const uint4 rhi = *reinterpret_cast<const uint4*>(recs + b + 4);
+            uint32_t r[kStreamItems] = {rlo.x, rlo.y, rlo.z, rlo.w, rhi.x, rhi.y, rhi.z, rhi.w};
+            unsigned long long o[kStreamItems];
 #pragma unroll
-        for (int round = 0; round < kStreamItems; ++round) {
+            for (int j = 0; j < kStreamItems; ++j) o[j] = tie[j] ? pair_order_key(meta[r[j]]) : 0ull;
+            bool moved = false;
 #pragma unroll
-            for (int j = round & 1; j + 1 < kStreamItems; j += 2) {
-                if (j >= w0 && j + 1 < w1 && k[j] == k[j + 1] && m[j].x > m[j + 1].x) {
-                    const uint4 tm = m[j]; m[j] = m[j + 1]; m[j + 1] = tm;
-                    const uint32_t tr = r[j]; r[j] = r[j + 1]; r[j + 1] = tr;
-                    moved = true;
+            for (int round = 0; round < kStreamItems; ++round) {
+#pragma unroll
+                for (int j = round & 1; j + 1 < kStreamItems; j += 2) {
+                    if (tie[j] && tie[j + 1] && k[j] == k[j + 1] && o[j] > o[j + 1]) {
+                        const unsigned long long to = o[j]; o[j] = o[j + 1]; o[j + 1] = to;
+                        const uint32_t tr = r[j]; r[j] = r[j + 1]; r[j + 1] = tr;
+                        moved = true;
+                    }
                 }
             }
-        }
-        if (w0 == 0 && w1 == kStreamItems) {
             if (moved) {
-                *reinterpret_cast<uint4*>(recs + b) = make_uint4(r[0], r[1], r[2], r[3]);
-                *reinterpret_cast<uint4*>(recs + b + 4) = make_uint4(r[4], r[5], r[6], r[7]);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(span_sorted + b);
 #pragma unroll
-            for (int j = 0; j < kStreamItems; j += 2) dst[j / 2] = make_uint4(m[j].y, m[j].z, m[j + 1].y, m[j + 1].z);
+                for (int j = 0; j < kStreamItems; ++j)
+                    if (tie[j]) recs[b + j] = r[j];
+            }
+        }
+        if (w1 < kStreamItems) finish_pair_run(keys, recs, meta, count, b + static_cast<uint32_t>(w1), long_runs, long_count, long_cap);
+        return;
+    }
+    // Last window: positions one by one.
+    uint32_t pc = b > 0 ? (prev_key & cell_mask) : ~0u;
+    for (uint32_t i = b; i < count; ++i) {
+        const uint32_t c = keys[i] & cell_mask;
+        if (c != pc) {
+            ranges[c].x = i;
+            if (i > 0) ranges[pc].y = i;
+        }
+        pc = c;
+    }
+    ranges[pc].y = count;
+    if (!fix) return;
+    uint32_t i = b;
+    if (b > 0)
+        while (i < count && keys[i] == prev_key) ++i;  // a run entering from the left
+    while (i < count) {
+        if (i + 1 < count && keys[i + 1] == keys[i]) {
+            finish_pair_run(keys, recs, meta, count, i, long_runs, long_count, long_cap);
+            const uint32_t k = keys[i];
+            while (i < count && keys[i] == k) ++i;
         } else {
-            // Only [w0, w1) is this thread's: the runs crossing the window edges are
-            // reordered by the threads where they start.
-#pragma unroll
-            for (int j = 0; j < kStreamItems; ++j) {
-                if (j >= w0 && j < w1) {
-                    if (moved) recs[b + j] = r[j];
-                    sink.put(b + j, m[j]);
-                }
-            }
-            if (w1 < kStreamItems) finish_run(keys, recs, meta, count, b + static_cast<uint32_t>(w1), sink);
-        }
-    } else if (b < count) {
-        // Last window: positions one by one.
-        uint32_t i = b;
-        if (b > 0) {
-            const uint32_t prev = keys[b - 1];
-            while (i < count && keys[i] == prev) ++i;  // a run entering from the left
-        }
-        while (i < count) {
-            if (i + 1 < count && keys[i + 1] == keys[i]) {
-                i = finish_run(keys, recs, meta, count, i, sink);
-            } else {
-                sink.put(i, meta[recs[i]]);
-                ++i;
-            }
+            ++i;
         }
     }
 }
 
-// Long equal-depth runs (> kLongRun splats) recorded by k_sorted_spans: one CTA per run
-// sorts (ordinal, record) in shared memory (bitonic, up to kLongRunCap) and writes the
-// records and their spans; longer runs are sorted in place in global memory.
+// Runs of more than kLongRun equal key words recorded by k_cell_fixup (many pairs of one
+// truncated depth in one cell, e.g. characters stacked on one spot): one CTA per run sorts
+// ((depth bits, ordinal), record) in shared memory (bitonic, up to kPairRunCap); longer
+// runs are sorted in place in global memory.
 __global__ void __launch_bounds__(256)
-k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
-            const uint32_t* long_count, uint32_t long_cap) {
-    __shared__ unsigned long long s_kv[kLongRunCap];
+k_pair_long_runs(uint32_t* recs, const uint4* meta, const uint2* long_runs, const uint32_t* long_count, uint32_t long_cap) {
+    __shared__ unsigned long long s_key[kPairRunCap];
+    __shared__ uint32_t s_rec[kPairRunCap];
     const uint32_t runs = min(*long_count, long_cap);
-    for (uint32_t r = blockIdx.x; r < runs; r += gridDim.x) {
-        const uint2 run = long_runs[r];
+    for (uint32_t q = blockIdx.x; q < runs; q += gridDim.x) {
+        const uint2 run = long_runs[q];
         const uint32_t s = run.x, n = run.y;
-        if (n <= kWarpRunCap) continue;  // k_long_runs_warp
-        if (n <= kLongRunCap) {
-            uint32_t P = 1;
-            while (P < n) P <<= 1;
+        uint32_t P = 1;
+        while (P < n) P <<= 1;
+        if (n <= kPairRunCap) {
             for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-                unsigned long long kv = ~0ull;
+                unsigned long long key = ~0ull;
+                uint32_t rec = 0u;
                 if (i < n) {
-                    const uint32_t rec = recs[s + i];
-                    kv = (static_cast<unsigned long long>(meta[rec].x) << 32) | rec;
+                    rec = recs[s + i];
+                    key = pair_order_key(meta[rec]);
                 }
-                s_kv[i] = kv;
+                s_key[i] = key;
+                s_rec[i] = rec;
             }
             __syncthreads();
             for (uint32_t k = 2; k <= P; k <<= 1) {
@@ -415,48 +452,38 @@ k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* 
                     for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
                         const uint32_t l = i ^ j;
                         if (l > i) {
-                            const unsigned long long a = s_kv[i], b = s_kv[l];
-                            const bool up = (i & k) == 0;
-                            if ((a > b) == up) {
-                                s_kv[i] = b;
-                                s_kv[l] = a;
+                            const unsigned long long a = s_key[i], c = s_key[l];
+                            if ((a > c) == ((i & k) == 0)) {
+                                s_key[i] = c;
+                                s_key[l] = a;
+                                const uint32_t t = s_rec[i]; s_rec[i] = s_rec[l]; s_rec[l] = t;
                             }
                         }
                     }
                     __syncthreads();
                 }
             }
-            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-                const uint32_t rec = static_cast<uint32_t>(s_kv[i]);
-                recs[s + i] = rec;
-                const uint4 m = meta[rec];
-                span_sorted[s + i] = make_uint2(m.y, m.z);
-            }
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) recs[s + i] = s_rec[i];
             __syncthreads();
         } else {
-            // Longer runs: bitonic in place in global memory over the whole CTA, in the
-            // all-ascending form (each merge starts by comparing i with its mirror in the
-            // block) so positions >= n act as +inf and are simply skipped. Ordinals are
-            // unique per splat.
+            // All-ascending bitonic in place (each merge opens with the mirror comparison),
+            // so positions >= n act as +inf and are skipped. Keys are unique per pair.
             uint32_t* r = recs + s;
-            uint32_t P = 1;
-            while (P < n) P <<= 1;
             for (uint32_t k = 2; k <= P; k <<= 1) {
                 for (uint32_t j = k >> 1; j > 0; j >>= 1) {
                     for (uint32_t t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+                        const uint32_t blk = t / j, off = t % j;
                         uint32_t i, l;
-                        if (j == (k >> 1)) {  // mirror step
-                            const uint32_t blk = t / j, off = t % j;
+                        if (j == (k >> 1)) {
                             i = blk * k + off;
                             l = blk * k + k - 1u - off;
-                        } else {  // half-cleaner
-                            const uint32_t blk = t / j, off = t % j;
+                        } else {
                             i = blk * 2u * j + off;
                             l = i + j;
                         }
                         if (l < n) {
                             const uint32_t ra = r[i], rb = r[l];
-                            if (meta[ra].x > meta[rb].x) {
+                            if (pair_order_key(meta[ra]) > pair_order_key(meta[rb])) {
                                 r[i] = rb;
                                 r[l] = ra;
                             }
@@ -465,62 +492,7 @@ k_long_runs(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* 
                     __syncthreads();
                 }
             }
-            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-                const uint4 m = meta[r[i]];
-                span_sorted[s + i] = make_uint2(m.y, m.z);
-            }
-            __syncthreads();
         }
-    }
-}
-
-// The runs of up to kWarpRunCap splats (most long runs: a few dozen same-depth splats):
-// one warp per run, bitonic on (ordinal, record) in the warp's shared slice.
-__global__ void __launch_bounds__(256)
-k_long_runs_warp(uint32_t* recs, const uint4* meta, uint2* span_sorted, const uint2* long_runs,
-                 const uint32_t* long_count, uint32_t long_cap) {
-    __shared__ unsigned long long s_kv[8][kWarpRunCap];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long* kv = s_kv[warp];
-    const uint32_t runs = min(*long_count, long_cap);
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp; r < runs; r += warps) {
-        const uint2 run = long_runs[r];
-        const uint32_t s = run.x, n = run.y;
-        if (n > kWarpRunCap) continue;  // k_long_runs
-        uint32_t P = 32;
-        while (P < n) P <<= 1;
-        for (uint32_t i = lane; i < P; i += 32) {
-            unsigned long long v = ~0ull;
-            if (i < n) {
-                const uint32_t rec = recs[s + i];
-                v = (static_cast<unsigned long long>(meta[rec].x) << 32) | rec;
-            }
-            kv[i] = v;
-        }
-        __syncwarp();
-        for (uint32_t k = 2; k <= P; k <<= 1) {
-            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-                for (uint32_t i = lane; i < P; i += 32) {
-                    const uint32_t l = i ^ j;
-                    if (l > i) {
-                        const unsigned long long a = kv[i], b = kv[l];
-                        if ((a > b) == ((i & k) == 0)) {
-                            kv[i] = b;
-                            kv[l] = a;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        for (uint32_t i = lane; i < n; i += 32) {
-            const uint32_t rec = static_cast<uint32_t>(kv[i]);
-            recs[s + i] = rec;
-            const uint4 m = meta[rec];
-            span_sorted[s + i] = make_uint2(m.y, m.z);
-        }
-        __syncwarp();
     }
 }
 
@@ -535,9 +507,9 @@ k_long_runs_warp(uint32_t* recs, const uint4* meta, uint2* span_sorted, const ui
 // k_sort_rows); else scatter them.
 template <bool kCount>
 __global__ void __launch_bounds__(kEmitThreads)
-k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sorted, uint32_t* block_digit,
-               const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads, uint32_t dmask,
-               uint32_t* pair_cell, uint32_t* pair_rec) {
+k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count, const uint2* span_sorted,
+               uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads,
+               uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec) {
     constexpr int kWarps = kEmitThreads / 32, kDigitsPerWarp = kRadix / kWarps, kPerLane = kEmitThreads / 32;
     static_assert(kRadix % kWarps == 0, "digits split evenly over the warps");
     constexpr uint32_t kStage = kEmitStage;            // pairs staged for coalesced writes
@@ -551,7 +523,7 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t i0 = blockIdx.x * kEmitSplats + 4u * tid;
     uint2 sp[4];
-    uint32_t rc[4];
+    uint32_t rc[4], tg[4] = {0u, 0u, 0u, 0u};
     if (i0 + 4 <= count) {
         const uint4 a = *reinterpret_cast<const uint4*>(span_sorted + i0);
         const uint4 b = *reinterpret_cast<const uint4*>(span_sorted + i0 + 2);
@@ -559,13 +531,21 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
         sp[0] = make_uint2(a.x, a.y); sp[1] = make_uint2(a.z, a.w);
         sp[2] = make_uint2(b.x, b.y); sp[3] = make_uint2(b.z, b.w);
         rc[0] = r.x; rc[1] = r.y; rc[2] = r.z; rc[3] = r.w;
+        if (!kCount && key_sorted) {
+            const uint4 t = *reinterpret_cast<const uint4*>(key_sorted + i0);
+            tg[0] = t.x; tg[1] = t.y; tg[2] = t.z; tg[3] = t.w;
+        }
     } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             sp[q] = i0 + q < count ? span_sorted[i0 + q] : make_uint2(0u, 0u);
             rc[q] = i0 + q < count ? rec_sorted[i0 + q] : 0u;
+            if (!kCount && key_sorted) tg[q] = i0 + q < count ? key_sorted[i0 + q] : 0u;
         }
     }
+    // Tag above the cell id: the low bits of the splat's truncated depth key (k_cell_fixup).
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tg[q] = key_sorted && tag_shift < 32 ? (tg[q] >> tag_drop) << tag_shift : 0u;
 #pragma unroll
     for (int d = 0; d < kRadix; ++d) s_cnt[d][tid] = 0u;
     if (!kCount && tid < kRadix) {  // global base of digit tid: scanned digit totals + this block's offset
@@ -619,15 +599,15 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
     const bool staged = total <= kStage;  // else every pair goes straight to its global slot
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const uint32_t rec = rc[q];
+        const uint32_t rec = rc[q], tag = tg[q];
         for_each_cell(sp[q], tiles_x, quads, [&](uint32_t c) {
             const uint32_t d = c & dmask;
             const uint32_t r = s_cnt[d][tid]++;  // rank among the block's pairs of digit d
             if (staged) {
-                s_stage_cell[s_local[d] + r] = c;
+                s_stage_cell[s_local[d] + r] = c | tag;
                 s_stage_rec[s_local[d] + r] = rec;
             } else {
-                pair_cell[s_base[d] + r] = c;
+                pair_cell[s_base[d] + r] = c | tag;
                 pair_rec[s_base[d] + r] = rec;
             }
         });
@@ -644,9 +624,10 @@ k_emit_scatter(const uint32_t* rec_sorted, uint32_t count, const uint2* span_sor
     }
 }
 
-void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, uint32_t count,
-                 const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total, int tiles_x, int quads,
-                 uint32_t dmask, uint32_t* pair_cell, uint32_t* pair_rec) {
+void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, const uint32_t* key_sorted,
+                 uint32_t count, const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
+                 int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
+                 uint32_t* pair_rec) {
     static bool attr = [] {
         cudaFuncSetAttribute(k_emit_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
         cudaFuncSetAttribute(k_emit_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
@@ -654,46 +635,13 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
     }();
     (void)attr;
     if (count_only)
-        k_emit_scatter<true><<<blocks, kEmitThreads, kRadix * kEmitThreads * 4, s>>>(rec_sorted, count, span_sorted, block_digit,
+        k_emit_scatter<true><<<blocks, kEmitThreads, kRadix * kEmitThreads * 4, s>>>(rec_sorted, key_sorted, count, span_sorted, block_digit,
                                                                     digit_total, blocks, tiles_x, quads, dmask,
-                                                                    pair_cell, pair_rec);
+                                                                    tag_drop, tag_shift, pair_cell, pair_rec);
     else
-        k_emit_scatter<false><<<blocks, kEmitThreads, kEmitSmem, s>>>(rec_sorted, count, span_sorted, block_digit,
+        k_emit_scatter<false><<<blocks, kEmitThreads, kEmitSmem, s>>>(rec_sorted, key_sorted, count, span_sorted, block_digit,
                                                                      digit_total, blocks, tiles_x, quads, dmask,
-                                                                     pair_cell, pair_rec);
-}
-
-// [start, end) of every cell in the cell-sorted pairs (the reference's bins).
-__global__ void __launch_bounds__(256)
-k_cell_ranges(const uint32_t* cells, uint32_t count, uint2* ranges) {
-    static_assert(kStreamItems == 8, "two uint4 loads per thread");
-    const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) * kStreamItems;
-    if (b >= count) return;
-    uint32_t prev = b > 0 ? cells[b - 1] : ~0u;
-    if (b + kStreamItems <= count) {
-        const uint4 lo = *reinterpret_cast<const uint4*>(cells + b);
-        const uint4 hi = *reinterpret_cast<const uint4*>(cells + b + 4);
-        const uint32_t c[kStreamItems] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-        for (int j = 0; j < kStreamItems; ++j) {
-            if (c[j] != prev) {
-                ranges[c[j]].x = b + j;
-                if (b + j > 0) ranges[prev].y = b + j;
-            }
-            prev = c[j];
-        }
-        if (b + kStreamItems == count) ranges[prev].y = count;
-        return;
-    }
-    for (uint32_t i = b; i < count; ++i) {
-        const uint32_t c = cells[i];
-        if (c != prev) {
-            ranges[c].x = i;
-            if (i > 0) ranges[prev].y = i;
-        }
-        prev = c;
-    }
-    ranges[prev].y = count;
+                                                                     tag_drop, tag_shift, pair_cell, pair_rec);
 }
 
 __global__ void k_iota2(uint32_t* a, uint32_t* b, uint32_t n) {

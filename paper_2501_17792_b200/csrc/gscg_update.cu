@@ -68,6 +68,7 @@ k_lod_plan(PlanParams p) {
         p.counters->depth_min_bits = 0xffffffffu;
         p.counters->depth_max_bits = 0u;
         p.counters->item_cursor = 0u;
+        p.counters->instances_culled = 0u;
         for (int q = 0; q < 8; ++q) p.counters->sort_ticket[q] = 0u;
     }
     __syncthreads();
@@ -110,7 +111,10 @@ k_lod_plan(PlanParams p) {
             count = p.groups[g].count;
             // Every rank numbers the whole crowd (ordinals are global); only its own
             // instance shard is projected.
-            if (i >= p.shard_begin && i < p.shard_end) atomicAdd(&s_gcount[g], 1u);
+            if (i >= p.shard_begin && i < p.shard_end) {
+                if (!p.visible || p.visible[i]) atomicAdd(&s_gcount[g], 1u);
+                else atomicAdd(&p.counters->instances_culled, 1u);
+            }
         }
         unsigned long long total;
         const unsigned long long excl =
@@ -153,7 +157,7 @@ k_lod_plan(PlanParams p) {
         for (int k = tid; k < 32 * kMaxGroups; k += blockDim.x) (&s_wcount[0][0])[k] = 0u;
         __syncthreads();
         const uint32_t i = tile + tid;
-        const bool valid = i < p.n && i >= p.shard_begin && i < p.shard_end;
+        const bool valid = i < p.n && i >= p.shard_begin && i < p.shard_end && (!p.visible || p.visible[i]);
         const uint32_t g = valid ? p.inst_group[i] : 0xffffffffu;
         const uint32_t peers = __match_any_sync(0xffffffffu, g);
         const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
@@ -283,6 +287,114 @@ k_fk_skin(FkParams p) {
                                 IB[c * 4 + 0], IB[c * 4 + 1], IB[c * 4 + 2], IB[c * 4 + 3]);
         if (r < 3) out[j * 12 + r * 4 + c] = sv;
     }
+}
+
+// Instance frustum cull. An instance is dropped from the projection work table only when
+// no Gaussian of it can survive gather_splats' cull (renderer.cpp:38-50: t.z > near and a
+// non-empty clipped 3-sigma rect), so the splat set, and everything after it, is unchanged.
+//
+// Ball of the posed means. posed = sum_k w_k (A_k m + t_k) over the nonzero weights
+// (avatar.cpp:182-190), with S_k = [A_k | t_k] the skin matrix. For any centre c:
+//   |posed - c| <= sum|w_k| (|A_k|_2 |m| + |t_k - c|) + |sum w_k - 1| |c|
+//               <= wabs (Amax mean_r + Tmax) + wdev |c|
+// with c the centre of the box of the joint translations, Tmax = max_j |t_j - c|,
+// |A_j|_2^2 <= max row sum of |A_j^T A_j| and the template bounds (TemplateDev).
+//
+// Rect of a splat at camera-space t (math.cpp:131-170): rx = 3 sqrt(C00) with
+// C00 = m0 S m0^T + 0.3 and m0 = (f/tz)(W0 - (tx/tz) W2), so
+//   rx <= 3 (f/tz) sqrt(1 + (tx/tz)^2) sigma + 3 sqrt(0.3)
+// (sigma^2 >= lambda_max of every covariance). The rect is empty on the left when
+// mx + rx < 0, on the right when mx - rx >= width (same for y). The test bounds tx/tz over
+// the ball in double precision with relative and pixel margins far above the float
+// rounding of the projection itself. Non-finite bounds never cull.
+__global__ void __launch_bounds__(256)
+k_inst_cull(CullParams p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t inst = p.first + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (inst >= p.n) return;
+    const TemplateDev tpl = p.templates[p.template_ids[inst]];
+    const int J = tpl.joint_count;
+    const float4* S = reinterpret_cast<const float4*>(p.skin + static_cast<size_t>(inst) * p.joint_stride * 12);
+    float tmin[3] = {INFINITY, INFINITY, INFINITY}, tmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+    float a2 = 0.0f;
+    float tj[2][3];
+    for (int r = 0; r < 2; ++r) for (int k = 0; k < 3; ++k) tj[r][k] = 0.0f;
+    bool bad = false;  // a non-finite matrix entry: never cull
+    for (int j = lane, r = 0; r < 2; j += 32, ++r) {  // joint_count <= 64 (GSCG_MAX_JOINTS)
+        if (j >= J) break;
+        const float4 r0 = S[3 * j + 0], r1 = S[3 * j + 1], r2 = S[3 * j + 2];
+        const float t[3] = {r0.w, r1.w, r2.w};
+        for (int k = 0; k < 3; ++k) {
+            tj[r][k] = t[k];
+            tmin[k] = fminf(tmin[k], t[k]);
+            tmax[k] = fmaxf(tmax[k], t[k]);
+            bad |= !isfinite(t[k]);
+        }
+        // G = A^T A; |A|_2^2 = lambda_max(G) <= max row sum of |G|.
+        const double a[3][3] = {{r0.x, r0.y, r0.z}, {r1.x, r1.y, r1.z}, {r2.x, r2.y, r2.z}};
+        double rowmax = 0.0;
+        for (int u = 0; u < 3; ++u) {
+            double row = 0.0;
+            for (int v = 0; v < 3; ++v) row += fabs(a[0][u] * a[0][v] + a[1][u] * a[1][v] + a[2][u] * a[2][v]);
+            rowmax = fmax(rowmax, row);
+        }
+        bad |= !(rowmax <= 1e30);
+        a2 = fmaxf(a2, static_cast<float>(rowmax * (1.0 + 1e-6)));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        for (int k = 0; k < 3; ++k) {
+            tmin[k] = fminf(tmin[k], __shfl_xor_sync(0xffffffffu, tmin[k], o));
+            tmax[k] = fmaxf(tmax[k], __shfl_xor_sync(0xffffffffu, tmax[k], o));
+        }
+        a2 = fmaxf(a2, __shfl_xor_sync(0xffffffffu, a2, o));
+    }
+    double c[3];
+    for (int k = 0; k < 3; ++k) c[k] = 0.5 * (static_cast<double>(tmin[k]) + static_cast<double>(tmax[k]));
+    double T = 0.0;
+    for (int j = lane, r = 0; r < 2; j += 32, ++r) {
+        if (j >= J) break;
+        const double d0 = tj[r][0] - c[0], d1 = tj[r][1] - c[1], d2 = tj[r][2] - c[2];
+        T = fmax(T, sqrt(d0 * d0 + d1 * d1 + d2 * d2));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) T = fmax(T, __shfl_xor_sync(0xffffffffu, T, o));
+    if (lane != 0) return;
+
+    const double cn = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    const double amax = sqrt(static_cast<double>(a2));
+    double rho = static_cast<double>(tpl.cull_wabs) * (amax * tpl.cull_mean_r + T) + static_cast<double>(tpl.cull_wdev) * cn;
+    rho = rho * 1.001 + 1e-3 * (1.0 + cn);
+    const CameraDev& cam = p.cam;
+    const double d[3] = {c[0] - cam.pos[0], c[1] - cam.pos[1], c[2] - cam.pos[2]};
+    double tc[3];
+    for (int i = 0; i < 3; ++i) tc[i] = cam.w[3 * i + 0] * d[0] + cam.w[3 * i + 1] * d[1] + cam.w[3 * i + 2] * d[2];
+    const double near_m = cam.near_m;
+    bool cull = false;
+    if (tc[2] + rho < near_m) {
+        cull = true;  // every point behind the near plane
+    } else {
+        const double zmin = fmax(near_m, tc[2] - rho), zmax = tc[2] + rho;
+        const double f = cam.focal, sigma = static_cast<double>(tpl.cull_sigma) * 1.001;
+        const double margin = 2.0;                             // pixels
+        const double pad = 3.0 * 0.5477225575051661 + 0.01;   // 3 sqrt(0.3)
+        // tx/tz and ty/tz over the ball: numerator bound over the tz that extremises it.
+        auto ratio_hi = [&](double num) { return num >= 0.0 ? num / zmin : num / zmax; };
+        auto ratio_lo = [&](double num) { return num >= 0.0 ? num / zmax : num / zmin; };
+        const double ux_hi = ratio_hi(tc[0] + rho), ux_lo = ratio_lo(tc[0] - rho);
+        const double uy_hi = ratio_hi(tc[1] + rho), uy_lo = ratio_lo(tc[1] - rho);
+        const double ux = fmax(fabs(ux_hi), fabs(ux_lo)), uy = fmax(fabs(uy_hi), fabs(uy_lo));
+        const double rx = 3.0 * (f / zmin) * sqrt(1.0 + ux * ux) * sigma * 1.001 + pad;
+        const double ry = 3.0 * (f / zmin) * sqrt(1.0 + uy * uy) * sigma * 1.001 + pad;
+        const double mx_hi = f * ux_hi + cam.cx, mx_lo = f * ux_lo + cam.cx;
+        const double my_hi = f * uy_hi + cam.cy, my_lo = f * uy_lo + cam.cy;
+        cull = (mx_hi + rx < -margin) || (mx_lo - rx > cam.width + margin) ||
+               (my_hi + ry < -margin) || (my_lo - ry > cam.height + margin);
+    }
+    // NaN anywhere makes the comparisons false; non-finite input never culls.
+    if (bad || !(rho < 1e30)) cull = false;
+    p.visible[inst] = cull ? 0u : 1u;
 }
 
 __global__ void k_copy_segments(CopySegs c) {

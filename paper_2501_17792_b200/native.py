@@ -23,6 +23,7 @@ GSCG_MEM_HOST = 0
 GSCG_MEM_DEVICE = 1
 GSCG_DEBUG_POSED = 1
 GSCG_DEBUG_RECORDS = 2
+GSCG_DEBUG_NO_CULL = 4
 GSCG_MAX_BANDS = 64
 GSCG_BAND_SPLAT_BYTES = 64
 MAX_LOD_THRESHOLDS = 8
@@ -158,6 +159,7 @@ GSCG_SYMBOLS = {
     "gscg_synchronize": (C.c_int, [_P]),
     "gscg_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "gscg_get_counts": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "gscg_get_instances_culled": (C.c_int, [_P, C.POINTER(C.c_uint32)]),
     "gscg_get_lod": (C.c_int, [_P, _P, C.c_uint32]),
     "gscg_get_instance_base": (C.c_int, [_P, _P, C.c_uint32]),
     "gscg_get_posed_means": (C.c_int, [_P, _P, C.c_uint64]),

@@ -115,3 +115,29 @@ def check_frame(scene, renderer, oracle_scene, gpu_out, orc_out, tile_size=16, f
     assert report["T_max_abs"] <= PIXEL_TOL, f"transmittance max abs {report['T_max_abs']}"
     assert report["psnr"] >= PSNR_MIN, f"PSNR {report['psnr']}"
     return report
+
+
+def check_cull_invariance(renderer, time_s=0.0, settings=None, static_pose=False, forced_lod=None) -> int:
+    """The instance frustum cull (k_inst_cull) only drops instances none of whose splats
+    can survive gather_splats' cull (renderer.cpp:38-50), so the frame with it must be
+    byte-identical to the frame without it: counts, the surviving splat records, the
+    per-cell sort order and ranges, pixels and T. Returns the number of culled instances."""
+    import paper_2501_17792_b200 as P
+
+    settings = settings or P.RenderSettings()
+    out = []
+    for flags in (N.GSCG_DEBUG_RECORDS | N.GSCG_DEBUG_NO_CULL, N.GSCG_DEBUG_RECORDS):
+        renderer.set_debug(flags)
+        rgb, T = renderer.render_frame(time_s, settings, static_pose, forced_lod)
+        rec = renderer.splat_records()
+        rec = rec[np.argsort(rec["ordinal"], kind="stable")]
+        out.append((rgb.copy(), T.copy(), renderer.counts(), rec.tobytes(), renderer.sorted_ordinals().copy(),
+                    renderer.cell_ranges().copy(), renderer.instances_culled()))
+    (a, b) = out
+    assert a[6] == 0, "GSCG_DEBUG_NO_CULL still culled instances"
+    assert a[2] == b[2], f"counts with/without cull {b[2]} / {a[2]}"
+    assert a[3] == b[3], "surviving splat records differ with the instance cull"
+    assert np.array_equal(a[4], b[4]), "per-cell sort order differs with the instance cull"
+    assert np.array_equal(a[5], b[5]), "cell ranges differ with the instance cull"
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes(), "pixels differ with the cull"
+    return b[6]

@@ -8,7 +8,7 @@ import pytest
 
 import paper_2501_17792_b200 as P
 from oracle import orc
-from tests.parity import check_frame, render_both
+from tests.parity import check_cull_invariance, check_frame, render_both
 
 pytestmark = pytest.mark.gpu
 
@@ -76,6 +76,8 @@ def test_culled_instances_behind_and_offscreen():
     s.instances = inst
     rep = parity(s, 0.2)
     assert rep["S"] < rep["G"]
+    r = P.Renderer(s)
+    assert check_cull_invariance(r, 0.2) >= 2  # the one behind and the one far sideways
 
 
 def test_hysteresis_across_frames():
@@ -335,6 +337,34 @@ def test_baseline_config(idx):
     s, extra = config_scene(idx)
     rep = parity(s, extra["time_s"], forced_lod=extra["forced_lod"])
     assert rep["S"] > 0 and rep["K"] > 0
+    check_cull_invariance(P.Renderer(s), extra["time_s"], forced_lod=extra["forced_lod"])
+
+
+# Cameras inside and around a crowd, looking along and across the rows, tilted, with wide
+# and narrow fields of view: instances straddle every frustum side and the near plane.
+CULL_CAMERAS = [
+    ((5.5, 1.6, -3.0), (5.5, 1.0, 5.0), 50.0, 16),
+    ((5.5, 1.7, 5.5), (12.0, 1.2, 6.0), 50.0, 16),
+    ((5.5, 1.7, 5.5), (-3.0, 1.0, 4.0), 70.0, 8),
+    ((5.5, 1.7, 5.5), (5.0, 1.5, -4.0), 30.0, 16),
+    ((5.5, 6.0, 5.5), (6.0, 0.0, 8.0), 60.0, 16),
+    ((5.5, 0.3, 2.0), (5.5, 2.5, 9.0), 40.0, 3),
+    ((14.0, 1.6, 5.5), (-1.0, 1.0, 5.5), 90.0, 16),
+    ((5.5, 1.0, 5.2), (5.6, 1.0, 5.9), 50.0, 16),   # nose against one character
+]
+
+
+@pytest.mark.parametrize("cam", CULL_CAMERAS)
+def test_instance_cull_is_invisible(cam):
+    pos, look, fov, tile = cam
+    cfg = P.SceneConfig(template_count=3, level_counts=(400, 120, 40), with_sh=True, motion_count=3,
+                        motion_frames=24, grid_rows=12, grid_cols=12, crowd_count=144, crowd_seed=5,
+                        cam_pos=pos, cam_look=look, width=320, height=200)
+    s = P.Scene(cfg)
+    s.set_camera(pos, look, fov_y_deg=fov, width=320, height=200)
+    r = P.Renderer(s)
+    culled = check_cull_invariance(r, 0.4, P.RenderSettings(tile_size=tile))
+    assert 0 <= culled < 144
 
 
 @pytest.mark.slow
@@ -347,6 +377,7 @@ def test_baseline_config3_headline():
     assert rep["G"] == 14972565 and rep["S"] > 10_000_000
     again, _ = r.render_frame(0.5, P.RenderSettings())
     assert again.tobytes() == g[0].tobytes()
+    assert check_cull_invariance(r, 0.5) > 500  # about a quarter of the crowd is off-screen
 
 
 @pytest.mark.slow
@@ -359,3 +390,4 @@ def test_baseline_config4_4k_ten_thousand():
     g, c = render_both(s, r, o, 0.25)
     rep = check_frame(s, r, o, g, c)
     assert rep["S"] > 20_000_000 and rep["K"] > 50_000_000
+    assert check_cull_invariance(r, 0.25) > 1000
