@@ -5,7 +5,7 @@
 //   H2D of the frame records (pinned staging, one copy)
 //   update:    k_fk_skin -> k_inst_cull -> k_lod_plan (1 CTA)
 //   gather:    k_project (persistent, template-major)       -> counters readback (sync)
-//   sort:      splats by the top <= 20 varying depth bits (k_sort_{upsweep,rows,downsweep} x P) ->
+//   sort:      splats by the top <= 25 varying depth bits (k_sort_{upsweep,rows,downsweep} x P) ->
 //              spans in sorted order (k_sorted_spans) ->
 //              pairs scattered in first-cell-pass order, keys tagged with the truncated depth
 //              (k_emit_scatter count, k_sort_rows, k_emit_scatter scatter) ->
@@ -72,6 +72,10 @@ struct DevBuf {
         return static_cast<T*>(ptr);
     }
 };
+
+// Varying depth bits the splat sort orders (LSD passes of <= 5 bits); the lower bits and
+// the ordinal tie-break are settled per cell by k_cell_fixup.
+constexpr uint32_t kDepthSortBits = 25;
 
 struct LevelStore {
     uint32_t count = 0;
@@ -147,6 +151,7 @@ struct gscg_ctx {
     DevBuf records, splat_meta, splat_depth;
     uint64_t splat_capacity = 0, pair_capacity = 0;
     uint32_t culled = 0;  // instances dropped by k_inst_cull in the last frame
+    uint32_t depth_sort_bits = kDepthSortBits;  // top varying depth bits the splat sort orders
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
@@ -327,9 +332,6 @@ void refresh_power_floor(gscg_ctx* ctx, float cutoff) {
     }
     tmp.release();
 }
-
-// Depth bits the splat sort orders (4 passes of <= 5 bits); lower bits are settled per cell.
-constexpr uint32_t kDepthSortBits = 20;
 
 // Digit layout of one LSD sort: pass q sorts bits [shift[q], shift[q] + bits[q]).
 struct RadixPlan {
@@ -783,7 +785,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         // 1. splats by the top (at most kDepthSortBits) varying bits of their depth keys;
         //    the dropped low bits and the ordinal tie-break are settled per cell in step 4.
         const uint32_t dbits = static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax));
-        const uint32_t drop = dbits > kDepthSortBits ? dbits - kDepthSortBits : 0u;
+        const uint32_t drop = dbits > ctx->depth_sort_bits ? dbits - ctx->depth_sort_bits : 0u;
         RadixPlan dplan{};
         if (!presorted) {
             dplan = make_plan(dbits - drop);
@@ -799,16 +801,14 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         const uint32_t cell_bits = std::max(1, bits_for(cells - 1));
         const uint32_t cell_mask = cell_bits >= 32 ? 0xffffffffu : (1u << cell_bits) - 1u;
         const uint32_t dmask = (1u << cplan.bits[0]) - 1u;
-        const uint32_t sblocks = (S32 + 1023) / 1024;                 // k_sorted_spans CTAs
         const uint32_t eblocks = (S32 + kEmitSplats - 1) / kEmitSplats;  // emission blocks
         CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
-        static_assert(kMetaThreads * kStreamItems == 1024, "one splat block per CTA");
         const int quads = geo.cells_per_tile == 4 ? 1 : 0;
-        k_sorted_spans<<<sblocks, kMetaThreads, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(), S32,
-                                                        ctx->span_sorted.as<uint2>());
-        ++launches;
         const uint32_t* tag_keys = presorted ? nullptr : ctx->skeys[sb].as<uint32_t>();
+        k_sorted_spans<<<(S32 + 1023) / 1024, kMetaThreads, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
+                                                                    S32, ctx->span_sorted.as<uint2>());
+        ++launches;
         launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), nullptr, geo.tiles_x, quads, dmask, drop, cell_bits, nullptr, nullptr);
         SortPassParams bp{};
@@ -833,18 +833,19 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                                                ctx->pcell, ctx->precs, K, rest, launches)
                                    : 1;
         // 4. cell ranges + every run of equal (cell, tag) ordered by (depth bits, ordinal).
-        const uint32_t long_cap = K / kLongRun + 1;  // runs longer than kLongRun: at most K / kLongRun
+        const uint32_t long_cap = K / kLongRun + K / 2048 + 2;  // see k_cell_fixup
         CUDA_TRY(ctx->long_runs.ensure(static_cast<size_t>(long_cap) * 8 + 16));
         uint32_t* long_count = reinterpret_cast<uint32_t*>(ctx->long_runs.as<uint2>() + long_cap);
         CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
-        const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);
+        const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);  // 2048 pairs per CTA
         k_cell_fixup<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), ctx->precs[cb].as<uint32_t>(),
                                              ctx->splat_meta.as<uint4>(), K, cell_mask, presorted ? 0 : 1,
                                              ctx->ranges.as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap);
         ++launches;
         if (!presorted) {
-            k_pair_long_runs<<<ctx->sm_count * 2, 256, 0, s>>>(ctx->precs[cb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
-                                                              ctx->long_runs.as<uint2>(), long_count, long_cap);
+            k_pair_long_runs<<<ctx->sm_count * 2, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K,
+                                                              ctx->precs[cb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
+                                                              ctx->long_runs.as<uint2>(), long_count);
             ++launches;
         }
         CUDA_TRY(cudaGetLastError());
@@ -970,6 +971,10 @@ int gscg_create(int device, gscg_ctx** out) {
         if (prop.major < 10)
             throw Status(GSCG_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (Blackwell)");
         ctx->sm_count = prop.multiProcessorCount;
+        if (const char* e = std::getenv("GSCG_DEPTH_SORT_BITS")) {  // tuning knob (see kDepthSortBits)
+            const int v = std::atoi(e);
+            if (v >= 1 && v <= 32) ctx->depth_sort_bits = static_cast<uint32_t>(v);
+        }
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
         for (auto& e : ctx->band_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

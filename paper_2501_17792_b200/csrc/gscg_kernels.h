@@ -173,14 +173,16 @@ __global__ void k_sort_rows(SortPassParams p);
 __global__ void k_sort_downsweep(SortPassParams p);
 
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
+__global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted);
 constexpr uint32_t kLongRun = 32;       // runs of equal pair keys longer than this go to k_pair_long_runs
 constexpr uint32_t kPairRunCap = 2048;  // k_pair_long_runs sorts runs up to this size in shared memory
-__global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted);
+// long_runs must hold count / kLongRun + count / 2048 + 2 entries (runs longer than
+// kLongRun, plus at most one run leaving each 2048-pair fix-up tile).
 __global__ void k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
                              uint32_t cell_mask, int fix, uint2* ranges, uint2* long_runs, uint32_t* long_count,
                              uint32_t long_cap);
-__global__ void k_pair_long_runs(uint32_t* recs, const uint4* meta, const uint2* long_runs, const uint32_t* long_count,
-                                 uint32_t long_cap);
+__global__ void k_pair_long_runs(const uint32_t* keys, uint32_t count, uint32_t* recs, const uint4* meta,
+                                 const uint2* long_runs, const uint32_t* long_count);
 constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
 constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
 constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes

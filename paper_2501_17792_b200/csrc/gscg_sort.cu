@@ -1,16 +1,19 @@
 // Stage "sort" on the B200: the reference's own two-step order — sort the splats by
 // depth, then bin them into tiles in that order (sort_splats_impl renderer.cpp:85-107,
-// binning renderer.cpp:143-161) — restated as three device passes:
+// binning renderer.cpp:143-161) — restated as four device steps:
 //
-//   1. LSD radix sort of the S splat depth keys (32-bit, only the bits that vary in the
-//      frame), values = record index; k_sorted_spans orders equal-depth runs by splat
-//      ordinal (instance base + gaussian index) = the reference's (instance, gaussian)
-//      tie-break. The splats are now in the reference's total order.
-//   2. k_sorted_spans + k_scan_sums + k_emit_pairs: every sorted splat emits one pair per
-//      overlapped binning cell (tile, or 8x8 quadrant of a 16-px tile), in sorted order.
-//   3. stable LSD radix sort of the pairs' cell ids; k_cell_ranges marks each cell's
-//      [start, end). Stability keeps the depth order inside every cell, so each cell
-//      list is exactly the reference's bin restricted to the cell.
+//   1. LSD radix sort of the S splat depth keys over their top (at most 25) varying bits,
+//      values = record index.
+//   2. k_sorted_spans gathers the spans in sorted order; k_emit_scatter (count: per-block
+//      digit counts; k_sort_rows; scatter): every sorted splat emits one pair per overlapped binning cell
+//      (tile, or 8x8 quadrant of a 16-px tile) straight into the order of the first
+//      stable cell pass; each pair's key word carries its splat's truncated depth above
+//      the cell id.
+//   3. the remaining stable LSD passes over the cell bits.
+//   4. k_cell_fixup: cell ranges, and every run of pairs with equal (cell, truncated
+//      depth) ordered by (depth bits, ordinal) — the dropped low bits and the reference's
+//      (instance, gaussian) tie-break (ordinal = instance base + gaussian index). Each
+//      cell list is then exactly the reference's bin restricted to the cell.
 //
 // Each LSD pass (digits of up to 5 bits; a b-bit key takes ceil(b/5) passes with the bits
 // spread evenly) is reduce-then-scan: k_sort_upsweep counts digits per 4096-key tile,
@@ -279,39 +282,14 @@ k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* s
 // cell. Inside a cell, a run of equal key words (same cell, same tag) holds pairs of equal
 // truncated depth, or, when tags alias, of increasing truncated depth; sorting every such
 // run by the full (depth bits, ordinal) key (renderer.cpp:85-107) therefore yields exactly
-// the reference's bin order. Runs are short (a few pairs; ties inside one 8x8 cell), so a
-// thread orders the runs inside its 8-pair window in registers (odd-even transposition),
-// finishes a run leaving its window in global memory, and hands runs longer than kLongRun
-// to k_pair_long_runs. Pairs outside runs are never gathered.
+// the reference's bin order. Runs are short (a few pairs; ties inside one 8x8 cell): a CTA
+// stages 2048 pairs in shared memory, gathers (depth, ordinal) for the tied pairs only,
+// and the thread where a run starts insertion-sorts it there; a run leaving the tile is
+// finished in global memory, and runs longer than kLongRun go to k_pair_long_runs.
 namespace {
 
 __device__ __forceinline__ unsigned long long pair_order_key(const uint4& m) {  // (depth bits, ordinal)
     return (static_cast<unsigned long long>(m.w) << 32) | m.x;
-}
-
-// Orders the run of equal key words starting at s (insertion sort in global memory).
-__device__ void finish_pair_run(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t s,
-                                uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
-    const uint32_t k = keys[s];
-    uint32_t end = s + 1;
-    while (end < count && keys[end] == k) ++end;
-    if (end - s > kLongRun) {
-        const uint32_t slot = atomicAdd(long_count, 1u);
-        if (slot < long_cap) {
-            long_runs[slot] = make_uint2(s, end - s);
-            return;
-        }
-    }
-    for (uint32_t a = s + 1; a < end; ++a) {
-        const uint32_t ra = recs[a];
-        const unsigned long long oa = pair_order_key(meta[ra]);
-        uint32_t j = a;
-        while (j > s && pair_order_key(meta[recs[j - 1]]) > oa) {
-            recs[j] = recs[j - 1];
-            --j;
-        }
-        recs[j] = ra;
-    }
 }
 
 }  // namespace
@@ -320,119 +298,203 @@ __global__ void __launch_bounds__(256)
 k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t cell_mask, int fix,
              uint2* ranges, uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
-    const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) * kStreamItems;
-    if (b >= count) return;
-    const uint32_t prev_key = b > 0 ? keys[b - 1] : 0u;
-    if (b + kStreamItems <= count) {
-        const uint4 lo = *reinterpret_cast<const uint4*>(keys + b);
-        const uint4 hi = *reinterpret_cast<const uint4*>(keys + b + 4);
-        const uint32_t k[kStreamItems] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        const bool has_next = b + kStreamItems < count;
-        const uint32_t next_key = has_next ? keys[b + kStreamItems] : 0u;
-        // Cell ranges (the reference's bins).
-        uint32_t pc = b > 0 ? (prev_key & cell_mask) : ~0u;
-#pragma unroll
-        for (int j = 0; j < kStreamItems; ++j) {
-            const uint32_t c = k[j] & cell_mask;
-            if (c != pc) {
-                ranges[c].x = b + j;
-                if (b + j > 0) ranges[pc].y = b + j;
-            }
-            pc = c;
+    constexpr uint32_t kThreads = 256, kTile = kThreads * kStreamItems;
+    constexpr uint32_t kHalo = 32;  // pairs past the tile: room for a run leaving the tile
+    // Tile position p lives at slot (p % 8) * 256 + p / 8: a thread's item j of all lanes
+    // is one contiguous row (conflict-free); the halo follows the tile.
+    __shared__ uint32_t s_key[kTile + kHalo];
+    __shared__ uint32_t s_rec[kTile + kHalo];
+    __shared__ unsigned long long s_ord[kTile + kHalo];  // (depth bits, ordinal) of the tied pairs
+    __shared__ uint16_t s_runs[kThreads / 32][32 * kStreamItems];  // run starts per warp
+    __shared__ uint32_t s_enter_end;
+    __shared__ uint32_t s_dirty[kThreads / 32];  // bit t % 32 of word t / 32: window of thread t moved
+    auto slot = [](uint32_t p) { return p < kTile ? (p & 7u) * kThreads + (p >> 3) : p; };
+    const uint32_t cta0 = blockIdx.x * kTile;
+    if (cta0 >= count) return;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t n_here = min(kTile, count - cta0);
+    const uint32_t n_ext = min(kTile + kHalo, count - cta0);
+    const bool has_prev = cta0 > 0;
+    const uint32_t prev_key = has_prev ? keys[cta0 - 1] : 0u;
+    const bool has_beyond = cta0 + n_ext < count;
+    const uint32_t beyond_key = fix && has_beyond ? keys[cta0 + n_ext] : 0u;
+    const uint32_t t0 = tid * kStreamItems;
+    uint32_t k[kStreamItems], r[kStreamItems];
+    if (n_here == kTile) {
+        const uint4 klo = *reinterpret_cast<const uint4*>(keys + cta0 + t0);
+        const uint4 khi = *reinterpret_cast<const uint4*>(keys + cta0 + t0 + 4);
+        k[0] = klo.x; k[1] = klo.y; k[2] = klo.z; k[3] = klo.w; k[4] = khi.x; k[5] = khi.y; k[6] = khi.z; k[7] = khi.w;
+        if (fix) {
+            const uint4 rlo = *reinterpret_cast<const uint4*>(recs + cta0 + t0);
+            const uint4 rhi = *reinterpret_cast<const uint4*>(recs + cta0 + t0 + 4);
+            r[0] = rlo.x; r[1] = rlo.y; r[2] = rlo.z; r[3] = rlo.w; r[4] = rhi.x; r[5] = rhi.y; r[6] = rhi.z; r[7] = rhi.w;
         }
-        if (!has_next) ranges[pc].y = count;
-        if (!fix) return;
-        // [w0, w1): positions whose runs start and end inside the window.
-        int w0 = 0;
-        if (b > 0 && k[0] == prev_key) {
-            w0 = 1;
+    } else {
 #pragma unroll
-            for (int j = 1; j < kStreamItems; ++j)
-                if (w0 == j && k[j] == k[j - 1]) w0 = j + 1;
+        for (uint32_t j = 0; j < kStreamItems; ++j) {
+            const bool in = t0 + j < n_here;
+            k[j] = in ? keys[cta0 + t0 + j] : 0u;
+            r[j] = in && fix ? recs[cta0 + t0 + j] : 0u;
         }
-        int w1 = kStreamItems;
-        if (has_next && k[kStreamItems - 1] == next_key) {
-            w1 = kStreamItems - 1;
-#pragma unroll
-            for (int j = kStreamItems - 2; j >= 0; --j)
-                if (w1 == j + 1 && k[j] == k[j + 1]) w1 = j;
-            w1 = max(w1, w0);
-        }
-        bool tie[kStreamItems];
-        bool any = false;
-#pragma unroll
-        for (int j = 0; j < kStreamItems; ++j) {
-            const bool l = j > 0 && k[j] == k[j - 1];
-            const bool r = j + 1 < kStreamItems && k[j] == k[j + 1];
-            tie[j] = j >= w0 && j < w1 && ((l && j - 1 >= w0) || (r && j + 1 < w1));
-            any |= tie[j];
-        }
-        if (any) {
-            const uint4 rlo = *reinterpret_cast<const uint4*>(recs + b);
-            const uint4 rhi = *reinterpret_cast<const uint4*>(recs + b + 4);
-            uint32_t r[kStreamItems] = {rlo.x, rlo.y, rlo.z, rlo.w, rhi.x, rhi.y, rhi.z, rhi.w};
-            unsigned long long o[kStreamItems];
-#pragma unroll
-            for (int j = 0; j < kStreamItems; ++j) o[j] = tie[j] ? pair_order_key(meta[r[j]]) : 0ull;
-            bool moved = false;
-#pragma unroll
-            for (int round = 0; round < kStreamItems; ++round) {
-#pragma unroll
-                for (int j = round & 1; j + 1 < kStreamItems; j += 2) {
-                    if (tie[j] && tie[j + 1] && k[j] == k[j + 1] && o[j] > o[j + 1]) {
-                        const unsigned long long to = o[j]; o[j] = o[j + 1]; o[j + 1] = to;
-                        const uint32_t tr = r[j]; r[j] = r[j + 1]; r[j + 1] = tr;
-                        moved = true;
-                    }
-                }
-            }
-            if (moved) {
-#pragma unroll
-                for (int j = 0; j < kStreamItems; ++j)
-                    if (tie[j]) recs[b + j] = r[j];
-            }
-        }
-        if (w1 < kStreamItems) finish_pair_run(keys, recs, meta, count, b + static_cast<uint32_t>(w1), long_runs, long_count, long_cap);
-        return;
     }
-    // Last window: positions one by one.
-    uint32_t pc = b > 0 ? (prev_key & cell_mask) : ~0u;
-    for (uint32_t i = b; i < count; ++i) {
-        const uint32_t c = keys[i] & cell_mask;
-        if (c != pc) {
-            ranges[c].x = i;
-            if (i > 0) ranges[pc].y = i;
-        }
-        pc = c;
+#pragma unroll
+    for (uint32_t j = 0; j < kStreamItems; ++j) {
+        s_key[j * kThreads + tid] = k[j];
+        if (fix) s_rec[j * kThreads + tid] = r[j];
     }
-    ranges[pc].y = count;
+    if (fix && tid < kHalo && kTile + tid < n_ext) {
+        s_key[kTile + tid] = keys[cta0 + kTile + tid];
+        s_rec[kTile + tid] = recs[cta0 + kTile + tid];
+    }
+    __syncthreads();
+    // Neighbours of the thread's window.
+    const bool has_left = t0 > 0 || has_prev;
+    const uint32_t left_key = t0 > 0 ? s_key[slot(t0 - 1)] : prev_key;
+    const bool has_right = t0 + kStreamItems < n_ext;
+    const uint32_t right_key = has_right ? s_key[slot(t0 + kStreamItems)] : 0u;
+    // Cell ranges (the reference's bins).
+#pragma unroll
+    for (uint32_t j = 0; j < kStreamItems; ++j) {
+        const uint32_t pos = t0 + j;
+        if (pos >= n_here) break;
+        const uint32_t c = k[j] & cell_mask;
+        const bool first = j == 0 && !has_left;
+        const uint32_t pc = (j > 0 ? k[j - 1] : left_key) & cell_mask;
+        if (first || c != pc) {
+            ranges[c].x = cta0 + pos;
+            if (!first) ranges[pc].y = cta0 + pos;
+        }
+        if (cta0 + pos + 1 == count) ranges[c].y = count;
+    }
     if (!fix) return;
-    uint32_t i = b;
-    if (b > 0)
-        while (i < count && keys[i] == prev_key) ++i;  // a run entering from the left
-    while (i < count) {
-        if (i + 1 < count && keys[i + 1] == keys[i]) {
-            finish_pair_run(keys, recs, meta, count, i, long_runs, long_count, long_cap);
-            const uint32_t k = keys[i];
-            while (i < count && keys[i] == k) ++i;
-        } else {
-            ++i;
+    // Tied pairs: equal key word on either side. All their gathers in flight at once.
+    bool tie[kStreamItems], left[kStreamItems];
+    uint4 m[kStreamItems];
+#pragma unroll
+    for (uint32_t j = 0; j < kStreamItems; ++j) {
+        const uint32_t pos = t0 + j;
+        const bool in = pos < n_here;
+        left[j] = in && (j > 0 ? k[j - 1] == k[j] : (has_left && left_key == k[j]));
+        const bool right = j + 1 < kStreamItems ? (pos + 1 < n_here && k[j + 1] == k[j]) : (has_right && right_key == k[j]);
+        tie[j] = in && (left[j] || right);
+        m[j] = tie[j] ? meta[r[j]] : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < kStreamItems; ++j)
+        if (tie[j]) s_ord[j * kThreads + tid] = pair_order_key(m[j]);
+    if (tid < kHalo && n_here == kTile) {  // the run leaving the tile, into the halo
+        const uint32_t p = kTile + tid;
+        const bool eq = p < n_ext && s_key[p] == s_key[slot(kTile - 1)];
+        const uint32_t in_run = __ffs(~__ballot_sync(0xffffffffu, eq)) - 1u;  // leading equal pairs (32: all)
+        if (tid < in_run) s_ord[p] = pair_order_key(meta[s_rec[p]]);
+    }
+    // Run starts of the warp, compacted (a run entering from the previous tile is that
+    // tile's): lanes then take one run each instead of walking their own windows.
+    const uint32_t lane = tid & 31u, warp = tid >> 5;
+    uint32_t starts = 0u;
+#pragma unroll
+    for (uint32_t j = 0; j < kStreamItems; ++j) starts |= (tie[j] && !left[j]) ? (1u << j) : 0u;
+    uint32_t n_starts = __popc(starts), before = n_starts;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, before, o);
+        if (lane >= static_cast<uint32_t>(o)) before += y;
+    }
+    const uint32_t warp_runs = __shfl_sync(0xffffffffu, before, 31);
+    before -= n_starts;
+    uint16_t* runs = s_runs[warp];
+    for (uint32_t bits = starts; bits; bits &= bits - 1u) runs[before++] = static_cast<uint16_t>(t0 + __ffs(bits) - 1);
+    // First position of the tile not in the run entering from the previous tile.
+    if (tid == 0) s_enter_end = n_here;
+    if (tid < kThreads / 32) s_dirty[tid] = 0u;
+    __syncthreads();
+    if (has_prev) {
+        uint32_t first_diff = kStreamItems;
+#pragma unroll
+        for (int j = kStreamItems - 1; j >= 0; --j)
+            if (t0 + j < n_here && k[j] != prev_key) first_diff = j;
+        if (first_diff < kStreamItems) atomicMin(&s_enter_end, t0 + first_diff);
+    } else if (tid == 0) {
+        s_enter_end = 0u;
+    }
+    // Each lane sorts whole runs by (depth bits, ordinal) in shared memory (insertion sort;
+    // the halo holds a run leaving the tile, whose halo part the lane stores itself). Runs
+    // longer than kLongRun or leaving the halo are deferred to k_pair_long_runs.
+    for (uint32_t q = lane; q < warp_runs; q += 32) {
+        const uint32_t pos = runs[q];
+        const uint32_t key = s_key[slot(pos)];
+        uint32_t end = pos + 1;
+        while (end < n_ext && s_key[slot(end)] == key) ++end;
+        if ((end == n_ext && has_beyond && beyond_key == key) || end - pos > kLongRun) {
+            const uint32_t at = atomicAdd(long_count, 1u);
+            if (at < long_cap) long_runs[at] = make_uint2(cta0 + pos, end - pos);  // true end: k_pair_long_runs
+            continue;
+        }
+        bool moved = false;
+        for (uint32_t a = pos + 1; a < end; ++a) {
+            const unsigned long long oa = s_ord[slot(a)];
+            const uint32_t ra = s_rec[slot(a)];
+            uint32_t i = a;
+            while (i > pos && s_ord[slot(i - 1)] > oa) {
+                s_ord[slot(i)] = s_ord[slot(i - 1)];
+                s_rec[slot(i)] = s_rec[slot(i - 1)];
+                --i;
+            }
+            if (i != a) {
+                s_ord[slot(i)] = oa;
+                s_rec[slot(i)] = ra;
+                moved = true;
+            }
+        }
+        if (!moved) continue;
+        for (uint32_t w = pos / kStreamItems; w <= (min(end, n_here) - 1) / kStreamItems; ++w)
+            atomicOr(&s_dirty[w / 32], 1u << (w % 32));
+        for (uint32_t i = max(pos, n_here); i < end; ++i) recs[cta0 + i] = s_rec[i];  // halo part
+    }
+    __syncthreads();
+    // The windows holding a reordered run back to memory (coalesced per thread), except
+    // the run entering from the previous tile (stored by that tile, or deferred).
+    const uint32_t e0 = s_enter_end;
+    if (!((s_dirty[warp] >> lane) & 1u)) return;
+    if (n_here == kTile && t0 >= e0) {
+        uint32_t o[kStreamItems];
+#pragma unroll
+        for (uint32_t j = 0; j < kStreamItems; ++j) o[j] = s_rec[j * kThreads + tid];
+        *reinterpret_cast<uint4*>(recs + cta0 + t0) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(recs + cta0 + t0 + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+        for (uint32_t j = 0; j < kStreamItems; ++j) {
+            const uint32_t pos = t0 + j;
+            if (pos >= e0 && pos < n_here) recs[cta0 + pos] = s_rec[j * kThreads + tid];
         }
     }
 }
 
 // Runs of more than kLongRun equal key words recorded by k_cell_fixup (many pairs of one
-// truncated depth in one cell, e.g. characters stacked on one spot): one CTA per run sorts
+// truncated depth in one cell, e.g. characters stacked on one spot), and runs leaving a
+// fix-up tile's halo: one CTA per run sorts
 // ((depth bits, ordinal), record) in shared memory (bitonic, up to kPairRunCap); longer
 // runs are sorted in place in global memory.
 __global__ void __launch_bounds__(256)
-k_pair_long_runs(uint32_t* recs, const uint4* meta, const uint2* long_runs, const uint32_t* long_count, uint32_t long_cap) {
+k_pair_long_runs(const uint32_t* keys, uint32_t count, uint32_t* recs, const uint4* meta, const uint2* long_runs,
+                 const uint32_t* long_count) {
     __shared__ unsigned long long s_key[kPairRunCap];
     __shared__ uint32_t s_rec[kPairRunCap];
-    const uint32_t runs = min(*long_count, long_cap);
+    __shared__ uint32_t s_n;
+    const uint32_t runs = *long_count;  // <= the capacity sized in k_cell_fixup's contract
     for (uint32_t q = blockIdx.x; q < runs; q += gridDim.x) {
         const uint2 run = long_runs[q];
-        const uint32_t s = run.x, n = run.y;
+        const uint32_t s = run.x;
+        if (threadIdx.x == 0) {  // a run recorded at a tile's halo may continue further
+            const uint32_t k = keys[s];
+            uint32_t n = run.y;
+            while (s + n < count && keys[s + n] == k) ++n;
+            s_n = n;
+        }
+        __syncthreads();
+        const uint32_t n = s_n;
+        __syncthreads();
         uint32_t P = 1;
         while (P < n) P <<= 1;
         if (n <= kPairRunCap) {
@@ -498,7 +560,7 @@ k_pair_long_runs(uint32_t* recs, const uint4* meta, const uint2* long_runs, cons
 
 // Emit the (cell, record) pairs of every sorted splat directly in the order of the first
 // stable cell-sort pass (LSD digit = cell & dmask): a pair's position is the digit's
-// global base + this block's offset for the digit (k_sort_rows over k_sorted_spans'
+// global base + this block's offset for the digit (k_sort_rows over the count pass's
 // block histograms) + the pairs of that digit from earlier threads of the block + its
 // rank among this thread's pairs of the digit. Threads own 4 consecutive sorted splats and
 // enumerate each splat's cells row by row, so pairs of one digit keep the splat order: the
