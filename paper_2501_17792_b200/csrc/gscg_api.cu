@@ -545,9 +545,9 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             fp.mats = ctx->d_mats.as<float>();
             fp.parents = ctx->d_parents.as<int32_t>();
             fp.skin = ctx->skin.as<float>();
-            const int per_block = 16;
+            const int per_block = kFkThreads / 16;
             const uint32_t m = shard_end - shard_begin;
-            k_fk_skin<<<(m + per_block - 1) / per_block, 256, per_block * js * 16 * 4, s>>>(fp);
+            k_fk_skin<<<(m + per_block - 1) / per_block, kFkThreads, per_block * kFkSmemPerInstance(js), s>>>(fp);
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -984,6 +984,8 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_band_counts), GSCG_MAX_BANDS * sizeof(unsigned long long)));
         CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
+        CUDA_TRY(cudaFuncSetAttribute(k_fk_skin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (kFkThreads / 16) * kFkSmemPerInstance(kMaxJoints)));
         CUDA_TRY(cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
     });

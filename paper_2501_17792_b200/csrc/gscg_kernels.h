@@ -140,6 +140,8 @@ struct CopySegs {
     uint32_t words[kMaxCopySegs];
 };
 __global__ void k_copy_segments(CopySegs c);
+constexpr int kFkThreads = 128;  // k_fk_skin: 8 instances (half-warps) per block
+constexpr int kFkSmemPerInstance(int joint_stride) { return joint_stride * 52 * 4; }  // world, bind, inverse, pose
 __global__ void k_fk_skin(FkParams p);
 __global__ void k_inst_cull(CullParams p);
 __global__ void k_project(ProjectParams p);

@@ -213,23 +213,36 @@ __device__ __forceinline__ float rot_elem(const float4 q, int r, int c) {
     }
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kFkThreads)
 k_fk_skin(FkParams p) {
-    extern __shared__ float s_world[];  // [16 half-warps][kMaxJoints... joint_stride][16]
+    // Per half-warp (one instance): world[J][16], then the instance's local_bind and
+    // inverse_bind matrices and pose quaternions, staged once so the joint chain below
+    // runs from shared memory instead of paying a global-memory latency per joint.
+    extern __shared__ __align__(16) float s_world[];
     const int half = threadIdx.x >> 4;        // half-warp within the block
     const int l = threadIdx.x & 15;           // matrix element, column-major
     const int r = l & 3, c = l >> 2;
     const uint32_t inst = p.first + blockIdx.x * (blockDim.x >> 4) + half;
     const unsigned hmask = 0xffffu << ((threadIdx.x & 31) & 16);
     if (inst >= p.n) return;
-    float* world = s_world + static_cast<size_t>(half) * p.joint_stride * 16;
+    const int js = static_cast<int>(p.joint_stride);
+    float* world = s_world + static_cast<size_t>(half) * js * 52;
+    float* slb = world + js * 16;
+    float* sib = slb + js * 16;
+    float* sq = sib + js * 16;
 
     const TemplateDev tpl = p.templates[p.template_ids[inst]];
     const int J = tpl.joint_count;
-    const float* lb = p.mats + static_cast<size_t>(tpl.mat_offset) * 16;
-    const float* ib = lb + static_cast<size_t>(J) * 16;
+    const float4* lb = reinterpret_cast<const float4*>(p.mats + static_cast<size_t>(tpl.mat_offset) * 16);
+    const float4* ib = lb + static_cast<size_t>(J) * 4;
     const int32_t* parents = p.parents + tpl.parent_offset;
     const float* pose = p.poses + static_cast<size_t>(inst) * p.pose_stride;
+    for (int k = l; k < J * 4; k += 16) {  // all loads in flight at once
+        reinterpret_cast<float4*>(slb)[k] = lb[k];
+        reinterpret_cast<float4*>(sib)[k] = ib[k];
+    }
+    for (int k = l; k < J * 4; k += 16) sq[k] = pose[4 + k];
+    __syncwarp(hmask);
 
     // Root transform (crowd.cpp:20-30) and root offset T(root_translation).
     const float x = p.placement[4 * inst + 0], z = p.placement[4 * inst + 1];
@@ -253,8 +266,8 @@ k_fk_skin(FkParams p) {
 
     float* out = p.skin + static_cast<size_t>(inst) * p.joint_stride * 12;
     for (int j = 0; j < J; ++j) {
-        const float4 q = *reinterpret_cast<const float4*>(pose + 4 + 4 * j);
-        const float* LB = lb + j * 16;
+        const float4 q = reinterpret_cast<const float4*>(sq)[j];
+        const float* LB = slb + j * 16;
         // local = local_bind[j] * rotation_matrix(q)
         const float local = chain4(LB[0 * 4 + r], LB[1 * 4 + r], LB[2 * 4 + r], LB[3 * 4 + r],
                                    rot_elem(q, 0, c), rot_elem(q, 1, c), rot_elem(q, 2, c),
@@ -281,7 +294,7 @@ k_fk_skin(FkParams p) {
         world[j * 16 + l] = wv;
         __syncwarp(hmask);
         // skin = world[j] * inverse_bind[j]
-        const float* IB = ib + j * 16;
+        const float* IB = sib + j * 16;
         const float* W = world + j * 16;
         const float sv = chain4(W[0 * 4 + r], W[1 * 4 + r], W[2 * 4 + r], W[3 * 4 + r],
                                 IB[c * 4 + 0], IB[c * 4 + 1], IB[c * 4 + 2], IB[c * 4 + 3]);
