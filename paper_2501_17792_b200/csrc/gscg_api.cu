@@ -5,7 +5,7 @@
 //   H2D of the frame records (pinned staging, one copy)
 //   update:    k_fk_skin -> k_inst_cull -> k_lod_plan (1 CTA)
 //   gather:    k_project (persistent, template-major)       -> counters readback (sync)
-//   sort:      splats by the top <= 28 varying depth bits (k_sort_{upsweep,rows,downsweep}_wide x P) ->
+//   sort:      splats by the top <= 25 varying depth bits (k_sort_{upsweep,rows,downsweep} x P) ->
 //              spans in sorted order (k_sorted_spans) ->
 //              pairs scattered in first-cell-pass order, keys tagged with the truncated depth
 //              (k_emit_scatter count, k_sort_rows, k_emit_scatter scatter) ->
@@ -73,10 +73,9 @@ struct DevBuf {
     }
 };
 
-// Varying depth bits the splat sort orders (4 wide LSD passes of <= 7 bits); lower bits and
+// Varying depth bits the splat sort orders (LSD passes of <= 5 bits); the lower bits and
 // the ordinal tie-break are settled per cell by k_cell_fixup.
-constexpr uint32_t kDepthSortBits = 22;
-constexpr uint32_t kDepthWidePasses = 1;
+constexpr uint32_t kDepthSortBits = 25;
 
 struct LevelStore {
     uint32_t count = 0;
@@ -153,7 +152,6 @@ struct gscg_ctx {
     uint64_t splat_capacity = 0, pair_capacity = 0;
     uint32_t culled = 0;  // instances dropped by k_inst_cull in the last frame
     uint32_t depth_sort_bits = kDepthSortBits;  // top varying depth bits the splat sort orders
-    uint32_t depth_wide_passes = kDepthWidePasses;  // of which the first passes take 7-bit digits
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
@@ -337,7 +335,6 @@ void refresh_power_floor(gscg_ctx* ctx, float cutoff) {
 
 // Digit layout of one LSD sort: pass q sorts bits [shift[q], shift[q] + bits[q]).
 struct RadixPlan {
-    uint32_t wide = 0;  // bit q: pass q uses the 7-bit digit kernels (k_sort_*_wide), else 5-bit
     uint32_t passes = 0;
     uint32_t shift[kMaxSortPasses] = {};
     uint32_t bits[kMaxSortPasses] = {};
@@ -705,12 +702,9 @@ int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, D
         sp.tiles = tiles;
         sp.counts = ctx->status.as<uint32_t>();
         sp.digit_base = ctx->hist.as<uint32_t>();
-        const bool wide = (plan.wide >> q) & 1u;
-        if (wide) k_sort_upsweep_wide<<<tiles, kSortThreads, 0, s>>>(sp);
-        else k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+        k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
         k_sort_rows<<<1u << plan.bits[q], 1024, 0, s>>>(sp);
-        if (wide) k_sort_downsweep_wide<<<tiles, kSortThreads, 0, s>>>(sp);
-        else k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+        k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
         launches += 3;
         out ^= 1;
     }
@@ -718,28 +712,19 @@ int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, D
     return out ^ 1;
 }
 
-// ceil(bits / 5) passes (wide: ceil(bits / 7)) with the bits spread evenly (27 -> 5,5,5,4,4,4;
-// wide 26 -> 7,7,6,6). 8-bit digits ranked with warp match (CUB onesweep style) measured
-// slower here: __match_any_sync is slow on sm_100 (upsweep 74 vs 31 us, downsweep 126 vs 77
-// us per pass); the wide passes rank with ballots and shared-memory warp counters.
-RadixPlan make_plan(uint32_t bits, uint32_t wide_passes = 0) {
+// ceil(bits / 5) passes with the bits spread evenly (27 -> 5,5,5,4,4,4). 8-bit digits
+// ranked with warp match (CUB onesweep style) measured slower here: __match_any_sync is
+// slow on sm_100 (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
+RadixPlan make_plan(uint32_t bits) {
     RadixPlan pl{};
     bits = std::max(bits, 1u);
-    // Up to wide_passes passes of <= 7 bits first, then passes of <= 5 bits.
-    uint32_t w = std::min(wide_passes, (bits + kWideBits - 1) / kWideBits);
-    const uint32_t wide_bits = std::min(bits, w * kWideBits);
-    const uint32_t narrow = (bits - wide_bits + kRadixBits - 1) / kRadixBits;
-    pl.passes = w + narrow;
+    pl.passes = (bits + kRadixBits - 1) / kRadixBits;
     uint32_t sh = 0;
     for (uint32_t q = 0; q < pl.passes; ++q) {
-        const bool wq = q < w;
-        const uint32_t left = wq ? wide_bits - sh : bits - sh;
-        const uint32_t n = wq ? w - q : pl.passes - q;
-        const uint32_t width = left / n + (left % n ? 1u : 0u);
+        const uint32_t w = (bits - sh) / (pl.passes - q) + ((bits - sh) % (pl.passes - q) ? 1u : 0u);
         pl.shift[q] = sh;
-        pl.bits[q] = width;
-        if (wq) pl.wide |= 1u << q;
-        sh += width;
+        pl.bits[q] = w;
+        sh += w;
     }
     return pl;
 }
@@ -747,8 +732,8 @@ RadixPlan make_plan(uint32_t bits, uint32_t wide_passes = 0) {
 void ensure_sort_buffers(gscg_ctx* ctx, uint32_t splats, uint32_t pairs) {
     const uint32_t max_elems = std::max(splats, pairs);
     const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
-    CUDA_TRY(ctx->status.ensure(std::max<size_t>(max_tiles, 1) * kWideRadix * 4));  // tile digit counts
-    CUDA_TRY(ctx->hist.ensure(kWideRadix * 4));                                        // digit bases
+    CUDA_TRY(ctx->status.ensure(std::max<size_t>(max_tiles, 1) * kRadix * 4));  // tile digit counts
+    CUDA_TRY(ctx->hist.ensure(kRadix * 4));                                        // digit bases
     for (int b = 0; b < 2; ++b) {
         CUDA_TRY(ctx->skeys[b].ensure(std::max<size_t>(splats, 1) * 4));
         CUDA_TRY(ctx->srecs[b].ensure(std::max<size_t>(splats, 1) * 4));
@@ -803,7 +788,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         const uint32_t drop = dbits > ctx->depth_sort_bits ? dbits - ctx->depth_sort_bits : 0u;
         RadixPlan dplan{};
         if (!presorted) {
-            dplan = make_plan(dbits - drop, ctx->depth_wide_passes);
+            dplan = make_plan(dbits - drop);
             for (uint32_t q = 0; q < dplan.passes; ++q) dplan.shift[q] += drop;
         }
         const int sb = presorted ? 0
@@ -989,10 +974,6 @@ int gscg_create(int device, gscg_ctx** out) {
         if (const char* e = std::getenv("GSCG_DEPTH_SORT_BITS")) {  // tuning knob (see kDepthSortBits)
             const int v = std::atoi(e);
             if (v >= 1 && v <= 32) ctx->depth_sort_bits = static_cast<uint32_t>(v);
-        }
-        if (const char* e = std::getenv("GSCG_DEPTH_WIDE_PASSES")) {
-            const int v = std::atoi(e);
-            if (v >= 0 && v <= 8) ctx->depth_wide_passes = static_cast<uint32_t>(v);
         }
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
