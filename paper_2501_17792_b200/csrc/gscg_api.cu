@@ -335,6 +335,7 @@ void refresh_power_floor(gscg_ctx* ctx, float cutoff) {
 
 // Digit layout of one LSD sort: pass q sorts bits [shift[q], shift[q] + bits[q]).
 struct RadixPlan {
+    uint32_t wide = 0;  // bit q: pass q uses the 7-bit digit kernels (k_sort_*_wide), else 5-bit
     uint32_t passes = 0;
     uint32_t shift[kMaxSortPasses] = {};
     uint32_t bits[kMaxSortPasses] = {};
@@ -702,9 +703,12 @@ int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, D
         sp.tiles = tiles;
         sp.counts = ctx->status.as<uint32_t>();
         sp.digit_base = ctx->hist.as<uint32_t>();
-        k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+        const bool wide = (plan.wide >> q) & 1u;
+        if (wide) k_sort_upsweep_wide<<<tiles, kSortThreads, 0, s>>>(sp);
+        else k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
         k_sort_rows<<<1u << plan.bits[q], 1024, 0, s>>>(sp);
-        k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+        if (wide) k_sort_downsweep_wide<<<tiles, kSortThreads, 0, s>>>(sp);
+        else k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
         launches += 3;
         out ^= 1;
     }
@@ -712,19 +716,35 @@ int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, D
     return out ^ 1;
 }
 
-// ceil(bits / 5) passes with the bits spread evenly (27 -> 5,5,5,4,4,4). 8-bit digits
-// ranked with warp match (CUB onesweep style) measured slower here: __match_any_sync is
-// slow on sm_100 (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
+// The cheapest LSD plan for `bits` key bits: w wide passes (<= 7 bits, ~1.36x the cost of
+// a 5-bit pass on this B200) then n 5-bit passes, minimising 1.36 w + n; bits spread evenly
+// within each kind (27 -> 7,5,5,5,5; 25 -> 5,5,5,5,5; 12 -> 7,5). 8-bit digits ranked with
+// warp match (CUB onesweep style) measured slower here: __match_any_sync is slow on sm_100
+// (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
 RadixPlan make_plan(uint32_t bits) {
     RadixPlan pl{};
     bits = std::max(bits, 1u);
-    pl.passes = (bits + kRadixBits - 1) / kRadixBits;
+    uint32_t best_w = 0, best_n = (bits + kRadixBits - 1) / kRadixBits;
+    for (uint32_t w = 1; w * kWideBits < bits + kWideBits; ++w) {
+        const uint32_t rest = bits > w * kWideBits ? bits - w * kWideBits : 0u;
+        const uint32_t n = (rest + kRadixBits - 1) / kRadixBits;
+        if (136 * w + 100 * n < 136 * best_w + 100 * best_n) {
+            best_w = w;
+            best_n = n;
+        }
+    }
+    pl.passes = best_w + best_n;
+    const uint32_t wide_bits = std::min(bits, best_w * static_cast<uint32_t>(kWideBits));
     uint32_t sh = 0;
     for (uint32_t q = 0; q < pl.passes; ++q) {
-        const uint32_t w = (bits - sh) / (pl.passes - q) + ((bits - sh) % (pl.passes - q) ? 1u : 0u);
+        const bool wq = q < best_w;
+        const uint32_t left = wq ? wide_bits - sh : bits - sh;
+        const uint32_t k = wq ? best_w - q : pl.passes - q;
+        const uint32_t width = left / k + (left % k ? 1u : 0u);
         pl.shift[q] = sh;
-        pl.bits[q] = w;
-        sh += w;
+        pl.bits[q] = width;
+        if (wq) pl.wide |= 1u << q;
+        sh += width;
     }
     return pl;
 }
@@ -732,8 +752,8 @@ RadixPlan make_plan(uint32_t bits) {
 void ensure_sort_buffers(gscg_ctx* ctx, uint32_t splats, uint32_t pairs) {
     const uint32_t max_elems = std::max(splats, pairs);
     const uint32_t max_tiles = (max_elems + kSortTile - 1) / kSortTile;
-    CUDA_TRY(ctx->status.ensure(std::max<size_t>(max_tiles, 1) * kRadix * 4));  // tile digit counts
-    CUDA_TRY(ctx->hist.ensure(kRadix * 4));                                        // digit bases
+    CUDA_TRY(ctx->status.ensure(std::max<size_t>(max_tiles, 1) * kWideRadix * 4));  // tile digit counts
+    CUDA_TRY(ctx->hist.ensure(kWideRadix * 4));                                        // digit bases
     for (int b = 0; b < 2; ++b) {
         CUDA_TRY(ctx->skeys[b].ensure(std::max<size_t>(splats, 1) * 4));
         CUDA_TRY(ctx->srecs[b].ensure(std::max<size_t>(splats, 1) * 4));
@@ -797,10 +817,10 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         // 2. cell spans in sorted order; the first cell-sort digit histogram per emission
         //    block; digit offsets; pairs emitted straight into the order of the first stable
         //    cell-sort pass, each key word tagged with its splat's truncated depth.
-        const RadixPlan cplan = make_plan(static_cast<uint32_t>(bits_for(cells - 1)));
         const uint32_t cell_bits = std::max(1, bits_for(cells - 1));
         const uint32_t cell_mask = cell_bits >= 32 ? 0xffffffffu : (1u << cell_bits) - 1u;
-        const uint32_t dmask = (1u << cplan.bits[0]) - 1u;
+        const uint32_t emit_bits = std::min<uint32_t>(cell_bits, kRadixBits);  // the first pass, folded into emission
+        const uint32_t dmask = (1u << emit_bits) - 1u;
         const uint32_t eblocks = (S32 + kEmitSplats - 1) / kEmitSplats;  // emission blocks
         CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
@@ -815,7 +835,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         bp.counts = ctx->block_sums.as<uint32_t>();
         bp.digit_base = ctx->hist.as<uint32_t>();
         bp.tiles = eblocks;
-        bp.bits = cplan.bits[0];
+        bp.bits = emit_bits;
         k_sort_rows<<<dmask + 1, 1024, 0, s>>>(bp);
         launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), geo.tiles_x, quads, dmask, drop, cell_bits,
@@ -824,10 +844,9 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         CUDA_TRY(cudaGetLastError());
         // 3. the remaining stable cell-sort passes (cell bits only; the tags ride along).
         RadixPlan rest{};
-        for (uint32_t q = 1; q < cplan.passes; ++q) {
-            rest.shift[rest.passes] = cplan.shift[q];
-            rest.bits[rest.passes] = cplan.bits[q];
-            ++rest.passes;
+        if (cell_bits > emit_bits) {
+            rest = make_plan(cell_bits - emit_bits);
+            for (uint32_t q = 0; q < rest.passes; ++q) rest.shift[q] += emit_bits;
         }
         const int cb = rest.passes ? run_radix(ctx, ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(),
                                                ctx->pcell, ctx->precs, K, rest, launches)
@@ -850,7 +869,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         }
         CUDA_TRY(cudaGetLastError());
         ctx->final_recs = ctx->precs[cb].as<uint32_t>();
-        passes = dplan.passes + cplan.passes;
+        passes = dplan.passes + 1 + rest.passes;
     }
     CUDA_TRY(cudaEventRecord(ctx->ev[4], s));
 

@@ -173,6 +173,10 @@ struct SortPassParams {
 __global__ void k_sort_upsweep(SortPassParams p);
 __global__ void k_sort_rows(SortPassParams p);
 __global__ void k_sort_downsweep(SortPassParams p);
+constexpr int kWideBits = 7;  // digit bits of the wide passes
+constexpr int kWideRadix = 1 << kWideBits;
+__global__ void k_sort_upsweep_wide(SortPassParams p);
+__global__ void k_sort_downsweep_wide(SortPassParams p);
 
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
 __global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted);

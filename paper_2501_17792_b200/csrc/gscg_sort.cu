@@ -249,6 +249,160 @@ __device__ __forceinline__ void for_each_cell(uint2 sp, int tiles_x, int quads, 
 
 }  // namespace
 
+// Wide-digit passes (up to kWideBits = 7 bits, 128 digits): the LSD plans use one where it
+// saves a pass (a wide pass costs ~1.36x a 5-bit pass), e.g. the 12 cell bits left after
+// emission at 3840x2160 take 7 + 5 instead of 4 + 4 + 4. Ranking keeps the ballot
+// multisplit (one ballot per digit bit gives each key the lanes sharing its digit); the
+// warp's running count per digit lives in shared memory (128 counters per warp, read by
+// every lane of a digit group, advanced by the group's highest lane) instead of in lane
+// registers.
+namespace {
+
+__device__ __forceinline__ uint32_t peers_of(uint32_t d, int bits, uint32_t valid) {
+    uint32_t peers = valid;
+#pragma unroll
+    for (int b = 0; b < kWideBits; ++b) {
+        if (b < bits) {
+            const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? bb : ~bb;
+        }
+    }
+    return peers;
+}
+
+// Exclusive scan of v over the first 128 threads (4 warps); s_tmp holds 4 words.
+__device__ __forceinline__ uint32_t scan128(uint32_t v, uint32_t* s_tmp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t x = warp_incl_scan(v, lane);
+    if (threadIdx.x < kWideRadix && lane == 31) s_tmp[warp] = x;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp && w < kWideRadix / 32; ++w) off += s_tmp[w];
+    __syncthreads();
+    return off + x - v;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kSortThreads)
+k_sort_upsweep_wide(SortPassParams p) {
+    __shared__ uint32_t s_hist[kSortWarps][kWideRadix];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kSortWarps * kWideRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0u;
+    const uint32_t base = blockIdx.x * kSortTile;
+    const uint32_t mask = (1u << p.bits) - 1u;
+    const int bits = static_cast<int>(p.bits);
+    uint32_t k[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
+        k[j] = idx < p.count ? p.keys_in[idx] : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
+        const uint32_t d = (k[j] >> p.shift) & mask;
+        const uint32_t peers = peers_of(d, bits, __ballot_sync(0xffffffffu, idx < p.count));
+        if (idx < p.count && lane == 31 - __clz(peers)) s_hist[warp][d] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x < kWideRadix) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) t += s_hist[w][threadIdx.x];
+        if (static_cast<uint32_t>(threadIdx.x) <= mask) p.counts[threadIdx.x * p.tiles + blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads, 3)
+k_sort_downsweep_wide(SortPassParams p) {
+    __shared__ uint32_t s_keys[kSortTile];
+    __shared__ uint16_t s_perm[kSortTile];  // tile-local source index of each staged key
+    __shared__ uint32_t s_woff[kSortWarps][kWideRadix];
+    __shared__ uint32_t s_block_excl[kWideRadix];
+    __shared__ uint32_t s_global[kWideRadix];
+    __shared__ uint32_t s_tmp[kWideRadix / 32];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t mask = (1u << p.bits) - 1u;
+    const int bits = static_cast<int>(p.bits);
+    for (int i = tid; i < kSortWarps * kWideRadix; i += blockDim.x) (&s_woff[0][0])[i] = 0u;
+    const uint32_t base = blockIdx.x * kSortTile;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t k[kSortItems], rank[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
+        k[j] = idx < p.count ? p.keys_in[idx] : 0u;
+    }
+    {  // global digit base (exclusive scan of the row totals) + this tile's offset
+        const uint32_t total = tid < kWideRadix && static_cast<uint32_t>(tid) <= mask ? p.digit_base[tid] : 0u;
+        const uint32_t excl = scan128(total, s_tmp);  // contains the block barrier for s_woff
+        if (tid < kWideRadix)
+            s_global[tid] = excl + (static_cast<uint32_t>(tid) <= mask ? p.counts[tid * p.tiles + blockIdx.x] : 0u);
+    }
+    uint32_t* wcnt = s_woff[warp];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
+        const uint32_t d = (k[j] >> p.shift) & mask;
+        const uint32_t peers = peers_of(d, bits, __ballot_sync(0xffffffffu, idx < p.count));
+        const uint32_t before = wcnt[d];
+        rank[j] = before + __popc(peers & lt);
+        __syncwarp();
+        if (idx < p.count && lane == 31 - __clz(peers)) wcnt[d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    uint32_t run = 0;
+    if (tid < kWideRadix) {  // digit tid: exclusive over warps
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t c = s_woff[w][tid];
+            s_woff[w][tid] = run;
+            run += c;
+        }
+    }
+    const uint32_t bex = scan128(tid < kWideRadix ? run : 0u, s_tmp);  // over digits
+    if (tid < kWideRadix) s_block_excl[tid] = bex;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
+        if (base + local < p.count) {
+            const uint32_t d = (k[j] >> p.shift) & mask;
+            const uint32_t pos = s_block_excl[d] + s_woff[warp][d] + rank[j];
+            s_keys[pos] = k[j];
+            s_perm[pos] = static_cast<uint16_t>(local);
+        }
+    }
+    __syncthreads();
+    const uint32_t n_here = p.count > base ? min(kSortTile, p.count - base) : 0u;
+    const uint32_t* __restrict__ vals_in = p.vals_in;
+    uint32_t okey[kSortItems], opos[kSortItems], oval[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t e = tid + j * kSortThreads;
+        if (e < n_here) {
+            okey[j] = s_keys[e];
+            const uint32_t dd = (okey[j] >> p.shift) & mask;
+            opos[j] = s_global[dd] + (e - s_block_excl[dd]);
+            const uint32_t src = base + s_perm[e];
+            oval[j] = vals_in ? __ldg(vals_in + src) : src;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const uint32_t e = tid + j * kSortThreads;
+        if (e < n_here) {
+            p.keys_out[opos[j]] = okey[j];
+            p.vals_out[opos[j]] = oval[j];
+        }
+    }
+}
+
 // After the depth sort: every sorted splat's binning span, gathered into sorted order
 // (one 16-byte meta gather per splat, all eight of a thread in flight).
 __global__ void __launch_bounds__(kMetaThreads)
