@@ -131,9 +131,9 @@ def test_moving_one_instance_changes_only_its_footprint():
 
 def test_long_equal_depth_runs_are_ordered_by_ordinal():
     """Stacked same-pose characters give every template Gaussian one depth per stack, so
-    the depth sort sees equal-key runs of each stack's size: <= 32 (k_sorted_spans in
-    registers), <= 256 (k_long_runs_warp), <= 4096 (k_long_runs, shared memory) and
-    beyond (k_long_runs, global bitonic). The reference orders ties by (instance,
+    every cell holds runs of equal (cell, depth) pairs of each stack's size: <= 32
+    (k_cell_fixup, shared memory), <= 2048 (k_pair_long_runs, shared-memory bitonic) and
+    beyond (k_pair_long_runs, global bitonic). The reference orders ties by (instance,
     gaussian) (renderer.cpp:91-96)."""
     cfg = P.SceneConfig(template_count=1, template_seed_base=5, level_counts=(24, 12, 6), with_sh=False,
                         motion_count=1, motion_frames=8, grid_rows=1, grid_cols=1, crowd_count=1, crowd_seed=1,
@@ -159,6 +159,17 @@ def test_long_equal_depth_runs_are_ordered_by_ordinal():
     r.render_frame(0.0, P.RenderSettings(), True, 0)
     _, run_len = np.unique(r.splat_records()["depth"], return_counts=True)
     assert run_len.max() >= 4097
+
+
+@pytest.mark.parametrize("bits", [6, 12, 18])
+def test_truncated_depth_sort_is_exact(bits, monkeypatch):
+    """The splat sort orders only the top GSCG_DEPTH_SORT_BITS varying depth bits; the
+    per-cell fix-up restores the full (depth bits, instance, gaussian) order. Few sorted
+    bits make most pairs tie inside their cells (long runs through k_pair_long_runs),
+    and every per-cell list must still equal the oracle's bins."""
+    monkeypatch.setenv("GSCG_DEPTH_SORT_BITS", str(bits))
+    rep = parity(basic_scene(count=48, rows=6, cols=8), 0.6)
+    assert rep["K"] > 0
 
 
 def test_repeated_frames_are_byte_identical():
