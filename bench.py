@@ -354,12 +354,14 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         from paper_2501_17792_b200.multigpu import DistributedRenderer
         drr = DistributedRenderer(scene, local_rank, exchange=ex, band=br)
 
-        def e2e_frame(f):
-            drr.render_frame(times_s[f], settings, forced_lod=forced)
+        band_out = (torch.empty((cfg.height, cfg.width, 3), dtype=torch.float32, pin_memory=True).numpy(), None)
+
+        def e2e_frame(f):  # colour read-back into page-locked memory, as the single-GPU leg
+            drr.render_frame(times_s[f], settings, forced_lod=forced, out=band_out)
 
         e2e_fps = time_e2e(e2e_frame)
     h2d = n * (4 + 16 + 4 + 4 + 4)  # template id, placement, previous LoD, motion id, phase offset
-    d2h = cfg.width * cfg.height * (12 if not band_path else 16) + n * 4
+    d2h = cfg.width * cfg.height * 12 + n * 4
 
     if dist:
         tot = torch.tensor([float(counts[1])], dtype=torch.float64, device=dev)

@@ -339,13 +339,14 @@ class DistributedRenderer:
         self.balance_every = 4  # frames between load-balance observations (each reads back small state)
 
     def render_frame(self, time_s: float, settings=None, static_pose: bool = False,
-                     forced_lod: Optional[int] = None, rows: Optional[Sequence[int]] = None):
-        """Returns (rgb, T) numpy on rank 0, None on the other ranks."""
+                     forced_lod: Optional[int] = None, rows: Optional[Sequence[int]] = None, out=None):
+        """Returns (rgb, T) numpy on rank 0, None on the other ranks. `out` = (rgb, T) host
+        arrays to fill (page-locked ones read back at full DMA speed); T may be None for a
+        colour-only read-back, as in Renderer.render_frame."""
         import torch
         import paper_2501_17792_b200 as P
 
         settings = settings or P.RenderSettings()
-        cfg = self.scene.cfg
         n = self.scene.counts()[2]
         if self.balancer is None or self.balancer.tile != settings.tile_size:
             self.balancer = LoadBalancer(self.scene, self.world, settings.tile_size)
@@ -355,22 +356,25 @@ class DistributedRenderer:
         fa = FrameArgs(time_s, static_pose, forced_lod)
         self.band.project(fa, settings, shard, rows)
         send = self.band.pack()
+        want_T = out is None or out[1] is not None
         with torch.cuda.stream(self.band.stream()):
             recv, rc = self.exchange.all_to_all(send, self.band.counts.tolist())
             rgb, T = self.band.render_band(recv, sum(rc), rows[self.rank], rows[self.rank + 1])
-            full = self.exchange.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
+            full_rgb = self.exchange.gather_rows(rgb, rows)
+            full_T = self.exchange.gather_rows(T, rows) if want_T else None
             self._frames = getattr(self, "_frames", 0) + 1
             if self._frames % self.balance_every == 1 or self.balance_every == 1:
                 self.balancer.observe(self.band.lods[:n], self.band.band_row_pairs(),
                                       rows[self.rank] // settings.tile_size, self.exchange)
-            if full is None:
+            if full_rgb is None:
                 return None
-            # one read-back into page-locked memory, then split into the API's two arrays
-            if getattr(self, "_pinned", None) is None or self._pinned.shape != full.shape:
-                self._pinned = torch.empty(full.shape, dtype=full.dtype, pin_memory=True)
-            self._pinned.copy_(full)
-        host = self._pinned.numpy()
-        return np.ascontiguousarray(host[..., :3]), np.ascontiguousarray(host[..., 3])
+            if out is None:
+                out = (np.empty(tuple(full_rgb.shape), np.float32), np.empty(tuple(full_T.shape), np.float32))
+            # straight into the caller's arrays: no staging copy, no host-side reshuffle
+            torch.from_numpy(out[0]).copy_(full_rgb)
+            if want_T:
+                torch.from_numpy(out[1]).copy_(full_T)
+        return out
 
 
 def render_frame_virtual(ranks: list[BandRank], time_s: float, settings=None, static_pose: bool = False,
