@@ -278,7 +278,8 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
             with torch.cuda.stream(stream):
                 recv, rc = ex.all_to_all(send, br.counts.tolist())
                 rgb, T = br.render_band(recv, sum(rc), rows[rank], rows[rank + 1])
-                ex.gather_rows(torch.cat([rgb, T[..., None]], dim=2), rows)
+                ex.gather_rows(rgb, rows)  # the bands assembled into the full frame on rank 0
+                ex.gather_rows(T, rows)
                 if f % 4 == 0:  # re-balance every 4th frame (the observation reads back LoDs and cell ranges)
                     balancer.observe(d_lods[:n].cpu().numpy(), br.band_row_pairs(), rows[rank] // settings.tile_size, ex)
             a, b = br.shard_times, br.band_times
