@@ -163,6 +163,19 @@ struct gscg_ctx {
     // read-back of fb_rgb/fb_T (the _alt members travel with their buffer).
     DevBuf fb_rgb_alt, fb_T_alt;
     cudaEvent_t rb_ev = nullptr, rb_ev_alt = nullptr;
+    // A pipelined frame's read-back is enqueued by the next call once that frame's
+    // mid-frame read-back of its counters is done (flush_readback): the 25 MB copy then
+    // runs under the next frame's sort and raster instead of delaying, on the same PCIe
+    // link, the next frame's input staging and counter read-back.
+    struct PendingReadback {
+        bool active = false;
+        float *dst_rgb = nullptr, *dst_T = nullptr;
+        const float *src_rgb = nullptr, *src_T = nullptr;
+        size_t rgb_bytes = 0, T_bytes = 0;
+        cudaEvent_t done = nullptr;  // the frame's raster finished (on the context stream)
+        cudaEvent_t rb = nullptr;    // recorded when the read-back has landed
+    } pending;
+    cudaEvent_t pend_ev = nullptr;
     // debug
     DevBuf posed_dbg, rec_dbg;
 
@@ -404,6 +417,8 @@ void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_came
 // instances [shard_begin, shard_end); sets S, K, G and the depth-bit range. Events 0..3.
 // lod_back: host frames get active_lod back with the mid-frame counter read-back (the LoD
 // is final after k_lod_plan), so the frame's end needs no host synchronisation for it.
+void flush_readback(gscg_ctx* ctx);
+
 void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
                    const gscg_lod_policy* lod, uint32_t shard_begin, uint32_t shard_end, uint32_t& launches,
                    bool lod_back = false) {
@@ -660,6 +675,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             CUDA_TRY(cudaGetLastError());
         }
         CUDA_TRY(cudaStreamSynchronize(s));
+        flush_readback(ctx);  // the previous pipelined frame's read-back now overlaps this frame's sort
         const uint64_t S = ctx->h_counters->splat_pair >> 32;
         const uint64_t K = ctx->h_counters->splat_pair & 0xffffffffull;
         if (S <= ctx->splat_capacity && K <= ctx->pair_capacity) {
@@ -778,12 +794,24 @@ bool is_host_pointer(const void* p) {
 // depth sort is skipped (rasterize_splats: bins follow the given order).
 // pipelined: render into the other framebuffer and leave its read-back running on the
 // copy stream (gscg_render_frame_async).
+// Enqueues a deferred pipelined read-back (see gscg_ctx::pending) on the copy stream.
+void flush_readback(gscg_ctx* ctx) {
+    auto& p = ctx->pending;
+    if (!p.active) return;
+    p.active = false;
+    CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, p.done, 0));
+    if (p.dst_rgb) CUDA_TRY(cudaMemcpyAsync(p.dst_rgb, p.src_rgb, p.rgb_bytes, cudaMemcpyDefault, ctx->copy_stream));
+    if (p.dst_T) CUDA_TRY(cudaMemcpyAsync(p.dst_T, p.src_T, p.T_bytes, cudaMemcpyDefault, ctx->copy_stream));
+    CUDA_TRY(cudaEventRecord(p.rb, ctx->copy_stream));
+}
+
 uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& launches, float* read_rgb = nullptr,
                      float* read_T = nullptr, bool presorted = false, bool pipelined = false) {
     cudaStream_t s = ctx->stream;
     const FrameGeom& geo = ctx->geom;
     const uint32_t tiles = static_cast<uint32_t>(geo.tiles_x) * static_cast<uint32_t>(tile_rows);
     const uint32_t cells = tiles * geo.cells_per_tile;
+    flush_readback(ctx);
     if (pipelined) {
         std::swap(ctx->fb_rgb, ctx->fb_rgb_alt);
         std::swap(ctx->fb_T, ctx->fb_T_alt);
@@ -908,10 +936,24 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                 bp.tile_row0 = tile_row0 + r0;
                 launch_raster(bp, static_cast<uint32_t>((r1 - r0) * geo.tiles_x), s);
                 ++launches;
-                CUDA_TRY(cudaEventRecord(ctx->band_ev[b], s));
-                CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_ev[b], 0));
                 const int y0 = r0 * geo.ts, y1 = std::min(r1 * geo.ts, geo.H - tile_row0 * geo.ts);
                 const size_t off = static_cast<size_t>(y0) * row_floats, n = static_cast<size_t>(y1 - y0) * row_floats;
+                if (pipelined) {  // deferred to the next call (flush_readback)
+                    CUDA_TRY(cudaEventRecord(ctx->pend_ev, s));
+                    auto& pr = ctx->pending;
+                    pr.active = true;
+                    pr.dst_rgb = read_rgb ? read_rgb + 3 * off : nullptr;
+                    pr.dst_T = read_T ? read_T + off : nullptr;
+                    pr.src_rgb = ctx->fb_rgb.as<float>() + 3 * off;
+                    pr.src_T = ctx->fb_T.as<float>() + off;
+                    pr.rgb_bytes = n * 12;
+                    pr.T_bytes = n * 4;
+                    pr.done = ctx->pend_ev;
+                    pr.rb = ctx->rb_ev;  // gscg_wait_readback waits on rb_ev
+                    continue;
+                }
+                CUDA_TRY(cudaEventRecord(ctx->band_ev[b], s));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_ev[b], 0));
                 if (read_rgb)
                     CUDA_TRY(cudaMemcpyAsync(read_rgb + 3 * off, ctx->fb_rgb.as<float>() + 3 * off, n * 12,
                                              cudaMemcpyDefault, ctx->copy_stream));
@@ -919,10 +961,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                     CUDA_TRY(cudaMemcpyAsync(read_T + off, ctx->fb_T.as<float>() + off, n * 4, cudaMemcpyDefault,
                                              ctx->copy_stream));
             }
-            if (pipelined) {
-                // The read-back overlaps the next frame; gscg_wait_readback waits on rb_ev.
-                CUDA_TRY(cudaEventRecord(ctx->rb_ev, ctx->copy_stream));
-            } else {
+            if (!pipelined) {
                 // The frame's stream resumes only after the read-back (ordering for the caller).
                 CUDA_TRY(cudaEventRecord(ctx->band_ev[kReadbackBands - 1], ctx->copy_stream));
                 CUDA_TRY(cudaStreamWaitEvent(s, ctx->band_ev[kReadbackBands - 1], 0));
@@ -999,6 +1038,7 @@ int gscg_create(int device, gscg_ctx** out) {
         for (auto& e : ctx->band_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->rb_ev, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->rb_ev_alt, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->pend_ev, cudaEventDisableTiming));
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_band_counts), GSCG_MAX_BANDS * sizeof(unsigned long long)));
@@ -1016,7 +1056,13 @@ int gscg_destroy(gscg_ctx* ctx) {
     if (!ctx) return GSCG_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);  // pipelined read-backs
+    if (ctx->copy_stream) {
+        try {
+            flush_readback(ctx);  // a deferred pipelined read-back still lands
+        } catch (...) {
+        }
+        cudaStreamSynchronize(ctx->copy_stream);  // pipelined read-backs
+    }
     for (TemplateStore& t : ctx->templates)
         for (LevelStore& l : t.levels) {
             l.core.release();
@@ -1045,6 +1091,7 @@ int gscg_destroy(gscg_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->rb_ev) cudaEventDestroy(ctx->rb_ev);
     if (ctx->rb_ev_alt) cudaEventDestroy(ctx->rb_ev_alt);
+    if (ctx->pend_ev) cudaEventDestroy(ctx->pend_ev);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1277,6 +1324,7 @@ int gscg_render_frame_async(gscg_ctx* ctx, const gscg_frame_desc* frame, const g
 int gscg_wait_readback(gscg_ctx* ctx, uint32_t frames_back) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
+        flush_readback(ctx);
         if (frames_back == 0) CUDA_TRY(cudaEventSynchronize(ctx->rb_ev));
         else if (frames_back == 1) CUDA_TRY(cudaEventSynchronize(ctx->rb_ev_alt));
     });
@@ -1764,6 +1812,7 @@ int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T) {
 int gscg_synchronize(gscg_ctx* ctx) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
+        flush_readback(ctx);
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
     });
