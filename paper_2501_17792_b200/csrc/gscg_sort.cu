@@ -59,10 +59,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 
 }  // namespace
 
-// Upsweep: per-tile digit counts, written digit-major (counts[d * tiles + t]).
-__global__ void __launch_bounds__(kSortThreads)
-k_sort_upsweep(SortPassParams p) {
-    __shared__ uint32_t s_hist[kSortWarps][kRadix];
+// Upsweep: per-tile digit counts, written digit-major (counts[d * tiles + t]). kFull: the
+// tile holds kSortTile keys (every tile but the last), so no bounds predicates.
+template <bool kFull>
+__device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (*s_hist)[kRadix]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t base = blockIdx.x * kSortTile;
     const uint32_t mask = (1u << p.bits) - 1u;
@@ -70,7 +70,7 @@ k_sort_upsweep(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {  // all loads in flight first
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = idx < p.count ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
     }
     // Lane d counts digit d of the warp's keys: per item, five ballots select the lanes
     // holding digit d.
@@ -86,7 +86,8 @@ k_sort_upsweep(SortPassParams p) {
         uint32_t differ = 0u;
 #pragma unroll
         for (int b = 0; b < kRadixBits; ++b) differ |= __ballot_sync(0xffffffffu, (d >> b) & 1u) ^ lane_mask[b];
-        cnt += __popc(__ballot_sync(0xffffffffu, idx < p.count) & ~differ);
+        const uint32_t valid = kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count);
+        cnt += __popc(valid & ~differ);
     }
     s_hist[warp][lane] = cnt;
     __syncthreads();
@@ -96,6 +97,13 @@ k_sort_upsweep(SortPassParams p) {
         for (int w = 0; w < kSortWarps; ++w) t += s_hist[w][threadIdx.x];
         p.counts[threadIdx.x * p.tiles + blockIdx.x] = t;
     }
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+k_sort_upsweep(SortPassParams p) {
+    __shared__ uint32_t s_hist[kSortWarps][kRadix];
+    if ((blockIdx.x + 1) * kSortTile <= p.count) upsweep_tile<true>(p, s_hist);
+    else upsweep_tile<false>(p, s_hist);
 }
 
 // Row scans: CTA d turns digit d's tile counts into exclusive offsets; row total ->
@@ -132,13 +140,21 @@ k_sort_rows(SortPassParams p) {
 // ballots give each key the lanes sharing its digit; lane d keeps the warp's running
 // count of digit d), stage the tile in shared memory in digit order, write it out
 // coalesced at digit_base[d] + counts[d][tile] + rank-within-digit.
-__global__ void __launch_bounds__(kSortThreads, 3)
-k_sort_downsweep(SortPassParams p) {
-    __shared__ uint32_t s_keys[kSortTile];
-    __shared__ uint16_t s_perm[kSortTile];  // tile-local source index of each staged key
-    __shared__ uint32_t s_woff[kSortWarps][kRadix];
-    __shared__ uint32_t s_block_excl[kRadix];
-    __shared__ uint32_t s_global[kRadix];
+struct DownsweepSmem {
+    uint32_t keys[kSortTile];
+    uint16_t perm[kSortTile];  // tile-local source index of each staged key
+    uint32_t woff[kSortWarps][kRadix];
+    uint32_t block_excl[kRadix];
+    uint32_t global[kRadix];
+};
+
+template <bool kFull>
+__device__ __forceinline__ void downsweep_tile(const SortPassParams& p, DownsweepSmem& sm) {
+    uint32_t* s_keys = sm.keys;
+    uint16_t* s_perm = sm.perm;
+    auto s_woff = sm.woff;
+    uint32_t* s_block_excl = sm.block_excl;
+    uint32_t* s_global = sm.global;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t mask = (1u << p.bits) - 1u;
@@ -153,7 +169,7 @@ k_sort_downsweep(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = idx < p.count ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
     }
     uint32_t lane_mask[kRadixBits];  // all-ones where lane's bit b is set
 #pragma unroll
@@ -163,7 +179,7 @@ k_sort_downsweep(SortPassParams p) {
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
-        const uint32_t vm = __ballot_sync(0xffffffffu, idx < p.count);
+        const uint32_t vm = kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count);
         uint32_t peers_differ = 0u, mine_differ = 0u;
 #pragma unroll
         for (int b = 0; b < kRadixBits; ++b) {
@@ -190,7 +206,7 @@ k_sort_downsweep(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
-        if (base + local < p.count) {
+        if (kFull || base + local < p.count) {
             const uint32_t d = (k[j] >> p.shift) & mask;
             const uint32_t pos = s_block_excl[d] + s_woff[warp][d] + rank[j];
             s_keys[pos] = k[j];
@@ -200,13 +216,13 @@ k_sort_downsweep(SortPassParams p) {
     __syncthreads();
     // Write-out: every gather of the thread issued before any store (the value gathers
     // stay inside this tile's 16 KB input window, so they hit L2).
-    const uint32_t n_here = p.count > base ? min(kSortTile, p.count - base) : 0u;
+    const uint32_t n_here = kFull ? kSortTile : (p.count > base ? min(kSortTile, p.count - base) : 0u);
     const uint32_t* __restrict__ vals_in = p.vals_in;
     uint32_t okey[kSortItems], opos[kSortItems], oval[kSortItems];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t e = tid + j * kSortThreads;
-        if (e < n_here) {
+        if (kFull || e < n_here) {
             okey[j] = s_keys[e];
             const uint32_t dd = (okey[j] >> p.shift) & mask;
             opos[j] = s_global[dd] + (e - s_block_excl[dd]);
@@ -217,11 +233,18 @@ k_sort_downsweep(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t e = tid + j * kSortThreads;
-        if (e < n_here) {
+        if (kFull || e < n_here) {
             p.keys_out[opos[j]] = okey[j];
             p.vals_out[opos[j]] = oval[j];
         }
     }
+}
+
+__global__ void __launch_bounds__(kSortThreads, 3)
+k_sort_downsweep(SortPassParams p) {
+    __shared__ DownsweepSmem sm;
+    if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_tile<true>(p, sm);
+    else downsweep_tile<false>(p, sm);
 }
 
 namespace {
