@@ -307,9 +307,8 @@ __device__ __forceinline__ uint32_t scan128(uint32_t v, uint32_t* s_tmp) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kSortThreads)
-k_sort_upsweep_wide(SortPassParams p) {
-    __shared__ uint32_t s_hist[kSortWarps][kWideRadix];
+template <bool kFull>
+__device__ __forceinline__ void upsweep_wide_tile(const SortPassParams& p, uint32_t (*s_hist)[kWideRadix]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kWideRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0u;
     const uint32_t base = blockIdx.x * kSortTile;
@@ -319,15 +318,15 @@ k_sort_upsweep_wide(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = idx < p.count ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
     }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
-        const uint32_t peers = peers_of(d, bits, __ballot_sync(0xffffffffu, idx < p.count));
-        if (idx < p.count && lane == 31 - __clz(peers)) s_hist[warp][d] += __popc(peers);
+        const uint32_t peers = peers_of(d, bits, kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count));
+        if ((kFull || idx < p.count) && lane == 31 - __clz(peers)) s_hist[warp][d] += __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -339,14 +338,30 @@ k_sort_upsweep_wide(SortPassParams p) {
     }
 }
 
-__global__ void __launch_bounds__(kSortThreads, 3)
-k_sort_downsweep_wide(SortPassParams p) {
-    __shared__ uint32_t s_keys[kSortTile];
-    __shared__ uint16_t s_perm[kSortTile];  // tile-local source index of each staged key
-    __shared__ uint32_t s_woff[kSortWarps][kWideRadix];
-    __shared__ uint32_t s_block_excl[kWideRadix];
-    __shared__ uint32_t s_global[kWideRadix];
-    __shared__ uint32_t s_tmp[kWideRadix / 32];
+__global__ void __launch_bounds__(kSortThreads)
+k_sort_upsweep_wide(SortPassParams p) {
+    __shared__ uint32_t s_hist[kSortWarps][kWideRadix];
+    if ((blockIdx.x + 1) * kSortTile <= p.count) upsweep_wide_tile<true>(p, s_hist);
+    else upsweep_wide_tile<false>(p, s_hist);
+}
+
+struct DownsweepWideSmem {
+    uint32_t keys[kSortTile];
+    uint16_t perm[kSortTile];  // tile-local source index of each staged key
+    uint32_t woff[kSortWarps][kWideRadix];
+    uint32_t block_excl[kWideRadix];
+    uint32_t global[kWideRadix];
+    uint32_t tmp[kWideRadix / 32];
+};
+
+template <bool kFull>
+__device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, DownsweepWideSmem& sm) {
+    uint32_t* s_keys = sm.keys;
+    uint16_t* s_perm = sm.perm;
+    auto s_woff = sm.woff;
+    uint32_t* s_block_excl = sm.block_excl;
+    uint32_t* s_global = sm.global;
+    uint32_t* s_tmp = sm.tmp;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t mask = (1u << p.bits) - 1u;
@@ -358,7 +373,7 @@ k_sort_downsweep_wide(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = idx < p.count ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
     }
     {  // global digit base (exclusive scan of the row totals) + this tile's offset
         const uint32_t total = tid < kWideRadix && static_cast<uint32_t>(tid) <= mask ? p.digit_base[tid] : 0u;
@@ -371,11 +386,11 @@ k_sort_downsweep_wide(SortPassParams p) {
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
-        const uint32_t peers = peers_of(d, bits, __ballot_sync(0xffffffffu, idx < p.count));
+        const uint32_t peers = peers_of(d, bits, kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count));
         const uint32_t before = wcnt[d];
         rank[j] = before + __popc(peers & lt);
         __syncwarp();
-        if (idx < p.count && lane == 31 - __clz(peers)) wcnt[d] = before + __popc(peers);
+        if ((kFull || idx < p.count) && lane == 31 - __clz(peers)) wcnt[d] = before + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -394,7 +409,7 @@ k_sort_downsweep_wide(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
-        if (base + local < p.count) {
+        if (kFull || base + local < p.count) {
             const uint32_t d = (k[j] >> p.shift) & mask;
             const uint32_t pos = s_block_excl[d] + s_woff[warp][d] + rank[j];
             s_keys[pos] = k[j];
@@ -402,13 +417,13 @@ k_sort_downsweep_wide(SortPassParams p) {
         }
     }
     __syncthreads();
-    const uint32_t n_here = p.count > base ? min(kSortTile, p.count - base) : 0u;
+    const uint32_t n_here = kFull ? kSortTile : (p.count > base ? min(kSortTile, p.count - base) : 0u);
     const uint32_t* __restrict__ vals_in = p.vals_in;
     uint32_t okey[kSortItems], opos[kSortItems], oval[kSortItems];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t e = tid + j * kSortThreads;
-        if (e < n_here) {
+        if (kFull || e < n_here) {
             okey[j] = s_keys[e];
             const uint32_t dd = (okey[j] >> p.shift) & mask;
             opos[j] = s_global[dd] + (e - s_block_excl[dd]);
@@ -419,11 +434,18 @@ k_sort_downsweep_wide(SortPassParams p) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t e = tid + j * kSortThreads;
-        if (e < n_here) {
+        if (kFull || e < n_here) {
             p.keys_out[opos[j]] = okey[j];
             p.vals_out[opos[j]] = oval[j];
         }
     }
+}
+
+__global__ void __launch_bounds__(kSortThreads, 3)
+k_sort_downsweep_wide(SortPassParams p) {
+    __shared__ DownsweepWideSmem sm;
+    if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_wide_tile<true>(p, sm);
+    else downsweep_wide_tile<false>(p, sm);
 }
 
 // After the depth sort: every sorted splat's binning span, gathered into sorted order
