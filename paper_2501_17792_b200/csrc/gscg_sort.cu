@@ -180,15 +180,15 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
         const uint32_t vm = kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count);
-        uint32_t peers_differ = 0u, mine_differ = 0u;
+        // Lane L's ballots give the lanes holding digit L; a key's own digit group is that
+        // mask fetched from lane d (one shuffle instead of five more mask chains).
+        uint32_t mine_differ = 0u;
 #pragma unroll
-        for (int b = 0; b < kRadixBits; ++b) {
-            const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            peers_differ |= bb ^ (0u - ((d >> b) & 1u));
-            mine_differ |= bb ^ lane_mask[b];
-        }
-        rank[j] = __shfl_sync(0xffffffffu, cnt, static_cast<int>(d)) + __popc(vm & ~peers_differ & lt);
-        cnt += __popc(vm & ~mine_differ);
+        for (int b = 0; b < kRadixBits; ++b) mine_differ |= __ballot_sync(0xffffffffu, (d >> b) & 1u) ^ lane_mask[b];
+        const uint32_t mine = vm & ~mine_differ;
+        const uint32_t peers = __shfl_sync(0xffffffffu, mine, static_cast<int>(d));
+        rank[j] = __shfl_sync(0xffffffffu, cnt, static_cast<int>(d)) + __popc(peers & lt);
+        cnt += __popc(mine);
     }
     s_woff[warp][lane] = cnt;
     __syncthreads();
