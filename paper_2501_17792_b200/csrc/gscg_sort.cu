@@ -193,14 +193,17 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
     s_woff[warp][lane] = cnt;
     __syncthreads();
     if (tid < 32) {  // digit tid: exclusive over warps, then over digits
-        uint32_t run = 0;
+        uint32_t run = 0, wrun[kSortWarps];
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w) {
-            const uint32_t c = s_woff[w][tid];
-            s_woff[w][tid] = run;
-            run += c;
+            wrun[w] = run;
+            run += s_woff[w][tid];
         }
-        s_block_excl[tid] = warp_incl_scan(run, tid) - run;
+        const uint32_t bex = warp_incl_scan(run, tid) - run;
+        s_block_excl[tid] = bex;
+        s_global[tid] -= bex;  // staged position e of digit d goes to s_global[d] + e
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) s_woff[w][tid] = bex + wrun[w];  // warp w's first slot of digit tid
     }
     __syncthreads();
 #pragma unroll
@@ -208,7 +211,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
         const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
         if (kFull || base + local < p.count) {
             const uint32_t d = (k[j] >> p.shift) & mask;
-            const uint32_t pos = s_block_excl[d] + s_woff[warp][d] + rank[j];
+            const uint32_t pos = s_woff[warp][d] + rank[j];
             s_keys[pos] = k[j];
             s_perm[pos] = static_cast<uint16_t>(local);
         }
@@ -224,8 +227,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
         const uint32_t e = tid + j * kSortThreads;
         if (kFull || e < n_here) {
             okey[j] = s_keys[e];
-            const uint32_t dd = (okey[j] >> p.shift) & mask;
-            opos[j] = s_global[dd] + (e - s_block_excl[dd]);
+            opos[j] = s_global[(okey[j] >> p.shift) & mask] + e;
             const uint32_t src = base + s_perm[e];
             oval[j] = vals_in ? __ldg(vals_in + src) : src;
         }
