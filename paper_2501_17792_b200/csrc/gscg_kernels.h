@@ -193,7 +193,7 @@ constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
 constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
 constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes
 constexpr int kEmitSmem = (32 * kEmitThreads + 2 * kEmitStage) * 4;  // dynamic shared bytes
-template <bool kCount>
+template <bool kCount, bool kQuads>
 __global__ void k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count,
                                const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
                                uint32_t blocks, int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop,

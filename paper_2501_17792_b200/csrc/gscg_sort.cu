@@ -251,23 +251,24 @@ k_sort_downsweep(SortPassParams p) {
 
 namespace {
 
-__device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x, int quads) {
-    return quads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
-                 : static_cast<uint32_t>(cy * tiles_x + cx);
+template <bool kQuads>
+__device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x) {
+    return kQuads ? static_cast<uint32_t>(((cy >> 1) * tiles_x + (cx >> 1)) * 4 + (cy & 1) * 2 + (cx & 1))
+                  : static_cast<uint32_t>(cy * tiles_x + cx);
 }
 
 // Calls f(cell) for every binning cell of a packed span, row by row (the emission order);
 // along a row the cell id advances without recomputing it (quadrant cells: +1 inside a
 // tile, +3 into the next tile).
-template <typename F>
-__device__ __forceinline__ void for_each_cell(uint2 sp, int tiles_x, int quads, F&& f) {
+template <bool kQuads, typename F>
+__device__ __forceinline__ void for_each_cell_t(uint2 sp, int tiles_x, F&& f) {
     const int cx0 = static_cast<int>(sp.x & 0xffffu), cy0 = static_cast<int>(sp.x >> 16);
     const int w = static_cast<int>(sp.y & 0xffffu), h = static_cast<int>(sp.y >> 16);
     for (int cy = cy0; cy < cy0 + h; ++cy) {
-        uint32_t c = cell_id(cx0, cy, tiles_x, quads);
+        uint32_t c = cell_id<kQuads>(cx0, cy, tiles_x);
         for (int cx = cx0; cx < cx0 + w; ++cx) {
             f(c);
-            c += quads ? ((cx & 1) ? 3u : 1u) : 1u;
+            c += kQuads ? 1u + 2u * static_cast<uint32_t>(cx & 1) : 1u;
         }
     }
 }
@@ -768,7 +769,7 @@ k_pair_long_runs(const uint32_t* keys, uint32_t count, uint32_t* recs, const uin
 // output equals emitting in sorted order and running the first LSD pass on it.
 // kCount: only count the block's pairs per digit (block_digit[d][block], the input of
 // k_sort_rows); else scatter them.
-template <bool kCount>
+template <bool kCount, bool kQuads>
 __global__ void __launch_bounds__(kEmitThreads)
 k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count, const uint2* span_sorted,
                uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads,
@@ -816,7 +817,7 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
         s_base[tid] = warp_incl_scan(t, lane) - t + (static_cast<uint32_t>(tid) <= dmask ? block_digit[tid * blocks + blockIdx.x] : 0u);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) for_each_cell(sp[q], tiles_x, quads, [&](uint32_t c) { ++s_cnt[c & dmask][tid]; });
+    for (int q = 0; q < 4; ++q) for_each_cell_t<kQuads>(sp[q], tiles_x, [&](uint32_t c) { ++s_cnt[c & dmask][tid]; });
     __syncthreads();
     if (kCount) {  // digit d's pairs in this block: warp w sums its digits over all threads
 #pragma unroll
@@ -863,7 +864,7 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t rec = rc[q], tag = tg[q];
-        for_each_cell(sp[q], tiles_x, quads, [&](uint32_t c) {
+        for_each_cell_t<kQuads>(sp[q], tiles_x, [&](uint32_t c) {
             const uint32_t d = c & dmask;
             const uint32_t r = s_cnt[d][tid]++;  // rank among the block's pairs of digit d
             if (staged) {
@@ -892,19 +893,18 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
                  int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
                  uint32_t* pair_rec) {
     static bool attr = [] {
-        cudaFuncSetAttribute(k_emit_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
-        cudaFuncSetAttribute(k_emit_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
         return true;
     }();
     (void)attr;
-    if (count_only)
-        k_emit_scatter<true><<<blocks, kEmitThreads, kRadix * kEmitThreads * 4, s>>>(rec_sorted, key_sorted, count, span_sorted, block_digit,
-                                                                    digit_total, blocks, tiles_x, quads, dmask,
-                                                                    tag_drop, tag_shift, pair_cell, pair_rec);
-    else
-        k_emit_scatter<false><<<blocks, kEmitThreads, kEmitSmem, s>>>(rec_sorted, key_sorted, count, span_sorted, block_digit,
-                                                                     digit_total, blocks, tiles_x, quads, dmask,
-                                                                     tag_drop, tag_shift, pair_cell, pair_rec);
+    const int smem = count_only ? kRadix * kEmitThreads * 4 : kEmitSmem;
+    auto kernel = count_only ? (quads ? k_emit_scatter<true, true> : k_emit_scatter<true, false>)
+                             : (quads ? k_emit_scatter<false, true> : k_emit_scatter<false, false>);
+    kernel<<<blocks, kEmitThreads, smem, s>>>(rec_sorted, key_sorted, count, span_sorted, block_digit, digit_total,
+                                              blocks, tiles_x, quads, dmask, tag_drop, tag_shift, pair_cell, pair_rec);
 }
 
 __global__ void k_iota2(uint32_t* a, uint32_t* b, uint32_t n) {
