@@ -165,7 +165,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
     const uint32_t base = blockIdx.x * kSortTile;
     const uint32_t lt = (1u << lane) - 1u;
 
-    uint32_t k[kSortItems], rank[kSortItems];
+    uint32_t k[kSortItems], rank2[kSortItems / 2];  // ranks (< 512) packed in pairs
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
@@ -187,7 +187,8 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
         for (int b = 0; b < kRadixBits; ++b) mine_differ |= __ballot_sync(0xffffffffu, (d >> b) & 1u) ^ lane_mask[b];
         const uint32_t mine = vm & ~mine_differ;
         const uint32_t peers = __shfl_sync(0xffffffffu, mine, static_cast<int>(d));
-        rank[j] = __shfl_sync(0xffffffffu, cnt, static_cast<int>(d)) + __popc(peers & lt);
+        const uint32_t r = __shfl_sync(0xffffffffu, cnt, static_cast<int>(d)) + __popc(peers & lt);
+        rank2[j / 2] = (j & 1) ? (rank2[j / 2] | (r << 16)) : r;
         cnt += __popc(mine);
     }
     s_woff[warp][lane] = cnt;
@@ -211,7 +212,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
         const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
         if (kFull || base + local < p.count) {
             const uint32_t d = (k[j] >> p.shift) & mask;
-            const uint32_t pos = s_woff[warp][d] + rank[j];
+            const uint32_t pos = s_woff[warp][d] + ((j & 1) ? (rank2[j / 2] >> 16) : (rank2[j / 2] & 0xffffu));
             s_keys[pos] = k[j];
             s_perm[pos] = static_cast<uint16_t>(local);
         }
@@ -221,28 +222,32 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
     // stay inside this tile's 16 KB input window, so they hit L2).
     const uint32_t n_here = kFull ? kSortTile : (p.count > base ? min(kSortTile, p.count - base) : 0u);
     const uint32_t* __restrict__ vals_in = p.vals_in;
-    uint32_t okey[kSortItems], opos[kSortItems], oval[kSortItems];
+    constexpr int kHalf = kSortItems / 2;  // two rounds: half the live registers
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-        const uint32_t e = tid + j * kSortThreads;
-        if (kFull || e < n_here) {
-            okey[j] = s_keys[e];
-            opos[j] = s_global[(okey[j] >> p.shift) & mask] + e;
-            const uint32_t src = base + s_perm[e];
-            oval[j] = vals_in ? __ldg(vals_in + src) : src;
+    for (int h = 0; h < 2; ++h) {
+        uint32_t okey[kHalf], opos[kHalf], oval[kHalf];
+#pragma unroll
+        for (int j = 0; j < kHalf; ++j) {
+            const uint32_t e = tid + (h * kHalf + j) * kSortThreads;
+            if (kFull || e < n_here) {
+                okey[j] = s_keys[e];
+                opos[j] = s_global[(okey[j] >> p.shift) & mask] + e;
+                const uint32_t src = base + s_perm[e];
+                oval[j] = vals_in ? __ldg(vals_in + src) : src;
+            }
         }
-    }
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-        const uint32_t e = tid + j * kSortThreads;
-        if (kFull || e < n_here) {
-            p.keys_out[opos[j]] = okey[j];
-            p.vals_out[opos[j]] = oval[j];
+        for (int j = 0; j < kHalf; ++j) {
+            const uint32_t e = tid + (h * kHalf + j) * kSortThreads;
+            if (kFull || e < n_here) {
+                p.keys_out[opos[j]] = okey[j];
+                p.vals_out[opos[j]] = oval[j];
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(kSortThreads, 3)
+__global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep(SortPassParams p) {
     __shared__ DownsweepSmem sm;
     if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_tile<true>(p, sm);
