@@ -5,23 +5,22 @@
 //   1. LSD radix sort of the S splat depth keys over their top (at most 25) varying bits,
 //      values = record index.
 //   2. k_sorted_spans gathers the spans in sorted order; k_emit_scatter (count: per-block
-//      digit counts; k_sort_rows; scatter): every sorted splat emits one pair per overlapped binning cell
-//      (tile, or 8x8 quadrant of a 16-px tile) straight into the order of the first
-//      stable cell pass; each pair's key word carries its splat's truncated depth above
-//      the cell id.
+//      digit counts; k_sort_rows; scatter): every sorted splat emits one pair per
+//      overlapped binning cell (tile, or 8x8 quadrant of a 16-px tile) straight into the
+//      order of the first stable cell pass; each pair's key word carries its splat's
+//      truncated depth above the cell id.
 //   3. the remaining stable LSD passes over the cell bits.
 //   4. k_cell_fixup: cell ranges, and every run of pairs with equal (cell, truncated
 //      depth) ordered by (depth bits, ordinal) — the dropped low bits and the reference's
 //      (instance, gaussian) tie-break (ordinal = instance base + gaussian index). Each
 //      cell list is then exactly the reference's bin restricted to the cell.
 //
-// Each LSD pass (digits of up to 5 bits; a b-bit key takes ceil(b/5) passes with the bits
-// spread evenly) is reduce-then-scan: k_sort_upsweep counts digits per 4096-key tile,
-// k_sort_rows turns the counts into per-tile offsets and digit totals, k_sort_downsweep ranks
-// keys stably inside the tile with a register-only warp multisplit (ballots + shuffles,
-// lane d keeps the warp's count of digit d), stages the tile in digit order and writes it
-// out coalesced. 8-bit digits with shared-memory counters were measured no faster overall
-// (fewer passes, but each ~1.6x slower). No tile waits on another: a decoupled look-back onesweep and
+// Each LSD pass (digits of up to 5 bits, or 7 in the wide passes a plan takes where they
+// save a pass) is reduce-then-scan: k_sort_upsweep counts digits per 4096-key tile,
+// k_sort_rows turns the counts into per-tile offsets and digit totals, k_sort_downsweep
+// ranks keys stably inside the tile with a register-only warp multisplit (ballots +
+// shuffles, lane d keeps the warp's count of digit d), stages the tile in digit order and
+// writes it out coalesced. No tile waits on another: a decoupled look-back onesweep and
 // 8-bit shared-atomic ranking were both measured slower here (serial look-back chains,
 // ATOMS throughput).
 #include "gscg_common.cuh"
