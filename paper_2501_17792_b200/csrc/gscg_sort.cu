@@ -376,7 +376,7 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
     for (int i = tid; i < kSortWarps * kWideRadix; i += blockDim.x) (&s_woff[0][0])[i] = 0u;
     const uint32_t base = blockIdx.x * kSortTile;
     const uint32_t lt = (1u << lane) - 1u;
-    uint32_t k[kSortItems], rank[kSortItems];
+    uint32_t k[kSortItems], rank2[kSortItems / 2];  // ranks (< 512) packed in pairs
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
@@ -395,7 +395,8 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
         const uint32_t d = (k[j] >> p.shift) & mask;
         const uint32_t peers = peers_of(d, bits, kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count));
         const uint32_t before = wcnt[d];
-        rank[j] = before + __popc(peers & lt);
+        const uint32_t r = before + __popc(peers & lt);
+        rank2[j / 2] = (j & 1) ? (rank2[j / 2] | (r << 16)) : r;
         __syncwarp();
         if ((kFull || idx < p.count) && lane == 31 - __clz(peers)) wcnt[d] = before + __popc(peers);
         __syncwarp();
@@ -418,7 +419,7 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
         const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
         if (kFull || base + local < p.count) {
             const uint32_t d = (k[j] >> p.shift) & mask;
-            const uint32_t pos = s_block_excl[d] + s_woff[warp][d] + rank[j];
+            const uint32_t pos = s_block_excl[d] + s_woff[warp][d] + ((j & 1) ? (rank2[j / 2] >> 16) : (rank2[j / 2] & 0xffffu));
             s_keys[pos] = k[j];
             s_perm[pos] = static_cast<uint16_t>(local);
         }
@@ -426,29 +427,33 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
     __syncthreads();
     const uint32_t n_here = kFull ? kSortTile : (p.count > base ? min(kSortTile, p.count - base) : 0u);
     const uint32_t* __restrict__ vals_in = p.vals_in;
-    uint32_t okey[kSortItems], opos[kSortItems], oval[kSortItems];
+    constexpr int kHalf = kSortItems / 2;  // two rounds: half the live registers
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-        const uint32_t e = tid + j * kSortThreads;
-        if (kFull || e < n_here) {
-            okey[j] = s_keys[e];
-            const uint32_t dd = (okey[j] >> p.shift) & mask;
-            opos[j] = s_global[dd] + (e - s_block_excl[dd]);
-            const uint32_t src = base + s_perm[e];
-            oval[j] = vals_in ? __ldg(vals_in + src) : src;
+    for (int h = 0; h < 2; ++h) {
+        uint32_t okey[kHalf], opos[kHalf], oval[kHalf];
+#pragma unroll
+        for (int j = 0; j < kHalf; ++j) {
+            const uint32_t e = tid + (h * kHalf + j) * kSortThreads;
+            if (kFull || e < n_here) {
+                okey[j] = s_keys[e];
+                const uint32_t dd = (okey[j] >> p.shift) & mask;
+                opos[j] = s_global[dd] + (e - s_block_excl[dd]);
+                const uint32_t src = base + s_perm[e];
+                oval[j] = vals_in ? __ldg(vals_in + src) : src;
+            }
         }
-    }
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-        const uint32_t e = tid + j * kSortThreads;
-        if (kFull || e < n_here) {
-            p.keys_out[opos[j]] = okey[j];
-            p.vals_out[opos[j]] = oval[j];
+        for (int j = 0; j < kHalf; ++j) {
+            const uint32_t e = tid + (h * kHalf + j) * kSortThreads;
+            if (kFull || e < n_here) {
+                p.keys_out[opos[j]] = okey[j];
+                p.vals_out[opos[j]] = oval[j];
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(kSortThreads, 3)
+__global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep_wide(SortPassParams p) {
     __shared__ DownsweepWideSmem sm;
     if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_wide_tile<true>(p, sm);
