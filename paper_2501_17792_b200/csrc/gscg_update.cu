@@ -315,7 +315,7 @@ k_fk_skin(FkParams p) {
 //
 // Rect of a splat at camera-space t (math.cpp:131-170): rx = 3 sqrt(C00) with
 // C00 = m0 S m0^T + 0.3 and m0 = (f/tz)(W0 - (tx/tz) W2), so
-//   rx <= 3 (f/tz) sqrt(1 + (tx/tz)^2) sigma + 3 sqrt(0.3)
+//   rx <= 3 (f/tz) |W0 - (tx/tz) W2| sigma + 3 sqrt(0.3)
 // (sigma^2 >= lambda_max of every covariance). The rect is empty on the left when
 // mx + rx < 0, on the right when mx - rx >= width (same for y). The test bounds tx/tz over
 // the ball in double precision with relative and pixel margins far above the float
@@ -381,25 +381,37 @@ k_inst_cull(CullParams p) {
     rho = rho * 1.001 + 1e-3 * (1.0 + cn);
     const CameraDev& cam = p.cam;
     const double d[3] = {c[0] - cam.pos[0], c[1] - cam.pos[1], c[2] - cam.pos[2]};
-    double tc[3];
-    for (int i = 0; i < 3; ++i) tc[i] = cam.w[3 * i + 0] * d[0] + cam.w[3 * i + 1] * d[1] + cam.w[3 * i + 2] * d[2];
+    double W[3][3], tc[3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) W[i][j] = cam.w[3 * i + j];
+    for (int i = 0; i < 3; ++i) tc[i] = W[i][0] * d[0] + W[i][1] * d[1] + W[i][2] * d[2];
+    // The ball in camera space: radius rho |W|_2 (|W|_2^2 <= max row sum of |W W^T|; 1 for
+    // the rotation CameraBasis builds, but the C-ABI takes any matrix).
+    double dot[3][3], wmax = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) dot[i][j] = W[i][0] * W[j][0] + W[i][1] * W[j][1] + W[i][2] * W[j][2];
+    for (int i = 0; i < 3; ++i) wmax = fmax(wmax, fabs(dot[i][0]) + fabs(dot[i][1]) + fabs(dot[i][2]));
+    const double rc = rho * sqrt(wmax) * (1.0 + 1e-9);
     const double near_m = cam.near_m;
     bool cull = false;
-    if (tc[2] + rho < near_m) {
+    if (tc[2] + rc < near_m) {
         cull = true;  // every point behind the near plane
     } else {
-        const double zmin = fmax(near_m, tc[2] - rho), zmax = tc[2] + rho;
+        const double zmin = fmax(near_m, tc[2] - rc), zmax = tc[2] + rc;
         const double f = cam.focal, sigma = static_cast<double>(tpl.cull_sigma) * 1.001;
         const double margin = 2.0;                             // pixels
         const double pad = 3.0 * 0.5477225575051661 + 0.01;   // 3 sqrt(0.3)
         // tx/tz and ty/tz over the ball: numerator bound over the tz that extremises it.
         auto ratio_hi = [&](double num) { return num >= 0.0 ? num / zmin : num / zmax; };
         auto ratio_lo = [&](double num) { return num >= 0.0 ? num / zmax : num / zmin; };
-        const double ux_hi = ratio_hi(tc[0] + rho), ux_lo = ratio_lo(tc[0] - rho);
-        const double uy_hi = ratio_hi(tc[1] + rho), uy_lo = ratio_lo(tc[1] - rho);
+        const double ux_hi = ratio_hi(tc[0] + rc), ux_lo = ratio_lo(tc[0] - rc);
+        const double uy_hi = ratio_hi(tc[1] + rc), uy_lo = ratio_lo(tc[1] - rc);
         const double ux = fmax(fabs(ux_hi), fabs(ux_lo)), uy = fmax(fabs(uy_hi), fabs(uy_lo));
-        const double rx = 3.0 * (f / zmin) * sqrt(1.0 + ux * ux) * sigma * 1.001 + pad;
-        const double ry = 3.0 * (f / zmin) * sqrt(1.0 + uy * uy) * sigma * 1.001 + pad;
+        // |W0 - u W2|^2 <= |W0|^2 + 2 |u| |W0.W2| + u^2 |W2|^2 (= 1 + u^2 for a rotation).
+        const double gx = dot[0][0] + 2.0 * ux * fabs(dot[0][2]) + ux * ux * dot[2][2];
+        const double gy = dot[1][1] + 2.0 * uy * fabs(dot[1][2]) + uy * uy * dot[2][2];
+        const double rx = 3.0 * (f / zmin) * sqrt(gx) * sigma * 1.001 + pad;
+        const double ry = 3.0 * (f / zmin) * sqrt(gy) * sigma * 1.001 + pad;
         const double mx_hi = f * ux_hi + cam.cx, mx_lo = f * ux_lo + cam.cx;
         const double my_hi = f * uy_hi + cam.cy, my_lo = f * uy_lo + cam.cy;
         cull = (mx_hi + rx < -margin) || (mx_lo - rx > cam.width + margin) ||

@@ -402,3 +402,58 @@ def test_baseline_config4_4k_ten_thousand():
     rep = check_frame(s, r, o, g, c)
     assert rep["S"] > 20_000_000 and rep["K"] > 50_000_000
     assert check_cull_invariance(r, 0.25) > 1000
+
+
+def test_instance_cull_is_invisible_for_any_camera_matrix():
+    """The C-ABI takes any world_to_view matrix, not only the rotation CameraBasis builds
+    (math.cpp:118-129). The cull bounds the camera-space ball by |W|_2 and the rect by
+    |W0 - u W2|, so a scaled and sheared matrix must still give a byte-identical frame."""
+    import ctypes as C
+    from paper_2501_17792_b200 import native as N
+    from paper_2501_17792_b200.multigpu import gscg_settings
+
+    pos, look = (5.5, 1.7, 5.5), (12.0, 1.2, 6.0)
+    cfg = P.SceneConfig(template_count=3, level_counts=(400, 120, 40), with_sh=True, motion_count=3,
+                        motion_frames=24, grid_rows=12, grid_cols=12, crowd_count=144, crowd_seed=5,
+                        cam_pos=pos, cam_look=look, width=320, height=200)
+    s = P.Scene(cfg)
+    r = P.Renderer(s, device_poses=True)
+    r.render_frame(0.4, P.RenderSettings())  # uploads templates and motion tables
+    tids, place, _ = r.sample_crowd(0.4)
+    n = len(tids)
+    inst = s.instances
+    mids = np.ascontiguousarray(inst["motion_id"]).astype(np.uint32)
+    phase = np.ascontiguousarray(inst["phase_offset_s"]).astype(np.float32)
+    cam = s.camera_basis()
+    scale = [1.3, 1.3, 1.3, 0.8, 0.8, 0.8, 1.1, 1.1, 1.1]
+    for i in range(9):
+        cam.world_to_view[i] *= scale[i]
+    cam.world_to_view[1] += 0.25  # shear
+    rs = gscg_settings(P.RenderSettings())
+    lp = N.GscgLodPolicy()
+    lp.threshold_count = len(cfg.lod_thresholds)
+    for i, v in enumerate(cfg.lod_thresholds):
+        lp.thresholds_m[i] = v
+    lib, ctx = N.gscg(), r.gpu
+    out = []
+    for flags in (N.GSCG_DEBUG_RECORDS | N.GSCG_DEBUG_NO_CULL, N.GSCG_DEBUG_RECORDS):
+        N.check_gscg(lib.gscg_set_debug(ctx, flags), ctx)
+        lods = np.full(n, 0xFFFFFFFF, dtype=np.uint32)
+        fd = N.GscgFrameDesc()
+        fd.instance_count, fd.joint_stride = n, r.joint_stride
+        fd.template_ids, fd.placement = tids.ctypes.data, place.ctypes.data
+        fd.active_lod, fd.forced_lod = lods.ctypes.data, -1
+        fd.memory, fd.pose_source, fd.time_s = N.GSCG_MEM_HOST, N.GSCG_POSES_SAMPLED, 0.4
+        fd.motion_ids, fd.phase_offsets = mids.ctypes.data, phase.ctypes.data
+        rgb = np.zeros((cfg.height, cfg.width, 3), np.float32)
+        T = np.zeros((cfg.height, cfg.width), np.float32)
+        N.check_gscg(lib.gscg_render_frame(ctx, C.byref(fd), C.byref(cam), C.byref(rs), C.byref(lp),
+                                           rgb.ctypes.data, T.ctypes.data, None), ctx)
+        rec = r.splat_records()
+        rec = rec[np.argsort(rec["ordinal"], kind="stable")]
+        out.append((rgb, T, r.counts(), rec.tobytes(), r.sorted_ordinals().copy(), r.instances_culled()))
+    (a, b) = out
+    assert a[5] == 0 and a[2] == b[2] and a[3] == b[3]
+    assert np.array_equal(a[4], b[4])
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    assert a[2][1] > 0  # something is on screen
