@@ -819,6 +819,16 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
     // Tag above the cell id: the low bits of the splat's truncated depth key (k_cell_fixup).
 #pragma unroll
     for (int q = 0; q < 4; ++q) tg[q] = key_sorted && tag_shift < 32 ? (tg[q] >> tag_drop) << tag_shift : 0u;
+    if (kCount) {  // block totals only: one shared atomic per pair on the block's 32 counters
+        uint32_t* s_tot = &s_cnt[0][0];
+        if (tid < kRadix) s_tot[tid] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) for_each_cell_t<kQuads>(sp[q], tiles_x, [&](uint32_t c) { atomicAdd(&s_tot[c & dmask], 1u); });
+        __syncthreads();
+        if (static_cast<uint32_t>(tid) <= dmask && tid < kRadix) block_digit[tid * blocks + blockIdx.x] = s_tot[tid];
+        return;
+    }
 #pragma unroll
     for (int d = 0; d < kRadix; ++d) s_cnt[d][tid] = 0u;
     if (!kCount && tid < kRadix) {  // global base of digit tid: scanned digit totals + this block's offset
@@ -909,7 +919,7 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
         return true;
     }();
     (void)attr;
-    const int smem = count_only ? kRadix * kEmitThreads * 4 : kEmitSmem;
+    const int smem = count_only ? kRadix * 4 : kEmitSmem;  // the count pass keeps 32 block counters
     auto kernel = count_only ? (quads ? k_emit_scatter<true, true> : k_emit_scatter<true, false>)
                              : (quads ? k_emit_scatter<false, true> : k_emit_scatter<false, false>);
     kernel<<<blocks, kEmitThreads, smem, s>>>(rec_sorted, key_sorted, count, span_sorted, block_digit, digit_total,
