@@ -61,7 +61,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 // Upsweep: per-tile digit counts, written digit-major (counts[d * tiles + t]). kFull: the
 // tile holds kSortTile keys (every tile but the last), so no bounds predicates.
 template <bool kFull>
-__device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (*s_hist)[kRadix]) {
+__device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (*s_hist)[kRadix][32]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t base = blockIdx.x * kSortTile;
     const uint32_t mask = (1u << p.bits) - 1u;
@@ -71,36 +71,34 @@ __device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
     }
-    // Lane d counts digit d of the warp's keys: per item, five ballots select the lanes
-    // holding digit d.
-    uint32_t lane_mask[kRadixBits];  // all-ones where lane's bit b is set
+    // Lane-private digit counters s_hist[warp][d][lane] (lane L's column sits in bank L:
+    // no conflicts), then lane d sums row d along a rotated walk (conflict-free too).
+    uint32_t(*h)[32] = s_hist[warp];
 #pragma unroll
-    for (int b = 0; b < kRadixBits; ++b) lane_mask[b] = 0u - ((static_cast<uint32_t>(lane) >> b) & 1u);
-    uint32_t cnt = 0;
+    for (int d = 0; d < kRadix; ++d) h[d][lane] = 0u;
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        const uint32_t d = (k[j] >> p.shift) & mask;
-        // Lanes whose digit differs from lane's index in some bit: OR of (ballot ^ lane mask).
-        uint32_t differ = 0u;
-#pragma unroll
-        for (int b = 0; b < kRadixBits; ++b) differ |= __ballot_sync(0xffffffffu, (d >> b) & 1u) ^ lane_mask[b];
-        const uint32_t valid = kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count);
-        cnt += __popc(valid & ~differ);
+        if (kFull || idx < p.count) ++h[(k[j] >> p.shift) & mask][lane];
     }
-    s_hist[warp][lane] = cnt;
+    __syncwarp();
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) cnt += h[lane][(c + lane) & 31];
+    __syncwarp();
+    h[0][lane] = cnt;  // warp's count of digit `lane`
     __syncthreads();
     if (threadIdx.x < kRadix) {
         uint32_t t = 0;
 #pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) t += s_hist[w][threadIdx.x];
+        for (int w = 0; w < kSortWarps; ++w) t += s_hist[w][0][threadIdx.x];
         p.counts[threadIdx.x * p.tiles + blockIdx.x] = t;
     }
 }
 
 __global__ void __launch_bounds__(kSortThreads)
 k_sort_upsweep(SortPassParams p) {
-    __shared__ uint32_t s_hist[kSortWarps][kRadix];
+    __shared__ uint32_t s_hist[kSortWarps][kRadix][32];
     if ((blockIdx.x + 1) * kSortTile <= p.count) upsweep_tile<true>(p, s_hist);
     else upsweep_tile<false>(p, s_hist);
 }
