@@ -853,19 +853,13 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
 #pragma unroll
     for (int dd = 0; dd < kDigitsPerWarp; ++dd) {
         const int d = warp * kDigitsPerWarp + dd;
-        uint32_t v[kPerLane], sum = 0;
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k) {
-            v[k] = s_cnt[d][lane * kPerLane + k];
-            sum += v[k];
-        }
+        static_assert(kPerLane == 4, "one 16-byte shared access per lane");
+        uint4* row = reinterpret_cast<uint4*>(&s_cnt[d][lane * kPerLane]);  // conflict-free LDS.128
+        const uint4 v = *row;
+        const uint32_t sum = v.x + v.y + v.z + v.w;
         const uint32_t incl = warp_incl_scan(sum, lane);
-        uint32_t run = incl - sum;
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k) {
-            s_cnt[d][lane * kPerLane + k] = run;
-            run += v[k];
-        }
+        const uint32_t r0 = incl - sum;
+        *row = make_uint4(r0, r0 + v.x, r0 + v.x + v.y, r0 + v.x + v.y + v.z);
         if (lane == 31) s_local[d] = incl;  // digit total for now
     }
     __syncthreads();
