@@ -411,8 +411,8 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                      "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
                      "algorithmic_bytes": kbytes, "peak_source": peaks["source"],
                      "limiter": ("issue-bound on exact no-FMA FP32 + integer work (ncu: ~65% issue, DRAM ~30%); "
-                                 "profiles/r01_ncu_full_v5.txt" if kernel == "k_project" else
-                                 "issue-bound, per-pixel list-walk divergence; profiles/r01_ncu_full_v5.txt")},
+                                 "profiles/r01_ncu_full_v6.txt" if kernel == "k_project" else
+                                 "issue-bound, per-pixel list-walk divergence; profiles/r01_ncu_full_v6.txt")},
         "e2e": {"value": round(e2e_fps, 3), "unit": "FPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": ("Renderer.render_frame(out=pinned, pipelined=True): frame k's read-back overlaps frame k+1"
                         if not band_path else "DistributedRenderer.render_frame"),
