@@ -210,7 +210,8 @@ int gscg_render_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
  * destinations it returns once the frame is rendered and the LoD state written back;
  * the framebuffer read-back into fb_rgb / fb_T keeps running on a copy stream,
  * overlapped with the next frame, which renders into a second device framebuffer.
- * fb_rgb / fb_T of a frame are valid after gscg_wait_readback; a caller alternating two
+ * fb_rgb / fb_T of a frame are valid after gscg_wait_readback, and must stay allocated
+ * until then (the copy lands after this call returns); a caller alternating two
  * host buffers submits frame k, then waits for frame k-1 (frames_back = 1). */
 int gscg_render_frame_async(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
                             const gscg_render_settings* settings, const gscg_lod_policy* lod,

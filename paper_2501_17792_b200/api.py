@@ -403,9 +403,13 @@ class Renderer:
 
         pipelined=True (gsch_render_async): returns once the frame is rendered while its
         read-back into `out` continues, overlapped with the next frame; the arrays are
-        valid after wait_readback(). Streaming callers alternate two `out` pairs."""
+        valid after wait_readback(). Streaming callers alternate two `out` pairs. The
+        read-back lands after this call returns, so `out` is required (ideally pinned
+        arrays from alloc_frame) and the Renderer keeps it alive until it has landed."""
         settings = settings or RenderSettings()
         W, H = self.scene.cfg.width, self.scene.cfg.height
+        if pipelined and out is None:
+            raise ValueError("render_frame(pipelined=True) needs `out` arrays: the read-back completes after the call")
         if out is None:
             rgb = np.empty((H, W, 3), dtype=np.float32)
             T = np.empty((H, W), dtype=np.float32)
@@ -418,6 +422,10 @@ class Renderer:
         fn = N.gsch().gsch_render_async if pipelined else N.gsch().gsch_render
         N.check_gsch(fn(self._h, time_s, int(static_pose), -1 if forced_lod is None else forced_lod,
                         C.byref(settings.native()), _ptr(rgb), None if T is None else _ptr(T), C.byref(st)))
+        # A pipelined frame's destination is written until a later call or wait_readback:
+        # hold the arrays of the last two pipelined submissions (older ones are complete).
+        if pipelined:
+            self._inflight = (getattr(self, "_inflight", []) + [(rgb, T)])[-2:]
         if times is not None:
             for f in ("update_ms", "gather_ms", "sort_ms", "rasterize_ms", "pose_ms", "splat_count", "pair_count",
                       "gaussian_count"):

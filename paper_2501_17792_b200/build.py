@@ -97,6 +97,15 @@ def build_oracle(verbose: bool = False) -> Path:
         print(res.stdout + res.stderr)
     if res.returncode != 0:
         raise RuntimeError("oracle build failed:\n" + res.stdout + res.stderr)
+    # oracle/_ref: the reference's own sources (read in place under /root/reference,
+    # which exists only in the build container) + the Eigen-subset shim. The built .so
+    # travels to the GPU box with the repo; there it is used prebuilt.
+    if Path("/root/reference/proj/src/renderer.cpp").exists():
+        res = subprocess.run(["make", "-C", str(oracle), "ref"], capture_output=True, text=True)
+        if verbose:
+            print(res.stdout + res.stderr)
+        if res.returncode != 0:
+            raise RuntimeError("reference build (oracle/_ref) failed:\n" + res.stdout + res.stderr)
     return oracle / "_build" / "liborc.so"
 
 

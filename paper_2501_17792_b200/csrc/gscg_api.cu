@@ -676,8 +676,15 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         }
         CUDA_TRY(cudaStreamSynchronize(s));
         flush_readback(ctx);  // the previous pipelined frame's read-back now overlaps this frame's sort
-        const uint64_t S = ctx->h_counters->splat_pair >> 32;
-        const uint64_t K = ctx->h_counters->splat_pair & 0xffffffffull;
+        const uint64_t S = ctx->h_counters->splats;
+        const uint64_t K = ctx->h_counters->pairs;
+        // Global ordinals (instance base + gaussian index) and record / pair indices are
+        // 32-bit: a frame past that is reported as out of memory (bench.cpp:94-97 skips it)
+        // instead of aliasing.
+        if (ctx->h_counters->gaussians > 0xffffffffull)
+            throw Status(GSCG_ERR_OOM, "instance-Gaussian count exceeds 32-bit ordinals");
+        if (S > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "splat count exceeds 32-bit indexing");
+        if (K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "tile-splat pair count exceeds 32-bit indexing");
         if (S <= ctx->splat_capacity && K <= ctx->pair_capacity) {
             if (lod_back && n) std::memcpy(frame->active_lod, ctx->h_lod, n * 4ull);
             ctx->S = S;
@@ -689,7 +696,6 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             break;
         }
         if (attempt > 2) throw Status(GSCG_ERR_STATE, "splat/pair capacity did not converge");
-        if (K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "tile-splat pair count exceeds 32-bit indexing");
         ctx->splat_capacity = std::max<uint64_t>(ctx->splat_capacity, S + S / 4 + 1024);
         ctx->pair_capacity = std::max<uint64_t>(ctx->pair_capacity, K + K / 4 + 1024);
     }
@@ -1464,7 +1470,7 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
         CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
         CUDA_TRY(cudaStreamSynchronize(s));
         ctx->S = recv_count;
-        ctx->K = ctx->h_counters->splat_pair;
+        ctx->K = ctx->h_counters->pairs;
         if (ctx->K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "band pair count exceeds 32-bit indexing");
         ctx->dmin = ctx->h_counters->depth_min_bits;
         ctx->dmax = ctx->h_counters->depth_max_bits;

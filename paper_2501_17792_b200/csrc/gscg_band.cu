@@ -154,7 +154,7 @@ k_band_unpack(BandUnpackParams p) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (s_pairs) atomicAdd(&p.counters->splat_pair, s_pairs);
+        if (s_pairs) atomicAdd(&p.counters->pairs, s_pairs);
         if (s_dmin != 0xffffffffu) atomicMin(&p.counters->depth_min_bits, s_dmin);
         atomicMax(&p.counters->depth_max_bits, s_dmax);
     }

@@ -60,8 +60,9 @@ struct CameraDev {
 
 // Frame-level counters written by the kernels and read back once per frame.
 struct FrameCounters {
-    unsigned long long splat_pair;  // (splats << 32) | pairs, advanced by block aggregates
-    unsigned long long gaussians;   // G of the frame
+    unsigned long long splats;     // S of the frame (record slots handed out), block aggregates
+    unsigned long long pairs;      // K of the frame (cell-splat pairs), warp aggregates
+    unsigned long long gaussians;  // G of the frame (global ordinals must stay below 2^32)
     uint32_t depth_min_bits;
     uint32_t depth_max_bits;
     uint32_t items_total;

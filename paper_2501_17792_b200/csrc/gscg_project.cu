@@ -291,7 +291,7 @@ k_project(ProjectParams p) {
             }
 
             // Record slots: ballot ranks inside the warp, warp counts across the CTA, one
-            // atomic per (CTA, instance) on the splat count (high word of splat_pair).
+            // atomic per (CTA, instance) on the frame's splat counter.
             pairs += n_tiles;
             const uint32_t bal = __ballot_sync(0xffffffffu, survive);
             if (lane == 0) s_wcnt[warp] = __popc(bal);
@@ -303,7 +303,7 @@ k_project(ProjectParams p) {
                 before += w < warp ? t : 0u;
                 total += t;
             }
-            if (tid == 0) s_base = atomicAdd(&p.counters->splat_pair, static_cast<unsigned long long>(total) << 32) >> 32;
+            if (tid == 0) s_base = atomicAdd(&p.counters->splats, static_cast<unsigned long long>(total));
             __syncthreads();
             const unsigned long long base = s_base;
             const uint32_t ordinal = gvalid ? s_member_base[k] + gi : 0u;
@@ -369,7 +369,7 @@ k_project(ProjectParams p) {
     if ((tid & 31) == 0) {
         if (dmin != 0xffffffffu) atomicMin(&p.counters->depth_min_bits, dmin);
         if (dmax != 0u) atomicMax(&p.counters->depth_max_bits, dmax);
-        if (pairs) atomicAdd(&p.counters->splat_pair, static_cast<unsigned long long>(pairs));  // low word: K
+        if (pairs) atomicAdd(&p.counters->pairs, static_cast<unsigned long long>(pairs));
     }
 }
 

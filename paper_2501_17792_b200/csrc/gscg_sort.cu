@@ -829,25 +829,13 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
     }
 #pragma unroll
     for (int d = 0; d < kRadix; ++d) s_cnt[d][tid] = 0u;
-    if (!kCount && tid < kRadix) {  // global base of digit tid: scanned digit totals + this block's offset
+    if (tid < kRadix) {  // global base of digit tid: scanned digit totals + this block's offset
         const uint32_t t = static_cast<uint32_t>(tid) <= dmask ? digit_total[tid] : 0u;
         s_base[tid] = warp_incl_scan(t, lane) - t + (static_cast<uint32_t>(tid) <= dmask ? block_digit[tid * blocks + blockIdx.x] : 0u);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) for_each_cell_t<kQuads>(sp[q], tiles_x, [&](uint32_t c) { ++s_cnt[c & dmask][tid]; });
     __syncthreads();
-    if (kCount) {  // digit d's pairs in this block: warp w sums its digits over all threads
-#pragma unroll
-        for (int dd = 0; dd < kDigitsPerWarp; ++dd) {
-            const int d = warp * kDigitsPerWarp + dd;
-            uint32_t v = 0;
-#pragma unroll
-            for (int k = 0; k < kPerLane; ++k) v += s_cnt[d][lane * kPerLane + k];
-            v = __reduce_add_sync(0xffffffffu, v);
-            if (lane == 0 && static_cast<uint32_t>(d) <= dmask) block_digit[d * blocks + blockIdx.x] = v;
-        }
-        return;
-    }
     // Exclusive scan over threads for each digit (warp w: kDigitsPerWarp digits, lane l:
     // kPerLane consecutive threads), then over digits: s_cnt becomes each thread's start.
 #pragma unroll

@@ -64,7 +64,8 @@ k_lod_plan(PlanParams p) {
         s_carry[g] = 0;
     }
     if (tid == 0) {
-        p.counters->splat_pair = 0ull;
+        p.counters->splats = 0ull;
+        p.counters->pairs = 0ull;
         p.counters->depth_min_bits = 0xffffffffu;
         p.counters->depth_max_bits = 0u;
         p.counters->item_cursor = 0u;

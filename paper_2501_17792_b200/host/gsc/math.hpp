@@ -253,17 +253,87 @@ inline Quat Quat::FromRotationMatrix(const Mat3& m) {
     return q;
 }
 
-// Eigen's setFromTwoVectors. The near-antiparallel branch (an SVD in Eigen) picks a
-// deterministic perpendicular axis instead; the synthetic generator almost never hits
-// it and the choice is documented as unpinned.
+// V.col(2) of Eigen's JacobiSVD<Matrix<float,2,3>>(m, ComputeFullV), m = [v0^T; v1^T], the
+// axis setFromTwoVectors takes for nearly opposite vectors. Eigen reaches it through the
+// R-SVD preconditioner: m is divided by its largest |coefficient|, ColPivHouseholderQR
+// factors the 3x2 adjoint (the larger-norm column first, ties keep the first;
+// makeHouseholder per column; the reflector applied to the other column), and V =
+// householderQ() is evaluated into the identity from the last reflector to the first; the
+// 2x2 Jacobi sweeps and the singular-value sort only rotate V's first two columns. The
+// synthetic generator hits this branch for about 3 Gaussians per 218 K-Gaussian template.
+inline Vec3 svd_null_axis(const Vec3& v0, const Vec3& v1) {
+    float scale = 0.0f;
+    for (int i = 0; i < 3; ++i) scale = std::fmax(scale, std::fmax(std::fabs(v0[i]), std::fabs(v1[i])));
+    if (scale == 0.0f) scale = 1.0f;
+    float a[2][3];
+    for (int i = 0; i < 3; ++i) {
+        a[0][i] = v0[i] / scale;
+        a[1][i] = v1[i] / scale;
+    }
+    const auto norm3 = [](const float* x) { return std::sqrt(x[0] * x[0] + (x[1] * x[1] + x[2] * x[2])); };
+    if (norm3(a[1]) > norm3(a[0])) {
+        for (int i = 0; i < 3; ++i) {
+            const float t = a[0][i];
+            a[0][i] = a[1][i];
+            a[1][i] = t;
+        }
+    }
+    float e0[2] = {0.0f, 0.0f}, tau0 = 0.0f;
+    {
+        const float c0 = a[0][0];
+        const float tail = a[0][1] * a[0][1] + a[0][2] * a[0][2];
+        if (tail > 1.17549435e-38f) {  // numeric_limits<float>::min()
+            float beta = std::sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0f) beta = -beta;
+            e0[0] = a[0][1] / (c0 - beta);
+            e0[1] = a[0][2] / (c0 - beta);
+            tau0 = (beta - c0) / beta;
+        }
+    }
+    float b[3] = {a[1][0], a[1][1], a[1][2]};
+    if (tau0 != 0.0f) {
+        float tmp = e0[0] * b[1] + e0[1] * b[2];
+        tmp = tmp + b[0];
+        b[0] = b[0] - tau0 * tmp;
+        b[1] = b[1] - tmp * (tau0 * e0[0]);
+        b[2] = b[2] - tmp * (tau0 * e0[1]);
+    }
+    float e1 = 0.0f, tau1 = 0.0f;
+    {
+        const float c0 = b[1];
+        const float tail = b[2] * b[2];
+        if (tail > 1.17549435e-38f) {
+            float beta = std::sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0f) beta = -beta;
+            e1 = b[2] / (c0 - beta);
+            tau1 = (beta - c0) / beta;
+        }
+    }
+    float q[3] = {0.0f, 0.0f, 1.0f};
+    if (tau1 != 0.0f) {
+        float tmp = e1 * q[2];
+        tmp = tmp + q[1];
+        q[1] = q[1] - tau1 * tmp;
+        q[2] = q[2] - tmp * (tau1 * e1);
+    }
+    if (tau0 != 0.0f) {
+        float tmp = e0[0] * q[1] + e0[1] * q[2];
+        tmp = tmp + q[0];
+        q[0] = q[0] - tau0 * tmp;
+        q[1] = q[1] - tmp * (tau0 * e0[0]);
+        q[2] = q[2] - tmp * (tau0 * e0[1]);
+    }
+    return Vec3(q[0], q[1], q[2]);
+}
+
+// Eigen's setFromTwoVectors (dummy_precision<float> = 1e-5).
 inline Quat Quat::FromTwoVectors(const Vec3& a, const Vec3& b) {
     const Vec3 v0 = a.normalized();
     const Vec3 v1 = b.normalized();
     float c = v1.dot(v0);
     if (c < -1.0f + 1e-5f) {
         c = std::fmax(c, -1.0f);
-        Vec3 axis = std::fabs(v0[0]) < 0.9f ? Vec3(1, 0, 0).cross(v0) : Vec3(0, 1, 0).cross(v0);
-        axis = axis.normalized();
+        const Vec3 axis = svd_null_axis(v0, v1);
         const float w2 = (1.0f + c) * 0.5f;
         const float s = std::sqrt(1.0f - w2);
         return Quat(std::sqrt(w2), axis[0] * s, axis[1] * s, axis[2] * s);

@@ -1,6 +1,8 @@
 """Golden fixtures (tests/golden/*.npz, made by tests/golden/make_golden.py).
 
-CPU: the host generator + oracle still reproduce every fixture bit for bit.
+CPU: the code each fixture came from (the reference build for RGB fixtures, the oracle for
+the SH-extension one) and the oracle restatement + the product's host generator both
+still reproduce every fixture bit for bit.
 GPU: the CUDA path reproduces the fixtures through the C-ABI with the same bars as the
 live-oracle parity tests (tests/parity.py), without running the oracle.
 """
@@ -48,19 +50,24 @@ def test_golden_fixtures_present():
     assert len(CASES) >= 2
 
 
+@pytest.mark.parametrize("source", ["fixture", "oracle"])
 @pytest.mark.parametrize("name", CASES)
-def test_oracle_reproduces_golden(name):
+def test_reproduces_golden(name, source):
     import sys
     sys.path.insert(0, str(GOLDEN))
     from make_golden import render_case
+    from oracle import ref
 
     meta, gold = load(name)
+    src = meta.get("source", "oracle") if source == "fixture" else "oracle"
+    if src == "reference" and not ref.available():
+        pytest.skip("reference build (oracle/_ref) unavailable")
     cfg = meta["config"]
     cfg = {k: tuple(v) if isinstance(v, list) else v for k, v in cfg.items()}
-    now = render_case(cfg, meta["render"])
+    now = render_case(cfg, meta["render"], src)
     for k, v in gold.items():
         assert now[k].dtype == v.dtype and now[k].shape == v.shape, k
-        assert now[k].tobytes() == v.tobytes(), f"{name}: {k} drifted from the golden fixture"
+        assert now[k].tobytes() == v.tobytes(), f"{name}: {k} drifted from the golden fixture ({src})"
 
 
 @pytest.mark.gpu

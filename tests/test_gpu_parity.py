@@ -335,8 +335,9 @@ def test_convex_hull_and_transmittance_range():
     assert T.min() >= 0.0 and T.max() <= 1.0
 
 
-def config_scene(idx):
+def config_scene(idx, sh=True):
     cfg, extra = P.baseline_config(idx)
+    cfg.with_sh = sh
     s = P.Scene(cfg)
     if extra["origin_instance"]:
         P.place_origin_instance(s)
@@ -457,3 +458,88 @@ def test_instance_cull_is_invisible_for_any_camera_matrix():
     assert np.array_equal(a[4], b[4])
     assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
     assert a[2][1] > 0  # something is on screen
+
+
+def config5_scene(count: int):
+    """BASELINE config 5 (LoD off: every character at the full 202,738-Gaussian level,
+    crowd.cpp:94-96 forced LoD) on its own grid and camera, the first `count` characters
+    (row-major cells: the near field, where splats are largest and pairs densest)."""
+    cfg, extra = P.baseline_config(5)
+    cfg.crowd_count = count
+    return P.Scene(cfg), extra
+
+
+@pytest.mark.slow
+def test_config5_forced_lod0_crowd_against_oracle():
+    """Config-5 code paths at crowd scale: 240 characters at LoD 0, 1920x1080 (48.7 M
+    instance-Gaussians, tens of millions of splats, horizon cells with long tied runs),
+    every bit-exact bar against the oracle."""
+    s, extra = config5_scene(240)
+    r = P.Renderer(s, device_poses=True)
+    o = orc.from_scene(s)
+    g, c = render_both(s, r, o, 0.25, forced_lod=extra["forced_lod"])
+    rep = check_frame(s, r, o, g, c)
+    assert rep["G"] == 240 * 202738 and rep["S"] > 20_000_000 and rep["K"] > 40_000_000
+
+
+def test_pair_count_past_32_bits_is_reported_as_oom():
+    """K >= 2^32 tile-splat pairs (config 5 at tile size 2: ~5 G pairs) must surface as
+    GSCG_ERR_OOM (the reference's bench skips such a cell as "out of memory",
+    bench.cpp:94-97) before any buffer is grown, not alias into the splat count; the
+    context stays usable afterwards."""
+    from paper_2501_17792_b200 import native as N
+
+    s, extra = config5_scene(3500)
+    r = P.Renderer(s, device_poses=True)
+    with pytest.raises(N.NativeError) as e:
+        r.render_frame(0.0, P.RenderSettings(tile_size=2), forced_lod=0)
+    assert e.value.status == N.GSCG_ERR_OOM and "pair count" in str(e.value)
+    rgb, _ = r.render_frame(0.0, P.RenderSettings(), forced_lod=2)  # same context, a normal frame
+    assert r.counts()[1] > 0 and np.isfinite(rgb).all()
+
+
+def test_instance_gaussians_past_32_bit_ordinals_is_reported_as_oom():
+    """Global ordinals (instance base + gaussian index, the reference's (instance,
+    gaussian) tie-break) are 32-bit: 22,500 characters at LoD 0 (4.56 G instance-
+    Gaussians) must fail with GSCG_ERR_OOM rather than wrap and break the sort order."""
+    from paper_2501_17792_b200 import native as N
+
+    cfg, _ = P.baseline_config(5)
+    cfg.grid_rows, cfg.grid_cols, cfg.crowd_count = 150, 150, 22500
+    r = P.Renderer(P.Scene(cfg), device_poses=True)
+    with pytest.raises(N.NativeError) as e:
+        r.render_frame(0.0, P.RenderSettings(), forced_lod=0)
+    assert e.value.status == N.GSCG_ERR_OOM and "ordinals" in str(e.value)
+
+
+def gpu_vs_reference_build(idx: int, device_poses: bool = False) -> dict:
+    """The CUDA path against the REFERENCE's own render_frame (oracle/_ref: its unmodified
+    sources built against the Eigen-subset shim; prebuilt .so shipped with the repo), on
+    the reference's own synthetic scene (RGB colour: the reference has no SH)."""
+    from oracle import ref
+
+    if not ref.LIB_PATH.exists():
+        pytest.skip("prebuilt reference (oracle/_ref/libgsc_ref.so) not shipped")
+    s, extra = config_scene(idx, sh=False)
+    rc, rextra = ref.baseline(idx)
+    rs = ref.RefScene(rc, rextra["origin_instance"])
+    assert s.instances.tobytes() == rs.instances.tobytes()
+    r = P.Renderer(s, device_poses=device_poses)
+    from paper_2501_17792_b200 import native as N
+    r.set_debug(N.GSCG_DEBUG_POSED | N.GSCG_DEBUG_RECORDS)
+    t = extra["time_s"] + 0.25
+    rgb, T = r.render_frame(t, P.RenderSettings(sh_colour=False), forced_lod=extra["forced_lod"])
+    out_r = rs.render(t, ref.settings(), forced_lod=extra["forced_lod"])
+    return check_frame(s, r, rs, (rgb, T), out_r)
+
+
+@pytest.mark.parametrize("idx", [1, 2])
+def test_gpu_matches_reference_build(idx):
+    rep = gpu_vs_reference_build(idx)
+    assert rep["S"] > 90_000
+
+
+@pytest.mark.slow
+def test_gpu_matches_reference_build_config3():
+    rep = gpu_vs_reference_build(3, device_poses=True)
+    assert rep["G"] == 14972565
