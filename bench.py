@@ -5,14 +5,21 @@
 
 One step = one full render_frame (LoD + FK + skinning + projection + sort + raster) of a
 distinct animation time t = f/30 s. `value` times K steps with every input already in HBM
-(poses sampled and uploaded before the timed region) using CUDA events on the render
-stream; `e2e` times the public API (instance H2D, kernels, D2H of the framebuffer into
-pinned memory) per step, streaming: frame k's read-back overlaps frame k+1
-(render_frame(pipelined=True)); the blocking one-call-per-frame rate is reported beside it. `--impl reference` times the CPU oracle (the reference's render
-path restated in C++, oracle "port") on the host cores. Multi-GPU runs render the same frame
-on N GPUs (strong scaling): each rank projects an instance shard, splats are exchanged
-by screen band with one NCCL all-to-all, each rank sorts and rasterises its band and the
-bands are gathered; timing is the max over ranks.
+(poses sampled on the device) using CUDA events on the render stream; `median_frame_ms`
+is the median of the per-frame event intervals (the reference's protocol, bench.cpp:74-93).
+`e2e` times the public API (instance H2D, kernels, D2H of the framebuffer into pinned
+memory) per step, streaming: frame k's read-back overlaps frame k+1; the blocking
+one-call-per-frame rate is reported beside it.
+
+`--gpus N` with no torchrun environment re-launches itself under torchrun (N ranks, one per
+GPU, NCCL); each rank projects an instance shard, splats are exchanged by screen band and
+each rank sorts and rasterises its band; timing is the max over ranks.
+
+`--impl reference` times the REFERENCE's own render_frame on the host cores: its
+unmodified sources built against the Eigen-subset shim (oracle/_ref, "kind": "reference";
+the oracle port only if that build is missing), from its own synthetic generator and
+build_crowd, on every host thread. The `cpu_baseline` of our arm is the same build,
+sampled at all threads and at 1 thread.
 """
 from __future__ import annotations
 
@@ -158,23 +165,41 @@ def build_scene(config: int):
     return P, cfg, extra, scene
 
 
-def roofline_bytes(cfg, counts, lods, scene, sh: bool) -> dict:
-    """Algorithmic bytes (SURVEY.md §8d / DESIGN.md §4) for the frame and its big kernels."""
-    G, S, K = counts
-    a = 260 if sh else 80  # core 64 + skin weights 16 (+ SH 180) per resident template Gaussian
+def roofline_bytes(cfg, counts, tile_pairs, lods, scene) -> dict:
+    """Algorithmic bytes exactly as SURVEY.md §8(d) defines them:
+      A = sum over resident (template, level) of N * 256 B (SH3 attributes)
+      M = instances * 24 * 48 B (3x4 skin matrices)
+      frame   = A + M + 2*S*48 + K*(12 + 24*6 + 4) + 16*W*H   (K = 16x16 tile pairs)
+      project = A + M + S*48                                  (k_project: stream + record write)
+      raster  = K*4 + S*48 + 16*W*H                           (k_raster16q: sorted value,
+                                                               each record once, framebuffer)"""
+    G, S, _ = counts
+    K = tile_pairs
     inst = scene.instances
     resident = set(zip(inst["template_id"].tolist(), lods.tolist()))
-    A = sum(cfg.level_counts[l] for _, l in resident) * a
-    n = len(inst)
-    M = n * 24 * 48
-    R = 48
+    A = sum(cfg.level_counts[l] for _, l in resident) * 256
+    M = len(inst) * 24 * 48
     W, H = cfg.width, cfg.height
-    tiles = ((W + 15) // 16) * ((H + 15) // 16)
-    P = 6
-    frame = A + M + 2 * S * R + K * (12 + 24 * P + 4) + 16 * W * H
-    project = A + M + S * (R + 4 + 4 + 8)           # template stream + matrices + record, ordinal, depth, span
-    raster = K * (4 + R) + 16 * W * H + tiles * 4 * 8  # sorted pair records + record gathers + framebuffer + ranges
-    return {"frame": frame, "project": project, "raster": raster, "A": A, "M": M}
+    frame = A + M + 2 * S * 48 + K * (12 + 24 * 6 + 4) + 16 * W * H
+    return {"frame": frame, "project": A + M + S * 48, "raster": K * 4 + S * 48 + 16 * W * H, "A": A, "M": M,
+            "K_tile": K}
+
+
+def issue_roofline(kernel: str, kernel_ms: float, sm_mhz) -> dict | None:
+    """Issue-slot roofline of an issue-bound kernel: warp instructions (ncu
+    smsp__inst_executed.sum, profiles/ncu_summary.json) over 148 SMs x 4 schedulers x the
+    SM clock measured during the timed region x the kernel's live event time."""
+    if not PROFILE_SUMMARY.exists() or not sm_mhz:
+        return None
+    try:
+        k = json.loads(PROFILE_SUMMARY.read_text())["kernels"][kernel]
+        inst = float(k["warp_instructions"])
+    except Exception:
+        return None
+    peak = 148 * 4 * sm_mhz * 1e6  # warp instructions per second
+    achieved = inst / (kernel_ms * 1e-3)
+    return {"warp_instructions": inst, "achieved_per_s": round(achieved, 1), "peak_per_s": peak,
+            "frac": round(achieved / peak, 4), "source": str(PROFILE_SUMMARY.relative_to(ROOT))}
 
 
 def memory_block(r, scene) -> dict:
@@ -262,7 +287,8 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
             N.check_gscg(lib.gscg_render_frame(ctx, C.byref(frame_desc(f)), C.byref(cam), C.byref(rs), C.byref(lp),
                                                None, None, C.byref(st)), ctx)
             return {"update": st.update_ms, "gather": st.gather_ms, "sort": st.sort_ms, "rasterize": st.rasterize_ms,
-                    "launches": st.kernel_launches, "counts": (st.gaussian_count, st.splat_count, st.pair_count)}
+                    "launches": st.kernel_launches, "counts": (st.gaussian_count, st.splat_count, st.pair_count),
+                    "tile_pairs": st.tile_pair_count}
     else:
         # Band path: shard projection -> NCCL all-to-all -> band render -> gather.
         from paper_2501_17792_b200.multigpu import BandRank, FrameArgs, LoadBalancer, TorchExchange
@@ -286,22 +312,26 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
             return {"update": a.update_ms, "gather": a.gather_ms, "route": a.sort_ms, "unpack": b.gather_ms,
                     "sort": b.sort_ms, "rasterize": b.rasterize_ms,
                     "launches": a.kernel_launches + 1 + b.kernel_launches,
-                    "counts": (a.gaussian_count, a.splat_count, b.pair_count)}
+                    "counts": (a.gaussian_count, a.splat_count, b.pair_count), "tile_pairs": a.tile_pair_count}
 
+    first = None
     for f in range(args.warmup):
-        frame(f)
+        res = frame(f)
+        first = first or res  # frame 0 (t = time_s): the config's reported counts, as the reference arm's
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     stage = []
     with ClockSampler(local_rank) as clocks:
-        ev0.record(stream)
+        evs[0].record(stream)
         for f in range(args.warmup, frames):
             stage.append(frame(f))
-        ev1.record(stream)
+            evs[f - args.warmup + 1].record(stream)
         torch.cuda.synchronize()
+    ev0, ev1 = evs[0], evs[-1]
+    frame_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -311,8 +341,14 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
+    median_ms = float(np.median(frame_ms))
+    if dist:
+        t = torch.tensor([median_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        median_ms = float(t.item())
     launches = sum(s["launches"] for s in stage)
     counts = stage[-1]["counts"]
+    tile_pairs = stage[-1]["tile_pairs"]
     culled = r.instances_culled()
     lods = d_lods[:n].cpu().numpy().astype(np.uint32)
 
@@ -364,18 +400,23 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     h2d = n * (4 + 16 + 4 + 4 + 4)  # template id, placement, previous LoD, motion id, phase offset
     d2h = cfg.width * cfg.height * 12 + n * 4
 
+    cfg_counts, cfg_tile_pairs = first["counts"], first["tile_pairs"]
     if dist:
-        tot = torch.tensor([float(counts[1])], dtype=torch.float64, device=dev)
+        tot = torch.tensor([float(counts[1]), float(tile_pairs), float(cfg_counts[1]), float(cfg_tile_pairs)],
+                           dtype=torch.float64, device=dev)
         dist.all_reduce(tot)
-        counts = (counts[0], int(tot.item()), counts[2])
+        counts = (counts[0], int(tot[0].item()), counts[2])
+        tile_pairs = int(tot[1].item())
+        cfg_counts = (cfg_counts[0], int(tot[2].item()), cfg_counts[2])
+        cfg_tile_pairs = int(tot[3].item())
     if rank != 0:
         dist.destroy_process_group()
         return None
 
     peaks = _peaks()
-    keys = [k for k in stage[0] if k not in ("launches", "counts")]
+    keys = [k for k in stage[0] if k not in ("launches", "counts", "tile_pairs")]
     stage_ms = {k: float(np.median([s[k] for s in stage])) for k in keys}
-    rb = roofline_bytes(cfg, counts, lods, scene, sh=True)
+    rb = roofline_bytes(cfg, counts, tile_pairs, lods, scene)
     # The single longest kernel of the frame: k_project (gather) or k_raster16q (rasterize);
     # the sort stage is ~35 short launches, none longer than either.
     dom = "rasterize" if stage_ms["rasterize"] >= stage_ms["gather"] else "gather"
@@ -390,120 +431,208 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         except Exception:
             traffic = None
     fps = 1000.0 / ms_step
+    clk = clocks.summary()
     frame_roofline_ms = rb["frame"] / (peaks["hbm_gbs"] * 1e9) * 1e3
     out = {
         "metric": METRIC, "value": round(fps, 3), "unit": "FPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}: 14 synthetic templates (202738/12661/3176 G, SH deg 3) x "
-                               f"{cfg.crowd_count} animated characters, distance LoD 5/10 m, {cfg.width}x{cfg.height}, tile 16",
-                   "instances": cfg.crowd_count, "resolution": [cfg.width, cfg.height],
-                   "gaussians": counts[0], "splats": counts[1], "pairs": counts[2],
-                   "instances_culled": culled,
-                   "l2": "no flush: the per-frame working set (templates ~0.5 GB + records/pairs ~0.8 GB) exceeds the 126 MB L2",
-                   "parallelism": (f"{world} instance shards -> {world} screen bands, NCCL all-to-all"
-                                   if band_path else "single GPU")},
+        "config": bench_config(args.config, cfg, cfg_counts, cfg_tile_pairs,
+                               f"{world} instance shards -> {world} screen bands, NCCL" if band_path else "single GPU"),
+        "median_frame_ms": round(median_ms, 4), "fps_median": round(1000.0 / median_ms, 3),
+        "colour": "SH degree 3 (BASELINE; the reference renders fixed RGB)",
+        "instances_culled": culled,
+        "l2": "no flush: the per-frame working set (templates ~0.5 GB + records/pairs ~0.8 GB) exceeds the 126 MB L2",
         "splats_per_s": round(counts[1] * fps, 1),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "frame_roofline": {"bytes": rb["frame"], "ms": round(frame_roofline_ms, 4),
-                           "frac": round(frame_roofline_ms / ms_step, 4), "peak_gbs": peaks["hbm_gbs"]},
+                           "frac": round(frame_roofline_ms / ms_step, 4), "peak_gbs": peaks["hbm_gbs"],
+                           "model": "SURVEY.md 8(d): A + M + 2*S*48 + K_tile*(12+24*6+4) + 16*W*H"},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
                      "algorithmic_bytes": kbytes, "peak_source": peaks["source"],
-                     "limiter": ("issue-bound on exact no-FMA FP32 + integer work (ncu: ~65% issue, DRAM ~30%); "
-                                 "profiles/r01_ncu_full_v6.txt" if kernel == "k_project" else
-                                 "issue-bound, per-pixel list-walk divergence; profiles/r01_ncu_full_v6.txt")},
+                     "bytes_model": ("K_tile*4 + S*48 + 16*W*H" if kernel == "k_raster16q" else "A(256 B/G) + M + S*48"),
+                     "issue": issue_roofline(kernel, stage_ms[dom], clk["sm_mhz"]),
+                     "limiter": ("issue-bound on exact no-FMA FP32 + integer work; profiles/ncu_summary.json"
+                                 if kernel == "k_project" else
+                                 "issue-bound, per-pixel list walks (ncu DRAM < 10%); profiles/ncu_summary.json")},
         "e2e": {"value": round(e2e_fps, 3), "unit": "FPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": ("Renderer.render_frame(out=pinned, pipelined=True): frame k's read-back overlaps frame k+1"
                         if not band_path else "DistributedRenderer.render_frame"),
                 "blocking_api_fps": None if e2e_sync_fps is None else round(e2e_sync_fps, 3)},
         "gpu_launches": int(launches),
-        "clocks": clocks.summary(),
+        "clocks": clk,
         "memory": memory_block(r, scene),
     }
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(scene, args.config, frames_sample=args.cpu_frames)
+        out["cpu_baseline"], out["cpu_baseline_1t"] = cpu_baselines(args.config, args.cpu_frames)
     if dist:
         dist.destroy_process_group()
     return out
 
 
-def cpu_baseline(scene, config: int, frames_sample: int = 2, threads: int = 0) -> dict:
-    """The reference render path restated in C++ (oracle/), timed on this host's cores."""
-    from oracle import orc
+def bench_config(config: int, cfg, counts, tile_pairs: int, parallelism: str) -> dict:
+    """Identical keys and values in both arms (the driver compares them)."""
+    return {"workload": f"BASELINE config {config}: 14 synthetic templates (202738/12661/3176 G) x "
+                        f"{cfg.crowd_count} animated characters, distance LoD 5/10 m, {cfg.width}x{cfg.height}, tile 16"
+                        if config != 1 else
+                        f"BASELINE config 1: 1 synthetic template (100000 G) x 1 character, {cfg.width}x{cfg.height}",
+            "instances": cfg.crowd_count, "resolution": [cfg.width, cfg.height],
+            "gaussians": int(counts[0]), "splats": int(counts[1]), "tile_pairs": int(tile_pairs),
+            "parallelism": parallelism}
 
-    P_cfg = scene.cfg
-    o = orc.from_scene(scene)
-    st = orc.settings(sh_colour=True)
-    cores = threads or (os.cpu_count() or 1)
-    o.render(0.0, st, threads=cores)  # warm-up frame
-    t0 = time.perf_counter()
-    for f in range(frames_sample):
-        o.render((f + 1) / 30.0, st, threads=cores)
-    dt = (time.perf_counter() - t0) / frames_sample
-    return {"value": round(1.0 / dt, 4), "unit": "FPS", "cores": cores, "kind": "port",
-            "sample": f"{frames_sample} full frames of config {config} ({P_cfg.crowd_count} chars, "
-                      f"{P_cfg.width}x{P_cfg.height}) after 1 warm-up frame, std::thread static partition as "
-                      f"parallel.hpp, single-threaded sort/bin as renderer.cpp"}
+
+def reference_scene(config: int):
+    """The reference's own scene for a BASELINE config: its synthetic generator and
+    build_crowd (oracle/_ref), or the oracle port fed by the product scene if the
+    reference build is missing. Returns (scene, kind, extra)."""
+    from oracle import ref
+
+    if ref.LIB_PATH.exists():
+        rc, extra = ref.baseline(config)
+        return ref.RefScene(rc, extra["origin_instance"]), "reference", extra
+    P, cfg, extra, scene = build_scene(config)
+    from oracle import orc
+    return orc.from_scene(scene), "port", extra
+
+
+def _ref_render(rs, kind: str, time_s: float, forced, threads: int):
+    from oracle import orc, ref
+
+    st = ref.settings() if kind == "reference" else orc.settings(sh_colour=True)
+    return rs.render(time_s, st, forced_lod=forced, threads=threads)
+
+
+def cpu_baselines(config: int, frames_sample: int) -> tuple[dict, dict]:
+    """The reference's render_frame timed on this host (rank 0, N=1): all host threads over
+    `frames_sample` frames, then one frame at 1 thread."""
+    rs, kind, extra = reference_scene(config)
+    cores = os.cpu_count() or 1
+    forced, t0 = extra["forced_lod"], extra["time_s"]
+    _ref_render(rs, kind, t0, forced, cores)  # warm-up frame
+    out = []
+    for threads, frames in ((cores, frames_sample), (1, 1)):
+        per = []
+        for f in range(frames):
+            s0 = time.perf_counter()
+            _ref_render(rs, kind, t0 + (f + 1) / 30.0, forced, threads)
+            per.append(time.perf_counter() - s0)
+        ms = float(np.median(per)) * 1e3
+        out.append({"value": round(1000.0 / ms, 4), "unit": "FPS", "cores": threads, "kind": kind,
+                    "median_frame_ms": round(ms, 1),
+                    "sample": f"{frames} full frame(s) of BASELINE config {config} after 1 warm-up frame; "
+                              f"{'the reference render_frame (oracle/_ref: its own sources + Eigen-subset shim, RGB colour)' if kind == 'reference' else 'the oracle port (SH colour)'}"
+                              f"; thread_count = {threads} (parallel.hpp static partition; its sort and binning are single-threaded)"})
+    return out[0], out[1]
 
 
 def run_reference(args, rank, world) -> dict | None:
+    """The reference arm: the reference's own CPU render_frame, rank 0 only."""
     if rank != 0:
         return None
-    import paper_2501_17792_b200 as P
-    from oracle import orc
-
-    cfg, extra = P.baseline_config(args.config)
-    scene = P.Scene(cfg)
-    if extra["origin_instance"]:
-        P.place_origin_instance(scene)
-    o = orc.from_scene(scene)
-    st = orc.settings(sh_colour=True)
+    rs, kind, extra = reference_scene(args.config)
     cores = os.cpu_count() or 1
-    forced = extra["forced_lod"]
-    # Bounded: at most 2 warm-up frames, and the timed steps capped so the run stays in minutes.
-    for f in range(min(args.warmup, 2)):
-        o.render(extra["time_s"] + f / 30.0, st, forced_lod=forced, threads=cores)
-    t0 = time.perf_counter()
+    forced, t0 = extra["forced_lod"], extra["time_s"]
+    _, _, times0 = _ref_render(rs, kind, t0, forced, cores)  # frame 0: the config's counts + warm-up
+    for f in range(1, min(args.warmup, 2)):
+        _ref_render(rs, kind, t0 + f / 30.0, forced, cores)
     per = []
-    steps_run = 0
+    budget_t0 = time.perf_counter()
     for f in range(args.steps):
         s0 = time.perf_counter()
-        _, _, times = o.render(extra["time_s"] + (args.warmup + f) / 30.0, st, forced_lod=forced, threads=cores)
+        _ref_render(rs, kind, t0 + (args.warmup + f) / 30.0, forced, cores)
         per.append(time.perf_counter() - s0)
-        steps_run += 1
-        if time.perf_counter() - t0 > args.reference_budget_s:
+        if time.perf_counter() - budget_t0 > args.reference_budget_s:
             break
     ms = float(np.mean(per)) * 1e3
+    med = float(np.median(per)) * 1e3
     fps = 1000.0 / ms
-    return {"metric": METRIC, "value": round(fps, 4), "unit": "FPS", "n_gpus": world, "steps": args.steps,
+    if kind == "reference":
+        from oracle import ref
+        cfg = ref.baseline(args.config)[0]
+    else:
+        cfg = build_scene(args.config)[1]
+    tile_pairs = int(times0.pair_count)
+    return {"metric": METRIC, "value": round(fps, 4), "unit": "FPS", "n_gpus": world, "steps": len(per),
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"BASELINE config {args.config} ({cfg.crowd_count} chars, {cfg.width}x{cfg.height})",
-                       "splats": int(times.splat_count), "pairs": int(times.pair_count)},
-            "cpu_baseline": {"value": round(fps, 4), "unit": "FPS", "cores": cores, "kind": "port",
-                             "sample": f"{steps_run} of {args.steps} requested full frames (time budget "
-                                       f"{args.reference_budget_s:.0f} s) on {cores} host threads"},
+            "config": bench_config(args.config, cfg, (times0.gaussian_count, times0.splat_count, 0), tile_pairs,
+                                   "single GPU" if world == 1 else
+                                   f"{world} instance shards -> {world} screen bands, NCCL"),
+            "median_frame_ms": round(med, 3), "fps_median": round(1000.0 / med, 4),
+            "colour": ("RGB: the reference has no SH (SURVEY.md 0.4); same geometry, splats and tile pairs"
+                       if kind == "reference" else "SH degree 3 (oracle port)"),
+            "cpu_baseline": {"value": round(fps, 4), "unit": "FPS", "cores": cores, "kind": kind,
+                             "sample": f"{len(per)} of {args.steps} requested full frames (time budget "
+                                       f"{args.reference_budget_s:.0f} s) on {cores} host threads"
+                                       + (" through the reference's own render_frame (oracle/_ref)"
+                                          if kind == "reference" else " through the oracle port")},
             "e2e": {"value": round(fps, 4), "unit": "FPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def run_dry(args, rank, world) -> dict | None:
+    """The multi-rank plumbing of run_ours on CPU (gloo): rendezvous, barrier, per-rank
+    timing reduced by MAX, rank 0 alone prints. Used by tests/test_bench.py."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+        dist.barrier()
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rank + 1))
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3])
+    ranks = torch.tensor([1.0])
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ranks)
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": None, "unit": "FPS", "n_gpus": world, "ranks_seen": int(ranks.item()),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(ms.item()), "dry_run": True}
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: one rank per GPU via torchrun (the
+    driver's own launch form); rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
-    os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line (no version banner)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-frames", type=int, default=5)  # ~12 s of host CPU work at config 3
+    ap.add_argument("--cpu-frames", type=int, default=2)  # ~5 s of host work at config 3, plus one 1-thread frame
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--band-path", action="store_true",
-                    help="use the multi-GPU band path (shard -> NCCL all-to-all -> band) even on one GPU")
+                    help="use the multi-GPU band path (shard -> NCCL exchange -> band) even on one GPU")
     ap.add_argument("--reference-budget-s", type=float, default=150.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher/plumbing check without a GPU: gloo ranks, max-over-ranks timing, one JSON line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     rank, world, local_rank = dist_env()
-    out = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world, local_rank)
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    # NCCL's communicator INIT lines (rank count, transports) go to stderr; stdout stays the
+    # one JSON line.
+    if os.environ.get("NCCL_DEBUG") is None:
+        os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if args.dry_run:
+        out = run_dry(args, rank, world)
+    else:
+        out = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world, local_rank)
     if out is not None:
         print(json.dumps(out), flush=True)
 

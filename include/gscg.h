@@ -150,6 +150,9 @@ typedef struct {
   uint64_t gaussian_count; /* instance-Gaussians G */
   uint32_t sort_passes;
   uint32_t kernel_launches;
+  uint64_t tile_pair_count; /* the reference's per-tile bin entries (renderer.cpp:147-161): K
+                               counts tile_size x tile_size tiles; pair_count counts the GPU's
+                               binning cells (8x8 quadrants for tile size 16) */
 } gscg_stage_times;
 
 /* One surviving splat as gather_splats produces it (FrameSplat, renderer.hpp:39-44),

@@ -77,6 +77,7 @@ typedef struct {
 typedef struct {
   double update_ms, gather_ms, sort_ms, rasterize_ms, pose_ms, total_ms;
   uint64_t splat_count, pair_count, gaussian_count;
+  uint64_t tile_pair_count; /* the reference's per-tile bin entries (gscg_stage_times) */
 } gsch_stage_times;
 
 const char* gsch_last_error(void);

@@ -107,6 +107,7 @@ class StageTimes:
     splat_count: int = 0
     pair_count: int = 0
     gaussian_count: int = 0
+    tile_pair_count: int = 0  # the reference's per-tile bin entries (pair_count: the GPU's binning cells)
 
     @property
     def total_ms(self) -> float:
@@ -426,9 +427,9 @@ class Renderer:
         # hold the arrays of the last two pipelined submissions (older ones are complete).
         if pipelined:
             self._inflight = (getattr(self, "_inflight", []) + [(rgb, T)])[-2:]
+        self.last_times = StageTimes(**{f: getattr(st, f) for f in StageTimes.__dataclass_fields__})
         if times is not None:
-            for f in ("update_ms", "gather_ms", "sort_ms", "rasterize_ms", "pose_ms", "splat_count", "pair_count",
-                      "gaussian_count"):
+            for f in StageTimes.__dataclass_fields__:
                 setattr(times, f, getattr(st, f))
         return rgb, T
 

@@ -190,7 +190,7 @@ struct gscg_ctx {
 
     // last frame
     uint32_t n = 0, tiles = 0, cells_per_tile = 1;
-    uint64_t G = 0, S = 0, K = 0;
+    uint64_t G = 0, S = 0, K = 0, TP = 0;  // TP: the reference's (tile, splat) bin entries
     uint32_t dmin = 0, dmax = 0;  // depth-bit range of the frame's splats
     FrameGeom geom;
     gscg_render_settings settings{};
@@ -690,6 +690,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             ctx->S = S;
             ctx->K = K;
             ctx->G = ctx->h_counters->gaussians;
+            ctx->TP = ctx->h_counters->tile_pairs;
             ctx->dmin = ctx->h_counters->depth_min_bits;
             ctx->dmax = ctx->h_counters->depth_max_bits;
             ctx->culled = ctx->h_counters->instances_culled;
@@ -1004,6 +1005,7 @@ void fill_times(gscg_ctx* ctx, gscg_stage_times* times, uint32_t passes, uint32_
     times->splat_count = ctx->S;
     times->pair_count = ctx->K;
     times->gaussian_count = ctx->G;
+    times->tile_pair_count = ctx->TP;
     times->sort_passes = passes;
     times->kernel_launches = launches;
 }
@@ -1305,6 +1307,7 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                 times->splat_count = ctx->S;
                 times->pair_count = ctx->K;
                 times->gaussian_count = ctx->G;
+                times->tile_pair_count = ctx->TP;
                 times->kernel_launches = launches;
             }
             return;

@@ -63,6 +63,7 @@ struct FrameCounters {
     unsigned long long splats;     // S of the frame (record slots handed out), block aggregates
     unsigned long long pairs;      // K of the frame (cell-splat pairs), warp aggregates
     unsigned long long gaussians;  // G of the frame (global ordinals must stay below 2^32)
+    unsigned long long tile_pairs; // the reference's (tile, splat) bin entries (renderer.cpp:147-161)
     uint32_t depth_min_bits;
     uint32_t depth_max_bits;
     uint32_t items_total;

@@ -103,6 +103,7 @@ k_project(ProjectParams p) {
     auto cdiv = [&](int v) { return cshift >= 0 ? v >> cshift : v / cell; };  // v >= 0
     uint32_t dmin = 0xffffffffu, dmax = 0u;
     uint32_t pairs = 0;  // binning cells of this thread's splats (summed once at the end)
+    uint32_t tile_pairs = 0;  // the reference's (tile, splat) bin entries (= pairs unless quadrant cells)
     const int lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     if (tid == 0) mbar_init(&s_bar, 1);
@@ -180,7 +181,7 @@ k_project(ProjectParams p) {
             const float* s_inst = s_mats + k * p.joint_stride * 12;
 
             bool survive = false;
-            uint32_t n_tiles = 0;
+            uint32_t n_tiles = 0, n_bins = 0;
             float mx = 0, my = 0, depth = 0, cxx = 0, cxy = 0, cyy = 0, ca = 0, cb = 0, cc = 0;
             float col0 = 0, col1 = 0, col2 = 0;
             int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
@@ -261,6 +262,9 @@ k_project(ProjectParams p) {
                         n_tiles = static_cast<uint32_t>((cx1 - cx0 + 1) * (cy1 - cy0 + 1));
                         span_lo = static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16);
                         span_hi = static_cast<uint32_t>(cx1 - cx0 + 1) | (static_cast<uint32_t>(cy1 - cy0 + 1) << 16);
+                        n_bins = cell == p.tile_size ? n_tiles
+                                                     : static_cast<uint32_t>(((cx1 >> 1) - (cx0 >> 1) + 1) *
+                                                                             ((cy1 >> 1) - (cy0 >> 1) + 1));
                         col0 = c2.z;
                         col1 = c2.w;
                         col2 = c3.x;
@@ -293,6 +297,7 @@ k_project(ProjectParams p) {
             // Record slots: ballot ranks inside the warp, warp counts across the CTA, one
             // atomic per (CTA, instance) on the frame's splat counter.
             pairs += n_tiles;
+            tile_pairs += n_bins;
             const uint32_t bal = __ballot_sync(0xffffffffu, survive);
             if (lane == 0) s_wcnt[warp] = __popc(bal);
             __syncthreads();
@@ -366,7 +371,9 @@ k_project(ProjectParams p) {
         dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     }
     pairs = __reduce_add_sync(0xffffffffu, pairs);
+    tile_pairs = __reduce_add_sync(0xffffffffu, tile_pairs);
     if ((tid & 31) == 0) {
+        if (tile_pairs) atomicAdd(&p.counters->tile_pairs, static_cast<unsigned long long>(tile_pairs));
         if (dmin != 0xffffffffu) atomicMin(&p.counters->depth_min_bits, dmin);
         if (dmax != 0u) atomicMax(&p.counters->depth_max_bits, dmax);
         if (pairs) atomicAdd(&p.counters->pairs, static_cast<unsigned long long>(pairs));

@@ -66,6 +66,7 @@ k_lod_plan(PlanParams p) {
     if (tid == 0) {
         p.counters->splats = 0ull;
         p.counters->pairs = 0ull;
+        p.counters->tile_pairs = 0ull;
         p.counters->depth_min_bits = 0xffffffffu;
         p.counters->depth_max_bits = 0u;
         p.counters->item_cursor = 0u;

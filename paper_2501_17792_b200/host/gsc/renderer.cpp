@@ -352,6 +352,7 @@ void render_frame_host(Crowd& crowd, const Camera& camera, float time_s, const R
         times->splat_count = st.splat_count;
         times->pair_count = st.pair_count;
         times->gaussian_count = st.gaussian_count;
+        times->tile_pair_count = st.tile_pair_count;
     }
 }
 }  // namespace

@@ -81,6 +81,7 @@ struct StageTimes {
     uint64_t splat_count = 0;
     uint64_t pair_count = 0;
     uint64_t gaussian_count = 0;
+    uint64_t tile_pair_count = 0;  // the reference's per-tile bin entries (renderer.cpp:147-161)
 };
 
 // Error from the C-ABI, rethrown as the reference's exception types.

@@ -525,6 +525,7 @@ static int render_host(gsch_renderer* r, float time_s, int32_t static_pose, int3
             times->splat_count = t.splat_count;
             times->pair_count = t.pair_count;
             times->gaussian_count = t.gaussian_count;
+            times->tile_pair_count = t.tile_pair_count;
         }
     });
 }

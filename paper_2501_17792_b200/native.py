@@ -66,7 +66,7 @@ class GscgStageTimes(C.Structure):
     _fields_ = [("update_ms", C.c_double), ("gather_ms", C.c_double), ("sort_ms", C.c_double),
                 ("rasterize_ms", C.c_double), ("h2d_ms", C.c_double), ("d2h_ms", C.c_double),
                 ("splat_count", C.c_uint64), ("pair_count", C.c_uint64), ("gaussian_count", C.c_uint64),
-                ("sort_passes", C.c_uint32), ("kernel_launches", C.c_uint32)]
+                ("sort_passes", C.c_uint32), ("kernel_launches", C.c_uint32), ("tile_pair_count", C.c_uint64)]
 
 
 class GscgMemoryUsage(C.Structure):
@@ -121,7 +121,8 @@ class GschMemoryReport(C.Structure):
 class GschStageTimes(C.Structure):
     _fields_ = [("update_ms", C.c_double), ("gather_ms", C.c_double), ("sort_ms", C.c_double),
                 ("rasterize_ms", C.c_double), ("pose_ms", C.c_double), ("total_ms", C.c_double),
-                ("splat_count", C.c_uint64), ("pair_count", C.c_uint64), ("gaussian_count", C.c_uint64)]
+                ("splat_count", C.c_uint64), ("pair_count", C.c_uint64), ("gaussian_count", C.c_uint64),
+                ("tile_pair_count", C.c_uint64)]
 
 
 _P = C.c_void_p

@@ -47,6 +47,10 @@ def check_frame(scene, renderer, oracle_scene, gpu_out, orc_out, tile_size=16, f
         f"counts G/S gpu {(G, S)} oracle {(times.gaussian_count, times.splat_count)}"
     if renderer.cell_layout()[1] == 1:
         assert K == times.pair_count, f"pairs gpu {K} oracle {times.pair_count}"
+    last = getattr(renderer, "last_times", None)
+    if last is not None:  # the reference's (tile, splat) bin entries, counted by k_project
+        assert last.tile_pair_count == times.pair_count, \
+            f"tile pairs gpu {last.tile_pair_count} oracle {times.pair_count}"
     report.update(G=G, S=S, K=K)
     if full:
         pm, opm = renderer.posed_means(), oracle_scene.posed()
