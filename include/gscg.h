@@ -128,6 +128,10 @@ typedef struct {
 #define GSCG_POSES_GIVEN 0
 #define GSCG_POSES_SAMPLED 1
 
+/* forced_lod value: every instance keeps the level in active_lod (unset = level 0), as
+ * the reference's gather_splats reads inst.active_lod (renderer.cpp:38-40). */
+#define GSCG_LOD_GIVEN (-2)
+
 /* A motion clip for device pose sampling: frame_count x (4 + 4*joint_count) floats, the
  * frame pose record layout above (MotionClip, avatar.hpp:40-48). */
 typedef struct {
@@ -282,6 +286,23 @@ typedef struct {
 int gscg_gather_splats(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
                        const gscg_render_settings* settings, const gscg_lod_policy* lod,
                        gscg_frame_splat* out, uint64_t capacity, uint64_t* count);
+/* update_crowd (crowd.cpp:86-140) up to the posed means: pose sampling (or the given
+ * poses), FK, skin matrices and LBS of every instance's level (forced_lod, or distance
+ * LoD, or GSCG_LOD_GIVEN) on the device; posed_out (host or device) receives the
+ * instance-Gaussians' posed means, G x 3 floats in instance order then gaussian index
+ * (the concatenation of every CrowdInstance::posed_means). out may be NULL to query G;
+ * otherwise capacity >= G. active_lod receives the levels used. */
+int gscg_skin_means(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
+                    const gscg_lod_policy* lod, float* posed_out, uint64_t capacity, uint64_t* gaussians);
+/* gather_splats (renderer.cpp:25-73) from posed means the caller holds (CrowdInstance::
+ * posed_means after update_crowd): frame->forced_lod must be GSCG_LOD_GIVEN (each
+ * instance projects its active_lod level); posed_means is G x 3 floats in the
+ * gscg_skin_means layout; project_mask (n, may be NULL = all) skips instances whose
+ * posed means are empty. Survivors come back in (instance, gaussian) order as
+ * gscg_gather_splats returns them. */
+int gscg_gather_posed(gscg_ctx* ctx, const gscg_frame_desc* frame, const float* posed_means, uint64_t gaussians,
+                      const uint32_t* project_mask, const gscg_camera* cam, const gscg_render_settings* settings,
+                      gscg_frame_splat* out, uint64_t capacity, uint64_t* count);
 /* sort_splats (renderer.cpp:85-107): in place, by (depth bits, instance_id, gaussian_index),
  * on the GPU (stable LSD passes: gaussian, then instance, then depth). */
 int gscg_sort_splats(gscg_ctx* ctx, gscg_frame_splat* splats, uint64_t n);

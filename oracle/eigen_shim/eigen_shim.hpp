@@ -410,5 +410,10 @@ using Vector2f = Matrix<float, 2, 1>;
 using Vector3f = Matrix<float, 3, 1>;
 using Vector4f = Matrix<float, 4, 1>;
 using RowVector4f = Matrix<float, 1, 4>;
+using Matrix3d = Matrix<double, 3, 3>;
+using Matrix4d = Matrix<double, 4, 4>;
+using Vector2d = Matrix<double, 2, 1>;
+using Vector3d = Matrix<double, 3, 1>;
+using Vector4d = Matrix<double, 4, 1>;
 
 }  // namespace Eigen

@@ -197,6 +197,9 @@ struct gscg_ctx {
     uint32_t launches = 0;
     // screen-band exchange: 0 none, 1 routed, 2 packed, 3 band rendered
     int band_state = 0;
+    // Stage-function modes of update_gather (gscg_skin_means / gscg_gather_posed).
+    enum class Mode { Frame, SkinOnly, PosedIn } mode = Mode::Frame;
+    DevBuf posed_in, project_mask, posed_out;
     BandParams band{};
     DevBuf band_scratch;
     unsigned long long* h_band_counts = nullptr;
@@ -429,6 +432,8 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
     const uint32_t n = frame->instance_count;
     const uint32_t js = std::max<uint32_t>(ctx->joint_stride, 1);
     const uint32_t pose_stride = 4 + 4 * frame->joint_stride;
+    const bool posed_mode = ctx->mode == gscg_ctx::Mode::PosedIn;  // posed means given: no pose / FK / cull
+    const bool skin_only = ctx->mode == gscg_ctx::Mode::SkinOnly;   // update_crowd: posed means out, no projection
 
     CUDA_TRY(ctx->template_ids.ensure(std::max<size_t>(n, 1) * 4));
     CUDA_TRY(ctx->placement.ensure(std::max<size_t>(n, 1) * 16));
@@ -505,7 +510,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         d_phase = frame->phase_offsets;
     }
     CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
-    if (sampled && shard_end > shard_begin) {
+    if (sampled && shard_end > shard_begin && !posed_mode) {
         // update_crowd's pose sampling on the device (gscg_pose.cu); FK reads ctx->poses.
         PoseParams pp{};
         pp.n = n;
@@ -526,7 +531,8 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
 
     const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + kBatch * static_cast<int>(js) * 12 * 4;
     int project_blocks_per_sm = 1;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project, kProjectThreads, project_smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project<false>, kProjectThreads,
+                                                           project_smem));
     project_blocks_per_sm = std::max(project_blocks_per_sm, 1);
 
     CameraDev camdev{};
@@ -548,7 +554,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             ctx->h_lod_cap = n;
         }
         // ---- update ---- (FK first: the cull reads the skin matrices, the plan the cull)
-        if (shard_end > shard_begin) {
+        if (shard_end > shard_begin && !posed_mode) {
             FkParams fp{};
             fp.n = shard_end;
             fp.first = shard_begin;
@@ -569,7 +575,8 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         }
         // Instance frustum cull (off with GSCG_DEBUG_POSED, which keeps every posed mean,
         // and GSCG_DEBUG_NO_CULL).
-        const bool cull = shard_end > shard_begin && !(ctx->debug & (GSCG_DEBUG_POSED | GSCG_DEBUG_NO_CULL));
+        const bool cull = shard_end > shard_begin && !posed_mode && !skin_only &&
+                          !(ctx->debug & (GSCG_DEBUG_POSED | GSCG_DEBUG_NO_CULL));
         if (cull) {
             CullParams cp{};
             cp.n = shard_end;
@@ -607,17 +614,40 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pp.group_inst_count = ctx->group_inst_count.as<uint32_t>();
         pp.group_item_start = ctx->group_item_start.as<uint32_t>();
         pp.members = ctx->members.as<uint32_t>();
-        pp.visible = cull ? ctx->visible.as<uint32_t>() : nullptr;
+        pp.visible = cull ? ctx->visible.as<uint32_t>() : posed_mode ? ctx->project_mask.as<uint32_t>() : nullptr;
         pp.counters = counters;
         k_lod_plan<<<1, 1024, 0, s>>>(pp);
         ++launches;
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
 
-        if (ctx->debug & GSCG_DEBUG_POSED) {
+        if ((ctx->debug & GSCG_DEBUG_POSED) || skin_only) {
             CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
-            CUDA_TRY(ctx->posed_dbg.ensure(std::max<uint64_t>(ctx->h_counters->gaussians, 1) * 12));
+            if (ctx->h_counters->gaussians > 0xffffffffull)
+                throw Status(GSCG_ERR_OOM, "instance-Gaussian count exceeds 32-bit ordinals");
+            CUDA_TRY((skin_only ? ctx->posed_out : ctx->posed_dbg).ensure(std::max<uint64_t>(ctx->h_counters->gaussians, 1) * 12));
+        }
+        if (skin_only) {  // update_crowd: the posed means of every instance, then stop
+            SkinParams sp{};
+            sp.n = n;
+            sp.joint_stride = js;
+            sp.inst_group = ctx->inst_group.as<uint32_t>();
+            sp.inst_base = ctx->inst_base.as<uint32_t>();
+            sp.groups = ctx->d_groups.as<GroupDev>();
+            sp.skin = ctx->skin.as<float>();
+            sp.posed = ctx->posed_out.as<float>();
+            uint32_t max_count = 0;
+            for (const TemplateStore& t : ctx->templates)
+                for (const LevelStore& l : t.levels) max_count = std::max(max_count, l.count);
+            if (n && max_count) {
+                k_skin_means<<<dim3((max_count + 255) / 256, std::min<uint32_t>(n, 65535u)), 256, 0, s>>>(sp);
+                ++launches;
+                CUDA_TRY(cudaGetLastError());
+            }
+            ctx->G = ctx->h_counters->gaussians;
+            ctx->n = n;
+            return;
         }
         if (ctx->splat_capacity == 0) {
             ctx->splat_capacity = 1u << 20;
@@ -650,10 +680,14 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pj.splat_meta = ctx->splat_meta.as<uint4>();
         pj.splat_capacity = ctx->splat_capacity;
         pj.pair_capacity = ctx->pair_capacity;
+        pj.posed_in = posed_mode ? ctx->posed_in.as<float>() : nullptr;
         pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
         pj.record_debug = (ctx->debug & GSCG_DEBUG_RECORDS) ? ctx->rec_dbg.as<gscg_splat_record>() : nullptr;
         if (shard_end > shard_begin && ctx->group_count > 0) {
-            k_project<<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
+            if (posed_mode)
+                k_project<true><<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
+            else
+                k_project<false><<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -1053,7 +1087,9 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
         CUDA_TRY(cudaFuncSetAttribute(k_fk_skin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (kFkThreads / 16) * kFkSmemPerInstance(kMaxJoints)));
-        CUDA_TRY(cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_TRY(cudaFuncSetAttribute(k_project<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_project<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
     });
     *out = ctx;
@@ -1661,6 +1697,120 @@ int gscg_gather_splats(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_c
         } else {
             CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         }
+    });
+}
+
+}  // extern "C"
+
+namespace {
+// Runs update_gather in a stage-function mode and restores the frame mode afterwards.
+template <typename F>
+void with_mode(gscg_ctx* ctx, gscg_ctx::Mode mode, F&& f) {
+    ctx->mode = mode;
+    try {
+        f();
+    } catch (...) {
+        ctx->mode = gscg_ctx::Mode::Frame;
+        throw;
+    }
+    ctx->mode = gscg_ctx::Mode::Frame;
+}
+
+void records_to_splats(gscg_ctx* ctx, gscg_frame_splat* out, uint64_t capacity) {
+    if (capacity < ctx->S) invalid("splat buffer smaller than the frame's splat count");
+    std::vector<gscg_splat_record> rec(ctx->S);
+    if (ctx->S)
+        CUDA_TRY(cudaMemcpyAsync(rec.data(), ctx->rec_dbg.ptr, ctx->S * sizeof(gscg_splat_record),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::sort(rec.begin(), rec.end(), [](const gscg_splat_record& a, const gscg_splat_record& b) {
+        return a.ordinal < b.ordinal;  // = (instance, gaussian) order, the reference's concatenation
+    });
+    for (size_t i = 0; i < rec.size(); ++i) {
+        const gscg_splat_record& r = rec[i];
+        gscg_frame_splat& o = out[i];
+        o.mean_px[0] = r.mean_px[0];
+        o.mean_px[1] = r.mean_px[1];
+        o.cov_xx = r.cov_xx;
+        o.cov_xy = r.cov_xy;
+        o.cov_yy = r.cov_yy;
+        o.depth = r.depth;
+        for (int c = 0; c < 3; ++c) o.color[c] = r.color[c];
+        o.opacity = r.opacity;
+        o.instance_id = r.instance_id;
+        o.gaussian_index = r.gaussian_index;
+        for (int c = 0; c < 4; ++c) o.rect[c] = r.rect[c];
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int gscg_skin_means(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam, const gscg_lod_policy* lod,
+                    float* posed_out, uint64_t capacity, uint64_t* gaussians) {
+    if (!ctx || !gaussians) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        gscg_render_settings rs = ctx->settings;
+        if (rs.tile_size < 1) {  // no frame rendered yet: any valid settings (they do not enter skinning)
+            rs = gscg_render_settings{16, {0, 0, 0}, 0.99f, 1.0f / 255.0f, 1e-4f, 0};
+        }
+        validate_frame(ctx, frame, cam, &rs, lod);
+        const uint32_t n = frame->instance_count;
+        uint32_t launches = 0;
+        ctx->band_state = 0;
+        with_mode(ctx, gscg_ctx::Mode::SkinOnly, [&] { update_gather(ctx, frame, cam, lod, 0, n, launches); });
+        if (n) CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDefault, ctx->stream));
+        *gaussians = ctx->G;
+        if (posed_out) {
+            if (capacity < ctx->G) invalid("posed buffer smaller than the crowd's instance-Gaussian count");
+            if (ctx->G) CUDA_TRY(cudaMemcpyAsync(posed_out, ctx->posed_out.ptr, ctx->G * 12, cudaMemcpyDefault, ctx->stream));
+        }
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gscg_gather_posed(gscg_ctx* ctx, const gscg_frame_desc* frame, const float* posed_means, uint64_t gaussians,
+                      const uint32_t* project_mask, const gscg_camera* cam, const gscg_render_settings* settings,
+                      gscg_frame_splat* out, uint64_t capacity, uint64_t* count) {
+    if (!ctx || !count || !frame) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (frame->forced_lod != GSCG_LOD_GIVEN) invalid("gscg_gather_posed: forced_lod must be GSCG_LOD_GIVEN");
+        gscg_frame_desc fd = *frame;  // no poses: the means are given
+        fd.pose_source = GSCG_POSES_SAMPLED;
+        fd.static_pose = 1;
+        fd.poses = nullptr;
+        gscg_lod_policy lp{};
+        validate_frame(ctx, &fd, cam, settings, &lp);
+        const uint32_t n = fd.instance_count;
+        if (gaussians && !posed_means) invalid("null posed means");
+        CUDA_TRY(ctx->posed_in.ensure(std::max<uint64_t>(gaussians, 1) * 12));
+        CUDA_TRY(ctx->project_mask.ensure(std::max<size_t>(n, 1) * 4));
+        if (gaussians)
+            CUDA_TRY(cudaMemcpyAsync(ctx->posed_in.ptr, posed_means, gaussians * 12, cudaMemcpyDefault, ctx->stream));
+        std::vector<uint32_t> all;
+        if (!project_mask) {
+            all.assign(std::max<uint32_t>(n, 1), 1u);
+            project_mask = all.data();
+        }
+        if (n) CUDA_TRY(cudaMemcpyAsync(ctx->project_mask.ptr, project_mask, n * 4ull, cudaMemcpyDefault, ctx->stream));
+        const uint32_t saved = ctx->debug;
+        ctx->debug = (saved | GSCG_DEBUG_RECORDS) & ~GSCG_DEBUG_POSED;
+        uint32_t launches = 0;
+        ctx->band_state = 0;
+        try {
+            with_mode(ctx, gscg_ctx::Mode::PosedIn, [&] { update_gather(ctx, &fd, cam, &lp, 0, n, launches); });
+        } catch (...) {
+            ctx->debug = saved;
+            throw;
+        }
+        ctx->debug = saved;
+        if (ctx->G != gaussians) invalid("posed means: " + std::to_string(gaussians) + " given, the levels hold " +
+                                         std::to_string(ctx->G));
+        *count = ctx->S;
+        if (out) records_to_splats(ctx, out, capacity);
+        else CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     });
 }
 

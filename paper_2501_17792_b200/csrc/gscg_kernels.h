@@ -78,6 +78,7 @@ struct ProjectParams {
     uint4* splat_meta;      // per record: ordinal, cx0 | cy0 << 16, across | down << 16, depth bits
     uint64_t splat_capacity;
     uint64_t pair_capacity;
+    const float* posed_in;           // k_project<true>: posed means G x 3 by ordinal (no skinning)
     // debug outputs (may be null)
     float* posed_debug;              // G x 3 by ordinal
     gscg_splat_record* record_debug; // per splat
@@ -144,7 +145,21 @@ constexpr int kFkThreads = 128;  // k_fk_skin: 8 instances (half-warps) per bloc
 constexpr int kFkSmemPerInstance(int joint_stride) { return joint_stride * 52 * 4; }  // world, bind, inverse, pose
 __global__ void k_fk_skin(FkParams p);
 __global__ void k_inst_cull(CullParams p);
-__global__ void k_project(ProjectParams p);
+template <bool kPosedIn>
+__global__ void k_project(ProjectParams p);  // <false>: LBS from skin matrices (the frame); <true>: given posed means
+
+// update_crowd's skin_means for every instance (gscg_skin_means): posed[ordinal] =
+// LBS of the instance's level (avatar.cpp:178-192), the arithmetic k_project uses.
+struct SkinParams {
+    uint32_t n;
+    uint32_t joint_stride;
+    const uint32_t* inst_group;
+    const uint32_t* inst_base;
+    const GroupDev* groups;
+    const float* skin;
+    float* posed;  // G x 3
+};
+__global__ void k_skin_means(SkinParams p);
 __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n);
 
 // sort: splats by depth, pairs emitted in that order, pairs stably by cell

@@ -80,6 +80,7 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
 
 }  // namespace
 
+template <bool kPosedIn>
 __global__ void __launch_bounds__(kProjectThreads, 4)
 k_project(ProjectParams p) {
     extern __shared__ float4 s_dyn[];
@@ -187,10 +188,17 @@ k_project(ProjectParams p) {
             int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
             uint32_t span_lo = 0, span_hi = 0;
             float ax = 0.0f, ay = 0.0f, az = 0.0f;
+            if (gvalid && kPosedIn) {  // posed means given (gather_splats after update_crowd)
+                const size_t o = 3ull * (s_member_base[k] + gi);
+                ax = p.posed_in[o + 0];
+                ay = p.posed_in[o + 1];
+                az = p.posed_in[o + 2];
+            }
             if (gvalid) {
                 // Linear blend skinning (avatar.cpp:182-190), accumulator starts at +0.
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
+                    if (kPosedIn) break;
                     if (wk[q] == 0.0f) continue;
                     const float4* S = reinterpret_cast<const float4*>(s_inst + jidx[q] * 12);  // 3 rows, 48-B aligned
                     const float4 r0 = S[0], r1 = S[1], r2 = S[2];
@@ -386,5 +394,8 @@ __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) core[4 * i + 3].y = pf[i];
 }
+
+template __global__ void k_project<false>(ProjectParams p);
+template __global__ void k_project<true>(ProjectParams p);
 
 }  // namespace gscg

@@ -87,6 +87,9 @@ k_lod_plan(PlanParams p) {
             uint32_t lod;
             if (p.forced_lod >= 0) {
                 lod = min(static_cast<uint32_t>(p.forced_lod), levels - 1u);
+            } else if (p.forced_lod == GSCG_LOD_GIVEN) {  // the caller's active_lod (renderer.cpp:38-40)
+                const uint32_t given = p.lod_prev[i];
+                lod = min(given == 0xffffffffu ? 0u : given, levels - 1u);
             } else {
                 // instance_distance((x, pelvis.y, z), camera.position): Eigen half-split norm.
                 const float dx = p.placement[4 * i + 0] - p.cam_pos[0];
@@ -430,6 +433,38 @@ __global__ void k_copy_segments(CopySegs c) {
     uint32_t* __restrict__ dst = c.dst[seg];
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c.words[seg]; i += gridDim.x * blockDim.x)
         dst[i] = src[i];
+}
+
+// skin_means (avatar.cpp:178-192) of every instance's level into posed[ordinal]: a 2-D
+// grid of (256-Gaussian chunk, instance) blocks; the LBS expression is k_project's.
+__global__ void __launch_bounds__(256) k_skin_means(SkinParams p) {
+    for (uint32_t inst = blockIdx.y; inst < p.n; inst += gridDim.y) {
+        const GroupDev grp = p.groups[p.inst_group[inst]];
+        const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+        if (gi >= grp.count) continue;
+        const float4 c0 = grp.core[4 * gi + 0], c3 = grp.core[4 * gi + 3], wv = grp.weights[gi];
+        const uint32_t i01 = __float_as_uint(c3.z), i23 = __float_as_uint(c3.w);
+        const uint32_t jidx[4] = {i01 & 0xffffu, i01 >> 16, i23 & 0xffffu, i23 >> 16};
+        const float wk[4] = {wv.x, wv.y, wv.z, wv.w};
+        const float* s_inst = p.skin + static_cast<size_t>(inst) * p.joint_stride * 12;
+        float ax = 0.0f, ay = 0.0f, az = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (wk[q] == 0.0f) continue;
+            const float4* S = reinterpret_cast<const float4*>(s_inst + jidx[q] * 12);
+            const float4 r0 = S[0], r1 = S[1], r2 = S[2];
+            const float vx = ((r0.x * c0.x + r0.y * c0.y) + r0.z * c0.z) + r0.w * 1.0f;
+            const float vy = ((r1.x * c0.x + r1.y * c0.y) + r1.z * c0.z) + r1.w * 1.0f;
+            const float vz = ((r2.x * c0.x + r2.y * c0.y) + r2.z * c0.z) + r2.w * 1.0f;
+            ax = ax + wk[q] * vx;
+            ay = ay + wk[q] * vy;
+            az = az + wk[q] * vz;
+        }
+        const size_t o = 3ull * (p.inst_base[inst] + gi);
+        p.posed[o + 0] = ax;
+        p.posed[o + 1] = ay;
+        p.posed[o + 2] = az;
+    }
 }
 
 }  // namespace gscg

@@ -2,7 +2,7 @@
 // /root/reference/proj/src/crowd.cpp (uniform01 :14-16, root_transform :20-30,
 // validate(SceneConfig) :32-44, build_crowd :46-84, memory model :142-210) and
 // /root/reference/proj/src/lod.cpp (validate :6-20, select_lod :22-37,
-// instance_distance :39-41). The per-frame update_crowd lives on the GPU.
+// instance_distance :39-41). update_crowd (its skinning runs on the GPU) is in renderer.cpp.
 #include "gsc/crowd.hpp"
 
 #include <cmath>
@@ -22,6 +22,10 @@ MemoryReport make_report(const MemoryLayoutModel& model, uint64_t resident,
     r.instance_count = instances;
     r.fixed_overhead_bytes = model.fixed_overhead_bytes;
     r.resident_template_bytes = resident * model.template_bytes_per_gaussian();
+    r.resident_channels = {resident * model.mean_bytes,    resident * model.rotation_bytes,
+                           resident * model.scale_bytes,   resident * model.opacity_bytes,
+                           resident * model.color_bytes,   resident * model.skin_index_bytes,
+                           resident * model.skin_weight_bytes};
     const uint64_t base = model.fixed_overhead_bytes + r.resident_template_bytes;
     r.posed_mean_bytes = instance_gaussians * model.posed_bytes_per_gaussian();
     r.naive_bytes = base + instance_gaussians * model.template_bytes_per_gaussian();
@@ -147,27 +151,6 @@ MemoryReport memory_report_cell(uint64_t instances, uint64_t gaussians,
                                 const MemoryLayoutModel& model) {
     validate(model);
     return make_report(model, instances > 0 ? gaussians : 0, instances * gaussians, instances);
-}
-
-void update_crowd(Crowd& crowd, const Camera& camera, const UpdateOptions& opts) {
-    if (opts.skin_rotations) throw std::invalid_argument("update_crowd: rotation skinning is not supported");
-    const TemplateStore& templates = *crowd.templates;
-    for (CrowdInstance& inst : crowd.instances) {
-        if (inst.template_id >= templates.size()) throw std::invalid_argument("update_crowd: missing template");
-        const AvatarTemplate& tpl = templates[inst.template_id];
-        const uint32_t last = static_cast<uint32_t>(tpl.levels.size()) - 1;
-        uint32_t lod;
-        if (opts.forced_lod) {
-            lod = std::min(*opts.forced_lod, last);
-        } else {
-            const Vec3 root_pos(inst.x, tpl.skeleton.bind[0].translation()[1], inst.z);
-            const float dist = instance_distance(root_pos, camera.position);
-            std::optional<uint32_t> prev;
-            if (inst.active_lod != kLodUnset) prev = inst.active_lod;
-            lod = std::min(select_lod(crowd.lod, dist, prev), last);
-        }
-        inst.active_lod = lod;
-    }
 }
 
 }  // namespace gsc

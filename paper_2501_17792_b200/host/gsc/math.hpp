@@ -13,6 +13,7 @@
 // SSE2 code without FMA contraction.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -23,6 +24,30 @@ inline constexpr float kAlphaCutoff = 1.0f / 255.0f;
 inline constexpr float kCovDilation = 0.3f;
 inline constexpr float kPsnrCap = 99.0f;
 
+// v.cast<T>() / m.cast<T>() as Eigen spells them: a proxy converting to any caller type
+// with Eigen-style element access (the reference's tests cast to Eigen's double types).
+template <typename T, int N>
+struct CastVector {
+    T v[N];
+    template <typename M>
+    operator M() const {  // NOLINT: implicit, as Eigen's cast expression
+        M out;
+        for (int i = 0; i < N; ++i) out(i) = v[i];
+        return out;
+    }
+};
+template <typename T, int R, int C>
+struct CastMatrix {
+    T m[R * C];  // column-major
+    template <typename M>
+    operator M() const {  // NOLINT
+        M out;
+        for (int c = 0; c < C; ++c)
+            for (int r = 0; r < R; ++r) out(r, c) = m[c * R + r];
+        return out;
+    }
+};
+
 struct Vec2 {
     float v[2] = {0.0f, 0.0f};
     Vec2() = default;
@@ -31,6 +56,8 @@ struct Vec2 {
     float y() const { return v[1]; }
     float& operator[](int i) { return v[i]; }
     float operator[](int i) const { return v[i]; }
+    template <typename T>
+    CastVector<T, 2> cast() const { return {{static_cast<T>(v[0]), static_cast<T>(v[1])}}; }
 };
 
 struct Vec3 {
@@ -64,6 +91,10 @@ struct Vec3 {
     Vec3 cwiseMin(float c) const {
         return Vec3(std::fmin(v[0], c), std::fmin(v[1], c), std::fmin(v[2], c));
     }
+    Vec3 cwiseAbs() const { return Vec3(std::fabs(v[0]), std::fabs(v[1]), std::fabs(v[2])); }
+    float maxCoeff() const { return std::fmax(v[0], std::fmax(v[1], v[2])); }
+    template <typename T>
+    CastVector<T, 3> cast() const { return {{static_cast<T>(v[0]), static_cast<T>(v[1]), static_cast<T>(v[2])}}; }
 };
 
 inline Vec3 operator+(const Vec3& a, const Vec3& b) {
@@ -83,6 +114,11 @@ struct Vec4 {
     Vec4(float x, float y, float z, float w) : v{x, y, z, w} {}
     float& operator[](int i) { return v[i]; }
     float operator[](int i) const { return v[i]; }
+    template <int N>
+    Vec3 head() const {
+        static_assert(N == 3, "head<3>() only");
+        return Vec3(v[0], v[1], v[2]);
+    }
 };
 
 // Column-major 3x3: m[c*3 + r].
@@ -98,6 +134,12 @@ struct Mat3 {
         return t;
     }
     float trace() const { return m[0] + (m[4] + m[8]); }
+    template <typename T>
+    CastMatrix<T, 3, 3> cast() const {
+        CastMatrix<T, 3, 3> out;
+        for (int i = 0; i < 9; ++i) out.m[i] = static_cast<T>(m[i]);
+        return out;
+    }
 };
 
 // Coefficient-based 3x3 product: inner reduction a0 + (a1 + a2).
@@ -135,6 +177,22 @@ struct Mat4 {
         m[12] = t[0];
         m[13] = t[1];
         m[14] = t[2];
+    }
+    template <int R, int C>
+    auto topRightCorner() const {  // Eigen's block of the translation column / rotation
+        static_assert(R == 3 && C == 1, "topRightCorner<3, 1>() only");
+        return translation();
+    }
+    template <int R, int C>
+    Mat3 topLeftCorner() const {
+        static_assert(R == 3 && C == 3, "topLeftCorner<3, 3>() only");
+        return topLeft3();
+    }
+    template <typename T>
+    CastMatrix<T, 4, 4> cast() const {
+        CastMatrix<T, 4, 4> out;
+        for (int i = 0; i < 16; ++i) out.m[i] = static_cast<T>(m[i]);
+        return out;
     }
 };
 
@@ -366,6 +424,19 @@ struct PixelRect {
     int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
     bool empty() const { return x0 >= x1 || y0 >= y1; }
 };
+
+// Integer 3-sigma rectangle clipped to [0, w) x [0, h) (math.cpp:106-116); k_project
+// computes the same rect per splat on the GPU.
+inline PixelRect splat_bounds(const Vec2& mean_px, float cov_xx, float cov_yy, int width, int height) {
+    const float rx = 3.0f * std::sqrt(cov_xx);
+    const float ry = 3.0f * std::sqrt(cov_yy);
+    PixelRect r;
+    r.x0 = std::max(0, static_cast<int>(std::floor(mean_px.x() - rx)));
+    r.y0 = std::max(0, static_cast<int>(std::floor(mean_px.y() - ry)));
+    r.x1 = std::min(width, static_cast<int>(std::floor(mean_px.x() + rx)) + 1);
+    r.y1 = std::min(height, static_cast<int>(std::floor(mean_px.y() + ry)) + 1);
+    return r;
+}
 
 // Sigma = R S S^T R^T (math.cpp:94-104); used at template load (LodLevel::finalize).
 Mat3 build_covariance(const Quat& rotation, const Vec3& scale);

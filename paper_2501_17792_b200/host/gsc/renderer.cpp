@@ -26,16 +26,6 @@ void check_gscg(int status, const gscg_ctx* ctx) {
     throw GpuError(status, msg);
 }
 
-unsigned resolve_thread_count(int hint) {
-    if (hint > 0) return static_cast<unsigned>(hint);
-    if (const char* env = std::getenv("GSCROWD_THREADS")) {
-        const long v = std::strtol(env, nullptr, 10);
-        if (v > 0) return static_cast<unsigned>(v);
-    }
-    const unsigned hw = std::thread::hardware_concurrency();
-    return hw > 0 ? hw : 1;
-}
-
 HostPool::HostPool(unsigned threads) {
     for (unsigned i = 1; i < threads; ++i) workers_.emplace_back([this, i] { worker(i); });
 }
@@ -433,23 +423,184 @@ void sort_splats(SplatFrame& frame, FrameContext& ctx) {
                ctx.gpu());
 }
 
-RasterOutput rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
-                            FrameContext& ctx) {
+FrameContext& default_frame_context() {
+    // One context per host thread (a gscg context is not thread-safe), never destroyed:
+    // process teardown may already have unloaded the CUDA runtime.
+    thread_local FrameContext* ctx = [] {
+        const char* env = std::getenv("GSCG_DEVICE");
+        return new FrameContext(env ? std::atoi(env) : 0);
+    }();
+    return *ctx;
+}
+
+void update_crowd(Crowd& crowd, const Camera& camera, const UpdateOptions& opts) {
+    update_crowd(crowd, camera, opts, default_frame_context());
+}
+
+void update_crowd(Crowd& crowd, const Camera& camera, const UpdateOptions& opts, FrameContext& ctx) {
+    if (opts.skin_rotations)
+        throw std::invalid_argument("update_crowd: rotation skinning is not supported by the B200 path");
+    const TemplateStore& templates = *crowd.templates;
+    // LoD (crowd.cpp:93-110) on the host, bit-exact with k_lod_plan.
+    bool stale = false;
+    for (CrowdInstance& inst : crowd.instances) {
+        if (inst.template_id >= templates.size()) throw std::invalid_argument("update_crowd: missing template");
+        const AvatarTemplate& tpl = templates[inst.template_id];
+        const uint32_t last = static_cast<uint32_t>(tpl.levels.size()) - 1;
+        uint32_t lod;
+        if (opts.forced_lod) {
+            lod = std::min(*opts.forced_lod, last);
+        } else {
+            const Vec3 root_pos(inst.x, tpl.skeleton.bind[0].translation()[1], inst.z);
+            const float dist = instance_distance(root_pos, camera.position);
+            std::optional<uint32_t> prev;
+            if (inst.active_lod != kLodUnset) prev = inst.active_lod;
+            lod = std::min(select_lod(crowd.lod, dist, prev), last);
+        }
+        if (lod != inst.active_lod) {
+            inst.active_lod = lod;
+            inst.posed_valid = false;
+        }
+        // crowd.cpp:112-116: a static instance with valid posed means is left alone.
+        if (!(opts.static_pose && inst.posed_valid &&
+              inst.posed_means.size() == tpl.levels[lod].gaussian_count()))
+            stale = true;
+    }
+    if (!stale) return;
+    // Pose + FK + skin matrices + LBS of every instance's active level on the GPU.
+    ctx.ensure_templates(crowd.templates);
+    ctx.sample_crowd(crowd, opts.time_s, opts.static_pose, opts.thread_count);
+    const uint32_t n = static_cast<uint32_t>(crowd.instances.size());
+    gscg_frame_desc fd{};
+    fd.instance_count = n;
+    fd.joint_stride = ctx.joint_stride;
+    fd.template_ids = ctx.template_ids.data();
+    fd.placement = ctx.placement.data();
+    fd.poses = ctx.poses.data();
+    fd.active_lod = ctx.lods.data();
+    fd.forced_lod = GSCG_LOD_GIVEN;
+    fd.memory = GSCG_MEM_HOST;
+    const gscg_camera cam = camera_basis(camera);
+    gscg_lod_policy lp{};
+    uint64_t G = 0;
+    for (const CrowdInstance& inst : crowd.instances)
+        G += templates[inst.template_id].levels[inst.active_lod].gaussian_count();
+    std::vector<float> posed(std::max<uint64_t>(G, 1) * 3);
+    uint64_t got = 0;
+    check_gscg(gscg_skin_means(ctx.gpu(), &fd, &cam, &lp, posed.data(), G, &got), ctx.gpu());
+    if (got != G) throw GpuError(GSCG_ERR_STATE, "update_crowd: instance-Gaussian count mismatch");
+    size_t off = 0;
+    for (CrowdInstance& inst : crowd.instances) {
+        const size_t cnt = templates[inst.template_id].levels[inst.active_lod].gaussian_count();
+        inst.posed_means.resize(cnt);
+        for (size_t g = 0; g < cnt; ++g)
+            inst.posed_means[g] = Vec3(posed[3 * (off + g)], posed[3 * (off + g) + 1], posed[3 * (off + g) + 2]);
+        off += cnt;
+        inst.posed_rotations.clear();
+        inst.posed_valid = opts.static_pose;
+    }
+}
+
+void gather_splats(const Crowd& crowd, const Camera& camera, int /*thread_count*/, FrameContext& ctx) {
+    ctx.frame.width = camera.width;
+    ctx.frame.height = camera.height;
+    ctx.frame.splats.clear();
+    ctx.ensure_templates(crowd.templates);
+    const TemplateStore& templates = *crowd.templates;
+    const uint32_t n = static_cast<uint32_t>(crowd.instances.size());
+    std::vector<uint32_t> tids(std::max<uint32_t>(n, 1)), lods(std::max<uint32_t>(n, 1)), mask(std::max<uint32_t>(n, 1));
+    std::vector<float> place(std::max<uint32_t>(n, 1) * 4, 0.0f);
+    uint64_t G = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        const CrowdInstance& inst = crowd.instances[i];
+        if (inst.template_id >= templates.size()) throw std::invalid_argument("gather_splats: missing template");
+        const AvatarTemplate& tpl = templates[inst.template_id];
+        const uint32_t lod = std::min<uint32_t>(inst.active_lod == kLodUnset ? 0 : inst.active_lod,
+                                                static_cast<uint32_t>(tpl.levels.size()) - 1);
+        const uint32_t cnt = tpl.levels[lod].gaussian_count();
+        if (!inst.posed_means.empty() && inst.posed_means.size() != cnt)
+            throw std::invalid_argument("gather_splats: posed_means do not match the active level (run update_crowd)");
+        tids[i] = inst.template_id;
+        lods[i] = inst.active_lod;
+        mask[i] = inst.posed_means.empty() ? 0u : 1u;  // renderer.cpp:41: n = posed_means.size()
+        G += cnt;
+    }
+    std::vector<float> posed(std::max<uint64_t>(G, 1) * 3, 0.0f);
+    size_t off = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        const CrowdInstance& inst = crowd.instances[i];
+        const AvatarTemplate& tpl = templates[inst.template_id];
+        const uint32_t lod = std::min<uint32_t>(inst.active_lod == kLodUnset ? 0 : inst.active_lod,
+                                                static_cast<uint32_t>(tpl.levels.size()) - 1);
+        for (size_t g = 0; g < inst.posed_means.size(); ++g)
+            for (int k = 0; k < 3; ++k) posed[3 * (off + g) + k] = inst.posed_means[g][k];
+        off += tpl.levels[lod].gaussian_count();
+    }
+    gscg_frame_desc fd{};
+    fd.instance_count = n;
+    fd.joint_stride = ctx.joint_stride;
+    fd.template_ids = tids.data();
+    fd.placement = place.data();
+    fd.active_lod = lods.data();
+    fd.forced_lod = GSCG_LOD_GIVEN;
+    fd.memory = GSCG_MEM_HOST;
+    const gscg_camera cam = camera_basis(camera);
+    const gscg_render_settings rs = to_gscg(RenderSettings{});  // colour as render_frame's defaults
+    uint64_t count = 0;
+    check_gscg(gscg_gather_posed(ctx.gpu(), &fd, posed.data(), G, mask.data(), &cam, &rs, nullptr, 0, &count),
+               ctx.gpu());
+    ctx.frame.splats.resize(count);
+    check_gscg(gscg_gather_posed(ctx.gpu(), &fd, posed.data(), G, mask.data(), &cam, &rs,
+                                 reinterpret_cast<gscg_frame_splat*>(ctx.frame.splats.data()), count, &count),
+               ctx.gpu());
+}
+
+SplatFrame gather_splats(const Crowd& crowd, const Camera& camera, int thread_count) {
+    FrameContext& ctx = default_frame_context();
+    gather_splats(crowd, camera, thread_count, ctx);
+    return std::move(ctx.frame);
+}
+
+void sort_splats(SplatFrame& frame) { sort_splats(frame, default_frame_context()); }
+
+void sort_splats(FrameContext& ctx) { sort_splats(ctx.frame, ctx); }
+
+void rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
+                    FrameContext& ctx) {
     validate(settings);
-    RasterOutput out;
-    out.color = Framebuffer(width, height);
-    out.transmittance.assign(static_cast<size_t>(width) * height, 0.0f);
+    if (width != frame.width || height != frame.height)
+        throw std::invalid_argument("rasterize: splat frame was gathered for another size");
+    if (ctx.out.color.width != width || ctx.out.color.height != height) {
+        ctx.out.color = Framebuffer(width, height);
+        ctx.out.transmittance.assign(static_cast<size_t>(width) * height, 0.0f);
+    }
     const gscg_render_settings rs = to_gscg(settings);
     check_gscg(gscg_rasterize_splats(ctx.gpu(), reinterpret_cast<const gscg_frame_splat*>(frame.splats.data()),
-                                     frame.splats.size(), width, height, &rs, out.color.rgb.data(),
-                                     out.transmittance.data()),
+                                     frame.splats.size(), width, height, &rs, ctx.out.color.rgb.data(),
+                                     ctx.out.transmittance.data()),
                ctx.gpu());
+}
+
+RasterOutput rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height) {
+    FrameContext& ctx = default_frame_context();
+    rasterize_full(frame, settings, width, height, ctx);
+    RasterOutput out;
+    out.color = std::move(ctx.out.color);
+    out.transmittance = std::move(ctx.out.transmittance);
+    ctx.out = RasterOutput{};
     return out;
 }
 
 Framebuffer rasterize(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
                       FrameContext& ctx) {
-    return std::move(rasterize_full(frame, settings, width, height, ctx).color);
+    rasterize_full(frame, settings, width, height, ctx);
+    Framebuffer fb = std::move(ctx.out.color);
+    ctx.out = RasterOutput{};
+    return fb;
+}
+
+Framebuffer rasterize(const SplatFrame& frame, const RenderSettings& settings, int width, int height) {
+    return rasterize(frame, settings, width, height, default_frame_context());
 }
 
 Framebuffer render_frame(Crowd& crowd, const Camera& camera, float time_s,

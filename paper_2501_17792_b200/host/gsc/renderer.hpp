@@ -7,6 +7,7 @@
 #pragma once
 
 #include "gsc/crowd.hpp"
+#include "gsc/parallel.hpp"
 #include "gscg.h"
 
 #include <condition_variable>
@@ -112,8 +113,6 @@ private:
     bool stop_ = false;
 };
 
-unsigned resolve_thread_count(int hint);
-
 // Per-instance pose records for the GPU (update_crowd up to the pose, crowd.cpp:118-124):
 // template ids, placement (x, z, cos yaw, sin yaw) and sampled poses, on the pool.
 void sample_crowd_records(const Crowd& crowd, float time_s, bool static_pose, uint32_t joint_stride,
@@ -138,6 +137,9 @@ public:
     // go to the GPU, which samples every clip itself (bit-identical to the host path).
     void fill_instances(const Crowd& crowd, bool static_pose);
 
+    // The reference's FrameContext members a caller reads (renderer.hpp:57-79): the
+    // gathered / sorted splat frame of the stage functions and the framebuffer + T.
+    SplatFrame frame;
     RasterOutput out;
     std::vector<uint32_t> template_ids;
     std::vector<float> placement;  // n x 4
@@ -176,16 +178,32 @@ void render_frame_async(Crowd& crowd, const Camera& camera, float time_s, const 
                         FrameContext& ctx, float* out_rgb, float* out_T);
 void wait_readback(FrameContext& ctx, uint32_t frames_back);
 
-// Stage functions (reference renderer.hpp:81-103) over host splat arrays, on the GPU.
-// gather_splats runs update + projection for time_s (the reference's update_crowd then
-// gather_splats) and returns the survivors in (instance, gaussian) order; sort_splats
-// orders them by (depth bits, instance, gaussian); rasterize / rasterize_full bin and
-// blend them in the given order.
+// The calling thread's GPU context (device 0, or GSCG_DEVICE), created on first use: the
+// reference's stage functions below take no FrameContext, or a reference-shaped one.
+FrameContext& default_frame_context();
+
+// update_crowd on an explicit context (the crowd.hpp form uses default_frame_context()).
+void update_crowd(Crowd& crowd, const Camera& camera, const UpdateOptions& opts, FrameContext& ctx);
+
+// ---- Stage functions, reference signatures (renderer.hpp:81-103), on the GPU ----
+// gather_splats projects every instance's posed_means (filled by update_crowd) with its
+// active level's covariance, colour and opacity; survivors in (instance, gaussian) order.
+SplatFrame gather_splats(const Crowd& crowd, const Camera& camera, int thread_count = 0);
+void gather_splats(const Crowd& crowd, const Camera& camera, int thread_count, FrameContext& ctx);  // -> ctx.frame
+// Ascending depth bits, ties by (instance_id, gaussian_index): a stable GPU radix sort.
+void sort_splats(SplatFrame& frame);
+void sort_splats(FrameContext& ctx);  // ctx.frame in place
+// Conic prep, tile binning in the given splat order, per-tile front-to-back blending.
+Framebuffer rasterize(const SplatFrame& frame, const RenderSettings& settings, int width, int height);
+RasterOutput rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height);
+void rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
+                    FrameContext& ctx);  // -> ctx.out
+
+// Explicit-context variants: the fused update + gather of one time step (the reference's
+// update_crowd then gather_splats, without host posed means), and sort / raster on ctx.
 SplatFrame gather_splats(Crowd& crowd, const Camera& camera, float time_s, const RenderSettings& settings,
                          bool static_pose, std::optional<uint32_t> forced_lod, FrameContext& ctx);
 void sort_splats(SplatFrame& frame, FrameContext& ctx);
-RasterOutput rasterize_full(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
-                            FrameContext& ctx);
 Framebuffer rasterize(const SplatFrame& frame, const RenderSettings& settings, int width, int height,
                       FrameContext& ctx);
 

@@ -483,7 +483,8 @@ def test_config5_forced_lod0_crowd_against_oracle():
 
 
 def test_pair_count_past_32_bits_is_reported_as_oom():
-    """K >= 2^32 tile-splat pairs (config 5 at tile size 2: ~5 G pairs) must surface as
+    """K >= 2^32 tile-splat pairs (config 5 at tile size 1: every splat's rect is at least
+    4x4 pixels after the 0.3 px^2 dilation, so K > 16 x 519 M) must surface as
     GSCG_ERR_OOM (the reference's bench skips such a cell as "out of memory",
     bench.cpp:94-97) before any buffer is grown, not alias into the splat count; the
     context stays usable afterwards."""
@@ -492,7 +493,7 @@ def test_pair_count_past_32_bits_is_reported_as_oom():
     s, extra = config5_scene(3500)
     r = P.Renderer(s, device_poses=True)
     with pytest.raises(N.NativeError) as e:
-        r.render_frame(0.0, P.RenderSettings(tile_size=2), forced_lod=0)
+        r.render_frame(0.0, P.RenderSettings(tile_size=1), forced_lod=0)
     assert e.value.status == N.GSCG_ERR_OOM and "pair count" in str(e.value)
     rgb, _ = r.render_frame(0.0, P.RenderSettings(), forced_lod=2)  # same context, a normal frame
     assert r.counts()[1] > 0 and np.isfinite(rgb).all()
