@@ -314,6 +314,9 @@ int gscg_rasterize_splats(gscg_ctx* ctx, const gscg_frame_splat* splats, uint64_
 
 /* The device pose sampler's sinf (glibc replica) over host arguments. */
 int gscg_eval_sinf(gscg_ctx* ctx, const float* in, float* out, uint32_t n);
+/* The rasteriser's expf (bit-exact replica of the host libm's, gscg_expf.cuh) over the n
+ * consecutive float bit patterns starting at first_bits. */
+int gscg_eval_expf(gscg_ctx* ctx, uint32_t first_bits, uint32_t n, float* out);
 
 /* ---- Multi-GPU frame: instance shards -> screen bands ----
  * The reference renders one frame in one process (renderer.cpp:249-280); these three

@@ -957,3 +957,14 @@ int orc_skin_means(orc_scene* s, uint32_t tid, uint32_t level, const float* worl
 extern "C" void orc_libm_sinf(const float* in, float* out, uint64_t n) {
     for (uint64_t i = 0; i < n; ++i) out[i] = std::sin(in[i]);
 }
+
+// The host libm's expf over consecutive float bit patterns [first_bits, first_bits + n):
+// what the reference's raster calls (renderer.cpp:205); the checker for the device replica.
+extern "C" void orc_libm_expf_range(uint32_t first_bits, uint64_t n, float* out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t b = first_bits + static_cast<uint32_t>(i);
+        float x;
+        std::memcpy(&x, &b, 4);
+        out[i] = std::exp(x);
+    }
+}

@@ -107,6 +107,7 @@ int orc_skin_means(orc_scene* s, uint32_t template_id, uint32_t level, const flo
 /* The host libm's sinf (what slerp_shortest calls, avatar.cpp:240-241) over an array: the
  * checker for the device pose sampler's replica. */
 void orc_libm_sinf(const float* in, float* out, uint64_t n);
+void orc_libm_expf_range(uint32_t first_bits, uint64_t n, float* out);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,7 @@ _SIGS = {
     "orc_get_bins": (C.c_int, [_P, _P, _P]),
     "orc_get_level_cov": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "orc_libm_sinf": (None, [_P, _P, C.c_uint64]),
+    "orc_libm_expf_range": (None, [C.c_uint32, C.c_uint64, _P]),
     "orc_build_covariance": (C.c_int, [_P, _P, _P]),
     "orc_camera": (C.c_int, [_P, _P, C.c_float, C.c_int32, C.c_int32, C.c_float, _P, _P, _P]),
     "orc_project": (C.c_int, [_P, _P, _P, C.c_float, _P, _P, C.c_float, C.c_int32, C.c_int32, C.c_float, _P]),
@@ -229,4 +230,12 @@ def libm_sinf(x: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=np.float32)
     out = np.empty_like(x)
     lib().orc_libm_sinf(_p(x), _p(out), x.size)
+    return out
+
+
+def libm_expf_range(first_bits: int, n: int) -> np.ndarray:
+    """The host libm's expf over n consecutive float bit patterns (checker for the
+    rasteriser's device expf replica)."""
+    out = np.empty(n, dtype=np.float32)
+    lib().orc_libm_expf_range(first_bits, n, _p(out))
     return out

@@ -1575,6 +1575,21 @@ int gscg_eval_sinf(gscg_ctx* ctx, const float* in, float* out, uint32_t n) {
     });
 }
 
+int gscg_eval_expf(gscg_ctx* ctx, uint32_t first_bits, uint32_t n, float* out) {
+    if (!ctx || (n && !out)) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        if (!n) return;
+        DevBuf b;
+        CUDA_TRY(b.ensure_exact(n * 4ull));
+        k_eval_expf<<<std::min<uint32_t>((n + 255) / 256, 8192), 256, 0, ctx->stream>>>(first_bits, n, b.as<float>());
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(out, b.ptr, n * 4ull, cudaMemcpyDefault, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        b.release();
+    });
+}
+
 int gscg_device_alloc(gscg_ctx* ctx, uint64_t bytes, void** out) {
     if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
     *out = nullptr;

@@ -128,6 +128,7 @@ struct PoseParams {
 
 __global__ void k_sample_poses(PoseParams p);
 __global__ void k_eval_sinf(const float* in, float* out, uint32_t n);
+__global__ void k_eval_expf(uint32_t first_bits, uint32_t n, float* out);
 
 __global__ void k_lod_plan(PlanParams p);
 

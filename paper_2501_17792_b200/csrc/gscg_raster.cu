@@ -10,15 +10,26 @@
 //     precomputed by the host (glibc, bit-identical to the reference);
 //   * the splat that pushes T below the floor is blended, then the pixel stops;
 //   * output = rgb + T * background, and T itself.
-// The per-pixel power is computed with round-to-nearest intrinsics in the reference
-// order (renderer.cpp:197-204) so the set of contributing (pixel, splat) pairs is the
-// reference's; alpha uses the hardware exp2 path (tolerance-checked).
+// Every operation of the per-pixel blend is single-rounded in the reference order
+// (renderer.cpp:197-226): power, alpha = opacity * expf(power) with a bit-exact replica of
+// the host libm's expf (gscg_expf.cuh), the clamp, w = T * alpha, rgb += w * colour (no
+// FMA), T *= 1 - alpha and rgb + T * background; so every pixel and T equal the
+// reference's bit for bit.
 #include "gscg_common.cuh"
+#include "gscg_expf.cuh"
 #include "gscg_kernels.h"
 
 namespace gscg {
 
 namespace {
+
+__constant__ unsigned long long c_exp2f_tab[32] = GSCG_EXP2F_TAB;
+
+// The expf table in shared memory (lanes index it independently; the constant bank would
+// serialise divergent indices).
+__device__ __forceinline__ void load_exp_table(unsigned long long* s_tab) {
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) s_tab[i] = c_exp2f_tab[i];
+}
 
 struct SplatView {
     float mx, my, a, b, c, o, pf, r, g, bl;
@@ -56,16 +67,17 @@ __device__ __forceinline__ float pixel_power(const SplatView& s, float fx, float
 
 // Blend one splat into one pixel; returns true when the pixel reaches the floor.
 __device__ __forceinline__ bool blend(const SplatView& s, int px, int py, float& T, float& cr,
-                                      float& cg, float& cb, float amax, float tfloor) {
+                                      float& cg, float& cb, float amax, float tfloor,
+                                      const unsigned long long* tab) {
     if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) return false;
     const float power = pixel_power(s, static_cast<float>(px) + 0.5f, static_cast<float>(py) + 0.5f);
     if (power < s.pf) return false;
-    const float alpha = fminf(s.o * __expf(power), amax);
-    const float w = T * alpha;
-    cr = fmaf(w, s.r, cr);
-    cg = fmaf(w, s.g, cg);
-    cb = fmaf(w, s.bl, cb);
-    T = T * (1.0f - alpha);
+    const float alpha = fminf(__fmul_rn(s.o, glibc_expf(power, tab)), amax);
+    const float w = __fmul_rn(T, alpha);
+    cr = __fadd_rn(cr, __fmul_rn(w, s.r));
+    cg = __fadd_rn(cg, __fmul_rn(w, s.g));
+    cb = __fadd_rn(cb, __fmul_rn(w, s.bl));
+    T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
     return T < tfloor;
 }
 
@@ -126,6 +138,9 @@ k_raster16q(RasterParams p) {
     __shared__ float4 s_geo[2][2][kStage];   // [warp][buffer][slot]
     __shared__ float4 s_col[2][2][kStage];
     __shared__ float4 s_ext[2][2][kStage];   // G, B, rect lo, rect hi
+    __shared__ unsigned long long s_tab[32];
+    load_exp_table(s_tab);
+    __syncthreads();
     const int tile = blockIdx.x >> 2, quad = blockIdx.x & 3;
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -187,13 +202,13 @@ k_raster16q(RasterParams p) {
             const float q = __fadd_rn(__fmul_rn(__fmul_rn(g.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
             const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(g.w, dx), dy));
             if (power < c.z) continue;
-            const float alpha = fminf(c.y * __expf(power), p.alpha_max);
-            const float w = T * alpha;
+            const float alpha = fminf(__fmul_rn(c.y, glibc_expf(power, s_tab)), p.alpha_max);
+            const float w = __fmul_rn(T, alpha);
             const float4 e = ext[k];
-            cr = fmaf(w, c.w, cr);
-            cg = fmaf(w, e.x, cg);
-            cb = fmaf(w, e.y, cb);
-            T = T * (1.0f - alpha);
+            cr = __fadd_rn(cr, __fmul_rn(w, c.w));
+            cg = __fadd_rn(cg, __fmul_rn(w, e.x));
+            cb = __fadd_rn(cb, __fmul_rn(w, e.y));
+            T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
             if (T < p.t_floor) {
                 done = true;
                 todo0 = todo1 = 0u;
@@ -205,9 +220,9 @@ k_raster16q(RasterParams p) {
     cp_async_wait<0>();
     if (inside) {
         const size_t o = static_cast<size_t>(py - p.out_row0) * p.width + px;
-        p.out_rgb[3 * o + 0] = cr + T * p.bg[0];
-        p.out_rgb[3 * o + 1] = cg + T * p.bg[1];
-        p.out_rgb[3 * o + 2] = cb + T * p.bg[2];
+        p.out_rgb[3 * o + 0] = __fadd_rn(cr, __fmul_rn(T, p.bg[0]));
+        p.out_rgb[3 * o + 1] = __fadd_rn(cg, __fmul_rn(T, p.bg[1]));
+        p.out_rgb[3 * o + 2] = __fadd_rn(cb, __fmul_rn(T, p.bg[2]));
         p.out_T[o] = T;
     }
 }
@@ -217,6 +232,8 @@ template <int PPT>
 __global__ void __launch_bounds__(256)
 k_raster_generic(RasterParams p) {
     __shared__ float4 s_rec[256 * 3];
+    __shared__ unsigned long long s_tab[32];
+    load_exp_table(s_tab);
     const int ts = p.tile_size;
     const int tile = blockIdx.x;
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
@@ -251,7 +268,7 @@ k_raster_generic(RasterParams p) {
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 if (!live[k]) continue;
-                if (blend(v, pxs[k], pys[k], T[k], cr[k], cg[k], cb[k], p.alpha_max, p.t_floor)) {
+                if (blend(v, pxs[k], pys[k], T[k], cr[k], cg[k], cb[k], p.alpha_max, p.t_floor, s_tab)) {
                     live[k] = false;
                     --live_count;
                 }
@@ -264,9 +281,9 @@ k_raster_generic(RasterParams p) {
         const int lp = threadIdx.x + k * 256;
         if (lp < ts * ts && pxs[k] < p.width && pys[k] < p.height) {
             const size_t o = static_cast<size_t>(pys[k] - p.out_row0) * p.width + pxs[k];
-            p.out_rgb[3 * o + 0] = cr[k] + T[k] * p.bg[0];
-            p.out_rgb[3 * o + 1] = cg[k] + T[k] * p.bg[1];
-            p.out_rgb[3 * o + 2] = cb[k] + T[k] * p.bg[2];
+            p.out_rgb[3 * o + 0] = __fadd_rn(cr[k], __fmul_rn(T[k], p.bg[0]));
+            p.out_rgb[3 * o + 1] = __fadd_rn(cg[k], __fmul_rn(T[k], p.bg[1]));
+            p.out_rgb[3 * o + 2] = __fadd_rn(cb[k], __fmul_rn(T[k], p.bg[2]));
             p.out_T[o] = T[k];
         }
     }
@@ -277,6 +294,15 @@ void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream) {
     else if (p.tile_size <= 16) k_raster_generic<1><<<tiles, 256, 0, stream>>>(p);
     else if (p.tile_size <= 32) k_raster_generic<4><<<tiles, 256, 0, stream>>>(p);
     else k_raster_generic<16><<<tiles, 256, 0, stream>>>(p);
+}
+
+// The expf replica over consecutive float bit patterns (gscg_eval_expf: parity check).
+__global__ void k_eval_expf(uint32_t first_bits, uint32_t n, float* out) {
+    __shared__ unsigned long long s_tab[32];
+    load_exp_table(s_tab);
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = glibc_expf(__uint_as_float(first_bits + i), s_tab);
 }
 
 }  // namespace gscg

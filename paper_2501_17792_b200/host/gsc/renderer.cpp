@@ -4,6 +4,7 @@
 // the GPU).
 #include "gsc/renderer.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <string>
@@ -331,7 +332,15 @@ void render_frame_host(Crowd& crowd, const Camera& camera, float time_s, const R
     check_gscg(pipelined ? gscg_render_frame_async(ctx.gpu(), &fd, &cam, &rs, &lp, out_rgb, out_T, &st)
                          : gscg_render_frame(ctx.gpu(), &fd, &cam, &rs, &lp, out_rgb, out_T, &st),
                ctx.gpu());
-    for (size_t i = 0; i < crowd.instances.size(); ++i) crowd.instances[i].active_lod = ctx.lods[i];
+    for (size_t i = 0; i < crowd.instances.size(); ++i) {
+        CrowdInstance& inst = crowd.instances[i];
+        inst.active_lod = ctx.lods[i];
+        // The frame's posed means live on the GPU: host copies from an earlier update_crowd
+        // are stale now; gather_splats re-derives this frame's from the stamp.
+        if (!inst.posed_means.empty()) inst.posed_means.clear();
+        inst.posed_valid = false;
+    }
+    crowd.gpu_pose = Crowd::GpuPoseStamp{time_s, static_pose};
 
     if (times) {
         times->pose_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -466,6 +475,7 @@ void update_crowd(Crowd& crowd, const Camera& camera, const UpdateOptions& opts,
               inst.posed_means.size() == tpl.levels[lod].gaussian_count()))
             stale = true;
     }
+    crowd.gpu_pose.reset();
     if (!stale) return;
     // Pose + FK + skin matrices + LBS of every instance's active level on the GPU.
     ctx.ensure_templates(crowd.templates);
@@ -501,11 +511,37 @@ void update_crowd(Crowd& crowd, const Camera& camera, const UpdateOptions& opts,
     }
 }
 
-void gather_splats(const Crowd& crowd, const Camera& camera, int /*thread_count*/, FrameContext& ctx) {
+void gather_splats(const Crowd& crowd, const Camera& camera, int thread_count, FrameContext& ctx) {
     ctx.frame.width = camera.width;
     ctx.frame.height = camera.height;
     ctx.frame.splats.clear();
     ctx.ensure_templates(crowd.templates);
+    const bool none_posed = std::all_of(crowd.instances.begin(), crowd.instances.end(),
+                                        [](const CrowdInstance& i) { return i.posed_means.empty(); });
+    if (crowd.gpu_pose && none_posed && !crowd.instances.empty()) {
+        // After render_frame: the posed means of that frame (its time, its levels) are
+        // re-derived on the GPU; identical to what update_crowd would have left behind.
+        ctx.sample_crowd(crowd, crowd.gpu_pose->time_s, crowd.gpu_pose->static_pose, thread_count);
+        gscg_frame_desc fd{};
+        fd.instance_count = static_cast<uint32_t>(crowd.instances.size());
+        fd.joint_stride = ctx.joint_stride;
+        fd.template_ids = ctx.template_ids.data();
+        fd.placement = ctx.placement.data();
+        fd.poses = ctx.poses.data();
+        fd.active_lod = ctx.lods.data();
+        fd.forced_lod = GSCG_LOD_GIVEN;
+        fd.memory = GSCG_MEM_HOST;
+        const gscg_camera cam = camera_basis(camera);
+        const gscg_render_settings rs = to_gscg(RenderSettings{});
+        gscg_lod_policy lp{};
+        uint64_t count = 0;
+        check_gscg(gscg_gather_splats(ctx.gpu(), &fd, &cam, &rs, &lp, nullptr, 0, &count), ctx.gpu());
+        ctx.frame.splats.resize(count);
+        check_gscg(gscg_gather_splats(ctx.gpu(), &fd, &cam, &rs, &lp,
+                                      reinterpret_cast<gscg_frame_splat*>(ctx.frame.splats.data()), count, &count),
+                   ctx.gpu());
+        return;
+    }
     const TemplateStore& templates = *crowd.templates;
     const uint32_t n = static_cast<uint32_t>(crowd.instances.size());
     std::vector<uint32_t> tids(std::max<uint32_t>(n, 1)), lods(std::max<uint32_t>(n, 1)), mask(std::max<uint32_t>(n, 1));

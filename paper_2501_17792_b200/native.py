@@ -136,6 +136,7 @@ GSCG_SYMBOLS = {
     "gscg_template_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "gscg_upload_motion": (C.c_int, [_P, C.c_uint32, C.POINTER(GscgMotionDesc)]),
     "gscg_eval_sinf": (C.c_int, [_P, _P, _P, C.c_uint32]),
+    "gscg_eval_expf": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "gscg_gather_splats": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                      C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, C.c_uint64,
                                      C.POINTER(C.c_uint64)]),
