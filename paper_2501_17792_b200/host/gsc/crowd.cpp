@@ -153,4 +153,27 @@ MemoryReport memory_report_cell(uint64_t instances, uint64_t gaussians,
     return make_report(model, instances > 0 ? gaussians : 0, instances * gaussians, instances);
 }
 
+void update_crowd_lod(Crowd& crowd, const Camera& camera, std::optional<uint32_t> forced_lod) {
+    const TemplateStore& templates = *crowd.templates;
+    for (CrowdInstance& inst : crowd.instances) {
+        if (inst.template_id >= templates.size()) throw std::invalid_argument("update_crowd: missing template");
+        const AvatarTemplate& tpl = templates[inst.template_id];
+        const uint32_t last = static_cast<uint32_t>(tpl.levels.size()) - 1;
+        uint32_t lod;
+        if (forced_lod) {
+            lod = std::min(*forced_lod, last);
+        } else {
+            const Vec3 root_pos(inst.x, tpl.skeleton.bind[0].translation()[1], inst.z);
+            const float dist = instance_distance(root_pos, camera.position);
+            std::optional<uint32_t> prev;
+            if (inst.active_lod != kLodUnset) prev = inst.active_lod;
+            lod = std::min(select_lod(crowd.lod, dist, prev), last);
+        }
+        if (lod != inst.active_lod) {
+            inst.active_lod = lod;
+            inst.posed_valid = false;
+        }
+    }
+}
+
 }  // namespace gsc

@@ -450,29 +450,12 @@ void update_crowd(Crowd& crowd, const Camera& camera, const UpdateOptions& opts,
     if (opts.skin_rotations)
         throw std::invalid_argument("update_crowd: rotation skinning is not supported by the B200 path");
     const TemplateStore& templates = *crowd.templates;
-    // LoD (crowd.cpp:93-110) on the host, bit-exact with k_lod_plan.
+    update_crowd_lod(crowd, camera, opts.forced_lod);
     bool stale = false;
-    for (CrowdInstance& inst : crowd.instances) {
-        if (inst.template_id >= templates.size()) throw std::invalid_argument("update_crowd: missing template");
-        const AvatarTemplate& tpl = templates[inst.template_id];
-        const uint32_t last = static_cast<uint32_t>(tpl.levels.size()) - 1;
-        uint32_t lod;
-        if (opts.forced_lod) {
-            lod = std::min(*opts.forced_lod, last);
-        } else {
-            const Vec3 root_pos(inst.x, tpl.skeleton.bind[0].translation()[1], inst.z);
-            const float dist = instance_distance(root_pos, camera.position);
-            std::optional<uint32_t> prev;
-            if (inst.active_lod != kLodUnset) prev = inst.active_lod;
-            lod = std::min(select_lod(crowd.lod, dist, prev), last);
-        }
-        if (lod != inst.active_lod) {
-            inst.active_lod = lod;
-            inst.posed_valid = false;
-        }
+    for (const CrowdInstance& inst : crowd.instances) {
         // crowd.cpp:112-116: a static instance with valid posed means is left alone.
         if (!(opts.static_pose && inst.posed_valid &&
-              inst.posed_means.size() == tpl.levels[lod].gaussian_count()))
+              inst.posed_means.size() == templates[inst.template_id].levels[inst.active_lod].gaussian_count()))
             stale = true;
     }
     crowd.gpu_pose.reset();

@@ -284,9 +284,9 @@ int gsch_scene_set_motion(gsch_scene* s, uint32_t m, float fps, uint32_t frames,
 int gsch_scene_update_crowd(gsch_scene* s, int32_t forced_lod) {
     return guarded([&] {
         if (!s) throw std::invalid_argument("null scene");
-        UpdateOptions opts;
-        if (forced_lod >= 0) opts.forced_lod = static_cast<uint32_t>(forced_lod);
-        update_crowd(s->crowd, s->camera, opts);
+        std::optional<uint32_t> forced;
+        if (forced_lod >= 0) forced = static_cast<uint32_t>(forced_lod);
+        update_crowd_lod(s->crowd, s->camera, forced);  // the LoD step (no GPU)
     });
 }
 

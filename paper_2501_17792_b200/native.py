@@ -141,6 +141,10 @@ GSCG_SYMBOLS = {
                                      C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, C.c_uint64,
                                      C.POINTER(C.c_uint64)]),
     "gscg_sort_splats": (C.c_int, [_P, _P, C.c_uint64]),
+    "gscg_skin_means": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera), C.POINTER(GscgLodPolicy), _P,
+                                  C.c_uint64, C.POINTER(C.c_uint64)]),
+    "gscg_gather_posed": (C.c_int, [_P, C.POINTER(GscgFrameDesc), _P, C.c_uint64, _P, C.POINTER(GscgCamera),
+                                    C.POINTER(GscgRenderSettings), _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     "gscg_rasterize_splats": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(GscgRenderSettings),
                                         _P, _P]),
     "gscg_set_debug": (C.c_int, [_P, C.c_uint32]),
