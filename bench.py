@@ -290,29 +290,24 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                     "launches": st.kernel_launches, "counts": (st.gaussian_count, st.splat_count, st.pair_count),
                     "tile_pairs": st.tile_pair_count}
     else:
-        # Band path: shard projection -> NCCL all-to-all -> band render -> gather.
-        from paper_2501_17792_b200.multigpu import BandRank, FrameArgs, LoadBalancer, TorchExchange
-        ex = TorchExchange()
-        br = BandRank(scene, device=local_rank, renderer=r)
-        balancer = LoadBalancer(scene, world, settings.tile_size)
+        # Band-split frame: rank r renders screen rows [rows[r], rows[r+1]) of
+        # the frame (its own instance cull + projection + sort + raster), and the bands are
+        # gathered into rank 0's framebuffer in HBM, one gscg_group_render_frame per frame.
+        from paper_2501_17792_b200.multigpu import BandGroup
+        group = BandGroup(r, rank, world, dist)
+        group.set_tile(settings.tile_size)
 
         def frame(f: int) -> dict:
-            # shards by last frame's Gaussians per instance, bands by last frame's pairs per tile row
-            shards, rows = balancer.plan()
-            br.project(FrameArgs(times_s[f], False, forced), settings, shards[rank], rows, frame=frame_desc(f))
-            send = br.pack()
-            with torch.cuda.stream(stream):
-                recv, rc = ex.all_to_all(send, br.counts.tolist())
-                rgb, T = br.render_band(recv, sum(rc), rows[rank], rows[rank + 1])
-                ex.gather_rows(rgb, rows)  # the bands assembled into the full frame on rank 0
-                ex.gather_rows(T, rows)
-                if f % 4 == 0:  # re-balance every 4th frame (the observation reads back LoDs and cell ranges)
-                    balancer.observe(d_lods[:n].cpu().numpy(), br.band_row_pairs(), rows[rank] // settings.tile_size, ex)
-            a, b = br.shard_times, br.band_times
-            return {"update": a.update_ms, "gather": a.gather_ms, "route": a.sort_ms, "unpack": b.gather_ms,
-                    "sort": b.sort_ms, "rasterize": b.rasterize_ms,
-                    "launches": a.kernel_launches + 1 + b.kernel_launches,
-                    "counts": (a.gaussian_count, a.splat_count, b.pair_count), "tile_pairs": a.tile_pair_count}
+            st = group.render(frame_desc(f), cam, rs, lp)
+            return {"update": st.update_ms, "gather": st.gather_ms, "sort": st.sort_ms, "rasterize": st.rasterize_ms,
+                    "launches": st.kernel_launches, "counts": (st.gaussian_count, st.splat_count, st.pair_count),
+                    "tile_pairs": st.tile_pair_count}
+
+        # Balance the bands on the warm-up frames (pairs per tile row over all ranks);
+        # the timed frames keep the last rows.
+        for f in range(2):
+            frame(f)
+            group.rebalance()
 
     first = None
     for f in range(args.warmup):
@@ -388,15 +383,31 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
 
         e2e_sync_fps = time_e2e(e2e_sync)
     else:
-        from paper_2501_17792_b200.multigpu import DistributedRenderer
-        drr = DistributedRenderer(scene, local_rank, exchange=ex, band=br)
+        # Public API per step: the instance records from pinned host memory, the band
+        # frame, the gather, and rank 0's read-back of the frame's colour into pinned memory.
+        rec = r.instance_records()
+        pinned = {k: P.pinned_array(v.shape, v.dtype) for k, v in rec.items()}
+        for k, v in rec.items():
+            pinned[k][...] = v
+        band_out = P.pinned_array((cfg.height, cfg.width, 3))
 
-        band_out = (torch.empty((cfg.height, cfg.width, 3), dtype=torch.float32, pin_memory=True).numpy(), None)
-
-        def e2e_frame(f):  # colour read-back into page-locked memory, as the single-GPU leg
-            drr.render_frame(times_s[f], settings, forced_lod=forced, out=band_out)
+        def e2e_frame(f):
+            fd = N.GscgFrameDesc()
+            fd.instance_count = n
+            fd.joint_stride = js
+            fd.template_ids = pinned["template_ids"].ctypes.data
+            fd.placement = pinned["placement"].ctypes.data
+            fd.active_lod = pinned["lods"].ctypes.data
+            fd.forced_lod = -1 if forced is None else forced
+            fd.memory = N.GSCG_MEM_HOST
+            fd.pose_source = N.GSCG_POSES_SAMPLED
+            fd.time_s = times_s[f]
+            fd.motion_ids = pinned["motion_ids"].ctypes.data
+            fd.phase_offsets = pinned["phase_offsets"].ctypes.data
+            group.render(fd, cam, rs, lp, band_out if rank == 0 else None)
 
         e2e_fps = time_e2e(e2e_frame)
+        group.close()
     h2d = n * (4 + 16 + 4 + 4 + 4)  # template id, placement, previous LoD, motion id, phase offset
     d2h = cfg.width * cfg.height * 12 + n * 4
 
@@ -438,7 +449,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": bench_config(args.config, cfg, cfg_counts, cfg_tile_pairs,
-                               f"{world} instance shards -> {world} screen bands, NCCL" if band_path else "single GPU"),
+                               f"{world} screen bands (one per GPU), NCCL gather to rank 0" if band_path else "single GPU"),
         "median_frame_ms": round(median_ms, 4), "fps_median": round(1000.0 / median_ms, 3),
         "colour": "SH degree 3 (BASELINE; the reference renders fixed RGB)",
         "instances_culled": culled,
@@ -458,7 +469,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
                                  "issue-bound, per-pixel list walks (ncu DRAM < 10%); profiles/ncu_summary.json")},
         "e2e": {"value": round(e2e_fps, 3), "unit": "FPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": ("Renderer.render_frame(out=pinned, pipelined=True): frame k's read-back overlaps frame k+1"
-                        if not band_path else "DistributedRenderer.render_frame"),
+                        if not band_path else "gscg_group_render_frame: host instance records in, frame colour out on rank 0"),
                 "blocking_api_fps": None if e2e_sync_fps is None else round(e2e_sync_fps, 3)},
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -558,7 +569,7 @@ def run_reference(args, rank, world) -> dict | None:
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": bench_config(args.config, cfg, (times0.gaussian_count, times0.splat_count, 0), tile_pairs,
                                    "single GPU" if world == 1 else
-                                   f"{world} instance shards -> {world} screen bands, NCCL"),
+                                   f"{world} screen bands (one per GPU), NCCL gather to rank 0"),
             "median_frame_ms": round(med, 3), "fps_median": round(1000.0 / med, 4),
             "colour": ("RGB: the reference has no SH (SURVEY.md 0.4); same geometry, splats and tile pairs"
                        if kind == "reference" else "SH degree 3 (oracle port)"),

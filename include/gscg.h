@@ -204,6 +204,16 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out);
 
 int gscg_set_debug(gscg_ctx* ctx, uint32_t flags);
 
+/* Band frames (the multi-GPU frame): gscg_render_frame / _async render
+ * only screen rows [row_begin, row_end) (tile-aligned; row_end may be the frame height):
+ * the instance cull and the projection keep the splats whose pixel rect meets those rows,
+ * the sort and the raster cover the band's tiles, and fb_rgb / fb_T receive the band's
+ * rows only ((row_end - row_begin) x width). Every band pixel is bit-identical to the same
+ * pixel of the whole frame: a tile's list is the reference's bin (renderer.cpp:147-161),
+ * ordinals and LoD are computed over the whole crowd. row_end <= row_begin (0, 0): the
+ * whole frame. Persistent per context. */
+int gscg_set_band(gscg_ctx* ctx, int32_t row_begin, int32_t row_end);
+
 /* Renders one frame. fb_rgb (W*H*3) and fb_T (W*H) receive the framebuffer and the
  * final transmittance; with memory == GSCG_MEM_HOST they are host pointers (copied back
  * before return), with GSCG_MEM_DEVICE they may be NULL (result stays in the context,
@@ -343,6 +353,29 @@ int gscg_project_shard(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_c
 int gscg_pack_bands(gscg_ctx* ctx, void* send_dev);
 int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, uint32_t row_begin,
                      uint32_t row_end, float* fb_rgb, float* fb_T, int32_t memory, gscg_stage_times* times);
+
+/* ---- Multi-GPU frame as one group call per frame ----
+ * One process per GPU. Rank 0 makes a unique id (gscg_group_unique_id), the caller's
+ * plumbing (e.g. torch.distributed) broadcasts the 128 bytes, every rank calls
+ * gscg_group_create on its own context (ncclCommInitRank: the group owns the NCCL
+ * communicator). gscg_group_render_frame renders rank r's band rows [band_rows[r],
+ * band_rows[r+1]) of the frame (band_rows: nranks + 1 ascending tile-aligned rows from 0 to
+ * the height; see gscg_set_band) and gathers every band into rank 0's framebuffer with
+ * grouped ncclSend/ncclRecv on the context stream; on rank 0 fb_rgb / fb_T (host or
+ * device, may be NULL) receive the whole frame, identical to gscg_render_frame's. The call
+ * does not synchronise the host unless rank 0 is given host destinations.
+ * gscg_group_row_costs: the pairs per tile row of the last frame over all ranks (an
+ * all-reduce), for re-balancing band_rows. */
+#define GSCG_UNIQUE_ID_BYTES 128
+typedef struct gscg_group gscg_group;
+int gscg_group_unique_id(uint8_t* out /* GSCG_UNIQUE_ID_BYTES */);
+int gscg_group_create(gscg_ctx* ctx, const uint8_t* unique_id, int32_t nranks, int32_t rank, gscg_group** out);
+int gscg_group_destroy(gscg_group* group);
+int gscg_group_render_frame(gscg_group* group, const gscg_frame_desc* frame, const gscg_camera* cam,
+                            const gscg_render_settings* settings, const gscg_lod_policy* lod, const uint32_t* band_rows,
+                            float* fb_rgb, float* fb_T, gscg_stage_times* times);
+int gscg_group_framebuffer_device(gscg_group* group, float** rgb, float** T); /* rank 0 */
+int gscg_group_row_costs(gscg_group* group, uint32_t tiles_y, uint64_t* out /* tiles_y */);
 
 #ifdef __cplusplus
 }

@@ -409,6 +409,9 @@ class Renderer:
         arrays from alloc_frame) and the Renderer keeps it alive until it has landed."""
         settings = settings or RenderSettings()
         W, H = self.scene.cfg.width, self.scene.cfg.height
+        band = getattr(self, "_band", None)
+        if band is not None:
+            H = min(band[1], H) - band[0]
         if pipelined and out is None:
             raise ValueError("render_frame(pipelined=True) needs `out` arrays: the read-back completes after the call")
         if out is None:
@@ -432,6 +435,13 @@ class Renderer:
             for f in StageTimes.__dataclass_fields__:
                 setattr(times, f, getattr(st, f))
         return rgb, T
+
+    def set_band(self, row_begin: int = 0, row_end: int = 0) -> None:
+        """Render only screen rows [row_begin, row_end) (tile-aligned; gscg_set_band):
+        render_frame then returns the band's rows, bit-identical to the same rows of the
+        whole frame. (0, 0) = the whole frame."""
+        N.check_gscg(N.gscg().gscg_set_band(self.gpu, row_begin, row_end), self.gpu)
+        self._band = (row_begin, row_end) if row_end > row_begin else None
 
     def wait_readback(self, frames_back: int = 0) -> None:
         """Blocks until the read-back of the pipelined frame submitted `frames_back`

@@ -17,12 +17,15 @@
 // sort and detects capacity overflow (buffers grow to the high-water mark and the
 // gather is replayed, as the reference's buffers grow, crowd.hpp:26-28).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -124,6 +127,8 @@ struct Status : std::runtime_error {
 struct FrameGeom {
     int W = 0, H = 0, ts = 16, tiles_x = 0, tiles_y = 0, cell = 8;
     uint32_t cells_per_tile = 1;
+    int band_y0 = 0, band_y1 = 0;  // rows rendered: the frame, or the band of gscg_set_band
+    int band_tile_row0 = 0, band_tile_rows = 0;
 };
 
 struct gscg_ctx {
@@ -132,6 +137,7 @@ struct gscg_ctx {
     cudaStream_t stream = nullptr;
     std::string error;
     uint32_t debug = 0;
+    int32_t band_req0 = 0, band_req1 = 0;  // gscg_set_band rows (0, 0: the whole frame)
 
     std::vector<TemplateStore> templates;
     std::vector<MotionStore> motions;
@@ -413,7 +419,24 @@ void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_came
     g.tiles_y = (g.H + g.ts - 1) / g.ts;
     g.cells_per_tile = g.ts == 16 ? 4u : 1u;  // 8x8 quadrant binning for tile 16
     g.cell = g.ts == 16 ? 8 : g.ts;
+    g.band_y0 = 0;  // the whole frame; gscg_render_frame applies gscg_set_band's rows (apply_band)
+    g.band_y1 = g.H;
+    g.band_tile_row0 = 0;
+    g.band_tile_rows = g.tiles_y;
     ctx->settings = *settings;
+}
+
+// gscg_set_band's rows for a render: the frame keeps only the splats whose rect meets
+// rows [band_y0, band_y1) and rasterises those rows (the multi-GPU band frame).
+void apply_band(gscg_ctx* ctx) {
+    FrameGeom& g = ctx->geom;
+    if (ctx->band_req1 <= ctx->band_req0) return;
+    if (ctx->band_req0 % g.ts != 0 || (ctx->band_req1 % g.ts != 0 && ctx->band_req1 != g.H) || ctx->band_req1 > g.H)
+        invalid("gscg_set_band: rows must be tile-aligned and inside the frame");
+    g.band_y0 = ctx->band_req0;
+    g.band_y1 = ctx->band_req1;
+    g.band_tile_row0 = g.band_y0 / g.ts;
+    g.band_tile_rows = (g.band_y1 - g.band_y0 + g.ts - 1) / g.ts;
 }
 
 // H2D of the frame records, update (LoD plan + FK) and gather (projection) for the
@@ -544,6 +567,8 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
     camdev.near_m = cam->near_m;
     camdev.width = geo.W;
     camdev.height = geo.H;
+    camdev.band_y0 = geo.band_y0;
+    camdev.band_y1 = geo.band_y1;
     auto* counters = ctx->counters.as<FrameCounters>();
     for (int attempt = 0;; ++attempt) {
         if (lod_back && n && ctx->h_lod_cap < n) {
@@ -1144,6 +1169,15 @@ int gscg_destroy(gscg_ctx* ctx) {
 
 const char* gscg_last_error(const gscg_ctx* ctx) { return ctx ? ctx->error.c_str() : "null context"; }
 
+int gscg_set_band(gscg_ctx* ctx, int32_t row_begin, int32_t row_end) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (row_begin < 0 || row_end < row_begin) invalid("gscg_set_band: bad row range");
+        ctx->band_req0 = row_begin;
+        ctx->band_req1 = row_end;
+    });
+}
+
 int gscg_set_debug(gscg_ctx* ctx, uint32_t flags) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     ctx->debug = flags;
@@ -1318,6 +1352,7 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
     return guarded(ctx, [&] {
         CUDA_TRY(cudaSetDevice(ctx->device));
         validate_frame(ctx, frame, cam, settings, lod);
+        apply_band(ctx);
         const bool host = frame->memory == GSCG_MEM_HOST;
         const uint32_t n = frame->instance_count;
         uint32_t launches = 0;
@@ -1327,10 +1362,11 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         // Device destinations: one device-to-device copy after the frame.
         const bool overlap = is_host_pointer(fb_rgb) || is_host_pointer(fb_T);
         pipelined = pipelined && overlap;
-        const uint32_t passes = overlap ? sort_raster(ctx, 0, ctx->geom.tiles_y, launches, fb_rgb, fb_T, false,
-                                                      pipelined)
-                                        : sort_raster(ctx, 0, ctx->geom.tiles_y, launches);
-        if (!overlap) copy_out(ctx, ctx->geom.H, fb_rgb, fb_T, host);
+        const FrameGeom& g = ctx->geom;  // a band frame renders rows [band_y0, band_y1) only
+        const uint32_t passes = overlap ? sort_raster(ctx, g.band_tile_row0, g.band_tile_rows, launches, fb_rgb, fb_T,
+                                                      false, pipelined)
+                                        : sort_raster(ctx, g.band_tile_row0, g.band_tile_rows, launches);
+        if (!overlap) copy_out(ctx, g.band_y1 - g.band_y0, fb_rgb, fb_T, host);
         if (n && !host)
             CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice,
                                      ctx->stream));
@@ -2076,6 +2112,211 @@ int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         CUDA_TRY(cudaMemcpyAsync(out, ctx->sorted_ordinals.ptr, pairs * 4, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// Multi-GPU frame: one process per GPU, each rank owns a
+// gscg_ctx and renders one horizontal screen band of the SAME frame (gscg_set_band: its
+// own instance cull + projection keep the splats that meet its rows; sort + raster cover
+// its tiles), then the bands are gathered into rank 0's framebuffer with grouped
+// ncclSend / ncclRecv on the context stream (NVLink / NVSwitch). The only exchange is the
+// gather of finished rows: a splat that meets several bands is projected by each of those
+// ranks, which costs less here than routing every projected splat through an all-to-all
+// (DESIGN.md §5 has the measurement). NCCL is this library's own communicator; the
+// caller's process-group plumbing (torch.distributed) only ships the 128-byte unique id.
+struct gscg_group {
+    gscg_ctx* ctx = nullptr;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    DevBuf full_rgb, full_T, row_costs, all_costs;
+};
+
+namespace {
+
+// NCCL is bound at run time (dlopen of libnccl.so.2): a process that already holds one
+// (torch's bundled NCCL) keeps it — linking at build time would pin the system copy first
+// and break torch's own symbol versions.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    bool ok = false;
+};
+
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return a;
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+        a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+        a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(h, "ncclSend"));
+        a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(h, "ncclRecv"));
+        a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.GroupStart && a.GroupEnd && a.Send && a.Recv &&
+               a.AllReduce && a.GetErrorString;
+        return a;
+    }();
+    if (!api.ok) throw Status(GSCG_ERR_NCCL, "libnccl.so.2 not found (multi-GPU groups need NCCL)");
+    return api;
+}
+
+#define NCCL_TRY(expr)                                                                                \
+    do {                                                                                              \
+        ncclResult_t _r = (expr);                                                                     \
+        if (_r != ncclSuccess) throw Status(GSCG_ERR_NCCL, std::string(#expr) + ": " + nccl().GetErrorString(_r)); \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int gscg_group_unique_id(uint8_t* out) {
+    if (!out) return GSCG_ERR_INVALID_ARGUMENT;
+    ncclUniqueId id;
+    try {
+        if (nccl().GetUniqueId(&id) != ncclSuccess) return GSCG_ERR_NCCL;
+    } catch (const Status&) {
+        return GSCG_ERR_NCCL;
+    }
+    static_assert(sizeof(id) == GSCG_UNIQUE_ID_BYTES, "NCCL unique id size");
+    std::memcpy(out, &id, sizeof(id));
+    return GSCG_OK;
+}
+
+int gscg_group_create(gscg_ctx* ctx, const uint8_t* unique_id, int32_t nranks, int32_t rank, gscg_group** out) {
+    if (!ctx || !unique_id || !out || nranks < 1 || rank < 0 || rank >= nranks) return GSCG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        auto g = std::make_unique<gscg_group>();
+        g->ctx = ctx;
+        g->nranks = nranks;
+        g->rank = rank;
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof(id));
+        NCCL_TRY(nccl().CommInitRank(&g->comm, nranks, id, rank));
+        *out = g.release();
+    });
+}
+
+int gscg_group_destroy(gscg_group* g) {
+    if (!g) return GSCG_OK;
+    cudaSetDevice(g->ctx->device);
+    cudaStreamSynchronize(g->ctx->stream);
+    if (g->comm) nccl().CommDestroy(g->comm);
+    g->full_rgb.release();
+    g->full_T.release();
+    g->row_costs.release();
+    g->all_costs.release();
+    delete g;
+    return GSCG_OK;
+}
+
+int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const gscg_camera* cam,
+                            const gscg_render_settings* settings, const gscg_lod_policy* lod, const uint32_t* band_rows,
+                            float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+    if (!g || !band_rows || !cam) return GSCG_ERR_INVALID_ARGUMENT;
+    gscg_ctx* ctx = g->ctx;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        const int W = cam->width, H = cam->height, P = g->nranks;
+        if (band_rows[0] != 0 || band_rows[P] != static_cast<uint32_t>(H)) invalid("band_rows must cover [0, height)");
+        for (int r = 0; r < P; ++r)
+            if (band_rows[r + 1] < band_rows[r]) invalid("band_rows must be ascending");
+        const uint32_t y0 = band_rows[g->rank], y1 = band_rows[g->rank + 1];
+        // This rank's band, rendered into the context's framebuffer (rows from 0).
+        const int32_t save0 = ctx->band_req0, save1 = ctx->band_req1;
+        ctx->band_req0 = static_cast<int32_t>(y0);
+        ctx->band_req1 = static_cast<int32_t>(y1);
+        gscg_frame_desc fd = *frame;
+        int rc = GSCG_OK;
+        if (y1 > y0) rc = render_frame_impl(ctx, &fd, cam, settings, lod, nullptr, nullptr, times, false);
+        ctx->band_req0 = save0;
+        ctx->band_req1 = save1;
+        if (rc != GSCG_OK) throw Status(rc, ctx->error);
+        cudaStream_t s = ctx->stream;
+        const size_t row_px = static_cast<size_t>(W);
+        // Gather the bands on rank 0 (grouped point-to-point; the frame is assembled in HBM).
+        if (g->rank == 0) {
+            CUDA_TRY(g->full_rgb.ensure(row_px * H * 12));
+            CUDA_TRY(g->full_T.ensure(row_px * H * 4));
+            if (y1 > y0) {
+                CUDA_TRY(cudaMemcpyAsync(g->full_rgb.ptr, ctx->fb_rgb.ptr, row_px * (y1 - y0) * 12, cudaMemcpyDeviceToDevice, s));
+                CUDA_TRY(cudaMemcpyAsync(g->full_T.ptr, ctx->fb_T.ptr, row_px * (y1 - y0) * 4, cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        if (P > 1) {
+            NCCL_TRY(nccl().GroupStart());
+            if (g->rank == 0) {
+                for (int r = 1; r < P; ++r) {
+                    const size_t rows = band_rows[r + 1] - band_rows[r];
+                    if (!rows) continue;
+                    NCCL_TRY(nccl().Recv(g->full_rgb.as<float>() + row_px * band_rows[r] * 3, row_px * rows * 3, ncclFloat32, r,
+                                      g->comm, s));
+                    NCCL_TRY(nccl().Recv(g->full_T.as<float>() + row_px * band_rows[r], row_px * rows, ncclFloat32, r,
+                                      g->comm, s));
+                }
+            } else if (y1 > y0) {
+                NCCL_TRY(nccl().Send(ctx->fb_rgb.ptr, row_px * (y1 - y0) * 3, ncclFloat32, 0, g->comm, s));
+                NCCL_TRY(nccl().Send(ctx->fb_T.ptr, row_px * (y1 - y0), ncclFloat32, 0, g->comm, s));
+            }
+            NCCL_TRY(nccl().GroupEnd());
+        }
+        if (g->rank == 0 && (fb_rgb || fb_T)) {
+            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, g->full_rgb.ptr, row_px * H * 12, cudaMemcpyDefault, s));
+            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, g->full_T.ptr, row_px * H * 4, cudaMemcpyDefault, s));
+            if (is_host_pointer(fb_rgb) || is_host_pointer(fb_T)) CUDA_TRY(cudaStreamSynchronize(s));
+        }
+    });
+}
+
+int gscg_group_framebuffer_device(gscg_group* g, float** rgb, float** T) {
+    if (!g || g->rank != 0) return GSCG_ERR_INVALID_ARGUMENT;
+    if (rgb) *rgb = g->full_rgb.as<float>();
+    if (T) *T = g->full_T.as<float>();
+    return GSCG_OK;
+}
+
+int gscg_group_row_costs(gscg_group* g, uint32_t tiles_y, uint64_t* out) {
+    if (!g || !out) return GSCG_ERR_INVALID_ARGUMENT;
+    gscg_ctx* ctx = g->ctx;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const FrameGeom& geo = ctx->geom;
+        CUDA_TRY(g->row_costs.ensure(static_cast<size_t>(tiles_y) * 8));
+        CUDA_TRY(g->all_costs.ensure(static_cast<size_t>(tiles_y) * 8 * g->nranks));
+        CUDA_TRY(cudaMemsetAsync(g->row_costs.ptr, 0, static_cast<size_t>(tiles_y) * 8, s));
+        // This rank's last band: its tile rows [band_tile_row0, + band_tile_rows).
+        const uint32_t rows = static_cast<uint32_t>(geo.band_tile_rows);
+        if (ctx->tiles && rows && static_cast<uint32_t>(geo.band_tile_row0) + rows <= tiles_y) {
+            k_row_costs<<<(rows + 7) / 8, 256, 0, s>>>(ctx->ranges.as<uint2>(), rows, geo.tiles_x * geo.cells_per_tile,
+                                                      g->row_costs.as<unsigned long long>() + geo.band_tile_row0);
+            CUDA_TRY(cudaGetLastError());
+        }
+        // Every rank's rows (disjoint bands) summed: all-reduce of the tiles_y vector.
+        if (g->nranks > 1)
+            NCCL_TRY(nccl().AllReduce(g->row_costs.ptr, g->all_costs.ptr, tiles_y, ncclUint64, ncclSum, g->comm, s));
+        else
+            CUDA_TRY(cudaMemcpyAsync(g->all_costs.ptr, g->row_costs.ptr, static_cast<size_t>(tiles_y) * 8,
+                                     cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(out, g->all_costs.ptr, static_cast<size_t>(tiles_y) * 8, cudaMemcpyDefault, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
     });
 }
 

@@ -56,6 +56,7 @@ struct CameraDev {
     float pos[3];
     float focal, cx, cy, near_m;
     int32_t width, height;
+    int32_t band_y0, band_y1;  // screen rows [band_y0, band_y1) this context renders (whole frame: 0, height)
 };
 
 // Frame-level counters written by the kernels and read back once per frame.

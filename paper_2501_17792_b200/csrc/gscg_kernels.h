@@ -253,6 +253,7 @@ struct BandUnpackParams {
 __global__ void k_band_count(BandParams p);
 __global__ void k_band_pack(BandParams p);
 __global__ void k_band_unpack(BandUnpackParams p);
+__global__ void k_row_costs(const uint2* ranges, uint32_t tile_rows, uint32_t cells_per_row, unsigned long long* out);
 
 // metrics
 constexpr int kSseThreads = 256;

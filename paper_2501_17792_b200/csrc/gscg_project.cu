@@ -91,6 +91,7 @@ k_project(ProjectParams p) {
     __shared__ uint32_t s_wcnt[kProjectThreads / 32];
     __shared__ unsigned long long s_base;
     __shared__ uint32_t s_item;
+    __shared__ uint32_t s_tile_pairs;  // the reference's (tile, splat) bin entries of this CTA
     __shared__ __align__(8) uint64_t s_bar;  // the work item's bulk copies (SH + skin matrices)
 
     const int tid = threadIdx.x;
@@ -104,10 +105,12 @@ k_project(ProjectParams p) {
     auto cdiv = [&](int v) { return cshift >= 0 ? v >> cshift : v / cell; };  // v >= 0
     uint32_t dmin = 0xffffffffu, dmax = 0u;
     uint32_t pairs = 0;  // binning cells of this thread's splats (summed once at the end)
-    uint32_t tile_pairs = 0;  // the reference's (tile, splat) bin entries (= pairs unless quadrant cells)
     const int lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    if (tid == 0) mbar_init(&s_bar, 1);
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        s_tile_pairs = 0u;
+    }
     uint32_t phase = 0;
 
     for (;;) {
@@ -252,7 +255,9 @@ k_project(ProjectParams p) {
                     y0 = max(0, x86_float_to_int(floorf(my - ry)));
                     x1 = min(cam.width, x86_float_to_int(floorf(mx + rx)) + 1);
                     y1 = min(cam.height, x86_float_to_int(floorf(my + ry)) + 1);
-                    if (x0 < x1 && y0 < y1) {
+                    // A band frame keeps the splats whose rect meets its rows (renderer.cpp
+                    // bins by rect, :147-161); the whole frame is the band [0, height).
+                    if (x0 < x1 && y0 < y1 && y0 < cam.band_y1 && y1 > cam.band_y0) {
                         survive = true;
                         cxx = C[0][0];
                         cxy = 0.5f * (C[0][1] + C[1][0]);
@@ -266,7 +271,8 @@ k_project(ProjectParams p) {
                         cc = cxx * inv_det;
                         // Binning cells of the rect: first cell, cells across, cells down.
                         const int cx0 = cdiv(x0), cx1 = cdiv(x1 - 1);
-                        const int cy0 = cdiv(y0), cy1 = cdiv(y1 - 1);
+                        const int cyb = cdiv(cam.band_y0);  // band's first cell row
+                        const int cy0 = cdiv(max(y0, cam.band_y0)) - cyb, cy1 = cdiv(min(y1, cam.band_y1) - 1) - cyb;
                         n_tiles = static_cast<uint32_t>((cx1 - cx0 + 1) * (cy1 - cy0 + 1));
                         span_lo = static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16);
                         span_hi = static_cast<uint32_t>(cx1 - cx0 + 1) | (static_cast<uint32_t>(cy1 - cy0 + 1) << 16);
@@ -305,7 +311,10 @@ k_project(ProjectParams p) {
             // Record slots: ballot ranks inside the warp, warp counts across the CTA, one
             // atomic per (CTA, instance) on the frame's splat counter.
             pairs += n_tiles;
-            tile_pairs += n_bins;
+            // Tile pairs (= pairs unless quadrant cells) are warp-reduced into shared memory
+            // here rather than carried in a register (the kernel sits at its 64-register cap).
+            const uint32_t wbins = __reduce_add_sync(0xffffffffu, n_bins);
+            if (lane == 0 && wbins) atomicAdd(&s_tile_pairs, wbins);
             const uint32_t bal = __ballot_sync(0xffffffffu, survive);
             if (lane == 0) s_wcnt[warp] = __popc(bal);
             __syncthreads();
@@ -379,9 +388,8 @@ k_project(ProjectParams p) {
         dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     }
     pairs = __reduce_add_sync(0xffffffffu, pairs);
-    tile_pairs = __reduce_add_sync(0xffffffffu, tile_pairs);
+    if (tid == 0 && s_tile_pairs) atomicAdd(&p.counters->tile_pairs, static_cast<unsigned long long>(s_tile_pairs));
     if ((tid & 31) == 0) {
-        if (tile_pairs) atomicAdd(&p.counters->tile_pairs, static_cast<unsigned long long>(tile_pairs));
         if (dmin != 0xffffffffu) atomicMin(&p.counters->depth_min_bits, dmin);
         if (dmax != 0u) atomicMax(&p.counters->depth_max_bits, dmax);
         if (pairs) atomicAdd(&p.counters->pairs, static_cast<unsigned long long>(pairs));

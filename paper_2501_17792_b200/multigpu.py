@@ -411,3 +411,83 @@ def render_frame_virtual(ranks: list[BandRank], time_s: float, settings=None, st
     rgb = torch.cat(bands_rgb).cpu().numpy()
     T = torch.cat(bands_T).cpu().numpy()
     return rgb, T
+
+
+# ---------------------------------------------------------------------------------------
+# the band-split frame as one C-ABI call per frame (gscg_group_*)
+
+
+def broadcast_unique_id(rank: int, world: int, dist=None, group=None) -> bytes:
+    """Rank 0's NCCL unique id (gscg_group_unique_id), shipped to every rank over the
+    caller's process group (torch.distributed, any backend: 128 bytes of plumbing)."""
+    uid = (C.c_uint8 * N.GSCG_UNIQUE_ID_BYTES)()
+    if rank == 0:
+        rc = N.gscg().gscg_group_unique_id(uid)
+        if rc != 0:
+            raise N.NativeError(rc, "gscg_group_unique_id failed")
+    data = bytes(uid)
+    if world > 1:
+        obj = [data]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        data = obj[0]
+    if len(data) != N.GSCG_UNIQUE_ID_BYTES:
+        raise ValueError("bad unique id")
+    return data
+
+
+class BandGroup:
+    """One rank of the band-split frame: rank r renders screen rows [rows[r], rows[r+1])
+    of every frame on its own GPU and the bands are gathered into rank 0's framebuffer,
+    all inside gscg_group_render_frame (NCCL point-to-point on the context stream; the
+    group owns its communicator). Band boundaries follow the previous frames' binned
+    pairs per tile row, summed over ranks (gscg_group_row_costs) whenever rebalance() is
+    called; every rank computes the same rows from the same all-reduced costs."""
+
+    def __init__(self, renderer, rank: int, world: int, dist=None, group=None, unique_id: Optional[bytes] = None):
+        self.renderer, self.rank, self.world = renderer, rank, world
+        cfg = renderer.scene.cfg
+        self.height, self.width = cfg.height, cfg.width
+        uid = unique_id if unique_id is not None else broadcast_unique_id(rank, world, dist, group)
+        buf = (C.c_uint8 * N.GSCG_UNIQUE_ID_BYTES).from_buffer_copy(uid)
+        h = C.c_void_p()
+        N.check_gscg(N.gscg().gscg_group_create(renderer.gpu, buf, world, rank, C.byref(h)), renderer.gpu)
+        self._h = h
+        self.tile = 16
+        self.rows = band_rows(self.height, self.tile, world)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.gscg().gscg_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_tile(self, tile: int) -> None:
+        self.tile = tile
+        self.rows = band_rows(self.height, tile, self.world)
+
+    def render(self, frame, cam, settings, lod, out_rgb=None, out_T=None) -> "N.GscgStageTimes":
+        """One frame (frame/cam/settings/lod: the gscg_render_frame descriptors). On rank 0,
+        out_rgb / out_T (numpy, host or None) receive the whole frame."""
+        st = N.GscgStageTimes()
+        rows = (C.c_uint32 * (self.world + 1))(*self.rows)
+        ptr = (lambda a: None if a is None else a.ctypes.data)
+        N.check_gscg(N.gscg().gscg_group_render_frame(self._h, C.byref(frame), C.byref(cam), C.byref(settings),
+                                                       C.byref(lod), rows, ptr(out_rgb), ptr(out_T), C.byref(st)),
+                     self.renderer.gpu)
+        return st
+
+    def row_costs(self) -> np.ndarray:
+        ty = (self.height + self.tile - 1) // self.tile
+        out = np.zeros(ty, dtype=np.uint64)
+        N.check_gscg(N.gscg().gscg_group_row_costs(self._h, ty, out.ctypes.data), self.renderer.gpu)
+        return out
+
+    def rebalance(self) -> list[int]:
+        """New band rows from the last frame's pairs per tile row over all ranks (plus a
+        per-row floor for the fixed per-pixel cost)."""
+        costs = self.row_costs().astype(np.float64)
+        if costs.sum() > 0:
+            self.rows = band_rows(self.height, self.tile, self.world, costs + 0.02 * costs.mean() + 1.0)
+        return self.rows
