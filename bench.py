@@ -385,11 +385,12 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
     else:
         # Public API per step: the instance records from pinned host memory, the band
         # frame, the gather, and rank 0's read-back of the frame's colour into pinned memory.
+        from paper_2501_17792_b200.api import pinned_array
         rec = r.instance_records()
-        pinned = {k: P.pinned_array(v.shape, v.dtype) for k, v in rec.items()}
+        pinned = {k: pinned_array(v.shape, v.dtype) for k, v in rec.items()}
         for k, v in rec.items():
             pinned[k][...] = v
-        band_out = P.pinned_array((cfg.height, cfg.width, 3))
+        band_out = pinned_array((cfg.height, cfg.width, 3))
 
         def e2e_frame(f):
             fd = N.GscgFrameDesc()
@@ -475,10 +476,148 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         "clocks": clk,
         "memory": memory_block(r, scene),
     }
+    if world == 1 and args.config == 5 and not args.no_ablation and not band_path:
+        out["layout_ablation"] = layout_ablation(args, local_rank)
+    if world == 1 and args.band_estimate and not band_path:
+        out["band_split_estimate"] = band_split_estimate(r, ctx, lib, frame, stream, cfg, args)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], out["cpu_baseline_1t"] = cpu_baselines(args.config, args.cpu_frames)
     if dist:
         dist.destroy_process_group()
+    return out
+
+
+def layout_ablation(args, local_rank: int) -> dict:
+    """The shared-attribute ablation of BASELINE config 5 / PAPER.md Tables 1-2 on the B200:
+    one template at a forced level of 202,738 / 12,661 / 3,176 Gaussians, duplicated over
+    1 / 100 / 400 / 1,000 / 5,000 characters (row-major cells of a 100 x 100 grid, camera
+    over the grid centre), 1280 x 720, RGB colour, with and without motion. Each cell is
+    rendered with the shared (template, level) store and with naive per-instance attribute
+    copies (gscg_set_layout); device memory is measured (cudaMemGetInfo after the frame,
+    and the attribute bytes each layout holds) and FPS is the median of CUDA-event frame
+    times with device-resident inputs. A cell whose allocation fails is reported as out of
+    memory, as the reference's run_benchmark does (bench.cpp:94-97)."""
+    import torch
+    import paper_2501_17792_b200 as P
+    from paper_2501_17792_b200 import native as N
+    from paper_2501_17792_b200.multigpu import gscg_settings
+
+    dev = torch.device("cuda", local_rank)
+    cfg = P.SceneConfig(template_count=1, template_seed_base=100, level_counts=P.api.LEVELS_PAPER, with_sh=False,
+                        motion_count=15, motion_seed_base=500, motion_frames=60, grid_rows=100, grid_cols=100,
+                        crowd_count=5000, crowd_seed=1, cam_pos=(49.5, 1.6, -3.0), cam_look=(49.5, 1.0, 5.0),
+                        width=1280, height=720)
+    scene = P.Scene(cfg)
+    all_inst = scene.instances
+    lib = N.gscg()
+    rs = gscg_settings(P.RenderSettings(sh_colour=False))
+    lp = N.GscgLodPolicy()
+    lp.threshold_count = 2
+    lp.thresholds_m[0], lp.thresholds_m[1] = 5.0, 10.0
+    counts = (1, 100, 400, 1000, 5000)
+    table = []
+    for level, gauss in enumerate(P.api.LEVELS_PAPER):
+        for layout in ("shared", "naive"):
+            for motion in (False, True):
+                row = {"gaussians": gauss, "layout": layout, "motion": motion, "cells": {}}
+                for nchar in counts:
+                    sub = all_inst[:nchar]
+                    scene.instances = sub
+                    r = P.Renderer(scene, device=local_rank, device_poses=True)
+                    try:
+                        r.set_layout(layout == "naive")
+                        r.render_frame(0.0, P.RenderSettings(sh_colour=False), static_pose=not motion,
+                                       forced_lod=level)
+                        tids = torch.from_numpy(np.ascontiguousarray(sub["template_id"]).astype(np.int32)).to(dev)
+                        _, place, _ = r.sample_crowd(0.0)
+                        d_place = torch.from_numpy(place).to(dev)
+                        d_mid = torch.from_numpy(np.ascontiguousarray(sub["motion_id"]).astype(np.int32)).to(dev)
+                        d_ph = torch.from_numpy(np.ascontiguousarray(sub["phase_offset_s"]).astype(np.float32)).to(dev)
+                        d_lod = torch.full((nchar,), -1, dtype=torch.int32, device=dev)
+                        cam = scene.camera_basis()
+                        sp = C.c_void_p()
+                        N.check_gscg(lib.gscg_stream(r.gpu, C.byref(sp)), r.gpu)
+                        stream = torch.cuda.ExternalStream(sp.value, device=dev)
+
+                        def frame(f):
+                            fd = N.GscgFrameDesc()
+                            fd.instance_count = nchar
+                            fd.joint_stride = r.joint_stride
+                            fd.template_ids = tids.data_ptr()
+                            fd.placement = d_place.data_ptr()
+                            fd.active_lod = d_lod.data_ptr()
+                            fd.forced_lod = level
+                            fd.memory = N.GSCG_MEM_DEVICE
+                            fd.pose_source = N.GSCG_POSES_SAMPLED
+                            fd.time_s = f / 30.0
+                            fd.static_pose = 0 if motion else 1
+                            fd.motion_ids = d_mid.data_ptr()
+                            fd.phase_offsets = d_ph.data_ptr()
+                            N.check_gscg(lib.gscg_render_frame(r.gpu, C.byref(fd), C.byref(cam), C.byref(rs),
+                                                               C.byref(lp), None, None, None), r.gpu)
+
+                        steps = 5 if gauss * nchar > 2e8 else 15
+                        for f in range(2):
+                            frame(f)
+                        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+                        evs[0].record(stream)
+                        for f in range(steps):
+                            frame(2 + f)
+                            evs[f + 1].record(stream)
+                        torch.cuda.synchronize()
+                        ms = float(np.median([evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]))
+                        mu = r.memory_usage()
+                        row["cells"][str(nchar)] = {
+                            "fps": round(1000.0 / ms, 2),
+                            "device_used_mib": round((mu["device_total_bytes"] - mu["device_free_bytes"]) / 2**20, 1),
+                            "attribute_mib": round((mu["template_bytes"] + mu["naive_attribute_bytes"]) / 2**20, 1),
+                            "frame_buffers_mib": round(mu["frame_bytes"] / 2**20, 1)}
+                    except (N.NativeError, MemoryError) as e:
+                        row["cells"][str(nchar)] = {"skipped": "out of memory" if getattr(e, "status", -4) == -4
+                                                    else str(e)[:80]}
+                    del r
+                    torch.cuda.synchronize()
+                table.append(row)
+    scene.instances = all_inst
+    return {"resolution": [1280, 720], "colour": "RGB", "template": "synthetic seed 100 (one template, duplicated)",
+            "note": "attribute_mib: the attribute store the layout reads (shared: one (template, level) store; naive: "
+                    "+ per-instance copies of 80 B / Gaussian); device_used_mib: cudaMemGetInfo after the cell",
+            "rows": table}
+
+
+def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
+    """One rank's work of the P-GPU band frame, measured on this GPU: each of P bands
+    (balanced by the frame's pairs per tile row, as BandGroup.rebalance does) is rendered
+    alone with gscg_set_band, K frames timed with CUDA events. The ranks of the multi-GPU
+    frame are independent until the gather of finished rows (W x H x 16 B in total), so
+    the slowest band bounds the P-GPU frame time from below. Not a multi-GPU measurement."""
+    import torch
+    from paper_2501_17792_b200 import native as N
+    from paper_2501_17792_b200.multigpu import band_rows
+
+    ranges = r.cell_ranges()
+    tiles, cpt = r.cell_layout()
+    tx = (cfg.width + 15) // 16
+    row_pairs = (ranges[:, 1] - ranges[:, 0]).astype(np.float64).reshape(-1, tx * cpt).sum(1)
+    out = {"method": "each band rendered alone on one B200 (gscg_set_band), median of K frames"}
+    for parts in (1, 2, 4, 8):
+        rows = band_rows(cfg.height, 16, parts, row_pairs + 0.02 * row_pairs.mean() + 1.0)
+        band_ms = []
+        for b in range(parts):
+            N.check_gscg(lib.gscg_set_band(ctx, rows[b], rows[b + 1]), ctx)
+            for f in range(3):
+                frame(f)
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+            evs[0].record(stream)
+            for f in range(args.steps):
+                frame(args.warmup + f)
+                evs[f + 1].record(stream)
+            torch.cuda.synchronize()
+            band_ms.append(float(np.median([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])))
+        N.check_gscg(lib.gscg_set_band(ctx, 0, 0), ctx)
+        out[str(parts)] = {"rows": rows, "band_ms": [round(x, 4) for x in band_ms], "max_ms": round(max(band_ms), 4)}
+    for parts in (2, 4, 8):
+        out[str(parts)]["speedup_vs_1"] = round(out["1"]["max_ms"] / out[str(parts)]["max_ms"], 3)
     return out
 
 
@@ -625,6 +764,9 @@ def main():
     ap.add_argument("--band-path", action="store_true",
                     help="use the multi-GPU band path (shard -> NCCL exchange -> band) even on one GPU")
     ap.add_argument("--reference-budget-s", type=float, default=150.0)
+    ap.add_argument("--no-ablation", action="store_true", help="config 5: skip the shared/naive layout grid")
+    ap.add_argument("--band-estimate", action="store_true",
+                    help="also time each band of a 2/4/8-way split alone on this GPU (one rank's work)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher/plumbing check without a GPU: gloo ranks, max-over-ranks timing, one JSON line")
     args = ap.parse_args()

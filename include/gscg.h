@@ -199,8 +199,18 @@ typedef struct {
   uint64_t frame_bytes;    /* per-frame device buffers at their high-water mark */
   uint64_t pinned_bytes;   /* page-locked staging */
   uint64_t device_free_bytes, device_total_bytes; /* cudaMemGetInfo */
+  uint64_t naive_attribute_bytes; /* per-instance attribute copies (GSCG_LAYOUT_NAIVE) */
 } gscg_memory_info;
 int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out);
+
+/* Attribute layout of the projection (the config-5 / PAPER.md Table 1-2 ablation):
+ * GSCG_LAYOUT_SHARED (default) reads every instance's Gaussians from the one shared
+ * (template, level) store; GSCG_LAYOUT_NAIVE gives every instance its own copy of its
+ * level's 80 B attributes (the reference MemoryLayoutModel's naive mode, crowd.cpp:142-210),
+ * held in HBM and read per instance; RGB colour only. Same pixels either way. */
+#define GSCG_LAYOUT_SHARED 0
+#define GSCG_LAYOUT_NAIVE 1
+int gscg_set_layout(gscg_ctx* ctx, int32_t layout);
 
 int gscg_set_debug(gscg_ctx* ctx, uint32_t flags);
 

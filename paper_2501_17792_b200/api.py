@@ -436,6 +436,13 @@ class Renderer:
                 setattr(times, f, getattr(st, f))
         return rgb, T
 
+    def set_layout(self, naive: bool) -> None:
+        """Attribute layout of the projection (gscg_set_layout): the shared (template,
+        level) store, or naive per-instance copies (the config-5 memory / FPS ablation;
+        RGB colour)."""
+        N.check_gscg(N.gscg().gscg_set_layout(self.gpu, N.GSCG_LAYOUT_NAIVE if naive else N.GSCG_LAYOUT_SHARED),
+                     self.gpu)
+
     def set_band(self, row_begin: int = 0, row_end: int = 0) -> None:
         """Render only screen rows [row_begin, row_end) (tile-aligned; gscg_set_band):
         render_frame then returns the band's rows, bit-identical to the same rows of the

@@ -205,6 +205,12 @@ struct gscg_ctx {
     int band_state = 0;
     // Stage-function modes of update_gather (gscg_skin_means / gscg_gather_posed).
     enum class Mode { Frame, SkinOnly, PosedIn } mode = Mode::Frame;
+    // Attribute layout (gscg_set_layout): the shared store, or the naive per-instance copies
+    // of the config-5 ablation, refilled when the instances' levels change.
+    int32_t layout = GSCG_LAYOUT_SHARED;
+    DevBuf naive_core, naive_w, naive_key;
+    uint64_t naive_G = 0;
+    bool naive_valid = false;
     DevBuf posed_in, project_mask, posed_out;
     BandParams band{};
     DevBuf band_scratch;
@@ -554,7 +560,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
 
     const int project_smem = (settings->sh_enabled ? kProjectThreads * kShFloats * 4 : 0) + kBatch * static_cast<int>(js) * 12 * 4;
     int project_blocks_per_sm = 1;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project<false>, kProjectThreads,
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&project_blocks_per_sm, k_project<false, false>, kProjectThreads,
                                                            project_smem));
     project_blocks_per_sm = std::max(project_blocks_per_sm, 1);
 
@@ -646,6 +652,43 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
 
+        const bool naive = ctx->layout == GSCG_LAYOUT_NAIVE && !posed_mode && !skin_only;
+        if (naive) {
+            // Per-instance copies sized by this frame's instance-Gaussians (a host read of the
+            // plan's counter); refilled only when the level assignment changes.
+            if (settings->sh_enabled) invalid("the naive layout ablation renders RGB colour (sh_enabled = 0)");
+            CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            const uint64_t G = ctx->h_counters->gaussians;
+            std::vector<uint32_t> key(n * 2ull + 1);
+            if (n) {
+                CUDA_TRY(cudaMemcpy(key.data(), ctx->inst_group.ptr, n * 4ull, cudaMemcpyDeviceToHost));
+                CUDA_TRY(cudaMemcpy(key.data() + n, ctx->inst_base.ptr, n * 4ull, cudaMemcpyDeviceToHost));
+            }
+            key[2ull * n] = n;
+            const bool same = ctx->naive_valid && G == ctx->naive_G && ctx->naive_key.cap >= key.size() * 4 &&
+                              [&] {
+                                  std::vector<uint32_t> old(key.size());
+                                  return cudaMemcpy(old.data(), ctx->naive_key.ptr, key.size() * 4, cudaMemcpyDeviceToHost) ==
+                                             cudaSuccess && old == key;
+                              }();
+            if (!same) {
+                CUDA_TRY(ctx->naive_core.ensure_exact(std::max<uint64_t>(G, 1) * 64));
+                CUDA_TRY(ctx->naive_w.ensure_exact(std::max<uint64_t>(G, 1) * 16));
+                if (n) {
+                    k_naive_fill<<<dim3(64, std::min<uint32_t>(n, 65535u)), 256, 0, s>>>(
+                        ctx->inst_group.as<uint32_t>(), ctx->inst_base.as<uint32_t>(), ctx->d_groups.as<GroupDev>(), n,
+                        ctx->naive_core.as<float4>(), ctx->naive_w.as<float4>());
+                    ++launches;
+                    CUDA_TRY(cudaGetLastError());
+                }
+                CUDA_TRY(ctx->naive_key.ensure(key.size() * 4));
+                CUDA_TRY(cudaMemcpyAsync(ctx->naive_key.ptr, key.data(), key.size() * 4, cudaMemcpyHostToDevice, s));
+                CUDA_TRY(cudaStreamSynchronize(s));
+                ctx->naive_G = G;
+                ctx->naive_valid = true;
+            }
+        }
         if ((ctx->debug & GSCG_DEBUG_POSED) || skin_only) {
             CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, counters, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
@@ -706,13 +749,18 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pj.splat_capacity = ctx->splat_capacity;
         pj.pair_capacity = ctx->pair_capacity;
         pj.posed_in = posed_mode ? ctx->posed_in.as<float>() : nullptr;
+        pj.naive_core = naive ? ctx->naive_core.as<float4>() : nullptr;
+        pj.naive_weights = naive ? ctx->naive_w.as<float4>() : nullptr;
         pj.posed_debug = (ctx->debug & GSCG_DEBUG_POSED) ? ctx->posed_dbg.as<float>() : nullptr;
         pj.record_debug = (ctx->debug & GSCG_DEBUG_RECORDS) ? ctx->rec_dbg.as<gscg_splat_record>() : nullptr;
         if (shard_end > shard_begin && ctx->group_count > 0) {
+            const dim3 grid(ctx->sm_count * project_blocks_per_sm);
             if (posed_mode)
-                k_project<true><<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
+                k_project<true, false><<<grid, kProjectThreads, project_smem, s>>>(pj);
+            else if (naive)
+                k_project<false, true><<<grid, kProjectThreads, project_smem, s>>>(pj);
             else
-                k_project<false><<<ctx->sm_count * project_blocks_per_sm, kProjectThreads, project_smem, s>>>(pj);
+                k_project<false, false><<<grid, kProjectThreads, project_smem, s>>>(pj);
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -1112,9 +1160,11 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(ctx->counters.ensure(sizeof(FrameCounters)));
         CUDA_TRY(cudaFuncSetAttribute(k_fk_skin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (kFkThreads / 16) * kFkSmemPerInstance(kMaxJoints)));
-        CUDA_TRY(cudaFuncSetAttribute(k_project<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_TRY(cudaFuncSetAttribute(k_project<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
-        CUDA_TRY(cudaFuncSetAttribute(k_project<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_TRY(cudaFuncSetAttribute(k_project<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_project<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
     });
     *out = ctx;
@@ -1175,6 +1225,20 @@ int gscg_set_band(gscg_ctx* ctx, int32_t row_begin, int32_t row_end) {
         if (row_begin < 0 || row_end < row_begin) invalid("gscg_set_band: bad row range");
         ctx->band_req0 = row_begin;
         ctx->band_req1 = row_end;
+    });
+}
+
+int gscg_set_layout(gscg_ctx* ctx, int32_t layout) {
+    if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (layout != GSCG_LAYOUT_SHARED && layout != GSCG_LAYOUT_NAIVE) invalid("gscg_set_layout: unknown layout");
+        ctx->layout = layout;
+        if (layout == GSCG_LAYOUT_SHARED) {  // the per-instance copies go away with the mode
+            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            ctx->naive_core.release();
+            ctx->naive_w.release();
+            ctx->naive_valid = false;
+        }
     });
 }
 
@@ -1586,6 +1650,7 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
                                 &ctx->long_runs};
         for (const DevBuf* b : bufs) out->frame_bytes += b->cap;
         out->pinned_bytes = ctx->pinned_cap + sizeof(FrameCounters) + GSCG_MAX_BANDS * 8;
+        out->naive_attribute_bytes = ctx->naive_core.cap + ctx->naive_w.cap;
         size_t fr = 0, tot = 0;
         CUDA_TRY(cudaMemGetInfo(&fr, &tot));
         out->device_free_bytes = fr;

@@ -78,7 +78,9 @@ struct ProjectParams {
     uint4* splat_meta;      // per record: ordinal, cx0 | cy0 << 16, across | down << 16, depth bits
     uint64_t splat_capacity;
     uint64_t pair_capacity;
-    const float* posed_in;           // k_project<true>: posed means G x 3 by ordinal (no skinning)
+    const float* posed_in;           // k_project<true, *>: posed means G x 3 by ordinal (no skinning)
+    const float4* naive_core;        // k_project<*, true>: per-instance attribute copies by ordinal
+    const float4* naive_weights;
     // debug outputs (may be null)
     float* posed_debug;              // G x 3 by ordinal
     gscg_splat_record* record_debug; // per splat
@@ -146,8 +148,12 @@ constexpr int kFkThreads = 128;  // k_fk_skin: 8 instances (half-warps) per bloc
 constexpr int kFkSmemPerInstance(int joint_stride) { return joint_stride * 52 * 4; }  // world, bind, inverse, pose
 __global__ void k_fk_skin(FkParams p);
 __global__ void k_inst_cull(CullParams p);
-template <bool kPosedIn>
-__global__ void k_project(ProjectParams p);  // <false>: LBS from skin matrices (the frame); <true>: given posed means
+// <false, false>: the frame (LBS from skin matrices, shared attribute store);
+// <true, false>: given posed means; <false, true>: the naive per-instance layout.
+template <bool kPosedIn, bool kNaive>
+__global__ void k_project(ProjectParams p);
+__global__ void k_naive_fill(const uint32_t* inst_group, const uint32_t* inst_base, const GroupDev* groups, uint32_t n,
+                             float4* core, float4* weights);
 
 // update_crowd's skin_means for every instance (gscg_skin_means): posed[ordinal] =
 // LBS of the instance's level (avatar.cpp:178-192), the arithmetic k_project uses.

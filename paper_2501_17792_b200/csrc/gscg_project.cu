@@ -80,7 +80,7 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
 
 }  // namespace
 
-template <bool kPosedIn>
+template <bool kPosedIn, bool kNaive>
 __global__ void __launch_bounds__(kProjectThreads, 4)
 k_project(ProjectParams p) {
     extern __shared__ float4 s_dyn[];
@@ -135,7 +135,7 @@ k_project(ProjectParams p) {
         const bool gvalid = gi < grp.count;
 
         float4 c0 = make_float4(0, 0, 0, 0), c1 = c0, c2 = c0, c3 = c0, wv = c0;
-        if (gvalid) {
+        if (gvalid && !kNaive) {
             c0 = grp.core[4 * gi + 0];
             c1 = grp.core[4 * gi + 1];
             c2 = grp.core[4 * gi + 2];
@@ -176,11 +176,27 @@ k_project(ProjectParams p) {
         __syncthreads();
         mbar_wait(&s_bar, phase);
         phase ^= 1u;
-        const uint32_t i01 = __float_as_uint(c3.z), i23 = __float_as_uint(c3.w);
-        const uint32_t jidx[4] = {i01 & 0xffffu, i01 >> 16, i23 & 0xffffu, i23 >> 16};
-        const float wk[4] = {wv.x, wv.y, wv.z, wv.w};
+        uint32_t i01 = __float_as_uint(c3.z), i23 = __float_as_uint(c3.w);
+        float wk[4] = {wv.x, wv.y, wv.z, wv.w};
 
         for (uint32_t k = 0; k < inst_count; ++k) {
+            if (kNaive && gvalid) {
+                // Naive layout (the config-5 ablation): every instance reads its own copy of
+                // the level's attributes, stored at its ordinals (instance base + index).
+                const size_t o = static_cast<size_t>(s_member_base[k]) + gi;
+                c0 = p.naive_core[4 * o + 0];
+                c1 = p.naive_core[4 * o + 1];
+                c2 = p.naive_core[4 * o + 2];
+                c3 = p.naive_core[4 * o + 3];
+                wv = p.naive_weights[o];
+                i01 = __float_as_uint(c3.z);
+                i23 = __float_as_uint(c3.w);
+                wk[0] = wv.x;
+                wk[1] = wv.y;
+                wk[2] = wv.z;
+                wk[3] = wv.w;
+            }
+            const uint32_t jidx[4] = {i01 & 0xffffu, i01 >> 16, i23 & 0xffffu, i23 >> 16};
             const uint32_t inst = s_member[k];
             const float* s_inst = s_mats + k * p.joint_stride * 12;
 
@@ -403,7 +419,22 @@ __global__ void k_set_power_floor(float4* core, const float* pf, uint32_t n) {
     if (i < n) core[4 * i + 3].y = pf[i];
 }
 
-template __global__ void k_project<false>(ProjectParams p);
-template __global__ void k_project<true>(ProjectParams p);
+template __global__ void k_project<false, false>(ProjectParams p);
+template __global__ void k_project<true, false>(ProjectParams p);
+template __global__ void k_project<false, true>(ProjectParams p);
+
+// Naive-layout copies (config-5 ablation): instance i's level attributes at its ordinals.
+__global__ void k_naive_fill(const uint32_t* inst_group, const uint32_t* inst_base, const GroupDev* groups, uint32_t n,
+                             float4* core, float4* weights) {
+    for (uint32_t inst = blockIdx.y; inst < n; inst += gridDim.y) {
+        const GroupDev g = groups[inst_group[inst]];
+        const size_t base = inst_base[inst];
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < g.count; i += gridDim.x * blockDim.x) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) core[4 * (base + i) + j] = g.core[4 * i + j];
+            weights[base + i] = g.weights[i];
+        }
+    }
+}
 
 }  // namespace gscg

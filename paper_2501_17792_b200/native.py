@@ -21,6 +21,8 @@ GSCG_ERR_OOM = -4
 GSCG_ERR_STATE = -5
 GSCG_UNIQUE_ID_BYTES = 128
 GSCG_LOD_GIVEN = -2
+GSCG_LAYOUT_SHARED = 0
+GSCG_LAYOUT_NAIVE = 1
 GSCG_MEM_HOST = 0
 GSCG_MEM_DEVICE = 1
 GSCG_DEBUG_POSED = 1
@@ -73,7 +75,8 @@ class GscgStageTimes(C.Structure):
 
 class GscgMemoryUsage(C.Structure):
     _fields_ = [("template_bytes", C.c_uint64), ("frame_bytes", C.c_uint64), ("pinned_bytes", C.c_uint64),
-                ("device_free_bytes", C.c_uint64), ("device_total_bytes", C.c_uint64)]
+                ("device_free_bytes", C.c_uint64), ("device_total_bytes", C.c_uint64),
+                ("naive_attribute_bytes", C.c_uint64)]
 
 
 class GscgSplatRecord(C.Structure):
@@ -140,6 +143,7 @@ GSCG_SYMBOLS = {
     "gscg_eval_sinf": (C.c_int, [_P, _P, _P, C.c_uint32]),
     "gscg_eval_expf": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "gscg_set_band": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "gscg_set_layout": (C.c_int, [_P, C.c_int32]),
     "gscg_group_unique_id": (C.c_int, [_P]),
     "gscg_group_create": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(_P)]),
     "gscg_group_destroy": (C.c_int, [_P]),

@@ -643,3 +643,24 @@ def test_group_single_rank_frame_equals_render_frame():
     rows = g.rebalance()
     assert rows[0] == 0 and rows[-1] == cfg.height
     g.close()
+
+
+@pytest.mark.parametrize("forced", [None, 0])
+def test_naive_layout_renders_the_same_frame(forced):
+    """gscg_set_layout(NAIVE): every instance reads its own copy of its level's attributes
+    (the config-5 ablation); the frame must be byte-identical to the shared store's, and
+    the copies must hold 80 B per instance-Gaussian."""
+    s, extra = config_scene(2, sh=False)
+    r = P.Renderer(s, device_poses=True)
+    st = P.RenderSettings(sh_colour=False)
+    a, Ta = r.render_frame(0.6, st, forced_lod=forced)
+    a, Ta = a.copy(), Ta.copy()
+    r.set_layout(True)
+    b, Tb = r.render_frame(0.6, st, forced_lod=forced)
+    G = r.counts()[0]
+    assert a.tobytes() == b.tobytes() and Ta.tobytes() == Tb.tobytes()
+    assert r.memory_usage()["naive_attribute_bytes"] == 80 * G
+    c, _ = r.render_frame(0.7, st, forced_lod=forced)  # second frame reuses the copies
+    r.set_layout(False)
+    d, _ = r.render_frame(0.7, st, forced_lod=forced)
+    assert c.tobytes() == d.tobytes() and r.memory_usage()["naive_attribute_bytes"] == 0
