@@ -228,6 +228,10 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
+    # Config 5's shared / naive grid first, while the device is empty (the headline frame's
+    # buffers grow to ~90 GB).
+    ablation = (layout_ablation(args, local_rank)
+                if world == 1 and args.config == 5 and not args.no_ablation and not band_path else None)
     P, cfg, extra, scene = build_scene(args.config)
     from paper_2501_17792_b200 import native as N
 
@@ -294,7 +298,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         # the frame (its own instance cull + projection + sort + raster), and the bands are
         # gathered into rank 0's framebuffer in HBM, one gscg_group_render_frame per frame.
         from paper_2501_17792_b200.multigpu import BandGroup
-        group = BandGroup(r, rank, world, dist)
+        group = BandGroup(r, rank, world, dist, axis=args.split_axis)
         group.set_tile(settings.tile_size)
 
         def frame(f: int) -> dict:
@@ -450,7 +454,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": bench_config(args.config, cfg, cfg_counts, cfg_tile_pairs,
-                               f"{world} screen bands (one per GPU), NCCL gather to rank 0" if band_path else "single GPU"),
+                               f"{world} screen regions ({args.split_axis}, one per GPU), NCCL gather to rank 0" if band_path else "single GPU"),
         "median_frame_ms": round(median_ms, 4), "fps_median": round(1000.0 / median_ms, 3),
         "colour": "SH degree 3 (BASELINE; the reference renders fixed RGB)",
         "instances_culled": culled,
@@ -476,8 +480,8 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         "clocks": clk,
         "memory": memory_block(r, scene),
     }
-    if world == 1 and args.config == 5 and not args.no_ablation and not band_path:
-        out["layout_ablation"] = layout_ablation(args, local_rank)
+    if ablation is not None:
+        out["layout_ablation"] = ablation
     if world == 1 and args.band_estimate and not band_path:
         out["band_split_estimate"] = band_split_estimate(r, ctx, lib, frame, stream, cfg, args)
     if world == 1 and not args.no_cpu_baseline:
@@ -523,8 +527,9 @@ def layout_ablation(args, local_rank: int) -> dict:
                 for nchar in counts:
                     sub = all_inst[:nchar]
                     scene.instances = sub
-                    r = P.Renderer(scene, device=local_rank, device_poses=True)
+                    r = frame = None
                     try:
+                        r = P.Renderer(scene, device=local_rank, device_poses=True)
                         r.set_layout(layout == "naive")
                         r.render_frame(0.0, P.RenderSettings(sh_colour=False), static_pose=not motion,
                                        forced_lod=level)
@@ -575,7 +580,10 @@ def layout_ablation(args, local_rank: int) -> dict:
                     except (N.NativeError, MemoryError) as e:
                         row["cells"][str(nchar)] = {"skipped": "out of memory" if getattr(e, "status", -4) == -4
                                                     else str(e)[:80]}
+                    frame = None
                     del r
+                    import gc
+                    gc.collect()
                     torch.cuda.synchronize()
                 table.append(row)
     scene.instances = all_inst
@@ -586,11 +594,12 @@ def layout_ablation(args, local_rank: int) -> dict:
 
 
 def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
-    """One rank's work of the P-GPU band frame, measured on this GPU: each of P bands
-    (balanced by the frame's pairs per tile row, as BandGroup.rebalance does) is rendered
-    alone with gscg_set_band, K frames timed with CUDA events. The ranks of the multi-GPU
-    frame are independent until the gather of finished rows (W x H x 16 B in total), so
-    the slowest band bounds the P-GPU frame time from below. Not a multi-GPU measurement."""
+    """One rank's work of the P-GPU region-split frame, measured on this GPU: each of P
+    regions (columns, the BandGroup default, and rows for comparison; cuts balanced by the
+    frame's pairs per tile line as BandGroup.rebalance does) is rendered alone with
+    gscg_set_region, K frames timed with CUDA events. The ranks of the multi-GPU frame are
+    independent until the gather of finished pixels (W x H x 16 B in total), so the slowest
+    region bounds the P-GPU frame time from below. Not a multi-GPU measurement."""
     import torch
     from paper_2501_17792_b200 import native as N
     from paper_2501_17792_b200.multigpu import band_rows
@@ -598,26 +607,36 @@ def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
     ranges = r.cell_ranges()
     tiles, cpt = r.cell_layout()
     tx = (cfg.width + 15) // 16
-    row_pairs = (ranges[:, 1] - ranges[:, 0]).astype(np.float64).reshape(-1, tx * cpt).sum(1)
-    out = {"method": "each band rendered alone on one B200 (gscg_set_band), median of K frames"}
-    for parts in (1, 2, 4, 8):
-        rows = band_rows(cfg.height, 16, parts, row_pairs + 0.02 * row_pairs.mean() + 1.0)
-        band_ms = []
-        for b in range(parts):
-            N.check_gscg(lib.gscg_set_band(ctx, rows[b], rows[b + 1]), ctx)
-            for f in range(3):
-                frame(f)
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-            evs[0].record(stream)
-            for f in range(args.steps):
-                frame(args.warmup + f)
-                evs[f + 1].record(stream)
-            torch.cuda.synchronize()
-            band_ms.append(float(np.median([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])))
-        N.check_gscg(lib.gscg_set_band(ctx, 0, 0), ctx)
-        out[str(parts)] = {"rows": rows, "band_ms": [round(x, 4) for x in band_ms], "max_ms": round(max(band_ms), 4)}
-    for parts in (2, 4, 8):
-        out[str(parts)]["speedup_vs_1"] = round(out["1"]["max_ms"] / out[str(parts)]["max_ms"], 3)
+    tile_pairs = (ranges[:, 1] - ranges[:, 0]).astype(np.float64).reshape(-1, cpt).sum(1).reshape(-1, tx)
+    out = {"method": "each region rendered alone on one B200 (gscg_set_region), median of K frames"}
+    for axis in ("cols", "rows"):
+        line = tile_pairs.sum(0) if axis == "cols" else tile_pairs.sum(1)
+        extent = cfg.width if axis == "cols" else cfg.height
+        res = {}
+        for parts in (1, 2, 4, 8):
+            cuts = band_rows(extent, 16, parts, line + 0.02 * line.mean() + 1.0)
+            region_ms = []
+            for b in range(parts):
+                if cuts[b + 1] <= cuts[b]:
+                    region_ms.append(0.0)
+                    continue
+                x0, y0, x1, y1 = (cuts[b], 0, cuts[b + 1], 0) if axis == "cols" else (0, cuts[b], 0, cuts[b + 1])
+                N.check_gscg(lib.gscg_set_region(ctx, x0, y0, x1, y1), ctx)
+                for f in range(3):
+                    frame(f)
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+                evs[0].record(stream)
+                for f in range(args.steps):
+                    frame(args.warmup + f)
+                    evs[f + 1].record(stream)
+                torch.cuda.synchronize()
+                region_ms.append(float(np.median([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])))
+            N.check_gscg(lib.gscg_set_region(ctx, 0, 0, 0, 0), ctx)
+            res[str(parts)] = {"cuts": cuts, "region_ms": [round(x, 4) for x in region_ms],
+                               "max_ms": round(max(region_ms), 4)}
+        for parts in (2, 4, 8):
+            res[str(parts)]["speedup_vs_1"] = round(res["1"]["max_ms"] / res[str(parts)]["max_ms"], 3)
+        out[axis] = res
     return out
 
 
@@ -708,7 +727,7 @@ def run_reference(args, rank, world) -> dict | None:
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": bench_config(args.config, cfg, (times0.gaussian_count, times0.splat_count, 0), tile_pairs,
                                    "single GPU" if world == 1 else
-                                   f"{world} screen bands (one per GPU), NCCL gather to rank 0"),
+                                   f"{world} screen regions ({args.split_axis}, one per GPU), NCCL gather to rank 0"),
             "median_frame_ms": round(med, 3), "fps_median": round(1000.0 / med, 4),
             "colour": ("RGB: the reference has no SH (SURVEY.md 0.4); same geometry, splats and tile pairs"
                        if kind == "reference" else "SH degree 3 (oracle port)"),
@@ -765,6 +784,8 @@ def main():
                     help="use the multi-GPU band path (shard -> NCCL exchange -> band) even on one GPU")
     ap.add_argument("--reference-budget-s", type=float, default=150.0)
     ap.add_argument("--no-ablation", action="store_true", help="config 5: skip the shared/naive layout grid")
+    ap.add_argument("--split-axis", default="cols", choices=["cols", "rows"],
+                    help="multi-GPU frame: screen columns (default) or rows per GPU")
     ap.add_argument("--band-estimate", action="store_true",
                     help="also time each band of a 2/4/8-way split alone on this GPU (one rank's work)")
     ap.add_argument("--dry-run", action="store_true",

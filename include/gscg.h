@@ -223,6 +223,10 @@ int gscg_set_debug(gscg_ctx* ctx, uint32_t flags);
  * ordinals and LoD are computed over the whole crowd. row_end <= row_begin (0, 0): the
  * whole frame. Persistent per context. */
 int gscg_set_band(gscg_ctx* ctx, int32_t row_begin, int32_t row_end);
+/* The general form: the region [x0, x1) x [y0, y1) (tile-aligned, or ending at the
+ * frame's width / height); fb_rgb / fb_T receive (y1 - y0) rows of (x1 - x0) pixels. An
+ * empty column range (x1 <= x0) means every column, an empty row range every row. */
+int gscg_set_region(gscg_ctx* ctx, int32_t x0, int32_t y0, int32_t x1, int32_t y1);
 
 /* Renders one frame. fb_rgb (W*H*3) and fb_T (W*H) receive the framebuffer and the
  * final transmittance; with memory == GSCG_MEM_HOST they are host pointers (copied back
@@ -368,24 +372,28 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
  * One process per GPU. Rank 0 makes a unique id (gscg_group_unique_id), the caller's
  * plumbing (e.g. torch.distributed) broadcasts the 128 bytes, every rank calls
  * gscg_group_create on its own context (ncclCommInitRank: the group owns the NCCL
- * communicator). gscg_group_render_frame renders rank r's band rows [band_rows[r],
- * band_rows[r+1]) of the frame (band_rows: nranks + 1 ascending tile-aligned rows from 0 to
- * the height; see gscg_set_band) and gathers every band into rank 0's framebuffer with
- * grouped ncclSend/ncclRecv on the context stream; on rank 0 fb_rgb / fb_T (host or
- * device, may be NULL) receive the whole frame, identical to gscg_render_frame's. The call
- * does not synchronise the host unless rank 0 is given host destinations.
- * gscg_group_row_costs: the pairs per tile row of the last frame over all ranks (an
- * all-reduce), for re-balancing band_rows. */
+ * communicator). gscg_group_render_frame renders rank r's screen region of the frame:
+ * columns [cuts[r], cuts[r+1]) x every row (axis GSCG_SPLIT_COLS) or rows [cuts[r],
+ * cuts[r+1]) x every column (GSCG_SPLIT_ROWS); cuts: nranks + 1 ascending tile-aligned
+ * positions from 0 to the width / height (see gscg_set_region). Every region is then
+ * gathered into rank 0's framebuffer with grouped ncclSend/ncclRecv on the context stream;
+ * on rank 0 fb_rgb / fb_T (host or device, may be NULL) receive the whole frame, identical
+ * to gscg_render_frame's. The call does not synchronise the host unless rank 0 is given
+ * host destinations. gscg_group_tile_costs: the binned pairs of every tile of the last
+ * frame (tiles_y x tiles_x, row-major) over all ranks (an all-reduce), for re-balancing
+ * the cuts. */
+#define GSCG_SPLIT_ROWS 0
+#define GSCG_SPLIT_COLS 1
 #define GSCG_UNIQUE_ID_BYTES 128
 typedef struct gscg_group gscg_group;
 int gscg_group_unique_id(uint8_t* out /* GSCG_UNIQUE_ID_BYTES */);
 int gscg_group_create(gscg_ctx* ctx, const uint8_t* unique_id, int32_t nranks, int32_t rank, gscg_group** out);
 int gscg_group_destroy(gscg_group* group);
 int gscg_group_render_frame(gscg_group* group, const gscg_frame_desc* frame, const gscg_camera* cam,
-                            const gscg_render_settings* settings, const gscg_lod_policy* lod, const uint32_t* band_rows,
-                            float* fb_rgb, float* fb_T, gscg_stage_times* times);
+                            const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
+                            const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times);
 int gscg_group_framebuffer_device(gscg_group* group, float** rgb, float** T); /* rank 0 */
-int gscg_group_row_costs(gscg_group* group, uint32_t tiles_y, uint64_t* out /* tiles_y */);
+int gscg_group_tile_costs(gscg_group* group, uint32_t tiles_x, uint32_t tiles_y, uint64_t* out /* tiles_y x tiles_x */);
 
 #ifdef __cplusplus
 }

@@ -409,9 +409,13 @@ class Renderer:
         arrays from alloc_frame) and the Renderer keeps it alive until it has landed."""
         settings = settings or RenderSettings()
         W, H = self.scene.cfg.width, self.scene.cfg.height
-        band = getattr(self, "_band", None)
-        if band is not None:
-            H = min(band[1], H) - band[0]
+        region = getattr(self, "_region", None)
+        if region is not None:
+            x0, y0, x1, y1 = region
+            if y1 > y0:
+                H = min(y1, H) - y0
+            if x1 > x0:
+                W = min(x1, W) - x0
         if pipelined and out is None:
             raise ValueError("render_frame(pipelined=True) needs `out` arrays: the read-back completes after the call")
         if out is None:
@@ -447,8 +451,14 @@ class Renderer:
         """Render only screen rows [row_begin, row_end) (tile-aligned; gscg_set_band):
         render_frame then returns the band's rows, bit-identical to the same rows of the
         whole frame. (0, 0) = the whole frame."""
-        N.check_gscg(N.gscg().gscg_set_band(self.gpu, row_begin, row_end), self.gpu)
-        self._band = (row_begin, row_end) if row_end > row_begin else None
+        self.set_region(0, row_begin, 0, row_end)
+
+    def set_region(self, x0: int, y0: int, x1: int, y1: int) -> None:
+        """Render only the region [x0, x1) x [y0, y1) (tile-aligned; gscg_set_region; an
+        empty range = the whole axis): render_frame returns those pixels, bit-identical to
+        the same pixels of the whole frame."""
+        N.check_gscg(N.gscg().gscg_set_region(self.gpu, x0, y0, x1, y1), self.gpu)
+        self._region = (x0, y0, x1, y1) if (x1 > x0 or y1 > y0) else None
 
     def wait_readback(self, frames_back: int = 0) -> None:
         """Blocks until the read-back of the pipelined frame submitted `frames_back`

@@ -127,8 +127,9 @@ struct Status : std::runtime_error {
 struct FrameGeom {
     int W = 0, H = 0, ts = 16, tiles_x = 0, tiles_y = 0, cell = 8;
     uint32_t cells_per_tile = 1;
-    int band_y0 = 0, band_y1 = 0;  // rows rendered: the frame, or the band of gscg_set_band
-    int band_tile_row0 = 0, band_tile_rows = 0;
+    // The region rendered: the frame, or gscg_set_region's rectangle (tile-aligned).
+    int band_x0 = 0, band_y0 = 0, band_x1 = 0, band_y1 = 0;
+    int band_tile_col0 = 0, band_tiles_x = 0, band_tile_row0 = 0, band_tile_rows = 0;
 };
 
 struct gscg_ctx {
@@ -137,7 +138,9 @@ struct gscg_ctx {
     cudaStream_t stream = nullptr;
     std::string error;
     uint32_t debug = 0;
-    int32_t band_req0 = 0, band_req1 = 0;  // gscg_set_band rows (0, 0: the whole frame)
+    // gscg_set_region request: rows [band_req0, band_req1) (empty: every row) x columns
+    // [col_req0, col_req1) (col_req1 <= 0: every column).
+    int32_t band_req0 = 0, band_req1 = 0, col_req0 = 0, col_req1 = 0;
 
     std::vector<TemplateStore> templates;
     std::vector<MotionStore> motions;
@@ -381,6 +384,15 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 namespace {
 
+void full_region(FrameGeom& g) {
+    g.band_x0 = g.band_y0 = 0;
+    g.band_x1 = g.W;
+    g.band_y1 = g.H;
+    g.band_tile_col0 = g.band_tile_row0 = 0;
+    g.band_tiles_x = g.tiles_x;
+    g.band_tile_rows = g.tiles_y;
+}
+
 void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
                     const gscg_render_settings* settings, const gscg_lod_policy* lod) {
     if (!frame || !cam || !settings || !lod) invalid("null argument");
@@ -425,10 +437,7 @@ void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_came
     g.tiles_y = (g.H + g.ts - 1) / g.ts;
     g.cells_per_tile = g.ts == 16 ? 4u : 1u;  // 8x8 quadrant binning for tile 16
     g.cell = g.ts == 16 ? 8 : g.ts;
-    g.band_y0 = 0;  // the whole frame; gscg_render_frame applies gscg_set_band's rows (apply_band)
-    g.band_y1 = g.H;
-    g.band_tile_row0 = 0;
-    g.band_tile_rows = g.tiles_y;
+    full_region(g);  // the whole frame; gscg_render_frame applies gscg_set_region's (apply_band)
     ctx->settings = *settings;
 }
 
@@ -436,13 +445,27 @@ void validate_frame(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_came
 // rows [band_y0, band_y1) and rasterises those rows (the multi-GPU band frame).
 void apply_band(gscg_ctx* ctx) {
     FrameGeom& g = ctx->geom;
-    if (ctx->band_req1 <= ctx->band_req0) return;
-    if (ctx->band_req0 % g.ts != 0 || (ctx->band_req1 % g.ts != 0 && ctx->band_req1 != g.H) || ctx->band_req1 > g.H)
-        invalid("gscg_set_band: rows must be tile-aligned and inside the frame");
-    g.band_y0 = ctx->band_req0;
-    g.band_y1 = ctx->band_req1;
+    const bool rows = ctx->band_req1 > ctx->band_req0, cols = ctx->col_req1 > ctx->col_req0;
+    if (!rows && !cols) return;
+    auto aligned = [&](int32_t a, int32_t b, int32_t limit) {
+        return a >= 0 && a % g.ts == 0 && (b % g.ts == 0 || b == limit) && b <= limit;
+    };
+    if (rows) {
+        if (!aligned(ctx->band_req0, ctx->band_req1, g.H))
+            invalid("gscg_set_region: rows must be tile-aligned and inside the frame");
+        g.band_y0 = ctx->band_req0;
+        g.band_y1 = ctx->band_req1;
+    }
+    if (cols) {
+        if (!aligned(ctx->col_req0, ctx->col_req1, g.W))
+            invalid("gscg_set_region: columns must be tile-aligned and inside the frame");
+        g.band_x0 = ctx->col_req0;
+        g.band_x1 = ctx->col_req1;
+    }
     g.band_tile_row0 = g.band_y0 / g.ts;
     g.band_tile_rows = (g.band_y1 - g.band_y0 + g.ts - 1) / g.ts;
+    g.band_tile_col0 = g.band_x0 / g.ts;
+    g.band_tiles_x = (g.band_x1 - g.band_x0 + g.ts - 1) / g.ts;
 }
 
 // H2D of the frame records, update (LoD plan + FK) and gather (projection) for the
@@ -573,7 +596,9 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
     camdev.near_m = cam->near_m;
     camdev.width = geo.W;
     camdev.height = geo.H;
+    camdev.band_x0 = geo.band_x0;
     camdev.band_y0 = geo.band_y0;
+    camdev.band_x1 = geo.band_x1;
     camdev.band_y1 = geo.band_y1;
     auto* counters = ctx->counters.as<FrameCounters>();
     for (int attempt = 0;; ++attempt) {
@@ -923,7 +948,9 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                      float* read_T = nullptr, bool presorted = false, bool pipelined = false) {
     cudaStream_t s = ctx->stream;
     const FrameGeom& geo = ctx->geom;
-    const uint32_t tiles = static_cast<uint32_t>(geo.tiles_x) * static_cast<uint32_t>(tile_rows);
+    // The region's tile columns (the whole frame's unless gscg_set_region narrowed them).
+    const int rtx = geo.band_tiles_x;
+    const uint32_t tiles = static_cast<uint32_t>(rtx) * static_cast<uint32_t>(tile_rows);
     const uint32_t cells = tiles * geo.cells_per_tile;
     flush_readback(ctx);
     if (pipelined) {
@@ -972,7 +999,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                                                                     S32, ctx->span_sorted.as<uint2>());
         ++launches;
         launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
-                    ctx->block_sums.as<uint32_t>(), nullptr, geo.tiles_x, quads, dmask, drop, cell_bits, nullptr, nullptr);
+                    ctx->block_sums.as<uint32_t>(), nullptr, rtx, quads, dmask, drop, cell_bits, nullptr, nullptr);
         SortPassParams bp{};
         bp.counts = ctx->block_sums.as<uint32_t>();
         bp.digit_base = ctx->hist.as<uint32_t>();
@@ -980,7 +1007,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         bp.bits = emit_bits;
         k_sort_rows<<<dmask + 1, 1024, 0, s>>>(bp);
         launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
-                    ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), geo.tiles_x, quads, dmask, drop, cell_bits,
+                    ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), rtx, quads, dmask, drop, cell_bits,
                     ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
         launches += 3;
         CUDA_TRY(cudaGetLastError());
@@ -1024,7 +1051,10 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         rp.width = geo.W;
         rp.height = geo.H;
         rp.tile_size = geo.ts;
-        rp.tiles_x = geo.tiles_x;
+        rp.tiles_x = rtx;
+        rp.tile_col0 = geo.band_tile_col0;
+        rp.out_col0 = geo.band_x0;
+        rp.out_stride = geo.band_x1 - geo.band_x0;
         rp.tile_row0 = tile_row0;
         rp.out_row0 = tile_row0 * geo.ts;
         for (int i = 0; i < 3; ++i) rp.bg[i] = ctx->settings.background[i];
@@ -1041,14 +1071,14 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             // band renders. Pipelined frames overlap the read-back with the next frame
             // instead, so their raster stays one launch (no per-band tail).
             const int bands = pipelined ? 1 : std::min(kReadbackBands, tile_rows);
-            const size_t row_floats = static_cast<size_t>(geo.W);
+            const size_t row_floats = static_cast<size_t>(geo.band_x1 - geo.band_x0);
             for (int b = 0; b < bands; ++b) {
                 const int r0 = tile_rows * b / bands, r1 = tile_rows * (b + 1) / bands;
                 if (r1 <= r0) continue;
                 RasterParams bp = rp;
-                bp.ranges = rp.ranges + static_cast<size_t>(r0) * geo.tiles_x * geo.cells_per_tile;
+                bp.ranges = rp.ranges + static_cast<size_t>(r0) * rtx * geo.cells_per_tile;
                 bp.tile_row0 = tile_row0 + r0;
-                launch_raster(bp, static_cast<uint32_t>((r1 - r0) * geo.tiles_x), s);
+                launch_raster(bp, static_cast<uint32_t>((r1 - r0) * rtx), s);
                 ++launches;
                 const int y0 = r0 * geo.ts, y1 = std::min(r1 * geo.ts, geo.H - tile_row0 * geo.ts);
                 const size_t off = static_cast<size_t>(y0) * row_floats, n = static_cast<size_t>(y1 - y0) * row_floats;
@@ -1094,7 +1124,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
 // D2H (host mode) or D2D of `rows` framebuffer rows starting at the context's row 0.
 void copy_out(gscg_ctx* ctx, int rows, float* fb_rgb, float* fb_T, bool host) {
     cudaStream_t s = ctx->stream;
-    const size_t px = static_cast<size_t>(ctx->geom.W) * rows;
+    const size_t px = static_cast<size_t>(ctx->geom.band_x1 - ctx->geom.band_x0) * rows;  // region width
     // Destinations may be host (pinned or pageable) or device memory in either mode: the
     // direction comes from unified addressing.
     (void)host;
@@ -1219,13 +1249,19 @@ int gscg_destroy(gscg_ctx* ctx) {
 
 const char* gscg_last_error(const gscg_ctx* ctx) { return ctx ? ctx->error.c_str() : "null context"; }
 
-int gscg_set_band(gscg_ctx* ctx, int32_t row_begin, int32_t row_end) {
+int gscg_set_region(gscg_ctx* ctx, int32_t x0, int32_t y0, int32_t x1, int32_t y1) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
-        if (row_begin < 0 || row_end < row_begin) invalid("gscg_set_band: bad row range");
-        ctx->band_req0 = row_begin;
-        ctx->band_req1 = row_end;
+        if (x0 < 0 || y0 < 0 || x1 < x0 || y1 < y0) invalid("gscg_set_region: bad rectangle");
+        ctx->col_req0 = x0;
+        ctx->col_req1 = x1;
+        ctx->band_req0 = y0;
+        ctx->band_req1 = y1;
     });
+}
+
+int gscg_set_band(gscg_ctx* ctx, int32_t row_begin, int32_t row_end) {
+    return gscg_set_region(ctx, 0, row_begin, 0, row_end);
 }
 
 int gscg_set_layout(gscg_ctx* ctx, int32_t layout) {
@@ -1430,7 +1466,7 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         const uint32_t passes = overlap ? sort_raster(ctx, g.band_tile_row0, g.band_tile_rows, launches, fb_rgb, fb_T,
                                                       false, pipelined)
                                         : sort_raster(ctx, g.band_tile_row0, g.band_tile_rows, launches);
-        if (!overlap) copy_out(ctx, g.band_y1 - g.band_y0, fb_rgb, fb_T, host);
+        if (!overlap) copy_out(ctx, g.band_y1 - g.band_y0, fb_rgb, fb_T, host);  // region rows x region width
         if (n && !host)
             CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice,
                                      ctx->stream));
@@ -2014,6 +2050,7 @@ int gscg_rasterize_splats(gscg_ctx* ctx, const gscg_frame_splat* splats, uint64_
         g.tiles_y = (g.H + g.ts - 1) / g.ts;
         g.cells_per_tile = g.ts == 16 ? 4u : 1u;
         g.cell = g.ts == 16 ? 8 : g.ts;
+        full_region(g);
         ctx->settings = *settings;
         ctx->band_state = 0;
         const uint32_t n32 = static_cast<uint32_t>(n);
@@ -2196,7 +2233,7 @@ struct gscg_group {
     gscg_ctx* ctx = nullptr;
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
-    DevBuf full_rgb, full_T, row_costs, all_costs;
+    DevBuf full_rgb, full_T, stage_rgb, stage_T, row_costs, all_costs;
 };
 
 namespace {
@@ -2286,6 +2323,8 @@ int gscg_group_destroy(gscg_group* g) {
     if (g->comm) nccl().CommDestroy(g->comm);
     g->full_rgb.release();
     g->full_T.release();
+    g->stage_rgb.release();
+    g->stage_T.release();
     g->row_costs.release();
     g->all_costs.release();
     delete g;
@@ -2293,58 +2332,97 @@ int gscg_group_destroy(gscg_group* g) {
 }
 
 int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const gscg_camera* cam,
-                            const gscg_render_settings* settings, const gscg_lod_policy* lod, const uint32_t* band_rows,
-                            float* fb_rgb, float* fb_T, gscg_stage_times* times) {
-    if (!g || !band_rows || !cam) return GSCG_ERR_INVALID_ARGUMENT;
+                            const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
+                            const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+    if (!g || !cuts || !cam || (axis != GSCG_SPLIT_ROWS && axis != GSCG_SPLIT_COLS)) return GSCG_ERR_INVALID_ARGUMENT;
     gscg_ctx* ctx = g->ctx;
     return guarded(ctx, [&] {
         CUDA_TRY(cudaSetDevice(ctx->device));
         const int W = cam->width, H = cam->height, P = g->nranks;
-        if (band_rows[0] != 0 || band_rows[P] != static_cast<uint32_t>(H)) invalid("band_rows must cover [0, height)");
+        const bool by_cols = axis == GSCG_SPLIT_COLS;
+        const uint32_t extent = static_cast<uint32_t>(by_cols ? W : H);
+        if (cuts[0] != 0 || cuts[P] != extent) invalid("cuts must cover the frame along the split axis");
         for (int r = 0; r < P; ++r)
-            if (band_rows[r + 1] < band_rows[r]) invalid("band_rows must be ascending");
-        const uint32_t y0 = band_rows[g->rank], y1 = band_rows[g->rank + 1];
-        // This rank's band, rendered into the context's framebuffer (rows from 0).
-        const int32_t save0 = ctx->band_req0, save1 = ctx->band_req1;
-        ctx->band_req0 = static_cast<int32_t>(y0);
-        ctx->band_req1 = static_cast<int32_t>(y1);
+            if (cuts[r + 1] < cuts[r]) invalid("cuts must be ascending");
+        const uint32_t a0 = cuts[g->rank], a1 = cuts[g->rank + 1];
+        // This rank's region, rendered into the context's framebuffer (region-major, from 0).
+        const int32_t s0 = ctx->band_req0, s1 = ctx->band_req1, s2 = ctx->col_req0, s3 = ctx->col_req1;
+        if (by_cols) {
+            ctx->band_req0 = ctx->band_req1 = 0;
+            ctx->col_req0 = static_cast<int32_t>(a0);
+            ctx->col_req1 = static_cast<int32_t>(a1);
+        } else {
+            ctx->band_req0 = static_cast<int32_t>(a0);
+            ctx->band_req1 = static_cast<int32_t>(a1);
+            ctx->col_req0 = ctx->col_req1 = 0;
+        }
         gscg_frame_desc fd = *frame;
         int rc = GSCG_OK;
-        if (y1 > y0) rc = render_frame_impl(ctx, &fd, cam, settings, lod, nullptr, nullptr, times, false);
-        ctx->band_req0 = save0;
-        ctx->band_req1 = save1;
+        if (a1 > a0) rc = render_frame_impl(ctx, &fd, cam, settings, lod, nullptr, nullptr, times, false);
+        ctx->band_req0 = s0;
+        ctx->band_req1 = s1;
+        ctx->col_req0 = s2;
+        ctx->col_req1 = s3;
         if (rc != GSCG_OK) throw Status(rc, ctx->error);
         cudaStream_t s = ctx->stream;
-        const size_t row_px = static_cast<size_t>(W);
-        // Gather the bands on rank 0 (grouped point-to-point; the frame is assembled in HBM).
+        // Region r holds (rows x width) pixels: full-width bands, or full-height columns.
+        auto region_px = [&](int r) -> size_t {
+            const size_t len = cuts[r + 1] - cuts[r];
+            return by_cols ? len * static_cast<size_t>(H) : len * static_cast<size_t>(W);
+        };
         if (g->rank == 0) {
-            CUDA_TRY(g->full_rgb.ensure(row_px * H * 12));
-            CUDA_TRY(g->full_T.ensure(row_px * H * 4));
-            if (y1 > y0) {
-                CUDA_TRY(cudaMemcpyAsync(g->full_rgb.ptr, ctx->fb_rgb.ptr, row_px * (y1 - y0) * 12, cudaMemcpyDeviceToDevice, s));
-                CUDA_TRY(cudaMemcpyAsync(g->full_T.ptr, ctx->fb_T.ptr, row_px * (y1 - y0) * 4, cudaMemcpyDeviceToDevice, s));
+            CUDA_TRY(g->full_rgb.ensure(static_cast<size_t>(W) * H * 12));
+            CUDA_TRY(g->full_T.ensure(static_cast<size_t>(W) * H * 4));
+            if (by_cols) {
+                CUDA_TRY(g->stage_rgb.ensure(static_cast<size_t>(W) * H * 12));
+                CUDA_TRY(g->stage_T.ensure(static_cast<size_t>(W) * H * 4));
             }
+        }
+        // Rank 0's own region, then every other rank's, gathered with grouped send/recv.
+        // Row bands land in place; column regions land packed in a staging buffer and are
+        // placed with one strided copy each.
+        size_t off = 0;  // pixels before region r in the packed layout
+        std::vector<size_t> offs(P + 1, 0);
+        for (int r = 0; r < P; ++r) {
+            offs[r] = off;
+            off += region_px(r);
+        }
+        auto dst_rgb = [&](int r) {
+            return by_cols ? g->stage_rgb.as<float>() + 3 * offs[r] : g->full_rgb.as<float>() + 3 * offs[r];
+        };
+        auto dst_T = [&](int r) { return by_cols ? g->stage_T.as<float>() + offs[r] : g->full_T.as<float>() + offs[r]; };
+        if (g->rank == 0 && a1 > a0) {
+            CUDA_TRY(cudaMemcpyAsync(dst_rgb(0), ctx->fb_rgb.ptr, region_px(0) * 12, cudaMemcpyDeviceToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(dst_T(0), ctx->fb_T.ptr, region_px(0) * 4, cudaMemcpyDeviceToDevice, s));
         }
         if (P > 1) {
             NCCL_TRY(nccl().GroupStart());
             if (g->rank == 0) {
                 for (int r = 1; r < P; ++r) {
-                    const size_t rows = band_rows[r + 1] - band_rows[r];
-                    if (!rows) continue;
-                    NCCL_TRY(nccl().Recv(g->full_rgb.as<float>() + row_px * band_rows[r] * 3, row_px * rows * 3, ncclFloat32, r,
-                                      g->comm, s));
-                    NCCL_TRY(nccl().Recv(g->full_T.as<float>() + row_px * band_rows[r], row_px * rows, ncclFloat32, r,
-                                      g->comm, s));
+                    if (!region_px(r)) continue;
+                    NCCL_TRY(nccl().Recv(dst_rgb(r), region_px(r) * 3, ncclFloat32, r, g->comm, s));
+                    NCCL_TRY(nccl().Recv(dst_T(r), region_px(r), ncclFloat32, r, g->comm, s));
                 }
-            } else if (y1 > y0) {
-                NCCL_TRY(nccl().Send(ctx->fb_rgb.ptr, row_px * (y1 - y0) * 3, ncclFloat32, 0, g->comm, s));
-                NCCL_TRY(nccl().Send(ctx->fb_T.ptr, row_px * (y1 - y0), ncclFloat32, 0, g->comm, s));
+            } else if (a1 > a0) {
+                NCCL_TRY(nccl().Send(ctx->fb_rgb.ptr, region_px(g->rank) * 3, ncclFloat32, 0, g->comm, s));
+                NCCL_TRY(nccl().Send(ctx->fb_T.ptr, region_px(g->rank), ncclFloat32, 0, g->comm, s));
             }
             NCCL_TRY(nccl().GroupEnd());
         }
+        if (g->rank == 0 && by_cols) {
+            for (int r = 0; r < P; ++r) {
+                const size_t wr = cuts[r + 1] - cuts[r];
+                if (!wr) continue;
+                CUDA_TRY(cudaMemcpy2DAsync(g->full_rgb.as<float>() + 3 * cuts[r], static_cast<size_t>(W) * 12, dst_rgb(r),
+                                           wr * 12, wr * 12, H, cudaMemcpyDeviceToDevice, s));
+                CUDA_TRY(cudaMemcpy2DAsync(g->full_T.as<float>() + cuts[r], static_cast<size_t>(W) * 4, dst_T(r), wr * 4,
+                                           wr * 4, H, cudaMemcpyDeviceToDevice, s));
+            }
+        }
         if (g->rank == 0 && (fb_rgb || fb_T)) {
-            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, g->full_rgb.ptr, row_px * H * 12, cudaMemcpyDefault, s));
-            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, g->full_T.ptr, row_px * H * 4, cudaMemcpyDefault, s));
+            const size_t px = static_cast<size_t>(W) * H;
+            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, g->full_rgb.ptr, px * 12, cudaMemcpyDefault, s));
+            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, g->full_T.ptr, px * 4, cudaMemcpyDefault, s));
             if (is_host_pointer(fb_rgb) || is_host_pointer(fb_T)) CUDA_TRY(cudaStreamSynchronize(s));
         }
     });
@@ -2357,30 +2435,32 @@ int gscg_group_framebuffer_device(gscg_group* g, float** rgb, float** T) {
     return GSCG_OK;
 }
 
-int gscg_group_row_costs(gscg_group* g, uint32_t tiles_y, uint64_t* out) {
+int gscg_group_tile_costs(gscg_group* g, uint32_t tiles_x, uint32_t tiles_y, uint64_t* out) {
     if (!g || !out) return GSCG_ERR_INVALID_ARGUMENT;
     gscg_ctx* ctx = g->ctx;
     return guarded(ctx, [&] {
         CUDA_TRY(cudaSetDevice(ctx->device));
         cudaStream_t s = ctx->stream;
         const FrameGeom& geo = ctx->geom;
-        CUDA_TRY(g->row_costs.ensure(static_cast<size_t>(tiles_y) * 8));
-        CUDA_TRY(g->all_costs.ensure(static_cast<size_t>(tiles_y) * 8 * g->nranks));
-        CUDA_TRY(cudaMemsetAsync(g->row_costs.ptr, 0, static_cast<size_t>(tiles_y) * 8, s));
-        // This rank's last band: its tile rows [band_tile_row0, + band_tile_rows).
-        const uint32_t rows = static_cast<uint32_t>(geo.band_tile_rows);
-        if (ctx->tiles && rows && static_cast<uint32_t>(geo.band_tile_row0) + rows <= tiles_y) {
-            k_row_costs<<<(rows + 7) / 8, 256, 0, s>>>(ctx->ranges.as<uint2>(), rows, geo.tiles_x * geo.cells_per_tile,
-                                                      g->row_costs.as<unsigned long long>() + geo.band_tile_row0);
+        const size_t n = static_cast<size_t>(tiles_x) * tiles_y;
+        CUDA_TRY(g->row_costs.ensure(n * 8));
+        CUDA_TRY(g->all_costs.ensure(n * 8));
+        CUDA_TRY(cudaMemsetAsync(g->row_costs.ptr, 0, n * 8, s));
+        // This rank's last region: tiles [band_tile_col0, +band_tiles_x) x [band_tile_row0, +band_tile_rows).
+        const uint32_t rtx = static_cast<uint32_t>(geo.band_tiles_x), rows = static_cast<uint32_t>(geo.band_tile_rows);
+        if (ctx->tiles && rtx && rows && static_cast<uint32_t>(geo.band_tile_row0) + rows <= tiles_y &&
+            static_cast<uint32_t>(geo.band_tile_col0) + rtx <= tiles_x) {
+            k_tile_costs<<<(rtx * rows + 255) / 256, 256, 0, s>>>(ctx->ranges.as<uint2>(), rtx, rows, geo.cells_per_tile,
+                                                                 geo.band_tile_col0, geo.band_tile_row0, tiles_x,
+                                                                 g->row_costs.as<unsigned long long>());
             CUDA_TRY(cudaGetLastError());
         }
-        // Every rank's rows (disjoint bands) summed: all-reduce of the tiles_y vector.
+        // Every rank's tiles (disjoint regions) summed: all-reduce of the tile map.
         if (g->nranks > 1)
-            NCCL_TRY(nccl().AllReduce(g->row_costs.ptr, g->all_costs.ptr, tiles_y, ncclUint64, ncclSum, g->comm, s));
+            NCCL_TRY(nccl().AllReduce(g->row_costs.ptr, g->all_costs.ptr, n, ncclUint64, ncclSum, g->comm, s));
         else
-            CUDA_TRY(cudaMemcpyAsync(g->all_costs.ptr, g->row_costs.ptr, static_cast<size_t>(tiles_y) * 8,
-                                     cudaMemcpyDeviceToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(out, g->all_costs.ptr, static_cast<size_t>(tiles_y) * 8, cudaMemcpyDefault, s));
+            CUDA_TRY(cudaMemcpyAsync(g->all_costs.ptr, g->row_costs.ptr, n * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(out, g->all_costs.ptr, n * 8, cudaMemcpyDefault, s));
         CUDA_TRY(cudaStreamSynchronize(s));
     });
 }

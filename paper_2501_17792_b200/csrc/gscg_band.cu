@@ -160,20 +160,19 @@ k_band_unpack(BandUnpackParams p) {
     }
 }
 
-// Per-tile-row pair counts of a frame (the band balance of the multi-GPU frame): one warp
-// per tile row sums its cells' range lengths.
-__global__ void k_row_costs(const uint2* ranges, uint32_t tile_rows, uint32_t cells_per_row, unsigned long long* out) {
-    const uint32_t row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const uint32_t lane = threadIdx.x & 31u;
-    if (row >= tile_rows) return;
+// Pairs per tile of a frame region (the region balance of the multi-GPU frame): one
+// thread per region tile sums its cells' range lengths into the frame's tile map.
+__global__ void k_tile_costs(const uint2* ranges, uint32_t region_tiles_x, uint32_t region_rows, uint32_t cells_per_tile,
+                             int32_t tile_col0, int32_t tile_row0, uint32_t tiles_x, unsigned long long* out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= region_tiles_x * region_rows) return;
     unsigned long long sum = 0;
-    for (uint32_t c = lane; c < cells_per_row; c += 32) {
-        const uint2 r = ranges[static_cast<size_t>(row) * cells_per_row + c];
+    for (uint32_t c = 0; c < cells_per_tile; ++c) {
+        const uint2 r = ranges[static_cast<size_t>(t) * cells_per_tile + c];
         sum += r.y - r.x;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) out[row] = sum;
+    const uint32_t tx = t % region_tiles_x + tile_col0, ty = t / region_tiles_x + tile_row0;
+    out[static_cast<size_t>(ty) * tiles_x + tx] = sum;
 }
 
 }  // namespace gscg

@@ -56,7 +56,8 @@ struct CameraDev {
     float pos[3];
     float focal, cx, cy, near_m;
     int32_t width, height;
-    int32_t band_y0, band_y1;  // screen rows [band_y0, band_y1) this context renders (whole frame: 0, height)
+    // The screen region this context renders (gscg_set_region; the whole frame: 0, 0, width, height).
+    int32_t band_x0, band_y0, band_x1, band_y1;
 };
 
 // Frame-level counters written by the kernels and read back once per frame.

@@ -93,6 +93,9 @@ struct RasterParams {
     int32_t width, height, tile_size, tiles_x;
     int32_t tile_row0;  // first tile row of the launch (screen band), 0 for a full frame
     int32_t out_row0;   // screen row stored in row 0 of out_rgb / out_T
+    int32_t tile_col0;  // first tile column of the region (tiles_x counts the region's columns)
+    int32_t out_col0;   // screen column stored in column 0 of out_rgb / out_T
+    int32_t out_stride; // pixels per output row (the region's width)
     float bg[3];
     float alpha_max;
     float t_floor;
@@ -259,7 +262,8 @@ struct BandUnpackParams {
 __global__ void k_band_count(BandParams p);
 __global__ void k_band_pack(BandParams p);
 __global__ void k_band_unpack(BandUnpackParams p);
-__global__ void k_row_costs(const uint2* ranges, uint32_t tile_rows, uint32_t cells_per_row, unsigned long long* out);
+__global__ void k_tile_costs(const uint2* ranges, uint32_t region_tiles_x, uint32_t region_rows, uint32_t cells_per_tile,
+                             int32_t tile_col0, int32_t tile_row0, uint32_t tiles_x, unsigned long long* out);
 
 // metrics
 constexpr int kSseThreads = 256;

@@ -273,7 +273,8 @@ k_project(ProjectParams p) {
                     y1 = min(cam.height, x86_float_to_int(floorf(my + ry)) + 1);
                     // A band frame keeps the splats whose rect meets its rows (renderer.cpp
                     // bins by rect, :147-161); the whole frame is the band [0, height).
-                    if (x0 < x1 && y0 < y1 && y0 < cam.band_y1 && y1 > cam.band_y0) {
+                    if (x0 < x1 && y0 < y1 && y0 < cam.band_y1 && y1 > cam.band_y0 && x0 < cam.band_x1 &&
+                        x1 > cam.band_x0) {
                         survive = true;
                         cxx = C[0][0];
                         cxy = 0.5f * (C[0][1] + C[1][0]);
@@ -286,8 +287,8 @@ k_project(ProjectParams p) {
                         cb = -cxy * inv_det;
                         cc = cxx * inv_det;
                         // Binning cells of the rect: first cell, cells across, cells down.
-                        const int cx0 = cdiv(x0), cx1 = cdiv(x1 - 1);
-                        const int cyb = cdiv(cam.band_y0);  // band's first cell row
+                        const int cxb = cdiv(cam.band_x0), cyb = cdiv(cam.band_y0);  // region's first cell
+                        const int cx0 = cdiv(max(x0, cam.band_x0)) - cxb, cx1 = cdiv(min(x1, cam.band_x1) - 1) - cxb;
                         const int cy0 = cdiv(max(y0, cam.band_y0)) - cyb, cy1 = cdiv(min(y1, cam.band_y1) - 1) - cyb;
                         n_tiles = static_cast<uint32_t>((cx1 - cx0 + 1) * (cy1 - cy0 + 1));
                         span_lo = static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0) << 16);

@@ -142,7 +142,7 @@ k_raster16q(RasterParams p) {
     load_exp_table(s_tab);
     __syncthreads();
     const int tile = blockIdx.x >> 2, quad = blockIdx.x & 3;
-    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
+    const int tx = tile % p.tiles_x + p.tile_col0, ty = tile / p.tiles_x + p.tile_row0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bx0 = tx * 16 + (quad & 1) * 8;
     const int by0 = ty * 16 + (quad >> 1) * 8 + warp * 4;
@@ -219,7 +219,7 @@ k_raster16q(RasterParams p) {
     }
     cp_async_wait<0>();
     if (inside) {
-        const size_t o = static_cast<size_t>(py - p.out_row0) * p.width + px;
+        const size_t o = static_cast<size_t>(py - p.out_row0) * p.out_stride + (px - p.out_col0);
         p.out_rgb[3 * o + 0] = __fadd_rn(cr, __fmul_rn(T, p.bg[0]));
         p.out_rgb[3 * o + 1] = __fadd_rn(cg, __fmul_rn(T, p.bg[1]));
         p.out_rgb[3 * o + 2] = __fadd_rn(cb, __fmul_rn(T, p.bg[2]));
@@ -236,7 +236,7 @@ k_raster_generic(RasterParams p) {
     load_exp_table(s_tab);
     const int ts = p.tile_size;
     const int tile = blockIdx.x;
-    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x + p.tile_row0;
+    const int tx = tile % p.tiles_x + p.tile_col0, ty = tile / p.tiles_x + p.tile_row0;
     float T[PPT], cr[PPT], cg[PPT], cb[PPT];
     int pxs[PPT], pys[PPT];
     bool live[PPT];
@@ -280,7 +280,7 @@ k_raster_generic(RasterParams p) {
     for (int k = 0; k < PPT; ++k) {
         const int lp = threadIdx.x + k * 256;
         if (lp < ts * ts && pxs[k] < p.width && pys[k] < p.height) {
-            const size_t o = static_cast<size_t>(pys[k] - p.out_row0) * p.width + pxs[k];
+            const size_t o = static_cast<size_t>(pys[k] - p.out_row0) * p.out_stride + (pxs[k] - p.out_col0);
             p.out_rgb[3 * o + 0] = __fadd_rn(cr[k], __fmul_rn(T[k], p.bg[0]));
             p.out_rgb[3 * o + 1] = __fadd_rn(cg[k], __fmul_rn(T[k], p.bg[1]));
             p.out_rgb[3 * o + 2] = __fadd_rn(cb[k], __fmul_rn(T[k], p.bg[2]));

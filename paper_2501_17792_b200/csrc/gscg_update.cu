@@ -419,7 +419,7 @@ k_inst_cull(CullParams p) {
         const double ry = 3.0 * (f / zmin) * sqrt(gy) * sigma * 1.001 + pad;
         const double mx_hi = f * ux_hi + cam.cx, mx_lo = f * ux_lo + cam.cx;
         const double my_hi = f * uy_hi + cam.cy, my_lo = f * uy_lo + cam.cy;
-        cull = (mx_hi + rx < -margin) || (mx_lo - rx > cam.width + margin) ||
+        cull = (mx_hi + rx < cam.band_x0 - margin) || (mx_lo - rx > cam.band_x1 + margin) ||
                (my_hi + ry < cam.band_y0 - margin) || (my_lo - ry > cam.band_y1 + margin);
     }
     // NaN anywhere makes the comparisons false; non-finite input never culls.

@@ -78,7 +78,10 @@ def band_rows(height: int, tile: int, parts: int, row_weights: Optional[Sequence
         cuts = [0]
         for b in range(1, parts):
             c = int(np.searchsorted(cum, cum[-1] * b / parts, side="left"))
-            cuts.append(min(max(c, cuts[-1]), trows))
+            # every band keeps at least one tile row while there are rows to hand out
+            lo = cuts[-1] + (1 if cuts[-1] < trows else 0)
+            hi = max(lo, trows - (parts - b)) if trows >= parts else trows
+            cuts.append(min(max(c, lo), hi, trows))
         cuts.append(trows)
     return [min(c * tile, height) for c in cuts]
 
@@ -436,14 +439,18 @@ def broadcast_unique_id(rank: int, world: int, dist=None, group=None) -> bytes:
 
 
 class BandGroup:
-    """One rank of the band-split frame: rank r renders screen rows [rows[r], rows[r+1])
-    of every frame on its own GPU and the bands are gathered into rank 0's framebuffer,
-    all inside gscg_group_render_frame (NCCL point-to-point on the context stream; the
-    group owns its communicator). Band boundaries follow the previous frames' binned
-    pairs per tile row, summed over ranks (gscg_group_row_costs) whenever rebalance() is
-    called; every rank computes the same rows from the same all-reduced costs."""
+    """One rank of the region-split frame: rank r renders screen columns [cuts[r],
+    cuts[r+1]) (axis "cols", the default) or rows (axis "rows") of every frame on its own
+    GPU, and the regions are gathered into rank 0's framebuffer, all inside
+    gscg_group_render_frame (NCCL point-to-point on the context stream; the group owns its
+    communicator). Cuts follow the binned pairs per tile of recent frames, summed over
+    ranks (gscg_group_tile_costs), whenever rebalance() is called; every rank computes the
+    same cuts from the same all-reduced costs. Columns balance a crowd seen along its rows
+    far better than rows: the distant characters crowd a few tile rows near the horizon
+    (DESIGN.md §5)."""
 
-    def __init__(self, renderer, rank: int, world: int, dist=None, group=None, unique_id: Optional[bytes] = None):
+    def __init__(self, renderer, rank: int, world: int, dist=None, group=None, unique_id: Optional[bytes] = None,
+                 axis: str = "cols"):
         self.renderer, self.rank, self.world = renderer, rank, world
         cfg = renderer.scene.cfg
         self.height, self.width = cfg.height, cfg.width
@@ -452,8 +459,10 @@ class BandGroup:
         h = C.c_void_p()
         N.check_gscg(N.gscg().gscg_group_create(renderer.gpu, buf, world, rank, C.byref(h)), renderer.gpu)
         self._h = h
-        self.tile = 16
-        self.rows = band_rows(self.height, self.tile, world)
+        if axis not in ("cols", "rows"):
+            raise ValueError("axis must be 'cols' or 'rows'")
+        self.axis = axis
+        self.set_tile(16)
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -463,31 +472,38 @@ class BandGroup:
     def __del__(self):
         self.close()
 
+    @property
+    def extent(self) -> int:
+        return self.width if self.axis == "cols" else self.height
+
     def set_tile(self, tile: int) -> None:
         self.tile = tile
-        self.rows = band_rows(self.height, tile, self.world)
+        self.cuts = band_rows(self.extent, tile, self.world)
 
     def render(self, frame, cam, settings, lod, out_rgb=None, out_T=None) -> "N.GscgStageTimes":
         """One frame (frame/cam/settings/lod: the gscg_render_frame descriptors). On rank 0,
         out_rgb / out_T (numpy, host or None) receive the whole frame."""
         st = N.GscgStageTimes()
-        rows = (C.c_uint32 * (self.world + 1))(*self.rows)
+        cuts = (C.c_uint32 * (self.world + 1))(*self.cuts)
+        axis = N.GSCG_SPLIT_COLS if self.axis == "cols" else N.GSCG_SPLIT_ROWS
         ptr = (lambda a: None if a is None else a.ctypes.data)
         N.check_gscg(N.gscg().gscg_group_render_frame(self._h, C.byref(frame), C.byref(cam), C.byref(settings),
-                                                       C.byref(lod), rows, ptr(out_rgb), ptr(out_T), C.byref(st)),
-                     self.renderer.gpu)
+                                                       C.byref(lod), axis, cuts, ptr(out_rgb), ptr(out_T),
+                                                       C.byref(st)), self.renderer.gpu)
         return st
 
-    def row_costs(self) -> np.ndarray:
+    def tile_costs(self) -> np.ndarray:
+        tx = (self.width + self.tile - 1) // self.tile
         ty = (self.height + self.tile - 1) // self.tile
-        out = np.zeros(ty, dtype=np.uint64)
-        N.check_gscg(N.gscg().gscg_group_row_costs(self._h, ty, out.ctypes.data), self.renderer.gpu)
+        out = np.zeros((ty, tx), dtype=np.uint64)
+        N.check_gscg(N.gscg().gscg_group_tile_costs(self._h, tx, ty, out.ctypes.data), self.renderer.gpu)
         return out
 
     def rebalance(self) -> list[int]:
-        """New band rows from the last frame's pairs per tile row over all ranks (plus a
-        per-row floor for the fixed per-pixel cost)."""
-        costs = self.row_costs().astype(np.float64)
-        if costs.sum() > 0:
-            self.rows = band_rows(self.height, self.tile, self.world, costs + 0.02 * costs.mean() + 1.0)
-        return self.rows
+        """New cuts from the last frame's pairs per tile over all ranks, summed along the
+        split axis (plus a small per-line floor for the fixed per-pixel cost)."""
+        costs = self.tile_costs().astype(np.float64)
+        line = costs.sum(0) if self.axis == "cols" else costs.sum(1)
+        if line.sum() > 0:
+            self.cuts = band_rows(self.extent, self.tile, self.world, line + 0.02 * line.mean() + 1.0)
+        return self.cuts

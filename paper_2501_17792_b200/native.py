@@ -21,6 +21,8 @@ GSCG_ERR_OOM = -4
 GSCG_ERR_STATE = -5
 GSCG_UNIQUE_ID_BYTES = 128
 GSCG_LOD_GIVEN = -2
+GSCG_SPLIT_ROWS = 0
+GSCG_SPLIT_COLS = 1
 GSCG_LAYOUT_SHARED = 0
 GSCG_LAYOUT_NAIVE = 1
 GSCG_MEM_HOST = 0
@@ -144,14 +146,15 @@ GSCG_SYMBOLS = {
     "gscg_eval_expf": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "gscg_set_band": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "gscg_set_layout": (C.c_int, [_P, C.c_int32]),
+    "gscg_set_region": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "gscg_group_unique_id": (C.c_int, [_P]),
     "gscg_group_create": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(_P)]),
     "gscg_group_destroy": (C.c_int, [_P]),
     "gscg_group_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
-                                          C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, _P, _P,
-                                          C.POINTER(GscgStageTimes)]),
+                                          C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), C.c_int32, _P,
+                                          _P, _P, C.POINTER(GscgStageTimes)]),
     "gscg_group_framebuffer_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),
-    "gscg_group_row_costs": (C.c_int, [_P, C.c_uint32, _P]),
+    "gscg_group_tile_costs": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "gscg_gather_splats": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                      C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), _P, C.c_uint64,
                                      C.POINTER(C.c_uint64)]),

@@ -638,8 +638,8 @@ def test_group_single_rank_frame_equals_render_frame():
     T = np.empty((cfg.height, cfg.width), np.float32)
     g.render(fd, s.camera_basis(), gscg_settings(P.RenderSettings()), lp, rgb, T)
     assert rgb.tobytes() == full_rgb.tobytes() and T.tobytes() == full_T.tobytes()
-    costs = g.row_costs()
-    assert int(costs.sum()) == K and len(costs) == (cfg.height + 15) // 16
+    costs = g.tile_costs()
+    assert int(costs.sum()) == K and costs.shape == ((cfg.height + 15) // 16, (cfg.width + 15) // 16)
     rows = g.rebalance()
     assert rows[0] == 0 and rows[-1] == cfg.height
     g.close()
@@ -664,3 +664,26 @@ def test_naive_layout_renders_the_same_frame(forced):
     r.set_layout(False)
     d, _ = r.render_frame(0.7, st, forced_lod=forced)
     assert c.tobytes() == d.tobytes() and r.memory_usage()["naive_attribute_bytes"] == 0
+
+
+COL_SPLITS = [[0, 1920], [0, 640, 1280, 1920], [0, 16, 512, 528, 1904, 1920]]
+
+
+@pytest.mark.parametrize("cols", COL_SPLITS)
+def test_column_regions_assemble_the_whole_frame_bit_for_bit(cols):
+    """gscg_set_region with column splits (the multi-GPU frame's default axis): the
+    full-height column regions side by side equal the whole frame byte for byte."""
+    s, extra = config_scene(2)
+    r = P.Renderer(s, device_poses=True)
+    full_rgb, full_T = r.render_frame(0.4, P.RenderSettings())
+    full_rgb, full_T = full_rgb.copy(), full_T.copy()
+    rb = P.Renderer(s, device_poses=True)
+    parts_rgb, parts_T = [], []
+    for b in range(len(cols) - 1):
+        rb.set_region(cols[b], 0, cols[b + 1], 0)
+        rgb, T = rb.render_frame(0.4, P.RenderSettings())
+        assert rgb.shape == (1080, cols[b + 1] - cols[b], 3)
+        parts_rgb.append(rgb.copy())
+        parts_T.append(T.copy())
+    assert np.concatenate(parts_rgb, axis=1).tobytes() == full_rgb.tobytes()
+    assert np.concatenate(parts_T, axis=1).tobytes() == full_T.tobytes()
