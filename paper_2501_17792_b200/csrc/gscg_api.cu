@@ -37,9 +37,29 @@ using namespace gscg;
 
 namespace {
 
+// Device buffer owned by the context: grow-only, freed on release() or destruction (so
+// every buffer a context ever grew goes with gscg_destroy).
 struct DevBuf {
     void* ptr = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), cap(o.cap) {
+        o.ptr = nullptr;
+        o.cap = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            ptr = o.ptr;
+            cap = o.cap;
+            o.ptr = nullptr;
+            o.cap = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
     void release() {
         if (ptr) cudaFree(ptr);
         ptr = nullptr;

@@ -640,8 +640,8 @@ def test_group_single_rank_frame_equals_render_frame():
     assert rgb.tobytes() == full_rgb.tobytes() and T.tobytes() == full_T.tobytes()
     costs = g.tile_costs()
     assert int(costs.sum()) == K and costs.shape == ((cfg.height + 15) // 16, (cfg.width + 15) // 16)
-    rows = g.rebalance()
-    assert rows[0] == 0 and rows[-1] == cfg.height
+    cuts = g.rebalance()  # column cuts (the default split axis)
+    assert cuts[0] == 0 and cuts[-1] == cfg.width
     g.close()
 
 
