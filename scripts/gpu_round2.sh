@@ -12,7 +12,7 @@ for c in 1 2 4; do python bench.py --config $c --no-cpu-baseline > gpurun_out/${
 timeout 1200 python bench.py --config 5 --no-cpu-baseline --steps 5 --warmup 3 > gpurun_out/${T}_bench_c5.log 2>gpurun_out/${T}_bench_c5.err; echo c5=$? >> gpurun_out/${T}_status.txt
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_ncu_launch.log 2>&1; echo launches=$? >> gpurun_out/${T}_status.txt
 python scripts/launch_table.py gpurun_out/${T}_launches.csv > gpurun_out/${T}_launches.txt 2>&1
-ncu --set full --clock-control none --import-source on -o /tmp/prof_${T} python scripts/profile_frame.py --frames 1 > gpurun_out/${T}_ncu_full.log 2>&1; echo full=$? >> gpurun_out/${T}_status.txt
+ncu --set full --clock-control none --import-source on --profile-from-start off -o /tmp/prof_${T} python scripts/profile_frame.py --frames 1 --warmup 2 > gpurun_out/${T}_ncu_full.log 2>&1; echo full=$? >> gpurun_out/${T}_status.txt
 python scripts/ncu_summary.py /tmp/prof_${T}.ncu-rep gpurun_out/${T}_ncu_summary.json > gpurun_out/${T}_ncu_full.txt 2>&1
 for k in k_raster16q k_project k_sort_downsweep k_sort_upsweep k_emit_scatter k_cell_fixup k_sorted_spans; do
   python scripts/ncu_source_top.py /tmp/prof_${T}.ncu-rep $k > gpurun_out/${T}_source_$k.txt 2>&1

@@ -1,7 +1,11 @@
 """Minimal profiling target: N config-3 frames through gscg_render_frame with device-resident
 inputs (no e2e / CPU legs), for ncu captures of the frame's kernels.
 
-  python scripts/profile_frame.py --frames 3 [--config 3]
+  python scripts/profile_frame.py --frames 3 [--config 3] [--warmup 2]
+
+Warm-up frames (which grow the buffers to their high-water mark) run outside the profiler
+range (cudaProfilerStart/Stop): capture with ncu --profile-from-start off to see one
+clean launch of every kernel per frame.
 """
 import argparse
 import ctypes as C
@@ -17,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
     args = ap.parse_args()
     import torch
 
@@ -54,13 +59,18 @@ def main():
     fd.pose_source = N.GSCG_POSES_SAMPLED  # poses sampled on the device, as bench.py
     fd.motion_ids, fd.phase_offsets = d_mid.data_ptr(), d_phase.data_ptr()
     lib = N.gscg()
-    for f in range(args.frames):
+    for f in range(args.warmup + args.frames):
+        if f == args.warmup:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         fd.time_s = extra["time_s"] + f / 30.0
         st = N.GscgStageTimes()
         N.check_gscg(lib.gscg_render_frame(r.gpu, C.byref(fd), C.byref(cam), C.byref(rs), C.byref(lp), None, None,
                                            C.byref(st)), r.gpu)
         print(f"frame {f}: update {st.update_ms:.3f} gather {st.gather_ms:.3f} sort {st.sort_ms:.3f} "
               f"raster {st.rasterize_ms:.3f} S={st.splat_count} K={st.pair_count} launches={st.kernel_launches}")
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 
 
 if __name__ == "__main__":
