@@ -35,6 +35,14 @@
 
 using namespace gscg;
 
+bool gscg::pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("GSCG_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 namespace {
 
 // Device buffer owned by the context: grow-only, freed on release() or destruction (so
@@ -563,7 +571,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         }
         if (nseg) {
             const uint32_t bx = std::min<uint32_t>((max_words + 255) / 256, 4u * ctx->sm_count);
-            k_copy_segments<<<dim3(bx, nseg), 256, 0, s>>>(segs);
+            CUDA_TRY(pdl_launch(k_copy_segments, dim3(bx, nseg), 256, 0, s, segs));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -596,7 +604,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pp.keys = ctx->d_keys.as<KeyPairDev>();
         pp.poses = ctx->poses.as<float>();
         const uint64_t threads = static_cast<uint64_t>(n) * (frame->joint_stride + 1);
-        k_sample_poses<<<static_cast<uint32_t>((threads + 255) / 256), 256, 0, s>>>(pp);
+        CUDA_TRY(pdl_launch(k_sample_poses, static_cast<uint32_t>((threads + 255) / 256), 256, 0, s, pp));
         ++launches;
         CUDA_TRY(cudaGetLastError());
     }
@@ -645,7 +653,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             fp.skin = ctx->skin.as<float>();
             const int per_block = kFkThreads / 16;
             const uint32_t m = shard_end - shard_begin;
-            k_fk_skin<<<(m + per_block - 1) / per_block, kFkThreads, per_block * kFkSmemPerInstance(js), s>>>(fp);
+            CUDA_TRY(pdl_launch(k_fk_skin, (m + per_block - 1) / per_block, kFkThreads, per_block * kFkSmemPerInstance(js), s, fp));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -664,7 +672,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             cp.cam = camdev;
             cp.visible = ctx->visible.as<uint32_t>();
             const uint32_t m = shard_end - shard_begin;
-            k_inst_cull<<<(m + 7) / 8, 256, 0, s>>>(cp);
+            CUDA_TRY(pdl_launch(k_inst_cull, (m + 7) / 8, 256, 0, s, cp));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -692,7 +700,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pp.members = ctx->members.as<uint32_t>();
         pp.visible = cull ? ctx->visible.as<uint32_t>() : posed_mode ? ctx->project_mask.as<uint32_t>() : nullptr;
         pp.counters = counters;
-        k_lod_plan<<<1, 1024, 0, s>>>(pp);
+        CUDA_TRY(pdl_launch(k_lod_plan, 1, 1024, 0, s, pp));
         ++launches;
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
@@ -801,11 +809,11 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         if (shard_end > shard_begin && ctx->group_count > 0) {
             const dim3 grid(ctx->sm_count * project_blocks_per_sm);
             if (posed_mode)
-                k_project<true, false><<<grid, kProjectThreads, project_smem, s>>>(pj);
+                CUDA_TRY(pdl_launch(k_project<true, false>, grid, kProjectThreads, project_smem, s, pj));
             else if (naive)
-                k_project<false, true><<<grid, kProjectThreads, project_smem, s>>>(pj);
+                CUDA_TRY(pdl_launch(k_project<false, true>, grid, kProjectThreads, project_smem, s, pj));
             else
-                k_project<false, false><<<grid, kProjectThreads, project_smem, s>>>(pj);
+                CUDA_TRY(pdl_launch(k_project<false, false>, grid, kProjectThreads, project_smem, s, pj));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -822,7 +830,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
                 segs.words[1] = n;
                 nseg = 2;
             }
-            k_copy_segments<<<dim3(std::min<uint32_t>((n + 255) / 256 + 1, 64u), nseg), 256, 0, s>>>(segs);
+            CUDA_TRY(pdl_launch(k_copy_segments, dim3(std::min<uint32_t>((n + 255) / 256 + 1, 64u), nseg), 256, 0, s, segs));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -879,11 +887,11 @@ int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, D
         sp.counts = ctx->status.as<uint32_t>();
         sp.digit_base = ctx->hist.as<uint32_t>();
         const bool wide = (plan.wide >> q) & 1u;
-        if (wide) k_sort_upsweep_wide<<<tiles, kSortThreads, 0, s>>>(sp);
-        else k_sort_upsweep<<<tiles, kSortThreads, 0, s>>>(sp);
-        k_sort_rows<<<1u << plan.bits[q], 1024, 0, s>>>(sp);
-        if (wide) k_sort_downsweep_wide<<<tiles, kSortThreads, 0, s>>>(sp);
-        else k_sort_downsweep<<<tiles, kSortThreads, 0, s>>>(sp);
+        if (wide) CUDA_TRY(pdl_launch(k_sort_upsweep_wide, tiles, kSortThreads, 0, s, sp));
+        else CUDA_TRY(pdl_launch(k_sort_upsweep, tiles, kSortThreads, 0, s, sp));
+        CUDA_TRY(pdl_launch(k_sort_rows, 1u << plan.bits[q], 1024, 0, s, sp));
+        if (wide) CUDA_TRY(pdl_launch(k_sort_downsweep_wide, tiles, kSortThreads, 0, s, sp));
+        else CUDA_TRY(pdl_launch(k_sort_downsweep, tiles, kSortThreads, 0, s, sp));
         launches += 3;
         out ^= 1;
     }
@@ -1015,8 +1023,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
         const int quads = geo.cells_per_tile == 4 ? 1 : 0;
         const uint32_t* tag_keys = presorted ? nullptr : ctx->skeys[sb].as<uint32_t>();
-        k_sorted_spans<<<(S32 + 1023) / 1024, kMetaThreads, 0, s>>>(ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
-                                                                    S32, ctx->span_sorted.as<uint2>());
+        CUDA_TRY(pdl_launch(k_sorted_spans, (S32 + 1023) / 1024, kMetaThreads, 0, s, ctx->srecs[sb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
+                                                                    S32, ctx->span_sorted.as<uint2>()));
         ++launches;
         launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), nullptr, rtx, quads, dmask, drop, cell_bits, nullptr, nullptr);
@@ -1025,7 +1033,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         bp.digit_base = ctx->hist.as<uint32_t>();
         bp.tiles = eblocks;
         bp.bits = emit_bits;
-        k_sort_rows<<<dmask + 1, 1024, 0, s>>>(bp);
+        CUDA_TRY(pdl_launch(k_sort_rows, dmask + 1, 1024, 0, s, bp));
         launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), rtx, quads, dmask, drop, cell_bits,
                     ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>());
@@ -1046,14 +1054,14 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         uint32_t* long_count = reinterpret_cast<uint32_t*>(ctx->long_runs.as<uint2>() + long_cap);
         CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
         const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);  // 2048 pairs per CTA
-        k_cell_fixup<<<kblocks, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), ctx->precs[cb].as<uint32_t>(),
+        CUDA_TRY(pdl_launch(k_cell_fixup, kblocks, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), ctx->precs[cb].as<uint32_t>(),
                                              ctx->splat_meta.as<uint4>(), K, cell_mask, presorted ? 0 : 1,
-                                             ctx->ranges.as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap);
+                                             ctx->ranges.as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap));
         ++launches;
         if (!presorted) {
-            k_pair_long_runs<<<ctx->sm_count * 2, 256, 0, s>>>(ctx->pcell[cb].as<uint32_t>(), K,
+            CUDA_TRY(pdl_launch(k_pair_long_runs, ctx->sm_count * 2, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), K,
                                                               ctx->precs[cb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
-                                                              ctx->long_runs.as<uint2>(), long_count);
+                                                              ctx->long_runs.as<uint2>(), long_count));
             ++launches;
         }
         CUDA_TRY(cudaGetLastError());

@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <utility>
 
 #include "gscg.h"
 
@@ -82,5 +83,36 @@ __device__ __forceinline__ int x86_float_to_int(float v) {
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Programmatic dependent launch (PDL): the frame's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so kernel N+1's CTAs are scheduled
+// while kernel N's last wave runs instead of after it drains. Every such kernel starts with
+// pdl_entry(): griddepcontrol.wait blocks until the predecessor grid has completed and its
+// memory is visible (so no kernel ever reads a predecessor's output early, and completion
+// stays transitive down the chain); launch_dependents then lets the successor launch once
+// every CTA of this grid has passed that point. A kernel launched without the attribute
+// passes straight through both.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // GSCG_NO_PDL=1 turns the attribute off (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace gscg

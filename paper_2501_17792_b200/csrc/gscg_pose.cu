@@ -58,6 +58,7 @@ __device__ __forceinline__ float glibc_sinf(float y) {
 // One thread per (instance, slot): slot 0 = root translation, slot 1 + j = joint j.
 __global__ void __launch_bounds__(256)
 k_sample_poses(PoseParams p) {
+    pdl_entry();
     const uint32_t slots = p.joint_stride + 1;
     const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g >= static_cast<uint64_t>(p.n) * slots) return;

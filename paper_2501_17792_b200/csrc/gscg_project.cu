@@ -83,6 +83,7 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
 template <bool kPosedIn, bool kNaive>
 __global__ void __launch_bounds__(kProjectThreads, 4)
 k_project(ProjectParams p) {
+    pdl_entry();
     extern __shared__ float4 s_dyn[];
     float* s_sh = reinterpret_cast<float*>(s_dyn);
     float* s_mats = s_sh + (p.sh_enabled ? kProjectThreads * kShFloats : 0);

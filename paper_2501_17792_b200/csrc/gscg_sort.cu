@@ -98,6 +98,7 @@ __device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (
 
 __global__ void __launch_bounds__(kSortThreads)
 k_sort_upsweep(SortPassParams p) {
+    pdl_entry();
     __shared__ uint32_t s_hist[kSortWarps][kRadix][32];
     if ((blockIdx.x + 1) * kSortTile <= p.count) upsweep_tile<true>(p, s_hist);
     else upsweep_tile<false>(p, s_hist);
@@ -110,6 +111,7 @@ k_sort_upsweep(SortPassParams p) {
 constexpr int kRowItems = 8;
 __global__ void __launch_bounds__(1024)
 k_sort_rows(SortPassParams p) {
+    pdl_entry();
     __shared__ uint32_t s_warp[32];
     uint32_t* row = p.counts + static_cast<size_t>(blockIdx.x) * p.tiles;
     uint32_t carry = 0;
@@ -246,6 +248,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
 
 __global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep(SortPassParams p) {
+    pdl_entry();
     __shared__ DownsweepSmem sm;
     if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_tile<true>(p, sm);
     else downsweep_tile<false>(p, sm);
@@ -345,6 +348,7 @@ __device__ __forceinline__ void upsweep_wide_tile(const SortPassParams& p, uint3
 
 __global__ void __launch_bounds__(kSortThreads)
 k_sort_upsweep_wide(SortPassParams p) {
+    pdl_entry();
     __shared__ uint32_t s_hist[kSortWarps][kWideRadix];
     if ((blockIdx.x + 1) * kSortTile <= p.count) upsweep_wide_tile<true>(p, s_hist);
     else upsweep_wide_tile<false>(p, s_hist);
@@ -453,6 +457,7 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
 
 __global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep_wide(SortPassParams p) {
+    pdl_entry();
     __shared__ DownsweepWideSmem sm;
     if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_wide_tile<true>(p, sm);
     else downsweep_wide_tile<false>(p, sm);
@@ -462,6 +467,7 @@ k_sort_downsweep_wide(SortPassParams p) {
 // (one 16-byte meta gather per splat, all eight of a thread in flight).
 __global__ void __launch_bounds__(kMetaThreads)
 k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted) {
+    pdl_entry();
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
     const uint32_t b = (blockIdx.x * kMetaThreads + threadIdx.x) * kStreamItems;
     if (b + kStreamItems <= count) {
@@ -506,6 +512,7 @@ __device__ __forceinline__ unsigned long long pair_order_key(const uint4& m) {  
 __global__ void __launch_bounds__(256)
 k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t cell_mask, int fix,
              uint2* ranges, uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
+    pdl_entry();
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
     constexpr uint32_t kThreads = 256, kTile = kThreads * kStreamItems;
     constexpr uint32_t kHalo = 32;  // pairs past the tile: room for a run leaving the tile
@@ -688,6 +695,7 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
 __global__ void __launch_bounds__(256)
 k_pair_long_runs(const uint32_t* keys, uint32_t count, uint32_t* recs, const uint4* meta, const uint2* long_runs,
                  const uint32_t* long_count) {
+    pdl_entry();
     __shared__ unsigned long long s_key[kPairRunCap];
     __shared__ uint32_t s_rec[kPairRunCap];
     __shared__ uint32_t s_n;
@@ -781,6 +789,7 @@ __global__ void __launch_bounds__(kEmitThreads)
 k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count, const uint2* span_sorted,
                uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads,
                uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec) {
+    pdl_entry();
     constexpr int kWarps = kEmitThreads / 32, kDigitsPerWarp = kRadix / kWarps, kPerLane = kEmitThreads / 32;
     static_assert(kRadix % kWarps == 0, "digits split evenly over the warps");
     constexpr uint32_t kStage = kEmitStage;            // pairs staged for coalesced writes
@@ -902,8 +911,8 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
     const int smem = count_only ? kRadix * 4 : kEmitSmem;  // the count pass keeps 32 block counters
     auto kernel = count_only ? (quads ? k_emit_scatter<true, true> : k_emit_scatter<true, false>)
                              : (quads ? k_emit_scatter<false, true> : k_emit_scatter<false, false>);
-    kernel<<<blocks, kEmitThreads, smem, s>>>(rec_sorted, key_sorted, count, span_sorted, block_digit, digit_total,
-                                              blocks, tiles_x, quads, dmask, tag_drop, tag_shift, pair_cell, pair_rec);
+    pdl_launch(kernel, blocks, kEmitThreads, smem, s, rec_sorted, key_sorted, count, span_sorted, block_digit, digit_total,
+               blocks, tiles_x, quads, dmask, tag_drop, tag_shift, pair_cell, pair_rec);
 }
 
 __global__ void k_iota2(uint32_t* a, uint32_t* b, uint32_t n) {

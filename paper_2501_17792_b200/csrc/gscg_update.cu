@@ -49,6 +49,7 @@ __device__ T block_exclusive_scan(T v, T* s_warp, T& total) {
 
 __global__ void __launch_bounds__(kPlanThreads)
 k_lod_plan(PlanParams p) {
+    pdl_entry();
     __shared__ unsigned long long s_scan64[32];
     __shared__ uint32_t s_scan32[32];
     __shared__ uint32_t s_gcount[kMaxGroups];
@@ -220,6 +221,7 @@ __device__ __forceinline__ float rot_elem(const float4 q, int r, int c) {
 
 __global__ void __launch_bounds__(kFkThreads)
 k_fk_skin(FkParams p) {
+    pdl_entry();
     // Per half-warp (one instance): world[J][16], then the instance's local_bind and
     // inverse_bind matrices and pose quaternions, staged once so the joint chain below
     // runs from shared memory instead of paying a global-memory latency per joint.
@@ -327,6 +329,7 @@ k_fk_skin(FkParams p) {
 // rounding of the projection itself. Non-finite bounds never cull.
 __global__ void __launch_bounds__(256)
 k_inst_cull(CullParams p) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const uint32_t inst = p.first + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (inst >= p.n) return;
@@ -428,6 +431,7 @@ k_inst_cull(CullParams p) {
 }
 
 __global__ void k_copy_segments(CopySegs c) {
+    pdl_entry();
     const uint32_t seg = blockIdx.y;
     const uint32_t* __restrict__ src = c.src[seg];
     uint32_t* __restrict__ dst = c.dst[seg];

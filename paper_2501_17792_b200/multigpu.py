@@ -423,6 +423,9 @@ def render_frame_virtual(ranks: list[BandRank], time_s: float, settings=None, st
 def broadcast_unique_id(rank: int, world: int, dist=None, group=None) -> bytes:
     """Rank 0's NCCL unique id (gscg_group_unique_id), shipped to every rank over the
     caller's process group (torch.distributed, any backend: 128 bytes of plumbing)."""
+    # libgscg binds NCCL at run time to whichever libnccl.so.2 the process holds: load
+    # torch's (a newer NCCL than the system copy, which torch cannot run against) first.
+    import torch  # noqa: F401
     uid = (C.c_uint8 * N.GSCG_UNIQUE_ID_BYTES)()
     if rank == 0:
         rc = N.gscg().gscg_group_unique_id(uid)
@@ -451,6 +454,7 @@ class BandGroup:
 
     def __init__(self, renderer, rank: int, world: int, dist=None, group=None, unique_id: Optional[bytes] = None,
                  axis: str = "cols"):
+        import torch  # noqa: F401  (torch's NCCL before libgscg binds one; see broadcast_unique_id)
         self.renderer, self.rank, self.world = renderer, rank, world
         cfg = renderer.scene.cfg
         self.height, self.width = cfg.height, cfg.width
