@@ -230,139 +230,6 @@ k_raster16q(RasterParams p) {
     }
 }
 
-// Tile size 16, quadrant form, two-phase blend. Same staging, coverage bits and transpose
-// as k_raster16q, but the per-pixel list walk is split by cost: alpha = opacity *
-// expf(power) of a (pixel, splat) pair does not depend on the pixel's transmittance, only
-// the accumulation does. For every 32 staged splats the warp
-//   A. writes each lane's ordered list of covering splats into a warp worklist (a warp
-//      prefix sum gives each lane its slice);
-//   B. computes power, the cutoff test and alpha for the worklist 32 entries at a time,
-//      every lane busy (the exact expf is most of a pair's instructions);
-//   C. walks each lane's slice in order doing only the transmittance / colour update.
-// ncu showed the one-phase walk at 12 of 32 lanes active per instruction: the expensive
-// part now runs converged and only the cheap part diverges. Pixels are unchanged: every
-// pair's arithmetic and every pixel's order are the same.
-template <int CH>
-__global__ void __launch_bounds__(64)
-k_raster16q2(RasterParams p) {
-    pdl_entry();
-    constexpr int kStage = 32 * CH;
-    __shared__ float4 s_geo[2][2][kStage];   // [warp][buffer][slot]
-    __shared__ float4 s_col[2][2][kStage];
-    __shared__ float4 s_ext[2][2][kStage];   // G, B, rect lo, rect hi
-    __shared__ uint16_t s_wl[2][32 * 32];    // [warp] worklist: owner lane << 5 | staged slot (mod 32)
-    __shared__ float s_alpha[2][32 * 32];    // [warp] alpha of each worklist entry (< 0: below the cutoff)
-    __shared__ unsigned long long s_tab[32];
-    load_exp_table(s_tab);
-    __syncthreads();
-    const int tile = blockIdx.x >> 2, quad = blockIdx.x & 3;
-    const int tx = tile % p.tiles_x + p.tile_col0, ty = tile / p.tiles_x + p.tile_row0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int bx0 = tx * 16 + (quad & 1) * 8;
-    const int by0 = ty * 16 + (quad >> 1) * 8 + warp * 4;
-    const int px = bx0 + (lane & 7);
-    const int py = by0 + (lane >> 3);
-    const bool inside = px < p.width && py < p.height;
-    const uint2 range = p.ranges[blockIdx.x];
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-    bool done = !inside;
-    uint16_t* wl = s_wl[warp];
-    float* al = s_alpha[warp];
-    auto stage = [&](int buf, uint32_t start) {
-#pragma unroll
-        for (int h = 0; h < CH; ++h) {
-            const uint32_t i = start + h * 32 + lane;
-            if (i < range.y) {
-                const float4* src = p.records + 3ull * p.recs[i];
-                cp_async16(&s_geo[warp][buf][h * 32 + lane], src + 0);
-                cp_async16(&s_col[warp][buf][h * 32 + lane], src + 1);
-                cp_async16(&s_ext[warp][buf][h * 32 + lane], src + 2);
-            }
-        }
-        cp_async_commit();
-    };
-    int buf = 0;
-    if (range.x < range.y) stage(0, range.x);
-    for (uint32_t start = range.x; start < range.y; start += kStage) {
-        if (__all_sync(0xffffffffu, done)) break;
-        if (start + kStage < range.y) {
-            stage(buf ^ 1, start + kStage);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncwarp();
-        const int n = static_cast<int>(min(static_cast<uint32_t>(kStage), range.y - start));
-#pragma unroll
-        for (int h = 0; h < CH; ++h) {
-            const float4* geo = s_geo[warp][buf] + h * 32;
-            const float4* col = s_col[warp][buf] + h * 32;
-            const float4* ext = s_ext[warp][buf] + h * 32;
-            uint32_t todo = transpose32(h * 32 + lane < n ? block_cover(ext[lane], bx0, by0) : 0u, lane);
-            if (done) todo = 0u;
-            // A. this lane's covering splats, in list order, at its slice of the worklist
-            const uint32_t cnt = __popc(todo);
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            if (total == 0) continue;
-            const uint32_t base = incl - cnt;
-            {
-                uint32_t t = todo, w = base;
-                while (t) {
-                    wl[w++] = static_cast<uint16_t>((lane << 5) | (__ffs(t) - 1));
-                    t &= t - 1u;
-                }
-            }
-            __syncwarp();
-            // B. power, cutoff and alpha of every entry, the whole warp at once
-            for (uint32_t j = lane; j < total; j += 32) {
-                const uint32_t e = wl[j];
-                const int owner = static_cast<int>(e >> 5), k = static_cast<int>(e & 31u);
-                const float fx = static_cast<float>(bx0 + (owner & 7)) + 0.5f;
-                const float fy = static_cast<float>(by0 + (owner >> 3)) + 0.5f;
-                const float4 g = geo[k];
-                const float4 c = col[k];
-                const float dx = __fsub_rn(fx, g.x);
-                const float dy = __fsub_rn(fy, g.y);
-                const float q = __fadd_rn(__fmul_rn(__fmul_rn(g.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
-                const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(g.w, dx), dy));
-                al[j] = power < c.z ? -1.0f : fminf(__fmul_rn(c.y, glibc_expf(power, s_tab)), p.alpha_max);
-            }
-            __syncwarp();
-            // C. this lane's slice in order: transmittance and colour only
-            for (uint32_t j = base; j < base + cnt && !done; ++j) {
-                const float alpha = al[j];
-                if (alpha < 0.0f) continue;
-                const int k = wl[j] & 31;
-                const float w = __fmul_rn(T, alpha);
-                const float4 c = col[k];
-                const float4 e = ext[k];
-                cr = __fadd_rn(cr, __fmul_rn(w, c.w));
-                cg = __fadd_rn(cg, __fmul_rn(w, e.x));
-                cb = __fadd_rn(cb, __fmul_rn(w, e.y));
-                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                if (T < p.t_floor) done = true;
-            }
-            __syncwarp();
-        }
-        __syncwarp();
-        buf ^= 1;
-    }
-    cp_async_wait<0>();
-    if (inside) {
-        const size_t o = static_cast<size_t>(py - p.out_row0) * p.out_stride + (px - p.out_col0);
-        p.out_rgb[3 * o + 0] = __fadd_rn(cr, __fmul_rn(T, p.bg[0]));
-        p.out_rgb[3 * o + 1] = __fadd_rn(cg, __fmul_rn(T, p.bg[1]));
-        p.out_rgb[3 * o + 2] = __fadd_rn(cb, __fmul_rn(T, p.bg[2]));
-        p.out_T[o] = T;
-    }
-}
-
 // Any tile size up to 16*sqrt(PPT): PPT pixels per thread, pixel p = tid + k*256.
 template <int PPT>
 __global__ void __launch_bounds__(256)
@@ -427,12 +294,7 @@ k_raster_generic(RasterParams p) {
 }
 
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream) {
-    static const bool one_phase = [] {  // GSCG_RASTER_ONE_PHASE=1: the one-phase walk (A/B runs)
-        const char* e = std::getenv("GSCG_RASTER_ONE_PHASE");
-        return e && e[0] == '1';
-    }();
-    if (p.tile_size == 16 && !one_phase) pdl_launch(k_raster16q2<2>, tiles * 4, 64, 0, stream, p);
-    else if (p.tile_size == 16) pdl_launch(k_raster16q<2>, tiles * 4, 64, 0, stream, p);
+    if (p.tile_size == 16) pdl_launch(k_raster16q<2>, tiles * 4, 64, 0, stream, p);
     else if (p.tile_size <= 16) pdl_launch(k_raster_generic<1>, tiles, 256, 0, stream, p);
     else if (p.tile_size <= 32) pdl_launch(k_raster_generic<4>, tiles, 256, 0, stream, p);
     else pdl_launch(k_raster_generic<16>, tiles, 256, 0, stream, p);
