@@ -193,7 +193,39 @@ struct SortPassParams {
     uint32_t tiles;      // ceil(count / kSortTile)
     uint32_t* counts;      // kRadix x tiles, digit-major: tile digit counts -> exclusive offsets
     uint32_t* digit_base;  // kRadix: row totals (scanned by each downsweep CTA)
+    // Device-resolved pass (frames enqueued without a host read of the counters): count =
+    // min(count, *count_dev) (count, tiles: the capacity the grid was sized for), and for a
+    // depth pass shift += depth_drop(*depth_counters, depth_bits).
+    const unsigned long long* count_dev;
+    const FrameCounters* depth_counters;
+    uint32_t depth_bits;
 };
+
+// Low depth-key bits a depth sort over `depth_bits` bits drops for the frame's depth range
+// (the per-cell fix-up orders what they leave tied).
+__host__ __device__ __forceinline__ uint32_t depth_drop(uint32_t dmin, uint32_t dmax, uint32_t depth_bits) {
+    const uint32_t x = dmin ^ dmax;
+#ifdef __CUDA_ARCH__
+    const uint32_t dbits = x ? 32u - __clz(x) : 0u;
+#else
+    const uint32_t dbits = x ? 32u - static_cast<uint32_t>(__builtin_clz(x)) : 0u;
+#endif
+    return dbits > depth_bits ? dbits - depth_bits : 0u;
+}
+
+__device__ __forceinline__ uint32_t resolve_count(uint32_t cap, const unsigned long long* count_dev) {
+    if (!count_dev) return cap;
+    const unsigned long long c = *count_dev;
+    return c < cap ? static_cast<uint32_t>(c) : cap;
+}
+
+__device__ __forceinline__ SortPassParams resolve_pass(const SortPassParams& p) {
+    SortPassParams q = p;
+    q.count = resolve_count(p.count, p.count_dev);
+    if (p.depth_counters)
+        q.shift = p.shift + depth_drop(p.depth_counters->depth_min_bits, p.depth_counters->depth_max_bits, p.depth_bits);
+    return q;
+}
 
 __global__ void k_sort_upsweep(SortPassParams p);
 __global__ void k_sort_rows(SortPassParams p);
@@ -204,32 +236,38 @@ __global__ void k_sort_upsweep_wide(SortPassParams p);
 __global__ void k_sort_downsweep_wide(SortPassParams p);
 
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
-__global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted);
+__global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, const unsigned long long* count_dev,
+                               uint2* span_sorted);
 constexpr uint32_t kLongRun = 32;       // runs of equal pair keys longer than this go to k_pair_long_runs
 constexpr uint32_t kPairRunCap = 2048;  // k_pair_long_runs sorts runs up to this size in shared memory
 // long_runs must hold count / kLongRun + count / 2048 + 2 entries (runs longer than
 // kLongRun, plus at most one run leaving each 2048-pair fix-up tile).
 __global__ void k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
-                             uint32_t cell_mask, int fix, uint2* ranges, uint2* long_runs, uint32_t* long_count,
-                             uint32_t long_cap);
-__global__ void k_pair_long_runs(const uint32_t* keys, uint32_t count, uint32_t* recs, const uint4* meta,
-                                 const uint2* long_runs, const uint32_t* long_count);
+                             const unsigned long long* count_dev, uint32_t cell_mask, int fix, uint2* ranges,
+                             uint2* long_runs, uint32_t* long_count, uint32_t long_cap);
+__global__ void k_pair_long_runs(const uint32_t* keys, uint32_t count, const unsigned long long* count_dev,
+                                 uint32_t* recs, const uint4* meta, const uint2* long_runs, const uint32_t* long_count);
 constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
 constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
 constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes
 constexpr int kEmitSmem = (32 * kEmitThreads + 2 * kEmitStage) * 4;  // dynamic shared bytes
+struct EmitCounts {  // device-resolved emission (null: the host values)
+    const unsigned long long* count_dev;
+    const FrameCounters* depth_counters;  // tag_drop = depth_drop(..., depth_bits)
+    uint32_t depth_bits;
+};
 template <bool kCount, bool kQuads>
 __global__ void k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count,
                                const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
                                uint32_t blocks, int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop,
-                               uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec);
+                               uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec, EmitCounts dc);
 // Launches count (true) or scatter (false); defined in the sort TU (template instantiation).
 // key_sorted (may be null: no tags) are the depth-sorted keys; a pair's key word is
 // cell | ((key >> tag_drop) << tag_shift) (see k_cell_fixup).
 void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, const uint32_t* key_sorted,
                  uint32_t count, const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
                  int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
-                 uint32_t* pair_rec);
+                 uint32_t* pair_rec, EmitCounts dc);
 constexpr int kStreamItems = 8;  // elements per thread in the streaming sort kernels
 
 // screen-band exchange (multi-GPU frame)

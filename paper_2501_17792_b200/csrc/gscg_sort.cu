@@ -100,8 +100,9 @@ __global__ void __launch_bounds__(kSortThreads)
 k_sort_upsweep(SortPassParams p) {
     pdl_entry();
     __shared__ uint32_t s_hist[kSortWarps][kRadix][32];
-    if ((blockIdx.x + 1) * kSortTile <= p.count) upsweep_tile<true>(p, s_hist);
-    else upsweep_tile<false>(p, s_hist);
+    const SortPassParams q = resolve_pass(p);
+    if ((blockIdx.x + 1) * kSortTile <= q.count) upsweep_tile<true>(q, s_hist);
+    else upsweep_tile<false>(q, s_hist);
 }
 
 // Row scans: CTA d turns digit d's tile counts into exclusive offsets; row total ->
@@ -250,8 +251,9 @@ __global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep(SortPassParams p) {
     pdl_entry();
     __shared__ DownsweepSmem sm;
-    if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_tile<true>(p, sm);
-    else downsweep_tile<false>(p, sm);
+    const SortPassParams q = resolve_pass(p);
+    if ((blockIdx.x + 1) * kSortTile <= q.count) downsweep_tile<true>(q, sm);
+    else downsweep_tile<false>(q, sm);
 }
 
 namespace {
@@ -350,8 +352,9 @@ __global__ void __launch_bounds__(kSortThreads)
 k_sort_upsweep_wide(SortPassParams p) {
     pdl_entry();
     __shared__ uint32_t s_hist[kSortWarps][kWideRadix];
-    if ((blockIdx.x + 1) * kSortTile <= p.count) upsweep_wide_tile<true>(p, s_hist);
-    else upsweep_wide_tile<false>(p, s_hist);
+    const SortPassParams q = resolve_pass(p);
+    if ((blockIdx.x + 1) * kSortTile <= q.count) upsweep_wide_tile<true>(q, s_hist);
+    else upsweep_wide_tile<false>(q, s_hist);
 }
 
 struct DownsweepWideSmem {
@@ -459,15 +462,18 @@ __global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep_wide(SortPassParams p) {
     pdl_entry();
     __shared__ DownsweepWideSmem sm;
-    if ((blockIdx.x + 1) * kSortTile <= p.count) downsweep_wide_tile<true>(p, sm);
-    else downsweep_wide_tile<false>(p, sm);
+    const SortPassParams q = resolve_pass(p);
+    if ((blockIdx.x + 1) * kSortTile <= q.count) downsweep_wide_tile<true>(q, sm);
+    else downsweep_wide_tile<false>(q, sm);
 }
 
 // After the depth sort: every sorted splat's binning span, gathered into sorted order
 // (one 16-byte meta gather per splat, all eight of a thread in flight).
 __global__ void __launch_bounds__(kMetaThreads)
-k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, uint2* span_sorted) {
+k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, const unsigned long long* count_dev,
+               uint2* span_sorted) {
     pdl_entry();
+    count = resolve_count(count, count_dev);
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
     const uint32_t b = (blockIdx.x * kMetaThreads + threadIdx.x) * kStreamItems;
     if (b + kStreamItems <= count) {
@@ -510,9 +516,11 @@ __device__ __forceinline__ unsigned long long pair_order_key(const uint4& m) {  
 }  // namespace
 
 __global__ void __launch_bounds__(256)
-k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count, uint32_t cell_mask, int fix,
-             uint2* ranges, uint2* long_runs, uint32_t* long_count, uint32_t long_cap) {
+k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
+             const unsigned long long* count_dev, uint32_t cell_mask, int fix, uint2* ranges, uint2* long_runs,
+             uint32_t* long_count, uint32_t long_cap) {
     pdl_entry();
+    count = resolve_count(count, count_dev);
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
     constexpr uint32_t kThreads = 256, kTile = kThreads * kStreamItems;
     constexpr uint32_t kHalo = 32;  // pairs past the tile: room for a run leaving the tile
@@ -693,9 +701,10 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
 // ((depth bits, ordinal), record) in shared memory (bitonic, up to kPairRunCap); longer
 // runs are sorted in place in global memory.
 __global__ void __launch_bounds__(256)
-k_pair_long_runs(const uint32_t* keys, uint32_t count, uint32_t* recs, const uint4* meta, const uint2* long_runs,
-                 const uint32_t* long_count) {
+k_pair_long_runs(const uint32_t* keys, uint32_t count, const unsigned long long* count_dev, uint32_t* recs,
+                 const uint4* meta, const uint2* long_runs, const uint32_t* long_count) {
     pdl_entry();
+    count = resolve_count(count, count_dev);
     __shared__ unsigned long long s_key[kPairRunCap];
     __shared__ uint32_t s_rec[kPairRunCap];
     __shared__ uint32_t s_n;
@@ -788,8 +797,12 @@ template <bool kCount, bool kQuads>
 __global__ void __launch_bounds__(kEmitThreads)
 k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count, const uint2* span_sorted,
                uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads,
-               uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec) {
+               uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec,
+               EmitCounts dc) {
     pdl_entry();
+    count = resolve_count(count, dc.count_dev);
+    if (dc.depth_counters)
+        tag_drop = depth_drop(dc.depth_counters->depth_min_bits, dc.depth_counters->depth_max_bits, dc.depth_bits);
     constexpr int kWarps = kEmitThreads / 32, kDigitsPerWarp = kRadix / kWarps, kPerLane = kEmitThreads / 32;
     static_assert(kRadix % kWarps == 0, "digits split evenly over the warps");
     constexpr uint32_t kStage = kEmitStage;            // pairs staged for coalesced writes
@@ -899,7 +912,7 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
 void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, const uint32_t* key_sorted,
                  uint32_t count, const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
                  int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
-                 uint32_t* pair_rec) {
+                 uint32_t* pair_rec, EmitCounts dc) {
     static bool attr = [] {
         cudaFuncSetAttribute(k_emit_scatter<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
         cudaFuncSetAttribute(k_emit_scatter<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
@@ -912,7 +925,7 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
     auto kernel = count_only ? (quads ? k_emit_scatter<true, true> : k_emit_scatter<true, false>)
                              : (quads ? k_emit_scatter<false, true> : k_emit_scatter<false, false>);
     pdl_launch(kernel, blocks, kEmitThreads, smem, s, rec_sorted, key_sorted, count, span_sorted, block_digit, digit_total,
-               blocks, tiles_x, quads, dmask, tag_drop, tag_shift, pair_cell, pair_rec);
+               blocks, tiles_x, quads, dmask, tag_drop, tag_shift, pair_cell, pair_rec, dc);
 }
 
 __global__ void k_iota2(uint32_t* a, uint32_t* b, uint32_t n) {
