@@ -1546,7 +1546,12 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                            : sort_raster(ctx, g.band_tile_row0, g.band_tile_rows, launches, nullptr, nullptr, false,
                                          false, device_counts);
         };
-        const bool deferred = ctx->splat_capacity > 0 && ctx->pair_capacity > 0 && !(ctx->debug & GSCG_DEBUG_POSED);
+        static const bool no_defer = [] {  // GSCG_NO_DEFER=1: read the counters before the sort (A/B runs)
+            const char* e = std::getenv("GSCG_NO_DEFER");
+            return e && e[0] == '1';
+        }();
+        const bool deferred = !no_defer && ctx->splat_capacity > 0 && ctx->pair_capacity > 0 &&
+                              !(ctx->debug & GSCG_DEBUG_POSED);
         uint32_t passes;
         nvtxRangePushA("gscg_render_frame");  // host-side ranges for nsys / ncu --nvtx
         if (deferred) {
