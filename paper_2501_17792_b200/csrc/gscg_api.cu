@@ -191,6 +191,7 @@ struct gscg_ctx {
     uint32_t culled = 0;  // instances dropped by k_inst_cull in the last frame
     uint32_t depth_sort_bits = kDepthSortBits;  // top varying depth bits the splat sort orders
     uint32_t dbits_prev = kDepthSortBits;       // varying depth bits of the last settled frame
+    uint32_t deferred_depth_top = 32;           // key bits a deferred frame's depth plan covers
     cudaEvent_t counters_ev = nullptr;          // the frame's counters are in h_counters
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
@@ -505,7 +506,8 @@ void apply_band(gscg_ctx* ctx) {
 // is final after k_lod_plan), so the frame's end needs no host synchronisation for it.
 void flush_readback(gscg_ctx* ctx);
 
-bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool lod_back, bool flush = true);
+bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool lod_back, bool flush = true,
+                   bool deferred_check = false);
 
 // deferred: return right after enqueueing (no host read of the counters); the caller
 // enqueues the sort on device counts and then calls settle_counts.
@@ -853,7 +855,8 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
 // the frame's S / K / G / depth range, the LoD write-back of host frames. Returns false,
 // with the capacities grown, when the frame's splats or pairs did not fit (its records were
 // clamped and it must be rendered again).
-bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool lod_back, bool flush) {
+bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool lod_back, bool flush,
+                   bool deferred_check) {
     CUDA_TRY(cudaEventSynchronize(ctx->counters_ev));
     if (flush) flush_readback(ctx);  // the previous pipelined frame's read-back overlaps this frame's sort
     const FrameCounters& c = *ctx->h_counters;
@@ -864,6 +867,9 @@ bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool
     if (c.gaussians > 0xffffffffull) throw Status(GSCG_ERR_OOM, "instance-Gaussian count exceeds 32-bit ordinals");
     if (S > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "splat count exceeds 32-bit indexing");
     if (K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "tile-splat pair count exceeds 32-bit indexing");
+    const uint32_t dbits = static_cast<uint32_t>(bits_for(c.depth_min_bits ^ c.depth_max_bits));
+    ctx->dbits_prev = dbits;
+    if (deferred_check && dbits > ctx->deferred_depth_top) return false;  // the plan missed high key bits
     if (S > ctx->splat_capacity || K > ctx->pair_capacity) {
         ctx->splat_capacity = std::max<uint64_t>(ctx->splat_capacity, S + S / 4 + 1024);
         ctx->pair_capacity = std::max<uint64_t>(ctx->pair_capacity, K + K / 4 + 1024);
@@ -877,7 +883,6 @@ bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool
     ctx->dmin = c.depth_min_bits;
     ctx->dmax = c.depth_max_bits;
     ctx->culled = c.instances_culled;
-    ctx->dbits_prev = static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax));
     return true;
 }
 
@@ -888,11 +893,9 @@ bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool
 // ping-pong buffers kb/vb; returns the buffer index holding the result. in_keys/in_vals
 // feed pass 0 (vals may be null = identity). ctx->status / ctx->hist must fit `count`.
 // count_dev (may be null): the pass count is min(count, *count_dev) on the device, count
-// then being the capacity the grid covers; depth_counters (may be null): every shift is
-// moved up by the frame's depth_drop over depth_bits (depth sort of a deferred frame).
+// then being the capacity the grid covers (deferred frames).
 int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb,
-              uint32_t count, const RadixPlan& plan, uint32_t& launches, const unsigned long long* count_dev = nullptr,
-              const FrameCounters* depth_counters = nullptr, uint32_t depth_bits = 0) {
+              uint32_t count, const RadixPlan& plan, uint32_t& launches, const unsigned long long* count_dev = nullptr) {
     cudaStream_t s = ctx->stream;
     const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
     int out = 0;
@@ -909,8 +912,6 @@ int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, D
         sp.counts = ctx->status.as<uint32_t>();
         sp.digit_base = ctx->hist.as<uint32_t>();
         sp.count_dev = count_dev;
-        sp.depth_counters = depth_counters;
-        sp.depth_bits = depth_bits;
         const bool wide = (plan.wide >> q) & 1u;
         if (wide) CUDA_TRY(pdl_launch(k_sort_upsweep_wide, tiles, kSortThreads, 0, s, sp));
         else CUDA_TRY(pdl_launch(k_sort_upsweep, tiles, kSortThreads, 0, s, sp));
@@ -1033,27 +1034,22 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         ensure_sort_buffers(ctx, S32, K);
         // 1. splats by the top (at most kDepthSortBits) varying bits of their depth keys;
         //    the dropped low bits and the ordinal tie-break are settled per cell in step 4.
-        // Deferred: the plan's width comes from the last settled frame's depth range (the
-        // drop of this frame's is resolved on the device; any width is exact, the fix-up
-        // orders what it leaves tied).
-        const uint32_t dbits = device_counts ? std::max(ctx->dbits_prev, 1u)
+        // Deferred frames plan on the last settled frame's depth range plus one bit of
+        // headroom (settle_counts re-renders a frame whose range outgrew it): the plan covers
+        // key bits [drop, top); any drop is exact, the fix-up orders what it leaves tied.
+        const uint32_t dbits = device_counts ? std::min(ctx->dbits_prev + 1u, 32u)
                                              : static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax));
-        const uint32_t drop = device_counts ? 0u : (dbits > ctx->depth_sort_bits ? dbits - ctx->depth_sort_bits : 0u);
+        const uint32_t drop = dbits > ctx->depth_sort_bits ? dbits - ctx->depth_sort_bits : 0u;
+        if (device_counts) ctx->deferred_depth_top = dbits;
         RadixPlan dplan{};
-        uint32_t plan_bits = 0;
         if (!presorted) {
-            if (device_counts) {
-                dplan = make_plan(std::min(dbits, ctx->depth_sort_bits));  // shifts += the device drop
-            } else {
-                dplan = make_plan(dbits - drop);
-                for (uint32_t q = 0; q < dplan.passes; ++q) dplan.shift[q] += drop;
-            }
-            for (uint32_t q = 0; q < dplan.passes; ++q) plan_bits += dplan.bits[q];
+            dplan = make_plan(dbits - drop);
+            for (uint32_t q = 0; q < dplan.passes; ++q) dplan.shift[q] += drop;
         }
         const int sb = presorted ? 0
                                  : run_radix(ctx, ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32,
-                                             dplan, launches, s_dev, device_counts ? dcnt : nullptr, plan_bits);
-        const EmitCounts ec{s_dev, device_counts ? dcnt : nullptr, plan_bits};
+                                             dplan, launches, s_dev);
+        const EmitCounts ec{s_dev};
         // 2. cell spans in sorted order; the first cell-sort digit histogram per emission
         //    block; digit offsets; pairs emitted straight into the order of the first stable
         //    cell-sort pass, each key word tagged with its splat's truncated depth.
@@ -1558,7 +1554,7 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
             update_gather(ctx, frame, cam, lod, 0, n, launches, host, true);
             passes = enqueue_sort(true);
             nvtxRangePushA("settle_counts");
-            const bool fits = settle_counts(ctx, frame, n, host, false);
+            const bool fits = settle_counts(ctx, frame, n, host, false, true);
             nvtxRangePop();
             if (!fits) {
                 nvtxRangePushA("re-render (capacity grown)");

@@ -193,38 +193,15 @@ struct SortPassParams {
     uint32_t tiles;      // ceil(count / kSortTile)
     uint32_t* counts;      // kRadix x tiles, digit-major: tile digit counts -> exclusive offsets
     uint32_t* digit_base;  // kRadix: row totals (scanned by each downsweep CTA)
-    // Device-resolved pass (frames enqueued without a host read of the counters): count =
-    // min(count, *count_dev) (count, tiles: the capacity the grid was sized for), and for a
-    // depth pass shift += depth_drop(*depth_counters, depth_bits).
+    // Deferred frames (enqueued before the host reads the counters): the pass count is
+    // min(count, *count_dev), count and tiles then being the capacity the grid covers.
     const unsigned long long* count_dev;
-    const FrameCounters* depth_counters;
-    uint32_t depth_bits;
 };
-
-// Low depth-key bits a depth sort over `depth_bits` bits drops for the frame's depth range
-// (the per-cell fix-up orders what they leave tied).
-__host__ __device__ __forceinline__ uint32_t depth_drop(uint32_t dmin, uint32_t dmax, uint32_t depth_bits) {
-    const uint32_t x = dmin ^ dmax;
-#ifdef __CUDA_ARCH__
-    const uint32_t dbits = x ? 32u - __clz(x) : 0u;
-#else
-    const uint32_t dbits = x ? 32u - static_cast<uint32_t>(__builtin_clz(x)) : 0u;
-#endif
-    return dbits > depth_bits ? dbits - depth_bits : 0u;
-}
 
 __device__ __forceinline__ uint32_t resolve_count(uint32_t cap, const unsigned long long* count_dev) {
     if (!count_dev) return cap;
     const unsigned long long c = *count_dev;
     return c < cap ? static_cast<uint32_t>(c) : cap;
-}
-
-__device__ __forceinline__ SortPassParams resolve_pass(const SortPassParams& p) {
-    SortPassParams q = p;
-    q.count = resolve_count(p.count, p.count_dev);
-    if (p.depth_counters)
-        q.shift = p.shift + depth_drop(p.depth_counters->depth_min_bits, p.depth_counters->depth_max_bits, p.depth_bits);
-    return q;
 }
 
 __global__ void k_sort_upsweep(SortPassParams p);
@@ -251,10 +228,8 @@ constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
 constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
 constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes
 constexpr int kEmitSmem = (32 * kEmitThreads + 2 * kEmitStage) * 4;  // dynamic shared bytes
-struct EmitCounts {  // device-resolved emission (null: the host values)
+struct EmitCounts {  // deferred frames: the splat count from the device counter (null: the host's)
     const unsigned long long* count_dev;
-    const FrameCounters* depth_counters;  // tag_drop = depth_drop(..., depth_bits)
-    uint32_t depth_bits;
 };
 template <bool kCount, bool kQuads>
 __global__ void k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count,

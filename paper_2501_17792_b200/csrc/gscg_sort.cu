@@ -58,10 +58,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 
 }  // namespace
 
-// Upsweep: per-tile digit counts, written digit-major (counts[d * tiles + t]). kFull: the
+// Upsweep: per-tile digit counts, written digit-major (p.counts[d * tiles + t]). kFull: the
 // tile holds kSortTile keys (every tile but the last), so no bounds predicates.
 template <bool kFull>
-__device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (*s_hist)[kRadix][32]) {
+__device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (*s_hist)[kRadix][32], uint32_t count) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t base = blockIdx.x * kSortTile;
     const uint32_t mask = (1u << p.bits) - 1u;
@@ -69,7 +69,7 @@ __device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {  // all loads in flight first
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < count) ? p.keys_in[idx] : 0u;
     }
     // Lane-private digit counters s_hist[warp][d][lane] (lane L's column sits in bank L:
     // no conflicts), then lane d sums row d along a rotated walk (conflict-free too).
@@ -79,7 +79,7 @@ __device__ __forceinline__ void upsweep_tile(const SortPassParams& p, uint32_t (
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        if (kFull || idx < p.count) ++h[(k[j] >> p.shift) & mask][lane];
+        if (kFull || idx < count) ++h[(k[j] >> p.shift) & mask][lane];
     }
     __syncwarp();
     uint32_t cnt = 0;
@@ -100,9 +100,15 @@ __global__ void __launch_bounds__(kSortThreads)
 k_sort_upsweep(SortPassParams p) {
     pdl_entry();
     __shared__ uint32_t s_hist[kSortWarps][kRadix][32];
-    const SortPassParams q = resolve_pass(p);
-    if ((blockIdx.x + 1) * kSortTile <= q.count) upsweep_tile<true>(q, s_hist);
-    else upsweep_tile<false>(q, s_hist);
+    // count: the host's, or the device counter clamped to it (deferred frames); only the
+    // partial (last) tile needs it, so the full-tile path keeps its registers.
+    const uint32_t count = resolve_count(p.count, p.count_dev);
+    if (blockIdx.x * kSortTile >= count) {  // past the device count (deferred frames): zero counts only
+        if (threadIdx.x < kRadix) p.counts[threadIdx.x * p.tiles + blockIdx.x] = 0u;
+        return;
+    }
+    if ((blockIdx.x + 1) * kSortTile <= count) upsweep_tile<true>(p, s_hist, kSortTile);
+    else upsweep_tile<false>(p, s_hist, count);
 }
 
 // Row scans: CTA d turns digit d's tile counts into exclusive offsets; row total ->
@@ -139,7 +145,7 @@ k_sort_rows(SortPassParams p) {
 // Downsweep: stable rank inside the tile with a register-only warp multisplit (five
 // ballots give each key the lanes sharing its digit; lane d keeps the warp's running
 // count of digit d), stage the tile in shared memory in digit order, write it out
-// coalesced at digit_base[d] + counts[d][tile] + rank-within-digit.
+// coalesced at digit_base[d] + p.counts[d][tile] + rank-within-digit.
 struct DownsweepSmem {
     uint32_t keys[kSortTile];
     uint16_t perm[kSortTile];  // tile-local source index of each staged key
@@ -149,7 +155,7 @@ struct DownsweepSmem {
 };
 
 template <bool kFull>
-__device__ __forceinline__ void downsweep_tile(const SortPassParams& p, DownsweepSmem& sm) {
+__device__ __forceinline__ void downsweep_tile(const SortPassParams& p, DownsweepSmem& sm, uint32_t count) {
     uint32_t* s_keys = sm.keys;
     uint16_t* s_perm = sm.perm;
     auto s_woff = sm.woff;
@@ -169,7 +175,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < count) ? p.keys_in[idx] : 0u;
     }
     uint32_t lane_mask[kRadixBits];  // all-ones where lane's bit b is set
 #pragma unroll
@@ -179,7 +185,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
-        const uint32_t vm = kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count);
+        const uint32_t vm = kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < count);
         // Lane L's ballots give the lanes holding digit L; a key's own digit group is that
         // mask fetched from lane d (one shuffle instead of five more mask chains).
         uint32_t mine_differ = 0u;
@@ -210,7 +216,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
-        if (kFull || base + local < p.count) {
+        if (kFull || base + local < count) {
             const uint32_t d = (k[j] >> p.shift) & mask;
             const uint32_t pos = s_woff[warp][d] + ((j & 1) ? (rank2[j / 2] >> 16) : (rank2[j / 2] & 0xffffu));
             s_keys[pos] = k[j];
@@ -220,7 +226,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
     __syncthreads();
     // Write-out: every gather of the thread issued before any store (the value gathers
     // stay inside this tile's 16 KB input window, so they hit L2).
-    const uint32_t n_here = kFull ? kSortTile : (p.count > base ? min(kSortTile, p.count - base) : 0u);
+    const uint32_t n_here = kFull ? kSortTile : (count > base ? min(kSortTile, count - base) : 0u);
     const uint32_t* __restrict__ vals_in = p.vals_in;
     constexpr int kHalf = kSortItems / 2;  // two rounds: half the live registers
 #pragma unroll
@@ -251,9 +257,12 @@ __global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep(SortPassParams p) {
     pdl_entry();
     __shared__ DownsweepSmem sm;
-    const SortPassParams q = resolve_pass(p);
-    if ((blockIdx.x + 1) * kSortTile <= q.count) downsweep_tile<true>(q, sm);
-    else downsweep_tile<false>(q, sm);
+    // count: the host's, or the device counter clamped to it (deferred frames); only the
+    // partial (last) tile needs it, so the full-tile path keeps its registers.
+    const uint32_t count = resolve_count(p.count, p.count_dev);
+    if (blockIdx.x * kSortTile >= count) return;  // past the device count (deferred frames)
+    if ((blockIdx.x + 1) * kSortTile <= count) downsweep_tile<true>(p, sm, kSortTile);
+    else downsweep_tile<false>(p, sm, count);
 }
 
 namespace {
@@ -318,7 +327,7 @@ __device__ __forceinline__ uint32_t scan128(uint32_t v, uint32_t* s_tmp) {
 }  // namespace
 
 template <bool kFull>
-__device__ __forceinline__ void upsweep_wide_tile(const SortPassParams& p, uint32_t (*s_hist)[kWideRadix]) {
+__device__ __forceinline__ void upsweep_wide_tile(const SortPassParams& p, uint32_t (*s_hist)[kWideRadix], uint32_t count) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kWideRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0u;
     const uint32_t base = blockIdx.x * kSortTile;
@@ -328,15 +337,15 @@ __device__ __forceinline__ void upsweep_wide_tile(const SortPassParams& p, uint3
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < count) ? p.keys_in[idx] : 0u;
     }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
-        const uint32_t peers = peers_of(d, bits, kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count));
-        if ((kFull || idx < p.count) && lane == 31 - __clz(peers)) s_hist[warp][d] += __popc(peers);
+        const uint32_t peers = peers_of(d, bits, kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < count));
+        if ((kFull || idx < count) && lane == 31 - __clz(peers)) s_hist[warp][d] += __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -352,9 +361,15 @@ __global__ void __launch_bounds__(kSortThreads)
 k_sort_upsweep_wide(SortPassParams p) {
     pdl_entry();
     __shared__ uint32_t s_hist[kSortWarps][kWideRadix];
-    const SortPassParams q = resolve_pass(p);
-    if ((blockIdx.x + 1) * kSortTile <= q.count) upsweep_wide_tile<true>(q, s_hist);
-    else upsweep_wide_tile<false>(q, s_hist);
+    // count: the host's, or the device counter clamped to it (deferred frames); only the
+    // partial (last) tile needs it, so the full-tile path keeps its registers.
+    const uint32_t count = resolve_count(p.count, p.count_dev);
+    if (blockIdx.x * kSortTile >= count) {  // past the device count (deferred frames): zero counts only
+        if (threadIdx.x < kWideRadix) p.counts[threadIdx.x * p.tiles + blockIdx.x] = 0u;
+        return;
+    }
+    if ((blockIdx.x + 1) * kSortTile <= count) upsweep_wide_tile<true>(p, s_hist, kSortTile);
+    else upsweep_wide_tile<false>(p, s_hist, count);
 }
 
 struct DownsweepWideSmem {
@@ -367,7 +382,7 @@ struct DownsweepWideSmem {
 };
 
 template <bool kFull>
-__device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, DownsweepWideSmem& sm) {
+__device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, DownsweepWideSmem& sm, uint32_t count) {
     uint32_t* s_keys = sm.keys;
     uint16_t* s_perm = sm.perm;
     auto s_woff = sm.woff;
@@ -385,7 +400,7 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
-        k[j] = (kFull || idx < p.count) ? p.keys_in[idx] : 0u;
+        k[j] = (kFull || idx < count) ? p.keys_in[idx] : 0u;
     }
     {  // global digit base (exclusive scan of the row totals) + this tile's offset
         const uint32_t total = tid < kWideRadix && static_cast<uint32_t>(tid) <= mask ? p.digit_base[tid] : 0u;
@@ -398,12 +413,12 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t idx = base + warp * (32 * kSortItems) + j * 32 + lane;
         const uint32_t d = (k[j] >> p.shift) & mask;
-        const uint32_t peers = peers_of(d, bits, kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < p.count));
+        const uint32_t peers = peers_of(d, bits, kFull ? 0xffffffffu : __ballot_sync(0xffffffffu, idx < count));
         const uint32_t before = wcnt[d];
         const uint32_t r = before + __popc(peers & lt);
         rank2[j / 2] = (j & 1) ? (rank2[j / 2] | (r << 16)) : r;
         __syncwarp();
-        if ((kFull || idx < p.count) && lane == 31 - __clz(peers)) wcnt[d] = before + __popc(peers);
+        if ((kFull || idx < count) && lane == 31 - __clz(peers)) wcnt[d] = before + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -422,7 +437,7 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint32_t local = warp * (32 * kSortItems) + j * 32 + lane;
-        if (kFull || base + local < p.count) {
+        if (kFull || base + local < count) {
             const uint32_t d = (k[j] >> p.shift) & mask;
             const uint32_t pos = s_block_excl[d] + s_woff[warp][d] + ((j & 1) ? (rank2[j / 2] >> 16) : (rank2[j / 2] & 0xffffu));
             s_keys[pos] = k[j];
@@ -430,7 +445,7 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
         }
     }
     __syncthreads();
-    const uint32_t n_here = kFull ? kSortTile : (p.count > base ? min(kSortTile, p.count - base) : 0u);
+    const uint32_t n_here = kFull ? kSortTile : (count > base ? min(kSortTile, count - base) : 0u);
     const uint32_t* __restrict__ vals_in = p.vals_in;
     constexpr int kHalf = kSortItems / 2;  // two rounds: half the live registers
 #pragma unroll
@@ -462,9 +477,12 @@ __global__ void __launch_bounds__(kSortThreads, 4)
 k_sort_downsweep_wide(SortPassParams p) {
     pdl_entry();
     __shared__ DownsweepWideSmem sm;
-    const SortPassParams q = resolve_pass(p);
-    if ((blockIdx.x + 1) * kSortTile <= q.count) downsweep_wide_tile<true>(q, sm);
-    else downsweep_wide_tile<false>(q, sm);
+    // count: the host's, or the device counter clamped to it (deferred frames); only the
+    // partial (last) tile needs it, so the full-tile path keeps its registers.
+    const uint32_t count = resolve_count(p.count, p.count_dev);
+    if (blockIdx.x * kSortTile >= count) return;  // past the device count (deferred frames)
+    if ((blockIdx.x + 1) * kSortTile <= count) downsweep_wide_tile<true>(p, sm, kSortTile);
+    else downsweep_wide_tile<false>(p, sm, count);
 }
 
 // After the depth sort: every sorted splat's binning span, gathered into sorted order
@@ -801,8 +819,11 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
                EmitCounts dc) {
     pdl_entry();
     count = resolve_count(count, dc.count_dev);
-    if (dc.depth_counters)
-        tag_drop = depth_drop(dc.depth_counters->depth_min_bits, dc.depth_counters->depth_max_bits, dc.depth_bits);
+    if (blockIdx.x * kEmitSplats >= count) {  // past the device count (deferred frames)
+        if (kCount && static_cast<uint32_t>(threadIdx.x) <= dmask && threadIdx.x < kRadix)
+            block_digit[threadIdx.x * blocks + blockIdx.x] = 0u;
+        return;
+    }
     constexpr int kWarps = kEmitThreads / 32, kDigitsPerWarp = kRadix / kWarps, kPerLane = kEmitThreads / 32;
     static_assert(kRadix % kWarps == 0, "digits split evenly over the warps");
     constexpr uint32_t kStage = kEmitStage;            // pairs staged for coalesced writes

@@ -7,4 +7,3 @@ GSCG_NO_DEFER=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv 
 python scripts/launch_table.py gpurun_out/${T}_nodefer.csv > gpurun_out/${T}_nodefer.txt 2>&1
 python bench.py --no-cpu-baseline > gpurun_out/${T}_bench_defer.log 2>&1
 GSCG_NO_DEFER=1 python bench.py --no-cpu-baseline > gpurun_out/${T}_bench_nodefer.log 2>&1
-TAG=${T} bash scripts/sanitize.sh
