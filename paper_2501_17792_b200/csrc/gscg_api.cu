@@ -36,12 +36,20 @@
 
 using namespace gscg;
 
+// PDL is used for frames of up to kPdlMaxSplats splats (the previous frame's count): there
+// the frame is a chain of short kernels and overlapping their launch with the previous
+// kernel's tail is worth 10% (config 1, region frames); on the big frames the sort is
+// launched from the host after the counters read and the PDL launch path measured ~1%
+// slower.
+constexpr uint64_t kPdlMaxSplats = 4000000;
+thread_local bool t_pdl_frame = true;
+
 bool gscg::pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("GSCG_NO_PDL");
         return !(e && e[0] == '1');
     }();
-    return on;
+    return on && t_pdl_frame;
 }
 
 namespace {
@@ -1542,12 +1550,15 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                            : sort_raster(ctx, g.band_tile_row0, g.band_tile_rows, launches, nullptr, nullptr, false,
                                          false, device_counts);
         };
-        static const bool no_defer = [] {  // GSCG_NO_DEFER=1: read the counters before the sort (A/B runs)
-            const char* e = std::getenv("GSCG_NO_DEFER");
+        // Deferred frames are opt-in (GSCG_DEFER=1): measured neutral on the device and 6-10%
+        // slower end to end at configs 1-3 (capacity-sized grids).
+        static const bool defer = [] {
+            const char* e = std::getenv("GSCG_DEFER");
             return e && e[0] == '1';
         }();
-        const bool deferred = !no_defer && ctx->splat_capacity > 0 && ctx->pair_capacity > 0 &&
+        const bool deferred = defer && ctx->splat_capacity > 0 && ctx->pair_capacity > 0 &&
                               !(ctx->debug & GSCG_DEBUG_POSED);
+        t_pdl_frame = ctx->S < kPdlMaxSplats;
         uint32_t passes;
         nvtxRangePushA("gscg_render_frame");  // host-side ranges for nsys / ncu --nvtx
         if (deferred) {

@@ -504,10 +504,18 @@ class BandGroup:
         return out
 
     def rebalance(self) -> list[int]:
-        """New cuts from the last frame's pairs per tile over all ranks, summed along the
-        split axis (plus a small per-line floor for the fixed per-pixel cost)."""
-        costs = self.tile_costs().astype(np.float64)
-        line = costs.sum(0) if self.axis == "cols" else costs.sum(1)
-        if line.sum() > 0:
-            self.cuts = band_rows(self.extent, self.tile, self.world, line + 0.02 * line.mean() + 1.0)
+        """New cuts from the last frame's pairs per tile over all ranks (every rank gets the
+        same all-reduced map, so every rank derives the same cuts)."""
+        self.cuts = cuts_from_tile_costs(self.tile_costs(), self.axis, self.extent, self.tile, self.world, self.cuts)
         return self.cuts
+
+
+def cuts_from_tile_costs(costs: np.ndarray, axis: str, extent: int, tile: int, parts: int,
+                         fallback: Optional[Sequence[int]] = None) -> list[int]:
+    """Region cuts along `axis` ("cols" / "rows") balancing the binned pairs per tile line
+    (tiles_y x tiles_x map), plus a small per-line floor for the fixed per-pixel cost."""
+    c = np.asarray(costs, dtype=np.float64)
+    line = c.sum(0) if axis == "cols" else c.sum(1)
+    if line.sum() <= 0:
+        return list(fallback) if fallback is not None else band_rows(extent, tile, parts)
+    return band_rows(extent, tile, parts, line + 0.02 * line.mean() + 1.0)

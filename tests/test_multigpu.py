@@ -251,3 +251,75 @@ def test_distributed_renderer_nccl_world1():
         assert out2[0].tobytes() == rgb0.tobytes()
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- region split (BandGroup)
+
+def _region_worker(rank: int, world: int, port: int, result_dir: str):
+    """One rank of the column-split frame on CPU (gloo): the NCCL unique id plumbing, the
+    all-reduced tile-cost map, identical cuts on every rank, and rank 0 assembling the
+    frame from every rank's column region (as gscg_group_render_frame gathers them)."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import orc
+    from paper_2501_17792_b200.multigpu import broadcast_unique_id, cuts_from_tile_costs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        uid = broadcast_unique_id(rank, world, dist)
+        ids = [None] * world
+        dist.all_gather_object(ids, uid)
+        assert len(uid) == 128 and all(i == uid for i in ids), "ranks disagree on the unique id"
+        scene = _small_scene()
+        o = orc.from_scene(scene)
+        rgb, T, _ = o.render(0.41, orc.settings(tile_size=16, sh_colour=True))
+        W, H = scene.cfg.width, scene.cfg.height
+        tx, ty = (W + 15) // 16, (H + 15) // 16
+        counts, _ = o.bins(tx * ty)
+        # first frame: even cuts; each rank contributes the tile costs of its own region
+        cuts = cuts_from_tile_costs(np.zeros((ty, tx)), "cols", W, 16, world)
+        mine = np.zeros((ty, tx), np.float64)
+        c0, c1 = cuts[rank] // 16, (cuts[rank + 1] + 15) // 16
+        mine[:, c0:c1] = counts.reshape(ty, tx)[:, c0:c1]
+        t = torch.from_numpy(mine)
+        dist.all_reduce(t)
+        assert np.array_equal(t.numpy(), counts.reshape(ty, tx).astype(np.float64))
+        cuts = cuts_from_tile_costs(t.numpy(), "cols", W, 16, world, cuts)
+        all_cuts = [None] * world
+        dist.all_gather_object(all_cuts, cuts)
+        assert all(c == cuts for c in all_cuts), "ranks derived different cuts"
+        assert cuts[0] == 0 and cuts[-1] == W and all(c % 16 == 0 for c in cuts[1:-1])
+        # the gather: every rank's column region, assembled on rank 0
+        region = torch.from_numpy(np.ascontiguousarray(np.concatenate([rgb, T[..., None]], axis=2)[:, cuts[rank]:cuts[rank + 1]]))
+        parts = [None] * world
+        dist.gather_object(region.numpy(), parts if rank == 0 else None, dst=0)
+        if rank == 0:
+            full = np.concatenate(parts, axis=1)
+            assert full[..., :3].tobytes() == rgb.tobytes() and full[..., 3].tobytes() == T.tobytes()
+        with open(os.path.join(result_dir, f"ok{rank}"), "w") as f:
+            f.write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_region_split_world2(tmp_path):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_region_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    assert (tmp_path / "ok0").exists() and (tmp_path / "ok1").exists()
+
+
+def test_cuts_from_tile_costs_balance_columns():
+    from paper_2501_17792_b200.multigpu import cuts_from_tile_costs
+
+    costs = np.zeros((68, 120))
+    costs[30:34, :] = 100.0        # a horizon row: spread across every column
+    costs[:, 50:60] += 20.0        # a near character: a few columns
+    for parts in (2, 4, 8):
+        cuts = cuts_from_tile_costs(costs, "cols", 1920, 16, parts)
+        assert cuts[0] == 0 and cuts[-1] == 1920 and all(cuts[i] < cuts[i + 1] for i in range(parts))
+        load = [costs[:, cuts[i] // 16:cuts[i + 1] // 16].sum() for i in range(parts)]
+        assert max(load) < 1.6 * costs.sum() / parts
