@@ -107,43 +107,6 @@ __device__ __forceinline__ uint32_t block_cover(float4 r2, int bx0, int by0) {
     return (row * 0x01010101u) & rows;
 }
 
-// The 8x4-pixel coverage bits of a splat restricted to its cutoff ellipse: a pixel can pass
-// the raster's test power >= power_floor only if a dx^2 + 2 b dx dy + c dy^2 <= -2 pf
-// (conic a, b, c; renderer.cpp:199-204), so for each block row the x extent is the
-// quadratic's root interval. Conservative by construction: a row is dropped only when its
-// discriminant is below -tol (1e-3 of its terms' magnitude), the interval is widened by a
-// pixel each side, and NaN anywhere keeps the rect's bits; every pixel kept is still
-// decided by the exact per-pixel test, so the contributing pairs are unchanged. At config
-// 3, 38% of the rect-covered evaluations before saturation fail the cutoff.
-__device__ __forceinline__ uint32_t ellipse_cover(float4 g, float4 c, float4 r2, int bx0, int by0) {
-    const uint32_t rect = block_cover(r2, bx0, by0);
-    if (!rect) return 0u;
-    const float a = g.z, b = g.w, cq = c.x, rhs = -2.0f * c.z;  // rhs = -2 power_floor >= 0
-    uint32_t out = 0u;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const uint32_t row = (rect >> (8 * r)) & 0xffu;
-        if (!row) continue;
-        const float dy = (static_cast<float>(by0 + r) + 0.5f) - g.y;
-        const float bdy = b * dy;
-        const float cdy = cq * dy * dy;
-        const float D = bdy * bdy - a * (cdy - rhs);
-        const float tol = 1e-3f * (bdy * bdy + a * (fabsf(cdy) + rhs + 1.0f));
-        if (D < -tol) continue;  // the row misses the ellipse (NaN falls through: kept)
-        const float hw = sqrtf(fmaxf(D, 0.0f) + tol) / a + 1.0f;  // half-width + a pixel
-        const float xc = g.x - bdy / a;
-        const float lo = floorf(xc - hw) - static_cast<float>(bx0), hi = ceilf(xc + hw) - static_cast<float>(bx0);
-        uint32_t m = 0xffu;
-        if (lo <= hi) {  // false for NaN: keep the whole row
-            const int l = static_cast<int>(fminf(fmaxf(lo, 0.0f), 8.0f));
-            const int h = static_cast<int>(fminf(fmaxf(hi, -1.0f), 7.0f));
-            m = h >= l ? (((2u << h) - 1u) & ~((1u << l) - 1u)) : 0u;
-        }
-        out |= (row & m) << (8 * r);
-    }
-    return out;
-}
-
 // Warp bit-matrix transpose: lane L receives bit L of every lane's word, in lane order.
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 #pragma unroll
@@ -222,9 +185,8 @@ k_raster16q(RasterParams p) {
         const float4* ext = s_ext[warp][buf];
         const int n = static_cast<int>(min(static_cast<uint32_t>(kStage), range.y - start));
         static_assert(CH == 2, "two explicit chunk words (a dynamically indexed array spills)");
-        uint32_t todo0 = transpose32(lane < n ? ellipse_cover(geo[lane], col[lane], ext[lane], bx0, by0) : 0u, lane);
-        uint32_t todo1 =
-            transpose32(32 + lane < n ? ellipse_cover(geo[32 + lane], col[32 + lane], ext[32 + lane], bx0, by0) : 0u, lane);
+        uint32_t todo0 = transpose32(lane < n ? block_cover(ext[lane], bx0, by0) : 0u, lane);
+        uint32_t todo1 = transpose32(32 + lane < n ? block_cover(ext[32 + lane], bx0, by0) : 0u, lane);
         if (done) todo0 = todo1 = 0u;
         while (__any_sync(0xffffffffu, (todo0 | todo1) != 0u)) {
             if ((todo0 | todo1) == 0u) continue;
