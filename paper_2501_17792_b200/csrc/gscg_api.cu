@@ -1658,7 +1658,6 @@ int gscg_project_shard(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_c
         bp.count = static_cast<uint32_t>(ctx->S);
         bp.bands = bands;
         for (uint32_t b = 0; b <= bands; ++b) bp.rows[b] = band_rows[b];
-        bp.cell = geo.cell;
         CUDA_TRY(ctx->band_scratch.ensure(2 * kMaxBands * sizeof(unsigned long long)));
         bp.band_counts = ctx->band_scratch.as<unsigned long long>();
         bp.band_cursor = bp.band_counts + kMaxBands;

@@ -30,14 +30,10 @@ __device__ __forceinline__ void band_range(const BandParams& p, uint32_t y0, uin
     b1 = b - 1;
 }
 
-// Pixel rows of a splat's binning cells (its full-frame span in splat_meta). The
-// record's rect is the raster rect (cut to the cutoff ellipse), so band routing uses the
-// 3-sigma span; bands start on tile rows, multiples of the cell, so a cell span meets a
-// band exactly when the 3-sigma rect does.
-__device__ __forceinline__ void splat_rows(const BandParams& p, uint32_t i, uint32_t& y0, uint32_t& y1) {
-    const uint4 m = p.meta[i];
-    y0 = (m.y >> 16) * static_cast<uint32_t>(p.cell);
-    y1 = y0 + (m.z >> 16) * static_cast<uint32_t>(p.cell);
+__device__ __forceinline__ void splat_rows(const float4* records, uint32_t i, uint32_t& y0, uint32_t& y1) {
+    const float4 r2 = records[3ull * i + 2];
+    y0 = __float_as_uint(r2.z) >> 16;
+    y1 = __float_as_uint(r2.w) >> 16;
 }
 
 }  // namespace
@@ -53,7 +49,7 @@ k_band_count(BandParams p) {
         const uint32_t i = base + k * 256u + threadIdx.x;
         if (i >= p.count) break;
         uint32_t y0, y1;
-        splat_rows(p, i, y0, y1);
+        splat_rows(p.records, i, y0, y1);
         int b0, b1;
         band_range(p, y0, y1, b0, b1);
         for (int b = b0; b <= b1; ++b) atomicAdd(&s_cnt[b], 1u);
@@ -78,7 +74,7 @@ k_band_pack(BandParams p) {
         b1s[k] = -1;
         if (i < p.count) {
             uint32_t y0, y1;
-            splat_rows(p, i, y0, y1);
+            splat_rows(p.records, i, y0, y1);
             band_range(p, y0, y1, b0s[k], b1s[k]);
             for (int b = b0s[k]; b <= b1s[k]; ++b) atomicAdd(&s_cnt[b], 1u);
         }
@@ -97,7 +93,7 @@ k_band_pack(BandParams p) {
         if (b1s[k] < b0s[k]) continue;
         const float4* src = p.records + 3ull * i;
         const float4 r0 = src[0], r1 = src[1], r2 = src[2];
-        const uint4 meta = make_uint4(p.meta[i].x, p.depth[i], p.meta[i].y, p.meta[i].z);
+        const uint4 meta = make_uint4(p.meta[i].x, p.depth[i], 0u, 0u);
         for (int b = b0s[k]; b <= b1s[k]; ++b) {
             const unsigned long long slot = s_base[b] + atomicAdd(&s_cnt[b], 1u);
             float4* dst = reinterpret_cast<float4*>(p.packed + 4ull * slot);
@@ -134,13 +130,14 @@ k_band_unpack(BandUnpackParams p) {
         dst[1] = r1;
         dst[2] = r2;
         p.depth[i] = meta.y;
-        // Binning span clipped to the band (full-frame cell span in meta.z/w), cell rows
-        // relative to the band.
-        const int cx0 = static_cast<int>(meta.z & 0xffffu);
-        const uint32_t across = meta.w & 0xffffu;
-        const int c0 = static_cast<int>(meta.z >> 16), c1 = c0 + static_cast<int>(meta.w >> 16) - 1;
-        const int cy0 = max(c0, p.row_begin / p.cell), cy1 = min(c1, (p.row_end - 1) / p.cell);
-        const uint32_t down = static_cast<uint32_t>(cy1 - cy0 + 1);
+        const uint32_t xy0 = __float_as_uint(r2.z), xy1 = __float_as_uint(r2.w);
+        const int x0 = static_cast<int>(xy0 & 0xffffu), y0 = static_cast<int>(xy0 >> 16);
+        const int x1 = static_cast<int>(xy1 & 0xffffu), y1 = static_cast<int>(xy1 >> 16);
+        // Binning span of the rect clipped to the band, cell rows relative to the band.
+        const int yc0 = max(y0, p.row_begin), yc1 = min(y1, p.row_end);
+        const int cx0 = x0 / p.cell, cy0 = yc0 / p.cell;
+        const uint32_t across = static_cast<uint32_t>((x1 - 1) / p.cell - cx0 + 1);
+        const uint32_t down = static_cast<uint32_t>((yc1 - 1) / p.cell - cy0 + 1);
         p.meta[i] = make_uint4(meta.x, static_cast<uint32_t>(cx0) | (static_cast<uint32_t>(cy0 - p.row_begin / p.cell) << 16),
                                across | (down << 16), meta.y);
         pairs += across * down;

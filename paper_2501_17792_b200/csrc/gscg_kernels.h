@@ -258,8 +258,7 @@ struct BandParams {
     unsigned long long* band_counts;  // count pass
     unsigned long long* band_cursor;  // pack pass (zeroed)
     unsigned long long band_offsets[kMaxBands];
-    uint4* packed;  // 4 x uint4 per BandSplat: r0, r1, r2, (ordinal, depth, span lo, span hi)
-    int32_t cell;   // binning cell edge in pixels
+    uint4* packed;  // 4 x uint4 per BandSplat: r0, r1, r2, (ordinal, depth, 0, 0)
 };
 
 struct BandUnpackParams {

@@ -48,42 +48,6 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float Y[15])
     Y[14] = (C36 * x) * (xx - 3.0f * yy);
 }
 
-// The record's raster rect: the 3-sigma rect [x0,x1)x[y0,y1) cut to the bounding box of
-// the cutoff ellipse power >= pf (renderer.cpp:201-203). The rasteriser only builds its
-// coverage bits from this rect; every pixel outside it fails the reference's power test,
-// so pixels are unchanged while ~20% of the rect's evaluations go (binning keeps the
-// 3-sigma rect: the per-tile lists stay the reference's). Conservative by construction:
-// with power = -Q/2, Q = a dx^2 + 2b dx dy + c dy^2 and kappa = ac/(ac - b^2), the float
-// evaluation of power errs by at most 14u*kappa*Q (u = 2^-24: the absolute-value form
-// is <= 4*kappa*Q), so any pixel the rasteriser accepts has Q <= R/(1 - 14u*kappa) with
-// R = -2 pf; at kappa <= 1024 that is R*1.00086, and the box uses R*1.002 plus one pixel
-// each side. Ill-conditioned ellipses (kappa > 1024), pf >= 0 and non-finite inputs keep
-// the 3-sigma rect.
-__device__ __forceinline__ void raster_rect(float mx, float my, float a, float b, float c, float pf, int x0, int y0,
-                                            int x1, int y1, uint32_t& lo, uint32_t& hi) {
-    const float R = -2.0f * pf;
-    const float D = a * c - b * b;
-    if (R > 0.0f && D > 0.0f && a * c <= 1024.0f * D) {
-        const float r2 = R * 1.002f / D;
-        const float hx = sqrtf(r2 * c) + 1.0f, hy = sqrtf(r2 * a) + 1.0f;
-        // Pixel px is kept iff |px + 0.5 - mx| <= hx.
-        const float fx0 = fmaxf(floorf(mx - 0.5f - hx), static_cast<float>(x0));
-        const float fx1 = fminf(floorf(mx - 0.5f + hx) + 1.0f, static_cast<float>(x1));
-        const float fy0 = fmaxf(floorf(my - 0.5f - hy), static_cast<float>(y0));
-        const float fy1 = fminf(floorf(my - 0.5f + hy) + 1.0f, static_cast<float>(y1));
-        if (fx0 <= fx1 && fy0 <= fy1) {  // false on NaN: keep the 3-sigma rect
-            x0 = static_cast<int>(fx0);
-            x1 = static_cast<int>(fx1);
-            y0 = static_cast<int>(fy0);
-            y1 = static_cast<int>(fy1);
-        } else if (fx0 > fx1 || fy0 > fy1) {
-            x1 = x0;  // no pixel centre inside the cutoff ellipse
-        }
-    }
-    lo = static_cast<uint32_t>(x0) | (static_cast<uint32_t>(y0) << 16);
-    hi = static_cast<uint32_t>(x1) | (static_cast<uint32_t>(y1) << 16);
-}
-
 // Bulk (TMA) copies global -> shared completing on an mbarrier: one instruction per
 // contiguous block instead of a 16-byte cp.async per thread and iteration.
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -398,9 +362,9 @@ k_project(ProjectParams p) {
                     float4* rec = p.records + 3 * ridx;
                     rec[0] = make_float4(mx, my, ca, cb);
                     rec[1] = make_float4(cc, c0.w, c3.y, col0);
-                    uint32_t rlo, rhi;
-                    raster_rect(mx, my, ca, cb, cc, c3.y, x0, y0, x1, y1, rlo, rhi);
-                    rec[2] = make_float4(col1, col2, __uint_as_float(rlo), __uint_as_float(rhi));
+                    rec[2] = make_float4(col1, col2,
+                                         __uint_as_float(static_cast<uint32_t>(x0) | (static_cast<uint32_t>(y0) << 16)),
+                                         __uint_as_float(static_cast<uint32_t>(x1) | (static_cast<uint32_t>(y1) << 16)));
                     if (p.record_debug) {
                         gscg_splat_record d;
                         d.ordinal = ordinal;
