@@ -204,6 +204,7 @@ struct gscg_ctx {
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
+    DevBuf buckets, bucket_staged;  // depth bucket sort: counts/starts/cursors, staged splats
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
     // output
     DevBuf fb_rgb, fb_T;
@@ -1049,14 +1050,49 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
                                              : static_cast<uint32_t>(bits_for(ctx->dmin ^ ctx->dmax));
         const uint32_t drop = dbits > ctx->depth_sort_bits ? dbits - ctx->depth_sort_bits : 0u;
         if (device_counts) ctx->deferred_depth_top = dbits;
+        // Host-settled frames take the bucket sort (gscg_depth.cu, spans gathered on the way);
+        // deferred frames (counts and depth range still on the device) the LSD passes.
+        const uint32_t tag_min = ctx->dmin >> drop, tag_range = (ctx->dmax >> drop) - tag_min;
+        const uint32_t range_bits = static_cast<uint32_t>(bits_for(tag_range));
+        const uint32_t local_bits = range_bits > 14 ? range_bits - 14 : 0u;
+        const bool buckets = !presorted && !device_counts && (1u << local_bits) <= kBucketLocalBins;
         RadixPlan dplan{};
-        if (!presorted) {
+        if (!presorted && !buckets) {
             dplan = make_plan(dbits - drop);
             for (uint32_t q = 0; q < dplan.passes; ++q) dplan.shift[q] += drop;
         }
-        const int sb = presorted ? 0
-                                 : run_radix(ctx, ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32,
-                                             dplan, launches, s_dev);
+        CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
+        int sb = 0;
+        if (buckets) {
+            DepthBucketParams bp{};
+            bp.depth = ctx->splat_depth.as<uint32_t>();
+            bp.meta = ctx->splat_meta.as<uint4>();
+            bp.count = S32;
+            bp.drop = drop;
+            bp.tag_min = tag_min;
+            bp.local_bits = local_bits;
+            bp.buckets = (tag_range >> local_bits) + 1u;
+            CUDA_TRY(ctx->buckets.ensure((3ull * kMaxDepthBuckets + 1) * 4));
+            CUDA_TRY(ctx->bucket_staged.ensure(static_cast<size_t>(S32) * 16));
+            bp.bucket_count = ctx->buckets.as<uint32_t>();
+            bp.bucket_start = bp.bucket_count + kMaxDepthBuckets;
+            bp.bucket_cursor = bp.bucket_start + kMaxDepthBuckets + 1;
+            bp.staged = ctx->bucket_staged.as<uint4>();
+            bp.keys_out = ctx->skeys[0].as<uint32_t>();
+            bp.recs_out = ctx->srecs[0].as<uint32_t>();
+            bp.spans_out = ctx->span_sorted.as<uint2>();
+            CUDA_TRY(cudaMemsetAsync(bp.bucket_count, 0, bp.buckets * 4ull, s));
+            const uint32_t grid = (S32 + kBucketTile - 1) / kBucketTile;
+            CUDA_TRY(pdl_launch(k_depth_bucket_count, grid, kBucketThreads, bp.buckets * 4ull, s, bp));
+            CUDA_TRY(pdl_launch(k_depth_bucket_scan, 1, 1024, 0, s, bp));
+            CUDA_TRY(pdl_launch(k_depth_bucket_scatter, grid, kBucketThreads, bp.buckets * 4ull, s, bp));
+            CUDA_TRY(pdl_launch(k_depth_bucket_local, bp.buckets, kBucketLocalThreads, 0, s, bp));
+            launches += 4;
+            dplan.passes = 2;  // reported sort passes: the two bucket levels
+        } else if (!presorted) {
+            sb = run_radix(ctx, ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan, launches,
+                           s_dev);
+        }
         const EmitCounts ec{s_dev};
         // 2. cell spans in sorted order; the first cell-sort digit histogram per emission
         //    block; digit offsets; pairs emitted straight into the order of the first stable
@@ -1066,13 +1102,14 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         const uint32_t emit_bits = std::min<uint32_t>(cell_bits, kRadixBits);  // the first pass, folded into emission
         const uint32_t dmask = (1u << emit_bits) - 1u;
         const uint32_t eblocks = (S32 + kEmitSplats - 1) / kEmitSplats;  // emission blocks
-        CUDA_TRY(ctx->span_sorted.ensure(static_cast<size_t>(S32) * 8));
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
         const int quads = geo.cells_per_tile == 4 ? 1 : 0;
         const uint32_t* tag_keys = presorted ? nullptr : ctx->skeys[sb].as<uint32_t>();
-        CUDA_TRY(pdl_launch(k_sorted_spans, (S32 + 1023) / 1024, kMetaThreads, 0, s, ctx->srecs[sb].as<uint32_t>(),
-                            ctx->splat_meta.as<uint4>(), S32, s_dev, ctx->span_sorted.as<uint2>()));
-        ++launches;
+        if (!buckets) {
+            CUDA_TRY(pdl_launch(k_sorted_spans, (S32 + 1023) / 1024, kMetaThreads, 0, s, ctx->srecs[sb].as<uint32_t>(),
+                                ctx->splat_meta.as<uint4>(), S32, s_dev, ctx->span_sorted.as<uint2>()));
+            ++launches;
+        }
         launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), nullptr, rtx, quads, dmask, drop, cell_bits, nullptr, nullptr, ec);
         SortPassParams bp{};
@@ -1272,6 +1309,10 @@ int gscg_create(int device, gscg_ctx** out) {
                                       kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_project<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kProjectThreads * kShFloats * 4 + kBatch * kMaxJoints * 12 * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_depth_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMaxDepthBuckets * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_depth_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMaxDepthBuckets * 4));
     });
     *out = ctx;
     return st;

@@ -1,0 +1,198 @@
+// Stage "sort", step 1 on the B200: the frame's splats in depth order by a two-level
+// bucket sort (reference: sort_splats_impl renderer.cpp:85-107 orders by (depth bits,
+// instance, gaussian); the depth bits are settled here, the tie-break per cell by
+// k_cell_fixup).
+//
+// The splat order only has to be non-decreasing in the truncated key T = dbits >> drop
+// (the top <= 25 varying bits): emission keeps it stable inside every cell and
+// k_cell_fixup orders each run of equal (cell, T-tag) pairs by the full (depth bits,
+// ordinal). Splats with equal T may therefore come out in any order, which lets both
+// levels rank with shared-memory atomics instead of a stable multisplit:
+//
+//   k_depth_bucket_count   histogram of the top bits of T (<= 16,384 buckets) per CTA of
+//                          16,384 splats, flushed with one global atomic per non-empty bin
+//   k_depth_bucket_scan    bucket starts (one CTA)
+//   k_depth_bucket_scatter every splat reserves its slot in its bucket (a shared atomic for
+//                          the rank inside the CTA, one global atomic per (CTA, bucket)) and
+//                          writes (dbits, record, binning span) there — the span rides along,
+//                          so no random meta gather follows the sort
+//   k_depth_bucket_local   one CTA per bucket: counting sort over the low bits of T (<= 2,048
+//                          bins) into the final keys / records / spans
+//
+// Two streaming passes over the S keys plus one over the staged buckets (L2-resident),
+// instead of five reduce-then-scan LSD passes and the span gather.
+#include "gscg_common.cuh"
+#include "gscg_kernels.h"
+
+namespace gscg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t depth_bucket(const DepthBucketParams& p, uint32_t dbits) {
+    return ((dbits >> p.drop) - p.tag_min) >> p.local_bits;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// Exclusive scan of one value per thread over the CTA (blockDim.x = 32 * warps).
+__device__ __forceinline__ uint32_t cta_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t x = warp_incl_scan_u32(v, lane);
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = warp_incl_scan_u32(lane < nw ? s_warp[lane] : 0u, lane);
+        if (lane < nw) s_warp[lane] = w;
+    }
+    __syncthreads();
+    total = s_warp[nw - 1];
+    const uint32_t r = (warp ? s_warp[warp - 1] : 0u) + x - v;
+    __syncthreads();
+    return r;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kBucketThreads)
+k_depth_bucket_count(DepthBucketParams p) {
+    pdl_entry();
+    extern __shared__ uint32_t s_hist[];  // p.buckets bins
+    for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) s_hist[b] = 0u;
+    __syncthreads();
+    const uint32_t base = blockIdx.x * kBucketTile;
+    uint32_t k[kBucketItems];
+#pragma unroll
+    for (int j = 0; j < kBucketItems; ++j) {  // all loads in flight first
+        const uint32_t i = base + j * kBucketThreads + threadIdx.x;
+        k[j] = i < p.count ? p.depth[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kBucketItems; ++j) {
+        const uint32_t i = base + j * kBucketThreads + threadIdx.x;
+        if (i < p.count) atomicAdd(&s_hist[depth_bucket(p, k[j])], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) {
+        const uint32_t h = s_hist[b];
+        if (h) atomicAdd(&p.bucket_count[b], h);
+    }
+}
+
+// Bucket starts: thread t scans buckets [t * per, (t + 1) * per).
+__global__ void __launch_bounds__(1024)
+k_depth_bucket_scan(DepthBucketParams p) {
+    pdl_entry();
+    __shared__ uint32_t s_warp[32];
+    const uint32_t per = (p.buckets + 1023) / 1024;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t sum = 0;
+    for (uint32_t b = b0; b < min(b0 + per, p.buckets); ++b) sum += p.bucket_count[b];
+    uint32_t total;
+    uint32_t run = cta_excl_scan(sum, s_warp, total);
+    for (uint32_t b = b0; b < min(b0 + per, p.buckets); ++b) {
+        p.bucket_start[b] = run;
+        p.bucket_cursor[b] = run;
+        run += p.bucket_count[b];
+    }
+    if (threadIdx.x == 0) p.bucket_start[p.buckets] = total;
+}
+
+__global__ void __launch_bounds__(kBucketThreads)
+k_depth_bucket_scatter(DepthBucketParams p) {
+    pdl_entry();
+    extern __shared__ uint32_t s_hist[];  // counts, then each bin's global slot base
+    for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) s_hist[b] = 0u;
+    __syncthreads();
+    const uint32_t base = blockIdx.x * kBucketTile;
+    // (bucket << 16 | rank in the CTA's share of the bucket); ranks < kBucketTile = 2^14.
+    uint32_t br[kBucketItems];
+#pragma unroll
+    for (int j = 0; j < kBucketItems; ++j) {
+        const uint32_t i = base + j * kBucketThreads + threadIdx.x;
+        br[j] = i < p.count ? p.depth[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kBucketItems; ++j) {
+        const uint32_t i = base + j * kBucketThreads + threadIdx.x;
+        if (i < p.count) {
+            const uint32_t b = depth_bucket(p, br[j]);
+            br[j] = (b << 16) | atomicAdd(&s_hist[b], 1u);
+        }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) {
+        const uint32_t h = s_hist[b];
+        if (h) s_hist[b] = atomicAdd(&p.bucket_cursor[b], h);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kBucketItems; ++j) {
+        const uint32_t i = base + j * kBucketThreads + threadIdx.x;
+        if (i < p.count) {
+            const uint4 m = p.meta[i];  // (ordinal, span lo, span hi, dbits), coalesced
+            p.staged[s_hist[br[j] >> 16] + (br[j] & 0xffffu)] = make_uint4(m.w, i, m.y, m.z);
+        }
+    }
+}
+
+// One CTA per bucket: counting sort over the bucket's low T bits (bins in shared memory;
+// ranks by shared atomics, so equal T land in any order — see the file comment).
+__global__ void __launch_bounds__(kBucketLocalThreads)
+k_depth_bucket_local(DepthBucketParams p) {
+    pdl_entry();
+    __shared__ uint32_t s_bin[kBucketLocalBins];
+    __shared__ uint32_t s_warp[32];
+    const uint32_t b = blockIdx.x;
+    const uint32_t s0 = p.bucket_start[b], n = p.bucket_start[b + 1] - s0;
+    if (n == 0) return;
+    const uint4* src = p.staged + s0;
+    if (n == 1) {
+        if (threadIdx.x == 0) {
+            const uint4 e = src[0];
+            p.keys_out[s0] = e.x;
+            p.recs_out[s0] = e.y;
+            p.spans_out[s0] = make_uint2(e.z, e.w);
+        }
+        return;
+    }
+    const uint32_t bins = 1u << p.local_bits, lmask = bins - 1u;
+    for (uint32_t d = threadIdx.x; d < bins; d += kBucketLocalThreads) s_bin[d] = 0u;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += kBucketLocalThreads)
+        atomicAdd(&s_bin[((src[i].x >> p.drop) - p.tag_min) & lmask], 1u);
+    __syncthreads();
+    // Exclusive scan of the bins: thread t owns bins [t * per, (t + 1) * per).
+    constexpr uint32_t kPer = kBucketLocalBins / kBucketLocalThreads;
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t d = threadIdx.x * kPer + q;
+        v[q] = d < bins ? s_bin[d] : 0u;
+        sum += v[q];
+    }
+    uint32_t total;
+    uint32_t run = cta_excl_scan(sum, s_warp, total);
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t d = threadIdx.x * kPer + q;
+        if (d < bins) s_bin[d] = run;
+        run += v[q];
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += kBucketLocalThreads) {
+        const uint4 e = src[i];
+        const uint32_t o = s0 + atomicAdd(&s_bin[((e.x >> p.drop) - p.tag_min) & lmask], 1u);
+        p.keys_out[o] = e.x;
+        p.recs_out[o] = e.y;
+        p.spans_out[o] = make_uint2(e.z, e.w);
+    }
+}
+
+}  // namespace gscg

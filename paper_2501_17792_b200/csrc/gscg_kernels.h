@@ -212,6 +212,34 @@ constexpr int kWideRadix = 1 << kWideBits;
 __global__ void k_sort_upsweep_wide(SortPassParams p);
 __global__ void k_sort_downsweep_wide(SortPassParams p);
 
+// Depth bucket sort (gscg_depth.cu): the splats in non-decreasing T = dbits >> drop.
+constexpr int kBucketThreads = 1024;
+constexpr int kBucketItems = 16;
+constexpr uint32_t kBucketTile = kBucketThreads * kBucketItems;  // splats per count / scatter CTA (ranks < 2^16)
+constexpr uint32_t kMaxDepthBuckets = 16384;                       // top bits of T (64 KB shared histogram)
+constexpr int kBucketLocalThreads = 256;
+constexpr uint32_t kBucketLocalBins = 2048;                        // low bits of T per bucket
+struct DepthBucketParams {
+    const uint32_t* depth;  // S depth key bits, record order
+    const uint4* meta;      // S (ordinal, span lo, span hi, dbits), record order
+    uint32_t count;         // S
+    uint32_t drop;          // T = dbits >> drop
+    uint32_t tag_min;       // min T of the frame
+    uint32_t local_bits;    // bucket = (T - tag_min) >> local_bits; local bins = 2^local_bits
+    uint32_t buckets;
+    uint32_t* bucket_count;   // [buckets], zeroed
+    uint32_t* bucket_start;   // [buckets + 1]
+    uint32_t* bucket_cursor;  // [buckets]
+    uint4* staged;            // [S] (dbits, record, span lo, span hi) grouped by bucket
+    uint32_t* keys_out;       // [S] dbits, depth order
+    uint32_t* recs_out;       // [S] record index
+    uint2* spans_out;         // [S] binning span
+};
+__global__ void k_depth_bucket_count(DepthBucketParams p);
+__global__ void k_depth_bucket_scan(DepthBucketParams p);
+__global__ void k_depth_bucket_scatter(DepthBucketParams p);
+__global__ void k_depth_bucket_local(DepthBucketParams p);
+
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
 __global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, const unsigned long long* count_dev,
                                uint2* span_sorted);
