@@ -85,21 +85,28 @@ k_depth_bucket_count(DepthBucketParams p) {
     }
 }
 
-// Bucket starts: thread t scans buckets [t * per, (t + 1) * per).
+// Bucket starts: thread t scans buckets [t * kPer, (t + 1) * kPer).
 __global__ void __launch_bounds__(1024)
 k_depth_bucket_scan(DepthBucketParams p) {
     pdl_entry();
     __shared__ uint32_t s_warp[32];
-    const uint32_t per = (p.buckets + 1023) / 1024;
-    const uint32_t b0 = threadIdx.x * per;
-    uint32_t sum = 0;
-    for (uint32_t b = b0; b < min(b0 + per, p.buckets); ++b) sum += p.bucket_count[b];
+    constexpr uint32_t kPer = kMaxDepthBuckets / 1024;
+    const uint32_t b0 = threadIdx.x * kPer;
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+        v[q] = b0 + q < p.buckets ? p.bucket_count[b0 + q] : 0u;
+        sum += v[q];
+    }
     uint32_t total;
     uint32_t run = cta_excl_scan(sum, s_warp, total);
-    for (uint32_t b = b0; b < min(b0 + per, p.buckets); ++b) {
-        p.bucket_start[b] = run;
-        p.bucket_cursor[b] = run;
-        run += p.bucket_count[b];
+#pragma unroll
+    for (uint32_t q = 0; q < kPer; ++q) {
+        if (b0 + q < p.buckets) {
+            p.bucket_start[b0 + q] = run;
+            p.bucket_cursor[b0 + q] = run;
+        }
+        run += v[q];
     }
     if (threadIdx.x == 0) p.bucket_start[p.buckets] = total;
 }
@@ -127,9 +134,25 @@ k_depth_bucket_scatter(DepthBucketParams p) {
         }
     }
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) {
-        const uint32_t h = s_hist[b];
-        if (h) s_hist[b] = atomicAdd(&p.bucket_cursor[b], h);
+    {  // one global reservation per non-empty bin, all of a thread's in flight at once
+        constexpr uint32_t kPer = kMaxDepthBuckets / kBucketThreads / 2;  // two halves (registers)
+#pragma unroll
+        for (uint32_t half = 0; half < 2; ++half) {
+            uint32_t h[kPer];
+#pragma unroll
+            for (uint32_t q = 0; q < kPer; ++q) {
+                const uint32_t b = (half * kPer + q) * kBucketThreads + threadIdx.x;
+                h[q] = b < p.buckets ? s_hist[b] : 0u;
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < kPer; ++q)
+                if (h[q]) h[q] = atomicAdd(&p.bucket_cursor[(half * kPer + q) * kBucketThreads + threadIdx.x], h[q]);
+#pragma unroll
+            for (uint32_t q = 0; q < kPer; ++q) {
+                const uint32_t b = (half * kPer + q) * kBucketThreads + threadIdx.x;
+                if (b < p.buckets) s_hist[b] = h[q];
+            }
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -143,7 +166,14 @@ k_depth_bucket_scatter(DepthBucketParams p) {
 }
 
 // One CTA per bucket: counting sort over the bucket's low T bits (bins in shared memory;
-// ranks by shared atomics, so equal T land in any order — see the file comment).
+// ranks by shared atomics, so equal T land in any order — see the file comment). A bucket
+// of up to kBucketLocalThreads * kLocalItems splats is held in registers between the two
+// passes (all loads in flight at once); larger ones stream through in rounds.
+namespace {
+constexpr int kLocalItems = 8;
+constexpr uint32_t kLocalRound = kBucketLocalThreads * kLocalItems;
+}  // namespace
+
 __global__ void __launch_bounds__(kBucketLocalThreads)
 k_depth_bucket_local(DepthBucketParams p) {
     pdl_entry();
@@ -153,27 +183,38 @@ k_depth_bucket_local(DepthBucketParams p) {
     const uint32_t s0 = p.bucket_start[b], n = p.bucket_start[b + 1] - s0;
     if (n == 0) return;
     const uint4* src = p.staged + s0;
+    const uint32_t tid = threadIdx.x;
+    auto put = [&](uint32_t o, const uint4& e) {
+        p.keys_out[o] = e.x;
+        p.recs_out[o] = e.y;
+        p.spans_out[o] = make_uint2(e.z, e.w);
+    };
     if (n == 1) {
-        if (threadIdx.x == 0) {
-            const uint4 e = src[0];
-            p.keys_out[s0] = e.x;
-            p.recs_out[s0] = e.y;
-            p.spans_out[s0] = make_uint2(e.z, e.w);
-        }
+        if (tid == 0) put(s0, src[0]);
         return;
     }
     const uint32_t bins = 1u << p.local_bits, lmask = bins - 1u;
-    for (uint32_t d = threadIdx.x; d < bins; d += kBucketLocalThreads) s_bin[d] = 0u;
+    auto bin = [&](uint32_t key) { return ((key >> p.drop) - p.tag_min) & lmask; };
+    for (uint32_t d = tid; d < bins; d += kBucketLocalThreads) s_bin[d] = 0u;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += kBucketLocalThreads)
-        atomicAdd(&s_bin[((src[i].x >> p.drop) - p.tag_min) & lmask], 1u);
+    uint4 e[kLocalItems];
+    for (uint32_t r0 = 0; r0 < n; r0 += kLocalRound) {
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) {
+            const uint32_t i = r0 + j * kBucketLocalThreads + tid;
+            if (i < n) e[j] = src[i];
+        }
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j)
+            if (r0 + j * kBucketLocalThreads + tid < n) atomicAdd(&s_bin[bin(e[j].x)], 1u);
+    }
     __syncthreads();
-    // Exclusive scan of the bins: thread t owns bins [t * per, (t + 1) * per).
+    // Exclusive scan of the bins: thread t owns bins [t * kPer, (t + 1) * kPer).
     constexpr uint32_t kPer = kBucketLocalBins / kBucketLocalThreads;
     uint32_t v[kPer], sum = 0;
 #pragma unroll
     for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t d = threadIdx.x * kPer + q;
+        const uint32_t d = tid * kPer + q;
         v[q] = d < bins ? s_bin[d] : 0u;
         sum += v[q];
     }
@@ -181,17 +222,26 @@ k_depth_bucket_local(DepthBucketParams p) {
     uint32_t run = cta_excl_scan(sum, s_warp, total);
 #pragma unroll
     for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t d = threadIdx.x * kPer + q;
+        const uint32_t d = tid * kPer + q;
         if (d < bins) s_bin[d] = run;
         run += v[q];
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += kBucketLocalThreads) {
-        const uint4 e = src[i];
-        const uint32_t o = s0 + atomicAdd(&s_bin[((e.x >> p.drop) - p.tag_min) & lmask], 1u);
-        p.keys_out[o] = e.x;
-        p.recs_out[o] = e.y;
-        p.spans_out[o] = make_uint2(e.z, e.w);
+    if (n <= kLocalRound) {  // the bucket is still in registers
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j)
+            if (j * kBucketLocalThreads + tid < n) put(s0 + atomicAdd(&s_bin[bin(e[j].x)], 1u), e[j]);
+        return;
+    }
+    for (uint32_t r0 = 0; r0 < n; r0 += kLocalRound) {
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) {
+            const uint32_t i = r0 + j * kBucketLocalThreads + tid;
+            if (i < n) e[j] = src[i];
+        }
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j)
+            if (r0 + j * kBucketLocalThreads + tid < n) put(s0 + atomicAdd(&s_bin[bin(e[j].x)], 1u), e[j]);
     }
 }
 
