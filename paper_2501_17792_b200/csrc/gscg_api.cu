@@ -1054,7 +1054,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         // deferred frames (counts and depth range still on the device) the LSD passes.
         const uint32_t tag_min = ctx->dmin >> drop, tag_range = (ctx->dmax >> drop) - tag_min;
         const uint32_t range_bits = static_cast<uint32_t>(bits_for(tag_range));
-        const uint32_t local_bits = range_bits > 14 ? range_bits - 14 : 0u;
+        const uint32_t local_bits = range_bits > kBucketTopBits ? range_bits - kBucketTopBits : 0u;
         const bool buckets = !presorted && !device_counts && (1u << local_bits) <= kBucketLocalBins;
         RadixPlan dplan{};
         if (!presorted && !buckets) {

@@ -9,14 +9,14 @@
 // ordinal). Splats with equal T may therefore come out in any order, which lets both
 // levels rank with shared-memory atomics instead of a stable multisplit:
 //
-//   k_depth_bucket_count   histogram of the top bits of T (<= 16,384 buckets) per CTA of
+//   k_depth_bucket_count   histogram of the top bits of T (<= 4,096 buckets) per CTA of
 //                          16,384 splats, flushed with one global atomic per non-empty bin
 //   k_depth_bucket_scan    bucket starts (one CTA)
 //   k_depth_bucket_scatter every splat reserves its slot in its bucket (a shared atomic for
 //                          the rank inside the CTA, one global atomic per (CTA, bucket)) and
 //                          writes (dbits, record, binning span) there — the span rides along,
 //                          so no random meta gather follows the sort
-//   k_depth_bucket_local   one CTA per bucket: counting sort over the low bits of T (<= 2,048
+//   k_depth_bucket_local   one CTA per bucket: counting sort over the low bits of T (<= 8,192
 //                          bins) into the final keys / records / spans
 //
 // Two streaming passes over the S keys plus one over the staged buckets (L2-resident),
@@ -195,7 +195,9 @@ k_depth_bucket_local(DepthBucketParams p) {
     }
     const uint32_t bins = 1u << p.local_bits, lmask = bins - 1u;
     auto bin = [&](uint32_t key) { return ((key >> p.drop) - p.tag_min) & lmask; };
-    for (uint32_t d = tid; d < bins; d += kBucketLocalThreads) s_bin[d] = 0u;
+    constexpr uint32_t kPer = kBucketLocalBins / kBucketLocalThreads;  // scan bins per thread
+    const uint32_t zbins = max(bins, kPer);                             // whole scan rows zeroed
+    for (uint32_t d = tid; d < zbins; d += kBucketLocalThreads) s_bin[d] = 0u;
     __syncthreads();
     uint4 e[kLocalItems];
     for (uint32_t r0 = 0; r0 < n; r0 += kLocalRound) {
@@ -209,23 +211,22 @@ k_depth_bucket_local(DepthBucketParams p) {
             if (r0 + j * kBucketLocalThreads + tid < n) atomicAdd(&s_bin[bin(e[j].x)], 1u);
     }
     __syncthreads();
-    // Exclusive scan of the bins: thread t owns bins [t * kPer, (t + 1) * kPer).
-    constexpr uint32_t kPer = kBucketLocalBins / kBucketLocalThreads;
-    uint32_t v[kPer], sum = 0;
+    // Exclusive scan of the bins: thread t owns bins [t * kPer, (t + 1) * kPer) (re-read
+    // from shared memory rather than held: the bucket stays in registers meanwhile).
+    const uint32_t d0 = tid * kPer;
+    uint32_t sum = 0;
+    if (d0 < bins)
 #pragma unroll
-    for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t d = tid * kPer + q;
-        v[q] = d < bins ? s_bin[d] : 0u;
-        sum += v[q];
-    }
+        for (uint32_t q = 0; q < kPer; ++q) sum += s_bin[d0 + q];
     uint32_t total;
     uint32_t run = cta_excl_scan(sum, s_warp, total);
+    if (d0 < bins)
 #pragma unroll
-    for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t d = tid * kPer + q;
-        if (d < bins) s_bin[d] = run;
-        run += v[q];
-    }
+        for (uint32_t q = 0; q < kPer; ++q) {
+            const uint32_t c = s_bin[d0 + q];
+            s_bin[d0 + q] = run;
+            run += c;
+        }
     __syncthreads();
     if (n <= kLocalRound) {  // the bucket is still in registers
 #pragma unroll
