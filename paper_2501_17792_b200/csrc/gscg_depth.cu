@@ -195,8 +195,7 @@ k_depth_bucket_local(DepthBucketParams p) {
     }
     const uint32_t bins = 1u << p.local_bits, lmask = bins - 1u;
     auto bin = [&](uint32_t key) { return ((key >> p.drop) - p.tag_min) & lmask; };
-    constexpr uint32_t kPer = kBucketLocalBins / kBucketLocalThreads;  // scan bins per thread
-    const uint32_t zbins = max(bins, kPer);                             // whole scan rows zeroed
+    const uint32_t zbins = max(bins, 32u);  // whole 32-bin scan chunks
     for (uint32_t d = tid; d < zbins; d += kBucketLocalThreads) s_bin[d] = 0u;
     __syncthreads();
     uint4 e[kLocalItems];
@@ -211,22 +210,25 @@ k_depth_bucket_local(DepthBucketParams p) {
             if (r0 + j * kBucketLocalThreads + tid < n) atomicAdd(&s_bin[bin(e[j].x)], 1u);
     }
     __syncthreads();
-    // Exclusive scan of the bins: thread t owns bins [t * kPer, (t + 1) * kPer) (re-read
-    // from shared memory rather than held: the bucket stays in registers meanwhile).
-    const uint32_t d0 = tid * kPer;
-    uint32_t sum = 0;
-    if (d0 < bins)
-#pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) sum += s_bin[d0 + q];
-    uint32_t total;
-    uint32_t run = cta_excl_scan(sum, s_warp, total);
-    if (d0 < bins)
-#pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) {
-            const uint32_t c = s_bin[d0 + q];
-            s_bin[d0 + q] = run;
-            run += c;
+    // Exclusive scan of the bins, warp w over chunks [w * C / W, (w + 1) * C / W) of 32
+    // consecutive bins (lane-contiguous: no bank conflicts), then the warp totals.
+    {
+        const int lane = tid & 31, warp = tid >> 5;
+        constexpr int kWarps = kBucketLocalThreads / 32;
+        const uint32_t chunks = zbins / 32, c0 = warp * chunks / kWarps, c1 = (warp + 1) * chunks / kWarps;
+        uint32_t wsum = 0;
+        for (uint32_t c = c0; c < c1; ++c) wsum += __reduce_add_sync(0xffffffffu, s_bin[c * 32 + lane]);
+        if (lane == 0) s_warp[warp] = wsum;
+        __syncthreads();
+        uint32_t carry = 0;
+        for (int w = 0; w < warp; ++w) carry += s_warp[w];
+        for (uint32_t c = c0; c < c1; ++c) {
+            const uint32_t v = s_bin[c * 32 + lane];
+            const uint32_t incl = warp_incl_scan_u32(v, lane);
+            s_bin[c * 32 + lane] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
+    }
     __syncthreads();
     if (n <= kLocalRound) {  // the bucket is still in registers
 #pragma unroll
