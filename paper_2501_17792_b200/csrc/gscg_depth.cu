@@ -9,14 +9,14 @@
 // ordinal). Splats with equal T may therefore come out in any order, which lets both
 // levels rank with shared-memory atomics instead of a stable multisplit:
 //
-//   k_depth_bucket_count   histogram of the top bits of T (<= 4,096 buckets) per CTA of
+//   k_depth_bucket_count   histogram of the top bits of T (<= 16,384 buckets) per CTA of
 //                          16,384 splats, flushed with one global atomic per non-empty bin
 //   k_depth_bucket_scan    bucket starts (one CTA)
 //   k_depth_bucket_scatter every splat reserves its slot in its bucket (a shared atomic for
 //                          the rank inside the CTA, one global atomic per (CTA, bucket)) and
 //                          writes (dbits, record, binning span) there — the span rides along,
 //                          so no random meta gather follows the sort
-//   k_depth_bucket_local   one CTA per bucket: counting sort over the low bits of T (<= 8,192
+//   k_depth_bucket_local   one CTA per bucket: counting sort over the low bits of T (<= 2,048
 //                          bins) into the final keys / records / spans
 //
 // Two streaming passes over the S keys plus one over the staged buckets (L2-resident),
@@ -166,19 +166,17 @@ k_depth_bucket_scatter(DepthBucketParams p) {
 }
 
 // One CTA per bucket: counting sort over the bucket's low T bits (bins in shared memory;
-// ranks by shared atomics, so equal T land in any order — see the file comment). A bucket
-// of up to kBucketLocalThreads * kLocalItems splats is held in registers between the two
-// passes (all loads in flight at once); larger ones stream through in rounds.
-namespace {
-constexpr int kLocalItems = 8;
-constexpr uint32_t kLocalRound = kBucketLocalThreads * kLocalItems;
-}  // namespace
-
+// ranks by shared atomics, so equal T land in any order — see the file comment). The
+// bucket (contiguous in the staged array) arrives by one bulk copy per chunk of
+// kBucketLocalCap splats into shared memory, completing on an mbarrier; buckets larger
+// than a chunk stream through twice.
 __global__ void __launch_bounds__(kBucketLocalThreads)
 k_depth_bucket_local(DepthBucketParams p) {
     pdl_entry();
+    extern __shared__ uint4 s_el[];  // kBucketLocalCap staged splats
     __shared__ uint32_t s_bin[kBucketLocalBins];
     __shared__ uint32_t s_warp[32];
+    __shared__ __align__(8) uint64_t s_bar;
     const uint32_t b = blockIdx.x;
     const uint32_t s0 = p.bucket_start[b], n = p.bucket_start[b + 1] - s0;
     if (n == 0) return;
@@ -193,23 +191,31 @@ k_depth_bucket_local(DepthBucketParams p) {
         if (tid == 0) put(s0, src[0]);
         return;
     }
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     const uint32_t bins = 1u << p.local_bits, lmask = bins - 1u;
-    auto bin = [&](uint32_t key) { return ((key >> p.drop) - p.tag_min) & lmask; };
     const uint32_t zbins = max(bins, 32u);  // whole 32-bin scan chunks
     for (uint32_t d = tid; d < zbins; d += kBucketLocalThreads) s_bin[d] = 0u;
     __syncthreads();
-    uint4 e[kLocalItems];
-    for (uint32_t r0 = 0; r0 < n; r0 += kLocalRound) {
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j) {
-            const uint32_t i = r0 + j * kBucketLocalThreads + tid;
-            if (i < n) e[j] = src[i];
+    auto bin = [&](uint32_t key) { return ((key >> p.drop) - p.tag_min) & lmask; };
+    uint32_t phase = 0;
+    auto load = [&](uint32_t c0) {  // chunk [c0, c0 + m) into s_el; returns m
+        const uint32_t m = min(kBucketLocalCap, n - c0);
+        if (tid == 0) {
+            mbar_arrive_expect_tx(&s_bar, m * 16u);
+            bulk_g2s(s_el, src + c0, m * 16u, &s_bar);
         }
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j)
-            if (r0 + j * kBucketLocalThreads + tid < n) atomicAdd(&s_bin[bin(e[j].x)], 1u);
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        return m;
+    };
+    for (uint32_t c0 = 0; c0 < n; c0 += kBucketLocalCap) {
+        const uint32_t m = load(c0);
+        for (uint32_t i = tid; i < m; i += kBucketLocalThreads) atomicAdd(&s_bin[bin(s_el[i].x)], 1u);
+        __syncthreads();  // the chunk buffer is free again
     }
-    __syncthreads();
     // Exclusive scan of the bins, warp w over chunks [w * C / W, (w + 1) * C / W) of 32
     // consecutive bins (lane-contiguous: no bank conflicts), then the warp totals.
     {
@@ -230,21 +236,20 @@ k_depth_bucket_local(DepthBucketParams p) {
         }
     }
     __syncthreads();
-    if (n <= kLocalRound) {  // the bucket is still in registers
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j)
-            if (j * kBucketLocalThreads + tid < n) put(s0 + atomicAdd(&s_bin[bin(e[j].x)], 1u), e[j]);
+    if (n <= kBucketLocalCap) {  // the bucket is still in shared memory
+        for (uint32_t i = tid; i < n; i += kBucketLocalThreads) {
+            const uint4 e = s_el[i];
+            put(s0 + atomicAdd(&s_bin[bin(e.x)], 1u), e);
+        }
         return;
     }
-    for (uint32_t r0 = 0; r0 < n; r0 += kLocalRound) {
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j) {
-            const uint32_t i = r0 + j * kBucketLocalThreads + tid;
-            if (i < n) e[j] = src[i];
+    for (uint32_t c0 = 0; c0 < n; c0 += kBucketLocalCap) {
+        const uint32_t m = load(c0);
+        for (uint32_t i = tid; i < m; i += kBucketLocalThreads) {
+            const uint4 e = s_el[i];
+            put(s0 + atomicAdd(&s_bin[bin(e.x)], 1u), e);
         }
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j)
-            if (r0 + j * kBucketLocalThreads + tid < n) put(s0 + atomicAdd(&s_bin[bin(e[j].x)], 1u), e[j]);
+        __syncthreads();
     }
 }
 
