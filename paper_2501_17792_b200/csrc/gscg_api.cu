@@ -1313,6 +1313,8 @@ int gscg_create(int device, gscg_ctx** out) {
                                       kMaxDepthBuckets * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_depth_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kMaxDepthBuckets * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_depth_bucket_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kBucketLocalCap * 16));
     });
     *out = ctx;
     return st;

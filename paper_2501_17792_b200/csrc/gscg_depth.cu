@@ -85,30 +85,37 @@ k_depth_bucket_count(DepthBucketParams p) {
     }
 }
 
-// Bucket starts: thread t scans buckets [t * kPer, (t + 1) * kPer).
+// Bucket starts: warp w scans buckets [w * 512, (w + 1) * 512) in lane-contiguous chunks
+// of 32 (coalesced loads and stores), then the warp totals.
 __global__ void __launch_bounds__(1024)
 k_depth_bucket_scan(DepthBucketParams p) {
     pdl_entry();
     __shared__ uint32_t s_warp[32];
-    constexpr uint32_t kPer = kMaxDepthBuckets / 1024;
-    const uint32_t b0 = threadIdx.x * kPer;
-    uint32_t v[kPer], sum = 0;
+    constexpr uint32_t kChunks = kMaxDepthBuckets / 1024;  // 32-bucket chunks per warp
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t v[kChunks], wsum = 0;
 #pragma unroll
-    for (uint32_t q = 0; q < kPer; ++q) {
-        v[q] = b0 + q < p.buckets ? p.bucket_count[b0 + q] : 0u;
-        sum += v[q];
+    for (uint32_t c = 0; c < kChunks; ++c) {
+        const uint32_t bk = (warp * kChunks + c) * 32u + lane;
+        v[c] = bk < p.buckets ? p.bucket_count[bk] : 0u;
+        wsum += v[c];
     }
-    uint32_t total;
-    uint32_t run = cta_excl_scan(sum, s_warp, total);
+    wsum = __reduce_add_sync(0xffffffffu, wsum);
+    if (lane == 0) s_warp[warp] = wsum;
+    __syncthreads();
+    uint32_t carry = 0;
+    for (uint32_t w = 0; w < warp; ++w) carry += s_warp[w];
 #pragma unroll
-    for (uint32_t q = 0; q < kPer; ++q) {
-        if (b0 + q < p.buckets) {
-            p.bucket_start[b0 + q] = run;
-            p.bucket_cursor[b0 + q] = run;
+    for (uint32_t c = 0; c < kChunks; ++c) {
+        const uint32_t bk = (warp * kChunks + c) * 32u + lane;
+        const uint32_t incl = warp_incl_scan_u32(v[c], static_cast<int>(lane));
+        if (bk < p.buckets) {
+            p.bucket_start[bk] = carry + incl - v[c];
+            p.bucket_cursor[bk] = carry + incl - v[c];
         }
-        run += v[q];
+        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (threadIdx.x == 0) p.bucket_start[p.buckets] = total;
+    if (threadIdx.x == 1023) p.bucket_start[p.buckets] = carry;
 }
 
 __global__ void __launch_bounds__(kBucketThreads)
@@ -175,6 +182,7 @@ k_depth_bucket_local(DepthBucketParams p) {
     pdl_entry();
     extern __shared__ uint4 s_el[];  // kBucketLocalCap staged splats
     __shared__ uint32_t s_bin[kBucketLocalBins];
+    __shared__ uint16_t s_inv[kBucketLocalCap];  // sorted position -> chunk index
     __shared__ uint32_t s_warp[32];
     __shared__ __align__(8) uint64_t s_bar;
     const uint32_t b = blockIdx.x;
@@ -236,11 +244,14 @@ k_depth_bucket_local(DepthBucketParams p) {
         }
     }
     __syncthreads();
-    if (n <= kBucketLocalCap) {  // the bucket is still in shared memory
-        for (uint32_t i = tid; i < n; i += kBucketLocalThreads) {
-            const uint4 e = s_el[i];
-            put(s0 + atomicAdd(&s_bin[bin(e.x)], 1u), e);
-        }
+    if (n <= kBucketLocalCap) {
+        // The bucket is still in shared memory: ranks into the inverse permutation, then
+        // every output row written coalesced (scattered 16-byte stores cost ~2 clocks per
+        // sector on this part; the staged reads here are shared-memory gathers).
+        for (uint32_t i = tid; i < n; i += kBucketLocalThreads)
+            s_inv[atomicAdd(&s_bin[bin(s_el[i].x)], 1u)] = static_cast<uint16_t>(i);
+        __syncthreads();
+        for (uint32_t j = tid; j < n; j += kBucketLocalThreads) put(s0 + j, s_el[s_inv[j]]);
         return;
     }
     for (uint32_t c0 = 0; c0 < n; c0 += kBucketLocalCap) {
