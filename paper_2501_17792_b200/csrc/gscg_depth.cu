@@ -174,15 +174,18 @@ k_depth_bucket_scatter(DepthBucketParams p) {
 
 // One CTA per bucket: counting sort over the bucket's low T bits (bins in shared memory;
 // ranks by shared atomics, so equal T land in any order — see the file comment). The
-// bucket (contiguous in the staged array) arrives by one bulk copy per chunk of
-// kBucketLocalCap splats into shared memory, completing on an mbarrier; buckets larger
-// than a chunk stream through twice.
+// bucket (contiguous in the staged array) arrives in chunks of kBucketLocalCap splats, one
+// bulk copy each into shared memory completing on an mbarrier. A bucket of up to
+// kBucketLocalChunks chunks is ranked into an inverse permutation (sorted position ->
+// bucket index) and written out coalesced, chunk by chunk (scattered 16-byte stores cost
+// ~2 clocks per sector here: the scattered writes were this kernel's whole cost). Larger
+// buckets stream through twice with scattered writes.
 __global__ void __launch_bounds__(kBucketLocalThreads)
 k_depth_bucket_local(DepthBucketParams p) {
     pdl_entry();
-    extern __shared__ uint4 s_el[];  // kBucketLocalCap staged splats
+    extern __shared__ uint4 s_el[];  // one chunk of staged splats
     __shared__ uint32_t s_bin[kBucketLocalBins];
-    __shared__ uint16_t s_inv[kBucketLocalCap];  // sorted position -> chunk index
+    __shared__ uint16_t s_inv[kBucketLocalCap * kBucketLocalChunks];  // sorted position -> bucket index
     __shared__ uint32_t s_warp[32];
     __shared__ __align__(8) uint64_t s_bar;
     const uint32_t b = blockIdx.x;
@@ -208,28 +211,32 @@ k_depth_bucket_local(DepthBucketParams p) {
     for (uint32_t d = tid; d < zbins; d += kBucketLocalThreads) s_bin[d] = 0u;
     __syncthreads();
     auto bin = [&](uint32_t key) { return ((key >> p.drop) - p.tag_min) & lmask; };
-    uint32_t phase = 0;
-    auto load = [&](uint32_t c0) {  // chunk [c0, c0 + m) into s_el; returns m
-        const uint32_t m = min(kBucketLocalCap, n - c0);
-        if (tid == 0) {
-            mbar_arrive_expect_tx(&s_bar, m * 16u);
-            bulk_g2s(s_el, src + c0, m * 16u, &s_bar);
+    const uint32_t chunks = (n + kBucketLocalCap - 1) / kBucketLocalCap;
+    uint32_t phase = 0, resident = 0xffffffffu;
+    auto load = [&](uint32_t c) {  // chunk c into s_el (callers sync before a reload); returns its size
+        const uint32_t c0 = c * kBucketLocalCap, m = min(kBucketLocalCap, n - c0);
+        if (c != resident) {
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&s_bar, m * 16u);
+                bulk_g2s(s_el, src + c0, m * 16u, &s_bar);
+            }
+            mbar_wait(&s_bar, phase);
+            phase ^= 1u;
+            resident = c;
         }
-        mbar_wait(&s_bar, phase);
-        phase ^= 1u;
         return m;
     };
-    for (uint32_t c0 = 0; c0 < n; c0 += kBucketLocalCap) {
-        const uint32_t m = load(c0);
+    for (uint32_t c = 0; c < chunks; ++c) {
+        const uint32_t m = load(c);
         for (uint32_t i = tid; i < m; i += kBucketLocalThreads) atomicAdd(&s_bin[bin(s_el[i].x)], 1u);
-        __syncthreads();  // the chunk buffer is free again
+        __syncthreads();  // the chunk buffer may be refilled
     }
     // Exclusive scan of the bins, warp w over chunks [w * C / W, (w + 1) * C / W) of 32
     // consecutive bins (lane-contiguous: no bank conflicts), then the warp totals.
     {
         const int lane = tid & 31, warp = tid >> 5;
         constexpr int kWarps = kBucketLocalThreads / 32;
-        const uint32_t chunks = zbins / 32, c0 = warp * chunks / kWarps, c1 = (warp + 1) * chunks / kWarps;
+        const uint32_t bc = zbins / 32, c0 = warp * bc / kWarps, c1 = (warp + 1) * bc / kWarps;
         uint32_t wsum = 0;
         for (uint32_t c = c0; c < c1; ++c) wsum += __reduce_add_sync(0xffffffffu, s_bin[c * 32 + lane]);
         if (lane == 0) s_warp[warp] = wsum;
@@ -244,18 +251,29 @@ k_depth_bucket_local(DepthBucketParams p) {
         }
     }
     __syncthreads();
-    if (n <= kBucketLocalCap) {
-        // The bucket is still in shared memory: ranks into the inverse permutation, then
-        // every output row written coalesced (scattered 16-byte stores cost ~2 clocks per
-        // sector on this part; the staged reads here are shared-memory gathers).
-        for (uint32_t i = tid; i < n; i += kBucketLocalThreads)
-            s_inv[atomicAdd(&s_bin[bin(s_el[i].x)], 1u)] = static_cast<uint16_t>(i);
-        __syncthreads();
-        for (uint32_t j = tid; j < n; j += kBucketLocalThreads) put(s0 + j, s_el[s_inv[j]]);
+    if (chunks <= kBucketLocalChunks) {
+        // Ranks into the inverse permutation (the resident chunk first), then each output
+        // row once, coalesced, from whichever chunk is resident.
+        for (uint32_t q = 0; q < chunks; ++q) {
+            const uint32_t c = chunks - 1 - q;
+            const uint32_t m = load(c);
+            for (uint32_t i = tid; i < m; i += kBucketLocalThreads)
+                s_inv[atomicAdd(&s_bin[bin(s_el[i].x)], 1u)] = static_cast<uint16_t>(c * kBucketLocalCap + i);
+            __syncthreads();
+        }
+        for (uint32_t q = 0; q < chunks; ++q) {  // chunk 0 is resident now
+            const uint32_t c0 = q * kBucketLocalCap;
+            load(q);
+            for (uint32_t j = tid; j < n; j += kBucketLocalThreads) {
+                const uint32_t i = s_inv[j];
+                if (chunks == 1 || i - c0 < kBucketLocalCap) put(s0 + j, s_el[i - c0]);
+            }
+            __syncthreads();
+        }
         return;
     }
-    for (uint32_t c0 = 0; c0 < n; c0 += kBucketLocalCap) {
-        const uint32_t m = load(c0);
+    for (uint32_t c = 0; c < chunks; ++c) {
+        const uint32_t m = load(c);
         for (uint32_t i = tid; i < m; i += kBucketLocalThreads) {
             const uint4 e = s_el[i];
             put(s0 + atomicAdd(&s_bin[bin(e.x)], 1u), e);
