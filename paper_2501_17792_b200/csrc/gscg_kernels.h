@@ -220,8 +220,8 @@ constexpr int kBucketTopBits = 14;
 constexpr uint32_t kMaxDepthBuckets = 1u << kBucketTopBits;       // top bits of T (64 KB shared histogram)
 constexpr int kBucketLocalThreads = 256;
 constexpr uint32_t kBucketLocalBins = 2048;                        // low bits of T per bucket (T <= 25 bits)
-constexpr uint32_t kBucketLocalCap = 4096;                         // splats per bulk-copied chunk (64 KB)
-constexpr uint32_t kBucketLocalChunks = 2;                         // buckets up to this many chunks write coalesced
+constexpr uint32_t kBucketLocalCap = 2048;                         // splats per bulk-copied chunk (32 KB)
+constexpr uint32_t kBucketLocalChunks = 4;                         // buckets up to this many chunks write coalesced
 struct DepthBucketParams {
     const uint32_t* depth;  // S depth key bits, record order
     const uint4* meta;      // S (ordinal, span lo, span hi, dbits), record order
