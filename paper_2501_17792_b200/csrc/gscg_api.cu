@@ -1085,7 +1085,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             const uint32_t grid = (S32 + kBucketTile - 1) / kBucketTile;
             CUDA_TRY(pdl_launch(k_depth_bucket_count, grid, kBucketThreads, bp.buckets * 4ull, s, bp));
             CUDA_TRY(pdl_launch(k_depth_bucket_scan, 1, 1024, 0, s, bp));
-            CUDA_TRY(pdl_launch(k_depth_bucket_scatter, grid, kBucketThreads, bp.buckets * 4ull, s, bp));
+            CUDA_TRY(pdl_launch(k_depth_bucket_scatter, (S32 + kBucketScatterTile - 1) / kBucketScatterTile, kBucketThreads,
+                                bp.buckets * 4ull, s, bp));
             CUDA_TRY(pdl_launch(k_depth_bucket_local, bp.buckets, kBucketLocalThreads, kBucketLocalCap * 16ull, s, bp));
             launches += 4;
             dplan.passes = 2;  // reported sort passes: the two bucket levels

@@ -122,27 +122,30 @@ __global__ void __launch_bounds__(kBucketThreads)
 k_depth_bucket_scatter(DepthBucketParams p) {
     pdl_entry();
     extern __shared__ uint32_t s_hist[];  // counts, then each bin's global slot base
+    const uint32_t base = blockIdx.x * kBucketScatterTile;
+    // Every load of the thread in flight at once (the splat meta carries the depth bits),
+    // so the CTA pays one memory latency, then the reservations' one.
+    uint4 m[kBucketScatterItems];
+#pragma unroll
+    for (int j = 0; j < kBucketScatterItems; ++j) {
+        const uint32_t i = base + j * kBucketThreads + threadIdx.x;
+        if (i < p.count) m[j] = p.meta[i];  // (ordinal, span lo, span hi, dbits), coalesced
+    }
     for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) s_hist[b] = 0u;
     __syncthreads();
-    const uint32_t base = blockIdx.x * kBucketTile;
-    // (bucket << 16 | rank in the CTA's share of the bucket); ranks < kBucketTile = 2^14.
-    uint32_t br[kBucketItems];
+    // (bucket << 16 | rank in the CTA's share of the bucket); ranks < kBucketScatterTile.
+    uint32_t br[kBucketScatterItems];
 #pragma unroll
-    for (int j = 0; j < kBucketItems; ++j) {
-        const uint32_t i = base + j * kBucketThreads + threadIdx.x;
-        br[j] = i < p.count ? p.depth[i] : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < kBucketItems; ++j) {
+    for (int j = 0; j < kBucketScatterItems; ++j) {
         const uint32_t i = base + j * kBucketThreads + threadIdx.x;
         if (i < p.count) {
-            const uint32_t b = depth_bucket(p, br[j]);
+            const uint32_t b = depth_bucket(p, m[j].w);
             br[j] = (b << 16) | atomicAdd(&s_hist[b], 1u);
         }
     }
     __syncthreads();
-    {  // one global reservation per non-empty bin, all of a thread's in flight at once
-        constexpr uint32_t kPer = kMaxDepthBuckets / kBucketThreads / 2;  // two halves (registers)
+    {  // one global reservation per non-empty bin, a half of the thread's bins in flight at once
+        constexpr uint32_t kPer = kMaxDepthBuckets / kBucketThreads / 2;
 #pragma unroll
         for (uint32_t half = 0; half < 2; ++half) {
             uint32_t h[kPer];
@@ -163,12 +166,10 @@ k_depth_bucket_scatter(DepthBucketParams p) {
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kBucketItems; ++j) {
+    for (int j = 0; j < kBucketScatterItems; ++j) {
         const uint32_t i = base + j * kBucketThreads + threadIdx.x;
-        if (i < p.count) {
-            const uint4 m = p.meta[i];  // (ordinal, span lo, span hi, dbits), coalesced
-            p.staged[s_hist[br[j] >> 16] + (br[j] & 0xffffu)] = make_uint4(m.w, i, m.y, m.z);
-        }
+        if (i < p.count)
+            p.staged[s_hist[br[j] >> 16] + (br[j] & 0xffffu)] = make_uint4(m[j].w, i, m[j].y, m[j].z);
     }
 }
 

@@ -215,13 +215,15 @@ __global__ void k_sort_downsweep_wide(SortPassParams p);
 // Depth bucket sort (gscg_depth.cu): the splats in non-decreasing T = dbits >> drop.
 constexpr int kBucketThreads = 1024;
 constexpr int kBucketItems = 16;
-constexpr uint32_t kBucketTile = kBucketThreads * kBucketItems;  // splats per count / scatter CTA (ranks < 2^16)
+constexpr uint32_t kBucketTile = kBucketThreads * kBucketItems;  // splats per count CTA
+constexpr int kBucketScatterItems = 8;
+constexpr uint32_t kBucketScatterTile = kBucketThreads * kBucketScatterItems;  // splats per scatter CTA (ranks < 2^16)
 constexpr int kBucketTopBits = 14;
 constexpr uint32_t kMaxDepthBuckets = 1u << kBucketTopBits;       // top bits of T (64 KB shared histogram)
 constexpr int kBucketLocalThreads = 256;
 constexpr uint32_t kBucketLocalBins = 2048;                        // low bits of T per bucket (T <= 25 bits)
 constexpr uint32_t kBucketLocalCap = 2048;                         // splats per bulk-copied chunk (32 KB)
-constexpr uint32_t kBucketLocalChunks = 4;                         // buckets up to this many chunks write coalesced
+constexpr uint32_t kBucketLocalChunks = 3;                         // buckets up to this many chunks write coalesced
 struct DepthBucketParams {
     const uint32_t* depth;  // S depth key bits, record order
     const uint4* meta;      // S (ordinal, span lo, span hi, dbits), record order
