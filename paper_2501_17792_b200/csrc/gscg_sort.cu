@@ -112,30 +112,36 @@ k_sort_upsweep(SortPassParams p) {
 }
 
 // Row scans: CTA d turns digit d's tile counts into exclusive offsets; row total ->
-// digit_base[d] (the downsweep scans the row totals itself). Each thread owns up to
-// kRowItems consecutive entries of a 1024 * kRowItems window, so a row of up to 8192 tiles
-// takes one block scan.
+// digit_base[d] (the downsweep scans the row totals itself). A 1024 * kRowItems window per
+// step: warp w owns kRowItems lane-contiguous chunks of 32 entries (coalesced loads and
+// stores), warp totals are scanned across the CTA, then each chunk with a warp scan.
 constexpr int kRowItems = 8;
 __global__ void __launch_bounds__(1024)
 k_sort_rows(SortPassParams p) {
     pdl_entry();
     __shared__ uint32_t s_warp[32];
     uint32_t* row = p.counts + static_cast<size_t>(blockIdx.x) * p.tiles;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t carry = 0;
     for (uint32_t b = 0; b < p.tiles; b += 1024 * kRowItems) {
-        const uint32_t i0 = b + threadIdx.x * kRowItems;
+        const uint32_t w0 = b + static_cast<uint32_t>(warp) * (32 * kRowItems) + lane;
         uint32_t v[kRowItems], sum = 0;
 #pragma unroll
         for (int k = 0; k < kRowItems; ++k) {
-            v[k] = i0 + k < p.tiles ? row[i0 + k] : 0u;
+            const uint32_t i = w0 + 32 * k;
+            v[k] = i < p.tiles ? row[i] : 0u;
             sum += v[k];
         }
+        sum = __reduce_add_sync(0xffffffffu, sum);  // the warp's window total
         uint32_t total;
-        uint32_t run = carry + block_excl_scan(sum, s_warp, total);
+        const uint32_t before = block_excl_scan(lane == 0 ? sum : 0u, s_warp, total);  // lane 0: earlier warps
+        uint32_t run = carry + __shfl_sync(0xffffffffu, before, 0);
 #pragma unroll
         for (int k = 0; k < kRowItems; ++k) {
-            if (i0 + k < p.tiles) row[i0 + k] = run;
-            run += v[k];
+            const uint32_t incl = warp_incl_scan(v[k], lane);
+            const uint32_t i = w0 + 32 * k;
+            if (i < p.tiles) row[i] = run + incl - v[k];
+            run += __shfl_sync(0xffffffffu, incl, 31);
         }
         carry += total;
     }
