@@ -42,6 +42,13 @@ using namespace gscg;
 // launched from the host after the counters read and the PDL launch path measured ~1%
 // slower.
 constexpr uint64_t kPdlMaxSplats = 4000000;
+uint64_t pdl_max_splats() {  // GSCG_PDL_MAX_SPLATS overrides the cut (A/B measurements)
+    static const uint64_t v = [] {
+        const char* e = std::getenv("GSCG_PDL_MAX_SPLATS");
+        return e ? std::strtoull(e, nullptr, 10) : kPdlMaxSplats;
+    }();
+    return v;
+}
 thread_local bool t_pdl_frame = true;
 
 bool gscg::pdl_enabled() {
@@ -1602,7 +1609,7 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
         }();
         const bool deferred = defer && ctx->splat_capacity > 0 && ctx->pair_capacity > 0 &&
                               !(ctx->debug & GSCG_DEBUG_POSED);
-        t_pdl_frame = ctx->S < kPdlMaxSplats;
+        t_pdl_frame = ctx->S < pdl_max_splats();
         uint32_t passes;
         nvtxRangePushA("gscg_render_frame");  // host-side ranges for nsys / ncu --nvtx
         if (deferred) {
