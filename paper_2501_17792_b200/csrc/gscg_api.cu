@@ -36,12 +36,10 @@
 
 using namespace gscg;
 
-// PDL is used for frames of up to kPdlMaxSplats splats (the previous frame's count): there
-// the frame is a chain of short kernels and overlapping their launch with the previous
-// kernel's tail is worth 10% (config 1, region frames); on the big frames the sort is
-// launched from the host after the counters read and the PDL launch path measured ~1%
-// slower.
-constexpr uint64_t kPdlMaxSplats = 4000000;
+// PDL is used for frames of up to kPdlMaxSplats splats (the previous frame's count). With
+// the bucket depth sort it pays on every BASELINE config (config 3: 546 vs 539 FPS device,
+// 548 vs 528 e2e); the cut stays as a knob for A/B runs.
+constexpr uint64_t kPdlMaxSplats = ~0ull;
 uint64_t pdl_max_splats() {  // GSCG_PDL_MAX_SPLATS overrides the cut (A/B measurements)
     static const uint64_t v = [] {
         const char* e = std::getenv("GSCG_PDL_MAX_SPLATS");
