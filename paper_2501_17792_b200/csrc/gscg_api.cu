@@ -210,10 +210,7 @@ struct gscg_ctx {
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
     DevBuf buckets, bucket_staged;  // depth bucket sort: counts/starts/cursors, staged splats
-    DevBuf tile_ranges, quad_recs, split_counts;  // quadrant split of tile lists
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
-    bool final_gapped = false;             // quadrant lists of a split frame: 4 x len slots per tile
-    uint64_t final_extent = 0;             // entries of final_recs
     // output
     DevBuf fb_rgb, fb_T;
     // Pipelined host frames alternate two framebuffers: one is read back on the copy
@@ -1047,21 +1044,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
     uint32_t passes = 0;
     if (cells) CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(cells) * 8, s));
     ctx->final_recs = nullptr;
-    ctx->final_gapped = false;
-    ctx->final_extent = 0;
-    // 16-px tiles: sort the reference's tile pairs (each carrying its quadrant mask) and
-    // split the tile lists into the rasteriser's quadrant lists (gscg_split.cu). Deferred,
-    // presorted and band frames, and frames past 2^28 splats, sort quadrant pairs.
-    static const bool no_split = [] {
-        const char* e = std::getenv("GSCG_NO_SPLIT");
-        return e && e[0] == '1';
-    }();
-    const bool split = !no_split && geo.cells_per_tile == 4 && !presorted && !device_counts && ctx->TP > 0 &&
-                       S32 < (1u << kRecMaskShift) && ctx->TP < (1ull << 30);
-    const uint32_t KP = split ? static_cast<uint32_t>(ctx->TP) : K;  // pairs through the cell sort
-    const uint32_t sort_cells = split ? tiles : cells;
     if (S32 > 0 && K > 0) {
-        ensure_sort_buffers(ctx, S32, KP);
+        ensure_sort_buffers(ctx, S32, K);
         // 1. splats by the top (at most kDepthSortBits) varying bits of their depth keys;
         //    the dropped low bits and the ordinal tie-break are settled per cell in step 4.
         // Deferred frames plan on the last settled frame's depth range plus one bit of
@@ -1119,13 +1103,13 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         // 2. cell spans in sorted order; the first cell-sort digit histogram per emission
         //    block; digit offsets; pairs emitted straight into the order of the first stable
         //    cell-sort pass, each key word tagged with its splat's truncated depth.
-        const uint32_t cell_bits = std::max(1, bits_for(sort_cells - 1));
+        const uint32_t cell_bits = std::max(1, bits_for(cells - 1));
         const uint32_t cell_mask = cell_bits >= 32 ? 0xffffffffu : (1u << cell_bits) - 1u;
         const uint32_t emit_bits = std::min<uint32_t>(cell_bits, kRadixBits);  // the first pass, folded into emission
         const uint32_t dmask = (1u << emit_bits) - 1u;
         const uint32_t eblocks = (S32 + kEmitSplats - 1) / kEmitSplats;  // emission blocks
         CUDA_TRY(ctx->block_sums.ensure(static_cast<size_t>(eblocks) * kRadix * 4));
-        const int quads = split ? 2 : geo.cells_per_tile == 4 ? 1 : 0;
+        const int quads = geo.cells_per_tile == 4 ? 1 : 0;
         const uint32_t* tag_keys = presorted ? nullptr : ctx->skeys[sb].as<uint32_t>();
         if (!buckets) {
             CUDA_TRY(pdl_launch(k_sorted_spans, (S32 + 1023) / 1024, kMetaThreads, 0, s, ctx->srecs[sb].as<uint32_t>(),
@@ -1152,60 +1136,26 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             for (uint32_t q = 0; q < rest.passes; ++q) rest.shift[q] += emit_bits;
         }
         const int cb = rest.passes ? run_radix(ctx, ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(),
-                                               ctx->pcell, ctx->precs, KP, rest, launches, k_dev)
+                                               ctx->pcell, ctx->precs, K, rest, launches, k_dev)
                                    : 1;
         // 4. cell ranges + every run of equal (cell, tag) ordered by (depth bits, ordinal).
-        const uint32_t long_cap = KP / kLongRun + KP / 2048 + 2;  // see k_cell_fixup
+        const uint32_t long_cap = K / kLongRun + K / 2048 + 2;  // see k_cell_fixup
         CUDA_TRY(ctx->long_runs.ensure(static_cast<size_t>(long_cap) * 8 + 16));
         uint32_t* long_count = reinterpret_cast<uint32_t*>(ctx->long_runs.as<uint2>() + long_cap);
         CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
-        uint2* cell_ranges = ctx->ranges.as<uint2>();
-        if (split) {
-            CUDA_TRY(ctx->tile_ranges.ensure(static_cast<size_t>(tiles) * 8));
-            cell_ranges = ctx->tile_ranges.as<uint2>();
-            CUDA_TRY(cudaMemsetAsync(cell_ranges, 0, static_cast<size_t>(tiles) * 8, s));
-        }
-        const uint32_t rec_mask = split ? kRecIndexMask : 0xffffffffu;
-        const uint32_t kblocks = (KP + 256 * kStreamItems - 1) / (256 * kStreamItems);  // 2048 pairs per CTA
+        const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);  // 2048 pairs per CTA
         CUDA_TRY(pdl_launch(k_cell_fixup, kblocks, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), ctx->precs[cb].as<uint32_t>(),
-                                             ctx->splat_meta.as<uint4>(), KP, k_dev, cell_mask, presorted ? 0 : 1,
-                                             cell_ranges, ctx->long_runs.as<uint2>(), long_count, long_cap, rec_mask));
+                                             ctx->splat_meta.as<uint4>(), K, k_dev, cell_mask, presorted ? 0 : 1,
+                                             ctx->ranges.as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap));
         ++launches;
         if (!presorted) {
-            CUDA_TRY(pdl_launch(k_pair_long_runs, ctx->sm_count * 2, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), KP, k_dev,
+            CUDA_TRY(pdl_launch(k_pair_long_runs, ctx->sm_count * 2, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), K, k_dev,
                                                               ctx->precs[cb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
-                                                              ctx->long_runs.as<uint2>(), long_count, rec_mask));
+                                                              ctx->long_runs.as<uint2>(), long_count));
             ++launches;
         }
         CUDA_TRY(cudaGetLastError());
         ctx->final_recs = ctx->precs[cb].as<uint32_t>();
-        ctx->final_extent = KP;
-        if (split) {  // 5. tile lists -> quadrant lists (+ the quadrant ranges the raster reads)
-            QuadSplitParams qp{};
-            qp.keys = ctx->pcell[cb].as<uint32_t>();
-            qp.recs = ctx->precs[cb].as<uint32_t>();
-            qp.count = KP;
-            qp.cell_mask = cell_mask;
-            qp.tile_ranges = cell_ranges;
-            qp.chunks = (KP + kQuadSplitChunk - 1) / kQuadSplitChunk;
-            CUDA_TRY(ctx->split_counts.ensure(static_cast<size_t>(qp.chunks) * 16));
-            CUDA_TRY(ctx->quad_recs.ensure(static_cast<size_t>(KP) * 16));
-            qp.chunk_counts = ctx->split_counts.as<uint32_t>();
-            qp.out = ctx->quad_recs.as<uint32_t>();
-            qp.quad_ranges = ctx->ranges.as<uint2>();
-            CUDA_TRY(pdl_launch(k_quad_split_count, qp.chunks, 256, 0, s, qp));
-            SortPassParams rp{};
-            rp.counts = qp.chunk_counts;
-            rp.digit_base = ctx->hist.as<uint32_t>();
-            rp.tiles = qp.chunks;
-            CUDA_TRY(pdl_launch(k_sort_rows, 4, 1024, 0, s, rp));
-            CUDA_TRY(pdl_launch(k_quad_split, qp.chunks, 256, 0, s, qp));
-            launches += 3;
-            CUDA_TRY(cudaGetLastError());
-            ctx->final_recs = qp.out;
-            ctx->final_gapped = true;
-            ctx->final_extent = 4ull * KP;
-        }
         passes = dplan.passes + 1 + rest.passes;
     }
     CUDA_TRY(cudaEventRecord(ctx->ev[4], s));
@@ -1857,7 +1807,6 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
         CUDA_TRY(cudaStreamSynchronize(s));
         ctx->S = recv_count;
         ctx->K = ctx->h_counters->pairs;
-        ctx->TP = 0;  // tile pairs not counted here: no quadrant split
         if (ctx->K > 0xF0000000ull) throw Status(GSCG_ERR_OOM, "band pair count exceeds 32-bit indexing");
         ctx->dmin = ctx->h_counters->depth_min_bits;
         ctx->dmax = ctx->h_counters->depth_max_bits;
@@ -1895,8 +1844,7 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
                                 &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                                 &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals,
                                 &ctx->fb_rgb, &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch,
-                                &ctx->long_runs, &ctx->buckets, &ctx->bucket_staged, &ctx->tile_ranges,
-                                &ctx->quad_recs, &ctx->split_counts};
+                                &ctx->long_runs};
         for (const DevBuf* b : bufs) out->frame_bytes += b->cap;
         out->pinned_bytes = ctx->pinned_cap + sizeof(FrameCounters) + GSCG_MAX_BANDS * 8;
         out->naive_attribute_bytes = ctx->naive_core.cap + ctx->naive_w.cap;
@@ -2079,31 +2027,6 @@ void with_mode(gscg_ctx* ctx, gscg_ctx::Mode mode, F&& f) {
         throw;
     }
     ctx->mode = gscg_ctx::Mode::Frame;
-}
-
-// Quadrant-split frames keep gaps in their quadrant lists (gscg_split.cu: 4 x len slots
-// per tile); the debug readers return the cell ranges and pair records compacted in cell
-// order, the layout a quadrant-pair sort produces.
-void compact_cells(gscg_ctx* ctx, std::vector<uint2>& ranges, std::vector<uint32_t>* recs) {
-    const size_t cells = static_cast<size_t>(ctx->tiles) * ctx->cells_per_tile;
-    ranges.assign(cells, make_uint2(0u, 0u));
-    if (cells) CUDA_TRY(cudaMemcpyAsync(ranges.data(), ctx->ranges.ptr, cells * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    std::vector<uint32_t> gapped;
-    if (recs && ctx->final_gapped && ctx->final_extent) {
-        gapped.resize(ctx->final_extent);
-        CUDA_TRY(cudaMemcpyAsync(gapped.data(), ctx->final_recs, ctx->final_extent * 4, cudaMemcpyDeviceToHost,
-                                 ctx->stream));
-    }
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (!ctx->final_gapped) return;
-    uint32_t at = 0;
-    if (recs) recs->clear();
-    for (uint2& r : ranges) {
-        const uint32_t n = r.y - r.x;
-        if (recs) recs->insert(recs->end(), gapped.begin() + r.x, gapped.begin() + r.y);
-        r = make_uint2(at, at + n);
-        at += n;
-    }
 }
 
 void records_to_splats(gscg_ctx* ctx, gscg_frame_splat* out, uint64_t capacity) {
@@ -2436,9 +2359,7 @@ int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells) {
     if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
         if (cells > ctx->tiles * ctx->cells_per_tile) invalid("more cells requested than rendered");
-        std::vector<uint2> ranges;
-        compact_cells(ctx, ranges, nullptr);
-        std::memcpy(out, ranges.data(), cells * 8ull);
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->ranges.ptr, cells * 8ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     });
 }
 
@@ -2447,18 +2368,10 @@ int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
     return guarded(ctx, [&] {
         if (pairs > ctx->K) invalid("more pairs requested than rendered");
         if (pairs == 0) return;
-        CUDA_TRY(ctx->sorted_ordinals.ensure(pairs * 8));
-        const uint32_t* recs = ctx->final_recs;
-        if (ctx->final_gapped) {  // the compacted quadrant lists, staged behind the output
-            std::vector<uint2> ranges;
-            std::vector<uint32_t> compact;
-            compact_cells(ctx, ranges, &compact);
-            uint32_t* staged = ctx->sorted_ordinals.as<uint32_t>() + pairs;
-            CUDA_TRY(cudaMemcpyAsync(staged, compact.data(), pairs * 4, cudaMemcpyHostToDevice, ctx->stream));
-            recs = staged;
-        }
+        CUDA_TRY(ctx->sorted_ordinals.ensure(pairs * 4));
         k_sorted_ordinals<<<std::min<uint64_t>((pairs + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-            recs, ctx->splat_meta.as<uint4>(), static_cast<uint32_t>(pairs), ctx->sorted_ordinals.as<uint32_t>());
+            ctx->final_recs, ctx->splat_meta.as<uint4>(), static_cast<uint32_t>(pairs),
+            ctx->sorted_ordinals.as<uint32_t>());
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         CUDA_TRY(cudaMemcpyAsync(out, ctx->sorted_ordinals.ptr, pairs * 4, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));

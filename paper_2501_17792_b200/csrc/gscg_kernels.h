@@ -248,20 +248,15 @@ __global__ void k_depth_bucket_local(DepthBucketParams p);
 constexpr int kMetaThreads = 128;  // k_sorted_spans: 128 threads x kStreamItems = one 1024-splat block
 __global__ void k_sorted_spans(const uint32_t* recs, const uint4* meta, uint32_t count, const unsigned long long* count_dev,
                                uint2* span_sorted);
-// Tile pairs of the quadrant split carry the tile's covered quadrants in the top bits of
-// their record word (record indices < 2^28 on that path).
-constexpr uint32_t kRecMaskShift = 28;
-constexpr uint32_t kRecIndexMask = (1u << kRecMaskShift) - 1u;
 constexpr uint32_t kLongRun = 32;       // runs of equal pair keys longer than this go to k_pair_long_runs
 constexpr uint32_t kPairRunCap = 2048;  // k_pair_long_runs sorts runs up to this size in shared memory
 // long_runs must hold count / kLongRun + count / 2048 + 2 entries (runs longer than
 // kLongRun, plus at most one run leaving each 2048-pair fix-up tile).
 __global__ void k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
                              const unsigned long long* count_dev, uint32_t cell_mask, int fix, uint2* ranges,
-                             uint2* long_runs, uint32_t* long_count, uint32_t long_cap, uint32_t rec_mask);
+                             uint2* long_runs, uint32_t* long_count, uint32_t long_cap);
 __global__ void k_pair_long_runs(const uint32_t* keys, uint32_t count, const unsigned long long* count_dev,
-                                 uint32_t* recs, const uint4* meta, const uint2* long_runs, const uint32_t* long_count,
-                                 uint32_t rec_mask);
+                                 uint32_t* recs, const uint4* meta, const uint2* long_runs, const uint32_t* long_count);
 constexpr int kEmitThreads = 128;  // k_emit_scatter: 4 sorted splats per thread
 constexpr uint32_t kEmitSplats = 4 * kEmitThreads;  // sorted splats per emission block
 constexpr uint32_t kEmitStage = 2048;  // pairs per block staged in shared memory for coalesced writes
@@ -269,7 +264,7 @@ constexpr int kEmitSmem = (32 * kEmitThreads + 2 * kEmitStage) * 4;  // dynamic 
 struct EmitCounts {  // deferred frames: the splat count from the device counter (null: the host's)
     const unsigned long long* count_dev;
 };
-template <bool kCount, int kCells>
+template <bool kCount, bool kQuads>
 __global__ void k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count,
                                const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
                                uint32_t blocks, int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop,
@@ -282,22 +277,6 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
                  int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
                  uint32_t* pair_rec, EmitCounts dc);
 constexpr int kStreamItems = 8;  // elements per thread in the streaming sort kernels
-// Quadrant split of tile lists (gscg_split.cu).
-constexpr uint32_t kQuadSplitChunk = 2048;  // tile pairs per CTA
-struct QuadSplitParams {
-    const uint32_t* keys;      // tile-sorted pair key words (tile id in the cell bits)
-    const uint32_t* recs;      // record | quadrant mask << kRecMaskShift
-    uint32_t count;            // tile pairs
-    uint32_t cell_mask;        // tile id bits of a key word
-    const uint2* tile_ranges;  // [tiles] from k_cell_fixup
-    uint32_t chunks;           // ceil(count / kQuadSplitChunk)
-    uint32_t* chunk_counts;    // [4][chunks]: quadrant-bit counts, then exclusive offsets (k_sort_rows)
-    uint32_t* out;             // [4 * count]: quadrant q of tile t at 4 x_t + q len_t
-    uint2* quad_ranges;        // [4 * tiles] (zeroed): the rasteriser's cells
-};
-__global__ void k_quad_split_count(QuadSplitParams p);
-__global__ void k_quad_split(QuadSplitParams p);
-
 
 // screen-band exchange (multi-GPU frame)
 constexpr int kMaxBands = GSCG_MAX_BANDS;

@@ -279,32 +279,18 @@ __device__ __forceinline__ uint32_t cell_id(int cx, int cy, int tiles_x) {
                   : static_cast<uint32_t>(cy * tiles_x + cx);
 }
 
-// Calls f(cell, qmask) for every binning cell of a packed span, row by row (the emission
-// order). kCells: 0 = the span's own cells (qmask 0); 1 = 8x8 quadrant cells (along a row
-// the id advances without recomputing it: +1 inside a tile, +3 into the next tile); 2 =
-// the 16-px tiles a quadrant span overlaps, qmask = the tile's quadrants it covers (bit
-// 2*row + col, the raster's quadrant order).
-template <int kCells, typename F>
+// Calls f(cell) for every binning cell of a packed span, row by row (the emission order);
+// along a row the cell id advances without recomputing it (quadrant cells: +1 inside a
+// tile, +3 into the next tile).
+template <bool kQuads, typename F>
 __device__ __forceinline__ void for_each_cell_t(uint2 sp, int tiles_x, F&& f) {
     const int cx0 = static_cast<int>(sp.x & 0xffffu), cy0 = static_cast<int>(sp.x >> 16);
     const int w = static_cast<int>(sp.y & 0xffffu), h = static_cast<int>(sp.y >> 16);
-    if (kCells == 2) {
-        const int cx1 = cx0 + w - 1, cy1 = cy0 + h - 1;
-        for (int ty = cy0 >> 1; ty <= (cy1 >> 1); ++ty) {
-            const uint32_t rows = (2 * ty >= cy0 ? 1u : 0u) | (2 * ty + 1 <= cy1 ? 2u : 0u);
-            uint32_t c = static_cast<uint32_t>(ty * tiles_x + (cx0 >> 1));
-            for (int tx = cx0 >> 1; tx <= (cx1 >> 1); ++tx, ++c) {
-                const uint32_t cols = (2 * tx >= cx0 ? 1u : 0u) | (2 * tx + 1 <= cx1 ? 2u : 0u);
-                f(c, ((rows & 1u) ? cols : 0u) | ((rows & 2u) ? cols << 2 : 0u));
-            }
-        }
-        return;
-    }
     for (int cy = cy0; cy < cy0 + h; ++cy) {
-        uint32_t c = cell_id<kCells == 1>(cx0, cy, tiles_x);
+        uint32_t c = cell_id<kQuads>(cx0, cy, tiles_x);
         for (int cx = cx0; cx < cx0 + w; ++cx) {
-            f(c, 0u);
-            c += kCells == 1 ? 1u + 2u * static_cast<uint32_t>(cx & 1) : 1u;
+            f(c);
+            c += kQuads ? 1u + 2u * static_cast<uint32_t>(cx & 1) : 1u;
         }
     }
 }
@@ -556,7 +542,7 @@ __device__ __forceinline__ unsigned long long pair_order_key(const uint4& m) {  
 __global__ void __launch_bounds__(256)
 k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t count,
              const unsigned long long* count_dev, uint32_t cell_mask, int fix, uint2* ranges, uint2* long_runs,
-             uint32_t* long_count, uint32_t long_cap, uint32_t rec_mask) {
+             uint32_t* long_count, uint32_t long_cap) {
     pdl_entry();
     count = resolve_count(count, count_dev);
     static_assert(kStreamItems == 8, "two uint4 loads per thread");
@@ -639,7 +625,7 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
         left[j] = in && (j > 0 ? k[j - 1] == k[j] : (has_left && left_key == k[j]));
         const bool right = j + 1 < kStreamItems ? (pos + 1 < n_here && k[j + 1] == k[j]) : (has_right && right_key == k[j]);
         tie[j] = in && (left[j] || right);
-        m[j] = tie[j] ? meta[r[j] & rec_mask] : make_uint4(0u, 0u, 0u, 0u);
+        m[j] = tie[j] ? meta[r[j]] : make_uint4(0u, 0u, 0u, 0u);
     }
 #pragma unroll
     for (uint32_t j = 0; j < kStreamItems; ++j)
@@ -648,7 +634,7 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
         const uint32_t p = kTile + tid;
         const bool eq = p < n_ext && s_key[p] == s_key[slot(kTile - 1)];
         const uint32_t in_run = __ffs(~__ballot_sync(0xffffffffu, eq)) - 1u;  // leading equal pairs (32: all)
-        if (tid < in_run) s_ord[p] = pair_order_key(meta[s_rec[p] & rec_mask]);
+        if (tid < in_run) s_ord[p] = pair_order_key(meta[s_rec[p]]);
     }
     // Run starts of the warp, compacted (a run entering from the previous tile is that
     // tile's): lanes then take one run each instead of walking their own windows.
@@ -740,7 +726,7 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
 // runs are sorted in place in global memory.
 __global__ void __launch_bounds__(256)
 k_pair_long_runs(const uint32_t* keys, uint32_t count, const unsigned long long* count_dev, uint32_t* recs,
-                 const uint4* meta, const uint2* long_runs, const uint32_t* long_count, uint32_t rec_mask) {
+                 const uint4* meta, const uint2* long_runs, const uint32_t* long_count) {
     pdl_entry();
     count = resolve_count(count, count_dev);
     __shared__ unsigned long long s_key[kPairRunCap];
@@ -767,7 +753,7 @@ k_pair_long_runs(const uint32_t* keys, uint32_t count, const unsigned long long*
                 uint32_t rec = 0u;
                 if (i < n) {
                     rec = recs[s + i];
-                    key = pair_order_key(meta[rec & rec_mask]);
+                    key = pair_order_key(meta[rec]);
                 }
                 s_key[i] = key;
                 s_rec[i] = rec;
@@ -809,7 +795,7 @@ k_pair_long_runs(const uint32_t* keys, uint32_t count, const unsigned long long*
                         }
                         if (l < n) {
                             const uint32_t ra = r[i], rb = r[l];
-                            if (pair_order_key(meta[ra & rec_mask]) > pair_order_key(meta[rb & rec_mask])) {
+                            if (pair_order_key(meta[ra]) > pair_order_key(meta[rb])) {
                                 r[i] = rb;
                                 r[l] = ra;
                             }
@@ -831,7 +817,7 @@ k_pair_long_runs(const uint32_t* keys, uint32_t count, const unsigned long long*
 // output equals emitting in sorted order and running the first LSD pass on it.
 // kCount: only count the block's pairs per digit (block_digit[d][block], the input of
 // k_sort_rows); else scatter them.
-template <bool kCount, int kCells>
+template <bool kCount, bool kQuads>
 __global__ void __launch_bounds__(kEmitThreads)
 k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count, const uint2* span_sorted,
                uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x, int quads,
@@ -885,7 +871,7 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
         if (tid < kRadix) s_tot[tid] = 0u;
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) for_each_cell_t<kCells>(sp[q], tiles_x, [&](uint32_t c, uint32_t) { atomicAdd(&s_tot[c & dmask], 1u); });
+        for (int q = 0; q < 4; ++q) for_each_cell_t<kQuads>(sp[q], tiles_x, [&](uint32_t c) { atomicAdd(&s_tot[c & dmask], 1u); });
         __syncthreads();
         if (static_cast<uint32_t>(tid) <= dmask && tid < kRadix) block_digit[tid * blocks + blockIdx.x] = s_tot[tid];
         return;
@@ -897,7 +883,7 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
         s_base[tid] = warp_incl_scan(t, lane) - t + (static_cast<uint32_t>(tid) <= dmask ? block_digit[tid * blocks + blockIdx.x] : 0u);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) for_each_cell_t<kCells>(sp[q], tiles_x, [&](uint32_t c, uint32_t) { ++s_cnt[c & dmask][tid]; });
+    for (int q = 0; q < 4; ++q) for_each_cell_t<kQuads>(sp[q], tiles_x, [&](uint32_t c) { ++s_cnt[c & dmask][tid]; });
     __syncthreads();
     // Exclusive scan over threads for each digit (warp w: kDigitsPerWarp digits, lane l:
     // kPerLane consecutive threads), then over digits: s_cnt becomes each thread's start.
@@ -926,16 +912,15 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t rec = rc[q], tag = tg[q];
-        for_each_cell_t<kCells>(sp[q], tiles_x, [&](uint32_t c, uint32_t qmask) {
+        for_each_cell_t<kQuads>(sp[q], tiles_x, [&](uint32_t c) {
             const uint32_t d = c & dmask;
             const uint32_t r = s_cnt[d][tid]++;  // rank among the block's pairs of digit d
-            const uint32_t rw = rec | (qmask << kRecMaskShift);  // tile pairs carry their quadrants
             if (staged) {
                 s_stage_cell[s_local[d] + r] = c | tag;
-                s_stage_rec[s_local[d] + r] = rw;
+                s_stage_rec[s_local[d] + r] = rec;
             } else {
                 pair_cell[s_base[d] + r] = c | tag;
-                pair_rec[s_base[d] + r] = rw;
+                pair_rec[s_base[d] + r] = rec;
             }
         });
     }
@@ -956,15 +941,16 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
                  int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
                  uint32_t* pair_rec, EmitCounts dc) {
     static bool attr = [] {
-        cudaFuncSetAttribute(k_emit_scatter<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
-        cudaFuncSetAttribute(k_emit_scatter<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
-        cudaFuncSetAttribute(k_emit_scatter<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
+        cudaFuncSetAttribute(k_emit_scatter<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmem);
         return true;
     }();
     (void)attr;
     const int smem = count_only ? kRadix * 4 : kEmitSmem;  // the count pass keeps 32 block counters
-    auto kernel = count_only ? (quads == 2 ? k_emit_scatter<true, 2> : quads ? k_emit_scatter<true, 1> : k_emit_scatter<true, 0>)
-                             : (quads == 2 ? k_emit_scatter<false, 2> : quads ? k_emit_scatter<false, 1> : k_emit_scatter<false, 0>);
+    auto kernel = count_only ? (quads ? k_emit_scatter<true, true> : k_emit_scatter<true, false>)
+                             : (quads ? k_emit_scatter<false, true> : k_emit_scatter<false, false>);
     pdl_launch(kernel, blocks, kEmitThreads, smem, s, rec_sorted, key_sorted, count, span_sorted, block_digit, digit_total,
                blocks, tiles_x, quads, dmask, tag_drop, tag_shift, pair_cell, pair_rec, dc);
 }
