@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python scripts/launch_table.py gpurun_out/${T}_launches.csv > gpurun_out/${T}_launches.txt 2>&1
 ncu --set full --clock-control none --import-source on --profile-from-start off -o /tmp/prof_${T} python scripts/profile_frame.py --frames 1 --warmup 2 > gpurun_out/${T}_ncu_full.log 2>&1; echo full=$? >> gpurun_out/${T}_status.txt
 python scripts/ncu_summary.py /tmp/prof_${T}.ncu-rep gpurun_out/${T}_ncu_summary.json > gpurun_out/${T}_ncu_full.txt 2>&1
-for k in k_raster16q k_project k_sort_downsweep k_sort_upsweep k_emit_scatter k_cell_fixup k_sorted_spans; do
+for k in k_raster16q k_project k_sort_downsweep k_sort_upsweep k_emit_scatter k_cell_fixup k_depth_bucket_scatter k_depth_bucket_local; do
   python scripts/ncu_source_top.py /tmp/prof_${T}.ncu-rep $k > gpurun_out/${T}_source_$k.txt 2>&1
 done
 ncu -i /tmp/prof_${T}.ncu-rep --page raw --csv --metrics smsp__thread_inst_executed_per_inst_executed.ratio,smsp__inst_executed.sum,launch__registers_per_thread > gpurun_out/${T}_ncu_extra.csv 2>&1
