@@ -121,6 +121,7 @@ struct DevBuf {
 // Varying depth bits the splat sort orders (LSD passes of <= 5 bits); the lower bits and
 // the ordinal tie-break are settled per cell by k_cell_fixup.
 constexpr uint32_t kDepthSortBits = 25;
+constexpr uint64_t kBucketMaxSplats = 1ull << 40;  // measured per config: see DESIGN.md §4
 
 struct LevelStore {
     uint32_t count = 0;
@@ -1060,7 +1061,13 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         const uint32_t tag_min = ctx->dmin >> drop, tag_range = (ctx->dmax >> drop) - tag_min;
         const uint32_t range_bits = static_cast<uint32_t>(bits_for(tag_range));
         const uint32_t local_bits = range_bits > kBucketTopBits ? range_bits - kBucketTopBits : 0u;
-        const bool buckets = !presorted && !device_counts && (1u << local_bits) <= kBucketLocalBins;
+        // GSCG_BUCKET_MAX_SPLATS: largest frame the bucket sort takes (A/B knob; past it the
+        // average bucket outgrows the coalesced local sort and the LSD passes win).
+        static const uint64_t bucket_max = [] {
+            const char* e = std::getenv("GSCG_BUCKET_MAX_SPLATS");
+            return e ? std::strtoull(e, nullptr, 10) : kBucketMaxSplats;
+        }();
+        const bool buckets = !presorted && !device_counts && (1u << local_bits) <= kBucketLocalBins && S32 <= bucket_max;
         RadixPlan dplan{};
         if (!presorted && !buckets) {
             dplan = make_plan(dbits - drop);
