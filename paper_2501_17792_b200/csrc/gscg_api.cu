@@ -207,6 +207,7 @@ struct gscg_ctx {
     uint64_t splat_capacity = 0, pair_capacity = 0;
     uint32_t culled = 0;  // instances dropped by k_inst_cull in the last frame
     uint32_t depth_sort_bits = kDepthSortBits;  // top varying depth bits the splat sort orders
+    uint64_t bucket_max_splats = kBucketMaxSplats;  // largest frame the bucket depth sort takes
     uint32_t dbits_prev = kDepthSortBits;       // varying depth bits of the last settled frame
     uint32_t deferred_depth_top = 32;           // key bits a deferred frame's depth plan covers
     cudaEvent_t counters_ev = nullptr;          // the frame's counters are in h_counters
@@ -1064,13 +1065,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         const uint32_t tag_min = ctx->dmin >> drop, tag_range = (ctx->dmax >> drop) - tag_min;
         const uint32_t range_bits = static_cast<uint32_t>(bits_for(tag_range));
         const uint32_t local_bits = range_bits > kBucketTopBits ? range_bits - kBucketTopBits : 0u;
-        // GSCG_BUCKET_MAX_SPLATS: largest frame the bucket sort takes (A/B knob; past it the
-        // average bucket outgrows the coalesced local sort and the LSD passes win).
-        static const uint64_t bucket_max = [] {
-            const char* e = std::getenv("GSCG_BUCKET_MAX_SPLATS");
-            return e ? std::strtoull(e, nullptr, 10) : kBucketMaxSplats;
-        }();
-        const bool buckets = !presorted && !device_counts && (1u << local_bits) <= kBucketLocalBins && S32 <= bucket_max;
+        const bool buckets = !presorted && !device_counts && (1u << local_bits) <= kBucketLocalBins &&
+                             S32 <= ctx->bucket_max_splats;
         RadixPlan dplan{};
         if (!presorted && !buckets) {
             dplan = make_plan(dbits - drop);
@@ -1306,6 +1302,8 @@ int gscg_create(int device, gscg_ctx** out) {
             const int v = std::atoi(e);
             if (v >= 1 && v <= 32) ctx->depth_sort_bits = static_cast<uint32_t>(v);
         }
+        if (const char* e = std::getenv("GSCG_BUCKET_MAX_SPLATS"))  // A/B knob: 0 = LSD depth passes always
+            ctx->bucket_max_splats = std::strtoull(e, nullptr, 10);
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
         for (auto& e : ctx->band_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -172,6 +172,26 @@ def test_truncated_depth_sort_is_exact(bits, monkeypatch):
     assert rep["K"] > 0
 
 
+@pytest.mark.parametrize("bits", [25, 12])
+def test_lsd_depth_sort_is_exact(bits, monkeypatch):
+    """Frames past GSCG_BUCKET_MAX_SPLATS (config 5) take the LSD depth passes instead of
+    the bucket sort; forced here on a small crowd, both must give the oracle's bins."""
+    monkeypatch.setenv("GSCG_BUCKET_MAX_SPLATS", "0")
+    monkeypatch.setenv("GSCG_DEPTH_SORT_BITS", str(bits))
+    rep = parity(basic_scene(count=48, rows=6, cols=8), 0.6)
+    assert rep["K"] > 0
+
+
+def test_bucket_sort_large_buckets_are_exact(monkeypatch):
+    """Config 2 sorted on 14 depth bits: 3.3 M splats in at most 16,384 buckets, thousands
+    per bucket where the crowd is dense, so the bucket sort's multi-chunk coalesced and
+    streamed local paths both run; every per-cell list must still equal the oracle's."""
+    monkeypatch.setenv("GSCG_DEPTH_SORT_BITS", "14")
+    s, extra = config_scene(2, sh=False)
+    rep = parity(s, extra["time_s"], forced_lod=extra["forced_lod"])
+    assert rep["S"] > 3_000_000
+
+
 def test_repeated_frames_are_byte_identical():
     s = basic_scene(count=16)
     r = P.Renderer(s)
