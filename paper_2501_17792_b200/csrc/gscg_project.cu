@@ -59,6 +59,8 @@ k_project(ProjectParams p) {
     float* s_mats = s_sh + (p.sh_enabled ? kProjectThreads * kShFloats : 0);
     __shared__ uint32_t s_item_start[kMaxGroups + 1];
     __shared__ uint32_t s_member[kBatch], s_member_base[kBatch];  // batch instance ids, ordinal bases
+    __shared__ uint32_t s_wcnt[kProjectThreads / 32];
+    __shared__ unsigned long long s_base;
     __shared__ uint32_t s_item;
     __shared__ uint32_t s_tile_pairs;  // the reference's (tile, splat) bin entries of this CTA
     __shared__ __align__(8) uint64_t s_bar;  // the work item's bulk copies (SH + skin matrices)
@@ -294,24 +296,33 @@ k_project(ProjectParams p) {
                 }
             }
 
-            // Record slots: ballot ranks inside the warp, one atomic per (warp, instance) on
-            // the frame's splat counter (no CTA barrier inside the instance loop).
+            // Record slots: ballot ranks inside the warp, warp counts across the CTA, one
+            // atomic per (CTA, instance) on the frame's splat counter.
             pairs += n_tiles;
             // Tile pairs (= pairs unless quadrant cells) are warp-reduced into shared memory
             // here rather than carried in a register (the kernel sits at its 64-register cap).
             const uint32_t wbins = __reduce_add_sync(0xffffffffu, n_bins);
             if (lane == 0 && wbins) atomicAdd(&s_tile_pairs, wbins);
             const uint32_t bal = __ballot_sync(0xffffffffu, survive);
-            unsigned long long wbase = 0;
-            if (lane == 0 && bal) wbase = atomicAdd(&p.counters->splats, static_cast<unsigned long long>(__popc(bal)));
-            const unsigned long long base = __shfl_sync(0xffffffffu, wbase, 0);
+            if (lane == 0) s_wcnt[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t before = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < kProjectThreads / 32; ++w) {
+                const uint32_t t = s_wcnt[w];
+                before += w < warp ? t : 0u;
+                total += t;
+            }
+            if (tid == 0) s_base = atomicAdd(&p.counters->splats, static_cast<unsigned long long>(total));
+            __syncthreads();
+            const unsigned long long base = s_base;
             const uint32_t ordinal = gvalid ? s_member_base[k] + gi : 0u;
             if (p.posed_debug && gvalid) {
                 p.posed_debug[3ull * ordinal + 0] = ax;
                 p.posed_debug[3ull * ordinal + 1] = ay;
                 p.posed_debug[3ull * ordinal + 2] = az;
             }
-            const uint64_t ridx = base + __popc(bal & lt);
+            const uint64_t ridx = base + before + __popc(bal & lt);
             const uint32_t dbits = __float_as_uint(depth);
             const bool stored = survive && ridx < p.splat_capacity;
             if (survive) {
