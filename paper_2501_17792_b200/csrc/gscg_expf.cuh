@@ -16,22 +16,43 @@
 
 namespace gscg {
 
-__device__ __forceinline__ float glibc_expf(float x, const unsigned long long* tab32) {
-    constexpr double kInvLn2N = 0x1.71547652b82fep+0 * 32;
+// For the rasterisers' hot loops: the table's 32-bit shared-memory address is held in a
+// register and the polynomial constants come from the constant bank (the compiler would
+// otherwise rebuild both, and the shared window base, on every call). k_eval_expf runs this
+// same function for the exhaustive check.
+struct ExpfRegs {
+    double inv_ln2n, c0, c1, c2;
+    uint32_t tab;
+};
+// Constants read from the constant bank (DMUL/DFMA take them as c[][] operands: no moves
+// in the loop).
+__constant__ double c_expf_k[4] = {0x1.71547652b82fep+0 * 32, 0x1.c6af84b912394p-5 / 32 / 32 / 32,
+                                   0x1.ebfce50fac4f3p-3 / 32 / 32, 0x1.62e42ff0c52d6p-1 / 32};
+__device__ __forceinline__ ExpfRegs expf_regs(const unsigned long long* s_tab) {
+    ExpfRegs k;
+    k.inv_ln2n = c_expf_k[0];
+    k.c0 = c_expf_k[1];
+    k.c1 = c_expf_k[2];
+    k.c2 = c_expf_k[3];
+    uint32_t t = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+    asm volatile("mov.b32 %0, %0;" : "+r"(t));  // kept in a register, not rebuilt per call
+    k.tab = t;
+    return k;
+}
+__device__ __forceinline__ float glibc_expf_regs(float x, const ExpfRegs& k) {
     constexpr double kShift = 0x1.8p+52;
-    constexpr double kC0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32;
-    constexpr double kC1 = 0x1.ebfce50fac4f3p-3 / 32 / 32;
-    constexpr double kC2 = 0x1.62e42ff0c52d6p-1 / 32;
     const double xd = static_cast<double>(x);
-    const double z = __dmul_rn(kInvLn2N, xd);
+    const double z = __dmul_rn(k.inv_ln2n, xd);
     double kd = __dadd_rn(z, kShift);
-    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
+    const uint32_t ki = static_cast<uint32_t>(__double2loint(kd));  // k's low bits (ki << 47 uses 17 of them)
     kd = __dsub_rn(kd, kShift);
-    const double r = __fma_rn(kInvLn2N, xd, -kd);
-    const double s = __longlong_as_double(static_cast<long long>(tab32[ki & 31u] + (ki << 47)));
-    const double zp = __fma_rn(kC0, r, kC1);
+    const double r = __fma_rn(k.inv_ln2n, xd, -kd);
+    uint32_t tlo, thi;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tlo), "=r"(thi) : "r"(k.tab + (ki & 31u) * 8u));
+    const double s = __hiloint2double(static_cast<int>(thi + (ki << 15)), static_cast<int>(tlo));  // tab + (ki << 47)
+    const double zp = __fma_rn(k.c0, r, k.c1);
     const double r2 = __dmul_rn(r, r);
-    double y = __fma_rn(kC2, r, 1.0);
+    double y = __fma_rn(k.c2, r, 1.0);
     y = __fma_rn(zp, r2, y);
     return __double2float_rn(__dmul_rn(y, s));
 }

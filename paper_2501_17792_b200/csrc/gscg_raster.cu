@@ -69,12 +69,11 @@ __device__ __forceinline__ float pixel_power(const SplatView& s, float fx, float
 
 // Blend one splat into one pixel; returns true when the pixel reaches the floor.
 __device__ __forceinline__ bool blend(const SplatView& s, int px, int py, float& T, float& cr,
-                                      float& cg, float& cb, float amax, float tfloor,
-                                      const unsigned long long* tab) {
+                                      float& cg, float& cb, float amax, float tfloor, const ExpfRegs& ek) {
     if (px < s.x0 || px >= s.x1 || py < s.y0 || py >= s.y1) return false;
     const float power = pixel_power(s, static_cast<float>(px) + 0.5f, static_cast<float>(py) + 0.5f);
     if (power < s.pf) return false;
-    const float alpha = fminf(__fmul_rn(s.o, glibc_expf(power, tab)), amax);
+    const float alpha = fminf(__fmul_rn(s.o, glibc_expf_regs(power, ek)), amax);
     const float w = __fmul_rn(T, alpha);
     cr = __fadd_rn(cr, __fmul_rn(w, s.r));
     cg = __fadd_rn(cg, __fmul_rn(w, s.g));
@@ -144,6 +143,7 @@ k_raster16q(RasterParams p) {
     __shared__ unsigned long long s_tab[32];
     load_exp_table(s_tab);
     __syncthreads();
+    const ExpfRegs ek = expf_regs(s_tab);
     const int tile = blockIdx.x >> 2, quad = blockIdx.x & 3;
     const int tx = tile % p.tiles_x + p.tile_col0, ty = tile / p.tiles_x + p.tile_row0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -189,15 +189,14 @@ k_raster16q(RasterParams p) {
         uint32_t todo1 = transpose32(32 + lane < n ? block_cover(ext[32 + lane], bx0, by0) : 0u, lane);
         if (done) todo0 = todo1 = 0u;
         while (__any_sync(0xffffffffu, (todo0 | todo1) != 0u)) {
-            if ((todo0 | todo1) == 0u) continue;
-            int k;
-            if (todo0) {  // list order: chunk 0 before chunk 1, lower bit first
-                k = __ffs(todo0) - 1;
-                todo0 &= todo0 - 1u;
-            } else {
-                k = 32 + __ffs(todo1) - 1;
-                todo1 &= todo1 - 1u;
-            }
+            // List order: chunk 0 before chunk 1, lower bit first (select, not branch).
+            const bool lo = todo0 != 0u;
+            const uint32_t word = lo ? todo0 : todo1;
+            if (word == 0u) continue;
+            const int k = __ffs(word) - 1 + (lo ? 0 : 32);
+            const uint32_t rest = word & (word - 1u);
+            todo0 = lo ? rest : todo0;
+            todo1 = lo ? todo1 : rest;
             const float4 g = geo[k];
             const float dx = __fsub_rn(fx, g.x);
             const float dy = __fsub_rn(fy, g.y);
@@ -205,7 +204,7 @@ k_raster16q(RasterParams p) {
             const float q = __fadd_rn(__fmul_rn(__fmul_rn(g.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
             const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(g.w, dx), dy));
             if (power < c.z) continue;
-            const float alpha = fminf(__fmul_rn(c.y, glibc_expf(power, s_tab)), p.alpha_max);
+            const float alpha = fminf(__fmul_rn(c.y, glibc_expf_regs(power, ek)), p.alpha_max);
             const float w = __fmul_rn(T, alpha);
             const float4 e = ext[k];
             cr = __fadd_rn(cr, __fmul_rn(w, c.w));
@@ -238,6 +237,7 @@ k_raster_generic(RasterParams p) {
     __shared__ float4 s_rec[256 * 3];
     __shared__ unsigned long long s_tab[32];
     load_exp_table(s_tab);
+    const ExpfRegs ek = expf_regs(s_tab);  // table read only after the block's first barrier
     const int ts = p.tile_size;
     const int tile = blockIdx.x;
     const int tx = tile % p.tiles_x + p.tile_col0, ty = tile / p.tiles_x + p.tile_row0;
@@ -272,7 +272,7 @@ k_raster_generic(RasterParams p) {
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 if (!live[k]) continue;
-                if (blend(v, pxs[k], pys[k], T[k], cr[k], cg[k], cb[k], p.alpha_max, p.t_floor, s_tab)) {
+                if (blend(v, pxs[k], pys[k], T[k], cr[k], cg[k], cb[k], p.alpha_max, p.t_floor, ek)) {
                     live[k] = false;
                     --live_count;
                 }
@@ -305,8 +305,9 @@ __global__ void k_eval_expf(uint32_t first_bits, uint32_t n, float* out) {
     __shared__ unsigned long long s_tab[32];
     load_exp_table(s_tab);
     __syncthreads();
+    const ExpfRegs ek = expf_regs(s_tab);  // the rasterisers' exact code path
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        out[i] = glibc_expf(__uint_as_float(first_bits + i), s_tab);
+        out[i] = glibc_expf_regs(__uint_as_float(first_bits + i), ek);
 }
 
 }  // namespace gscg
