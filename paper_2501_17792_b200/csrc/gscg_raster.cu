@@ -137,9 +137,9 @@ __global__ void __launch_bounds__(64)
 k_raster16q(RasterParams p) {
     pdl_entry();
     constexpr int kStage = 32 * CH;
-    __shared__ float4 s_geo[2][2][kStage];   // [warp][buffer][slot]
-    __shared__ float4 s_col[2][2][kStage];
-    __shared__ float4 s_ext[2][2][kStage];   // G, B, rect lo, rect hi
+    // [warp][buffer][slot][geo | colour | ext (G, B, rect lo, rect hi)]: one slot base per
+    // record, the three rows at fixed offsets.
+    __shared__ float4 s_rec[2][2][kStage][3];
     __shared__ unsigned long long s_tab[32];
     load_exp_table(s_tab);
     __syncthreads();
@@ -162,9 +162,10 @@ k_raster16q(RasterParams p) {
             const uint32_t i = start + h * 32 + lane;
             if (i < range.y) {
                 const float4* src = p.records + 3ull * p.recs[i];
-                cp_async16(&s_geo[warp][buf][h * 32 + lane], src + 0);
-                cp_async16(&s_col[warp][buf][h * 32 + lane], src + 1);
-                cp_async16(&s_ext[warp][buf][h * 32 + lane], src + 2);
+                float4* dst = s_rec[warp][buf][h * 32 + lane];
+                cp_async16(dst + 0, src + 0);
+                cp_async16(dst + 1, src + 1);
+                cp_async16(dst + 2, src + 2);
             }
         }
         cp_async_commit();
@@ -180,13 +181,11 @@ k_raster16q(RasterParams p) {
             cp_async_wait<0>();
         }
         __syncwarp();
-        const float4* geo = s_geo[warp][buf];
-        const float4* col = s_col[warp][buf];
-        const float4* ext = s_ext[warp][buf];
+        const float4 (*rec)[3] = s_rec[warp][buf];
         const int n = static_cast<int>(min(static_cast<uint32_t>(kStage), range.y - start));
         static_assert(CH == 2, "two explicit chunk words (a dynamically indexed array spills)");
-        uint32_t todo0 = transpose32(lane < n ? block_cover(ext[lane], bx0, by0) : 0u, lane);
-        uint32_t todo1 = transpose32(32 + lane < n ? block_cover(ext[32 + lane], bx0, by0) : 0u, lane);
+        uint32_t todo0 = transpose32(lane < n ? block_cover(rec[lane][2], bx0, by0) : 0u, lane);
+        uint32_t todo1 = transpose32(32 + lane < n ? block_cover(rec[32 + lane][2], bx0, by0) : 0u, lane);
         if (done) todo0 = todo1 = 0u;
         while (__any_sync(0xffffffffu, (todo0 | todo1) != 0u)) {
             // List order: chunk 0 before chunk 1, lower bit first (select, not branch).
@@ -197,16 +196,16 @@ k_raster16q(RasterParams p) {
             const uint32_t rest = word & (word - 1u);
             todo0 = lo ? rest : todo0;
             todo1 = lo ? todo1 : rest;
-            const float4 g = geo[k];
+            const float4 g = rec[k][0];
             const float dx = __fsub_rn(fx, g.x);
             const float dy = __fsub_rn(fy, g.y);
-            const float4 c = col[k];
+            const float4 c = rec[k][1];
             const float q = __fadd_rn(__fmul_rn(__fmul_rn(g.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
             const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(g.w, dx), dy));
             if (power < c.z) continue;
             const float alpha = fminf(__fmul_rn(c.y, glibc_expf_regs(power, ek)), p.alpha_max);
             const float w = __fmul_rn(T, alpha);
-            const float4 e = ext[k];
+            const float4 e = rec[k][2];
             cr = __fadd_rn(cr, __fmul_rn(w, c.w));
             cg = __fadd_rn(cg, __fmul_rn(w, e.x));
             cb = __fadd_rn(cb, __fmul_rn(w, e.y));
