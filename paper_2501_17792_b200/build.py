@@ -2,6 +2,7 @@
 
   lib/libgscg.so      CUDA kernels + C-ABI (include/gscg.h), sm_100a only
   lib/libgsc_host.so  C++ host API (namespace gsc) + C-ABI for Python (include/gsch.h)
+  lib_checked/        both again with device bounds checks (-DGSCG_DEVICE_CHECKS)
 
 Parity-critical translation units (update, project) are compiled with --fmad=false so
 no multiply-add is contracted; host code uses -ffp-contract=off and no -march, the
@@ -22,6 +23,8 @@ CSRC = PKG / "csrc"
 HOST = PKG / "host"
 LIB = PKG / "lib"
 OBJ = PKG / "_obj"
+LIB_CHECKED = PKG / "lib_checked"
+OBJ_CHECKED = PKG / "_obj_checked"
 INCLUDE = ROOT / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,6 +61,15 @@ def _run(cmd: list[str], log: list[str]) -> None:
 
 
 def build(verbose: bool = False, force: bool = False) -> dict[str, Path]:
+    out = _build_variant(LIB, OBJ, [], verbose, force)
+    # lib_checked/: the same sources with device bounds checks (GSCG_DCHECK, gscg_common.cuh),
+    # loaded by the checked-build GPU test through GSCG_LIB_DIR (compute-sanitizer is closed
+    # on the GPU pool).
+    _build_variant(LIB_CHECKED, OBJ_CHECKED, ["-DGSCG_DEVICE_CHECKS"], verbose, force)
+    return out
+
+
+def _build_variant(LIB: Path, OBJ: Path, defines: list[str], verbose: bool, force: bool) -> dict[str, Path]:
     LIB.mkdir(exist_ok=True)
     OBJ.mkdir(exist_ok=True)
     nvcc = _nvcc()
@@ -70,7 +82,7 @@ def build(verbose: bool = False, force: bool = False) -> dict[str, Path]:
         obj = OBJ / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            flags = list(NVCC_FLAGS) + (["--fmad=false"] if src.name in EXACT_TUS else [])
+            flags = list(NVCC_FLAGS) + defines + (["--fmad=false"] if src.name in EXACT_TUS else [])
             jobs.append([nvcc, "-c", str(src), "-o", str(obj)] + flags)
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         for f in [ex.submit(_run, j, log) for j in jobs]:

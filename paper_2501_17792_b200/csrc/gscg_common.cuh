@@ -7,6 +7,8 @@
 // order, so no FMA contraction or reassociation can change a bit.
 #pragma once
 
+#include <cstdio>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <utility>
@@ -81,6 +83,24 @@ __device__ __forceinline__ int x86_float_to_int(float v) {
     // |v| < 2^31 is exactly the in-range set: -2^31 itself converts to INT_MIN either way.
     return fabsf(v) < 2147483648.0f ? __float2int_rz(v) : INT32_MIN;
 }
+
+// Device bounds checks of the checked build (lib_checked/, -DGSCG_DEVICE_CHECKS; the pool
+// has no compute-sanitizer): a failed check prints its site and traps, so the API call
+// returns a CUDA error. Compiled out of the product build.
+#ifdef GSCG_DEVICE_CHECKS
+#define GSCG_DCHECK(cond)                                                                          \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("GSCG_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,          \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x), #cond);            \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define GSCG_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 

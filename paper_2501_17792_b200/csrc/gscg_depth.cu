@@ -76,7 +76,10 @@ k_depth_bucket_count(DepthBucketParams p) {
 #pragma unroll
     for (int j = 0; j < kBucketItems; ++j) {
         const uint32_t i = base + j * kBucketThreads + threadIdx.x;
-        if (i < p.count) atomicAdd(&s_hist[depth_bucket(p, k[j])], 1u);
+        if (i < p.count) {
+            GSCG_DCHECK(depth_bucket(p, k[j]) < p.buckets);
+            atomicAdd(&s_hist[depth_bucket(p, k[j])], 1u);
+        }
     }
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) {
@@ -140,6 +143,7 @@ k_depth_bucket_scatter(DepthBucketParams p) {
         const uint32_t i = base + j * kBucketThreads + threadIdx.x;
         if (i < p.count) {
             const uint32_t b = depth_bucket(p, m[j].w);
+            GSCG_DCHECK(b < p.buckets);
             br[j] = (b << 16) | atomicAdd(&s_hist[b], 1u);
         }
     }
@@ -168,8 +172,10 @@ k_depth_bucket_scatter(DepthBucketParams p) {
 #pragma unroll
     for (int j = 0; j < kBucketScatterItems; ++j) {
         const uint32_t i = base + j * kBucketThreads + threadIdx.x;
-        if (i < p.count)
+        if (i < p.count) {
+            GSCG_DCHECK(s_hist[br[j] >> 16] + (br[j] & 0xffffu) < p.count);
             p.staged[s_hist[br[j] >> 16] + (br[j] & 0xffffu)] = make_uint4(m[j].w, i, m[j].y, m[j].z);
+        }
     }
 }
 
@@ -191,10 +197,12 @@ k_depth_bucket_local(DepthBucketParams p) {
     __shared__ __align__(8) uint64_t s_bar;
     const uint32_t b = blockIdx.x;
     const uint32_t s0 = p.bucket_start[b], n = p.bucket_start[b + 1] - s0;
+    GSCG_DCHECK(s0 <= p.count && n <= p.count - s0);
     if (n == 0) return;
     const uint4* src = p.staged + s0;
     const uint32_t tid = threadIdx.x;
     auto put = [&](uint32_t o, const uint4& e) {
+        GSCG_DCHECK(o >= s0 && o < s0 + n && e.y < p.count);
         p.keys_out[o] = e.x;
         p.recs_out[o] = e.y;
         p.spans_out[o] = make_uint2(e.z, e.w);
@@ -259,7 +267,11 @@ k_depth_bucket_local(DepthBucketParams p) {
             const uint32_t c = chunks - 1 - q;
             const uint32_t m = load(c);
             for (uint32_t i = tid; i < m; i += kBucketLocalThreads)
-                s_inv[atomicAdd(&s_bin[bin(s_el[i].x)], 1u)] = static_cast<uint16_t>(c * kBucketLocalCap + i);
+            {
+                const uint32_t slot = atomicAdd(&s_bin[bin(s_el[i].x)], 1u);
+                GSCG_DCHECK(slot < n);
+                s_inv[slot] = static_cast<uint16_t>(c * kBucketLocalCap + i);
+            }
             __syncthreads();
         }
         for (uint32_t q = 0; q < chunks; ++q) {  // chunk 0 is resident now

@@ -252,6 +252,7 @@ __device__ __forceinline__ void downsweep_tile(const SortPassParams& p, Downswee
         for (int j = 0; j < kHalf; ++j) {
             const uint32_t e = tid + (h * kHalf + j) * kSortThreads;
             if (kFull || e < n_here) {
+                GSCG_DCHECK(opos[j] < p.count);
                 p.keys_out[opos[j]] = okey[j];
                 p.vals_out[opos[j]] = oval[j];
             }
@@ -472,6 +473,7 @@ __device__ __forceinline__ void downsweep_wide_tile(const SortPassParams& p, Dow
         for (int j = 0; j < kHalf; ++j) {
             const uint32_t e = tid + (h * kHalf + j) * kSortThreads;
             if (kFull || e < n_here) {
+                GSCG_DCHECK(opos[j] < p.count);
                 p.keys_out[opos[j]] = okey[j];
                 p.vals_out[opos[j]] = oval[j];
             }

@@ -9,9 +9,12 @@ render path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
+if os.environ.get("GSCG_LIB_DIR"):  # e.g. lib_checked/ (device bounds checks)
+    LIB_DIR = Path(os.environ["GSCG_LIB_DIR"]).resolve()
 
 GSCG_OK = 0
 GSCG_ERR_INVALID_ARGUMENT = -1
