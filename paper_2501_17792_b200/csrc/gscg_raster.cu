@@ -132,14 +132,14 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 // across all CH chunks before re-converging (a lane busy in one chunk and idle in the
 // other balances within the round: 12% faster than one chunk per round). Each pixel
 // still walks the tile's list in order, so results equal the reference's per-tile loop.
-template <int CH, int NBUF>
+template <int CH>
 __global__ void __launch_bounds__(64)
 k_raster16q(RasterParams p) {
     pdl_entry();
     constexpr int kStage = 32 * CH;
     // [warp][buffer][slot][geo | colour | ext (G, B, rect lo, rect hi)]: one slot base per
     // record, the three rows at fixed offsets.
-    __shared__ float4 s_rec[2][NBUF][kStage][3];
+    __shared__ float4 s_rec[2][2][kStage][3];
     __shared__ unsigned long long s_tab[32];
     load_exp_table(s_tab);
     __syncthreads();
@@ -171,13 +171,10 @@ k_raster16q(RasterParams p) {
         cp_async_commit();
     };
     int buf = 0;
-    if (NBUF == 2 && range.x < range.y) stage(0, range.x);
+    if (range.x < range.y) stage(0, range.x);
     for (uint32_t start = range.x; start < range.y; start += kStage) {
         if (__all_sync(0xffffffffu, done)) break;
-        if (NBUF == 1) {  // single buffer: more resident warps hide the copy instead
-            stage(0, start);
-            cp_async_wait<0>();
-        } else if (start + kStage < range.y) {
+        if (start + kStage < range.y) {
             stage(buf ^ 1, start + kStage);
             cp_async_wait<1>();
         } else {
@@ -219,7 +216,7 @@ k_raster16q(RasterParams p) {
             }
         }
         __syncwarp();
-        buf ^= NBUF - 1;
+        buf ^= 1;
     }
     cp_async_wait<0>();
     if (inside) {
@@ -296,14 +293,7 @@ k_raster_generic(RasterParams p) {
 }
 
 void launch_raster(const RasterParams& p, uint32_t tiles, cudaStream_t stream) {
-    static const bool single = [] {  // GSCG_RASTER_BUFS=1: single-buffered staging (A/B)
-        const char* e = std::getenv("GSCG_RASTER_BUFS");
-        return e && e[0] == '1';
-    }();
-    if (p.tile_size == 16) {
-        if (single) pdl_launch(k_raster16q<2, 1>, tiles * 4, 64, 0, stream, p);
-        else pdl_launch(k_raster16q<2, 2>, tiles * 4, 64, 0, stream, p);
-    }
+    if (p.tile_size == 16) pdl_launch(k_raster16q<2>, tiles * 4, 64, 0, stream, p);
     else if (p.tile_size <= 16) pdl_launch(k_raster_generic<1>, tiles, 256, 0, stream, p);
     else if (p.tile_size <= 32) pdl_launch(k_raster_generic<4>, tiles, 256, 0, stream, p);
     else pdl_launch(k_raster_generic<16>, tiles, 256, 0, stream, p);
