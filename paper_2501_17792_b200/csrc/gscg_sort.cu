@@ -23,8 +23,6 @@
 // writes it out coalesced. No tile waits on another: a decoupled look-back onesweep and
 // 8-bit shared-atomic ranking were both measured slower here (serial look-back chains,
 // ATOMS throughput).
-#include <cstdlib>
-
 #include "gscg_common.cuh"
 #include "gscg_kernels.h"
 
@@ -940,150 +938,6 @@ k_emit_scatter(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t 
     }
 }
 
-// Load-balanced scatter pass (same output as k_emit_scatter<false, .>): the block's pairs
-// are numbered p = 0..P-1 in (splat, row, column) order — the order the first stable cell
-// pass keeps — and thread t takes p = round * 128 + t, so a splat spanning many cells no
-// longer serialises its thread. A pair's splat comes from a shared map filled per window of
-// kEmitWindow pairs; its rank among the block's pairs of its digit = the digit's running
-// count + the earlier warps' counts this round + its rank inside the warp (five ballots).
-// Per-warp digit counts and the running counts are double-buffered, so a round costs one
-// barrier.
-constexpr uint32_t kEmitWindow = 4096;
-template <bool kQuads>
-__global__ void __launch_bounds__(kEmitThreads)
-k_emit_balanced(const uint32_t* rec_sorted, const uint32_t* key_sorted, uint32_t count, const uint2* span_sorted,
-                const uint32_t* block_digit, const uint32_t* digit_total, uint32_t blocks, int tiles_x,
-                uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell, uint32_t* pair_rec,
-                EmitCounts dc) {
-    pdl_entry();
-    count = resolve_count(count, dc.count_dev);
-    if (blockIdx.x * kEmitSplats >= count) return;
-    constexpr int kWarps = kEmitThreads / 32;
-    constexpr uint32_t kStage = kEmitStage;
-    extern __shared__ uint32_t s_dyn_emit[];
-    uint32_t* s_stage_cell = s_dyn_emit;
-    uint32_t* s_stage_rec = s_stage_cell + kStage;
-    __shared__ uint2 s_sp[kEmitSplats];
-    __shared__ uint32_t s_rec[kEmitSplats], s_tag[kEmitSplats], s_off[kEmitSplats];
-    __shared__ float s_invw[kEmitSplats];
-    __shared__ uint16_t s_of[kEmitWindow];        // pair (in window) -> splat of the block
-    __shared__ uint32_t s_wc[2][kWarps][kRadix];  // per-warp digit counts of a round (double-buffered)
-    __shared__ uint32_t s_run[2][kRadix];         // block's pairs per digit before the round
-    __shared__ uint32_t s_base[kRadix], s_local[kRadix];
-    __shared__ uint32_t s_scan[32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t b = blockIdx.x;
-    const uint32_t i0 = b * kEmitSplats + 4u * tid;
-    // Phase A: the thread's 4 sorted splats, their cell counts, block offsets.
-    uint32_t nc[4], sum = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint32_t i = i0 + q;
-        const uint2 sp = i < count ? span_sorted[i] : make_uint2(0u, 0u);
-        const uint32_t w = sp.y & 0xffffu, h = sp.y >> 16;
-        nc[q] = w * h;
-        sum += nc[q];
-        const int s = 4 * tid + q;
-        s_sp[s] = sp;
-        s_rec[s] = i < count ? rec_sorted[i] : 0u;
-        const uint32_t key = i < count && key_sorted ? key_sorted[i] : 0u;
-        s_tag[s] = key_sorted && tag_shift < 32 ? (key >> tag_drop) << tag_shift : 0u;
-        s_invw[s] = w ? 1.0f / static_cast<float>(w) : 0.0f;
-    }
-    uint32_t total;
-    uint32_t run = block_excl_scan(sum, s_scan, total);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        s_off[4 * tid + q] = run;
-        run += nc[q];
-    }
-    if (tid < kRadix) {
-        const uint32_t d = static_cast<uint32_t>(tid);
-        const bool live = d <= dmask;
-        const uint32_t t = live ? digit_total[d] : 0u;
-        const uint32_t mine = live ? block_digit[d * blocks + b] : 0u;
-        const uint32_t next = !live ? 0u : (b + 1 < blocks ? block_digit[d * blocks + b + 1] : t);
-        s_base[d] = warp_incl_scan(t, lane) - t + mine;
-        const uint32_t cnt = next - mine;
-        s_local[d] = warp_incl_scan(cnt, lane) - cnt;
-        s_run[0][d] = 0u;
-    }
-    const uint32_t P = total;
-    const bool staged = P <= kStage;  // else every pair goes straight to its global slot
-    const uint32_t lt = (1u << lane) - 1u;
-    uint32_t round = 0;
-    for (uint32_t w0 = 0; w0 < P; w0 += kEmitWindow) {
-        const uint32_t w1 = min(P, w0 + kEmitWindow);
-        __syncthreads();  // the previous window's map is consumed (and phase A is visible)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {  // map the window's pairs to their splats
-            const uint32_t o = s_off[4 * tid + q];
-            for (uint32_t p = max(o, w0); p < min(o + nc[q], w1); ++p) s_of[p - w0] = static_cast<uint16_t>(4 * tid + q);
-        }
-        __syncthreads();
-        for (uint32_t r0 = w0; r0 < w1; r0 += kEmitThreads, ++round) {
-            const uint32_t p = r0 + tid;
-            const bool valid = p < w1;
-            uint32_t cell = 0u, d = 0u, s = 0u;
-            if (valid) {
-                s = s_of[p - w0];
-                const uint32_t e = p - s_off[s];
-                const uint2 sp = s_sp[s];
-                const uint32_t w = sp.y & 0xffffu;
-                uint32_t row = static_cast<uint32_t>(static_cast<float>(e) * s_invw[s]);
-                int32_t col = static_cast<int32_t>(e) - static_cast<int32_t>(row * w);
-                if (col < 0) { --row; col += static_cast<int32_t>(w); }
-                if (col >= static_cast<int32_t>(w)) { ++row; col -= static_cast<int32_t>(w); }
-                cell = cell_id<kQuads>(static_cast<int>(sp.x & 0xffffu) + col, static_cast<int>(sp.x >> 16) + static_cast<int>(row),
-                                       tiles_x);
-                d = cell & dmask;
-            }
-            // Warp multisplit on the digit: peers of this lane's digit, and lane L's count
-            // of digit L for the round's table.
-            const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-            uint32_t peers = vmask, mine_cnt = vmask;
-#pragma unroll
-            for (int bit = 0; bit < kRadixBits; ++bit) {
-                const uint32_t bb = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
-                peers &= ((d >> bit) & 1u) ? bb : ~bb;
-                mine_cnt &= ((static_cast<uint32_t>(lane) >> bit) & 1u) ? bb : ~bb;
-            }
-            const int buf = round & 1;
-            s_wc[buf][warp][lane] = __popc(mine_cnt);
-            __syncthreads();
-            if (tid < kRadix) {  // running counts for the next round
-                uint32_t t = s_run[buf][tid];
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) t += s_wc[buf][w][tid];
-                s_run[buf ^ 1][tid] = t;
-            }
-            if (valid) {
-                uint32_t pos = s_run[buf][d] + __popc(peers & lt);
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) pos += w < warp ? s_wc[buf][w][d] : 0u;
-                const uint32_t cw = cell | s_tag[s], rw = s_rec[s];
-                if (staged) {
-                    s_stage_cell[s_local[d] + pos] = cw;
-                    s_stage_rec[s_local[d] + pos] = rw;
-                } else {
-                    pair_cell[s_base[d] + pos] = cw;
-                    pair_rec[s_base[d] + pos] = rw;
-                }
-            }
-        }
-    }
-    if (!staged) return;
-    __syncthreads();
-    // Staged pairs are in digit order: each digit's run goes to consecutive global slots.
-    for (uint32_t e = tid; e < P; e += kEmitThreads) {
-        const uint32_t c = s_stage_cell[e];
-        const uint32_t d = c & dmask;
-        const uint32_t pos = s_base[d] + (e - s_local[d]);
-        pair_cell[pos] = c;
-        pair_rec[pos] = s_stage_rec[e];
-    }
-}
-
 void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_t* rec_sorted, const uint32_t* key_sorted,
                  uint32_t count, const uint2* span_sorted, uint32_t* block_digit, const uint32_t* digit_total,
                  int tiles_x, int quads, uint32_t dmask, uint32_t tag_drop, uint32_t tag_shift, uint32_t* pair_cell,
@@ -1096,23 +950,6 @@ void launch_emit(bool count_only, uint32_t blocks, cudaStream_t s, const uint32_
         return true;
     }();
     (void)attr;
-    static const bool balanced = [] {  // GSCG_EMIT_BALANCED=1: load-balanced scatter (A/B)
-        const char* e = std::getenv("GSCG_EMIT_BALANCED");
-        return e && e[0] == '1';
-    }();
-    if (!count_only && balanced) {
-        static bool battr = [] {
-            cudaFuncSetAttribute(k_emit_balanced<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitStage * 8);
-            cudaFuncSetAttribute(k_emit_balanced<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitStage * 8);
-            return true;
-        }();
-        (void)battr;
-        auto bk = quads ? k_emit_balanced<true> : k_emit_balanced<false>;
-        pdl_launch(bk, blocks, kEmitThreads, kEmitStage * 8, s, rec_sorted, key_sorted, count, span_sorted,
-                   static_cast<const uint32_t*>(block_digit), digit_total, blocks, tiles_x, dmask, tag_drop, tag_shift,
-                   pair_cell, pair_rec, dc);
-        return;
-    }
     const int smem = count_only ? kRadix * 4 : kEmitSmem;  // the count pass keeps 32 block counters
     auto kernel = count_only ? (quads ? k_emit_scatter<true, true> : k_emit_scatter<true, false>)
                              : (quads ? k_emit_scatter<false, true> : k_emit_scatter<false, false>);
