@@ -290,6 +290,9 @@ int gscg_get_splat_records(gscg_ctx* ctx, gscg_splat_record* out, uint64_t splat
 int gscg_get_cell_layout(gscg_ctx* ctx, uint32_t* tiles, uint32_t* cells_per_tile);
 int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells); /* cells x 2: [start, end) */
 int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs);
+/* SURVEY.md §8(b)'s proposed name: the sorted pair values, reported as splat ordinals
+ * (instance base + gaussian index, a frame-independent identity). Same as above. */
+int gscg_get_sorted_values(gscg_ctx* ctx, uint32_t* out, uint64_t pairs);
 /* ---- Stage functions (reference renderer.hpp:85-103) over host splat arrays ----
  * FrameSplat (renderer.hpp:39-44): the projected Splat2D, its instance and gaussian
  * index, and its pixel rect; 64 bytes. */
@@ -388,6 +391,8 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
 typedef struct gscg_group gscg_group;
 int gscg_group_unique_id(uint8_t* out /* GSCG_UNIQUE_ID_BYTES */);
 int gscg_group_create(gscg_ctx* ctx, const uint8_t* unique_id, int32_t nranks, int32_t rank, gscg_group** out);
+/* SURVEY.md §8(b)'s proposed name for gscg_group_create (same arguments and behaviour). */
+int gscg_create_group(gscg_ctx* ctx, const uint8_t* unique_id, int32_t nranks, int32_t rank, gscg_group** out);
 int gscg_group_destroy(gscg_group* group);
 int gscg_group_render_frame(gscg_group* group, const gscg_frame_desc* frame, const gscg_camera* cam,
                             const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,

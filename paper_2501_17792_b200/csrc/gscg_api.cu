@@ -2386,6 +2386,10 @@ int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
     });
 }
 
+int gscg_get_sorted_values(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
+    return gscg_get_sorted_ordinals(ctx, out, pairs);
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------------------
@@ -2483,6 +2487,10 @@ int gscg_group_create(gscg_ctx* ctx, const uint8_t* unique_id, int32_t nranks, i
         NCCL_TRY(nccl().CommInitRank(&g->comm, nranks, id, rank));
         *out = g.release();
     });
+}
+
+int gscg_create_group(gscg_ctx* ctx, const uint8_t* unique_id, int32_t nranks, int32_t rank, gscg_group** out) {
+    return gscg_group_create(ctx, unique_id, nranks, rank, out);
 }
 
 int gscg_group_destroy(gscg_group* g) {

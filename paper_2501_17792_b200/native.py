@@ -152,6 +152,7 @@ GSCG_SYMBOLS = {
     "gscg_set_region": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "gscg_group_unique_id": (C.c_int, [_P]),
     "gscg_group_create": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "gscg_create_group": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(_P)]),
     "gscg_group_destroy": (C.c_int, [_P]),
     "gscg_group_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                           C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), C.c_int32, _P,
@@ -194,6 +195,7 @@ GSCG_SYMBOLS = {
     "gscg_get_cell_layout": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "gscg_get_tile_ranges": (C.c_int, [_P, _P, C.c_uint32]),
     "gscg_get_sorted_ordinals": (C.c_int, [_P, _P, C.c_uint64]),
+    "gscg_get_sorted_values": (C.c_int, [_P, _P, C.c_uint64]),
     "gscg_project_shard": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                      C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), C.c_uint32,
                                      C.c_uint32, C.c_uint32, _P, _P, C.POINTER(GscgStageTimes)]),
