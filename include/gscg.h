@@ -187,6 +187,8 @@ int gscg_device_count(int* out);
 int gscg_upload_skeleton(gscg_ctx* ctx, uint32_t template_id, const gscg_skeleton_desc* desc);
 int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level,
                       const gscg_level_desc* desc);
+/* SURVEY.md §8(b)'s proposed name for gscg_upload_level (same arguments and behaviour). */
+int gscg_upload_template(gscg_ctx* ctx, uint32_t template_id, uint32_t level, const gscg_level_desc* desc);
 /* Device bytes held by uploaded templates (shared attribute store). */
 int gscg_template_bytes(const gscg_ctx* ctx, uint64_t* out);
 /* Replaces (id < count) or appends (id == count) a motion clip. */

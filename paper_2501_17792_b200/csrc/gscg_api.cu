@@ -1439,6 +1439,10 @@ int gscg_upload_skeleton(gscg_ctx* ctx, uint32_t template_id, const gscg_skeleto
     });
 }
 
+int gscg_upload_template(gscg_ctx* ctx, uint32_t template_id, uint32_t level, const gscg_level_desc* desc) {
+    return gscg_upload_level(ctx, template_id, level, desc);
+}
+
 int gscg_upload_level(gscg_ctx* ctx, uint32_t template_id, uint32_t level, const gscg_level_desc* d) {
     if (!ctx) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {

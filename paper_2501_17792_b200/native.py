@@ -143,6 +143,7 @@ GSCG_SYMBOLS = {
     "gscg_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "gscg_upload_skeleton": (C.c_int, [_P, C.c_uint32, _P]),
     "gscg_upload_level": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
+    "gscg_upload_template": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "gscg_template_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "gscg_upload_motion": (C.c_int, [_P, C.c_uint32, C.POINTER(GscgMotionDesc)]),
     "gscg_eval_sinf": (C.c_int, [_P, _P, _P, C.c_uint32]),
