@@ -1097,7 +1097,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             CUDA_TRY(pdl_launch(k_depth_bucket_count, grid, kBucketThreads, bp.buckets * 4ull, s, bp));
             CUDA_TRY(pdl_launch(k_depth_bucket_scan, 1, 1024, 0, s, bp));
             CUDA_TRY(pdl_launch(k_depth_bucket_scatter, (S32 + kBucketScatterTile - 1) / kBucketScatterTile, kBucketThreads,
-                                kBucketScatterSmem, s, bp));
+                                bp.buckets * 4ull, s, bp));
             CUDA_TRY(pdl_launch(k_depth_bucket_local, bp.buckets, kBucketLocalThreads, kBucketLocalCap * 16ull, s, bp));
             launches += 4;
             dplan.passes = 2;  // reported sort passes: the two bucket levels
@@ -1326,7 +1326,7 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaFuncSetAttribute(k_depth_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kMaxDepthBuckets * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_depth_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kBucketScatterSmem));
+                                      kMaxDepthBuckets * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_depth_bucket_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kBucketLocalCap * 16));
     });

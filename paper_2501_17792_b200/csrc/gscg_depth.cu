@@ -121,28 +121,20 @@ k_depth_bucket_scan(DepthBucketParams p) {
     if (threadIdx.x == 1023) p.bucket_start[p.buckets] = carry;
 }
 
-// The CTA's splats are first placed in shared memory in bucket order (local start of the
-// bucket + rank), then written out by consecutive local positions: the CTA's share of a
-// bucket is one run of consecutive global slots, so neighbouring threads write
-// neighbouring 16-byte slots instead of one scattered sector each. s_hist holds the
-// counts, then the local starts, then (global base - local start) per bucket.
 __global__ void __launch_bounds__(kBucketThreads)
 k_depth_bucket_scatter(DepthBucketParams p) {
     pdl_entry();
-    extern __shared__ uint32_t s_dyn_scatter[];
-    uint32_t* s_hist = s_dyn_scatter;                                            // kMaxDepthBuckets + 1
-    uint4* s_stage = reinterpret_cast<uint4*>(s_dyn_scatter + kMaxDepthBuckets + 4);  // kBucketScatterTile
-    __shared__ uint32_t s_warp[32];
+    extern __shared__ uint32_t s_hist[];  // counts, then each bin's global slot base
     const uint32_t base = blockIdx.x * kBucketScatterTile;
-    const uint32_t n_here = min(kBucketScatterTile, p.count - base);
-    // Every load of the thread in flight at once (the splat meta carries the depth bits).
+    // Every load of the thread in flight at once (the splat meta carries the depth bits),
+    // so the CTA pays one memory latency, then the reservations' one.
     uint4 m[kBucketScatterItems];
 #pragma unroll
     for (int j = 0; j < kBucketScatterItems; ++j) {
         const uint32_t i = base + j * kBucketThreads + threadIdx.x;
         if (i < p.count) m[j] = p.meta[i];  // (ordinal, span lo, span hi, dbits), coalesced
     }
-    for (uint32_t b = threadIdx.x; b <= kMaxDepthBuckets; b += kBucketThreads) s_hist[b] = 0u;  // the scan reads all
+    for (uint32_t b = threadIdx.x; b < p.buckets; b += kBucketThreads) s_hist[b] = 0u;
     __syncthreads();
     // (bucket << 16 | rank in the CTA's share of the bucket); ranks < kBucketScatterTile.
     uint32_t br[kBucketScatterItems];
@@ -156,55 +148,34 @@ k_depth_bucket_scatter(DepthBucketParams p) {
         }
     }
     __syncthreads();
-    // Local starts: exclusive scan of the counts, thread t owning kPer consecutive bins.
-    constexpr uint32_t kPer = kMaxDepthBuckets / kBucketThreads;
-    {
-        const uint32_t b0 = threadIdx.x * kPer;
-        uint32_t v[kPer], sum = 0;
+    {  // one global reservation per non-empty bin, a half of the thread's bins in flight at once
+        constexpr uint32_t kPer = kMaxDepthBuckets / kBucketThreads / 2;
 #pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) {
-            v[q] = s_hist[b0 + q];  // bins past p.buckets are zero
-            sum += v[q];
-        }
-        uint32_t total;
-        uint32_t run = cta_excl_scan(sum, s_warp, total);
+        for (uint32_t half = 0; half < 2; ++half) {
+            uint32_t h[kPer];
 #pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) {
-            s_hist[b0 + q] = run;
-            run += v[q];
+            for (uint32_t q = 0; q < kPer; ++q) {
+                const uint32_t b = (half * kPer + q) * kBucketThreads + threadIdx.x;
+                h[q] = b < p.buckets ? s_hist[b] : 0u;
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < kPer; ++q)
+                if (h[q]) h[q] = atomicAdd(&p.bucket_cursor[(half * kPer + q) * kBucketThreads + threadIdx.x], h[q]);
+#pragma unroll
+            for (uint32_t q = 0; q < kPer; ++q) {
+                const uint32_t b = (half * kPer + q) * kBucketThreads + threadIdx.x;
+                if (b < p.buckets) s_hist[b] = h[q];
+            }
         }
-        if (threadIdx.x == 0) s_hist[kMaxDepthBuckets] = total;
     }
     __syncthreads();
-    // Bucket order in shared memory.
 #pragma unroll
     for (int j = 0; j < kBucketScatterItems; ++j) {
         const uint32_t i = base + j * kBucketThreads + threadIdx.x;
-        if (i < p.count) s_stage[s_hist[br[j] >> 16] + (br[j] & 0xffffu)] = make_uint4(m[j].w, i, m[j].y, m[j].z);
-    }
-    // One global reservation per non-empty bin (all of a thread's in flight), then
-    // s_hist[b] = global base - local start.
-    {
-        const uint32_t b0 = threadIdx.x * kPer;
-        uint32_t st[kPer + 1];
-#pragma unroll
-        for (uint32_t q = 0; q <= kPer; ++q) st[q] = s_hist[b0 + q];
-        uint32_t g[kPer];
-#pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) {
-            const uint32_t c = st[q + 1] - st[q];
-            g[q] = c && b0 + q < p.buckets ? atomicAdd(&p.bucket_cursor[b0 + q], c) : 0u;
+        if (i < p.count) {
+            GSCG_DCHECK(s_hist[br[j] >> 16] + (br[j] & 0xffffu) < p.count);
+            p.staged[s_hist[br[j] >> 16] + (br[j] & 0xffffu)] = make_uint4(m[j].w, i, m[j].y, m[j].z);
         }
-        __syncthreads();  // every start read (and every element placed) before the overwrite
-#pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) s_hist[b0 + q] = g[q] - st[q];
-    }
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < n_here; q += kBucketThreads) {
-        const uint4 e = s_stage[q];
-        const uint32_t dst = s_hist[depth_bucket(p, e.x)] + q;
-        GSCG_DCHECK(dst < p.count);
-        p.staged[dst] = e;
     }
 }
 

@@ -220,7 +220,6 @@ constexpr int kBucketScatterItems = 8;
 constexpr uint32_t kBucketScatterTile = kBucketThreads * kBucketScatterItems;  // splats per scatter CTA (ranks < 2^16)
 constexpr int kBucketTopBits = 14;
 constexpr uint32_t kMaxDepthBuckets = 1u << kBucketTopBits;       // top bits of T (64 KB shared histogram)
-constexpr int kBucketScatterSmem = (kMaxDepthBuckets + 4) * 4 + kBucketScatterTile * 16;  // bins + staged tile
 constexpr int kBucketLocalThreads = 256;
 constexpr uint32_t kBucketLocalBins = 2048;                        // low bits of T per bucket (T <= 25 bits)
 constexpr uint32_t kBucketLocalCap = 2048;                         // splats per bulk-copied chunk (32 KB)
