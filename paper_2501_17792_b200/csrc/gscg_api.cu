@@ -944,11 +944,20 @@ int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, D
     return out ^ 1;
 }
 
-// The cheapest LSD plan for `bits` key bits: w wide passes (<= 7 bits, ~1.36x the cost of
-// a 5-bit pass on this B200) then n 5-bit passes, minimising 1.36 w + n; bits spread evenly
-// within each kind (27 -> 7,5,5,5,5; 25 -> 5,5,5,5,5; 12 -> 7,5). 8-bit digits ranked with
-// warp match (CUB onesweep style) measured slower here: __match_any_sync is slow on sm_100
-// (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
+// The cheapest LSD plan for `bits` key bits: w wide passes (<= 7 bits) then n 5-bit
+// passes, minimising cost(wide) w + n. A wide pass measures 2.16x a 5-bit pass on the
+// 61.7 M cell pairs of config 4 (529 vs 245 us: its upsweep ranks with shared counters),
+// more than the two 5-bit passes it would replace, so plans use 5-bit passes only (12 cell
+// bits -> 4, 4, 4); GSCG_WIDE_PASSES=1 restores the round-1 cost model (1.36) for A/B.
+// 8-bit digits ranked with warp match (CUB onesweep style) measured slower still:
+// __match_any_sync is slow on sm_100 (upsweep 74 vs 31 us, downsweep 126 vs 77 us per pass).
+uint32_t wide_cost() {  // per 100 of a 5-bit pass
+    static const uint32_t c = [] {
+        const char* e = std::getenv("GSCG_WIDE_PASSES");
+        return e && e[0] == '1' ? 136u : 216u;
+    }();
+    return c;
+}
 RadixPlan make_plan(uint32_t bits) {
     RadixPlan pl{};
     bits = std::max(bits, 1u);
@@ -956,7 +965,7 @@ RadixPlan make_plan(uint32_t bits) {
     for (uint32_t w = 1; w * kWideBits < bits + kWideBits; ++w) {
         const uint32_t rest = bits > w * kWideBits ? bits - w * kWideBits : 0u;
         const uint32_t n = (rest + kRadixBits - 1) / kRadixBits;
-        if (136 * w + 100 * n < 136 * best_w + 100 * best_n) {
+        if (wide_cost() * w + 100 * n < wide_cost() * best_w + 100 * best_n) {
             best_w = w;
             best_n = n;
         }
