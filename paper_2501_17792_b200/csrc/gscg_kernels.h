@@ -218,7 +218,7 @@ constexpr int kBucketItems = 16;
 constexpr uint32_t kBucketTile = kBucketThreads * kBucketItems;  // splats per count CTA
 constexpr int kBucketScatterItems = 8;
 constexpr uint32_t kBucketScatterTile = kBucketThreads * kBucketScatterItems;  // splats per scatter CTA (ranks < 2^16)
-constexpr int kBucketTopBits = 14;
+constexpr int kBucketTopBits = 15;
 constexpr uint32_t kMaxDepthBuckets = 1u << kBucketTopBits;       // top bits of T (64 KB shared histogram)
 constexpr int kBucketLocalThreads = 256;
 constexpr uint32_t kBucketLocalBins = 2048;                        // low bits of T per bucket (T <= 25 bits)
