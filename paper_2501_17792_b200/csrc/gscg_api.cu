@@ -121,10 +121,11 @@ struct DevBuf {
 // Varying depth bits the splat sort orders (LSD passes of <= 5 bits); the lower bits and
 // the ordinal tie-break are settled per cell by k_cell_fixup.
 constexpr uint32_t kDepthSortBits = 25;
-// Frames past this many splats take the LSD depth passes: the average bucket (S / 16,384)
-// outgrows the coalesced local sort. Measured: config 3 (10.9 M) 0.99 -> 0.82 ms sort,
-// config 4 (25.7 M) equal, config 5 (519 M) 51 vs 85 ms in favour of LSD.
-constexpr uint64_t kBucketMaxSplats = 20000000;
+// Frames past this many splats take the LSD depth passes: the average bucket outgrows the
+// coalesced local sort. Measured sort stage: config 3 (10.9 M) 0.99 -> 0.82 ms, config 4
+// (25.7 M, 2^15 buckets) 2.59 -> 2.40 ms, config 5 (519 M) 51 vs 85 ms in favour of LSD.
+constexpr uint64_t kBucketMaxSplats = 40000000;
+constexpr uint32_t kBucketWideSplats = 16000000;  // frames past this use 2^15 top-level buckets
 
 struct LevelStore {
     uint32_t count = 0;
@@ -1073,7 +1074,10 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         // deferred frames (counts and depth range still on the device) the LSD passes.
         const uint32_t tag_min = ctx->dmin >> drop, tag_range = (ctx->dmax >> drop) - tag_min;
         const uint32_t range_bits = static_cast<uint32_t>(bits_for(tag_range));
-        const uint32_t local_bits = range_bits > kBucketTopBits ? range_bits - kBucketTopBits : 0u;
+        // Top-level buckets: 2^14 up to 16 M splats, 2^15 above (config 3: 14 bits 0.82 vs 15 bits
+        // 0.86 ms sort; config 4: 15 bits 2.40 ms vs the LSD passes' 2.59).
+        const uint32_t top_bits = S32 > kBucketWideSplats ? static_cast<uint32_t>(kBucketTopBits) : 14u;
+        const uint32_t local_bits = range_bits > top_bits ? range_bits - top_bits : 0u;
         const bool buckets = !presorted && !device_counts && (1u << local_bits) <= kBucketLocalBins &&
                              S32 <= ctx->bucket_max_splats;
         RadixPlan dplan{};

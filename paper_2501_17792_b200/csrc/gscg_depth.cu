@@ -150,9 +150,7 @@ k_depth_bucket_scatter(DepthBucketParams p) {
     __syncthreads();
     {  // one global reservation per non-empty bin, a batch of the thread's bins in flight at once
         constexpr uint32_t kPer = 8;  // bins per batch (registers)
-        constexpr uint32_t kBatches = kMaxDepthBuckets / kBucketThreads / kPer;
-#pragma unroll
-        for (uint32_t half = 0; half < kBatches; ++half) {
+        for (uint32_t half = 0; half * kPer * kBucketThreads < p.buckets; ++half) {
             uint32_t h[kPer];
 #pragma unroll
             for (uint32_t q = 0; q < kPer; ++q) {

@@ -219,7 +219,7 @@ constexpr uint32_t kBucketTile = kBucketThreads * kBucketItems;  // splats per c
 constexpr int kBucketScatterItems = 8;
 constexpr uint32_t kBucketScatterTile = kBucketThreads * kBucketScatterItems;  // splats per scatter CTA (ranks < 2^16)
 constexpr int kBucketTopBits = 15;
-constexpr uint32_t kMaxDepthBuckets = 1u << kBucketTopBits;       // top bits of T (64 KB shared histogram)
+constexpr uint32_t kMaxDepthBuckets = 1u << kBucketTopBits;       // top bits of T (<= 128 KB shared histogram)
 constexpr int kBucketLocalThreads = 256;
 constexpr uint32_t kBucketLocalBins = 2048;                        // low bits of T per bucket (T <= 25 bits)
 constexpr uint32_t kBucketLocalCap = 2048;                         // splats per bulk-copied chunk (32 KB)
