@@ -88,19 +88,20 @@ k_depth_bucket_count(DepthBucketParams p) {
     }
 }
 
-// Bucket starts: warp w scans buckets [w * 512, (w + 1) * 512) in lane-contiguous chunks
-// of 32 (coalesced loads and stores), then the warp totals.
+// Bucket starts: warp w scans buckets [w * 32 c, (w + 1) * 32 c), c = ceil(buckets / 1024)
+// lane-contiguous chunks of 32 (coalesced loads and stores), then the warp totals.
 __global__ void __launch_bounds__(1024)
 k_depth_bucket_scan(DepthBucketParams p) {
     pdl_entry();
     __shared__ uint32_t s_warp[32];
-    constexpr uint32_t kChunks = kMaxDepthBuckets / 1024;  // 32-bucket chunks per warp
+    constexpr uint32_t kChunks = kMaxDepthBuckets / 1024;  // most 32-bucket chunks per warp
+    const uint32_t nch = (p.buckets + 1023) / 1024;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     uint32_t v[kChunks], wsum = 0;
 #pragma unroll
     for (uint32_t c = 0; c < kChunks; ++c) {
-        const uint32_t bk = (warp * kChunks + c) * 32u + lane;
-        v[c] = bk < p.buckets ? p.bucket_count[bk] : 0u;
+        const uint32_t bk = (warp * nch + c) * 32u + lane;
+        v[c] = c < nch && bk < p.buckets ? p.bucket_count[bk] : 0u;
         wsum += v[c];
     }
     wsum = __reduce_add_sync(0xffffffffu, wsum);
@@ -110,7 +111,8 @@ k_depth_bucket_scan(DepthBucketParams p) {
     for (uint32_t w = 0; w < warp; ++w) carry += s_warp[w];
 #pragma unroll
     for (uint32_t c = 0; c < kChunks; ++c) {
-        const uint32_t bk = (warp * kChunks + c) * 32u + lane;
+        if (c >= nch) break;
+        const uint32_t bk = (warp * nch + c) * 32u + lane;
         const uint32_t incl = warp_incl_scan_u32(v[c], static_cast<int>(lane));
         if (bk < p.buckets) {
             p.bucket_start[bk] = carry + incl - v[c];
