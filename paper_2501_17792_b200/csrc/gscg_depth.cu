@@ -9,8 +9,8 @@
 // ordinal). Splats with equal T may therefore come out in any order, which lets both
 // levels rank with shared-memory atomics instead of a stable multisplit:
 //
-//   k_depth_bucket_count   histogram of the top bits of T (<= 16,384 buckets) per CTA of
-//                          16,384 splats, flushed with one global atomic per non-empty bin
+//   k_depth_bucket_count   histogram of the top 14 bits of T (15 past 16 M splats) per CTA
+//                          of 16,384 splats, flushed with one global atomic per non-empty bin
 //   k_depth_bucket_scan    bucket starts (one CTA)
 //   k_depth_bucket_scatter every splat reserves its slot in its bucket (a shared atomic for
 //                          the rank inside the CTA, one global atomic per (CTA, bucket)) and
