@@ -1,3 +1,4 @@
+# Print the bench lines of a gpu_env_ab.sh run (TAG as the argument).
 T=$1
 cat gpurun_out/${T}_status.txt
 for f in $(ls gpurun_out/${T}_*.log | sort -V); do python - $f <<'PY'

@@ -1,3 +1,4 @@
+# Print the tests, bench line and launch list of a gpu_quick.sh run (TAG as the argument).
 T=$1
 cat gpurun_out/${T}_status.txt; tail -1 gpurun_out/${T}_tests.log
 python - $T <<'PY'
