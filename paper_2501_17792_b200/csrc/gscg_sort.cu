@@ -569,19 +569,29 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
     const bool has_beyond = cta0 + n_ext < count;
     const uint32_t beyond_key = fix && has_beyond ? keys[cta0 + n_ext] : 0u;
     const uint32_t t0 = tid * kStreamItems;
-    // Keys only: a pair's record is read (and staged) only if it ties with a neighbour (~2%
-    // of the pairs at config 3); untied records never move.
-    uint32_t k[kStreamItems];
+    uint32_t k[kStreamItems], r[kStreamItems];
     if (n_here == kTile) {
         const uint4 klo = *reinterpret_cast<const uint4*>(keys + cta0 + t0);
         const uint4 khi = *reinterpret_cast<const uint4*>(keys + cta0 + t0 + 4);
         k[0] = klo.x; k[1] = klo.y; k[2] = klo.z; k[3] = klo.w; k[4] = khi.x; k[5] = khi.y; k[6] = khi.z; k[7] = khi.w;
+        if (fix) {
+            const uint4 rlo = *reinterpret_cast<const uint4*>(recs + cta0 + t0);
+            const uint4 rhi = *reinterpret_cast<const uint4*>(recs + cta0 + t0 + 4);
+            r[0] = rlo.x; r[1] = rlo.y; r[2] = rlo.z; r[3] = rlo.w; r[4] = rhi.x; r[5] = rhi.y; r[6] = rhi.z; r[7] = rhi.w;
+        }
     } else {
 #pragma unroll
-        for (uint32_t j = 0; j < kStreamItems; ++j) k[j] = t0 + j < n_here ? keys[cta0 + t0 + j] : 0u;
+        for (uint32_t j = 0; j < kStreamItems; ++j) {
+            const bool in = t0 + j < n_here;
+            k[j] = in ? keys[cta0 + t0 + j] : 0u;
+            r[j] = in && fix ? recs[cta0 + t0 + j] : 0u;
+        }
     }
 #pragma unroll
-    for (uint32_t j = 0; j < kStreamItems; ++j) s_key[j * kThreads + tid] = k[j];
+    for (uint32_t j = 0; j < kStreamItems; ++j) {
+        s_key[j * kThreads + tid] = k[j];
+        if (fix) s_rec[j * kThreads + tid] = r[j];
+    }
     if (fix && tid < kHalo && kTile + tid < n_ext) {
         s_key[kTile + tid] = keys[cta0 + kTile + tid];
         s_rec[kTile + tid] = recs[cta0 + kTile + tid];
@@ -617,18 +627,11 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
         left[j] = in && (j > 0 ? k[j - 1] == k[j] : (has_left && left_key == k[j]));
         const bool right = j + 1 < kStreamItems ? (pos + 1 < n_here && k[j + 1] == k[j]) : (has_right && right_key == k[j]);
         tie[j] = in && (left[j] || right);
+        m[j] = tie[j] ? meta[r[j]] : make_uint4(0u, 0u, 0u, 0u);
     }
-    uint32_t r[kStreamItems];
-#pragma unroll
-    for (uint32_t j = 0; j < kStreamItems; ++j) r[j] = tie[j] ? recs[cta0 + t0 + j] : 0u;
-#pragma unroll
-    for (uint32_t j = 0; j < kStreamItems; ++j) m[j] = tie[j] ? meta[r[j]] : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
     for (uint32_t j = 0; j < kStreamItems; ++j)
-        if (tie[j]) {
-            s_rec[j * kThreads + tid] = r[j];
-            s_ord[j * kThreads + tid] = pair_order_key(m[j]);
-        }
+        if (tie[j]) s_ord[j * kThreads + tid] = pair_order_key(m[j]);
     if (tid < kHalo && n_here == kTile) {  // the run leaving the tile, into the halo
         const uint32_t p = kTile + tid;
         const bool eq = p < n_ext && s_key[p] == s_key[slot(kTile - 1)];
@@ -703,10 +706,18 @@ k_cell_fixup(const uint32_t* keys, uint32_t* recs, const uint4* meta, uint32_t c
     // the run entering from the previous tile (stored by that tile, or deferred).
     const uint32_t e0 = s_enter_end;
     if (!((s_dirty[warp] >> lane) & 1u)) return;
+    if (n_here == kTile && t0 >= e0) {
+        uint32_t o[kStreamItems];
 #pragma unroll
-    for (uint32_t j = 0; j < kStreamItems; ++j) {  // only tied pairs can have moved
-        const uint32_t pos = t0 + j;
-        if (tie[j] && pos >= e0 && pos < n_here) recs[cta0 + pos] = s_rec[j * kThreads + tid];
+        for (uint32_t j = 0; j < kStreamItems; ++j) o[j] = s_rec[j * kThreads + tid];
+        *reinterpret_cast<uint4*>(recs + cta0 + t0) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(recs + cta0 + t0 + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+        for (uint32_t j = 0; j < kStreamItems; ++j) {
+            const uint32_t pos = t0 + j;
+            if (pos >= e0 && pos < n_here) recs[cta0 + pos] = s_rec[j * kThreads + tid];
+        }
     }
 }
 
