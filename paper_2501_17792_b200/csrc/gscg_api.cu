@@ -48,6 +48,13 @@ uint64_t pdl_max_splats() {  // GSCG_PDL_MAX_SPLATS overrides the cut (A/B measu
     return v;
 }
 thread_local bool t_pdl_frame = true;
+bool overlap_update() {  // GSCG_OVERLAP_UPDATE=1: the update stage on its own stream (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("GSCG_OVERLAP_UPDATE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 bool gscg::pdl_enabled() {
     static const bool on = [] {
@@ -212,6 +219,12 @@ struct gscg_ctx {
     uint32_t dbits_prev = kDepthSortBits;       // varying depth bits of the last settled frame
     uint32_t deferred_depth_top = 32;           // key bits a deferred frame's depth plan covers
     cudaEvent_t counters_ev = nullptr;          // the frame's counters are in h_counters
+    // Update-stage overlap (render_frame): the next frame's pose sampling, FK, cull and plan
+    // run on upd_stream once upd_ok (this frame's project, counters and LoD write-back) has
+    // passed, i.e. under this frame's sort and raster; the project waits on upd_done.
+    cudaStream_t upd_stream = nullptr;
+    cudaEvent_t upd_ok = nullptr, upd_done = nullptr;
+    bool upd_ok_recorded = false;
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
@@ -533,8 +546,17 @@ bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool
 // enqueues the sort on device counts and then calls settle_counts.
 void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
                    const gscg_lod_policy* lod, uint32_t shard_begin, uint32_t shard_end, uint32_t& launches,
-                   bool lod_back = false, bool deferred = false) {
+                   bool lod_back = false, bool deferred = false, bool overlap_update = false) {
     cudaStream_t s = ctx->stream;
+    // The update stage (H2D, poses, FK, cull, plan) on the update stream when overlapped.
+    cudaStream_t su = overlap_update ? ctx->upd_stream : s;
+    if (overlap_update) {
+        // After an overlapped frame: wait for its project / counters / LoD write-back only.
+        // Otherwise for everything enqueued on the render stream so far.
+        if (!ctx->upd_ok_recorded) CUDA_TRY(cudaEventRecord(ctx->upd_ok, s));
+        CUDA_TRY(cudaStreamWaitEvent(su, ctx->upd_ok, 0));
+    }
+    ctx->upd_ok_recorded = false;
     const FrameGeom& geo = ctx->geom;
     const gscg_render_settings* settings = &ctx->settings;
     const bool host = frame->memory == GSCG_MEM_HOST;
@@ -559,7 +581,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
     CUDA_TRY(ctx->skin.ensure(std::max<size_t>(n, 1) * js * 12 * 4));
 
     // ---- H2D ----
-    CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
+    CUDA_TRY(cudaEventRecord(ctx->ev[0], su));
     const uint32_t *d_tid, *d_lodprev;
     const float *d_place, *d_poses;
     const bool sampled = frame->pose_source == GSCG_POSES_SAMPLED;
@@ -600,7 +622,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         }
         if (nseg) {
             const uint32_t bx = std::min<uint32_t>((max_words + 255) / 256, 4u * ctx->sm_count);
-            CUDA_TRY(pdl_launch(k_copy_segments, dim3(bx, nseg), 256, 0, s, segs));
+            CUDA_TRY(pdl_launch(k_copy_segments, dim3(bx, nseg), 256, 0, su, segs));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -618,7 +640,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         d_mid = frame->motion_ids;
         d_phase = frame->phase_offsets;
     }
-    CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
+    CUDA_TRY(cudaEventRecord(ctx->ev[1], su));
     if (sampled && shard_end > shard_begin && !posed_mode) {
         // update_crowd's pose sampling on the device (gscg_pose.cu); FK reads ctx->poses.
         PoseParams pp{};
@@ -633,7 +655,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pp.keys = ctx->d_keys.as<KeyPairDev>();
         pp.poses = ctx->poses.as<float>();
         const uint64_t threads = static_cast<uint64_t>(n) * (frame->joint_stride + 1);
-        CUDA_TRY(pdl_launch(k_sample_poses, static_cast<uint32_t>((threads + 255) / 256), 256, 0, s, pp));
+        CUDA_TRY(pdl_launch(k_sample_poses, static_cast<uint32_t>((threads + 255) / 256), 256, 0, su, pp));
         ++launches;
         CUDA_TRY(cudaGetLastError());
     }
@@ -682,7 +704,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             fp.skin = ctx->skin.as<float>();
             const int per_block = kFkThreads / 16;
             const uint32_t m = shard_end - shard_begin;
-            CUDA_TRY(pdl_launch(k_fk_skin, (m + per_block - 1) / per_block, kFkThreads, per_block * kFkSmemPerInstance(js), s, fp));
+            CUDA_TRY(pdl_launch(k_fk_skin, (m + per_block - 1) / per_block, kFkThreads, per_block * kFkSmemPerInstance(js), su, fp));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -701,7 +723,7 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             cp.cam = camdev;
             cp.visible = ctx->visible.as<uint32_t>();
             const uint32_t m = shard_end - shard_begin;
-            CUDA_TRY(pdl_launch(k_inst_cull, (m + 7) / 8, 256, 0, s, cp));
+            CUDA_TRY(pdl_launch(k_inst_cull, (m + 7) / 8, 256, 0, su, cp));
             ++launches;
             CUDA_TRY(cudaGetLastError());
         }
@@ -729,10 +751,14 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pp.members = ctx->members.as<uint32_t>();
         pp.visible = cull ? ctx->visible.as<uint32_t>() : posed_mode ? ctx->project_mask.as<uint32_t>() : nullptr;
         pp.counters = counters;
-        CUDA_TRY(pdl_launch(k_lod_plan, 1, 1024, 0, s, pp));
+        CUDA_TRY(pdl_launch(k_lod_plan, 1, 1024, 0, su, pp));
         ++launches;
         CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
+        CUDA_TRY(cudaEventRecord(ctx->ev[2], su));
+        if (su != s) {  // the render stream (project, counters) waits for the update stage
+            CUDA_TRY(cudaEventRecord(ctx->upd_done, su));
+            CUDA_TRY(cudaStreamWaitEvent(s, ctx->upd_done, 0));
+        }
 
         const bool naive = ctx->layout == GSCG_LAYOUT_NAIVE && !posed_mode && !skin_only;
         if (naive) {
@@ -1324,6 +1350,9 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->rb_ev_alt, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->pend_ev, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->counters_ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->upd_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->upd_ok, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->upd_done, cudaEventDisableTiming));
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_band_counts), GSCG_MAX_BANDS * sizeof(unsigned long long)));
@@ -1388,6 +1417,12 @@ int gscg_destroy(gscg_ctx* ctx) {
     if (ctx->rb_ev_alt) cudaEventDestroy(ctx->rb_ev_alt);
     if (ctx->pend_ev) cudaEventDestroy(ctx->pend_ev);
     if (ctx->counters_ev) cudaEventDestroy(ctx->counters_ev);
+    if (ctx->upd_stream) {
+        cudaStreamSynchronize(ctx->upd_stream);
+        cudaStreamDestroy(ctx->upd_stream);
+    }
+    if (ctx->upd_ok) cudaEventDestroy(ctx->upd_ok);
+    if (ctx->upd_done) cudaEventDestroy(ctx->upd_done);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1648,12 +1683,21 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                 nvtxRangePop();
             }
         } else {
-            update_gather(ctx, frame, cam, lod, 0, n, launches, host);
+            update_gather(ctx, frame, cam, lod, 0, n, launches, host, false, overlap_update());
+            if (overlap_update()) {
+                // The LoD write-back now (lod_out is final), then upd_ok: the next frame's
+                // update stage may start under this frame's sort and raster.
+                if (n && !host)
+                    CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice,
+                                             ctx->stream));
+                CUDA_TRY(cudaEventRecord(ctx->upd_ok, ctx->stream));
+                ctx->upd_ok_recorded = true;
+            }
             passes = enqueue_sort(false);
         }
         nvtxRangePop();
         if (!overlap) copy_out(ctx, g.band_y1 - g.band_y0, fb_rgb, fb_T, host);  // region rows x region width
-        if (n && !host)
+        if (n && !host && (deferred || !overlap_update()))
             CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice,
                                      ctx->stream));
         CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->stream));
