@@ -133,7 +133,10 @@ class Scene:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            N.gsch().gsch_scene_destroy(self._h)
+            try:
+                N.gsch().gsch_scene_destroy(self._h)
+            except TypeError:  # interpreter shutdown: the module's globals are already gone
+                pass
             self._h = None
 
     @property
@@ -346,7 +349,10 @@ class Renderer:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            N.gsch().gsch_renderer_destroy(self._h)
+            try:
+                N.gsch().gsch_renderer_destroy(self._h)
+            except TypeError:  # interpreter shutdown: the module's globals are already gone
+                pass
             self._h = None
 
     @property

@@ -48,10 +48,12 @@ uint64_t pdl_max_splats() {  // GSCG_PDL_MAX_SPLATS overrides the cut (A/B measu
     return v;
 }
 thread_local bool t_pdl_frame = true;
-bool overlap_update() {  // GSCG_OVERLAP_UPDATE=1: the update stage on its own stream (A/B)
+// The update stage of render_frame on its own stream, under the previous frame's sort and
+// raster (config 3: 591 vs 573 FPS device); GSCG_OVERLAP_UPDATE=0 keeps it in line (A/B).
+bool overlap_update() {
     static const bool on = [] {
         const char* e = std::getenv("GSCG_OVERLAP_UPDATE");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
     return on;
 }
