@@ -48,8 +48,9 @@ uint64_t pdl_max_splats() {  // GSCG_PDL_MAX_SPLATS overrides the cut (A/B measu
     return v;
 }
 thread_local bool t_pdl_frame = true;
-// The update stage of render_frame on its own stream, under the previous frame's sort and
-// raster (config 3: 591 vs 573 FPS device); GSCG_OVERLAP_UPDATE=0 keeps it in line (A/B).
+// Frame pipelining of render_frame (see gscg_ctx::upd_stream); GSCG_OVERLAP_UPDATE=0 keeps
+// every frame on one stream (A/B).
+constexpr uint64_t kPipelineMaxSplats = 64000000;
 bool overlap_update() {
     static const bool on = [] {
         const char* e = std::getenv("GSCG_OVERLAP_UPDATE");
@@ -213,7 +214,13 @@ struct gscg_ctx {
     DevBuf inst_group, inst_base, members, group_inst_start, group_inst_count, group_item_start, visible;
     DevBuf skin, counters;
     // gather outputs
-    DevBuf records, splat_meta, splat_depth;
+    // Per-splat outputs of the projection, one set per frame slot: with frame pipelining the
+    // next frame's projection writes one slot while this frame's sort and raster read the other.
+    DevBuf records_s[2], splat_meta_s[2], splat_depth_s[2];
+    int slot = 0;
+    DevBuf& rec() { return records_s[slot]; }
+    DevBuf& meta() { return splat_meta_s[slot]; }
+    DevBuf& depth() { return splat_depth_s[slot]; }
     uint64_t splat_capacity = 0, pair_capacity = 0;
     uint32_t culled = 0;  // instances dropped by k_inst_cull in the last frame
     uint32_t depth_sort_bits = kDepthSortBits;  // top varying depth bits the splat sort orders
@@ -221,12 +228,17 @@ struct gscg_ctx {
     uint32_t dbits_prev = kDepthSortBits;       // varying depth bits of the last settled frame
     uint32_t deferred_depth_top = 32;           // key bits a deferred frame's depth plan covers
     cudaEvent_t counters_ev = nullptr;          // the frame's counters are in h_counters
-    // Update-stage overlap (render_frame): the next frame's pose sampling, FK, cull and plan
-    // run on upd_stream once upd_ok (this frame's project, counters and LoD write-back) has
-    // passed, i.e. under this frame's sort and raster; the project waits on upd_done.
+    // Frame pipelining (render_frame): a frame's front half (H2D, poses, FK, cull, plan,
+    // projection, counters, LoD write-back) runs on upd_stream, its back half (sort, raster,
+    // read-back) on `stream`, so the next frame's front half runs under this frame's back
+    // half. The projection writes the frame's slot (records / meta / depth), which the back
+    // half of the frame two back read: slot_free[slot] marks that raster's end. upd_done
+    // marks the end of the last front half (later work on `stream` waits for it); upd_ok the
+    // tail of `stream` a first front half waits for.
     cudaStream_t upd_stream = nullptr;
-    cudaEvent_t upd_ok = nullptr, upd_done = nullptr;
-    bool upd_ok_recorded = false;
+    cudaEvent_t upd_ok = nullptr, upd_done = nullptr, slot_free[2] = {nullptr, nullptr};
+    bool front_active = false;     // the last update_gather ran as a front half
+    bool slot_free_rec[2] = {false, false};
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
     DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
     DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
@@ -549,16 +561,21 @@ bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool
 void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camera* cam,
                    const gscg_lod_policy* lod, uint32_t shard_begin, uint32_t shard_end, uint32_t& launches,
                    bool lod_back = false, bool deferred = false, bool overlap_update = false) {
-    cudaStream_t s = ctx->stream;
-    // The update stage (H2D, poses, FK, cull, plan) on the update stream when overlapped.
-    cudaStream_t su = overlap_update ? ctx->upd_stream : s;
+    // A front half (overlap_update, frame pipelining) runs whole on the update stream.
+    cudaStream_t s = overlap_update ? ctx->upd_stream : ctx->stream;
+    cudaStream_t su = s;
     if (overlap_update) {
-        // After an overlapped frame: wait for its project / counters / LoD write-back only.
-        // Otherwise for everything enqueued on the render stream so far.
-        if (!ctx->upd_ok_recorded) CUDA_TRY(cudaEventRecord(ctx->upd_ok, s));
-        CUDA_TRY(cudaStreamWaitEvent(su, ctx->upd_ok, 0));
+        // Following other work: wait for everything on the render stream. Following a front
+        // half: only for the raster that last read this frame's slot.
+        if (!ctx->front_active) {
+            CUDA_TRY(cudaEventRecord(ctx->upd_ok, ctx->stream));
+            CUDA_TRY(cudaStreamWaitEvent(s, ctx->upd_ok, 0));
+        }
+        if (ctx->slot_free_rec[ctx->slot]) CUDA_TRY(cudaStreamWaitEvent(s, ctx->slot_free[ctx->slot], 0));
+    } else if (ctx->front_active) {
+        CUDA_TRY(cudaStreamWaitEvent(s, ctx->upd_done, 0));  // the last front half's tail
     }
-    ctx->upd_ok_recorded = false;
+    ctx->front_active = overlap_update;
     const FrameGeom& geo = ctx->geom;
     const gscg_render_settings* settings = &ctx->settings;
     const bool host = frame->memory == GSCG_MEM_HOST;
@@ -757,10 +774,6 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         ++launches;
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(ctx->ev[2], su));
-        if (su != s) {  // the render stream (project, counters) waits for the update stage
-            CUDA_TRY(cudaEventRecord(ctx->upd_done, su));
-            CUDA_TRY(cudaStreamWaitEvent(s, ctx->upd_done, 0));
-        }
 
         const bool naive = ctx->layout == GSCG_LAYOUT_NAIVE && !posed_mode && !skin_only;
         if (naive) {
@@ -831,9 +844,9 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
             ctx->splat_capacity = 1u << 20;
             ctx->pair_capacity = 1u << 21;
         }
-        CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
-        CUDA_TRY(ctx->splat_meta.ensure(ctx->splat_capacity * 16));
-        CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->rec().ensure(ctx->splat_capacity * 48));
+        CUDA_TRY(ctx->meta().ensure(ctx->splat_capacity * 16));
+        CUDA_TRY(ctx->depth().ensure(ctx->splat_capacity * 4));
         if (ctx->debug & GSCG_DEBUG_RECORDS)
             CUDA_TRY(ctx->rec_dbg.ensure(ctx->splat_capacity * sizeof(gscg_splat_record)));
 
@@ -853,9 +866,9 @@ void update_gather(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_camer
         pj.inst_base = ctx->inst_base.as<uint32_t>();
         pj.skin = ctx->skin.as<float>();
         pj.counters = counters;
-        pj.records = ctx->records.as<float4>();
-        pj.splat_depth = ctx->splat_depth.as<uint32_t>();
-        pj.splat_meta = ctx->splat_meta.as<uint4>();
+        pj.records = ctx->rec().as<float4>();
+        pj.splat_depth = ctx->depth().as<uint32_t>();
+        pj.splat_meta = ctx->meta().as<uint4>();
         pj.splat_capacity = ctx->splat_capacity;
         pj.pair_capacity = ctx->pair_capacity;
         pj.posed_in = posed_mode ? ctx->posed_in.as<float>() : nullptr;
@@ -1117,8 +1130,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         int sb = 0;
         if (buckets) {
             DepthBucketParams bp{};
-            bp.depth = ctx->splat_depth.as<uint32_t>();
-            bp.meta = ctx->splat_meta.as<uint4>();
+            bp.depth = ctx->depth().as<uint32_t>();
+            bp.meta = ctx->meta().as<uint4>();
             bp.count = S32;
             bp.drop = drop;
             bp.tag_min = tag_min;
@@ -1143,7 +1156,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             launches += 4;
             dplan.passes = 2;  // reported sort passes: the two bucket levels
         } else if (!presorted) {
-            sb = run_radix(ctx, ctx->splat_depth.as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan, launches,
+            sb = run_radix(ctx, ctx->depth().as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan, launches,
                            s_dev);
         }
         const EmitCounts ec{s_dev};
@@ -1160,7 +1173,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         const uint32_t* tag_keys = presorted ? nullptr : ctx->skeys[sb].as<uint32_t>();
         if (!buckets) {
             CUDA_TRY(pdl_launch(k_sorted_spans, (S32 + 1023) / 1024, kMetaThreads, 0, s, ctx->srecs[sb].as<uint32_t>(),
-                                ctx->splat_meta.as<uint4>(), S32, s_dev, ctx->span_sorted.as<uint2>()));
+                                ctx->meta().as<uint4>(), S32, s_dev, ctx->span_sorted.as<uint2>()));
             ++launches;
         }
         launch_emit(true, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
@@ -1192,12 +1205,12 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
         const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);  // 2048 pairs per CTA
         CUDA_TRY(pdl_launch(k_cell_fixup, kblocks, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), ctx->precs[cb].as<uint32_t>(),
-                                             ctx->splat_meta.as<uint4>(), K, k_dev, cell_mask, presorted ? 0 : 1,
+                                             ctx->meta().as<uint4>(), K, k_dev, cell_mask, presorted ? 0 : 1,
                                              ctx->ranges.as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap));
         ++launches;
         if (!presorted) {
             CUDA_TRY(pdl_launch(k_pair_long_runs, ctx->sm_count * 2, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), K, k_dev,
-                                                              ctx->precs[cb].as<uint32_t>(), ctx->splat_meta.as<uint4>(),
+                                                              ctx->precs[cb].as<uint32_t>(), ctx->meta().as<uint4>(),
                                                               ctx->long_runs.as<uint2>(), long_count));
             ++launches;
         }
@@ -1212,7 +1225,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         RasterParams rp{};
         rp.ranges = ctx->ranges.as<uint2>();
         rp.recs = ctx->final_recs;
-        rp.records = ctx->records.as<float4>();
+        rp.records = ctx->rec().as<float4>();
         rp.width = geo.W;
         rp.height = geo.H;
         rp.tile_size = geo.ts;
@@ -1355,6 +1368,7 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->upd_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->upd_ok, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->upd_done, cudaEventDisableTiming));
+        for (auto& e : ctx->slot_free) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), sizeof(FrameCounters)));
         CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_band_counts), GSCG_MAX_BANDS * sizeof(unsigned long long)));
@@ -1399,8 +1413,8 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->template_ids, &ctx->placement, &ctx->poses, &ctx->lod_prev,
                       &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members, &ctx->visible,
                       &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
-                      &ctx->skin, &ctx->counters, &ctx->records, &ctx->splat_meta,
-                      &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
+                      &ctx->skin, &ctx->counters, &ctx->records_s[0], &ctx->records_s[1], &ctx->splat_meta_s[0], &ctx->splat_meta_s[1],
+                      &ctx->splat_depth_s[0], &ctx->splat_depth_s[1], &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
                       &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                       &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
                       &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch, &ctx->d_motions, &ctx->d_roots,
@@ -1425,6 +1439,8 @@ int gscg_destroy(gscg_ctx* ctx) {
     }
     if (ctx->upd_ok) cudaEventDestroy(ctx->upd_ok);
     if (ctx->upd_done) cudaEventDestroy(ctx->upd_done);
+    for (auto& e : ctx->slot_free)
+        if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1685,21 +1701,27 @@ int render_frame_impl(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_ca
                 nvtxRangePop();
             }
         } else {
-            update_gather(ctx, frame, cam, lod, 0, n, launches, host, false, overlap_update());
-            if (overlap_update()) {
-                // The LoD write-back now (lod_out is final), then upd_ok: the next frame's
-                // update stage may start under this frame's sort and raster.
-                if (n && !host)
+            // Frame pipelining: the front half on the update stream into the other slot (frames
+            // past kPipelineMaxSplats keep one slot: the second would not fit with them).
+            const bool front = overlap_update() && ctx->S <= kPipelineMaxSplats;
+            if (front) ctx->slot ^= 1;
+            update_gather(ctx, frame, cam, lod, 0, n, launches, host, false, front);
+            if (front) {
+                if (n && !host)  // the LoD write-back (lod_out is final) ends the front half
                     CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice,
-                                             ctx->stream));
-                CUDA_TRY(cudaEventRecord(ctx->upd_ok, ctx->stream));
-                ctx->upd_ok_recorded = true;
+                                             ctx->upd_stream));
+                CUDA_TRY(cudaEventRecord(ctx->upd_done, ctx->upd_stream));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->upd_done, 0));  // the back half follows
             }
             passes = enqueue_sort(false);
+            if (front) {
+                CUDA_TRY(cudaEventRecord(ctx->slot_free[ctx->slot], ctx->stream));
+                ctx->slot_free_rec[ctx->slot] = true;
+            }
         }
         nvtxRangePop();
         if (!overlap) copy_out(ctx, g.band_y1 - g.band_y0, fb_rgb, fb_T, host);  // region rows x region width
-        if (n && !host && (deferred || !overlap_update()))
+        if (n && !host && !ctx->front_active)
             CUDA_TRY(cudaMemcpyAsync(frame->active_lod, ctx->lod_out.ptr, n * 4ull, cudaMemcpyDeviceToDevice,
                                      ctx->stream));
         CUDA_TRY(cudaEventRecord(ctx->ev[6], ctx->stream));
@@ -1772,9 +1794,9 @@ int gscg_project_shard(gscg_ctx* ctx, const gscg_frame_desc* frame, const gscg_c
         // Route: splats per destination band.
         BandParams& bp = ctx->band;
         bp = BandParams{};
-        bp.records = ctx->records.as<float4>();
-        bp.meta = ctx->splat_meta.as<uint4>();
-        bp.depth = ctx->splat_depth.as<uint32_t>();
+        bp.records = ctx->rec().as<float4>();
+        bp.meta = ctx->meta().as<uint4>();
+        bp.depth = ctx->depth().as<uint32_t>();
         bp.count = static_cast<uint32_t>(ctx->S);
         bp.bands = bands;
         for (uint32_t b = 0; b <= bands; ++b) bp.rows[b] = band_rows[b];
@@ -1849,9 +1871,9 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
         // The band's splats replace the context's records (the shard's were packed already).
         const uint64_t cap = std::max<uint64_t>(recv_count, 1);
         if (cap > ctx->splat_capacity) ctx->splat_capacity = cap + cap / 4;
-        CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
-        CUDA_TRY(ctx->splat_meta.ensure(ctx->splat_capacity * 16));
-        CUDA_TRY(ctx->splat_depth.ensure(ctx->splat_capacity * 4));
+        CUDA_TRY(ctx->rec().ensure(ctx->splat_capacity * 48));
+        CUDA_TRY(ctx->meta().ensure(ctx->splat_capacity * 16));
+        CUDA_TRY(ctx->depth().ensure(ctx->splat_capacity * 4));
         FrameCounters init{};
         init.depth_min_bits = 0xffffffffu;
         *ctx->h_counters = init;
@@ -1863,9 +1885,9 @@ int gscg_render_band(gscg_ctx* ctx, const void* recv_dev, uint64_t recv_count, u
         up.row_begin = static_cast<int32_t>(row_begin);
         up.row_end = static_cast<int32_t>(row_end);
         up.cell = geo.cell;
-        up.records = ctx->records.as<float4>();
-        up.depth = ctx->splat_depth.as<uint32_t>();
-        up.meta = ctx->splat_meta.as<uint4>();
+        up.records = ctx->rec().as<float4>();
+        up.depth = ctx->depth().as<uint32_t>();
+        up.meta = ctx->meta().as<uint4>();
         up.counters = counters;
         const uint32_t grid = (up.count + 256 * kStreamItems - 1) / (256 * kStreamItems);
         if (grid) {
@@ -1910,8 +1932,8 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
                                 &ctx->template_ids, &ctx->placement, &ctx->poses, &ctx->lod_prev,
                                 &ctx->lod_out, &ctx->inst_group, &ctx->inst_base, &ctx->members, &ctx->visible,
                                 &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
-                                &ctx->skin, &ctx->counters, &ctx->records, &ctx->splat_meta,
-                                &ctx->splat_depth, &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
+                                &ctx->skin, &ctx->counters, &ctx->records_s[0], &ctx->records_s[1], &ctx->splat_meta_s[0], &ctx->splat_meta_s[1],
+                                &ctx->splat_depth_s[0], &ctx->splat_depth_s[1], &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
                                 &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
                                 &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals,
                                 &ctx->fb_rgb, &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch,
@@ -2323,11 +2345,11 @@ int gscg_rasterize_splats(gscg_ctx* ctx, const gscg_frame_splat* splats, uint64_
         cudaStream_t s = ctx->stream;
         const uint64_t cap = std::max<uint64_t>(n32, 1);
         if (cap > ctx->splat_capacity) ctx->splat_capacity = cap + cap / 4;
-        CUDA_TRY(ctx->records.ensure(ctx->splat_capacity * 48));
-        CUDA_TRY(ctx->splat_meta.ensure(ctx->splat_capacity * 16));
+        CUDA_TRY(ctx->rec().ensure(ctx->splat_capacity * 48));
+        CUDA_TRY(ctx->meta().ensure(ctx->splat_capacity * 16));
         if (n32) {
-            CUDA_TRY(cudaMemcpyAsync(ctx->records.ptr, rec.data(), rec.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(ctx->splat_meta.ptr, meta.data(), meta.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(ctx->rec().ptr, rec.data(), rec.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(ctx->meta().ptr, meta.data(), meta.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
         }
         ctx->S = n32;
         ctx->K = pairs;
@@ -2441,7 +2463,7 @@ int gscg_get_sorted_ordinals(gscg_ctx* ctx, uint32_t* out, uint64_t pairs) {
         if (pairs == 0) return;
         CUDA_TRY(ctx->sorted_ordinals.ensure(pairs * 4));
         k_sorted_ordinals<<<std::min<uint64_t>((pairs + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-            ctx->final_recs, ctx->splat_meta.as<uint4>(), static_cast<uint32_t>(pairs),
+            ctx->final_recs, ctx->meta().as<uint4>(), static_cast<uint32_t>(pairs),
             ctx->sorted_ordinals.as<uint32_t>());
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
