@@ -235,12 +235,19 @@ struct gscg_ctx {
     // half of the frame two back read: slot_free[slot] marks that raster's end. upd_done
     // marks the end of the last front half (later work on `stream` waits for it); upd_ok the
     // tail of `stream` a first front half waits for.
-    cudaStream_t upd_stream = nullptr;
-    cudaEvent_t upd_ok = nullptr, upd_done = nullptr, slot_free[2] = {nullptr, nullptr};
+    cudaStream_t upd_stream = nullptr, sort_stream = nullptr;  // front halves; a pipelined frame's sort
+    cudaEvent_t upd_ok = nullptr, upd_done = nullptr, sort_done = nullptr, slot_free[2] = {nullptr, nullptr};
     bool front_active = false;     // the last update_gather ran as a front half
     bool slot_free_rec[2] = {false, false};
     // sort: splat keys/records (ping-pong), pair cells/records (ping-pong), scan scratch
-    DevBuf skeys[2], srecs[2], pcell[2], precs[2], span_sorted, block_sums, hist, status, ranges, sorted_ordinals;
+    DevBuf skeys[2], srecs[2], span_sorted, block_sums, hist, status, sorted_ordinals;
+    // The sort's outputs the raster reads (cell-sorted pair keys / records, cell ranges), one
+    // set per frame slot: with frame pipelining the next frame's sort writes one slot while
+    // this frame's raster reads the other.
+    DevBuf pcell_s[2][2], precs_s[2][2], ranges_s[2];
+    DevBuf* pcell() { return pcell_s[slot]; }
+    DevBuf* precs() { return precs_s[slot]; }
+    DevBuf& ranges() { return ranges_s[slot]; }
     DevBuf long_runs;  // long runs of equal pair keys found by k_cell_fixup (+ their count)
     DevBuf buckets, bucket_staged;  // depth bucket sort: counts/starts/cursors, staged splats
     const uint32_t* final_recs = nullptr;  // cell-sorted pair records of the last frame
@@ -1036,8 +1043,8 @@ void ensure_sort_buffers(gscg_ctx* ctx, uint32_t splats, uint32_t pairs) {
     for (int b = 0; b < 2; ++b) {
         CUDA_TRY(ctx->skeys[b].ensure(std::max<size_t>(splats, 1) * 4));
         CUDA_TRY(ctx->srecs[b].ensure(std::max<size_t>(splats, 1) * 4));
-        CUDA_TRY(ctx->pcell[b].ensure(std::max<size_t>(pairs, 1) * 4));
-        CUDA_TRY(ctx->precs[b].ensure(std::max<size_t>(pairs, 1) * 4));
+        CUDA_TRY(ctx->pcell()[b].ensure(std::max<size_t>(pairs, 1) * 4));
+        CUDA_TRY(ctx->precs()[b].ensure(std::max<size_t>(pairs, 1) * 4));
     }
 }
 
@@ -1071,7 +1078,16 @@ void flush_readback(gscg_ctx* ctx) {
 uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& launches, float* read_rgb = nullptr,
                      float* read_T = nullptr, bool presorted = false, bool pipelined = false,
                      bool device_counts = false) {
-    cudaStream_t s = ctx->stream;
+    // A pipelined frame's sort runs on the sort stream (after its front half, and after the
+    // raster that last read this slot's pair buffers), its raster on the render stream after
+    // the sort: the next frame's sort may run under this frame's raster.
+    cudaStream_t rs_ = ctx->stream;
+    const bool split = ctx->front_active && !presorted && !device_counts;
+    cudaStream_t s = split ? ctx->sort_stream : rs_;
+    if (split) {
+        CUDA_TRY(cudaStreamWaitEvent(s, ctx->upd_done, 0));
+        if (ctx->slot_free_rec[ctx->slot]) CUDA_TRY(cudaStreamWaitEvent(s, ctx->slot_free[ctx->slot], 0));
+    }
     const FrameGeom& geo = ctx->geom;
     // The region's tile columns (the whole frame's unless gscg_set_region narrowed them).
     const int rtx = geo.band_tiles_x;
@@ -1086,8 +1102,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
     CUDA_TRY(ctx->fb_rgb.ensure(static_cast<size_t>(geo.W) * geo.H * 12));
     CUDA_TRY(ctx->fb_T.ensure(static_cast<size_t>(geo.W) * geo.H * 4));
     // An earlier pipelined frame may still be reading this framebuffer back.
-    CUDA_TRY(cudaStreamWaitEvent(s, ctx->rb_ev, 0));
-    CUDA_TRY(ctx->ranges.ensure(std::max<size_t>(cells, 1) * 8));
+    CUDA_TRY(cudaStreamWaitEvent(rs_, ctx->rb_ev, 0));
+    CUDA_TRY(ctx->ranges().ensure(std::max<size_t>(cells, 1) * 8));
 
     // Deferred frames (device_counts): the host has not read this frame's counters yet, so
     // grids and buffers cover the capacities and every kernel takes its count (and the depth
@@ -1098,7 +1114,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
     const unsigned long long* s_dev = device_counts ? &dcnt->splats : nullptr;
     const unsigned long long* k_dev = device_counts ? &dcnt->pairs : nullptr;
     uint32_t passes = 0;
-    if (cells) CUDA_TRY(cudaMemsetAsync(ctx->ranges.ptr, 0, static_cast<size_t>(cells) * 8, s));
+    if (cells) CUDA_TRY(cudaMemsetAsync(ctx->ranges().ptr, 0, static_cast<size_t>(cells) * 8, s));
     ctx->final_recs = nullptr;
     if (S32 > 0 && K > 0) {
         ensure_sort_buffers(ctx, S32, K);
@@ -1186,7 +1202,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         CUDA_TRY(pdl_launch(k_sort_rows, dmask + 1, 1024, 0, s, bp));
         launch_emit(false, eblocks, s, ctx->srecs[sb].as<uint32_t>(), tag_keys, S32, ctx->span_sorted.as<uint2>(),
                     ctx->block_sums.as<uint32_t>(), ctx->hist.as<uint32_t>(), rtx, quads, dmask, drop, cell_bits,
-                    ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(), ec);
+                    ctx->pcell()[1].as<uint32_t>(), ctx->precs()[1].as<uint32_t>(), ec);
         launches += 3;
         CUDA_TRY(cudaGetLastError());
         // 3. the remaining stable cell-sort passes (cell bits only; the tags ride along).
@@ -1195,8 +1211,8 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             rest = make_plan(cell_bits - emit_bits);
             for (uint32_t q = 0; q < rest.passes; ++q) rest.shift[q] += emit_bits;
         }
-        const int cb = rest.passes ? run_radix(ctx, ctx->pcell[1].as<uint32_t>(), ctx->precs[1].as<uint32_t>(),
-                                               ctx->pcell, ctx->precs, K, rest, launches, k_dev)
+        const int cb = rest.passes ? run_radix(ctx, ctx->pcell()[1].as<uint32_t>(), ctx->precs()[1].as<uint32_t>(),
+                                               ctx->pcell(), ctx->precs(), K, rest, launches, k_dev)
                                    : 1;
         // 4. cell ranges + every run of equal (cell, tag) ordered by (depth bits, ordinal).
         const uint32_t long_cap = K / kLongRun + K / 2048 + 2;  // see k_cell_fixup
@@ -1204,26 +1220,31 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
         uint32_t* long_count = reinterpret_cast<uint32_t*>(ctx->long_runs.as<uint2>() + long_cap);
         CUDA_TRY(cudaMemsetAsync(long_count, 0, 4, s));
         const uint32_t kblocks = (K + 256 * kStreamItems - 1) / (256 * kStreamItems);  // 2048 pairs per CTA
-        CUDA_TRY(pdl_launch(k_cell_fixup, kblocks, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), ctx->precs[cb].as<uint32_t>(),
+        CUDA_TRY(pdl_launch(k_cell_fixup, kblocks, 256, 0, s, ctx->pcell()[cb].as<uint32_t>(), ctx->precs()[cb].as<uint32_t>(),
                                              ctx->meta().as<uint4>(), K, k_dev, cell_mask, presorted ? 0 : 1,
-                                             ctx->ranges.as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap));
+                                             ctx->ranges().as<uint2>(), ctx->long_runs.as<uint2>(), long_count, long_cap));
         ++launches;
         if (!presorted) {
-            CUDA_TRY(pdl_launch(k_pair_long_runs, ctx->sm_count * 2, 256, 0, s, ctx->pcell[cb].as<uint32_t>(), K, k_dev,
-                                                              ctx->precs[cb].as<uint32_t>(), ctx->meta().as<uint4>(),
+            CUDA_TRY(pdl_launch(k_pair_long_runs, ctx->sm_count * 2, 256, 0, s, ctx->pcell()[cb].as<uint32_t>(), K, k_dev,
+                                                              ctx->precs()[cb].as<uint32_t>(), ctx->meta().as<uint4>(),
                                                               ctx->long_runs.as<uint2>(), long_count));
             ++launches;
         }
         CUDA_TRY(cudaGetLastError());
-        ctx->final_recs = ctx->precs[cb].as<uint32_t>();
+        ctx->final_recs = ctx->precs()[cb].as<uint32_t>();
         passes = dplan.passes + 1 + rest.passes;
     }
     CUDA_TRY(cudaEventRecord(ctx->ev[4], s));
+    if (split) {
+        CUDA_TRY(cudaEventRecord(ctx->sort_done, s));
+        CUDA_TRY(cudaStreamWaitEvent(rs_, ctx->sort_done, 0));
+    }
+    s = rs_;  // the raster and read-back on the render stream
 
     // ---- rasterize ----
     if (tiles) {
         RasterParams rp{};
-        rp.ranges = ctx->ranges.as<uint2>();
+        rp.ranges = ctx->ranges().as<uint2>();
         rp.recs = ctx->final_recs;
         rp.records = ctx->rec().as<float4>();
         rp.width = geo.W;
@@ -1366,6 +1387,8 @@ int gscg_create(int device, gscg_ctx** out) {
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->pend_ev, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->counters_ev, cudaEventDisableTiming));
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->upd_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->sort_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->sort_done, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->upd_ok, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->upd_done, cudaEventDisableTiming));
         for (auto& e : ctx->slot_free) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1415,8 +1438,9 @@ int gscg_destroy(gscg_ctx* ctx) {
                       &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
                       &ctx->skin, &ctx->counters, &ctx->records_s[0], &ctx->records_s[1], &ctx->splat_meta_s[0], &ctx->splat_meta_s[1],
                       &ctx->splat_depth_s[0], &ctx->splat_depth_s[1], &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
-                      &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
-                      &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals, &ctx->fb_rgb,
+                      &ctx->pcell_s[0][0], &ctx->pcell_s[0][1], &ctx->precs_s[0][0], &ctx->precs_s[0][1],
+                      &ctx->pcell_s[1][0], &ctx->pcell_s[1][1], &ctx->precs_s[1][0], &ctx->precs_s[1][1], &ctx->span_sorted,
+                      &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges_s[0], &ctx->ranges_s[1], &ctx->sorted_ordinals, &ctx->fb_rgb,
                       &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch, &ctx->d_motions, &ctx->d_roots,
                       &ctx->d_keys, &ctx->motion_ids, &ctx->phases, &ctx->long_runs, &ctx->fb_rgb_alt,
                       &ctx->fb_T_alt};
@@ -1437,6 +1461,11 @@ int gscg_destroy(gscg_ctx* ctx) {
         cudaStreamSynchronize(ctx->upd_stream);
         cudaStreamDestroy(ctx->upd_stream);
     }
+    if (ctx->sort_stream) {
+        cudaStreamSynchronize(ctx->sort_stream);
+        cudaStreamDestroy(ctx->sort_stream);
+    }
+    if (ctx->sort_done) cudaEventDestroy(ctx->sort_done);
     if (ctx->upd_ok) cudaEventDestroy(ctx->upd_ok);
     if (ctx->upd_done) cudaEventDestroy(ctx->upd_done);
     for (auto& e : ctx->slot_free)
@@ -1934,8 +1963,9 @@ int gscg_memory_usage(gscg_ctx* ctx, gscg_memory_info* out) {
                                 &ctx->group_inst_start, &ctx->group_inst_count, &ctx->group_item_start,
                                 &ctx->skin, &ctx->counters, &ctx->records_s[0], &ctx->records_s[1], &ctx->splat_meta_s[0], &ctx->splat_meta_s[1],
                                 &ctx->splat_depth_s[0], &ctx->splat_depth_s[1], &ctx->skeys[0], &ctx->skeys[1], &ctx->srecs[0], &ctx->srecs[1],
-                                &ctx->pcell[0], &ctx->pcell[1], &ctx->precs[0], &ctx->precs[1], &ctx->span_sorted,
-                                &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges, &ctx->sorted_ordinals,
+                                &ctx->pcell_s[0][0], &ctx->pcell_s[0][1], &ctx->precs_s[0][0], &ctx->precs_s[0][1],
+                      &ctx->pcell_s[1][0], &ctx->pcell_s[1][1], &ctx->precs_s[1][0], &ctx->precs_s[1][1], &ctx->span_sorted,
+                                &ctx->block_sums, &ctx->hist, &ctx->status, &ctx->ranges_s[0], &ctx->ranges_s[1], &ctx->sorted_ordinals,
                                 &ctx->fb_rgb, &ctx->fb_T, &ctx->posed_dbg, &ctx->rec_dbg, &ctx->band_scratch,
                                 &ctx->long_runs};
         for (const DevBuf* b : bufs) out->frame_bytes += b->cap;
@@ -2452,7 +2482,7 @@ int gscg_get_tile_ranges(gscg_ctx* ctx, uint32_t* out, uint32_t cells) {
     if (!ctx || !out) return GSCG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
         if (cells > ctx->tiles * ctx->cells_per_tile) invalid("more cells requested than rendered");
-        CUDA_TRY(cudaMemcpyAsync(out, ctx->ranges.ptr, cells * 8ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->ranges().ptr, cells * 8ull, cudaMemcpyDeviceToHost, ctx->stream)); CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     });
 }
 
@@ -2712,7 +2742,7 @@ int gscg_group_tile_costs(gscg_group* g, uint32_t tiles_x, uint32_t tiles_y, uin
         const uint32_t rtx = static_cast<uint32_t>(geo.band_tiles_x), rows = static_cast<uint32_t>(geo.band_tile_rows);
         if (ctx->tiles && rtx && rows && static_cast<uint32_t>(geo.band_tile_row0) + rows <= tiles_y &&
             static_cast<uint32_t>(geo.band_tile_col0) + rtx <= tiles_x) {
-            k_tile_costs<<<(rtx * rows + 255) / 256, 256, 0, s>>>(ctx->ranges.as<uint2>(), rtx, rows, geo.cells_per_tile,
+            k_tile_costs<<<(rtx * rows + 255) / 256, 256, 0, s>>>(ctx->ranges().as<uint2>(), rtx, rows, geo.cells_per_tile,
                                                                  geo.band_tile_col0, geo.band_tile_row0, tiles_x,
                                                                  g->row_costs.as<unsigned long long>());
             CUDA_TRY(cudaGetLastError());
