@@ -963,8 +963,9 @@ bool settle_counts(gscg_ctx* ctx, const gscg_frame_desc* frame, uint32_t n, bool
 // count_dev (may be null): the pass count is min(count, *count_dev) on the device, count
 // then being the capacity the grid covers (deferred frames).
 int run_radix(gscg_ctx* ctx, const uint32_t* in_keys, const uint32_t* in_vals, DevBuf* kb, DevBuf* vb,
-              uint32_t count, const RadixPlan& plan, uint32_t& launches, const unsigned long long* count_dev = nullptr) {
-    cudaStream_t s = ctx->stream;
+              uint32_t count, const RadixPlan& plan, uint32_t& launches, const unsigned long long* count_dev = nullptr,
+              cudaStream_t stream = nullptr) {
+    cudaStream_t s = stream ? stream : ctx->stream;
     const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
     int out = 0;
     for (uint32_t q = 0; q < plan.passes; ++q) {
@@ -1082,7 +1083,11 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
     // raster that last read this slot's pair buffers), its raster on the render stream after
     // the sort: the next frame's sort may run under this frame's raster.
     cudaStream_t rs_ = ctx->stream;
-    const bool split = ctx->front_active && !presorted && !device_counts;
+    static const bool split_on = [] {  // GSCG_SPLIT_SORT=0: the sort stays on the render stream (A/B)
+        const char* e = std::getenv("GSCG_SPLIT_SORT");
+        return !(e && e[0] == '0');
+    }();
+    const bool split = split_on && ctx->front_active && !presorted && !device_counts;
     cudaStream_t s = split ? ctx->sort_stream : rs_;
     if (split) {
         CUDA_TRY(cudaStreamWaitEvent(s, ctx->upd_done, 0));
@@ -1173,7 +1178,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             dplan.passes = 2;  // reported sort passes: the two bucket levels
         } else if (!presorted) {
             sb = run_radix(ctx, ctx->depth().as<uint32_t>(), nullptr, ctx->skeys, ctx->srecs, S32, dplan, launches,
-                           s_dev);
+                           s_dev, s);
         }
         const EmitCounts ec{s_dev};
         // 2. cell spans in sorted order; the first cell-sort digit histogram per emission
@@ -1212,7 +1217,7 @@ uint32_t sort_raster(gscg_ctx* ctx, int tile_row0, int tile_rows, uint32_t& laun
             for (uint32_t q = 0; q < rest.passes; ++q) rest.shift[q] += emit_bits;
         }
         const int cb = rest.passes ? run_radix(ctx, ctx->pcell()[1].as<uint32_t>(), ctx->precs()[1].as<uint32_t>(),
-                                               ctx->pcell(), ctx->precs(), K, rest, launches, k_dev)
+                                               ctx->pcell(), ctx->precs(), K, rest, launches, k_dev, s)
                                    : 1;
         // 4. cell ranges + every run of equal (cell, tag) ordered by (depth bits, ordinal).
         const uint32_t long_cap = K / kLongRun + K / 2048 + 2;  // see k_cell_fixup
