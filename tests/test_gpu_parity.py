@@ -707,3 +707,64 @@ def test_column_regions_assemble_the_whole_frame_bit_for_bit(cols):
         parts_T.append(T.copy())
     assert np.concatenate(parts_rgb, axis=1).tobytes() == full_rgb.tobytes()
     assert np.concatenate(parts_T, axis=1).tobytes() == full_T.tobytes()
+
+
+def test_pipelined_device_frames_follow_the_lod_chain():
+    """Device-memory frames enqueued back to back without a host wait (the bench's path:
+    a frame's update + projection run under the previous frame's sort and raster, two frame
+    slots), the camera moving so hysteresis flips levels: every frame equals the oracle's,
+    which carries the LoD state frame to frame (the front half must see the previous
+    frame's levels)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2501_17792_b200 import native as N
+    from paper_2501_17792_b200.multigpu import gscg_settings
+
+    s = basic_scene(count=16, rows=4, cols=4, sh=False)
+    s.set_lod_policy((3.5, 6.0), hysteresis=1.0)
+    r = P.Renderer(s, device=0, device_poses=True)
+    o = orc.from_scene(s)
+    o.set_lod((3.5, 6.0), 1.0)
+    st = P.RenderSettings(sh_colour=False)
+    r.render_frame(0.0, st)  # templates + motion tables
+    rec = r.instance_records()
+    dev = torch.device("cuda", 0)
+    d = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int32) if v.dtype == np.uint32 else v).to(dev)
+         for k, v in rec.items()}
+    d_lods = torch.full((len(rec["lods"]),), -1, dtype=torch.int32, device=dev)
+    n, lib, ctx = len(rec["lods"]), N.gscg(), r.gpu
+    rs = gscg_settings(st)
+    lp = N.GscgLodPolicy()
+    lp.threshold_count = 2
+    lp.thresholds_m[0], lp.thresholds_m[1] = 3.5, 6.0
+    lp.hysteresis_band_m = 1.0
+    zs = (-0.5, 0.0, 0.4, 0.8, 0.4, -0.3, 2.8, 3.3, 2.9)
+    H, W = s.cfg.height, s.cfg.width
+    outs = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in zs]
+    cams = []
+    for f, z in enumerate(zs):
+        s.set_camera((0.0, 1.6, -3.0 - z), (0.0, 1.0, 5.0))
+        cam = s.camera_basis()
+        cams.append(cam)
+        fd = N.GscgFrameDesc()
+        fd.instance_count, fd.joint_stride = n, r.joint_stride
+        fd.template_ids, fd.placement = d["template_ids"].data_ptr(), d["placement"].data_ptr()
+        fd.active_lod, fd.forced_lod = d_lods.data_ptr(), -1
+        fd.memory, fd.pose_source, fd.time_s = N.GSCG_MEM_DEVICE, N.GSCG_POSES_SAMPLED, 0.1 + f / 30.0
+        fd.motion_ids, fd.phase_offsets = d["motion_ids"].data_ptr(), d["phase_offsets"].data_ptr()
+        N.check_gscg(lib.gscg_render_frame(ctx, C.byref(fd), C.byref(cam), C.byref(rs), C.byref(lp),
+                                           C.c_void_p(outs[f].data_ptr()), None, None), ctx)
+    N.check_gscg(lib.gscg_synchronize(ctx), ctx)
+    flips = 0
+    prev = None
+    for f, z in enumerate(zs):
+        o.set_camera((0.0, 1.6, -3.0 - z), (0.0, 1.0, 5.0), 50.0, W, H)
+        orgb, _, _ = o.render(0.1 + f / 30.0, orc.settings(sh_colour=False))
+        lods = o.lods(n)
+        flips += int(prev is not None and not np.array_equal(prev, lods))
+        prev = lods.copy()
+        assert outs[f].cpu().numpy().tobytes() == orgb.tobytes(), f"frame {f} differs from the oracle"
+    assert flips >= 2  # the sequence really moves levels
+    assert np.array_equal(d_lods.cpu().numpy().astype(np.uint32), prev)
