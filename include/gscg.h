@@ -272,7 +272,11 @@ int gscg_psnr(gscg_ctx* ctx, const float* a, const float* b, uint64_t floats, fl
 /* Device pointers of the context's framebuffer (valid until the next render). */
 int gscg_framebuffer_device(gscg_ctx* ctx, float** rgb, float** T);
 int gscg_synchronize(gscg_ctx* ctx);
-/* The context's CUDA stream (cudaStream_t), for event timing by the caller. */
+/* The context's render stream (cudaStream_t), for event timing by the caller. A frame's
+ * work spans three context streams (front half: update + projection; sort; raster +
+ * read-back; each waiting for the previous part of the same frame, so the next frame's
+ * front half and sort overlap this frame's raster); a frame's output is ready on the
+ * render stream, and work the caller orders on it runs after the frame. */
 int gscg_stream(gscg_ctx* ctx, void** stream);
 
 /* Parity / debug exports of the last frame. */
