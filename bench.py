@@ -620,7 +620,7 @@ def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
     tiles, cpt = r.cell_layout()
     tx = (cfg.width + 15) // 16
     tile_pairs = (ranges[:, 1] - ranges[:, 0]).astype(np.float64).reshape(-1, cpt).sum(1).reshape(-1, tx)
-    out = {"method": "each region rendered alone on one B200 (gscg_set_region), median of K frames"}
+    out = {"method": "each region rendered alone on one B200 (gscg_set_region), median interval of K pipelined frames"}
     for axis in ("cols", "rows"):
         line = tile_pairs.sum(0) if axis == "cols" else tile_pairs.sum(1)
         extent = cfg.width if axis == "cols" else cfg.height
@@ -635,11 +635,12 @@ def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
                 x0, y0, x1, y1 = (cuts[b], 0, cuts[b + 1], 0) if axis == "cols" else (0, cuts[b], 0, cuts[b + 1])
                 N.check_gscg(lib.gscg_set_region(ctx, x0, y0, x1, y1), ctx)
                 for f in range(3):
-                    frame(f)
+                    frame(f, timed=True)
+                torch.cuda.synchronize()
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
                 evs[0].record(stream)
-                for f in range(args.steps):
-                    frame(args.warmup + f)
+                for f in range(args.steps):  # pipelined frames, as each rank renders them
+                    frame(args.warmup + f, timed=True)
                     evs[f + 1].record(stream)
                 torch.cuda.synchronize()
                 region_ms.append(float(np.median([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])))
