@@ -768,3 +768,61 @@ def test_pipelined_device_frames_follow_the_lod_chain():
         assert outs[f].cpu().numpy().tobytes() == orgb.tobytes(), f"frame {f} differs from the oracle"
     assert flips >= 2  # the sequence really moves levels
     assert np.array_equal(d_lods.cpu().numpy().astype(np.uint32), prev)
+
+
+def _patch_extreme_gaussians(path):
+    """Rewrites level 0 of a v1 GSAT file (io.cpp layout, tests/test_io.py) with extreme but
+    valid Gaussians (the LodLevel invariants, avatar.cpp validate): a near-zero and two
+    screen-covering scales, tiny / denormal / unit opacities, a pure-blue colour, a mean far
+    above the crowd and one behind the camera, equal four-joint weights."""
+    import struct
+
+    b = bytearray(path.read_bytes())
+    J = int.from_bytes(b[8:10], "little")
+    off = 11 + 66 * J
+    n = int.from_bytes(b[off:off + 4], "little")
+    means = off + 4
+    rot = means + 12 * n
+    sc = rot + 16 * n
+    op = sc + 12 * n
+    col = op + 4 * n
+    sw = col + 12 * n + 8 * n
+
+    def put(base, i, vals):
+        stride = 4 * len(vals)
+        b[base + stride * i:base + stride * (i + 1)] = struct.pack("<%df" % len(vals), *vals)
+
+    put(sc, 0, (1e-30, 1e-30, 1e-30))
+    put(sc, 1, (50.0, 50.0, 50.0))
+    put(sc, 2, (30.0, 1e-3, 1e-3))
+    put(op, 3, (1e-30,))
+    put(op, 4, (1.0,))
+    put(op, 5, (1.4e-45,))
+    put(col, 6, (0.0, 0.0, 1.0))
+    put(means, 7, (0.0, 1e6, 0.0))
+    put(means, 8, (0.0, 0.0, -1e3))
+    put(sw, 9, (0.25, 0.25, 0.25, 0.25))
+    path.write_bytes(bytes(b))
+
+
+@pytest.mark.parametrize("size,tile", [((200, 120), 16), ((640, 360), 16), ((200, 120), 8)])
+def test_extreme_gaussians_match_the_oracle(tmp_path, size, tile):
+    """Screen-covering splats (every cell's list, emission blocks past the staged-pair
+    capacity at 640x360), vanishing ones, opacities that never or always saturate, and
+    splats culled far away or behind the camera: the frame still equals the oracle's."""
+    w, h = size
+    cfg = P.SceneConfig(template_count=1, template_seed_base=1, level_counts=(60, 24, 8), with_sh=False,
+                        motion_count=1, motion_seed_base=2, motion_frames=24, grid_rows=2, grid_cols=2,
+                        grid_spacing=1.2, crowd_count=4, crowd_seed=42, cam_pos=(0.6, 1.5, -3.5),
+                        cam_look=(0.6, 1.0, 2.0), width=w, height=h)
+    s = P.Scene(cfg)
+    path = tmp_path / "extreme.gsat"
+    s.save_template(0, path)
+    _patch_extreme_gaussians(path)
+    s.load_template(path, 0)
+    r = P.Renderer(s)
+    o = orc.from_scene(s)
+    for t, static in ((0.3, False), (0.0, True)):
+        g, c = render_both(s, r, o, t, tile_size=tile, static_pose=static, forced_lod=0, sh=False)
+        rep = check_frame(s, r, o, g, c, tile_size=tile)
+        assert rep["S"] <= 4 * 58  # the far and the behind-camera Gaussians culled in every instance
