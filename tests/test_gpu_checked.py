@@ -17,7 +17,8 @@ CHECKED = ROOT / "paper_2501_17792_b200" / "lib_checked"
 CASES = ("test_fixture_scene or test_tile_sizes or test_forced_lod or test_hysteresis_across_frames "
          "or test_long_equal_depth_runs or test_truncated_depth_sort or test_lsd_depth_sort "
          "or test_bucket_sort_large_buckets or test_baseline_config or test_band_frames "
-         "or test_column_regions or test_naive_layout or test_empty_crowd or test_extreme_gaussians")
+         "or test_column_regions or test_naive_layout or test_empty_crowd or test_extreme_gaussians "
+         "or test_extreme_cameras")
 
 
 @pytest.mark.gpu

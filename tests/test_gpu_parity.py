@@ -826,3 +826,30 @@ def test_extreme_gaussians_match_the_oracle(tmp_path, size, tile):
         g, c = render_both(s, r, o, t, tile_size=tile, static_pose=static, forced_lod=0, sh=False)
         rep = check_frame(s, r, o, g, c, tile_size=tile)
         assert rep["S"] <= 4 * 58  # the far and the behind-camera Gaussians culled in every instance
+
+
+# (pos, look, fov_y_deg, (width, height), near_m, tile): nose against a character, the
+# widest and narrowest fields of view, degenerate resolutions, a tiny and a far near plane.
+EXTREME_CAMERAS = [
+    ((2.5, 1.1, 2.3), (2.6, 1.0, 3.5), 50.0, (160, 96), 0.1, 16),
+    ((2.5, 1.7, -1.0), (2.5, 1.0, 5.0), 170.0, (160, 96), 0.1, 16),
+    ((2.5, 1.7, -8.0), (2.5, 1.0, 5.0), 1.0, (160, 96), 0.1, 16),
+    ((2.5, 1.7, -3.0), (2.5, 1.0, 5.0), 50.0, (17, 3), 0.1, 16),
+    ((2.5, 1.7, -3.0), (2.5, 1.0, 5.0), 50.0, (1, 1), 0.1, 4),
+    ((2.5, 1.2, 1.0), (2.5, 1.0, 5.0), 60.0, (160, 96), 1e-3, 16),
+    ((2.5, 1.7, -3.0), (2.5, 1.0, 5.0), 50.0, (160, 96), 5.0, 16),
+]
+
+
+@pytest.mark.parametrize("cam", EXTREME_CAMERAS)
+def test_extreme_cameras_match_the_oracle(cam):
+    pos, look, fov, (w, h), near, tile = cam
+    cfg = P.SceneConfig(template_count=2, level_counts=(200, 60, 20), with_sh=False, motion_count=2,
+                        motion_frames=24, grid_rows=6, grid_cols=6, crowd_count=36, crowd_seed=9,
+                        cam_pos=pos, cam_look=look, width=w, height=h)
+    s = P.Scene(cfg)
+    s.set_camera(pos, look, fov_y_deg=fov, width=w, height=h, near_m=near)
+    r = P.Renderer(s)
+    o = orc.from_scene(s)
+    g, c = render_both(s, r, o, 0.25, tile_size=tile, background=(0.1, 0.2, 0.3), sh=False)
+    check_frame(s, r, o, g, c, tile_size=tile)
