@@ -309,17 +309,26 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
         group = BandGroup(r, rank, world, dist, axis=args.split_axis)
         group.set_tile(settings.tile_size)
 
-        def frame(f: int, timed: bool = False) -> dict:
+        def frame(f: int, timed: bool = False):
+            # Timed frames read no stage events (as on one GPU): the frames stay in flight,
+            # each rank's next update and projection under its sort, raster and gather.
+            if timed:
+                group.render(frame_desc(f), cam, rs, lp, stage_times=False)
+                return None
             st = group.render(frame_desc(f), cam, rs, lp)
             return {"update": st.update_ms, "gather": st.gather_ms, "sort": st.sort_ms, "rasterize": st.rasterize_ms,
                     "launches": st.kernel_launches, "counts": (st.gaussian_count, st.splat_count, st.pair_count),
                     "tile_pairs": st.tile_pair_count}
 
-        # Balance the bands on the warm-up frames (pairs per tile row over all ranks);
-        # the timed frames keep the last rows.
+        # Balance the regions on the warm-up frames: pairs per tile line over all ranks,
+        # then every rank's measured region time (its stage times); the timed frames keep
+        # the last cuts.
         for f in range(2):
             frame(f)
             group.rebalance()
+        if world > 1:
+            res = frame(2)
+            group.rebalance_by_time(res["update"] + res["gather"] + res["sort"] + res["rasterize"])
 
     first = None
     for f in range(args.warmup):
@@ -421,7 +430,7 @@ def run_ours(args, rank, world, local_rank) -> dict | None:
             fd.time_s = times_s[f]
             fd.motion_ids = pinned["motion_ids"].ctypes.data
             fd.phase_offsets = pinned["phase_offsets"].ctypes.data
-            group.render(fd, cam, rs, lp, band_out if rank == 0 else None)
+            group.render(fd, cam, rs, lp, band_out if rank == 0 else None, stage_times=False)
 
         e2e_fps = time_e2e(e2e_frame)
         group.close()
@@ -614,7 +623,7 @@ def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
     region bounds the P-GPU frame time from below. Not a multi-GPU measurement."""
     import torch
     from paper_2501_17792_b200 import native as N
-    from paper_2501_17792_b200.multigpu import band_rows
+    from paper_2501_17792_b200.multigpu import band_rows, cuts_from_region_times
 
     ranges = r.cell_ranges()
     tiles, cpt = r.cell_layout()
@@ -625,10 +634,11 @@ def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
         line = tile_pairs.sum(0) if axis == "cols" else tile_pairs.sum(1)
         extent = cfg.width if axis == "cols" else cfg.height
         res = {}
-        for parts in (1, 2, 4, 8):
-            cuts = band_rows(extent, 16, parts, line + 0.02 * line.mean() + 1.0)
+        weights = line + 0.02 * line.mean() + 1.0
+
+        def measure(cuts):
             region_ms = []
-            for b in range(parts):
+            for b in range(len(cuts) - 1):
                 if cuts[b + 1] <= cuts[b]:
                     region_ms.append(0.0)
                     continue
@@ -645,10 +655,22 @@ def band_split_estimate(r, ctx, lib, frame, stream, cfg, args) -> dict:
                 torch.cuda.synchronize()
                 region_ms.append(float(np.median([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])))
             N.check_gscg(lib.gscg_set_region(ctx, 0, 0, 0, 0), ctx)
+            return region_ms
+
+        for parts in (1, 2, 4, 8):
+            cuts = band_rows(extent, 16, parts, weights)
+            region_ms = measure(cuts)
             res[str(parts)] = {"cuts": cuts, "region_ms": [round(x, 4) for x in region_ms],
                                "max_ms": round(max(region_ms), 4)}
+            if parts > 1:  # BandGroup.rebalance_by_time: cuts re-weighted by the measured region times
+                tcuts = cuts_from_region_times(weights, extent, 16, cuts, region_ms)
+                tms = measure(tcuts)
+                res[str(parts)]["time_balanced"] = {"cuts": tcuts, "region_ms": [round(x, 4) for x in tms],
+                                                    "max_ms": round(max(tms), 4)}
         for parts in (2, 4, 8):
             res[str(parts)]["speedup_vs_1"] = round(res["1"]["max_ms"] / res[str(parts)]["max_ms"], 3)
+            tb = res[str(parts)]["time_balanced"]
+            tb["speedup_vs_1"] = round(res["1"]["max_ms"] / tb["max_ms"], 3)
         out[axis] = res
     return out
 

@@ -456,6 +456,7 @@ class BandGroup:
                  axis: str = "cols"):
         import torch  # noqa: F401  (torch's NCCL before libgscg binds one; see broadcast_unique_id)
         self.renderer, self.rank, self.world = renderer, rank, world
+        self._dist, self._group = dist, group
         cfg = renderer.scene.cfg
         self.height, self.width = cfg.height, cfg.width
         uid = unique_id if unique_id is not None else broadcast_unique_id(rank, world, dist, group)
@@ -484,16 +485,20 @@ class BandGroup:
         self.tile = tile
         self.cuts = band_rows(self.extent, tile, self.world)
 
-    def render(self, frame, cam, settings, lod, out_rgb=None, out_T=None) -> "N.GscgStageTimes":
+    def render(self, frame, cam, settings, lod, out_rgb=None, out_T=None,
+               stage_times: bool = True) -> Optional["N.GscgStageTimes"]:
         """One frame (frame/cam/settings/lod: the gscg_render_frame descriptors). On rank 0,
-        out_rgb / out_T (numpy, host or None) receive the whole frame."""
-        st = N.GscgStageTimes()
+        out_rgb / out_T (numpy, host or None) receive the whole frame. stage_times=False
+        returns None and leaves the frame in flight: reading the stage events makes the
+        call wait for the region's raster, so the next frame's update and projection could
+        not overlap this one's sort, raster and gather."""
+        st = N.GscgStageTimes() if stage_times else None
         cuts = (C.c_uint32 * (self.world + 1))(*self.cuts)
         axis = N.GSCG_SPLIT_COLS if self.axis == "cols" else N.GSCG_SPLIT_ROWS
         ptr = (lambda a: None if a is None else a.ctypes.data)
         N.check_gscg(N.gscg().gscg_group_render_frame(self._h, C.byref(frame), C.byref(cam), C.byref(settings),
                                                        C.byref(lod), axis, cuts, ptr(out_rgb), ptr(out_T),
-                                                       C.byref(st)), self.renderer.gpu)
+                                                       None if st is None else C.byref(st)), self.renderer.gpu)
         return st
 
     def tile_costs(self) -> np.ndarray:
@@ -508,6 +513,47 @@ class BandGroup:
         same all-reduced map, so every rank derives the same cuts)."""
         self.cuts = cuts_from_tile_costs(self.tile_costs(), self.axis, self.extent, self.tile, self.world, self.cuts)
         return self.cuts
+
+    def rebalance_by_time(self, region_ms: float) -> list[int]:
+        """Cuts re-weighted by every rank's measured time for its region (region_ms: this
+        rank's, all-gathered; cuts_from_region_times), on top of the pairs per tile line:
+        the centre columns of a crowd frame cost more per pair (whole instances projected,
+        the longest quadrant lists). Every rank derives the same cuts."""
+        import torch
+
+        times = [float(region_ms)]
+        if self.world > 1:
+            dist, group = self._dist, self._group
+            on_gpu = dist.get_backend(group) == "nccl"
+            t = torch.tensor([float(region_ms)], dtype=torch.float64,
+                             device=torch.device("cuda", torch.cuda.current_device()) if on_gpu else "cpu")
+            out = [torch.zeros_like(t) for _ in range(self.world)]
+            dist.all_gather(out, t, group=group)
+            times = [float(x.item()) for x in out]
+        c = np.asarray(self.tile_costs(), dtype=np.float64)
+        line = c.sum(0) if self.axis == "cols" else c.sum(1)
+        if line.sum() > 0:
+            self.cuts = cuts_from_region_times(line + 0.02 * line.mean() + 1.0, self.extent, self.tile, self.cuts,
+                                               times)
+        return self.cuts
+
+
+def cuts_from_region_times(line_weights: Sequence[float], extent: int, tile: int, cuts: Sequence[int],
+                           region_ms: Sequence[float]) -> list[int]:
+    """Cuts re-balanced by measured region times: every tile line of region r is weighted
+    by its binned pairs scaled so that the region's lines sum to its measured time (the
+    raster's cost is not proportional to pairs, and a region's projection covers whole
+    instances), then the cumulative weight is split evenly again (band_rows)."""
+    w = np.asarray(line_weights, dtype=np.float64).copy()
+    parts = len(cuts) - 1
+    if len(region_ms) != parts:
+        raise ValueError("one time per region")
+    for r in range(parts):
+        a, b = cuts[r] // tile, (cuts[r + 1] + tile - 1) // tile
+        tot = w[a:b].sum()
+        if b > a and tot > 0 and region_ms[r] > 0:
+            w[a:b] *= region_ms[r] / tot
+    return band_rows(extent, tile, parts, w)
 
 
 def cuts_from_tile_costs(costs: np.ndarray, axis: str, extent: int, tile: int, parts: int,

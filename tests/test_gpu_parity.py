@@ -853,3 +853,55 @@ def test_extreme_cameras_match_the_oracle(cam):
     o = orc.from_scene(s)
     g, c = render_both(s, r, o, 0.25, tile_size=tile, background=(0.1, 0.2, 0.3), sh=False)
     check_frame(s, r, o, g, c, tile_size=tile)
+
+
+def test_group_frames_in_flight_follow_the_lod_chain():
+    """Region-split frames as the multi-GPU bench times them (one-rank NCCL group,
+    device-memory inputs, no stage times read, so frames stay in flight back to back) with
+    the camera moving through hysteresis: the last gathered frame equals the oracle's after
+    the same LoD chain, and a time-based rebalance keeps one rank's cuts whole."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2501_17792_b200 import native as N
+    from paper_2501_17792_b200.multigpu import BandGroup, gscg_settings
+
+    s = basic_scene(count=16, rows=4, cols=4, sh=False)
+    s.set_lod_policy((3.5, 6.0), hysteresis=1.0)
+    r = P.Renderer(s, device=0, device_poses=True)
+    o = orc.from_scene(s)
+    o.set_lod((3.5, 6.0), 1.0)
+    st = P.RenderSettings(sh_colour=False)
+    r.render_frame(0.0, st)  # templates + motion tables
+    rec = r.instance_records()
+    dev = torch.device("cuda", 0)
+    d = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int32) if v.dtype == np.uint32 else v).to(dev)
+         for k, v in rec.items()}
+    n = len(rec["lods"])
+    d_lods = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    lp = N.GscgLodPolicy()
+    lp.threshold_count = 2
+    lp.thresholds_m[0], lp.thresholds_m[1] = 3.5, 6.0
+    lp.hysteresis_band_m = 1.0
+    g = BandGroup(r, 0, 1)
+    H, W = s.cfg.height, s.cfg.width
+    zs = (-0.5, 0.0, 0.4, 0.8, 0.4, -0.3, 2.8, 3.3, 2.9)
+    rgb = np.empty((H, W, 3), np.float32)
+    for f, z in enumerate(zs):
+        s.set_camera((0.0, 1.6, -3.0 - z), (0.0, 1.0, 5.0))
+        fd = N.GscgFrameDesc()
+        fd.instance_count, fd.joint_stride = n, r.joint_stride
+        fd.template_ids, fd.placement = d["template_ids"].data_ptr(), d["placement"].data_ptr()
+        fd.active_lod, fd.forced_lod = d_lods.data_ptr(), -1
+        fd.memory, fd.pose_source, fd.time_s = N.GSCG_MEM_DEVICE, N.GSCG_POSES_SAMPLED, 0.1 + f / 30.0
+        fd.motion_ids, fd.phase_offsets = d["motion_ids"].data_ptr(), d["phase_offsets"].data_ptr()
+        last = f == len(zs) - 1
+        g.render(fd, s.camera_basis(), gscg_settings(st), lp, rgb if last else None, stage_times=last)
+    for f, z in enumerate(zs):
+        o.set_camera((0.0, 1.6, -3.0 - z), (0.0, 1.0, 5.0), 50.0, W, H)
+        orgb, _, _ = o.render(0.1 + f / 30.0, orc.settings(sh_colour=False))
+    assert rgb.tobytes() == orgb.tobytes()
+    assert np.array_equal(d_lods.cpu().numpy().astype(np.uint32), o.lods(n))
+    assert g.rebalance_by_time(0.5) == [0, W]
+    g.close()

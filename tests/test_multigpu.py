@@ -292,6 +292,17 @@ def _region_worker(rank: int, world: int, port: int, result_dir: str):
         dist.all_gather_object(all_cuts, cuts)
         assert all(c == cuts for c in all_cuts), "ranks derived different cuts"
         assert cuts[0] == 0 and cuts[-1] == W and all(c % 16 == 0 for c in cuts[1:-1])
+        # BandGroup.rebalance_by_time: every rank's region time all-gathered, same new cuts
+        from paper_2501_17792_b200.multigpu import cuts_from_region_times
+        t_mine = torch.tensor([1.0 + rank], dtype=torch.float64)
+        t_all = [torch.zeros_like(t_mine) for _ in range(world)]
+        dist.all_gather(t_all, t_mine)
+        line = t.numpy().sum(0)
+        tcuts = cuts_from_region_times(line + 0.02 * line.mean() + 1.0, W, 16, cuts, [float(x) for x in t_all])
+        all_t = [None] * world
+        dist.all_gather_object(all_t, tcuts)
+        assert all(c == tcuts for c in all_t), "ranks derived different time-balanced cuts"
+        assert tcuts[1] >= cuts[1]  # rank 1 reported the slower region: it shrinks
         # the gather: every rank's column region, assembled on rank 0
         region = torch.from_numpy(np.ascontiguousarray(np.concatenate([rgb, T[..., None]], axis=2)[:, cuts[rank]:cuts[rank + 1]]))
         parts = [None] * world
@@ -323,3 +334,16 @@ def test_cuts_from_tile_costs_balance_columns():
         assert cuts[0] == 0 and cuts[-1] == 1920 and all(cuts[i] < cuts[i + 1] for i in range(parts))
         load = [costs[:, cuts[i] // 16:cuts[i + 1] // 16].sum() for i in range(parts)]
         assert max(load) < 1.6 * costs.sum() / parts
+
+
+def test_cuts_from_region_times_shrink_the_slow_region():
+    from paper_2501_17792_b200.multigpu import band_rows, cuts_from_region_times
+
+    w = np.ones(120)
+    cuts = band_rows(1920, 16, 4, w)
+    assert cuts_from_region_times(w, 1920, 16, cuts, [1.0, 1.0, 1.0, 1.0]) == cuts
+    slow = cuts_from_region_times(w, 1920, 16, cuts, [1.0, 2.0, 1.0, 1.0])
+    assert slow[0] == 0 and slow[-1] == 1920 and all(slow[i] < slow[i + 1] for i in range(4))
+    assert slow[2] - slow[1] < cuts[2] - cuts[1]  # region 1 was twice as slow per pair
+    with pytest.raises(ValueError):
+        cuts_from_region_times(w, 1920, 16, cuts, [1.0, 1.0])
