@@ -2708,7 +2708,7 @@ int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const g
             return by_cols ? g->stage_rgb.as<float>() + 3 * offs[r] : g->full_rgb.as<float>() + 3 * offs[r];
         };
         auto dst_T = [&](int r) { return by_cols ? g->stage_T.as<float>() + offs[r] : g->full_T.as<float>() + offs[r]; };
-        if (g->rank == 0 && a1 > a0) {
+        if (g->rank == 0 && a1 > a0 && !by_cols) {  // rank 0's own column region is placed from its framebuffer below
             CUDA_TRY(cudaMemcpyAsync(dst_rgb(0), ctx->fb_rgb.ptr, region_px(0) * 12, cudaMemcpyDeviceToDevice, s));
             CUDA_TRY(cudaMemcpyAsync(dst_T(0), ctx->fb_T.ptr, region_px(0) * 4, cudaMemcpyDeviceToDevice, s));
         }
@@ -2730,9 +2730,11 @@ int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const g
             for (int r = 0; r < P; ++r) {
                 const size_t wr = cuts[r + 1] - cuts[r];
                 if (!wr) continue;
-                CUDA_TRY(cudaMemcpy2DAsync(g->full_rgb.as<float>() + 3 * cuts[r], static_cast<size_t>(W) * 12, dst_rgb(r),
+                const float* src_rgb = r == 0 ? ctx->fb_rgb.as<float>() : dst_rgb(r);
+                const float* src_T = r == 0 ? ctx->fb_T.as<float>() : dst_T(r);
+                CUDA_TRY(cudaMemcpy2DAsync(g->full_rgb.as<float>() + 3 * cuts[r], static_cast<size_t>(W) * 12, src_rgb,
                                            wr * 12, wr * 12, H, cudaMemcpyDeviceToDevice, s));
-                CUDA_TRY(cudaMemcpy2DAsync(g->full_T.as<float>() + cuts[r], static_cast<size_t>(W) * 4, dst_T(r), wr * 4,
+                CUDA_TRY(cudaMemcpy2DAsync(g->full_T.as<float>() + cuts[r], static_cast<size_t>(W) * 4, src_T, wr * 4,
                                            wr * 4, H, cudaMemcpyDeviceToDevice, s));
             }
         }
