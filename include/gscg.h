@@ -403,6 +403,13 @@ int gscg_group_destroy(gscg_group* group);
 int gscg_group_render_frame(gscg_group* group, const gscg_frame_desc* frame, const gscg_camera* cam,
                             const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
                             const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times);
+/* The same frame with rank 0's read-back into host fb_rgb / fb_T left running on the
+ * context's copy stream under the next frame (two whole-frame device buffers alternate):
+ * the destinations must stay valid until gscg_group_wait_readback. */
+int gscg_group_render_frame_async(gscg_group* group, const gscg_frame_desc* frame, const gscg_camera* cam,
+                                  const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
+                                  const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times);
+int gscg_group_wait_readback(gscg_group* group);
 int gscg_group_framebuffer_device(gscg_group* group, float** rgb, float** T); /* rank 0 */
 int gscg_group_tile_costs(gscg_group* group, uint32_t tiles_x, uint32_t tiles_y, uint64_t* out /* tiles_y x tiles_x */);
 

@@ -2547,6 +2547,12 @@ struct gscg_group {
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
     DevBuf full_rgb, full_T, stage_rgb, stage_T, row_costs, all_costs;
+    // Async frames (gscg_group_render_frame_async): rank 0 alternates two whole-frame
+    // buffers; rb_ev[i] marks the end of buffer i's host read-back on the copy stream.
+    DevBuf full_rgb_alt, full_T_alt;
+    cudaEvent_t rb_ev[2] = {nullptr, nullptr}, done_ev = nullptr;
+    bool rb_rec[2] = {false, false};
+    int cur = 0;
 };
 
 namespace {
@@ -2637,9 +2643,15 @@ int gscg_group_destroy(gscg_group* g) {
     if (!g) return GSCG_OK;
     cudaSetDevice(g->ctx->device);
     cudaStreamSynchronize(g->ctx->stream);
+    cudaStreamSynchronize(g->ctx->copy_stream);
     if (g->comm) nccl().CommDestroy(g->comm);
+    for (auto& e : g->rb_ev)
+        if (e) cudaEventDestroy(e);
+    if (g->done_ev) cudaEventDestroy(g->done_ev);
     g->full_rgb.release();
     g->full_T.release();
+    g->full_rgb_alt.release();
+    g->full_T_alt.release();
     g->stage_rgb.release();
     g->stage_T.release();
     g->row_costs.release();
@@ -2648,9 +2660,10 @@ int gscg_group_destroy(gscg_group* g) {
     return GSCG_OK;
 }
 
-int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const gscg_camera* cam,
-                            const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
-                            const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+namespace {
+int group_render_impl(gscg_group* g, const gscg_frame_desc* frame, const gscg_camera* cam,
+                      const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
+                      const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times, bool async) {
     if (!g || !cuts || !cam || (axis != GSCG_SPLIT_ROWS && axis != GSCG_SPLIT_COLS)) return GSCG_ERR_INVALID_ARGUMENT;
     gscg_ctx* ctx = g->ctx;
     return guarded(ctx, [&] {
@@ -2688,6 +2701,12 @@ int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const g
             return by_cols ? len * static_cast<size_t>(H) : len * static_cast<size_t>(W);
         };
         if (g->rank == 0) {
+            if (async) {  // the other whole-frame buffer, once its last read-back has landed
+                std::swap(g->full_rgb, g->full_rgb_alt);
+                std::swap(g->full_T, g->full_T_alt);
+                g->cur ^= 1;
+                if (g->rb_rec[g->cur]) CUDA_TRY(cudaStreamWaitEvent(s, g->rb_ev[g->cur], 0));
+            }
             CUDA_TRY(g->full_rgb.ensure(static_cast<size_t>(W) * H * 12));
             CUDA_TRY(g->full_T.ensure(static_cast<size_t>(W) * H * 4));
             if (by_cols) {
@@ -2740,10 +2759,45 @@ int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const g
         }
         if (g->rank == 0 && (fb_rgb || fb_T)) {
             const size_t px = static_cast<size_t>(W) * H;
-            if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, g->full_rgb.ptr, px * 12, cudaMemcpyDefault, s));
-            if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, g->full_T.ptr, px * 4, cudaMemcpyDefault, s));
-            if (is_host_pointer(fb_rgb) || is_host_pointer(fb_T)) CUDA_TRY(cudaStreamSynchronize(s));
+            if (async) {  // read-back on the copy stream, under the next frame
+                if (!g->done_ev) {
+                    CUDA_TRY(cudaEventCreateWithFlags(&g->done_ev, cudaEventDisableTiming));
+                    for (auto& e : g->rb_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                }
+                CUDA_TRY(cudaEventRecord(g->done_ev, s));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, g->done_ev, 0));
+                if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, g->full_rgb.ptr, px * 12, cudaMemcpyDefault, ctx->copy_stream));
+                if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, g->full_T.ptr, px * 4, cudaMemcpyDefault, ctx->copy_stream));
+                CUDA_TRY(cudaEventRecord(g->rb_ev[g->cur], ctx->copy_stream));
+                g->rb_rec[g->cur] = true;
+            } else {
+                if (fb_rgb) CUDA_TRY(cudaMemcpyAsync(fb_rgb, g->full_rgb.ptr, px * 12, cudaMemcpyDefault, s));
+                if (fb_T) CUDA_TRY(cudaMemcpyAsync(fb_T, g->full_T.ptr, px * 4, cudaMemcpyDefault, s));
+                if (is_host_pointer(fb_rgb) || is_host_pointer(fb_T)) CUDA_TRY(cudaStreamSynchronize(s));
+            }
         }
+    });
+}
+}  // namespace
+
+int gscg_group_render_frame(gscg_group* g, const gscg_frame_desc* frame, const gscg_camera* cam,
+                            const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
+                            const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+    return group_render_impl(g, frame, cam, settings, lod, axis, cuts, fb_rgb, fb_T, times, false);
+}
+
+int gscg_group_render_frame_async(gscg_group* g, const gscg_frame_desc* frame, const gscg_camera* cam,
+                                  const gscg_render_settings* settings, const gscg_lod_policy* lod, int32_t axis,
+                                  const uint32_t* cuts, float* fb_rgb, float* fb_T, gscg_stage_times* times) {
+    return group_render_impl(g, frame, cam, settings, lod, axis, cuts, fb_rgb, fb_T, times, true);
+}
+
+int gscg_group_wait_readback(gscg_group* g) {
+    if (!g) return GSCG_ERR_INVALID_ARGUMENT;
+    gscg_ctx* ctx = g->ctx;
+    return guarded(ctx, [&] {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
     });
 }
 

@@ -486,20 +486,28 @@ class BandGroup:
         self.cuts = band_rows(self.extent, tile, self.world)
 
     def render(self, frame, cam, settings, lod, out_rgb=None, out_T=None,
-               stage_times: bool = True) -> Optional["N.GscgStageTimes"]:
+               stage_times: bool = True, pipelined: bool = False) -> Optional["N.GscgStageTimes"]:
         """One frame (frame/cam/settings/lod: the gscg_render_frame descriptors). On rank 0,
         out_rgb / out_T (numpy, host or None) receive the whole frame. stage_times=False
         returns None and leaves the frame in flight: reading the stage events makes the
         call wait for the region's raster, so the next frame's update and projection could
-        not overlap this one's sort, raster and gather."""
+        not overlap this one's sort, raster and gather. pipelined=True
+        (gscg_group_render_frame_async): rank 0's host read-back runs under the next frame;
+        the arrays are valid after wait_readback() (streaming callers alternate two)."""
         st = N.GscgStageTimes() if stage_times else None
+        if pipelined:
+            self._inflight = (getattr(self, "_inflight", []) + [(out_rgb, out_T)])[-2:]
         cuts = (C.c_uint32 * (self.world + 1))(*self.cuts)
         axis = N.GSCG_SPLIT_COLS if self.axis == "cols" else N.GSCG_SPLIT_ROWS
         ptr = (lambda a: None if a is None else a.ctypes.data)
-        N.check_gscg(N.gscg().gscg_group_render_frame(self._h, C.byref(frame), C.byref(cam), C.byref(settings),
-                                                       C.byref(lod), axis, cuts, ptr(out_rgb), ptr(out_T),
-                                                       None if st is None else C.byref(st)), self.renderer.gpu)
+        fn = N.gscg().gscg_group_render_frame_async if pipelined else N.gscg().gscg_group_render_frame
+        N.check_gscg(fn(self._h, C.byref(frame), C.byref(cam), C.byref(settings), C.byref(lod), axis, cuts,
+                        ptr(out_rgb), ptr(out_T), None if st is None else C.byref(st)), self.renderer.gpu)
         return st
+
+    def wait_readback(self) -> None:
+        """Blocks until rank 0's pipelined read-backs have landed."""
+        N.check_gscg(N.gscg().gscg_group_wait_readback(self._h), self.renderer.gpu)
 
     def tile_costs(self) -> np.ndarray:
         tx = (self.width + self.tile - 1) // self.tile

@@ -158,6 +158,10 @@ GSCG_SYMBOLS = {
     "gscg_group_render_frame": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
                                           C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), C.c_int32, _P,
                                           _P, _P, C.POINTER(GscgStageTimes)]),
+    "gscg_group_render_frame_async": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),
+                                                C.POINTER(GscgRenderSettings), C.POINTER(GscgLodPolicy), C.c_int32,
+                                                _P, _P, _P, C.POINTER(GscgStageTimes)]),
+    "gscg_group_wait_readback": (C.c_int, [_P]),
     "gscg_group_framebuffer_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),
     "gscg_group_tile_costs": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P]),
     "gscg_gather_splats": (C.c_int, [_P, C.POINTER(GscgFrameDesc), C.POINTER(GscgCamera),

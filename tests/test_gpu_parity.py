@@ -905,3 +905,57 @@ def test_group_frames_in_flight_follow_the_lod_chain():
     assert np.array_equal(d_lods.cpu().numpy().astype(np.uint32), o.lods(n))
     assert g.rebalance_by_time(0.5) == [0, W]
     g.close()
+
+
+def test_group_async_readback_matches_blocking_frames():
+    """gscg_group_render_frame_async (rank 0's host read-back under the next frame, two
+    device frame buffers alternating): every frame read back equals the blocking call's."""
+    from paper_2501_17792_b200 import native as N
+    from paper_2501_17792_b200.api import pinned_array
+    from paper_2501_17792_b200.multigpu import BandGroup, gscg_settings
+
+    s, extra = config_scene(2)
+    r = P.Renderer(s, device_poses=True)
+    r.render_frame(0.3, P.RenderSettings())
+    g = BandGroup(r, 0, 1)
+    rec = r.instance_records()
+    n = len(rec["template_ids"])
+    lods = np.full(n, 0xFFFFFFFF, np.uint32)
+    cfg = s.cfg
+    lp = N.GscgLodPolicy()
+    lp.threshold_count = len(cfg.lod_thresholds)
+    for i, v in enumerate(cfg.lod_thresholds):
+        lp.thresholds_m[i] = v
+
+    def fd_at(t):
+        fd = N.GscgFrameDesc()
+        fd.instance_count, fd.joint_stride = n, r.joint_stride
+        fd.template_ids, fd.placement = rec["template_ids"].ctypes.data, rec["placement"].ctypes.data
+        fd.active_lod, fd.forced_lod = lods.ctypes.data, -1
+        fd.memory, fd.pose_source, fd.time_s = N.GSCG_MEM_HOST, N.GSCG_POSES_SAMPLED, t
+        fd.motion_ids, fd.phase_offsets = rec["motion_ids"].ctypes.data, rec["phase_offsets"].ctypes.data
+        return fd
+
+    times = (0.3, 0.5, 0.7, 0.9)
+    st = gscg_settings(P.RenderSettings())
+    cam = s.camera_basis()
+    ref = []
+    for t in times:
+        out = np.empty((cfg.height, cfg.width, 3), np.float32)
+        g.render(fd_at(t), cam, st, lp, out)
+        ref.append(out)
+    bufs = [pinned_array((cfg.height, cfg.width, 3)) for _ in range(2)]
+    for wait_each in (True, False):  # each frame checked, then frames streamed back to back
+        lods[:] = 0xFFFFFFFF  # the blocking pass's LoD chain start
+        got = []
+        for k, t in enumerate(times):
+            g.render(fd_at(t), cam, st, lp, bufs[k % 2], stage_times=False, pipelined=True)
+            if wait_each:
+                g.wait_readback()
+                got.append(bufs[k % 2].copy())
+        g.wait_readback()
+        if wait_each:
+            assert all(a.tobytes() == b.tobytes() for a, b in zip(got, ref))
+        assert bufs[(len(times) - 1) % 2].tobytes() == ref[-1].tobytes()
+        assert bufs[(len(times) - 2) % 2].tobytes() == ref[-2].tobytes()
+    g.close()
