@@ -2705,8 +2705,10 @@ int group_render_impl(gscg_group* g, const gscg_frame_desc* frame, const gscg_ca
                 std::swap(g->full_rgb, g->full_rgb_alt);
                 std::swap(g->full_T, g->full_T_alt);
                 g->cur ^= 1;
-                if (g->rb_rec[g->cur]) CUDA_TRY(cudaStreamWaitEvent(s, g->rb_ev[g->cur], 0));
             }
+            // A buffer may still be read back from an async frame (also when a blocking
+            // call follows async ones).
+            if (g->rb_rec[g->cur]) CUDA_TRY(cudaStreamWaitEvent(s, g->rb_ev[g->cur], 0));
             CUDA_TRY(g->full_rgb.ensure(static_cast<size_t>(W) * H * 12));
             CUDA_TRY(g->full_T.ensure(static_cast<size_t>(W) * H * 4));
             if (by_cols) {
