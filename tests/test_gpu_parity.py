@@ -958,4 +958,10 @@ def test_group_async_readback_matches_blocking_frames():
             assert all(a.tobytes() == b.tobytes() for a, b in zip(got, ref))
         assert bufs[(len(times) - 1) % 2].tobytes() == ref[-1].tobytes()
         assert bufs[(len(times) - 2) % 2].tobytes() == ref[-2].tobytes()
+    # a blocking frame right after async ones (the buffer's read-back may be in flight)
+    g.render(fd_at(times[0]), cam, st, lp, bufs[0], stage_times=False, pipelined=True)
+    out = np.empty((cfg.height, cfg.width, 3), np.float32)
+    g.render(fd_at(times[-1]), cam, st, lp, out)
+    g.wait_readback()
+    assert out.tobytes() == ref[-1].tobytes() and bufs[0].tobytes() == ref[0].tobytes()
     g.close()
